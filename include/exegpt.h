@@ -1,0 +1,199 @@
+/*
+ * exegpt.h -- C-ABI of libexegpt.so, a B200-native (sm_100a) runner for the
+ * decoupled-inference computation that ExeGPT (arXiv 2404.07947) schedules.
+ *
+ * The calls follow the paper's problem statement (§5):
+ * profile the cost model (XProfiler), pick the max-
+ * throughput schedule under a latency bound for the given input/output
+ * length distributions (XSimulator + XScheduler, §5-§6,
+ * host code), and run that schedule on a request batch (XRunner,
+ * PAPER.md:171-176) returning greedy tokens and per-request latencies.
+ *
+ * Conventions
+ *  - Plain C types only; no torch/CUDA types cross this boundary.
+ *  - Every function returns an exg_status and never throws or exits; on an
+ *    error exg_last_error() (thread-local) holds a message and output
+ *    buffers are unspecified.
+ *  - The caller owns every input array and every output buffer; the library
+ *    copies inputs before returning.  Opaque objects are library-owned and
+ *    released with their *_free / exg_destroy.
+ *  - Host pointers unless stated otherwise.
+ */
+#ifndef EXEGPT_H
+#define EXEGPT_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define EXG_ABI_VERSION 1
+
+typedef enum {
+  EXG_OK = 0,
+  EXG_E_INPUT = 1,       /* invalid argument (SPEC.md:562 exit code 1)            */
+  EXG_E_INFEASIBLE = 2,  /* no schedule meets L_B / memory / WAA on < 2 GPUs (2)  */
+  EXG_E_CUDA = 3,
+  EXG_E_NCCL = 4,
+  EXG_E_OOM = 5,
+  EXG_E_INTERNAL = 6     /* e.g. a NaN logit                  */
+} exg_status;
+
+typedef enum { EXG_ARCH_OPT = 0, EXG_ARCH_GPT3 = 1, EXG_ARCH_T5 = 2 } exg_arch; /* tiny = GPT3-style */
+typedef enum { EXG_BF16 = 0, EXG_FP32 = 1 } exg_dtype;
+typedef enum { EXG_RRA = 1, EXG_WAA_C = 2, EXG_WAA_M = 4 } exg_strategy;    /* bitmask */
+
+/* Model shape (Table 1) plus the weight seed of the
+ * counter-hash generator.  n_enc_layers = 0 for
+ * decoder-only models. */
+typedef struct {
+  exg_arch arch;
+  int32_t n_enc_layers, n_dec_layers, d_model, n_heads, d_head, d_ff, vocab, max_pos;
+  exg_dtype dtype;
+  uint64_t weight_seed;
+} exg_model_spec;
+
+/* Cluster: GPUs used and usable bytes per GPU (memory check);
+ * workspace_bytes is reserved per GPU for activations / scratch. */
+typedef struct {
+  int32_t n_gpus;
+  int64_t mem_per_gpu_bytes;
+  int64_t workspace_bytes;
+} exg_cluster_spec;
+
+/* A length distribution P(len = k) = prob[k-1], k = 1..max_len. */
+typedef struct {
+  int32_t max_len;
+  const double* prob;
+} exg_pmf;
+
+/* Control variables: B_E, B_D, B_m, T_P (degree and
+ * applied GPU count), F_E = 1/N_D, strategy S; plus the resolved layout:
+ * stage k covers GPUs [stage_first_gpu[k], +stage_n_gpus[k]) and layers
+ * [stage_layer_begin[k], stage_layer_end[k]).  For WAA the n_enc_gpus
+ * encoder stages come first, then the decoder stages. */
+#define EXG_MAX_STAGES 8
+typedef struct {
+  exg_strategy strategy;
+  int32_t b_e, b_d, b_m, n_d;
+  int32_t tp_degree, tp_gpus;
+  int32_t n_enc_gpus;
+  int32_t n_stages;
+  int32_t stage_first_gpu[EXG_MAX_STAGES], stage_n_gpus[EXG_MAX_STAGES];
+  int32_t stage_layer_begin[EXG_MAX_STAGES], stage_layer_end[EXG_MAX_STAGES];
+} exg_schedule;
+
+/* Simulator estimate: steady-state throughput and the
+ * latency of a target_len-long query. */
+typedef struct {
+  double thrput_seq_s, thrput_tok_s, latency_s;
+  int64_t perf_evals;
+  int32_t feasible;
+} exg_estimate;
+
+/* Algorithm 1 options: tolerances as fractions of T* / L_B,
+ * search ranges, and the Little's-law completion fraction option
+ * (SURVEY.md §8(c) S3). */
+typedef struct {
+  double eps_t_frac, eps_l_frac;
+  int32_t b_e_max, n_d_max, m_max;
+  int32_t use_little_fraction;
+} exg_search_opts;
+
+/* XProfiler sweep axes. */
+typedef struct {
+  int32_t n_batch;  const int32_t* batch;   /* attention: batch sweep              */
+  int32_t n_ctx;    const int32_t* ctx;     /* attention: context sweep per batch  */
+  int32_t n_tokens; const int32_t* tokens;  /* rest of the layer: input-size sweep */
+  int32_t n_tp;     const int32_t* tp;      /* TP degrees                          */
+  int32_t reps;                             /* timed repetitions per point         */
+} exg_profile_grid;
+
+/* One request: input ids (length input_len >= 1) and the forced output
+ * length (no EOS). */
+typedef struct {
+  const int32_t* input_ids;
+  int32_t input_len, output_len;
+} exg_request;
+
+typedef struct {
+  float* logits_out;          /* optional fp32 [sum dumped output_len][vocab]   */
+  const uint8_t* dump_mask;   /* optional [n]: 1 = dump this request's logits   */
+  int32_t slot_ctx;           /* KV slot length; 0 -> max(input_len+output_len) */
+  int32_t pin_nccl_algo;      /* reserved for multi-GPU parity runs             */
+} exg_run_opts;
+
+/* Measured run statistics.  Times come from device
+ * events on one clock. */
+typedef struct {
+  double tok_s, tok_s_steady, seq_s;
+  double lat_p50_s, lat_p99_s, lat_max_s;
+  double wall_s;                       /* first encode start -> last iteration end */
+  int64_t out_tokens, decode_iters, encode_phases;
+  double mean_decode_batch;            /* measured, vs the simulated B_D           */
+  double encode_s, decode_s;           /* device time spent per phase kind         */
+} exg_run_stats;
+
+typedef struct exg_ctx exg_ctx;           /* one per rank: device state + comms */
+typedef struct exg_profile exg_profile;   /* profile-v1 table     */
+
+/* ---- lifecycle ---------------------------------------------------------- */
+/* Library ABI version (EXG_ABI_VERSION). */
+int32_t exg_abi_version(void);
+/* Thread-local message of the last failing call on this thread. */
+const char* exg_last_error(void);
+
+/* NCCL unique id for a multi-rank context (call on rank 0, broadcast the
+ * 128 bytes).  Single-GPU runs may pass NULL uid to exg_create. */
+exg_status exg_get_unique_id(uint8_t uid[128]);
+
+/* Create a rank's context on `device`: allocates and generates this rank's
+ * weights on the GPU from spec->weight_seed (K14).  Collective over `world`
+ * ranks when world > 1.  *out is owned by the library (exg_destroy). */
+exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device, int32_t rank,
+                      int32_t world, const uint8_t* uid, exg_ctx** out);
+void exg_destroy(exg_ctx* ctx);
+
+/* ---- XProfiler --------------------------------------- */
+/* Times one encoder layer and one decoder layer on the real kernels:
+ * attention over (batch x ctx) and the rest of the layer over tokens, per
+ * TP degree, plus TP all-reduce and PP send costs.  Collective. */
+exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profile** out);
+/* profile-v1 text file ("%.17g" numbers, lossless). */
+exg_status exg_profile_save(const exg_profile* p, const char* path);
+exg_status exg_profile_load(const char* path, exg_profile** out);
+void exg_profile_free(exg_profile* p);
+
+/* ---- XSimulator / XScheduler (pure host, deterministic) ----------------- */
+/* Estimate of one schedule.  sched must be a resolved
+ * schedule (as returned by exg_schedule_find / exg_schedule_resolve). */
+exg_status exg_simulate(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                        const exg_pmf* in, const exg_pmf* out_len, int32_t target_len, const exg_schedule* sched,
+                        exg_estimate* est);
+/* Resolve derived fields (B_D, B_m, stage layout) of a schedule given by its
+ * control variables (strategy, b_e, n_d | b_m-count, tp_degree, tp_gpus). */
+exg_status exg_schedule_resolve(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                                const exg_pmf* in, const exg_pmf* out_len, int32_t m_count, exg_schedule* sched);
+/* argmax Throughput s.t. Latency < latency_bound_s by
+ * Algorithm 1 inside the strategy x TP-degree x
+ * applied-GPU loops.  latency_bound_s may be +inf.
+ * Returns EXG_E_INFEASIBLE if no configuration meets the bound. */
+exg_status exg_schedule_find(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                             const exg_pmf* in, const exg_pmf* out_len, int32_t target_len, double latency_bound_s,
+                             uint32_t strategy_mask, const exg_search_opts* opts, exg_schedule* out,
+                             exg_estimate* est);
+
+/* ---- XRunner ------------------------------------------ */
+/* Run `sched` on the closed request batch reqs[0..n) (all available at t=0).
+ * out_tokens: int32 [sum output_len] in request order (prefix-sum offsets);
+ * out_latency_s: [n], from the start of the encode phase that admitted the
+ * request to the end of the iteration that emitted its last token.
+ * Greedy decoding, token accounting SURVEY.md §8(c) T6.  Collective. */
+exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* reqs, int32_t n, int32_t* out_tokens,
+                   double* out_latency_s, exg_run_stats* stats, const exg_run_opts* opts);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXEGPT_H */

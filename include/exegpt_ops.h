@@ -1,0 +1,85 @@
+/*
+ * exegpt_ops.h -- op-level C-ABI of libexegpt.so: the individual sm_100a
+ * kernels of the hot path, exposed for kernel parity tests and for timing
+ * the dominant kernel in bench.py.  Same conventions as exegpt.h, except:
+ *
+ *  - every data pointer here is a DEVICE pointer (cudaMalloc'd or a torch
+ *    CUDA tensor's data_ptr) owned by the caller;
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *    stream); the call only enqueues work (asynchronous);
+ *  - bf16 tensors are passed as void* holding IEEE bfloat16 values.
+ *
+ * Operation definitions cite PAPER.md / SURVEY.md §8(c); shapes below.
+ */
+#ifndef EXEGPT_OPS_H
+#define EXEGPT_OPS_H
+
+#include <stdint.h>
+
+#include "exegpt.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* K14 -- seeded weights.  dst: bf16 [rows][ld]; element
+ * (r,c) is value index i = transposed ? (c+col_off)*canon_cols + (r+row_off)
+ * : (r+row_off)*canon_cols + (c+col_off) of tensor `tensor_id`;
+ * gain = 1 for norm gains 1+U(+-0.1), else U(+-sqrt(3)*0.02). */
+exg_status exg_op_weightgen(void* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t tensor_id,
+                            int32_t gain, int32_t transposed, int64_t canon_cols, int64_t row_off, int64_t col_off,
+                            void* stream);
+
+/* K3/K5/K8 -- Y[tokens][features] = X[tokens][K] . W[features][K]^T with
+ * epilogue `mode`: 0 bf16(acc+bias) -> out; 1 bf16(act(acc+bias)) -> out
+ * (act 1 = ReLU, 2 = GELU-tanh); 2 resid(fp32) += acc+bias; 3 fp32 acc+bias
+ * -> out.  bias: bf16 [features] or NULL.  decode = 1 selects the swap-AB
+ * tcgen05 path (tokens on the MMA N axis), else the prefill path; split > 1
+ * reduces K in `split` fixed parts in order (ws: fp32 split*tokens*features). */
+exg_status exg_op_linear(const void* X, int64_t ldx, const void* W, int64_t ldw, int32_t tokens, int32_t features,
+                         int32_t K, int32_t mode, int32_t act, const void* bias, void* out, int64_t ldo, float* resid,
+                         int64_t ldr, int32_t decode, int32_t split, float* ws, void* stream);
+
+/* K2 -- y bf16 [T][ldy] = LN(x fp32 [T][ldx]) * g + b, eps, fp32 statistics. */
+exg_status exg_op_layernorm(void* y, int64_t ldy, const float* x, int64_t ldx, const void* g, const void* b, int32_t T,
+                            int32_t d, float eps, void* stream);
+
+/* K1 -- x fp32 [T][d] = tok_emb[ids[t]] + pos_emb[pos[t]] (bf16 tables). */
+exg_status exg_op_embed(float* x, const int32_t* ids, const int32_t* pos, const void* tok_emb, const void* pos_emb,
+                        int32_t T, int32_t d, void* stream);
+
+/* K7 -- copy the K and V column blocks of qkv bf16 [T][3*H*dh] into cache
+ * [slot][H][max_ctx][dh] at (slot[t], pos[t]). */
+exg_status exg_op_kv_scatter(void* kc, void* vc, const void* qkv, const int32_t* slot, const int32_t* pos, int32_t T,
+                             int32_t H, int32_t dh, int32_t max_ctx, void* stream);
+
+/* K6 -- ragged decode attention (incremental decoding):
+ * out[i][h] = bf16( softmax_j( fp32(q_i,h . K[slot_i][h][j]) * scale ) . V )
+ * over j < n_keys[i].  q: bf16 rows of stride ldq (head h at h*dh); out:
+ * bf16 [B][ldo].  Keys are split in fixed chunks of split_len; partial: fp32
+ * [B][H][max_splits][dh+2] scratch when max_splits > 1. */
+exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, const void* vc, const int32_t* slot,
+                                   const int32_t* n_keys, void* out, int64_t ldo, int32_t B, int32_t H, int32_t dh,
+                                   int32_t max_ctx, float scale, int32_t split_len, int32_t max_splits, float* partial,
+                                   void* stream);
+
+/* K4 -- causal prefill attention over packed requests (cu_seqlens [R+1]);
+ * request r's tokens sit at positions pos0[r].. of slot[r] and attend to
+ * cached keys 0..own position (keys scattered beforehand). */
+exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, const void* vc,
+                                    const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0, int32_t R,
+                                    int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh, int32_t max_ctx,
+                                    float scale, void* stream);
+
+/* K8 -- out[i] = argmax_v logits[i][v] (fp32 [B][ld]), lowest index on ties;
+ * *err_flag (device int32, may be NULL) set to 1 on a NaN. */
+exg_status exg_op_argmax(int32_t* out, const float* logits, int64_t ld, int32_t B, int32_t V, int32_t* err_flag,
+                         void* stream);
+
+/* Split-K factor the runner uses for a decode GEMM of this weight shape. */
+int32_t exg_op_decode_split_k(int32_t features, int32_t K);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EXEGPT_OPS_H */

@@ -1,0 +1,387 @@
+// extern "C" boundary of libexegpt.so (include/exegpt.h, include/exegpt_ops.h).
+// Every entry point catches all exceptions and maps them to an exg_status
+// with a thread-local message; nothing throws across the ABI.
+#include <cmath>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <new>
+#include <sstream>
+#include <string>
+
+#include "../../include/exegpt.h"
+#include "../../include/exegpt_ops.h"
+#include "engine.cuh"
+#include "planner.h"
+#include "profiler.h"
+#include "runner.h"
+
+struct exg_ctx {
+  std::unique_ptr<exg::Engine> engine;
+  exg_model_spec spec;
+  exg_cluster_spec cluster;
+  int rank = 0, world = 1, device = 0;
+};
+
+struct exg_profile {
+  exg::plan::Profile p;
+};
+
+namespace {
+thread_local std::string g_err;
+
+exg_status fail(exg_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+template <class F>
+exg_status guarded(F&& f) {
+  try {
+    g_err.clear();
+    return f();
+  } catch (const exg::CudaError& e) {
+    const std::string m = e.what();
+    if (m.find("out of memory") != std::string::npos) return fail(EXG_E_OOM, m);
+    return fail(EXG_E_CUDA, m);
+  } catch (const std::bad_alloc&) {
+    return fail(EXG_E_OOM, "out of memory");
+  } catch (const std::invalid_argument& e) {
+    return fail(EXG_E_INPUT, e.what());
+  } catch (const exg::plan::OutOfHull&) {
+    return fail(EXG_E_INFEASIBLE, "query outside the profiled hull");
+  } catch (const std::exception& e) {
+    return fail(EXG_E_INTERNAL, e.what());
+  } catch (...) {
+    return fail(EXG_E_INTERNAL, "unknown error");
+  }
+}
+
+std::vector<double> pmf_vec(const exg_pmf* p) {
+  if (!p || p->max_len < 1 || !p->prob) throw std::invalid_argument("bad pmf");
+  std::vector<double> v(p->prob, p->prob + p->max_len);
+  for (double x : v)
+    if (!(x >= 0.0)) throw std::invalid_argument("pmf has a negative or NaN entry");
+  return v;
+}
+
+void check_spec(const exg_model_spec* s) {
+  if (!s) throw std::invalid_argument("null model spec");
+  if (s->n_dec_layers < 1 || s->d_model < 1 || s->n_heads < 1 || s->d_head < 1 || s->d_ff < 1 || s->vocab < 2 ||
+      s->max_pos < 2)
+    throw std::invalid_argument("invalid model spec");
+}
+
+void to_c(const exg::plan::Sched& s, exg_schedule* o) {
+  std::memset(o, 0, sizeof(*o));
+  o->strategy = (exg_strategy)s.strategy;
+  o->b_e = s.b_e;
+  o->b_d = s.b_d;
+  o->b_m = s.b_m;
+  o->n_d = s.n_d;
+  o->tp_degree = s.tp_degree;
+  o->tp_gpus = s.tp_gpus;
+  o->n_enc_gpus = s.n_enc_gpus;
+  o->n_stages = (int32_t)s.stages.size();
+  for (size_t k = 0; k < s.stages.size() && k < EXG_MAX_STAGES; ++k) {
+    o->stage_first_gpu[k] = s.stages[k].first_gpu;
+    o->stage_n_gpus[k] = s.stages[k].n_gpus;
+    o->stage_layer_begin[k] = s.stages[k].layer_begin;
+    o->stage_layer_end[k] = s.stages[k].layer_end;
+  }
+}
+
+exg::plan::Sched from_c(const exg_schedule* o) {
+  exg::plan::Sched s;
+  s.strategy = o->strategy;
+  s.b_e = o->b_e;
+  s.b_d = o->b_d;
+  s.b_m = o->b_m;
+  s.n_d = o->n_d;
+  s.tp_degree = o->tp_degree;
+  s.tp_gpus = o->tp_gpus;
+  s.n_enc_gpus = o->n_enc_gpus;
+  if (o->n_stages < 1 || o->n_stages > EXG_MAX_STAGES) throw std::invalid_argument("schedule has no stages");
+  for (int k = 0; k < o->n_stages; ++k)
+    s.stages.push_back({o->stage_first_gpu[k], o->stage_n_gpus[k], o->stage_layer_begin[k], o->stage_layer_end[k]});
+  return s;
+}
+}  // namespace
+
+extern "C" {
+
+int32_t exg_abi_version(void) { return EXG_ABI_VERSION; }
+const char* exg_last_error(void) { return g_err.c_str(); }
+
+exg_status exg_get_unique_id(uint8_t uid[128]) {
+  return guarded([&] {
+    if (!uid) throw std::invalid_argument("null uid");
+    std::memset(uid, 0, 128);
+    return fail(EXG_E_NCCL, "multi-rank contexts are not built in this version");
+  });
+}
+
+exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device, int32_t rank,
+                      int32_t world, const uint8_t* uid, exg_ctx** out) {
+  return guarded([&] {
+    if (!out) throw std::invalid_argument("null out");
+    *out = nullptr;
+    check_spec(spec);
+    if (world != 1 || rank != 0) return fail(EXG_E_NCCL, "multi-rank contexts are not built in this version");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EXG_E_CUDA, "no CUDA device");
+    if (device < 0 || device >= ndev) throw std::invalid_argument("bad device index");
+    auto c = std::make_unique<exg_ctx>();
+    c->spec = *spec;
+    if (cluster) c->cluster = *cluster;
+    c->rank = rank;
+    c->world = world;
+    c->device = device;
+    c->engine = std::make_unique<exg::Engine>(*spec, device);
+    *out = c.release();
+    return EXG_OK;
+  });
+}
+
+void exg_destroy(exg_ctx* ctx) {
+  try {
+    delete ctx;
+  } catch (...) {
+  }
+}
+
+exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profile** out) {
+  return guarded([&] {
+    if (!ctx || !grid || !out) throw std::invalid_argument("null argument");
+    auto p = std::make_unique<exg_profile>();
+    exg::profile_layers(*ctx->engine, *grid, &p->p);
+    *out = p.release();
+    return EXG_OK;
+  });
+}
+
+exg_status exg_profile_save(const exg_profile* p, const char* path) {
+  return guarded([&] {
+    if (!p || !path) throw std::invalid_argument("null argument");
+    std::ofstream f(path);
+    if (!f) throw std::invalid_argument(std::string("cannot open ") + path);
+    f << p->p.dumps();
+    return EXG_OK;
+  });
+}
+
+exg_status exg_profile_load(const char* path, exg_profile** out) {
+  return guarded([&] {
+    if (!path || !out) throw std::invalid_argument("null argument");
+    std::ifstream f(path);
+    if (!f) throw std::invalid_argument(std::string("cannot open ") + path);
+    std::stringstream ss;
+    ss << f.rdbuf();
+    auto p = std::make_unique<exg_profile>();
+    p->p = exg::plan::Profile::loads(ss.str());
+    *out = p.release();
+    return EXG_OK;
+  });
+}
+
+void exg_profile_free(exg_profile* p) { delete p; }
+
+exg_status exg_simulate(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                        const exg_pmf* in, const exg_pmf* out_len, int32_t target_len, const exg_schedule* sched,
+                        exg_estimate* est) {
+  return guarded([&] {
+    if (!p || !cluster || !sched || !est) throw std::invalid_argument("null argument");
+    check_spec(spec);
+    exg::plan::Simulator S(p->p, *spec, *cluster, pmf_vec(in), pmf_vec(out_len), target_len, false);
+    exg::plan::Est e = S.simulate(from_c(sched));
+    est->thrput_seq_s = e.thr;
+    est->thrput_tok_s = e.tok;
+    est->latency_s = e.lat;
+    est->perf_evals = 1;
+    est->feasible = e.feasible;
+    return EXG_OK;
+  });
+}
+
+exg_status exg_schedule_resolve(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                                const exg_pmf* in, const exg_pmf* out_len, int32_t m_count, exg_schedule* sched) {
+  return guarded([&] {
+    if (!p || !cluster || !sched) throw std::invalid_argument("null argument");
+    check_spec(spec);
+    exg::plan::Simulator S(p->p, *spec, *cluster, pmf_vec(in), pmf_vec(out_len), 1, false);
+    exg::plan::Sched s;
+    if (sched->strategy == EXG_RRA) {
+      if (sched->b_e < 1 || sched->n_d < 1) throw std::invalid_argument("RRA needs b_e >= 1, n_d >= 1");
+      s = S.rra_schedule(sched->b_e, sched->n_d, std::max(1, sched->tp_degree), sched->tp_gpus);
+    } else if (sched->strategy == EXG_WAA_C) {
+      s = S.waa_schedule(sched->b_e, std::max(1, m_count), std::max(1, sched->tp_degree), sched->tp_gpus);
+      if (!s.valid) return fail(EXG_E_INFEASIBLE, "WAA needs >= 2 GPUs and tp_gpus <= decoder GPUs");
+    } else {
+      throw std::invalid_argument("unknown strategy");
+    }
+    to_c(s, sched);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_schedule_find(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                             const exg_pmf* in, const exg_pmf* out_len, int32_t target_len, double latency_bound_s,
+                             uint32_t strategy_mask, const exg_search_opts* opts, exg_schedule* out,
+                             exg_estimate* est) {
+  return guarded([&] {
+    if (!p || !cluster || !out) throw std::invalid_argument("null argument");
+    check_spec(spec);
+    if (!(strategy_mask & (EXG_RRA | EXG_WAA_C | EXG_WAA_M))) throw std::invalid_argument("unknown strategy");
+    if (target_len < 1) throw std::invalid_argument("target_len < 1");
+    exg_search_opts o{0.02, 0.02, 256, 0, 8, 0};
+    if (opts) o = *opts;
+    exg::plan::Simulator S(p->p, *spec, *cluster, pmf_vec(in), pmf_vec(out_len), target_len,
+                           o.use_little_fraction != 0);
+    exg::plan::Found f;
+    if (!exg::plan::schedule_find(S, latency_bound_s, strategy_mask, o, &f))
+      return fail(EXG_E_INFEASIBLE, "no schedule satisfies the latency bound");
+    to_c(f.sched, out);
+    if (est) {
+      est->thrput_seq_s = f.est.thr;
+      est->thrput_tok_s = f.est.tok;
+      est->latency_s = f.est.lat;
+      est->perf_evals = f.evals;
+      est->feasible = f.est.feasible;
+    }
+    return EXG_OK;
+  });
+}
+
+exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* reqs, int32_t n, int32_t* out_tokens,
+                   double* out_latency_s, exg_run_stats* stats, const exg_run_opts* opts) {
+  return guarded([&] {
+    if (!ctx || !sched || (!reqs && n > 0)) throw std::invalid_argument("null argument");
+    if (n < 1) throw std::invalid_argument("empty request batch");
+    EXG_CUDA(cudaSetDevice(ctx->device));
+    if (sched->strategy != EXG_RRA)
+      return fail(EXG_E_INFEASIBLE, "WAA needs >= 2 GPUs (SPEC.md:233); this context has 1");
+    if (sched->tp_degree > 1 || sched->n_stages > 1)
+      return fail(EXG_E_INFEASIBLE, "schedule needs more GPUs than this context has");
+    exg::run_rra(*ctx->engine, *sched, reqs, n, out_tokens, out_latency_s, stats, opts);
+    return EXG_OK;
+  });
+}
+
+// ----------------------------------------------------------------- ops ----
+exg_status exg_op_weightgen(void* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t tensor_id,
+                            int32_t gain, int32_t transposed, int64_t canon_cols, int64_t row_off, int64_t col_off,
+                            void* stream) {
+  return guarded([&] {
+    exg::GenParams g{seed, tensor_id, gain, (float)(2.0 * std::sqrt(3.0) * 0.02), 0.2f, transposed, canon_cols,
+                     row_off, col_off};
+    exg::weightgen((exg::bf16*)dst, rows, cols, ld, g, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_linear(const void* X, int64_t ldx, const void* W, int64_t ldw, int32_t tokens, int32_t features,
+                         int32_t K, int32_t mode, int32_t act, const void* bias, void* out, int64_t ldo, float* resid,
+                         int64_t ldr, int32_t decode, int32_t split, float* ws, void* stream) {
+  return guarded([&] {
+    if (K % 8) throw std::invalid_argument("K must be a multiple of 8");
+    exg::LinearArgs a;
+    a.X = (const exg::bf16*)X;
+    a.ldx = ldx;
+    a.W = (const exg::bf16*)W;
+    a.ldw = ldw;
+    a.K = K;
+    a.ep.mode = mode;
+    a.ep.act = act;
+    a.ep.bias = (const exg::bf16*)bias;
+    a.ep.out_bf16 = (exg::bf16*)out;
+    a.ep.out_f32 = (float*)out;
+    a.ep.ldo = ldo;
+    a.ep.resid = resid;
+    a.ep.ldr = ldr;
+    a.ep.tokens = tokens;
+    a.ep.features = features;
+    a.decode = decode != 0;
+    a.split = split;
+    a.ws = ws;
+    exg::linear(a, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_layernorm(void* y, int64_t ldy, const float* x, int64_t ldx, const void* g, const void* b, int32_t T,
+                            int32_t d, float eps, void* stream) {
+  return guarded([&] {
+    exg::layernorm((exg::bf16*)y, ldy, x, ldx, (const exg::bf16*)g, (const exg::bf16*)b, T, d, eps,
+                   (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_embed(float* x, const int32_t* ids, const int32_t* pos, const void* tok_emb, const void* pos_emb,
+                        int32_t T, int32_t d, void* stream) {
+  return guarded([&] {
+    exg::embed(x, ids, pos, (const exg::bf16*)tok_emb, (const exg::bf16*)pos_emb, T, d, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_kv_scatter(void* kc, void* vc, const void* qkv, const int32_t* slot, const int32_t* pos, int32_t T,
+                             int32_t H, int32_t dh, int32_t max_ctx, void* stream) {
+  return guarded([&] {
+    exg::kv_scatter((exg::bf16*)kc, (exg::bf16*)vc, (const exg::bf16*)qkv, slot, pos, T, H, dh, max_ctx,
+                    (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, const void* vc, const int32_t* slot,
+                                   const int32_t* n_keys, void* out, int64_t ldo, int32_t B, int32_t H, int32_t dh,
+                                   int32_t max_ctx, float scale, int32_t split_len, int32_t max_splits, float* partial,
+                                   void* stream) {
+  return guarded([&] {
+    if (max_splits > 1 && !partial) throw std::invalid_argument("max_splits > 1 needs a partial buffer");
+    exg::DecodeAttnArgs a;
+    a.q = (const exg::bf16*)q;
+    a.ldq = ldq;
+    a.kc = (const exg::bf16*)kc;
+    a.vc = (const exg::bf16*)vc;
+    a.slot = slot;
+    a.n_keys = n_keys;
+    a.out = (exg::bf16*)out;
+    a.ldo = ldo;
+    a.B = B;
+    a.H = H;
+    a.dh = dh;
+    a.max_ctx = max_ctx;
+    a.scale = scale;
+    a.split_len = split_len;
+    a.max_splits = max_splits;
+    a.partial = partial;
+    exg::decode_attention(a, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, const void* vc,
+                                    const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0, int32_t R,
+                                    int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh, int32_t max_ctx,
+                                    float scale, void* stream) {
+  return guarded([&] {
+    exg::PrefillAttnArgs a{(const exg::bf16*)q, ldq, (const exg::bf16*)kc, (const exg::bf16*)vc, cu_seqlens, slot,
+                           pos0, R, max_len, (exg::bf16*)out, ldo, H, dh, max_ctx, scale};
+    exg::prefill_attention(a, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_argmax(int32_t* out, const float* logits, int64_t ld, int32_t B, int32_t V, int32_t* err_flag,
+                         void* stream) {
+  return guarded([&] {
+    exg::argmax_rows(out, logits, ld, B, V, err_flag, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+int32_t exg_op_decode_split_k(int32_t features, int32_t K) { return exg::decode_split_k(features, K); }
+
+}  // extern "C"

@@ -1,0 +1,370 @@
+// Engine: seeded weights, workspace, encode / decode forward passes.
+//
+// Layer (pre-LN) with the rounding points of T4:
+//   h   = bf16(LN1(x))                 x: fp32 residual
+//   qkv = bf16(h W_qkv + b)            -> K,V scattered into the row's slot
+//   ctx = bf16(attention(q, K, V))     fp32 scores / softmax / P.V
+//   x  += ctx W_o + b_o                fp32 epilogue
+//   h   = bf16(LN2(x))
+//   f   = bf16(act(h W_1 + b_1))       act in fp32
+//   x  += f W_2 + b_2                  fp32 epilogue
+// final: logits = bf16(LN_f(x)) E^T (fp32), argmax.
+#include <cmath>
+#include <cstring>
+
+#include "engine.cuh"
+
+namespace exg {
+
+namespace {
+enum Kind {
+  K_TOK = 0, K_POS = 1, K_LN1G = 2, K_LN1B = 3, K_WQKV = 4, K_BQKV = 5, K_WO = 6, K_BO = 7, K_LN2G = 8,
+  K_LN2B = 9, K_W1 = 10, K_B1 = 11, K_W2 = 12, K_B2 = 13, K_LNFG = 14, K_LNFB = 15
+};
+inline uint64_t tid_of(int slot, int kind) { return (uint64_t)slot * 64 + kind; }
+
+__global__ void embed_decode_kernel(float* __restrict__ x, const int32_t* __restrict__ last_tok,
+                                    const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
+                                    const bf16* __restrict__ tok, const bf16* __restrict__ pe, int d) {
+  const int i = blockIdx.x;
+  const bf16* a = tok + (int64_t)last_tok[slot[i]] * d;
+  const bf16* b = pe + (int64_t)pos[i] * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) x[(int64_t)i * d + j] = __fadd_rn(bf2f(a[j]), bf2f(b[j]));
+}
+
+// argmax over a logits row, lowest index on ties, result scattered to the
+// request's output slot and to last_tok[slot] (the next iteration's input)
+__global__ void __launch_bounds__(256) argmax_scatter_kernel(const float* __restrict__ logits, int V,
+                                                              const int32_t* __restrict__ slot,
+                                                              const int32_t* __restrict__ out_off,
+                                                              int32_t* __restrict__ last_tok,
+                                                              int32_t* __restrict__ out_tokens, int32_t* err) {
+  __shared__ float sv[256];
+  __shared__ int si[256];
+  const float* row = logits + (int64_t)blockIdx.x * V;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  bool nan = false;
+  for (int j = threadIdx.x; j < V; j += 256) {
+    const float v = row[j];
+    if (v != v) nan = true;
+    if (v > best || (v == best && j < bi)) {
+      best = v;
+      bi = j;
+    }
+  }
+  if (nan) atomicExch(err, 1);
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const float ov = sv[threadIdx.x + s];
+      const int oi = si[threadIdx.x + s];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const int y = si[0] == 0x7fffffff ? 0 : si[0];
+    last_tok[slot[blockIdx.x]] = y;
+    if (out_tokens) out_tokens[out_off[blockIdx.x]] = y;
+  }
+}
+
+template <typename T>
+T* carve(uint8_t*& p, size_t n) {
+  T* r = reinterpret_cast<T*>(p);
+  p += (n * sizeof(T) + 255) & ~size_t(255);
+  return r;
+}
+}  // namespace
+
+Engine::Engine(const exg_model_spec& s, int device) : dev_(device) {
+  if (s.arch == EXG_ARCH_T5 || s.n_enc_layers != 0) throw std::invalid_argument("encoder-decoder models: not built yet");
+  D.arch = s.arch;
+  D.L = s.n_dec_layers;
+  D.d = s.d_model;
+  D.H = s.n_heads;
+  D.dh = s.d_head;
+  D.inner = s.n_heads * s.d_head;
+  D.ff = s.d_ff;
+  D.V = s.vocab;
+  D.max_pos = s.max_pos;
+  D.seed = s.weight_seed;
+  D.act = s.arch == EXG_ARCH_OPT ? ACT_RELU : ACT_GELU;
+  if (D.d % 64 || D.inner % 64 || D.ff % 64) throw std::invalid_argument("d, H*dh, d_ff must be multiples of 64");
+  if (D.dh != 16 && D.dh != 64 && D.dh != 128) throw std::invalid_argument("d_head must be 16, 64 or 128");
+  EXG_CUDA(cudaSetDevice(dev_));
+  EXG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  EXG_CUDA(cudaMalloc(&err_, sizeof(int32_t)));
+  EXG_CUDA(cudaMemsetAsync(err_, 0, sizeof(int32_t), st_));
+  split_qkv_ = decode_split_k(3 * D.inner, D.d);
+  split_o_ = decode_split_k(D.d, D.inner);
+  split_f1_ = decode_split_k(D.ff, D.d);
+  split_f2_ = decode_split_k(D.d, D.ff);
+  split_head_ = decode_split_k(D.V, D.d);
+  gen_weights();
+}
+
+Engine::~Engine() {
+  cudaSetDevice(dev_);
+  cudaStreamSynchronize(st_);
+  for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)last_tok_, (void*)err_, (void*)prof_tables_})
+    if (p) cudaFree(p);
+  if (st_) cudaStreamDestroy(st_);
+}
+
+void Engine::gen_weights() {
+  const size_t d = D.d, inner = D.inner, ff = D.ff;
+  auto al = [](size_t n) { return (n * 2 + 255) & ~size_t(255); };
+  size_t per_layer = al(d) * 4 + al(3 * inner * d) + al(3 * inner) + al(inner * d) + al(d) + al(ff * d) + al(ff) +
+                     al(d * ff) + al(d);
+  wbytes_ = al((size_t)D.V * d) + al((size_t)D.max_pos * d) + 2 * al(d) + per_layer * D.L;
+  EXG_CUDA(cudaMalloc(&wbuf_, wbytes_));
+  uint8_t* p = wbuf_;
+  const float c_mat = (float)(2.0 * std::sqrt(3.0) * 0.02);
+  const float c_gain = 0.2f;
+  auto gen = [&](bf16* dst, int64_t rows, int64_t cols, int slot, int kind, int gain, int transposed,
+                 int64_t canon_cols) {
+    GenParams g{D.seed, tid_of(slot, kind), gain, c_mat, c_gain, transposed, canon_cols, 0, 0};
+    weightgen(dst, rows, cols, cols, g, st_);
+  };
+  tok_emb_ = carve<bf16>(p, (size_t)D.V * d);
+  gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d);
+  pos_emb_ = carve<bf16>(p, (size_t)D.max_pos * d);
+  gen(pos_emb_, D.max_pos, d, 0, K_POS, 0, 0, d);
+  lnf_g_ = carve<bf16>(p, d);
+  gen(lnf_g_, 1, d, 0, K_LNFG, 1, 0, d);
+  lnf_b_ = carve<bf16>(p, d);
+  gen(lnf_b_, 1, d, 0, K_LNFB, 0, 0, d);
+  layers_.resize(D.L);
+  for (int l = 0; l < D.L; ++l) {
+    const int s = 1001 + l;
+    LayerW& w = layers_[l];
+    w.ln1_g = carve<bf16>(p, d);  gen(w.ln1_g, 1, d, s, K_LN1G, 1, 0, d);
+    w.ln1_b = carve<bf16>(p, d);  gen(w.ln1_b, 1, d, s, K_LN1B, 0, 0, d);
+    w.ln2_g = carve<bf16>(p, d);  gen(w.ln2_g, 1, d, s, K_LN2G, 1, 0, d);
+    w.ln2_b = carve<bf16>(p, d);  gen(w.ln2_b, 1, d, s, K_LN2B, 0, 0, d);
+    // matrices stored W^T [out][in] (K-major for tcgen05), canonical W[in][out]
+    w.Wqkv = carve<bf16>(p, 3 * inner * d);  gen(w.Wqkv, 3 * inner, d, s, K_WQKV, 0, 1, 3 * inner);
+    w.bqkv = carve<bf16>(p, 3 * inner);      gen(w.bqkv, 1, 3 * inner, s, K_BQKV, 0, 0, 3 * inner);
+    w.Wo = carve<bf16>(p, inner * d);        gen(w.Wo, d, inner, s, K_WO, 0, 1, d);
+    w.bo = carve<bf16>(p, d);                gen(w.bo, 1, d, s, K_BO, 0, 0, d);
+    w.W1 = carve<bf16>(p, ff * d);           gen(w.W1, ff, d, s, K_W1, 0, 1, ff);
+    w.b1 = carve<bf16>(p, ff);               gen(w.b1, 1, ff, s, K_B1, 0, 0, ff);
+    w.W2 = carve<bf16>(p, d * ff);           gen(w.W2, d, ff, s, K_W2, 0, 1, d);
+    w.b2 = carve<bf16>(p, d);                gen(w.b2, 1, d, s, K_B2, 0, 0, d);
+  }
+  EXG_CUDA(cudaStreamSynchronize(st_));
+}
+
+void Engine::ensure_workspace(int max_tokens, int max_rows) {
+  max_tokens = std::max(max_tokens, max_rows);
+  if (max_tokens <= cap_tokens_ && max_rows <= cap_rows_) return;
+  EXG_CUDA(cudaStreamSynchronize(st_));
+  if (x_) EXG_CUDA(cudaFree(x_));
+  cap_tokens_ = std::max(max_tokens, cap_tokens_);
+  cap_rows_ = std::max(max_rows, cap_rows_);
+  const size_t T = cap_tokens_, R = cap_rows_;
+  size_t sk = 0;
+  auto upd = [&](int split, int features) {
+    if (split > 1) sk = std::max(sk, (size_t)split * R * features);
+  };
+  upd(split_qkv_, 3 * D.inner);
+  upd(split_o_, D.d);
+  upd(split_f1_, D.ff);
+  upd(split_f2_, D.d);
+  upd(split_head_, D.V);
+  splitk_cap_ = sk;
+  max_splits_cap_ = (D.max_pos + split_len_ - 1) / split_len_;
+  const size_t parts = R * D.H * (size_t)max_splits_cap_ * (D.dh + 2);
+  auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t bytes = al(T * D.d * 4) + al(T * D.d * 2) + al(T * 3 * D.inner * 2) + al(T * D.inner * 2) +
+                       al(T * D.ff * 2) + al(R * D.V * 4) + al(sk * 4) + al(parts * 4);
+  uint8_t* p;
+  EXG_CUDA(cudaMalloc(&p, bytes));
+  x_ = carve<float>(p, T * D.d);
+  h_ = carve<bf16>(p, T * D.d);
+  qkv_ = carve<bf16>(p, T * 3 * D.inner);
+  ctx_ = carve<bf16>(p, T * D.inner);
+  ff_ = carve<bf16>(p, T * D.ff);
+  logits_ = carve<float>(p, R * D.V);
+  splitk_ws_ = carve<float>(p, sk);
+  attn_part_ = carve<float>(p, parts);
+  EXG_CUDA(cudaMemsetAsync(x_, 0, bytes, st_));
+}
+
+void Engine::ensure_kv(int slots, int slot_ctx, int layers) {
+  if (slot_ctx > D.max_pos) throw std::invalid_argument("slot_ctx exceeds max_pos");
+  if (layers < 0) layers = D.L;
+  if (slots <= kv_slots_ && slot_ctx == slot_ctx_ && layers <= kv_layers_) return;
+  EXG_CUDA(cudaStreamSynchronize(st_));
+  if (kv_) EXG_CUDA(cudaFree(kv_));
+  if (last_tok_) EXG_CUDA(cudaFree(last_tok_));
+  kv_ = nullptr;
+  last_tok_ = nullptr;
+  kv_slots_ = std::max(slots, 1);
+  slot_ctx_ = slot_ctx;
+  kv_layers_ = layers;
+  const size_t bytes = (size_t)layers * 2 * kv_layer_elems() * sizeof(bf16);
+  cudaError_t e = cudaMalloc(&kv_, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    kv_slots_ = 0;
+    kv_layers_ = 0;
+    throw std::bad_alloc();
+  }
+  EXG_CUDA(cudaMemsetAsync(kv_, 0, bytes, st_));
+  EXG_CUDA(cudaMalloc(&last_tok_, sizeof(int32_t) * kv_slots_));
+}
+
+void Engine::linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep) {
+  LinearArgs a;
+  a.X = X;
+  a.ldx = ldx;
+  a.W = W;
+  a.ldw = K;
+  a.K = K;
+  ep.tokens = tokens;
+  ep.features = features;
+  a.ep = ep;
+  a.decode = true;
+  a.split = decode_split_k(features, K);
+  a.ws = splitk_ws_;
+  linear(a, st_);
+}
+
+void Engine::linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep) {
+  LinearArgs a;
+  a.X = X;
+  a.ldx = ldx;
+  a.W = W;
+  a.ldw = K;
+  a.K = K;
+  ep.tokens = tokens;
+  ep.features = features;
+  a.ep = ep;
+  a.decode = false;
+  linear(a, st_);
+}
+
+static EpiParams epi_bf16(const bf16* bias, bf16* out, int64_t ldo, int act = ACT_NONE) {
+  EpiParams e;
+  e.mode = act == ACT_NONE ? EPI_BF16 : EPI_BF16_ACT;
+  e.act = act;
+  e.bias = bias;
+  e.out_bf16 = out;
+  e.ldo = ldo;
+  return e;
+}
+static EpiParams epi_resid(const bf16* bias, float* resid, int64_t ldr) {
+  EpiParams e;
+  e.mode = EPI_RESID;
+  e.bias = bias;
+  e.resid = resid;
+  e.ldr = ldr;
+  return e;
+}
+
+void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest) {
+  const LayerW& w = layers_[l];
+  const int T = eb.T, d = D.d, inner = D.inner;
+  const float scale = (float)(1.0 / std::sqrt((double)D.dh));
+  if (rest) {
+    layernorm(h_, d, x_, d, w.ln1_g, w.ln1_b, T, d, 1e-5f, st_);
+    linear_pre(h_, d, T, w.Wqkv, 3 * inner, d, epi_bf16(w.bqkv, qkv_, 3 * inner));
+    kv_scatter(kc(l), vc(l), qkv_, eb.tslot, eb.pos, T, D.H, D.dh, slot_ctx_, st_);
+  }
+  if (attn) {
+    PrefillAttnArgs pa{qkv_, 3 * inner, kc(l), vc(l), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,
+                       ctx_, inner, D.H, D.dh, slot_ctx_, scale};
+    prefill_attention(pa, st_);
+  }
+  if (rest) {
+    linear_pre(ctx_, inner, T, w.Wo, d, inner, epi_resid(w.bo, x_, d));
+    layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, T, d, 1e-5f, st_);
+    linear_pre(h_, d, T, w.W1, D.ff, d, epi_bf16(w.b1, ff_, D.ff, D.act));
+    linear_pre(ff_, D.ff, T, w.W2, d, D.ff, epi_resid(w.b2, x_, d));
+  }
+}
+
+void Engine::encode(const EncodeBatch& eb) {
+  if (eb.T <= 0) return;
+  if (eb.T > cap_tokens_) throw std::invalid_argument("encode batch exceeds workspace");
+  embed(x_, eb.ids, eb.pos, tok_emb_, pos_emb_, eb.T, D.d, st_);
+  for (int l = 0; l < D.L; ++l) layer_encode(l, eb, true, true);
+}
+
+void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest) {
+  const LayerW& w = layers_[l];
+  const int B = db.B, d = D.d, inner = D.inner;
+  const float scale = (float)(1.0 / std::sqrt((double)D.dh));
+  if (rest) {
+    layernorm(h_, d, x_, d, w.ln1_g, w.ln1_b, B, d, 1e-5f, st_);
+    linear_dec(h_, d, B, w.Wqkv, 3 * inner, d, epi_bf16(w.bqkv, qkv_, 3 * inner));
+    kv_scatter(kc(l), vc(l), qkv_, db.slot, db.pos, B, D.H, D.dh, slot_ctx_, st_);
+  }
+  if (attn) {
+    DecodeAttnArgs da;
+    da.q = qkv_;
+    da.ldq = 3 * inner;
+    da.kc = kc(l);
+    da.vc = vc(l);
+    da.slot = db.slot;
+    da.n_keys = db.nkeys;
+    da.out = ctx_;
+    da.ldo = inner;
+    da.B = B;
+    da.H = D.H;
+    da.dh = D.dh;
+    da.max_ctx = slot_ctx_;
+    da.scale = scale;
+    da.split_len = split_len_;
+    da.max_splits = std::max(1, (db.max_keys + split_len_ - 1) / split_len_);
+    da.partial = attn_part_;
+    decode_attention(da, st_);
+  }
+  if (rest) {
+    linear_dec(ctx_, inner, B, w.Wo, d, inner, epi_resid(w.bo, x_, d));
+    layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, B, d, 1e-5f, st_);
+    linear_dec(h_, d, B, w.W1, D.ff, d, epi_bf16(w.b1, ff_, D.ff, D.act));
+    linear_dec(ff_, D.ff, B, w.W2, d, D.ff, epi_resid(w.b2, x_, d));
+  }
+}
+
+void Engine::decode(const DecodeBatch& db) {
+  const int B = db.B;
+  if (B <= 0) return;
+  if (B > cap_rows_) throw std::invalid_argument("decode batch exceeds workspace");
+  embed_decode_kernel<<<B, 256, 0, st_>>>(x_, last_tok_, db.slot, db.pos, tok_emb_, pos_emb_, D.d);
+  EXG_CHECK_LAUNCH();
+  for (int l = 0; l < D.L; ++l) layer_decode(l, db, true, true);
+  layernorm(h_, D.d, x_, D.d, lnf_g_, lnf_b_, B, D.d, 1e-5f, st_);
+  EpiParams e;
+  e.mode = EPI_F32;
+  e.out_f32 = logits_;
+  e.ldo = D.V;
+  linear_dec(h_, D.d, B, tok_emb_, D.V, D.d, e);
+  argmax_scatter_kernel<<<B, 256, 0, st_>>>(logits_, D.V, db.slot, db.out_off, last_tok_, db.out_tokens, err_);
+  EXG_CHECK_LAUNCH();
+}
+
+}  // namespace exg
+
+namespace exg {
+namespace {
+__global__ void set_last_tokens_kernel(int32_t* last_tok, const int32_t* rslot, const int32_t* tok, int n) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < n) last_tok[rslot[k]] = tok[k];
+}
+}  // namespace
+void set_last_tokens(int32_t* last_tok, const int32_t* rslot, const int32_t* tok, int n, cudaStream_t st) {
+  if (n <= 0) return;
+  set_last_tokens_kernel<<<(n + 127) / 128, 128, 0, st>>>(last_tok, rslot, tok, n);
+  EXG_CHECK_LAUNCH();
+}
+}  // namespace exg

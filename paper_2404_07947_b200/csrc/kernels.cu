@@ -1,0 +1,483 @@
+// Non-GEMM kernels (see kernels.cuh for the contracts).
+#include "kernels.cuh"
+
+namespace exg {
+
+// ============================================================================
+// K14 weight generator
+// ============================================================================
+__device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void weightgen_kernel(bf16* __restrict__ dst, int64_t rows, int64_t cols, int64_t ld, GenParams p) {
+  const int64_t n = rows * cols;
+  const uint64_t key = p.seed ^ (p.tensor_id << 40);
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / cols, c = e % cols;
+    const int64_t i = p.transposed ? (c + p.col_off) * p.canon_cols + (r + p.row_off)
+                                   : (r + p.row_off) * p.canon_cols + (c + p.col_off);
+    const uint64_t h = splitmix64(key ^ (uint64_t)i);
+    const float u = __fmul_rn((float)(uint32_t)(h >> 40), 5.9604644775390625e-08f);  // * 2^-24, exact
+    const float cen = __fsub_rn(u, 0.5f);                                           // exact
+    const float v = p.gain ? __fadd_rn(1.0f, __fmul_rn(cen, p.c_gain)) : __fmul_rn(cen, p.c_mat);
+    dst[r * ld + c] = __float2bfloat16_rn(v);
+  }
+}
+
+void weightgen(bf16* dst, int64_t rows, int64_t cols, int64_t ld, const GenParams& p, cudaStream_t st) {
+  const int64_t n = rows * cols;
+  if (n <= 0) return;
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  weightgen_kernel<<<blocks, 256, 0, st>>>(dst, rows, cols, ld, p);
+  EXG_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// K1 embedding
+// ============================================================================
+__global__ void embed_kernel(float* __restrict__ x, const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
+                             const bf16* __restrict__ tok, const bf16* __restrict__ pe, int d) {
+  const int t = blockIdx.x;
+  const bf16* a = tok + (int64_t)ids[t] * d;
+  const bf16* b = pe + (int64_t)pos[t] * d;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) x[(int64_t)t * d + j] = __fadd_rn(bf2f(a[j]), bf2f(b[j]));
+}
+
+void embed(float* x, const int32_t* ids, const int32_t* pos, const bf16* tok_emb, const bf16* pos_emb, int T, int d,
+           cudaStream_t st) {
+  if (T <= 0) return;
+  embed_kernel<<<T, 256, 0, st>>>(x, ids, pos, tok_emb, pos_emb, d);
+  EXG_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// K2 LayerNorm (fp32 statistics, biased variance)
+// ============================================================================
+__device__ __forceinline__ float block_sum_256(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += red[i];
+  return s;
+}
+
+__global__ void __launch_bounds__(256) layernorm_kernel(bf16* __restrict__ y, int64_t ldy, const float* __restrict__ x,
+                                                        int64_t ldx, const bf16* __restrict__ g,
+                                                        const bf16* __restrict__ b, int d, float eps) {
+  __shared__ float red[8];
+  const float* xr = x + (int64_t)blockIdx.x * ldx;
+  float s = 0.f;
+  for (int j = threadIdx.x; j < d; j += 256) s += xr[j];
+  const float mean = block_sum_256(s, red) / (float)d;
+  float q = 0.f;
+  for (int j = threadIdx.x; j < d; j += 256) {
+    const float c = xr[j] - mean;
+    q += c * c;
+  }
+  const float var = block_sum_256(q, red) / (float)d;
+  const float rstd = rsqrtf(var + eps);
+  bf16* yr = y + (int64_t)blockIdx.x * ldy;
+  for (int j = threadIdx.x; j < d; j += 256) yr[j] = f2bf((xr[j] - mean) * rstd * bf2f(g[j]) + bf2f(b[j]));
+}
+
+void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
+               float eps, cudaStream_t st) {
+  if (T <= 0) return;
+  layernorm_kernel<<<T, 256, 0, st>>>(y, ldy, x, ldx, g, b, d, eps);
+  EXG_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// K7 KV scatter
+// ============================================================================
+__global__ void kv_scatter_kernel(bf16* __restrict__ kc, bf16* __restrict__ vc, const bf16* __restrict__ qkv,
+                                  const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int T, int H,
+                                  int dh, int max_ctx) {
+  const int inner = H * dh;
+  const int chunks = inner / 8;  // 16-byte chunks per K (or V) row
+  const int64_t n = (int64_t)T * 2 * chunks;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int t = (int)(e / (2 * chunks));
+    const int rem = (int)(e % (2 * chunks));
+    const int which = rem / chunks, c = rem % chunks;
+    const int h = (c * 8) / dh, j = (c * 8) % dh;
+    const int4 v = *reinterpret_cast<const int4*>(qkv + (int64_t)t * 3 * inner + (1 + which) * inner + c * 8);
+    bf16* dst = (which ? vc : kc) + (((int64_t)slot[t] * H + h) * max_ctx + pos[t]) * dh + j;
+    *reinterpret_cast<int4*>(dst) = v;
+  }
+}
+
+void kv_scatter(bf16* kc, bf16* vc, const bf16* qkv, const int32_t* slot, const int32_t* pos, int T, int H, int dh,
+                int max_ctx, cudaStream_t st) {
+  if (T <= 0) return;
+  const int64_t n = (int64_t)T * 2 * (H * dh / 8);
+  const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
+  kv_scatter_kernel<<<blocks, 256, 0, st>>>(kc, vc, qkv, slot, pos, T, H, dh, max_ctx);
+  EXG_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// K6 ragged decode attention
+//
+// One CTA (4 warps) per (row, head, split).  Thread 0 streams the split's K
+// and V rows (contiguous per (slot, head)) through a 4-stage ring of
+// cp.async.bulk copies completing on mbarriers; every warp owns a fixed
+// subset of keys of each tile, keeps its own online-softmax state, and the
+// four warp states are merged at the end in warp order.
+// ============================================================================
+template <int DH>
+struct DecodeCfg {
+  static constexpr int CH = DH / 8;                 // 16-byte chunks per key row
+  static constexpr int LPK = CH >= 4 ? 4 : CH;      // lanes per key (dot product)
+  static constexpr int CPL = CH / LPK;              // chunks per lane
+  static constexpr int KPW = 32 / LPK;              // keys per warp per tile
+  static constexpr int KT = 4 * KPW;                // keys per tile
+  static constexpr int ROWB = DH * 2;               // bytes per key row
+  static constexpr int STAGES = 4;
+  static constexpr int DPL = DH >= 32 ? DH / 32 : 1;  // output dims per lane (P.V)
+  static constexpr size_t SMEM = (size_t)STAGES * KT * ROWB * 2;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a) {
+  using C = DecodeCfg<DH>;
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint8_t* sk = dsm;
+  uint8_t* sv = dsm + C::STAGES * C::KT * C::ROWB;
+  __shared__ uint64_t bar[C::STAGES];
+  __shared__ float qs[DH];
+  __shared__ float wm[4], wl[4];
+  __shared__ float wo[4][DH];
+
+  const int i = blockIdx.x / a.H, h = blockIdx.x % a.H;
+  const int sp = blockIdx.y;
+  const int nk = a.n_keys[i];
+  const int k_begin = sp * a.split_len;
+  if (k_begin >= nk) return;
+  const int n = min(nk - k_begin, a.split_len);
+  const int ntiles = (n + C::KT - 1) / C::KT;
+  const int nsplit = (nk + a.split_len - 1) / a.split_len;
+  const int64_t head_off = ((int64_t)a.slot[i] * a.H + h) * a.max_ctx + k_begin;
+  const bf16* kbase = a.kc + head_off * DH;
+  const bf16* vbase = a.vc + head_off * DH;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_barrier_init();
+  }
+  if (tid < DH) qs[tid] = bf2f(a.q[(int64_t)i * a.ldq + h * DH + tid]);
+  __syncthreads();
+
+  auto issue = [&](int t) {
+    const int s = t % C::STAGES;
+    const int nkt = min(C::KT, n - t * C::KT);
+    const uint32_t bytes = (uint32_t)nkt * C::ROWB;
+    mbar_arrive_expect_tx(&bar[s], 2 * bytes);
+    bulk_load(sk + s * C::KT * C::ROWB, kbase + (int64_t)t * C::KT * DH, bytes, &bar[s]);
+    bulk_load(sv + s * C::KT * C::ROWB, vbase + (int64_t)t * C::KT * DH, bytes, &bar[s]);
+  };
+  if (tid == 0)
+    for (int t = 0; t < min(C::STAGES, ntiles); ++t) issue(t);
+
+  const int part = lane % C::LPK;
+  const int g = lane / C::LPK;                     // key slot inside this warp's group
+  const int key_local = warp * C::KPW + g;         // key index inside a tile
+  const int rot = (C::CPL > 1) ? (g & 1) : 0;      // bank-conflict rotation
+  float qreg[C::CPL * 8];
+#pragma unroll
+  for (int j = 0; j < C::CPL; ++j) {
+    const int chunk = ((j + rot) % C::CPL) * C::LPK + part;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qreg[j * 8 + e] = qs[chunk * 8 + e];
+  }
+
+  float m = -INFINITY, l = 0.f;
+  float o[C::DPL];
+#pragma unroll
+  for (int d = 0; d < C::DPL; ++d) o[d] = 0.f;
+  const bool pv_lane = lane * C::DPL < DH;
+
+  for (int t = 0; t < ntiles; ++t) {
+    const int s = t % C::STAGES;
+    mbar_wait(&bar[s], (t / C::STAGES) & 1);
+    const int nkt = min(C::KT, n - t * C::KT);
+    const uint8_t* krow = sk + s * C::KT * C::ROWB;
+    const uint8_t* vrow = sv + s * C::KT * C::ROWB;
+    float dot = 0.f;
+    const bool valid = key_local < nkt;
+    if (valid) {
+#pragma unroll
+      for (int j = 0; j < C::CPL; ++j) {
+        const int chunk = ((j + rot) % C::CPL) * C::LPK + part;
+        const int4 raw = *reinterpret_cast<const int4*>(krow + key_local * C::ROWB + chunk * 16);
+        const __nv_bfloat162* kv2 = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float2 f = __bfloat1622float2(kv2[e]);
+          dot = fmaf(qreg[j * 8 + 2 * e], f.x, dot);
+          dot = fmaf(qreg[j * 8 + 2 * e + 1], f.y, dot);
+        }
+      }
+    }
+#pragma unroll
+    for (int o2 = 1; o2 < C::LPK; o2 <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
+    const float score = valid ? dot * a.scale : -INFINITY;
+    const float tmax = warp_max(score);
+    const float m_new = fmaxf(m, tmax);
+    const float alpha = (m == -INFINITY) ? 0.f : __expf(m - m_new);
+    const float p = valid ? __expf(score - m_new) : 0.f;
+    const float psum = warp_sum(part == 0 ? p : 0.f);
+    l = l * alpha + psum;
+#pragma unroll
+    for (int d = 0; d < C::DPL; ++d) o[d] *= alpha;
+    const int kw = min(C::KPW, nkt - warp * C::KPW);
+    for (int kk = 0; kk < kw; ++kk) {
+      const float pk = __shfl_sync(0xffffffffu, p, kk * C::LPK);
+      if (pv_lane) {
+        const bf16* vr = reinterpret_cast<const bf16*>(vrow + (warp * C::KPW + kk) * C::ROWB) + lane * C::DPL;
+        if constexpr (C::DPL == 4) {
+          const uint2 raw = *reinterpret_cast<const uint2*>(vr);
+          const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.x));
+          const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&raw.y));
+          o[0] = fmaf(pk, f0.x, o[0]);
+          o[1] = fmaf(pk, f0.y, o[1]);
+          o[2] = fmaf(pk, f1.x, o[2]);
+          o[3] = fmaf(pk, f1.y, o[3]);
+        } else {
+#pragma unroll
+          for (int d = 0; d < C::DPL; ++d) o[d] = fmaf(pk, bf2f(vr[d]), o[d]);
+        }
+      }
+    }
+    m = m_new;
+    __syncthreads();  // every warp is done with stage s
+    if (tid == 0 && t + C::STAGES < ntiles) issue(t + C::STAGES);
+  }
+
+  if (lane == 0) {
+    wm[warp] = m;
+    wl[warp] = l;
+  }
+  if (pv_lane) {
+#pragma unroll
+    for (int d = 0; d < C::DPL; ++d) wo[warp][lane * C::DPL + d] = o[d];
+  }
+  __syncthreads();
+  if (tid < DH) {
+    float M = wm[0];
+#pragma unroll
+    for (int w = 1; w < 4; ++w) M = fmaxf(M, wm[w]);
+    float L = 0.f, O = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const float c = (wm[w] == -INFINITY) ? 0.f : __expf(wm[w] - M);
+      L += wl[w] * c;
+      O += wo[w][tid] * c;
+    }
+    if (nsplit == 1) {
+      a.out[(int64_t)i * a.ldo + h * DH + tid] = f2bf(O / L);
+    } else {
+      float* pp = a.partial + (((int64_t)i * a.H + h) * a.max_splits + sp) * (DH + 2);
+      if (tid == 0) {
+        pp[0] = M;
+        pp[1] = L;
+      }
+      pp[2 + tid] = O;
+    }
+  }
+}
+
+template <int DH>
+__global__ void decode_combine_kernel(DecodeAttnArgs a) {
+  const int i = blockIdx.x / a.H, h = blockIdx.x % a.H;
+  const int nk = a.n_keys[i];
+  const int nsplit = (nk + a.split_len - 1) / a.split_len;
+  if (nsplit <= 1) return;
+  const float* base = a.partial + ((int64_t)i * a.H + h) * a.max_splits * (DH + 2);
+  float M = -INFINITY;
+  for (int s = 0; s < nsplit; ++s) M = fmaxf(M, base[s * (DH + 2)]);
+  for (int d = threadIdx.x; d < DH; d += blockDim.x) {
+    float L = 0.f, O = 0.f;
+    for (int s = 0; s < nsplit; ++s) {
+      const float* pp = base + s * (DH + 2);
+      const float c = __expf(pp[0] - M);
+      L += pp[1] * c;
+      O += pp[2 + d] * c;
+    }
+    a.out[(int64_t)i * a.ldo + h * DH + d] = f2bf(O / L);
+  }
+}
+
+template <int DH>
+void decode_attention_t(const DecodeAttnArgs& a, cudaStream_t st) {
+  using C = DecodeCfg<DH>;
+  static bool attr = false;
+  if (!attr) {
+    EXG_CUDA(cudaFuncSetAttribute(decode_attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    attr = true;
+  }
+  dim3 grid(a.B * a.H, a.max_splits);
+  decode_attn_kernel<DH><<<grid, 128, C::SMEM, st>>>(a);
+  EXG_CHECK_LAUNCH();
+  if (a.max_splits > 1) {
+    decode_combine_kernel<DH><<<a.B * a.H, DH < 32 ? 32 : DH, 0, st>>>(a);
+    EXG_CHECK_LAUNCH();
+  }
+}
+
+void decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
+  if (a.B <= 0) return;
+  switch (a.dh) {
+    case 16: decode_attention_t<16>(a, st); break;
+    case 64: decode_attention_t<64>(a, st); break;
+    case 128: decode_attention_t<128>(a, st); break;
+    default: throw CudaError("decode_attention: unsupported head dim " + std::to_string(a.dh));
+  }
+}
+
+// ============================================================================
+// K4 causal prefill attention (SIMT, fp32 softmax and P.V)
+//
+// CTA = 32 queries x 4 lanes of one (request, head); K/V tiles of 32 keys are
+// staged in shared memory; each lane owns DH/4 dims of q and of the output.
+// ============================================================================
+template <int DH>
+__global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
+  constexpr int QPB = 32, LPQ = 4, DPL = DH / LPQ, KTILE = 32;
+  __shared__ __align__(16) bf16 ks[KTILE][DH];
+  __shared__ __align__(16) bf16 vs[KTILE][DH];
+  const int r = blockIdx.z, h = blockIdx.y;
+  const int t0 = a.cu_seqlens[r], len = a.cu_seqlens[r + 1] - t0;
+  const int qb = blockIdx.x * QPB;
+  if (qb >= len) return;
+  const int tid = threadIdx.x, qi = tid / LPQ, part = tid % LPQ;
+  const int qidx = qb + qi;
+  const bool qvalid = qidx < len;
+  const int p0 = a.pos0[r];
+  const int my_pos = p0 + qidx;
+  const int64_t head_off = ((int64_t)a.slot[r] * a.H + h) * a.max_ctx;
+  const bf16* kbase = a.kc + head_off * DH;
+  const bf16* vbase = a.vc + head_off * DH;
+
+  float q[DPL], o[DPL];
+#pragma unroll
+  for (int d = 0; d < DPL; ++d) {
+    q[d] = qvalid ? bf2f(a.q[(int64_t)(t0 + qidx) * a.ldq + h * DH + part * DPL + d]) : 0.f;
+    o[d] = 0.f;
+  }
+  float m = -INFINITY, l = 0.f;
+  const int last_key = p0 + min(len, qb + QPB) - 1;  // inclusive, for the whole CTA
+  for (int kt = 0; kt <= last_key; kt += KTILE) {
+    const int nkt = min(KTILE, last_key + 1 - kt);
+    __syncthreads();
+    for (int e = tid; e < nkt * DH / 8; e += blockDim.x) {
+      const int row = e / (DH / 8), c = e % (DH / 8);
+      *reinterpret_cast<int4*>(&ks[row][c * 8]) =
+          *reinterpret_cast<const int4*>(kbase + (int64_t)(kt + row) * DH + c * 8);
+      *reinterpret_cast<int4*>(&vs[row][c * 8]) =
+          *reinterpret_cast<const int4*>(vbase + (int64_t)(kt + row) * DH + c * 8);
+    }
+    __syncthreads();
+    float sc[KTILE];
+    float tmax = -INFINITY;
+#pragma unroll 4
+    for (int j = 0; j < KTILE; ++j) {
+      float dot = 0.f;
+      if (j < nkt) {
+#pragma unroll
+        for (int d = 0; d < DPL; ++d) dot = fmaf(q[d], bf2f(ks[j][part * DPL + d]), dot);
+      }
+      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+      const bool ok = qvalid && j < nkt && (kt + j) <= my_pos;
+      sc[j] = ok ? dot * a.scale : -INFINITY;
+      tmax = fmaxf(tmax, sc[j]);
+    }
+    if (tmax == -INFINITY) continue;
+    const float m_new = fmaxf(m, tmax);
+    const float alpha = (m == -INFINITY) ? 0.f : __expf(m - m_new);
+    l *= alpha;
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) o[d] *= alpha;
+#pragma unroll 4
+    for (int j = 0; j < KTILE; ++j) {
+      if (sc[j] == -INFINITY) continue;
+      const float p = __expf(sc[j] - m_new);
+      l += p;
+#pragma unroll
+      for (int d = 0; d < DPL; ++d) o[d] = fmaf(p, bf2f(vs[j][part * DPL + d]), o[d]);
+    }
+    m = m_new;
+  }
+  if (qvalid) {
+    const float inv = 1.f / l;
+#pragma unroll
+    for (int d = 0; d < DPL; ++d) a.out[(int64_t)(t0 + qidx) * a.ldo + h * DH + part * DPL + d] = f2bf(o[d] * inv);
+  }
+}
+
+void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st) {
+  if (a.R <= 0 || a.max_len <= 0) return;
+  dim3 grid((a.max_len + 31) / 32, a.H, a.R);
+  switch (a.dh) {
+    case 16: prefill_attn_kernel<16><<<grid, 128, 0, st>>>(a); break;
+    case 64: prefill_attn_kernel<64><<<grid, 128, 0, st>>>(a); break;
+    case 128: prefill_attn_kernel<128><<<grid, 128, 0, st>>>(a); break;
+    default: throw CudaError("prefill_attention: unsupported head dim");
+  }
+  EXG_CHECK_LAUNCH();
+}
+
+// ============================================================================
+// K8 argmax (lowest index on ties)
+// ============================================================================
+__global__ void __launch_bounds__(256) argmax_kernel(int32_t* __restrict__ out, const float* __restrict__ logits,
+                                                      int64_t ld, int V, int32_t* err) {
+  __shared__ float sv[256];
+  __shared__ int si[256];
+  const float* row = logits + (int64_t)blockIdx.x * ld;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  bool nan = false;
+  for (int j = threadIdx.x; j < V; j += 256) {
+    const float v = row[j];
+    if (v != v) nan = true;
+    if (v > best || (v == best && j < bi)) {
+      best = v;
+      bi = j;
+    }
+  }
+  if (nan && err) atomicExch(err, 1);
+  sv[threadIdx.x] = best;
+  si[threadIdx.x] = bi;
+  __syncthreads();
+  for (int s = 128; s > 0; s >>= 1) {
+    if (threadIdx.x < s) {
+      const float ov = sv[threadIdx.x + s];
+      const int oi = si[threadIdx.x + s];
+      if (ov > sv[threadIdx.x] || (ov == sv[threadIdx.x] && oi < si[threadIdx.x])) {
+        sv[threadIdx.x] = ov;
+        si[threadIdx.x] = oi;
+      }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = si[0] == 0x7fffffff ? 0 : si[0];
+}
+
+void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, int32_t* err_flag, cudaStream_t st) {
+  if (B <= 0) return;
+  argmax_kernel<<<B, 256, 0, st>>>(out, logits, ld, V, err_flag);
+  EXG_CHECK_LAUNCH();
+}
+
+}  // namespace exg

@@ -1,0 +1,87 @@
+// Non-GEMM kernels of the hot path: K14 weight generator,
+// K1 embedding, K2 LayerNorm, K7 KV scatter/append, K6 ragged decode
+// attention, K4 prefill attention, K8 argmax, K9 row compaction.
+#pragma once
+#include "common.cuh"
+
+namespace exg {
+
+// ---- K14: seeded weights -----------------------------
+// dst is a [rows][cols] bf16 matrix (leading dim ld).  Element (r, c) takes
+// the canonical index
+//   transposed = 0: i = (r + row_off) * canon_cols + (c + col_off)
+//   transposed = 1: i = (c + col_off) * canon_cols + (r + row_off)
+// (transposed = 1 stores W^T[out][in] of a canonical W[in][out]).
+struct GenParams {
+  uint64_t seed;
+  uint64_t tensor_id;
+  int gain;            // 1: 1 + U(+-0.1); 0: U(+-sqrt(3) sigma)
+  float c_mat;         // fp32(2 sqrt(3) sigma)
+  float c_gain;        // fp32(0.2)
+  int transposed;
+  int64_t canon_cols;
+  int64_t row_off, col_off;
+};
+void weightgen(bf16* dst, int64_t rows, int64_t cols, int64_t ld, const GenParams& p, cudaStream_t st);
+
+// ---- K1: x[t] = tok_emb[ids[t]] + pos_emb[pos[t]]  (fp32 residual) ---------
+void embed(float* x, const int32_t* ids, const int32_t* pos, const bf16* tok_emb, const bf16* pos_emb, int T,
+           int d, cudaStream_t st);
+
+// ---- K2: y = bf16(LN(x) * g + b), fp32 statistics, eps 1e-5 ----------------
+void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
+               float eps, cudaStream_t st);
+
+// ---- K7: scatter the K,V columns of a fused qkv buffer into cache slots -----
+// qkv: [T][3*inner] bf16; token t goes to (slot[t], pos[t]).
+// Cache layout per layer: [slot][H][max_ctx][dh] for K and for V.
+void kv_scatter(bf16* kc, bf16* vc, const bf16* qkv, const int32_t* slot, const int32_t* pos, int T, int H,
+                int dh, int max_ctx, cudaStream_t st);
+
+// ---- K6: ragged decode attention -------------------------------------------
+// Row i attends with q_i (head h at q + i*ldq + h*dh) over keys 0..n_keys[i]-1
+// of slot[i].  out[i][h*dh..] = bf16(softmax(fp32(q.k) * scale) . V).
+// Keys are processed in fixed chunks of `split_len` (a constant of the
+// model, never the batch) -- splits > 1 are merged by a combine pass in
+// split order, so a row's bits never depend on its batch-mates (T13).
+struct DecodeAttnArgs {
+  const bf16* q;
+  int64_t ldq;
+  const bf16* kc;
+  const bf16* vc;
+  const int32_t* slot;
+  const int32_t* n_keys;
+  bf16* out;
+  int64_t ldo;
+  int B, H, dh, max_ctx;
+  float scale;
+  int split_len;
+  int max_splits;      // >= ceil(max_i n_keys[i] / split_len)
+  float* partial;      // [B][H][max_splits][dh + 2] when max_splits > 1
+};
+void decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
+
+// ---- K4: causal prefill attention over packed variable-length requests -----
+// Token t of request r (cu_seqlens[r] <= t < cu_seqlens[r+1]) sits at
+// position pos0[r] + (t - cu_seqlens[r]) of slot[r]; it attends to cached
+// keys 0..its own position (the keys must already be scattered).
+struct PrefillAttnArgs {
+  const bf16* q;
+  int64_t ldq;
+  const bf16* kc;
+  const bf16* vc;
+  const int32_t* cu_seqlens;   // [R+1]
+  const int32_t* slot;         // [R]
+  const int32_t* pos0;         // [R]
+  int R, max_len;
+  bf16* out;
+  int64_t ldo;
+  int H, dh, max_ctx;
+  float scale;
+};
+void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);
+
+// ---- K8: greedy argmax per row (lowest index wins ties; NaN -> err flag) ---
+void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, int32_t* err_flag, cudaStream_t st);
+
+}  // namespace exg

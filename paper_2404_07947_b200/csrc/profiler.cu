@@ -1,0 +1,156 @@
+// XProfiler: "for a single encoding and decoding layer,
+// the profiler separately measures the execution times of the attention
+// kernel and the rest of the encoding/decoding layer ... sweeps across batch
+// sizes and, for each batch size, ... over possible sequence lengths.  For
+// the latter, ... sweeping input sizes (batch x input length)."
+//
+// Each point runs the real sm_100a kernels of one layer (layer 0) on
+// synthetic tables, 1 warm-up + `reps` timed repetitions, CUDA events on the
+// engine stream, median kept.  TP degree 1 on a single-GPU context (TP>1
+// all-reduce and PP send timings need a multi-rank context).
+#include <algorithm>
+#include <vector>
+
+#include "profiler.h"
+
+namespace exg {
+
+namespace {
+struct Timer {
+  cudaEvent_t a, b;
+  cudaStream_t st;
+  explicit Timer(cudaStream_t s) : st(s) {
+    EXG_CUDA(cudaEventCreate(&a));
+    EXG_CUDA(cudaEventCreate(&b));
+  }
+  ~Timer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  template <class F>
+  double median(int reps, F&& f) {
+    f();  // warm-up
+    std::vector<double> v;
+    for (int r = 0; r < reps; ++r) {
+      EXG_CUDA(cudaEventRecord(a, st));
+      f();
+      EXG_CUDA(cudaEventRecord(b, st));
+      EXG_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      EXG_CUDA(cudaEventElapsedTime(&ms, a, b));
+      v.push_back(ms * 1e-3);
+    }
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  }
+};
+}  // namespace
+
+void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
+  if (g.n_batch < 1 || g.n_ctx < 1 || g.n_tokens < 1) throw std::invalid_argument("empty profile grid");
+  const Dims& D = E.dims();
+  const int reps = std::max(1, g.reps);
+  std::vector<int> bs(g.batch, g.batch + g.n_batch), cs(g.ctx, g.ctx + g.n_ctx), ts(g.tokens, g.tokens + g.n_tokens);
+  for (auto* v : {&bs, &cs, &ts})
+    for (size_t i = 0; i < v->size(); ++i)
+      if ((*v)[i] < 1 || (i && (*v)[i] <= (*v)[i - 1])) throw std::invalid_argument("grid axes must be increasing, >= 1");
+  const int max_b = bs.back(), max_c = std::min(cs.back(), D.max_pos), max_t = ts.back();
+  const int max_enc_tokens = std::max(max_t, max_b * max_c);
+  const int ctx_cap = max_c;
+  const int slots = std::max(max_b, (max_enc_tokens + ctx_cap - 1) / ctx_cap);
+  E.ensure_kv(slots, ctx_cap, 1);
+  E.ensure_workspace(max_enc_tokens, std::max(max_b, max_t));
+  cudaStream_t st = E.stream();
+
+  // synthetic tables: token t -> (slot t / ctx_cap, pos t % ctx_cap)
+  const int n_tok = max_enc_tokens;
+  std::vector<int32_t> h_ids(n_tok), h_pos(n_tok), h_slot(n_tok);
+  for (int t = 0; t < n_tok; ++t) {
+    h_ids[t] = t % D.V;
+    h_pos[t] = t % ctx_cap;
+    h_slot[t] = t / ctx_cap;
+  }
+  int32_t* d;
+  const size_t nints = (size_t)3 * n_tok + 4 * (slots + 1);
+  EXG_CUDA(cudaMalloc(&d, nints * sizeof(int32_t)));
+  int32_t *d_ids = d, *d_pos = d + n_tok, *d_slot = d + 2 * n_tok;
+  int32_t *d_cu = d + 3 * n_tok, *d_rs = d_cu + slots + 1, *d_p0 = d_rs + slots + 1, *d_aux = d_p0 + slots + 1;
+  EXG_CUDA(cudaMemcpy(d_ids, h_ids.data(), n_tok * 4, cudaMemcpyHostToDevice));
+  EXG_CUDA(cudaMemcpy(d_pos, h_pos.data(), n_tok * 4, cudaMemcpyHostToDevice));
+  EXG_CUDA(cudaMemcpy(d_slot, h_slot.data(), n_tok * 4, cudaMemcpyHostToDevice));
+  std::vector<int32_t> h_rs(slots + 1), h_p0(slots + 1, 0);
+  for (int i = 0; i <= slots; ++i) h_rs[i] = i;
+  EXG_CUDA(cudaMemcpy(d_rs, h_rs.data(), (slots + 1) * 4, cudaMemcpyHostToDevice));
+  EXG_CUDA(cudaMemcpy(d_p0, h_p0.data(), (slots + 1) * 4, cudaMemcpyHostToDevice));
+
+  Timer tm(st);
+  plan::Profile& P = *out;
+  P = plan::Profile();
+  P.tps = {1};
+  plan::Table2D ae, ad;
+  ae.b.assign(bs.begin(), bs.end());
+  ae.c.assign(cs.begin(), cs.end());
+  ad = ae;
+  ae.t.assign(bs.size(), std::vector<double>(cs.size()));
+  ad.t.assign(bs.size(), std::vector<double>(cs.size()));
+  std::vector<int32_t> h_cu(slots + 1), h_nk(max_b);
+  for (size_t ib = 0; ib < bs.size(); ++ib) {
+    const int b = bs[ib];
+    for (size_t ic = 0; ic < cs.size(); ++ic) {
+      const int c = std::min(cs[ic], ctx_cap);
+      // encode attention: b requests of c tokens each, request k in slot k
+      for (int k = 0; k <= b; ++k) h_cu[k] = k * c;
+      EXG_CUDA(cudaMemcpy(d_cu, h_cu.data(), (b + 1) * 4, cudaMemcpyHostToDevice));
+      EncodeBatch eb;
+      eb.T = b * c;
+      eb.R = b;
+      eb.max_len = c;
+      eb.ids = d_ids;
+      eb.pos = d_pos;
+      eb.tslot = d_slot;
+      eb.cu = d_cu;
+      eb.rslot = d_rs;
+      eb.pos0 = d_p0;
+      ae.t[ib][ic] = tm.median(reps, [&] { E.layer_encode(0, eb, true, false); });
+      // decode attention: b rows, c keys each, row i in slot i
+      for (int i = 0; i < b; ++i) h_nk[i] = c;
+      EXG_CUDA(cudaMemcpy(d_aux, h_nk.data(), b * 4, cudaMemcpyHostToDevice));
+      DecodeBatch db;
+      db.B = b;
+      db.max_keys = c;
+      db.slot = d_rs;
+      db.pos = d_p0;
+      db.nkeys = d_aux;
+      ad.t[ib][ic] = tm.median(reps, [&] { E.layer_decode(0, db, true, false); });
+    }
+  }
+  P.attn[{"enc", 1}] = ae;
+  P.attn[{"dec", 1}] = ad;
+  plan::Table1D re, rd;
+  for (int T : ts) {
+    EncodeBatch eb;
+    eb.T = T;
+    eb.R = 1;
+    eb.max_len = T;
+    eb.ids = d_ids;
+    eb.pos = d_pos;
+    eb.tslot = d_slot;
+    re.x.push_back(T);
+    re.t.push_back(tm.median(reps, [&] { E.layer_encode(0, eb, false, true); }));
+    // decode rest: T rows (row i in slot i % slots, position 0)
+    DecodeBatch db;
+    db.B = T;
+    db.max_keys = 1;
+    db.slot = d_slot;  // t / ctx_cap
+    db.pos = d_pos;
+    db.nkeys = d_aux;
+    rd.x.push_back(T);
+    rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }));
+  }
+  P.rest[{"enc", 1}] = re;
+  P.rest[{"dec", 1}] = rd;
+  EXG_CUDA(cudaStreamSynchronize(st));
+  cudaFree(d);
+}
+
+}  // namespace exg

@@ -1,0 +1,318 @@
+// XRunner schedule executor (RRA PAPER.md:216-220).
+//
+// RRA cycle on one GPU: an encode phase admitting
+//   min(B_E, B_D - active, remaining)
+// requests FIFO, then N_D decode iterations over the active
+// rows; rows leave the batch the iteration they emit their last token (early
+// termination + compaction).  KV stays in its slot (slot
+// indirection), so compaction is a host row-table edit: the next iteration's
+// row table simply omits the finished rows.  When no requests remain the
+// decode phases drain without encoding.
+//
+// The host never waits on the GPU inside the loop: row tables go through a
+// ring of pinned staging buffers recycled by events, tokens are written by
+// the argmax kernel straight into a device output array, and times come from
+// events recorded at phase / iteration boundaries (one device clock).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <stdexcept>
+#include <vector>
+
+#include "engine.cuh"
+#include "runner.h"
+
+namespace exg {
+
+namespace {
+struct Staging {
+  struct Slot {
+    int32_t* host = nullptr;
+    cudaEvent_t ev = nullptr;
+    bool used = false;
+  };
+  std::vector<Slot> slots;
+  size_t cap_ints = 0;
+  int next = 0;
+  Staging(int n, size_t cap) : slots(n), cap_ints(cap) {
+    for (auto& s : slots) {
+      EXG_CUDA(cudaMallocHost(&s.host, cap * sizeof(int32_t)));
+      EXG_CUDA(cudaEventCreateWithFlags(&s.ev, cudaEventDisableTiming));
+    }
+  }
+  ~Staging() {
+    for (auto& s : slots) {
+      if (s.ev) cudaEventSynchronize(s.ev), cudaEventDestroy(s.ev);
+      if (s.host) cudaFreeHost(s.host);
+    }
+  }
+  Slot& acquire() {
+    Slot& s = slots[next];
+    next = (next + 1) % (int)slots.size();
+    if (s.used) EXG_CUDA(cudaEventSynchronize(s.ev));
+    s.used = true;
+    return s;
+  }
+};
+
+struct Row {
+  int req, slot, pos, emitted;
+};
+
+struct EventPool {
+  std::vector<cudaEvent_t> evs;
+  int used = 0;
+  cudaEvent_t get() {
+    if (used == (int)evs.size()) {
+      cudaEvent_t e;
+      EXG_CUDA(cudaEventCreate(&e));
+      evs.push_back(e);
+    }
+    return evs[used++];
+  }
+  ~EventPool() {
+    for (auto e : evs) cudaEventDestroy(e);
+  }
+};
+
+double pct(std::vector<double> v, double q) {
+  if (v.empty()) return 0.0;
+  std::sort(v.begin(), v.end());
+  const double r = q * (v.size() - 1);
+  const size_t lo = (size_t)std::floor(r), hi = (size_t)std::ceil(r);
+  return v[lo] + (r - lo) * (v[hi] - v[lo]);
+}
+}  // namespace
+
+void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, int32_t* out_tokens,
+             double* out_latency, exg_run_stats* stats, const exg_run_opts* opts) {
+  const Dims& D = E.dims();
+  if (s.strategy != EXG_RRA) throw std::invalid_argument("run_rra: strategy is not RRA");
+  if (s.b_e < 1 || s.b_d < s.b_e || s.n_d < 1) throw std::invalid_argument("RRA needs 1 <= B_E <= B_D, N_D >= 1");
+  int max_in = 1, max_ctx = 1;
+  int64_t total_out = 0;
+  std::vector<int64_t> base(n + 1, 0);
+  for (int r = 0; r < n; ++r) {
+    const exg_request& q = reqs[r];
+    if (q.input_len < 1 || q.output_len < 1 || !q.input_ids) throw std::invalid_argument("request lengths must be >= 1");
+    if (q.input_len + q.output_len > D.max_pos) throw std::invalid_argument("input_len + output_len > max_pos");
+    for (int j = 0; j < q.input_len; ++j)
+      if (q.input_ids[j] < 0 || q.input_ids[j] >= D.V) throw std::invalid_argument("token id out of range");
+    max_in = std::max(max_in, q.input_len);
+    max_ctx = std::max(max_ctx, q.input_len + q.output_len);
+    base[r + 1] = base[r] + q.output_len;
+  }
+  total_out = base[n];
+  const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : max_ctx;
+  if (slot_ctx < max_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
+  const int B_D = s.b_d, B_E = s.b_e;
+  E.ensure_kv(B_D, slot_ctx);
+  E.ensure_workspace(B_E * (max_in - 1), B_D);
+  cudaStream_t st = E.stream();
+
+  // device arrays: output tokens, encode tables, decode tables
+  int32_t* d_out = nullptr;
+  int32_t* d_tab = nullptr;
+  const size_t enc_ints = (size_t)3 * B_E * max_in + 3 * (B_E + 1) + 2 * B_E;
+  const size_t dec_ints = (size_t)4 * B_D;
+  const size_t tab_ints = std::max(enc_ints, dec_ints);
+  EXG_CUDA(cudaMalloc(&d_out, sizeof(int32_t) * std::max<int64_t>(total_out, 1)));
+  EXG_CUDA(cudaMalloc(&d_tab, sizeof(int32_t) * (enc_ints + dec_ints)));
+  int32_t* d_enc = d_tab;
+  int32_t* d_dec = d_tab + enc_ints;
+  Staging stage(64, tab_ints);
+  EventPool evp;
+  std::vector<float> dump_host;
+  const bool dumping = opts && opts->logits_out && opts->dump_mask;
+  std::vector<int64_t> dump_base(n + 1, 0);
+  if (dumping)
+    for (int r = 0; r < n; ++r) dump_base[r + 1] = dump_base[r] + (opts->dump_mask[r] ? reqs[r].output_len : 0);
+
+  std::vector<int> free_slots(B_D);
+  for (int i = 0; i < B_D; ++i) free_slots[i] = B_D - 1 - i;
+  std::vector<Row> active;
+  active.reserve(B_D);
+  std::vector<int> admit_ev(n, -1), done_ev(n, -1);
+  std::vector<cudaEvent_t> evs;
+  std::vector<int> ev_kind;        // 0 = phase start, 1 = encode end, 2 = iteration end
+  std::vector<int> ev_tokens;      // tokens emitted by the iteration ending at this event
+  auto record = [&](int kind, int toks) {
+    cudaEvent_t e = evp.get();
+    EXG_CUDA(cudaEventRecord(e, st));
+    evs.push_back(e);
+    ev_kind.push_back(kind);
+    ev_tokens.push_back(toks);
+    return (int)evs.size() - 1;
+  };
+
+  int next_req = 0;
+  int64_t decode_iters = 0, encode_phases = 0, batch_sum = 0;
+  EXG_CUDA(cudaMemsetAsync(E.err_flag(), 0, sizeof(int32_t), st));
+  record(0, 0);
+  while (next_req < n || !active.empty()) {
+    // ---------------- encode phase ----------------
+    const int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
+    const int ev_phase = record(0, 0);
+    if (admit > 0) {
+      Staging::Slot& sl = stage.acquire();
+      int32_t* h = sl.host;
+      int T = 0, maxlen = 0;
+      for (int k = 0; k < admit; ++k) T += reqs[next_req + k].input_len - 1;
+      int32_t* ids = h;
+      int32_t* pos = ids + T;
+      int32_t* tsl = pos + T;
+      int32_t* cu = tsl + T;
+      int32_t* rsl = cu + admit + 1;
+      int32_t* p0 = rsl + admit;
+      int32_t* last = p0 + admit;
+      int t = 0;
+      cu[0] = 0;
+      for (int k = 0; k < admit; ++k) {
+        const int r = next_req + k;
+        const exg_request& q = reqs[r];
+        const int slot = free_slots.back();
+        free_slots.pop_back();
+        for (int j = 0; j < q.input_len - 1; ++j, ++t) {
+          ids[t] = q.input_ids[j];
+          pos[t] = j;
+          tsl[t] = slot;
+        }
+        cu[k + 1] = t;
+        rsl[k] = slot;
+        p0[k] = 0;
+        last[k] = q.input_ids[q.input_len - 1];
+        maxlen = std::max(maxlen, q.input_len - 1);
+        active.push_back(Row{r, slot, q.input_len - 1, 0});
+        admit_ev[r] = ev_phase;
+      }
+      const size_t nints = (size_t)3 * T + (admit + 1) + 3 * admit;
+      EXG_CUDA(cudaMemcpyAsync(d_enc, h, nints * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      EXG_CUDA(cudaEventRecord(sl.ev, st));
+      // last_tok[slot] = x[n-1] for the admitted rows
+      set_last_tokens(E.last_tok(), d_enc + 3 * T + (admit + 1), d_enc + 3 * T + (admit + 1) + 2 * admit, admit, st);
+      EncodeBatch eb;
+      eb.T = T;
+      eb.R = admit;
+      eb.max_len = maxlen;
+      eb.ids = d_enc;
+      eb.pos = d_enc + T;
+      eb.tslot = d_enc + 2 * T;
+      eb.cu = d_enc + 3 * T;
+      eb.rslot = eb.cu + admit + 1;
+      eb.pos0 = eb.rslot + admit;
+      E.encode(eb);
+      next_req += admit;
+      ++encode_phases;
+    }
+    record(1, 0);
+    // ---------------- N_D decode iterations ----------------
+    for (int u = 0; u < s.n_d && !active.empty(); ++u) {
+      const int B = (int)active.size();
+      Staging::Slot& sl = stage.acquire();
+      int32_t* h = sl.host;
+      int max_keys = 0;
+      for (int i = 0; i < B; ++i) {
+        const Row& rw = active[i];
+        h[i] = rw.slot;
+        h[B + i] = rw.pos;
+        h[2 * B + i] = rw.pos + 1;
+        h[3 * B + i] = (int32_t)(base[rw.req] + rw.emitted);
+        max_keys = std::max(max_keys, rw.pos + 1);
+      }
+      EXG_CUDA(cudaMemcpyAsync(d_dec, h, (size_t)4 * B * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      EXG_CUDA(cudaEventRecord(sl.ev, st));
+      DecodeBatch db;
+      db.B = B;
+      db.max_keys = max_keys;
+      db.slot = d_dec;
+      db.pos = d_dec + B;
+      db.nkeys = d_dec + 2 * B;
+      db.out_off = d_dec + 3 * B;
+      db.out_tokens = d_out;
+      E.decode(db);
+      if (dumping) {
+        for (int i = 0; i < B; ++i) {
+          const Row& rw = active[i];
+          if (!opts->dump_mask[rw.req]) continue;
+          float* dst = opts->logits_out + (dump_base[rw.req] + rw.emitted) * (int64_t)D.V;
+          EXG_CUDA(cudaMemcpyAsync(dst, E.logits() + (int64_t)i * D.V, sizeof(float) * D.V, cudaMemcpyDeviceToHost, st));
+        }
+      }
+      const int ev_it = record(2, B);
+      ++decode_iters;
+      batch_sum += B;
+      // early termination + stable compaction of the row table
+      int w = 0;
+      for (int i = 0; i < B; ++i) {
+        Row rw = active[i];
+        rw.emitted += 1;
+        rw.pos += 1;
+        if (rw.emitted == reqs[rw.req].output_len) {
+          done_ev[rw.req] = ev_it;
+          free_slots.push_back(rw.slot);
+        } else {
+          active[w++] = rw;
+        }
+      }
+      active.resize(w);
+    }
+  }
+  EXG_CUDA(cudaStreamSynchronize(st));
+  int32_t err = 0;
+  EXG_CUDA(cudaMemcpy(&err, E.err_flag(), sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (out_tokens) EXG_CUDA(cudaMemcpy(out_tokens, d_out, sizeof(int32_t) * total_out, cudaMemcpyDeviceToHost));
+  cudaFree(d_out);
+  cudaFree(d_tab);
+  if (err) throw std::runtime_error("NaN logit encountered (T7)");
+
+  // ---------------- timing ----------------
+  const int nev = (int)evs.size();
+  std::vector<double> t(nev, 0.0);
+  for (int k = 1; k < nev; ++k) {
+    float ms = 0.f;
+    EXG_CUDA(cudaEventElapsedTime(&ms, evs[0], evs[k]));
+    t[k] = ms * 1e-3;
+  }
+  std::vector<double> lat(n);
+  for (int r = 0; r < n; ++r) {
+    lat[r] = t[done_ev[r]] - t[admit_ev[r]];
+    if (out_latency) out_latency[r] = lat[r];
+  }
+  if (stats) {
+    std::memset(stats, 0, sizeof(*stats));
+    const double wall = t[nev - 1] - t[0];
+    stats->wall_s = wall;
+    stats->out_tokens = total_out;
+    stats->decode_iters = decode_iters;
+    stats->encode_phases = encode_phases;
+    stats->tok_s = wall > 0 ? total_out / wall : 0;
+    stats->seq_s = wall > 0 ? n / wall : 0;
+    stats->lat_p50_s = pct(lat, 0.50);
+    stats->lat_p99_s = pct(lat, 0.99);
+    stats->lat_max_s = lat.empty() ? 0 : *std::max_element(lat.begin(), lat.end());
+    stats->mean_decode_batch = decode_iters ? (double)batch_sum / decode_iters : 0;
+    double enc = 0, dec = 0;
+    for (int k = 1; k < nev; ++k) {
+      if (ev_kind[k] == 1) enc += t[k] - t[k - 1];
+      if (ev_kind[k] == 2) dec += t[k] - t[k - 1];
+    }
+    stats->encode_s = enc;
+    stats->decode_s = dec;
+    // steady-state window: admission of request ceil(0.1 n) .. admission of
+    // the last request
+    const int r0 = std::min(n - 1, (int)std::ceil(0.1 * n));
+    const double w0 = t[admit_ev[r0]], w1 = t[admit_ev[n - 1]];
+    if (w1 > w0) {
+      int64_t toks = 0;
+      for (int k = 0; k < nev; ++k)
+        if (ev_kind[k] == 2 && t[k] > w0 && t[k] <= w1) toks += ev_tokens[k];
+      stats->tok_s_steady = toks / (w1 - w0);
+    } else {
+      stats->tok_s_steady = stats->tok_s;
+    }
+  }
+}
+
+}  // namespace exg

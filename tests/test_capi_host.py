@@ -1,0 +1,164 @@
+"""Host-side checks of libexegpt.so (no GPU needed):
+
+* the library loads and exports every symbol include/*.h declares;
+* the C++ planner (XSimulator + Algorithm 1) is bit-identical to the oracle
+  on the same profile-v1 file (test tier T1);
+* error statuses follow the header contract.
+"""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="session")
+def L():
+    from paper_2404_07947_b200 import _lib
+    from paper_2404_07947_b200.build import build
+    build()
+    return _lib
+
+
+def _declared_symbols():
+    names = set()
+    for h in ("exegpt.h", "exegpt_ops.h"):
+        txt = open(os.path.join(ROOT, "include", h)).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        for m in re.finditer(r"\b(exg_[a-z0-9_]+)\s*\(", txt):
+            names.add(m.group(1))
+    return names
+
+
+def test_library_exports_every_declared_symbol(L):
+    import ctypes
+    lib = ctypes.CDLL(L.LIB_PATH)
+    names = _declared_symbols()
+    assert len(names) >= 20
+    for n in sorted(names):
+        assert hasattr(lib, n), n
+    assert L.lib().exg_abi_version() == 1
+
+
+def _setup(task="S", model="opt-13b", n_gpus=1, mem=180e9, ws=4e9):
+    from oracle import simulator as sim
+    from workload import MODELS, task_dists
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_oracle_scheduler import _synthetic_profile
+    spec = MODELS[model]
+    m = sim.SimModel.from_spec(spec)
+    prof = _synthetic_profile(m)
+    d = task_dists(task)
+    return spec, m, prof, d, sim.SimCluster(n_gpus, mem, ws)
+
+
+def _c_objects(L, spec, prof, d, cl, tmp_path):
+    path = str(tmp_path / "prof.txt")
+    prof.save(path)
+    P = L.Profile.load(path)
+    mspec = L.model_spec(spec, 1)
+    ccl = L.cluster_spec(cl.n_gpus, cl.mem_per_gpu_bytes, cl.workspace_bytes)
+    return P, mspec, ccl, L.Pmf(d.pmf_in), L.Pmf(d.pmf_out)
+
+
+def test_profile_roundtrip_through_library(L, tmp_path):
+    spec, m, prof, d, cl = _setup()
+    P, *_ = _c_objects(L, spec, prof, d, cl, tmp_path)
+    out = str(tmp_path / "again.txt")
+    P.save(out)
+    assert open(out).read() == prof.dumps()
+
+
+@pytest.mark.parametrize("b_e,n_d", [(1, 1), (4, 7), (16, 13), (52, 13), (49, 7), (64, 80), (200, 3)])
+def test_simulate_rra_bit_identical(L, tmp_path, b_e, n_d):
+    from oracle import simulator as sim
+    spec, m, prof, d, cl = _setup()
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    S = sim.Simulator(prof, m, cl, d.pmf_in, d.pmf_out, d.target_len)
+    s_o = S.rra_schedule(b_e, n_d, 1, 0)
+    e_o = S.simulate(s_o)
+    s_c = L.rra_schedule(b_e, 0, n_d)
+    L.schedule_resolve(P, mspec, ccl, pin, pout, s_c)
+    assert s_c.b_d == s_o.b_d and s_c.stages() == s_o.stages
+    e_c = L.simulate(P, mspec, ccl, pin, pout, d.target_len, s_c)
+    assert bool(e_c.feasible) == e_o.feasible
+    if e_o.feasible:
+        assert e_c.thrput_seq_s == e_o.thrput_seq_s and e_c.latency_s == e_o.latency_s
+
+
+@pytest.mark.parametrize("n_gpus,t,c", [(4, 1, 0), (8, 2, 4), (8, 4, 8)])
+def test_simulate_pipeline_bit_identical(L, tmp_path, n_gpus, t, c):
+    from oracle import simulator as sim
+    spec, m, prof, d, cl = _setup("G", "opt-66b", n_gpus)
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    S = sim.Simulator(prof, m, cl, d.pmf_in, d.pmf_out, d.target_len)
+    for b_e, n_d in [(8, 10), (32, 50), (3, 480)]:
+        s_o = S.rra_schedule(b_e, n_d, t, c)
+        e_o = S.simulate(s_o)
+        s_c = L.rra_schedule(b_e, 0, n_d)
+        s_c.tp_degree, s_c.tp_gpus = t, c
+        L.schedule_resolve(P, mspec, ccl, pin, pout, s_c)
+        assert s_c.stages() == s_o.stages
+        e_c = L.simulate(P, mspec, ccl, pin, pout, d.target_len, s_c)
+        assert (e_c.thrput_seq_s, e_c.latency_s) == (e_o.thrput_seq_s, e_o.latency_s)
+    # WAA with partial TP on the decoder side
+    for b_e, M in [(2, 1), (4, 3), (8, 8)]:
+        s_o = S.waa_schedule(b_e, M, t, c if c <= n_gpus - 1 else 0)
+        if s_o is None:
+            continue
+        e_o = S.simulate(s_o)
+        s_c = L.exg_schedule()
+        s_c.strategy, s_c.b_e, s_c.tp_degree, s_c.tp_gpus = 2, b_e, s_o.tp_degree, s_o.tp_gpus
+        L.schedule_resolve(P, mspec, ccl, pin, pout, s_c, M)
+        assert (s_c.b_d, s_c.b_m, s_c.n_enc_gpus) == (s_o.b_d, s_o.b_m, s_o.n_enc_gpus)
+        assert s_c.stages() == s_o.stages
+        e_c = L.simulate(P, mspec, ccl, pin, pout, d.target_len, s_c)
+        assert (e_c.thrput_seq_s, e_c.latency_s) == (e_o.thrput_seq_s, e_o.latency_s)
+
+
+@pytest.mark.parametrize("task,model,n_gpus,mask", [("S", "opt-13b", 1, 1), ("S", "opt-13b", 4, 3),
+                                                    ("G", "opt-66b", 8, 3), ("C1", "gpt3-175b", 8, 3)])
+def test_schedule_find_bit_identical(L, tmp_path, task, model, n_gpus, mask):
+    from oracle import bnb, simulator as sim
+    spec, m, prof, d, cl = _setup(task, model, n_gpus)
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    S = sim.Simulator(prof, m, cl, d.pmf_in, d.pmf_out, d.target_len)
+    opts = bnb.SearchOpts(b_e_max=48, m_max=6)
+    copts = L.search_opts(b_e_max=48, m_max=6)
+    for L_b in (0.3, 1.0, 3.0, math.inf):
+        f = bnb.schedule_find(S, L_b, mask, opts)
+        if f is None:
+            with pytest.raises(L.ExgError) as ei:
+                L.schedule_find(P, mspec, ccl, pin, pout, d.target_len, L_b, mask, copts)
+            assert ei.value.status == L.EXG_E_INFEASIBLE
+            continue
+        s, est = L.schedule_find(P, mspec, ccl, pin, pout, d.target_len, L_b, mask, copts)
+        assert (s.strategy, s.b_e, s.b_d, s.b_m, s.n_d, s.tp_degree, s.tp_gpus, s.n_enc_gpus) == (
+            f.schedule.strategy, f.schedule.b_e, f.schedule.b_d, f.schedule.b_m, f.schedule.n_d,
+            f.schedule.tp_degree, f.schedule.tp_gpus, f.schedule.n_enc_gpus)
+        assert s.stages() == f.schedule.stages
+        assert est.thrput_seq_s == f.estimate.thrput_seq_s and est.latency_s == f.estimate.latency_s
+        assert est.perf_evals == f.evals
+        assert est.latency_s < L_b
+
+
+def test_error_statuses(L, tmp_path):
+    spec, m, prof, d, cl = _setup()
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    with pytest.raises(L.ExgError) as ei:
+        L.schedule_find(P, mspec, ccl, pin, pout, d.target_len, 1e-9, 1, L.search_opts())
+    assert ei.value.status == L.EXG_E_INFEASIBLE
+    with pytest.raises(L.ExgError) as ei:
+        L.schedule_find(P, mspec, ccl, pin, pout, 0, 1.0, 1, L.search_opts())
+    assert ei.value.status == L.EXG_E_INPUT
+    with pytest.raises(L.ExgError) as ei:
+        L.Profile.load(str(tmp_path / "missing.txt"))
+    assert ei.value.status == L.EXG_E_INPUT
+    bad = str(tmp_path / "bad.txt")
+    open(bad, "w").write("profile-v1\ntp 1 1\nbogus\n")
+    with pytest.raises(L.ExgError):
+        L.Profile.load(bad)

@@ -1,0 +1,111 @@
+"""End-to-end parity of the CUDA runner (exg_run through the C-ABI) with the
+oracle on config 1 (tiny model, RRA B_E=4, B_D=8, N_D=6; BASELINE.json
+configs[0]) -- SURVEY.md §8(c) T4/T4a:
+
+* greedy ids equal oracle mode (iii) (bf16-emulating KV loop), free-running;
+  a mismatch at a step whose oracle top-2 margin exceeds 2*tol is a hard
+  failure (tol = 2e-2);
+* logits within max-abs 2e-2 of mode (iii) on every step;
+* logits also compared with mode (ii) (fp64) teacher-forced on the run's own
+  prefix;
+* batch invariance (T13): every request run alone, and under another RRA
+  schedule, gives bit-identical ids and logits.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def setup():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2404_07947_b200 as X
+    from oracle import transformer as T
+    from workload import MODELS, config1_requests, weight_seed
+    spec = MODELS["tiny"]
+    seed = weight_seed(1)
+    reqs = config1_requests()
+    ctx = X.Context(spec, seed)
+    W = T.Weights(spec, seed)
+    ora = T.greedy_kv(W, reqs, "bf16", record_logits=True)
+    return X, T, spec, W, reqs, ctx, ora
+
+
+def test_config1_ids_and_logits(setup):
+    X, T, spec, W, reqs, ctx, ora = setup
+    toks, lat, stats, logits = ctx.run(X.rra_schedule(4, 8, 6), reqs, dump=range(len(reqs)))
+    worst = 0.0
+    for r, q in enumerate(reqs):
+        for t in range(q.output_len):
+            if toks[r][t] != ora.tokens[r][t]:
+                m = ora.margins[r][t]
+                assert m <= 2 * TOL, "hard mismatch req %d step %d margin %.4g" % (r, t, m)
+                pytest.fail("near-tie divergence req %d step %d (margin %.3g)" % (r, t, m))
+            worst = max(worst, float(np.abs(logits[r][t] - ora.logits[r][t]).max()))
+    assert worst <= TOL, worst
+    assert stats["out_tokens"] == sum(q.output_len for q in reqs)
+    assert stats["encode_phases"] >= 2 and stats["decode_iters"] >= max(q.output_len for q in reqs)
+    assert np.all(lat > 0)
+
+
+def test_config1_logits_vs_fp64_teacher_forced(setup):
+    X, T, spec, W, reqs, ctx, ora = setup
+    toks, _, _, logits = ctx.run(X.rra_schedule(4, 8, 6), reqs, dump=range(len(reqs)))
+    worst = 0.0
+    for r, q in enumerate(reqs):
+        tf = T.teacher_forced_logits(W, q, toks[r], "fp64")
+        for t in range(q.output_len):
+            worst = max(worst, float(np.abs(logits[r][t] - tf[t]).max()))
+    assert worst <= TOL, worst
+
+
+def test_batch_invariance_across_schedules(setup):
+    X, T, spec, W, reqs, ctx, ora = setup
+    base_t, _, _, base_l = ctx.run(X.rra_schedule(4, 8, 6), reqs, dump=range(len(reqs)))
+    for sched in (X.rra_schedule(1, 1, 1), X.rra_schedule(2, 3, 2), X.rra_schedule(8, 8, 24)):
+        t2, _, _, l2 = ctx.run(sched, reqs, dump=range(len(reqs)))
+        assert t2 == base_t
+        for r in range(len(reqs)):
+            assert np.array_equal(l2[r], base_l[r]), r
+    for r in range(len(reqs)):
+        t1, _, _, l1 = ctx.run(X.rra_schedule(1, 1, 3), [reqs[r]], dump=[0])
+        assert t1[0] == base_t[r] and np.array_equal(l1[0], base_l[r])
+
+
+def test_single_token_input_and_long_requests(setup):
+    X, T, spec, W, reqs, ctx, ora = setup
+    from workload import Request
+    rng = np.random.default_rng(0)
+    extra = [Request(np.array([5], np.int32), 1, 7),
+             Request(rng.integers(0, 512, 40).astype(np.int32), 40, 24),
+             Request(rng.integers(0, 512, 2).astype(np.int32), 2, 1)]
+    o = T.greedy_kv(W, extra, "bf16", record_logits=True)
+    toks, _, _, lg = ctx.run(X.rra_schedule(2, 3, 4), extra, dump=range(3))
+    for r in range(3):
+        n_ok = 0
+        for t in range(extra[r].output_len):
+            if toks[r][t] != o.tokens[r][t]:
+                assert o.margins[r][t] <= 2 * TOL
+                break
+            assert np.abs(lg[r][t] - o.logits[r][t]).max() <= TOL
+            n_ok += 1
+        assert n_ok >= 1
+
+
+def test_input_errors(setup):
+    X, T, spec, W, reqs, ctx, ora = setup
+    from workload import Request
+    with pytest.raises(X.ExgError) as ei:
+        ctx.run(X.rra_schedule(1, 1, 1), [Request(np.array([600], np.int32), 1, 2)])
+    assert ei.value.status == 1
+    with pytest.raises(X.ExgError) as ei:
+        ctx.run(X.rra_schedule(1, 1, 1), [Request(np.arange(60, dtype=np.int32), 60, 10)])
+    assert ei.value.status == 1
+    bad = X.rra_schedule(4, 2, 1)
+    with pytest.raises(X.ExgError):
+        ctx.run(bad, reqs)
