@@ -245,8 +245,8 @@ def test_kv_scatter_exact(L):
     kc = torch.zeros((3, H, max_ctx, dh), dtype=torch.bfloat16, device=dev())
     vc = torch.zeros_like(kc)
     tq = bf16_tensor(qkv)
-    _run(L, "exg_op_kv_scatter", ptr(kc), ptr(vc), ptr(tq), ptr(torch.from_numpy(slot).to(dev())),
-         ptr(torch.from_numpy(pos).to(dev())), T, H, dh, max_ctx, stream())
+    ts, tp = torch.from_numpy(slot).to(dev()), torch.from_numpy(pos).to(dev())   # keep alive
+    _run(L, "exg_op_kv_scatter", ptr(kc), ptr(vc), ptr(tq), ptr(ts), ptr(tp), T, H, dh, max_ctx, stream())
     torch.cuda.synchronize()
     K, V = to_np(kc), to_np(vc)
     for t in range(T):
@@ -261,9 +261,8 @@ def test_layernorm_parity(L):
         g = bf16_round_np(1 + 0.1 * rng.standard_normal(d))
         b = bf16_round_np(0.02 * rng.standard_normal(d))
         y = torch.zeros((T, d), dtype=torch.bfloat16, device=dev())
-        tx = torch.from_numpy(x).to(dev())
-        _run(L, "exg_op_layernorm", ptr(y), d, ptr(tx), d, ptr(bf16_tensor(g)), ptr(bf16_tensor(b)), T, d, 1e-5,
-             stream())
+        tx, tg, tb = torch.from_numpy(x).to(dev()), bf16_tensor(g), bf16_tensor(b)
+        _run(L, "exg_op_layernorm", ptr(y), d, ptr(tx), d, ptr(tg), ptr(tb), T, d, 1e-5, stream())
         torch.cuda.synchronize()
         xd = x.astype(np.float64)
         mu = xd.mean(1, keepdims=True)
@@ -279,8 +278,8 @@ def test_embed_exact(L):
     ids = rng.integers(0, V, T).astype(np.int32)
     pos = rng.integers(0, P, T).astype(np.int32)
     x = torch.zeros((T, d), dtype=torch.float32, device=dev())
-    _run(L, "exg_op_embed", ptr(x), ptr(torch.from_numpy(ids).to(dev())), ptr(torch.from_numpy(pos).to(dev())),
-         ptr(bf16_tensor(te)), ptr(bf16_tensor(pe)), T, d, stream())
+    keep = [torch.from_numpy(ids).to(dev()), torch.from_numpy(pos).to(dev()), bf16_tensor(te), bf16_tensor(pe)]
+    _run(L, "exg_op_embed", ptr(x), *[ptr(k) for k in keep], T, d, stream())
     torch.cuda.synchronize()
     ref = (te[ids].astype(np.float32) + pe[pos].astype(np.float32))
     assert np.array_equal(x.cpu().numpy(), ref)
