@@ -25,20 +25,33 @@ extern "C" {
 /* K14 -- seeded weights.  dst: bf16 [rows][ld]; element
  * (r,c) is value index i = transposed ? (c+col_off)*canon_cols + (r+row_off)
  * : (r+row_off)*canon_cols + (c+col_off) of tensor `tensor_id`;
- * gain = 1 for norm gains 1+U(+-0.1), else U(+-sqrt(3)*0.02). */
+ * gain = 1 for norm gains 1+U(+-0.1), else U(+-sqrt(3)*0.02).  blocked = 1
+ * writes the GEMM blocked layout (below) of the [rows][cols] matrix instead
+ * (ld ignored, exg_op_blocked_elems(rows, cols) elements, zero padded). */
 exg_status exg_op_weightgen(void* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t tensor_id,
                             int32_t gain, int32_t transposed, int64_t canon_cols, int64_t row_off, int64_t col_off,
-                            void* stream);
+                            int32_t blocked, void* stream);
 
-/* K3/K5/K8 -- Y[tokens][features] = X[tokens][K] . W[features][K]^T with
+/* GEMM weight layout: W [rows][K] is stored as 128 x 64 tiles, tile (m, kb)
+ * a contiguous 16 KB block at element (m*ceil(K/64) + kb) * 8192 holding
+ * row r's 8-element chunk c at r*64 + ((c ^ (r & 7)) * 8) (the SWIZZLE_128B
+ * shared-memory image), zero padded to whole tiles.  pack: row-major src
+ * [rows][ld] -> blocked dst. */
+exg_status exg_op_pack_weight(void* dst, const void* src, int64_t rows, int64_t K, int64_t ld, void* stream);
+int64_t exg_op_blocked_elems(int64_t rows, int64_t K);
+
+/* K3/K5/K8 -- Y[tokens][features] = X[tokens][K] . W[features][K]^T, X
+ * row-major with leading dim ldx, W given as Wb in the blocked layout, with
  * epilogue `mode`: 0 bf16(acc+bias) -> out; 1 bf16(act(acc+bias)) -> out
  * (act 1 = ReLU, 2 = GELU-tanh); 2 resid(fp32) += acc+bias; 3 fp32 acc+bias
  * -> out.  bias: bf16 [features] or NULL.  decode = 1 selects the swap-AB
- * tcgen05 path (tokens on the MMA N axis), else the prefill path; split > 1
- * reduces K in `split` fixed parts in order (ws: fp32 split*tokens*features). */
-exg_status exg_op_linear(const void* X, int64_t ldx, const void* W, int64_t ldw, int32_t tokens, int32_t features,
-                         int32_t K, int32_t mode, int32_t act, const void* bias, void* out, int64_t ldo, float* resid,
-                         int64_t ldr, int32_t decode, int32_t split, float* ws, void* stream);
+ * tcgen05 path (tokens on the MMA N axis) with a deterministic stream-K split
+ * of the weight stream (cut points depend on the weight shape only; ws:
+ * fp32 scratch of exg_op_decode_workspace(features, K, tokens) floats), else
+ * the data-parallel prefill path (ws unused). */
+exg_status exg_op_linear(const void* X, int64_t ldx, const void* Wb, int32_t tokens, int32_t features, int32_t K,
+                         int32_t mode, int32_t act, const void* bias, void* out, int64_t ldo, float* resid,
+                         int64_t ldr, int32_t decode, float* ws, int64_t ws_floats, void* stream);
 
 /* K2 -- y bf16 [T][ldy] = LN(x fp32 [T][ldx]) * g + b, eps, fp32 statistics. */
 exg_status exg_op_layernorm(void* y, int64_t ldy, const float* x, int64_t ldx, const void* g, const void* b, int32_t T,
@@ -76,8 +89,9 @@ exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, 
 exg_status exg_op_argmax(int32_t* out, const float* logits, int64_t ld, int32_t B, int32_t V, int32_t* err_flag,
                          void* stream);
 
-/* Split-K factor the runner uses for a decode GEMM of this weight shape. */
-int32_t exg_op_decode_split_k(int32_t features, int32_t K);
+/* fp32 scratch (floats) a decode GEMM of this weight shape needs for up to
+ * `tokens` rows (stream-K partial segments). */
+int64_t exg_op_decode_workspace(int32_t features, int32_t K, int32_t tokens);
 
 #ifdef __cplusplus
 }

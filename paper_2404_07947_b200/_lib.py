@@ -123,9 +123,11 @@ _SIGS = {
                           C.POINTER(C.c_double), C.POINTER(exg_run_stats), C.POINTER(exg_run_opts)]),
     # ops (device pointers as void*)
     "exg_op_weightgen": (C.c_int, [_P, C.c_int64, C.c_int64, C.c_int64, C.c_uint64, C.c_uint64, C.c_int32,
-                                   C.c_int32, C.c_int64, C.c_int64, C.c_int64, _P]),
-    "exg_op_linear": (C.c_int, [_P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                C.c_int32, _P, _P, C.c_int64, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P]),
+                                   C.c_int32, C.c_int64, C.c_int64, C.c_int64, C.c_int32, _P]),
+    "exg_op_pack_weight": (C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64, _P]),
+    "exg_op_blocked_elems": (C.c_int64, [C.c_int64, C.c_int64]),
+    "exg_op_linear": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                C.c_int32, _P, _P, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64, _P]),
     "exg_op_layernorm": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_float, _P]),
     "exg_op_embed": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, _P]),
     "exg_op_kv_scatter": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
@@ -134,7 +136,7 @@ _SIGS = {
     "exg_op_prefill_attention": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, C.c_int32, _P,
                                            C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_float, _P]),
     "exg_op_argmax": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P]),
-    "exg_op_decode_split_k": (C.c_int32, [C.c_int32, C.c_int32]),
+    "exg_op_decode_workspace": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
 }
 
 _lib = None

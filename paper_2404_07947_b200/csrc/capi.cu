@@ -270,25 +270,33 @@ exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* r
 // ----------------------------------------------------------------- ops ----
 exg_status exg_op_weightgen(void* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t tensor_id,
                             int32_t gain, int32_t transposed, int64_t canon_cols, int64_t row_off, int64_t col_off,
-                            void* stream) {
+                            int32_t blocked, void* stream) {
   return guarded([&] {
-    exg::GenParams g{seed, tensor_id, gain, (float)(2.0 * std::sqrt(3.0) * 0.02), 0.2f, transposed, canon_cols,
-                     row_off, col_off};
+    exg::GenParams g{seed,   tensor_id, gain,    (float)(2.0 * std::sqrt(3.0) * 0.02), 0.2f, transposed, canon_cols,
+                     row_off, col_off,  blocked};
     exg::weightgen((exg::bf16*)dst, rows, cols, ld, g, (cudaStream_t)stream);
     return EXG_OK;
   });
 }
 
-exg_status exg_op_linear(const void* X, int64_t ldx, const void* W, int64_t ldw, int32_t tokens, int32_t features,
-                         int32_t K, int32_t mode, int32_t act, const void* bias, void* out, int64_t ldo, float* resid,
-                         int64_t ldr, int32_t decode, int32_t split, float* ws, void* stream) {
+exg_status exg_op_pack_weight(void* dst, const void* src, int64_t rows, int64_t K, int64_t ld, void* stream) {
+  return guarded([&] {
+    exg::pack_blocked((exg::bf16*)dst, (const exg::bf16*)src, rows, K, ld, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+int64_t exg_op_blocked_elems(int64_t rows, int64_t K) { return exg::blocked_elems(rows, K); }
+
+exg_status exg_op_linear(const void* X, int64_t ldx, const void* Wb, int32_t tokens, int32_t features, int32_t K,
+                         int32_t mode, int32_t act, const void* bias, void* out, int64_t ldo, float* resid,
+                         int64_t ldr, int32_t decode, float* ws, int64_t ws_floats, void* stream) {
   return guarded([&] {
     if (K % 8) throw std::invalid_argument("K must be a multiple of 8");
     exg::LinearArgs a;
     a.X = (const exg::bf16*)X;
     a.ldx = ldx;
-    a.W = (const exg::bf16*)W;
-    a.ldw = ldw;
+    a.Wb = (const exg::bf16*)Wb;
     a.K = K;
     a.ep.mode = mode;
     a.ep.act = act;
@@ -301,8 +309,8 @@ exg_status exg_op_linear(const void* X, int64_t ldx, const void* W, int64_t ldw,
     a.ep.tokens = tokens;
     a.ep.features = features;
     a.decode = decode != 0;
-    a.split = split;
     a.ws = ws;
+    a.ws_floats = ws_floats > 0 ? (size_t)ws_floats : 0;
     exg::linear(a, (cudaStream_t)stream);
     return EXG_OK;
   });
@@ -382,6 +390,12 @@ exg_status exg_op_argmax(int32_t* out, const float* logits, int64_t ld, int32_t 
   });
 }
 
-int32_t exg_op_decode_split_k(int32_t features, int32_t K) { return exg::decode_split_k(features, K); }
+int64_t exg_op_decode_workspace(int32_t features, int32_t K, int32_t tokens) {
+  try {
+    return (int64_t)exg::decode_ws_floats(features, K, tokens);
+  } catch (...) {
+    return -1;
+  }
+}
 
 }  // extern "C"

@@ -27,9 +27,10 @@ __global__ void embed_decode_kernel(float* __restrict__ x, const int32_t* __rest
                                     const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
                                     const bf16* __restrict__ tok, const bf16* __restrict__ pe, int d) {
   const int i = blockIdx.x;
-  const bf16* a = tok + (int64_t)last_tok[slot[i]] * d;
+  const int64_t id = last_tok[slot[i]];
   const bf16* b = pe + (int64_t)pos[i] * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) x[(int64_t)i * d + j] = __fadd_rn(bf2f(a[j]), bf2f(b[j]));
+  for (int j = threadIdx.x; j < d; j += blockDim.x)
+    x[(int64_t)i * d + j] = __fadd_rn(bf2f(tok[blocked_index(id, j, d)]), bf2f(b[j]));
 }
 
 // argmax over a logits row, lowest index on ties, result scattered to the
@@ -102,11 +103,6 @@ Engine::Engine(const exg_model_spec& s, int device) : dev_(device) {
   EXG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   EXG_CUDA(cudaMalloc(&err_, sizeof(int32_t)));
   EXG_CUDA(cudaMemsetAsync(err_, 0, sizeof(int32_t), st_));
-  split_qkv_ = decode_split_k(3 * D.inner, D.d);
-  split_o_ = decode_split_k(D.d, D.inner);
-  split_f1_ = decode_split_k(D.ff, D.d);
-  split_f2_ = decode_split_k(D.d, D.ff);
-  split_head_ = decode_split_k(D.V, D.d);
   gen_weights();
 }
 
@@ -121,20 +117,24 @@ Engine::~Engine() {
 void Engine::gen_weights() {
   const size_t d = D.d, inner = D.inner, ff = D.ff;
   auto al = [](size_t n) { return (n * 2 + 255) & ~size_t(255); };
-  size_t per_layer = al(d) * 4 + al(3 * inner * d) + al(3 * inner) + al(inner * d) + al(d) + al(ff * d) + al(ff) +
-                     al(d * ff) + al(d);
-  wbytes_ = al((size_t)D.V * d) + al((size_t)D.max_pos * d) + 2 * al(d) + per_layer * D.L;
+  auto bl = [&](size_t rows, size_t K) { return al((size_t)blocked_elems(rows, K)); };
+  size_t per_layer = al(d) * 4 + bl(3 * inner, d) + al(3 * inner) + bl(d, inner) + al(d) + bl(ff, d) + al(ff) +
+                     bl(d, ff) + al(d);
+  wbytes_ = bl(D.V, d) + al((size_t)D.max_pos * d) + 2 * al(d) + per_layer * D.L;
   EXG_CUDA(cudaMalloc(&wbuf_, wbytes_));
   uint8_t* p = wbuf_;
   const float c_mat = (float)(2.0 * std::sqrt(3.0) * 0.02);
   const float c_gain = 0.2f;
   auto gen = [&](bf16* dst, int64_t rows, int64_t cols, int slot, int kind, int gain, int transposed,
-                 int64_t canon_cols) {
-    GenParams g{D.seed, tid_of(slot, kind), gain, c_mat, c_gain, transposed, canon_cols, 0, 0};
+                 int64_t canon_cols, int blocked = 0) {
+    GenParams g{D.seed, tid_of(slot, kind), gain, c_mat, c_gain, transposed, canon_cols, 0, 0, blocked};
     weightgen(dst, rows, cols, cols, g, st_);
   };
-  tok_emb_ = carve<bf16>(p, (size_t)D.V * d);
-  gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d);
+  auto carve_blk = [&](size_t rows, size_t K) { return carve<bf16>(p, (size_t)blocked_elems(rows, K)); };
+  // token embedding in the GEMM blocked layout: it is the A operand of the
+  // tied LM head (decode swap-AB); the embedding gather indexes it directly
+  tok_emb_ = carve_blk(D.V, d);
+  gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d, 1);
   pos_emb_ = carve<bf16>(p, (size_t)D.max_pos * d);
   gen(pos_emb_, D.max_pos, d, 0, K_POS, 0, 0, d);
   lnf_g_ = carve<bf16>(p, d);
@@ -149,15 +149,16 @@ void Engine::gen_weights() {
     w.ln1_b = carve<bf16>(p, d);  gen(w.ln1_b, 1, d, s, K_LN1B, 0, 0, d);
     w.ln2_g = carve<bf16>(p, d);  gen(w.ln2_g, 1, d, s, K_LN2G, 1, 0, d);
     w.ln2_b = carve<bf16>(p, d);  gen(w.ln2_b, 1, d, s, K_LN2B, 0, 0, d);
-    // matrices stored W^T [out][in] (K-major for tcgen05), canonical W[in][out]
-    w.Wqkv = carve<bf16>(p, 3 * inner * d);  gen(w.Wqkv, 3 * inner, d, s, K_WQKV, 0, 1, 3 * inner);
-    w.bqkv = carve<bf16>(p, 3 * inner);      gen(w.bqkv, 1, 3 * inner, s, K_BQKV, 0, 0, 3 * inner);
-    w.Wo = carve<bf16>(p, inner * d);        gen(w.Wo, d, inner, s, K_WO, 0, 1, d);
-    w.bo = carve<bf16>(p, d);                gen(w.bo, 1, d, s, K_BO, 0, 0, d);
-    w.W1 = carve<bf16>(p, ff * d);           gen(w.W1, ff, d, s, K_W1, 0, 1, ff);
-    w.b1 = carve<bf16>(p, ff);               gen(w.b1, 1, ff, s, K_B1, 0, 0, ff);
-    w.W2 = carve<bf16>(p, d * ff);           gen(w.W2, d, ff, s, K_W2, 0, 1, d);
-    w.b2 = carve<bf16>(p, d);                gen(w.b2, 1, d, s, K_B2, 0, 0, d);
+    // matrices stored W^T [out][in] (K-major for tcgen05) in the blocked,
+    // pre-swizzled GEMM layout; canonical index from W[in][out]
+    w.Wqkv = carve_blk(3 * inner, d);   gen(w.Wqkv, 3 * inner, d, s, K_WQKV, 0, 1, 3 * inner, 1);
+    w.bqkv = carve<bf16>(p, 3 * inner); gen(w.bqkv, 1, 3 * inner, s, K_BQKV, 0, 0, 3 * inner);
+    w.Wo = carve_blk(d, inner);         gen(w.Wo, d, inner, s, K_WO, 0, 1, d, 1);
+    w.bo = carve<bf16>(p, d);           gen(w.bo, 1, d, s, K_BO, 0, 0, d);
+    w.W1 = carve_blk(ff, d);            gen(w.W1, ff, d, s, K_W1, 0, 1, ff, 1);
+    w.b1 = carve<bf16>(p, ff);          gen(w.b1, 1, ff, s, K_B1, 0, 0, ff);
+    w.W2 = carve_blk(d, ff);            gen(w.W2, d, ff, s, K_W2, 0, 1, d, 1);
+    w.b2 = carve<bf16>(p, d);           gen(w.b2, 1, d, s, K_B2, 0, 0, d);
   }
   EXG_CUDA(cudaStreamSynchronize(st_));
 }
@@ -171,14 +172,9 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   cap_rows_ = std::max(max_rows, cap_rows_);
   const size_t T = cap_tokens_, R = cap_rows_;
   size_t sk = 0;
-  auto upd = [&](int split, int features) {
-    if (split > 1) sk = std::max(sk, (size_t)split * R * features);
-  };
-  upd(split_qkv_, 3 * D.inner);
-  upd(split_o_, D.d);
-  upd(split_f1_, D.ff);
-  upd(split_f2_, D.d);
-  upd(split_head_, D.V);
+  for (auto fk : {std::make_pair(3 * D.inner, D.d), std::make_pair(D.d, D.inner), std::make_pair(D.ff, D.d),
+                  std::make_pair(D.d, D.ff), std::make_pair(D.V, D.d)})
+    sk = std::max(sk, decode_ws_floats(fk.first, fk.second, (int)R));
   splitk_cap_ = sk;
   max_splits_cap_ = (D.max_pos + split_len_ - 1) / split_len_;
   const size_t parts = R * D.H * (size_t)max_splits_cap_ * (D.dh + 2);
@@ -226,15 +222,14 @@ void Engine::linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, i
   LinearArgs a;
   a.X = X;
   a.ldx = ldx;
-  a.W = W;
-  a.ldw = K;
+  a.Wb = W;
   a.K = K;
   ep.tokens = tokens;
   ep.features = features;
   a.ep = ep;
   a.decode = true;
-  a.split = decode_split_k(features, K);
   a.ws = splitk_ws_;
+  a.ws_floats = splitk_cap_;
   linear(a, st_);
 }
 
@@ -242,8 +237,7 @@ void Engine::linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, i
   LinearArgs a;
   a.X = X;
   a.ldx = ldx;
-  a.W = W;
-  a.ldw = K;
+  a.Wb = W;
   a.K = K;
   ep.tokens = tokens;
   ep.features = features;
@@ -295,7 +289,7 @@ void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest) {
 void Engine::encode(const EncodeBatch& eb) {
   if (eb.T <= 0) return;
   if (eb.T > cap_tokens_) throw std::invalid_argument("encode batch exceeds workspace");
-  embed(x_, eb.ids, eb.pos, tok_emb_, pos_emb_, eb.T, D.d, st_);
+  embed(x_, eb.ids, eb.pos, tok_emb_, pos_emb_, eb.T, D.d, st_, 1);
   for (int l = 0; l < D.L; ++l) layer_encode(l, eb, true, true);
 }
 

@@ -92,7 +92,6 @@ class Engine {
   bf16* kv_ = nullptr;
   int kv_slots_ = 0, slot_ctx_ = 0, kv_layers_ = 0;
   int32_t* last_tok_ = nullptr;
-  int split_qkv_ = 1, split_o_ = 1, split_f1_ = 1, split_f2_ = 1, split_head_ = 1;
   // profiler scratch tables
   int32_t* prof_tables_ = nullptr;
 

@@ -1,10 +1,22 @@
 // tcgen05 GEMM (K3 prefill, K5 decode swap-AB, K8 LM head).
 //
-// One 128 x BN output tile per CTA, K in 64-wide blocks through an
-// STAGES-deep TMA -> shared ring (SWIZZLE_128B, K-major), single-thread
-// tcgen05.mma issue with the fp32 accumulator in TMEM, 4 epilogue warps
-// draining TMEM with tcgen05.ld.  Warp roles: 0 = TMA producer, 1 = MMA
-// issuer, 2 = TMEM allocator, 4..7 = epilogue.
+// Persistent kernel, one CTA per SM.  128 x BN accumulator tiles in TMEM,
+// double buffered so the epilogue of one work unit overlaps the MMAs of the
+// next.  K streams in 64-wide blocks through an S-deep shared-memory ring
+// (SWIZZLE_128B, K-major): activations arrive by 2-D TMA, weights by 1-D bulk
+// copies of whole pre-swizzled 16 KB blocks (see gemm_tc.cuh).  Warp roles:
+// 0 = producer, 1 = MMA issuer (one thread), 2 = TMEM allocator,
+// 4..7 = epilogue (TMEM lanes 32*(w%4)..).
+//
+// Work decomposition
+//  * prefill (data-parallel): unit = whole tile, tiles t = cta, cta+G, ...
+//  * decode (stream-K): per BN-column chunk of tokens, the iteration space
+//    tiles_m x k-blocks is cut into G equal contiguous ranges (G = min(#SMs,
+//    iterations): a function of the weight shape only).  A tile cut by a range
+//    boundary leaves fp32 partial segments; the CTA that completes a tile's
+//    last segment (atomic counter) sums the segments in segment order and
+//    runs the epilogue.  Cut points never depend on the batch, so a token's
+//    bits do not depend on its batch-mates (T13).
 #include <cuda.h>
 
 #include <mutex>
@@ -32,24 +44,38 @@ PFN_encodeTiled_t encode_fn() {
   return fn;
 }
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    EXG_CUDA(cudaGetDevice(&dev));
+    EXG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 constexpr int BM = 128;
 constexpr int BK = 64;
-constexpr int A_BYTES = BM * BK * 2;
+constexpr int A_BYTES = BM * BK * 2;     // one 16 KB block
+constexpr int BLK_ELEMS = BM * BK;
 
 __device__ __forceinline__ float gelu_tanh(float x) {
   const float k0 = 0.7978845608028654f;  // sqrt(2/pi)
   return 0.5f * x * (1.0f + tanhf(k0 * (x + 0.044715f * x * x * x)));
 }
 
-__device__ __forceinline__ void epi_store(const EpiParams& ep, int tok, int feat, float acc) {
+__device__ __forceinline__ float epi_value(const EpiParams& ep, int feat, float acc) {
   float v = acc;
   if (ep.bias) v += bf2f(ep.bias[feat]);
+  if (ep.mode == EPI_BF16_ACT) v = ep.act == ACT_RELU ? fmaxf(v, 0.0f) : (ep.act == ACT_GELU ? gelu_tanh(v) : v);
+  return v;
+}
+
+__device__ __forceinline__ void epi_store(const EpiParams& ep, int tok, int feat, float acc) {
+  const float v = epi_value(ep, feat, acc);
   switch (ep.mode) {
     case EPI_BF16:
-      ep.out_bf16[(int64_t)tok * ep.ldo + feat] = f2bf(v);
-      break;
     case EPI_BF16_ACT:
-      v = ep.act == ACT_RELU ? fmaxf(v, 0.0f) : (ep.act == ACT_GELU ? gelu_tanh(v) : v);
       ep.out_bf16[(int64_t)tok * ep.ldo + feat] = f2bf(v);
       break;
     case EPI_RESID: {
@@ -62,98 +88,298 @@ __device__ __forceinline__ void epi_store(const EpiParams& ep, int tok, int feat
   }
 }
 
-template <int BN, int STAGES>
-__global__ void __launch_bounds__(256, 1)
-    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N,
-                   int K, int kb_per_split, int swap, EpiParams ep, float* __restrict__ partial) {
+// 16 consecutive features of one token row (prefill orientation), vectorised
+__device__ __forceinline__ void epi_store_row16(const EpiParams& ep, int tok, int f0, int N, const float* v) {
+  if (f0 + 16 <= N) {
+    if (ep.mode == EPI_BF16 || ep.mode == EPI_BF16_ACT) {
+      if ((ep.ldo & 7) == 0) {
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          __nv_bfloat162 h2 =
+              __floats2bfloat162_rn(epi_value(ep, f0 + 2 * j, v[2 * j]), epi_value(ep, f0 + 2 * j + 1, v[2 * j + 1]));
+          pk[j] = *reinterpret_cast<uint32_t*>(&h2);
+        }
+        uint4* dst = reinterpret_cast<uint4*>(ep.out_bf16 + (int64_t)tok * ep.ldo + f0);
+        dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        return;
+      }
+    } else if (ep.mode == EPI_RESID) {
+      if ((ep.ldr & 3) == 0) {
+        float4* r = reinterpret_cast<float4*>(ep.resid + (int64_t)tok * ep.ldr + f0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          float4 x = r[q];
+          x.x += epi_value(ep, f0 + 4 * q, v[4 * q]);
+          x.y += epi_value(ep, f0 + 4 * q + 1, v[4 * q + 1]);
+          x.z += epi_value(ep, f0 + 4 * q + 2, v[4 * q + 2]);
+          x.w += epi_value(ep, f0 + 4 * q + 3, v[4 * q + 3]);
+          r[q] = x;
+        }
+        return;
+      }
+    } else if ((ep.ldo & 3) == 0) {
+      float4* o = reinterpret_cast<float4*>(ep.out_f32 + (int64_t)tok * ep.ldo + f0);
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        o[q] = make_float4(epi_value(ep, f0 + 4 * q, v[4 * q]), epi_value(ep, f0 + 4 * q + 1, v[4 * q + 1]),
+                           epi_value(ep, f0 + 4 * q + 2, v[4 * q + 2]), epi_value(ep, f0 + 4 * q + 3, v[4 * q + 3]));
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j)
+    if (f0 + j < N) epi_store(ep, tok, f0 + j, v[j]);
+}
+
+// ---- work units -------------------------------------------------------------
+struct Work {
+  int dp;          // 1 = data-parallel tiles, 0 = stream-K
+  int tiles_m, tiles_n, nkb, G, max_segs;
+  int gm;          // data-parallel raster group (m-tiles)
+  int64_t I;       // stream-K iterations per chunk = tiles_m * nkb
+};
+
+struct Unit {
+  int m, n, kb0, kb1, seg;
+  bool full;
+};
+
+__host__ __device__ __forceinline__ int64_t sk_start(const Work& w, int c) { return (int64_t)c * w.I / w.G; }
+// CTA whose range contains iteration x
+__host__ __device__ __forceinline__ int sk_owner(const Work& w, int64_t x) {
+  return (int)(((x + 1) * w.G + w.I - 1) / w.I) - 1;
+}
+
+struct UnitIter {
+  Work w;
+  int c, t, chunk;
+  int64_t x, xe;
+  __device__ void init(const Work& w_, int cta) {
+    w = w_;
+    c = cta;
+    t = cta;
+    chunk = 0;
+    x = sk_start(w, c);
+    xe = sk_start(w, c + 1);
+  }
+  __device__ bool next(Unit& u) {
+    if (w.dp) {
+      if (t >= w.tiles_m * w.tiles_n) return false;
+      // grouped raster: GM m-tiles (a ~32 MB slab of A) sweep all n-tiles
+      // before the next slab, so A stays L2-resident while B streams
+      const int per_group = w.gm * w.tiles_n;
+      const int g = t / per_group, within = t % per_group;
+      const int gm_count = min(w.gm, w.tiles_m - g * w.gm);
+      u.m = g * w.gm + within % gm_count;
+      u.n = within / gm_count;
+      u.kb0 = 0;
+      u.kb1 = w.nkb;
+      u.seg = 0;
+      u.full = true;
+      t += w.G;
+      return true;
+    }
+    while (x >= xe) {
+      if (++chunk >= w.tiles_n) return false;
+      x = sk_start(w, c);
+      xe = sk_start(w, c + 1);
+    }
+    u.m = (int)(x / w.nkb);
+    u.kb0 = (int)(x % w.nkb);
+    const int64_t e = min((int64_t)(u.m + 1) * w.nkb, xe);
+    u.kb1 = u.kb0 + (int)(e - x);
+    u.n = chunk;
+    u.full = (u.kb0 == 0 && u.kb1 == w.nkb);
+    u.seg = c - sk_owner(w, (int64_t)u.m * w.nkb);
+    x = e;
+    return true;
+  }
+};
+
+constexpr int EPI_WARPS = 8;
+constexpr int GEMM_THREADS = 128 + 32 * EPI_WARPS;
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory"); }
+
+// SWAP = 1 (decode): A = weights (blocked), B = activations (TMA 2-D).
+// SWAP = 0 (prefill): A = activations (TMA 2-D), B = weights (blocked).
+template <int BN, int STAGES, int SWAP>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ Wb, int M, int N, int n_wblk,
+                   Work work, EpiParams ep, float* __restrict__ partial, int* __restrict__ counters) {
   constexpr int B_BYTES = BN * BK * 2;
+  constexpr uint32_t TMEM_COLS =
+      (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + STAGES * A_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + STAGES;      // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_holder + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
-  const int nkb_total = (K + BK - 1) / BK;
-  const int kb0 = blockIdx.z * kb_per_split;
-  const int nkb = min(kb_per_split, nkb_total - kb0);
-
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tmA);
-    prefetch_tmap(&tmB);
+    prefetch_tmap(&tmX);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tfull, 1);
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], EPI_WARPS);
+    }
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_holder, BN);
+  if (warp == 2) tmem_alloc(tmem_holder, TMEM_COLS);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
 
+  UnitIter it;
+  it.init(work, blockIdx.x);
+  Unit u;
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        if (kb >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-        mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-        tma_load_2d(sA + s * A_BYTES, &tmA, &full[s], (kb0 + kb) * BK, m0);
-        tma_load_2d(sB + s * B_BYTES, &tmB, &full[s], (kb0 + kb) * BK, n0);
+      uint32_t g = 0;
+      while (it.next(u)) {
+        for (int kb = u.kb0; kb < u.kb1; ++kb, ++g) {
+          const uint32_t s = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          if (g >= STAGES) mbar_wait(&empty[s], ph ^ 1);
+          if (SWAP) {
+            mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+            bulk_load(sA + s * A_BYTES, Wb + ((int64_t)u.m * work.nkb + kb) * BLK_ELEMS, A_BYTES, &full[s]);
+            tma_load_2d(sB + s * B_BYTES, &tmX, &full[s], kb * BK, u.n * BN);
+          } else {
+            // weight rows [n*BN, n*BN+BN) = blocks (n*BN)/128 .. ; BN = 64 uses half a block
+            const int row0 = u.n * BN;
+            int bytes = 0;
+            for (int rr = 0; rr < BN; rr += BM) {
+              const int blk = (row0 + rr) / BM;
+              if (blk >= n_wblk) break;
+              bytes += (BN < BM ? BN : BM) * BK * 2;
+            }
+            mbar_arrive_expect_tx(&full[s], A_BYTES + bytes);
+            tma_load_2d(sA + s * A_BYTES, &tmX, &full[s], kb * BK, u.m * BM);
+            for (int rr = 0; rr < BN; rr += BM) {
+              const int blk = (row0 + rr) / BM;
+              if (blk >= n_wblk) break;
+              const int sub = (row0 + rr) % BM;  // 0 or 64 (BN = 64)
+              bulk_load(sB + s * B_BYTES + rr * BK * 2,
+                        Wb + ((int64_t)blk * work.nkb + kb) * BLK_ELEMS + (int64_t)sub * BK,
+                        (uint32_t)((BN < BM ? BN : BM) * BK * 2), &full[s]);
+            }
+          }
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % STAGES;
-        const uint32_t ph = (kb / STAGES) & 1;
-        mbar_wait(&full[s], ph);
+      uint32_t g = 0, ui = 0;
+      while (it.next(u)) {
+        const uint32_t a = ui & 1;
+        if (ui >= 2) mbar_wait(&tempty[a], ((ui >> 1) & 1) ^ 1);
         tc_fence_after();
-        const uint32_t a_base = smem_u32(sA + s * A_BYTES);
-        const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+        const uint32_t d = tmem + a * BN;
+        for (int kb = u.kb0; kb < u.kb1; ++kb, ++g) {
+          const uint32_t s = g % STAGES;
+          const uint32_t ph = (g / STAGES) & 1;
+          mbar_wait(&full[s], ph);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * B_BYTES);
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          umma_bf16(tmem, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
-                    (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(d, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                      (kb != u.kb0 || k) ? 1u : 0u);
+          umma_commit(&empty[s]);
         }
-        umma_commit(&empty[s]);
+        umma_commit(&tfull[a]);
+        ++ui;
       }
-      umma_commit(tfull);
     }
   } else if (warp >= 4) {
-    mbar_wait(tfull, 0);
-    tc_fence_after();
-    const int q = warp - 4;
-    const int r = q * 32 + lane;  // accumulator row == TMEM lane
-    const int gm = m0 + r;
-    const bool row_ok = gm < M;
-    for (int c = 0; c < BN; c += 16) {
-      float v[16];
-      tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + c, v);
-      if (!row_ok) continue;
-      if (nkb <= 0) {  // empty K range (last split): contributes zeros
+    // 8 epilogue warps: warp w reads TMEM lanes 32*(w%4).. (hardware rule)
+    // and one half of the accumulator columns
+    const int q = warp & 3;
+    const int half = (warp - 4) >> 2;
+    const int c_lo = half * (BN / 2), c_hi = c_lo + BN / 2;
+    const int r = q * 32 + lane;
+    uint32_t ui = 0;
+    while (it.next(u)) {
+      const uint32_t a = ui & 1;
+      mbar_wait(&tfull[a], (ui >> 1) & 1);
+      tc_fence_after();
+      const int gm = u.m * BM + r;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
+      const bool row_ok = gm < M;
+      float* pp = nullptr;
+      if (!u.full) {
+        // fp32 partial segment, column-major [BN][128] per (chunk, tile, seg)
+        pp = partial + (((int64_t)u.n * work.tiles_m + u.m) * work.max_segs + u.seg) * (int64_t)(BM * BN);
+        for (int c = c_lo; c < c_hi; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.0f;
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int gn = n0 + c + j;
-        if (gn >= N) break;
-        const int tok = swap ? gn : gm;
-        const int feat = swap ? gm : gn;
-        if (partial) {
-          partial[((int64_t)blockIdx.z * ep.tokens + tok) * ep.features + feat] = v[j];
-        } else {
-          epi_store(ep, tok, feat, v[j]);
+          for (int j = 0; j < 16; ++j) pp[(int64_t)(c + j) * BM + r] = v[j];
         }
+      } else if (SWAP) {
+        // rows = features, columns = tokens
+        for (int c = c_lo; c < c_hi; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              const int tok = u.n * BN + c + j;
+              if (tok < N) epi_store(ep, tok, gm, v[j]);
+            }
+          }
+        }
+      } else {
+        for (int c = c_lo; c < c_hi; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
+          if (row_ok) epi_store_row16(ep, gm, u.n * BN + c, N, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a]);
+      ++ui;
+      if (!u.full) {
+        // stream-K fixup: the CTA completing the tile's last segment reduces
+        const int64_t x0 = (int64_t)u.m * work.nkb;
+        const int nseg = sk_owner(work, x0 + work.nkb - 1) - sk_owner(work, x0) + 1;
+        int* cnt = counters + (u.n * work.tiles_m + u.m);
+        __threadfence();
+        epi_bar();
+        if (threadIdx.x == 128) *s_last = (atomicAdd(cnt, 1) == nseg - 1);
+        epi_bar();
+        if (*s_last) {
+          __threadfence();
+          const float* base = partial + ((int64_t)u.n * work.tiles_m + u.m) * work.max_segs * (int64_t)(BM * BN);
+          for (int c = c_lo; c < c_hi; ++c) {
+            float acc = 0.f;
+            for (int s = 0; s < nseg; ++s) acc += __ldcg(base + (int64_t)s * BM * BN + (int64_t)c * BM + r);
+            const int tok = u.n * BN + c;
+            if (row_ok && tok < N) {
+              if (SWAP)
+                epi_store(ep, tok, gm, acc);
+              else
+                epi_store(ep, gm, tok, acc);
+            }
+          }
+          if (threadIdx.x == 128) *cnt = 0;
+        }
+        epi_bar();
       }
     }
   }
@@ -161,17 +387,7 @@ __global__ void __launch_bounds__(256, 1)
   __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, BN);
-  }
-}
-
-// split-K reduction in split order, then the epilogue (deterministic)
-__global__ void splitk_reduce_kernel(const float* __restrict__ partial, int split, EpiParams ep) {
-  const int64_t n = (int64_t)ep.tokens * ep.features;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float acc = 0.0f;
-    for (int s = 0; s < split; ++s) acc += partial[(int64_t)s * n + i];
-    epi_store(ep, (int)(i / ep.features), (int)(i % ep.features), acc);
+    tmem_dealloc(tmem, TMEM_COLS);
   }
 }
 
@@ -183,26 +399,81 @@ constexpr int stages_for() {
 template <int BN>
 size_t smem_bytes() {
   constexpr int S = stages_for<BN>();
-  return 1024 + (size_t)S * (A_BYTES + BN * BK * 2) + (2 * S + 1) * 8 + 16;
+  return 1024 + (size_t)S * (A_BYTES + BN * BK * 2) + (2 * S + 4) * 8 + 16;
 }
 
-template <int BN>
-void launch(const CUtensorMap& ta, const CUtensorMap& tb, int M, int N, int K, int split, int swap,
-            const EpiParams& ep, float* partial, cudaStream_t st) {
+Work make_work(int M, int N, int K, int BN, bool streamk) {
+  Work w;
+  w.tiles_m = (M + BM - 1) / BM;
+  w.tiles_n = (N + BN - 1) / BN;
+  w.nkb = (K + BK - 1) / BK;
+  w.I = (int64_t)w.tiles_m * w.nkb;
+  // raster group: m-tiles whose A slab is ~32 MB (kept L2-resident)
+  w.gm = (int)std::max<int64_t>(1, std::min<int64_t>(w.tiles_m, (32ll << 20) / ((int64_t)BM * K * 2)));
+  const int sms = num_sms();
+  if (streamk) {
+    w.dp = 0;
+    w.G = (int)std::min<int64_t>(sms, w.I);
+    const int64_t per = w.I / w.G;  // >= 1
+    w.max_segs = (int)((w.nkb + per - 1) / per) + 2;
+  } else {
+    w.dp = 1;
+    w.G = std::min(sms, w.tiles_m * w.tiles_n);
+    w.max_segs = 1;
+  }
+  return w;
+}
+
+// Workspace layout: [fixup counters: CNT_CAP ints][partial segments].  The
+// counter region sits at a fixed offset for every shape and token tile so
+// the zero state each fixup leaves behind is where the next launch looks.
+constexpr size_t CNT_CAP = 16384;
+size_t ws_need(const Work& w, int BN) {
+  const size_t parts = (size_t)w.tiles_n * w.tiles_m * w.max_segs * BM * BN;
+  return CNT_CAP + parts;
+}
+
+template <int BN, int SWAP>
+void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wblk, const EpiParams& ep, float* ws,
+            size_t ws_floats, cudaStream_t st) {
   constexpr int S = stages_for<BN>();
   static bool attr_set = false;
   const size_t smem = smem_bytes<BN>();
   if (!attr_set) {
-    EXG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    EXG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, S, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)smem));
     attr_set = true;
   }
-  const int nkb = (K + BK - 1) / BK;
-  const int kbps = (nkb + split - 1) / split;
-  dim3 grid((M + BM - 1) / BM, (N + BN - 1) / BN, split);
-  gemm_tc_kernel<BN, S><<<grid, 256, smem, st>>>(ta, tb, M, N, K, kbps, swap, ep, partial);
+  Work w = make_work(M, N, K, BN, SWAP != 0);
+  float* partial = nullptr;
+  int* counters = nullptr;
+  if (SWAP) {
+    const size_t need = ws_need(w, BN);
+    if (!ws || need > ws_floats) throw CudaError("stream-K workspace too small");
+    if ((size_t)w.tiles_n * w.tiles_m > CNT_CAP) throw CudaError("stream-K: too many tiles for the counter region");
+    counters = reinterpret_cast<int*>(ws);
+    partial = ws + CNT_CAP;
+  }
+  gemm_tc_kernel<BN, S, SWAP><<<w.G, GEMM_THREADS, smem, st>>>(tx, Wb, M, N, n_wblk, w, ep, partial, counters);
   EXG_CHECK_LAUNCH();
 }
+
+__global__ void pack_blocked_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, int64_t rows, int64_t K,
+                                    int64_t ld) {
+  const int64_t rp = (rows + 127) / 128 * 128, kp = (K + 63) / 64 * 64;
+  const int64_t n = rp * kp;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / kp, k = e % kp;
+    dst[blocked_index(r, k, K)] = (r < rows && k < K) ? src[r * ld + k] : __float2bfloat16_rn(0.f);
+  }
+}
 }  // namespace
+
+void pack_blocked(bf16* dst, const bf16* src, int64_t rows, int64_t K, int64_t ld, cudaStream_t st) {
+  const int64_t n = blocked_elems(rows, K);
+  pack_blocked_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(dst, src, rows, K, ld);
+  EXG_CHECK_LAUNCH();
+}
 
 CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
   CUtensorMap m;
@@ -219,24 +490,6 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
-int decode_split_k(int features, int K) {
-  const int tiles = (features + BM - 1) / BM;
-  const int nkb = (K + BK - 1) / BK;
-  int best = 1;
-  double best_eff = 0.0;
-  for (int s = 1; s <= 16; ++s) {
-    if (nkb / s < 4) break;
-    const double ctas = (double)tiles * s;
-    const double waves = std::ceil(ctas / 148.0);
-    const double eff = ctas / (waves * 148.0);
-    if (eff > best_eff + 0.02) {
-      best_eff = eff;
-      best = s;
-    }
-  }
-  return best;
-}
-
 int decode_bn(int tokens) {
   if (tokens <= 32) return 32;
   if (tokens <= 64) return 64;
@@ -244,51 +497,38 @@ int decode_bn(int tokens) {
   return 256;
 }
 
+size_t decode_ws_floats(int features, int K, int max_tokens) {
+  size_t best = 0;
+  for (int bn : {32, 64, 128, 256}) {
+    const int n = bn == 256 ? std::max(max_tokens, 1) : bn;
+    best = std::max(best, ws_need(make_work(features, n, K, bn, true), bn));
+  }
+  return best;
+}
+
 void linear(const LinearArgs& a, cudaStream_t st) {
   const int tokens = a.ep.tokens, features = a.ep.features;
   if (tokens <= 0 || features <= 0) return;
-  int BN;
-  CUtensorMap ta, tb;
-  int M, N;
+  const int n_wblk = (features + BM - 1) / BM;
   if (a.decode) {
-    BN = a.bn ? a.bn : decode_bn(tokens);
-    M = features;
-    N = tokens;
-    if (a.cached) {
-      ta = a.cached->a;
-      tb = a.cached->b;
-    } else {
-      ta = make_tmap_bf16(a.W, features, a.K, a.ldw, BM);
-      tb = make_tmap_bf16(a.X, tokens, a.K, a.ldx, BN);
+    const int BN = a.bn ? a.bn : decode_bn(tokens);
+    const CUtensorMap tx = make_tmap_bf16(a.X, tokens, a.K, a.ldx, BN);
+    switch (BN) {
+      case 32: launch<32, 1>(tx, a.Wb, features, tokens, a.K, n_wblk, a.ep, a.ws, a.ws_floats, st); break;
+      case 64: launch<64, 1>(tx, a.Wb, features, tokens, a.K, n_wblk, a.ep, a.ws, a.ws_floats, st); break;
+      case 128: launch<128, 1>(tx, a.Wb, features, tokens, a.K, n_wblk, a.ep, a.ws, a.ws_floats, st); break;
+      case 256: launch<256, 1>(tx, a.Wb, features, tokens, a.K, n_wblk, a.ep, a.ws, a.ws_floats, st); break;
+      default: throw CudaError("bad BN");
     }
   } else {
-    BN = a.bn ? a.bn : (features >= 256 ? 256 : (features > 64 ? 128 : 64));
-    M = tokens;
-    N = features;
-    if (a.cached) {
-      ta = a.cached->a;
-      tb = a.cached->b;
-    } else {
-      ta = make_tmap_bf16(a.X, tokens, a.K, a.ldx, BM);
-      tb = make_tmap_bf16(a.W, features, a.K, a.ldw, BN);
+    const int BN = a.bn ? a.bn : (features > 128 ? 256 : (features > 64 ? 128 : 64));
+    const CUtensorMap tx = make_tmap_bf16(a.X, tokens, a.K, a.ldx, BM);
+    switch (BN) {
+      case 64: launch<64, 0>(tx, a.Wb, tokens, features, a.K, n_wblk, a.ep, nullptr, 0, st); break;
+      case 128: launch<128, 0>(tx, a.Wb, tokens, features, a.K, n_wblk, a.ep, nullptr, 0, st); break;
+      case 256: launch<256, 0>(tx, a.Wb, tokens, features, a.K, n_wblk, a.ep, nullptr, 0, st); break;
+      default: throw CudaError("bad BN");
     }
-  }
-  const int split = a.split > 1 ? a.split : 1;
-  float* partial = split > 1 ? a.ws : nullptr;
-  if (split > 1 && !partial) throw CudaError("split-K GEMM without workspace");
-  const int swap = a.decode ? 1 : 0;
-  switch (BN) {
-    case 32: launch<32>(ta, tb, M, N, a.K, split, swap, a.ep, partial, st); break;
-    case 64: launch<64>(ta, tb, M, N, a.K, split, swap, a.ep, partial, st); break;
-    case 128: launch<128>(ta, tb, M, N, a.K, split, swap, a.ep, partial, st); break;
-    case 256: launch<256>(ta, tb, M, N, a.K, split, swap, a.ep, partial, st); break;
-    default: throw CudaError("bad BN");
-  }
-  if (split > 1) {
-    const int64_t n = (int64_t)tokens * features;
-    const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 8);
-    splitk_reduce_kernel<<<blocks, 256, 0, st>>>(partial, split, a.ep);
-    EXG_CHECK_LAUNCH();
   }
 }
 

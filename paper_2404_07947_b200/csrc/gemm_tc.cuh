@@ -1,6 +1,14 @@
 // tcgen05 / TMEM / TMA GEMM for the prefill GEMMs (K3), decode projections
-// (K5, swap-AB) and LM head (K8).  D[M][N] = A[M][K] . B[N][K]^T, bf16 in,
-// fp32 accumulate in TMEM, fused epilogues (bias / activation / residual).
+// (K5, swap-AB) and LM head (K8).  Y[token][feature] = X[token][K] .
+// W[feature][K]^T, bf16 in, fp32 accumulate in TMEM, fused epilogues.
+//
+// Weights live in HBM in a pre-tiled, pre-swizzled blocked layout: the
+// 128-row x 64-column tile (m, kb) of W is one contiguous 16 KB block at
+// element offset (m * nkb + kb) * 8192, holding row r's 16-byte chunk c at
+// r*64 + ((c ^ (r & 7)) * 8) -- byte-for-byte the shared-memory image a
+// SWIZZLE_128B TMA box would produce.  A CTA therefore streams its weight
+// range with 1-D bulk copies of whole contiguous blocks (decode is a pure
+// HBM stream) instead of 128 scattered 128-byte rows per box.
 #pragma once
 #include "common.cuh"
 
@@ -14,9 +22,6 @@ enum EpiMode : int {
 };
 enum ActKind : int { ACT_NONE = 0, ACT_RELU = 1, ACT_GELU = 2 };
 
-// Output orientation is always Y[token][feature]; `swap` says whether the
-// GEMM's M axis is tokens (swap = 0: A = activations, B = weights) or
-// features (swap = 1: A = weights, B = activations; decode).
 struct EpiParams {
   int mode = EPI_BF16;
   int act = ACT_NONE;
@@ -29,37 +34,43 @@ struct EpiParams {
   int tokens = 0, features = 0;
 };
 
-struct GemmTmaps {
-  CUtensorMap a, b;
-};
+// ---- blocked weight layout ---------------------------------------------------
+inline int64_t blocked_elems(int64_t rows, int64_t K) {
+  return ((rows + 127) / 128) * ((K + 63) / 64) * 128 * 64;
+}
+// element offset of W[row][k] in the blocked layout
+__host__ __device__ inline int64_t blocked_index(int64_t row, int64_t k, int64_t K) {
+  const int64_t nkb = (K + 63) / 64;
+  const int64_t m = row >> 7, r = row & 127, kb = k >> 6, c = k & 63;
+  return ((m * nkb + kb) << 13) + (r << 6) + ((((c >> 3) ^ (r & 7))) << 3) + (c & 7);
+}
+// pack a row-major W [rows][ld] (first K columns) into the blocked layout
+// (zero padding to whole tiles)
+void pack_blocked(bf16* dst, const bf16* src, int64_t rows, int64_t K, int64_t ld, cudaStream_t st);
 
-// Build a 2-D TMA map over a row-major bf16 matrix [rows][ld] using the
-// first `cols` columns; box = 64 columns x box_rows rows, 128B swizzle.
 CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t ld, int box_rows);
 
-// Choose the split-K factor for a decode (swap-AB) GEMM from the weight
-// shape only (never the batch), so results are batch invariant (T13).
-int decode_split_k(int features, int K);
+// fp32 workspace (floats) a decode (stream-K) GEMM of this weight shape
+// needs for partial segments + fixup counters, for up to max_tokens tokens.
+size_t decode_ws_floats(int features, int K, int max_tokens);
 
-// Y = X . W^T with epilogue.  X: [tokens][K] (ldx), W: [features][K] (ldw).
-// decode = true selects swap-AB (tokens on the MMA N axis).  `ws` is an fp32
-// workspace for split-K partials of at least split*tokens*features floats.
+// Y = X . W^T with epilogue.  X: row-major [tokens][ldx]; W: blocked layout
+// of a [features][K] matrix.  decode = true selects swap-AB with stream-K
+// (tokens on the MMA N axis); `ws` must hold decode_ws_floats() floats and
+// be zero-initialised once (its fixup counters return to zero after use).
 struct LinearArgs {
   const bf16* X = nullptr;
   int64_t ldx = 0;
-  const bf16* W = nullptr;
-  int64_t ldw = 0;
+  const bf16* Wb = nullptr;   // blocked
   int K = 0;
   EpiParams ep;
   bool decode = false;
-  int split = 1;
   float* ws = nullptr;
-  const GemmTmaps* cached = nullptr;   // optional prebuilt maps (A,B as the kernel sees them)
-  int bn = 0;                         // 0 -> auto
+  size_t ws_floats = 0;
+  int bn = 0;                 // 0 -> auto
 };
 void linear(const LinearArgs& a, cudaStream_t st);
 
-// token tile (MMA N) used for a decode GEMM with `tokens` rows
 int decode_bn(int tokens);
 
 }  // namespace exg

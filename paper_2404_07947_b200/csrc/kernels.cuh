@@ -21,12 +21,14 @@ struct GenParams {
   int transposed;
   int64_t canon_cols;
   int64_t row_off, col_off;
+  int blocked;         // 1: write the GEMM blocked layout (gemm_tc.cuh), zero padded
 };
 void weightgen(bf16* dst, int64_t rows, int64_t cols, int64_t ld, const GenParams& p, cudaStream_t st);
 
 // ---- K1: x[t] = tok_emb[ids[t]] + pos_emb[pos[t]]  (fp32 residual) ---------
+// tok_blocked = 1: tok_emb is in the GEMM blocked layout ([V][d] blocks).
 void embed(float* x, const int32_t* ids, const int32_t* pos, const bf16* tok_emb, const bf16* pos_emb, int T,
-           int d, cudaStream_t st);
+           int d, cudaStream_t st, int tok_blocked = 0);
 
 // ---- K2: y = bf16(LN(x) * g + b), fp32 statistics, eps 1e-5 ----------------
 void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,

@@ -11,7 +11,7 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-from gpu_util import bf16_round_np, bf16_tensor, dev, ptr, stream, to_np  # noqa: E402
+from gpu_util import bf16_round_np, bf16_tensor, blocked, dev, ptr, stream, to_np  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -29,16 +29,24 @@ def _run(L, fn, *args):
 
 # ------------------------------------------------------------------- GEMM --
 GEMM_CASES = [
-    # tokens, features, K, decode, split
-    (1, 64, 64, True, 1), (5, 200, 256, True, 1), (33, 1024, 1000, True, 1), (64, 192, 512, True, 3),
-    (130, 320, 128, True, 1), (256, 256, 256, True, 2), (300, 128, 192, True, 1),
-    (1, 64, 64, False, 1), (100, 300, 320, False, 1), (257, 512, 64, False, 1), (1000, 96, 136, False, 1),
+    # tokens, features, K, decode   (decode uses stream-K over the weight stream)
+    (1, 64, 64, True), (5, 200, 256, True), (33, 1024, 1000, True), (64, 192, 512, True),
+    (130, 320, 128, True), (256, 256, 256, True), (300, 128, 192, True), (20, 5120, 5120, True),
+    (513, 384, 4096, True), (7, 20480, 320, True),
+    (1, 64, 64, False), (100, 300, 320, False), (257, 512, 64, False), (1000, 96, 136, False),
+    (700, 2048, 1024, False),
 ]
 
 
-@pytest.mark.parametrize("tokens,features,K,decode,split", GEMM_CASES)
+def _ws(L, features, K, tokens):
+    n = L.lib().exg_op_decode_workspace(features, K, tokens)
+    assert n >= 0
+    return torch.zeros(max(int(n), 1), dtype=torch.float32, device=dev()), int(n)
+
+
+@pytest.mark.parametrize("tokens,features,K,decode", GEMM_CASES)
 @pytest.mark.parametrize("mode,act", [(0, 0), (1, 1), (1, 2), (2, 0), (3, 0)])
-def test_linear_parity(L, tokens, features, K, decode, split, mode, act):
+def test_linear_parity(L, tokens, features, K, decode, mode, act):
     rng = np.random.default_rng(tokens * 7 + features + K)
     X = bf16_round_np(rng.standard_normal((tokens, K)) * 0.5)
     W = bf16_round_np(rng.standard_normal((features, K)) * 0.05)
@@ -46,11 +54,12 @@ def test_linear_parity(L, tokens, features, K, decode, split, mode, act):
     acc = X @ W.T + b
     mag = np.abs(X) @ np.abs(W).T + np.abs(b)
     tX, tW, tb = bf16_tensor(X), bf16_tensor(W), bf16_tensor(b)
-    ws = torch.zeros(max(split, 1) * tokens * features, dtype=torch.float32, device=dev())
+    tWb = blocked(L, tW)
+    ws, nws = _ws(L, features, K, tokens)
     if mode in (0, 1):
         out = torch.zeros((tokens, features), dtype=torch.bfloat16, device=dev())
-        _run(L, "exg_op_linear", ptr(tX), K, ptr(tW), K, tokens, features, K, mode, act, ptr(tb), ptr(out),
-             features, None, 0, int(decode), split, ptr(ws), stream())
+        _run(L, "exg_op_linear", ptr(tX), K, ptr(tWb), tokens, features, K, mode, act, ptr(tb), ptr(out),
+             features, None, 0, int(decode), ptr(ws), nws, stream())
         torch.cuda.synchronize()
         ref = acc if mode == 0 else (np.maximum(acc, 0) if act == 1 else
                                      0.5 * acc * (1 + np.tanh(math.sqrt(2 / math.pi) * (acc + 0.044715 * acc ** 3))))
@@ -60,15 +69,15 @@ def test_linear_parity(L, tokens, features, K, decode, split, mode, act):
     elif mode == 2:
         r0 = rng.standard_normal((tokens, features)).astype(np.float32)
         resid = torch.from_numpy(r0).to(dev())
-        _run(L, "exg_op_linear", ptr(tX), K, ptr(tW), K, tokens, features, K, 2, 0, ptr(tb), None, 0,
-             ptr(resid), features, int(decode), split, ptr(ws), stream())
+        _run(L, "exg_op_linear", ptr(tX), K, ptr(tWb), tokens, features, K, 2, 0, ptr(tb), None, 0,
+             ptr(resid), features, int(decode), ptr(ws), nws, stream())
         torch.cuda.synchronize()
         ref = r0.astype(np.float64) + acc
         assert np.all(np.abs(resid.cpu().numpy() - ref) <= 1e-4 * mag + 1e-5 * np.abs(ref) + 1e-6)
     else:
         out = torch.zeros((tokens, features), dtype=torch.float32, device=dev())
-        _run(L, "exg_op_linear", ptr(tX), K, ptr(tW), K, tokens, features, K, 3, 0, ptr(tb), ptr(out), features,
-             None, 0, int(decode), split, ptr(ws), stream())
+        _run(L, "exg_op_linear", ptr(tX), K, ptr(tWb), tokens, features, K, 3, 0, ptr(tb), ptr(out), features,
+             None, 0, int(decode), ptr(ws), nws, stream())
         torch.cuda.synchronize()
         assert np.all(np.abs(out.cpu().numpy() - acc) <= 1e-4 * mag + 1e-6)
 
@@ -80,10 +89,12 @@ def test_linear_strided_operands(L):
     Xf = bf16_round_np(rng.standard_normal((tokens, ld)))
     Wf = bf16_round_np(rng.standard_normal((features, ld)) * 0.05)
     tX, tW = bf16_tensor(Xf), bf16_tensor(Wf)
+    tWb = blocked(L, tW[:, :K])
+    ws, nws = _ws(L, features, K, tokens)
     for decode in (0, 1):
         out = torch.zeros((tokens, 256), dtype=torch.float32, device=dev())
-        _run(L, "exg_op_linear", ptr(tX), ld, ptr(tW), ld, tokens, features, K, 3, 0, None, ptr(out), 256, None, 0,
-             decode, 1, None, stream())
+        _run(L, "exg_op_linear", ptr(tX), ld, ptr(tWb), tokens, features, K, 3, 0, None, ptr(out), 256, None, 0,
+             decode, ptr(ws), nws, stream())
         torch.cuda.synchronize()
         ref = Xf[:, :K] @ Wf[:, :K].T
         assert np.abs(out.cpu().numpy()[:, :features] - ref).max() < 1e-3
@@ -94,18 +105,16 @@ def test_decode_gemm_batch_invariant(L):
     """T13: a token row's decode-GEMM bits do not depend on its batch-mates
     or its row position (tokens ride the MMA N axis)."""
     rng = np.random.default_rng(9)
-    K, features = 512, 384
-    W = bf16_tensor(bf16_round_np(rng.standard_normal((features, K)) * 0.05))
+    K, features = 2048, 1280       # stream-K with tiles cut between CTAs
+    W = blocked(L, bf16_tensor(bf16_round_np(rng.standard_normal((features, K)) * 0.05)))
     X = bf16_round_np(rng.standard_normal((200, K)))
-    tX = bf16_tensor(X)
-    split = L.lib().exg_op_decode_split_k(features, K)
-    ws = torch.zeros(16 * 200 * features, dtype=torch.float32, device=dev())
+    ws, nws = _ws(L, features, K, 200)
 
     def run(rows):
         x = bf16_tensor(X[rows])
         out = torch.zeros((len(rows), features), dtype=torch.float32, device=dev())
-        _run(L, "exg_op_linear", ptr(x), K, ptr(W), K, len(rows), features, K, 3, 0, None, ptr(out), features, None,
-             0, 1, split, ptr(ws), stream())
+        _run(L, "exg_op_linear", ptr(x), K, ptr(W), len(rows), features, K, 3, 0, None, ptr(out), features, None,
+             0, 1, ptr(ws), nws, stream())
         torch.cuda.synchronize()
         return out.cpu().numpy()
 
@@ -314,9 +323,16 @@ def test_weightgen_bit_identical_to_oracle(L, kind, transposed, rows, cols, cano
     tid = wg.tensor_id(1001 if kind not in ("tok_emb",) else 0, kind)
     out = torch.zeros((rows, cols), dtype=torch.bfloat16, device=dev())
     _run(L, "exg_op_weightgen", ptr(out), rows, cols, cols, seed, tid, int(kind in wg.GAIN_KINDS), transposed, canon,
-         0, 0, stream())
+         0, 0, 0, stream())
     torch.cuda.synchronize()
     got = out.float().cpu().numpy()
     vals = wg.gen_values(seed, tid, rows * cols, kind)
     ref = vals.reshape(cols, rows).T if transposed else vals.reshape(rows, cols)
     assert np.array_equal(got.view(np.uint32), np.ascontiguousarray(ref).view(np.uint32))
+    # blocked layout: generating in place == packing the row-major tensor
+    blk = torch.zeros(int(L.lib().exg_op_blocked_elems(rows, cols)), dtype=torch.bfloat16, device=dev())
+    _run(L, "exg_op_weightgen", ptr(blk), rows, cols, cols, seed, tid, int(kind in wg.GAIN_KINDS), transposed, canon,
+         0, 0, 1, stream())
+    packed = blocked(L, out)
+    torch.cuda.synchronize()
+    assert torch.equal(blk, packed)

@@ -1,0 +1,117 @@
+"""Kernel timing probe at the workload's shapes (OPT-13B, task S): prefill
+GEMMs, decode GEMMs, decode attention, prefill attention.  Prints achieved
+TFLOP/s or GB/s per kernel (CUDA events, L2 flushed between reps)."""
+import math
+import sys
+import os
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2404_07947_b200 import _lib as L  # noqa: E402
+
+dev = torch.device("cuda:0")
+st = lambda: torch.cuda.current_stream().cuda_stream
+flush = torch.empty(256 * 1024 * 1024, dtype=torch.int8, device=dev)
+
+
+def timeit(fn, reps=10):
+    fn()
+    ts = []
+    for _ in range(reps):
+        flush.sum()          # read-only L2 flush: leaves no dirty lines to write back
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(); fn(); b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b) * 1e-3)
+    return float(np.median(ts))
+
+
+def gemm(tokens, features, K, decode, mode=0):
+    X = torch.randn(tokens, K, device=dev).to(torch.bfloat16)
+    W0 = (torch.randn(features, K, device=dev) * 0.02).to(torch.bfloat16)
+    W = torch.empty(int(L.lib().exg_op_blocked_elems(features, K)), dtype=torch.bfloat16, device=dev)
+    L.check(L.lib().exg_op_pack_weight(W.data_ptr(), W0.data_ptr(), features, K, K, st()))
+    out = torch.zeros(tokens, features, device=dev, dtype=torch.float32 if mode in (2, 3) else torch.bfloat16)
+    nws = int(L.lib().exg_op_decode_workspace(features, K, tokens)) if decode else 0
+    ws = torch.empty(max(nws, 1), device=dev, dtype=torch.float32)
+    resid = out.data_ptr() if mode == 2 else None
+    split = nws
+
+    def fn():
+        L.check(L.lib().exg_op_linear(X.data_ptr(), K, W.data_ptr(), tokens, features, K, mode, 0, None,
+                                      out.data_ptr(), features, resid, features, int(decode), ws.data_ptr(), nws,
+                                      st()))
+    t = timeit(fn)
+    flops = 2.0 * tokens * features * K
+    byts = 2.0 * (features * K + tokens * K + tokens * features)
+    print("gemm %s T=%5d N=%5d K=%5d split=%d: %8.1f us  %7.1f TFLOP/s  %7.1f GB/s" %
+          ("dec" if decode else "pre", tokens, features, K, split, t * 1e6, flops / t / 1e12, byts / t / 1e9))
+
+
+def dattn(B, c, H=40, dh=128, split_len=512):
+    max_ctx = ((c + 63) // 64) * 64
+    kc = torch.randn(B, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    vc = torch.randn(B, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    q = torch.randn(B, 3 * H * dh, device=dev).to(torch.bfloat16)
+    slot = torch.arange(B, dtype=torch.int32, device=dev)
+    nk = torch.full((B,), c, dtype=torch.int32, device=dev)
+    ms = (c + split_len - 1) // split_len
+    part = torch.empty(B * H * ms * (dh + 2), device=dev)
+    out = torch.empty(B, H * dh, device=dev, dtype=torch.bfloat16)
+
+    def fn():
+        L.check(L.lib().exg_op_decode_attention(q.data_ptr(), 3 * H * dh, kc.data_ptr(), vc.data_ptr(),
+                                                slot.data_ptr(), nk.data_ptr(), out.data_ptr(), H * dh, B, H, dh,
+                                                max_ctx, 0.0883883, split_len, ms, part.data_ptr(), st()))
+    t = timeit(fn)
+    byts = B * H * (2.0 * c * dh * 2 + 2 * dh * 2)
+    print("decode-attn B=%4d c=%5d H=%d: %8.1f us  %7.1f GB/s" % (B, c, H, t * 1e6, byts / t / 1e9))
+
+
+def pattn(R, n, H=40, dh=128):
+    T = R * n
+    max_ctx = n
+    kc = torch.randn(R, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    vc = torch.randn(R, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    q = torch.randn(T, 3 * H * dh, device=dev).to(torch.bfloat16)
+    cu = torch.arange(0, T + 1, n, dtype=torch.int32, device=dev)
+    slot = torch.arange(R, dtype=torch.int32, device=dev)
+    p0 = torch.zeros(R, dtype=torch.int32, device=dev)
+    out = torch.empty(T, H * dh, device=dev, dtype=torch.bfloat16)
+
+    def fn():
+        L.check(L.lib().exg_op_prefill_attention(q.data_ptr(), 3 * H * dh, kc.data_ptr(), vc.data_ptr(),
+                                                 cu.data_ptr(), slot.data_ptr(), p0.data_ptr(), R, n, out.data_ptr(),
+                                                 H * dh, H, dh, max_ctx, 0.0883883, st()))
+    t = timeit(fn)
+    flops = 4.0 * H * dh * R * n * (n + 1) / 2
+    print("prefill-attn R=%d n=%d: %8.1f us  %7.1f TFLOP/s" % (R, n, t * 1e6, flops / t / 1e12))
+
+
+if __name__ == "__main__":
+    if len(sys.argv) > 1 and sys.argv[1] == "gemm":
+        T, N, K = map(int, sys.argv[2:5])
+        gemm(T, N, K, sys.argv[5] == "dec", int(sys.argv[6]) if len(sys.argv) > 6 else 0)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "dattn":
+        dattn(int(sys.argv[2]), int(sys.argv[3]))
+        sys.exit(0)
+    d, ff = 5120, 20480
+    for T in (2048, 8192):
+        gemm(T, 3 * d, d, False)
+        gemm(T, d, d, False, 2)
+        gemm(T, ff, d, False)
+        gemm(T, d, ff, False, 2)
+    for B in (16, 64, 256):
+        gemm(B, 3 * d, d, True)
+        gemm(B, d, d, True, 2)
+        gemm(B, ff, d, True)
+        gemm(B, d, ff, True, 2)
+        gemm(B, 50272, d, True, 3)
+    for B, c in ((64, 300), (256, 300), (256, 592), (16, 1600)):
+        dattn(B, c)
+    pattn(16, 256)
+    pattn(8, 512)
