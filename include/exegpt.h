@@ -42,7 +42,11 @@ typedef enum {
 
 typedef enum { EXG_ARCH_OPT = 0, EXG_ARCH_GPT3 = 1, EXG_ARCH_T5 = 2 } exg_arch; /* tiny = GPT3-style */
 typedef enum { EXG_BF16 = 0, EXG_FP32 = 1 } exg_dtype;
-typedef enum { EXG_RRA = 1, EXG_WAA_C = 2, EXG_WAA_M = 4 } exg_strategy;    /* bitmask */
+/* bitmask of scheduling policies.  EXG_STATIC is the
+ * FasterTransformer-style static batch (fixed batch, no early
+ * termination) used only by exg_simulate, to derive latency bounds by the
+ * paper's recipe; b_e = the static batch size. */
+typedef enum { EXG_RRA = 1, EXG_WAA_C = 2, EXG_WAA_M = 4, EXG_STATIC = 8 } exg_strategy;
 
 /* Model shape (Table 1) plus the weight seed of the
  * counter-hash generator.  n_enc_layers = 0 for
@@ -122,7 +126,20 @@ typedef struct {
   const uint8_t* dump_mask;   /* optional [n]: 1 = dump this request's logits   */
   int32_t slot_ctx;           /* KV slot length; 0 -> max(input_len+output_len) */
   int32_t pin_nccl_algo;      /* reserved for multi-GPU parity runs             */
+  int32_t kernel_timing;      /* 1: CUDA events around every launch of the
+                                 kernel classes below (roofline evidence)       */
 } exg_run_opts;
+
+/* Kernel classes timed when exg_run_opts.kernel_timing = 1.  Work is the
+ * algorithmic amount: FLOPs for the tensor-core kernels,
+ * HBM bytes for the bandwidth kernels. */
+enum {
+  EXG_K_PREFILL_GEMM = 0,  /* 2*T*F*K flops                                          */
+  EXG_K_DECODE_GEMM = 1,   /* weight + activation + output bytes                     */
+  EXG_K_DECODE_ATTN = 2,   /* sum_i c_i*2*H*dh*2 (K,V read) + B*H*dh*2*2 (q in, o out) */
+  EXG_K_PREFILL_ATTN = 3,  /* 4*H*dh*sum_i n_i(n_i+1)/2 flops                        */
+  EXG_K_CLASSES = 4
+};
 
 /* Measured run statistics.  Times come from device
  * events on one clock. */
@@ -133,6 +150,10 @@ typedef struct {
   int64_t out_tokens, decode_iters, encode_phases;
   double mean_decode_batch;            /* measured, vs the simulated B_D           */
   double encode_s, decode_s;           /* device time spent per phase kind         */
+  int64_t kernel_launches;             /* library kernels launched by this run     */
+  double k_time_s[EXG_K_CLASSES];      /* summed launch durations per class        */
+  double k_work[EXG_K_CLASSES];        /* summed algorithmic work per class        */
+  int64_t k_launches[EXG_K_CLASSES];
 } exg_run_stats;
 
 typedef struct exg_ctx exg_ctx;           /* one per rank: device state + comms */

@@ -450,5 +450,24 @@ class Simulator:
         lat = T_trav + handoff + T_E + (self.target_len - 1) * T_D + fill(td, M)
         return Estimate(thr, thr * self.s_d, lat)
 
+    # -- FT-style static batch ----------
+    def simulate_static(self, B: int) -> Estimate:
+        """Encode B requests, then decode all B rows for max_out iterations
+        with no early termination (dead rows still computed): the baseline
+        the paper derives its latency bounds from.  Latency applies to a
+        max-length output; throughput = B / latency.  P = 1 (TP maxed within
+        the box is the paper's FT setting; single-GPU here)."""
+        st = stage_layout(self.cl.n_gpus, 1, 0, self.n_layers)
+        if not self.mem_ok(st, B, self.max_in + self.max_out):
+            return Estimate(0.0, 0.0, INF, False)
+        try:
+            t_enc = self.stage_times(st, "enc", float(B))
+            t_dec = self.stage_times(st, "dec", float(B))
+        except OutOfHull:
+            return Estimate(0.0, 0.0, INF, False)
+        lat = fill(t_enc, 1) + self.max_out * fill(t_dec, 1)
+        thr = B / lat
+        return Estimate(thr, thr * self.s_d, lat)
+
     def simulate(self, s: Schedule) -> Estimate:
         return self.simulate_rra(s) if s.strategy == RRA else self.simulate_waa(s)

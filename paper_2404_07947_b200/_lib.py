@@ -86,7 +86,10 @@ class exg_request(C.Structure):
 
 class exg_run_opts(C.Structure):
     _fields_ = [("logits_out", C.POINTER(C.c_float)), ("dump_mask", C.POINTER(C.c_uint8)),
-                ("slot_ctx", C.c_int32), ("pin_nccl_algo", C.c_int32)]
+                ("slot_ctx", C.c_int32), ("pin_nccl_algo", C.c_int32), ("kernel_timing", C.c_int32)]
+
+
+K_CLASSES = ["prefill_gemm", "decode_gemm", "decode_attn", "prefill_attn"]
 
 
 class exg_run_stats(C.Structure):
@@ -94,10 +97,14 @@ class exg_run_stats(C.Structure):
                 ("lat_p50_s", C.c_double), ("lat_p99_s", C.c_double), ("lat_max_s", C.c_double),
                 ("wall_s", C.c_double), ("out_tokens", C.c_int64), ("decode_iters", C.c_int64),
                 ("encode_phases", C.c_int64), ("mean_decode_batch", C.c_double), ("encode_s", C.c_double),
-                ("decode_s", C.c_double)]
+                ("decode_s", C.c_double), ("kernel_launches", C.c_int64), ("k_time_s", C.c_double * 4),
+                ("k_work", C.c_double * 4), ("k_launches", C.c_int64 * 4)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("k_")}
+        d["kernels"] = {K_CLASSES[c]: {"time_s": self.k_time_s[c], "work": self.k_work[c],
+                                       "launches": self.k_launches[c]} for c in range(4)}
+        return d
 
 
 _P = C.c_void_p
@@ -216,7 +223,8 @@ class Context:
         check(lib().exg_profile_run(self.h, C.byref(g), C.byref(h)))
         return Profile(h)
 
-    def run(self, sched: exg_schedule, requests, dump: Optional[Sequence[int]] = None, slot_ctx: int = 0):
+    def run(self, sched: exg_schedule, requests, dump: Optional[Sequence[int]] = None, slot_ctx: int = 0,
+            kernel_timing: bool = False):
         """Returns (tokens per request, latencies [s], stats dict, logits per
         dumped request [S_r][V] or None)."""
         n = len(requests)
@@ -230,7 +238,7 @@ class Context:
         out = np.zeros(total, dtype=np.int32)
         lat = np.zeros(n, dtype=np.float64)
         stats = exg_run_stats()
-        opts = exg_run_opts(None, None, slot_ctx, 0)
+        opts = exg_run_opts(None, None, slot_ctx, 0, int(kernel_timing))
         logits = None
         if dump is not None:
             mask = np.zeros(n, dtype=np.uint8)

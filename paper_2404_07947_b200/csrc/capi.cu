@@ -193,7 +193,8 @@ exg_status exg_simulate(const exg_profile* p, const exg_model_spec* spec, const 
     if (!p || !cluster || !sched || !est) throw std::invalid_argument("null argument");
     check_spec(spec);
     exg::plan::Simulator S(p->p, *spec, *cluster, pmf_vec(in), pmf_vec(out_len), target_len, false);
-    exg::plan::Est e = S.simulate(from_c(sched));
+    if (sched->strategy == EXG_STATIC && sched->b_e < 1) throw std::invalid_argument("static batch b_e < 1");
+    exg::plan::Est e = sched->strategy == EXG_STATIC ? S.simulate_static(sched->b_e) : S.simulate(from_c(sched));
     est->thrput_seq_s = e.thr;
     est->thrput_tok_s = e.tok;
     est->latency_s = e.lat;

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <cstdio>
 #include <stdexcept>
 #include <string>
@@ -24,7 +25,17 @@ struct CudaError : std::runtime_error {
                              " (" __FILE__ ":" + std::to_string(__LINE__) + ")");    \
   } while (0)
 
-#define EXG_CHECK_LAUNCH() EXG_CUDA(cudaGetLastError())
+// Every kernel launch of the library is followed by EXG_CHECK_LAUNCH(), which
+// also counts it (reported as exg_run_stats.kernel_launches).
+inline std::atomic<long long>& launch_counter() {
+  static std::atomic<long long> c{0};
+  return c;
+}
+#define EXG_CHECK_LAUNCH()                                   \
+  do {                                                       \
+    ::exg::launch_counter().fetch_add(1, std::memory_order_relaxed); \
+    EXG_CUDA(cudaGetLastError());                            \
+  } while (0)
 
 typedef __nv_bfloat16 bf16;
 

@@ -111,6 +111,7 @@ Engine::~Engine() {
   cudaStreamSynchronize(st_);
   for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)last_tok_, (void*)err_, (void*)prof_tables_})
     if (p) cudaFree(p);
+  for (cudaEvent_t e : kev_) cudaEventDestroy(e);
   if (st_) cudaStreamDestroy(st_);
 }
 
@@ -230,7 +231,48 @@ void Engine::linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, i
   a.decode = true;
   a.ws = splitk_ws_;
   a.ws_floats = splitk_cap_;
+  const int k = kbegin();
   linear(a, st_);
+  const double out_b = ep.mode == EPI_RESID ? 8.0 : (ep.mode == EPI_F32 ? 4.0 : 2.0);
+  kend(k, EXG_K_DECODE_GEMM,
+       2.0 * features * K + 2.0 * tokens * K + out_b * tokens * features);
+}
+
+int Engine::kbegin() {
+  if (!ktiming_) return -1;
+  const int idx = (int)krec_.size();
+  while ((int)kev_.size() < 2 * (idx + 1)) {
+    cudaEvent_t e;
+    EXG_CUDA(cudaEventCreate(&e));
+    kev_.push_back(e);
+  }
+  EXG_CUDA(cudaEventRecord(kev_[2 * idx], st_));
+  krec_.push_back(KRec{-1, idx, 0.0});
+  return idx;
+}
+
+void Engine::kend(int idx, int cls, double work) {
+  if (idx < 0) return;
+  EXG_CUDA(cudaEventRecord(kev_[2 * idx + 1], st_));
+  krec_[idx].cls = cls;
+  krec_[idx].work = work;
+}
+
+void Engine::set_kernel_timing(bool on) {
+  ktiming_ = on;
+  krec_.clear();
+}
+
+void Engine::collect_kernel_timing(double* t, double* w, int64_t* n) {
+  for (const KRec& r : krec_) {
+    if (r.cls < 0) continue;
+    float ms = 0.f;
+    EXG_CUDA(cudaEventElapsedTime(&ms, kev_[2 * r.ev], kev_[2 * r.ev + 1]));
+    t[r.cls] += ms * 1e-3;
+    w[r.cls] += r.work;
+    n[r.cls] += 1;
+  }
+  krec_.clear();
 }
 
 void Engine::linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep) {
@@ -243,7 +285,9 @@ void Engine::linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, i
   ep.features = features;
   a.ep = ep;
   a.decode = false;
+  const int k = kbegin();
   linear(a, st_);
+  kend(k, EXG_K_PREFILL_GEMM, 2.0 * tokens * features * K);
 }
 
 static EpiParams epi_bf16(const bf16* bias, bf16* out, int64_t ldo, int act = ACT_NONE) {
@@ -276,7 +320,9 @@ void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest) {
   if (attn) {
     PrefillAttnArgs pa{qkv_, 3 * inner, kc(l), vc(l), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,
                        ctx_, inner, D.H, D.dh, slot_ctx_, scale};
+    const int k = kbegin();
     prefill_attention(pa, st_);
+    kend(k, EXG_K_PREFILL_ATTN, 4.0 * D.H * D.dh * eb.attn_pairs);
   }
   if (rest) {
     linear_pre(ctx_, inner, T, w.Wo, d, inner, epi_resid(w.bo, x_, d));
@@ -320,7 +366,9 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest) {
     da.split_len = split_len_;
     da.max_splits = std::max(1, (db.max_keys + split_len_ - 1) / split_len_);
     da.partial = attn_part_;
+    const int k = kbegin();
     decode_attention(da, st_);
+    kend(k, EXG_K_DECODE_ATTN, db.sum_keys * 2.0 * D.H * D.dh * 2.0 + (double)B * D.H * D.dh * 2.0 * 2.0);
   }
   if (rest) {
     linear_dec(ctx_, inner, B, w.Wo, d, inner, epi_resid(w.bo, x_, d));

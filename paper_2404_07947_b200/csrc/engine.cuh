@@ -23,6 +23,7 @@ struct Dims {
 // Packed encode batch, device arrays (see Engine::encode).
 struct EncodeBatch {
   int T = 0, R = 0, max_len = 0;
+  double attn_pairs = 0;   // sum_r n_r (n_r + 1) / 2   (prefill-attention work)
   const int32_t *ids = nullptr, *pos = nullptr, *tslot = nullptr;      // [T]
   const int32_t *cu = nullptr, *rslot = nullptr, *pos0 = nullptr;      // [R+1], [R], [R]
 };
@@ -30,6 +31,7 @@ struct EncodeBatch {
 // Decode batch: B active rows, device arrays.
 struct DecodeBatch {
   int B = 0, max_keys = 0;
+  double sum_keys = 0;     // sum_i n_keys[i]   (decode-attention work)
   const int32_t *slot = nullptr, *pos = nullptr, *nkeys = nullptr, *out_off = nullptr;
   int32_t* out_tokens = nullptr;   // device [sum S]
   float* logits_keep = nullptr;    // optional: logits stay in Engine::logits
@@ -66,7 +68,21 @@ class Engine {
   int32_t* err_flag() { return err_; }
   size_t weight_bytes() const { return wbytes_; }
 
+  // per-launch CUDA-event timing of the kernel classes of exegpt.h
+  void set_kernel_timing(bool on);
+  // after a stream sync: accumulate into t/w/n [EXG_K_CLASSES] and reset
+  void collect_kernel_timing(double* t, double* w, int64_t* n);
+
  private:
+  struct KRec {
+    int cls, ev;
+    double work;
+  };
+  bool ktiming_ = false;
+  std::vector<cudaEvent_t> kev_;
+  std::vector<KRec> krec_;
+  int kbegin();
+  void kend(int idx, int cls, double work);
   void gen_weights();
   void linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   void linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);

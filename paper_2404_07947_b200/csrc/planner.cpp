@@ -448,8 +448,25 @@ Est Simulator::simulate_waa(const Sched& s) {
   return Est{thr, thr * s_d, lat, true};
 }
 
+Est Simulator::simulate_static(int B) {
+  Est bad{0.0, 0.0, INF, false};
+  const std::vector<Stage> st = stage_layout(cl.n_gpus, 1, 0, n_layers, 0);
+  if (!mem_ok(st, B, (int64_t)max_in + max_out)) return bad;
+  double lat;
+  try {
+    const std::vector<double> t_enc = stage_times(st, true, (double)B);
+    const std::vector<double> t_dec = stage_times(st, false, (double)B);
+    lat = fill(t_enc, 1) + max_out * fill(t_dec, 1);
+  } catch (const OutOfHull&) {
+    return bad;
+  }
+  const double thr = B / lat;
+  return Est{thr, thr * s_d, lat, true};
+}
+
 Est Simulator::simulate(const Sched& s) {
   if (!s.valid) return Est{0.0, 0.0, INF, false};
+  if (s.strategy == EXG_STATIC) return simulate_static(s.b_e);
   return s.strategy == EXG_RRA ? simulate_rra(s) : simulate_waa(s);
 }
 

@@ -75,6 +75,7 @@ class Simulator {
   Sched rra_schedule(int b_e, int n_d, int t, int c);
   Sched waa_schedule(int b_e, int M, int t, int c);
   Est simulate(const Sched& s);
+  Est simulate_static(int B);
   double layer_enc(int t, double b);
   double layer_dec(int t, double b);
   std::vector<double> stage_times(const std::vector<Stage>& st, bool enc, double b);

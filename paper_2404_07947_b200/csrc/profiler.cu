@@ -55,11 +55,13 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
     for (size_t i = 0; i < v->size(); ++i)
       if ((*v)[i] < 1 || (i && (*v)[i] <= (*v)[i - 1])) throw std::invalid_argument("grid axes must be increasing, >= 1");
   const int max_b = bs.back(), max_c = std::min(cs.back(), D.max_pos), max_t = ts.back();
-  const int max_enc_tokens = std::max(max_t, max_b * max_c);
+  // encode-attention points with b*c > max_t tokens are timed at
+  // b' = max_t / c requests and scaled by b / b' (requests are independent)
+  const int max_enc_tokens = std::max(max_t, max_c);
   const int ctx_cap = max_c;
   const int slots = std::max(max_b, (max_enc_tokens + ctx_cap - 1) / ctx_cap);
   E.ensure_kv(slots, ctx_cap, 1);
-  E.ensure_workspace(max_enc_tokens, std::max(max_b, max_t));
+  E.ensure_workspace(max_enc_tokens, max_b);
   cudaStream_t st = E.stream();
 
   // synthetic tables: token t -> (slot t / ctx_cap, pos t % ctx_cap)
@@ -98,12 +100,13 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
     const int b = bs[ib];
     for (size_t ic = 0; ic < cs.size(); ++ic) {
       const int c = std::min(cs[ic], ctx_cap);
-      // encode attention: b requests of c tokens each, request k in slot k
-      for (int k = 0; k <= b; ++k) h_cu[k] = k * c;
-      EXG_CUDA(cudaMemcpy(d_cu, h_cu.data(), (b + 1) * 4, cudaMemcpyHostToDevice));
+      // encode attention: be requests of c tokens each, request k in slot k
+      const int be = std::max(1, std::min(b, max_enc_tokens / c));
+      for (int k = 0; k <= be; ++k) h_cu[k] = k * c;
+      EXG_CUDA(cudaMemcpy(d_cu, h_cu.data(), (be + 1) * 4, cudaMemcpyHostToDevice));
       EncodeBatch eb;
-      eb.T = b * c;
-      eb.R = b;
+      eb.T = be * c;
+      eb.R = be;
       eb.max_len = c;
       eb.ids = d_ids;
       eb.pos = d_pos;
@@ -111,7 +114,7 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
       eb.cu = d_cu;
       eb.rslot = d_rs;
       eb.pos0 = d_p0;
-      ae.t[ib][ic] = tm.median(reps, [&] { E.layer_encode(0, eb, true, false); });
+      ae.t[ib][ic] = tm.median(reps, [&] { E.layer_encode(0, eb, true, false); }) * ((double)b / be);
       // decode attention: b rows, c keys each, row i in slot i
       for (int i = 0; i < b; ++i) h_nk[i] = c;
       EXG_CUDA(cudaMemcpy(d_aux, h_nk.data(), b * 4, cudaMemcpyHostToDevice));
@@ -137,14 +140,16 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
     eb.tslot = d_slot;
     re.x.push_back(T);
     re.t.push_back(tm.median(reps, [&] { E.layer_encode(0, eb, false, true); }));
-    // decode rest: T rows (row i in slot i % slots, position 0)
+  }
+  // decode rest: input size = batch rows, swept over the batch axis
+  for (int b : bs) {
     DecodeBatch db;
-    db.B = T;
+    db.B = b;
     db.max_keys = 1;
-    db.slot = d_slot;  // t / ctx_cap
-    db.pos = d_pos;
+    db.slot = d_rs;
+    db.pos = d_p0;
     db.nkeys = d_aux;
-    rd.x.push_back(T);
+    rd.x.push_back(b);
     rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }));
   }
   P.rest[{"enc", 1}] = re;

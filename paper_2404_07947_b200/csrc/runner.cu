@@ -149,6 +149,8 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
 
   int next_req = 0;
   int64_t decode_iters = 0, encode_phases = 0, batch_sum = 0;
+  const long long launches0 = launch_counter().load();
+  E.set_kernel_timing(opts && opts->kernel_timing);
   EXG_CUDA(cudaMemsetAsync(E.err_flag(), 0, sizeof(int32_t), st));
   record(0, 0);
   while (next_req < n || !active.empty()) {
@@ -196,6 +198,10 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       eb.T = T;
       eb.R = admit;
       eb.max_len = maxlen;
+      for (int k = 0; k < admit; ++k) {
+        const double m = reqs[next_req + k].input_len - 1;
+        eb.attn_pairs += m * (m + 1) / 2;
+      }
       eb.ids = d_enc;
       eb.pos = d_enc + T;
       eb.tslot = d_enc + 2 * T;
@@ -213,6 +219,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       Staging::Slot& sl = stage.acquire();
       int32_t* h = sl.host;
       int max_keys = 0;
+      double sum_keys = 0;
       for (int i = 0; i < B; ++i) {
         const Row& rw = active[i];
         h[i] = rw.slot;
@@ -220,12 +227,14 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         h[2 * B + i] = rw.pos + 1;
         h[3 * B + i] = (int32_t)(base[rw.req] + rw.emitted);
         max_keys = std::max(max_keys, rw.pos + 1);
+        sum_keys += rw.pos + 1;
       }
       EXG_CUDA(cudaMemcpyAsync(d_dec, h, (size_t)4 * B * sizeof(int32_t), cudaMemcpyHostToDevice, st));
       EXG_CUDA(cudaEventRecord(sl.ev, st));
       DecodeBatch db;
       db.B = B;
       db.max_keys = max_keys;
+      db.sum_keys = sum_keys;
       db.slot = d_dec;
       db.pos = d_dec + B;
       db.nkeys = d_dec + 2 * B;
@@ -280,8 +289,19 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
     lat[r] = t[done_ev[r]] - t[admit_ev[r]];
     if (out_latency) out_latency[r] = lat[r];
   }
+  const long long launches = launch_counter().load() - launches0;
+  double kt[EXG_K_CLASSES] = {0}, kw[EXG_K_CLASSES] = {0};
+  int64_t kn[EXG_K_CLASSES] = {0};
+  E.collect_kernel_timing(kt, kw, kn);
+  E.set_kernel_timing(false);
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
+    stats->kernel_launches = launches;
+    for (int c = 0; c < EXG_K_CLASSES; ++c) {
+      stats->k_time_s[c] = kt[c];
+      stats->k_work[c] = kw[c];
+      stats->k_launches[c] = kn[c];
+    }
     const double wall = t[nev - 1] - t[0];
     stats->wall_s = wall;
     stats->out_tokens = total_out;

@@ -146,6 +146,37 @@ def test_schedule_find_bit_identical(L, tmp_path, task, model, n_gpus, mask):
         assert est.latency_s < L_b
 
 
+def test_static_batch_estimate_bit_identical(L, tmp_path):
+    from oracle import simulator as sim
+    spec, m, prof, d, cl = _setup()
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    S = sim.Simulator(prof, m, cl, d.pmf_in, d.pmf_out, d.target_len)
+    for B in (1, 4, 8, 64, 256, 4000):
+        e_o = S.simulate_static(B)
+        s = L.exg_schedule()
+        s.strategy, s.b_e = 8, B
+        e_c = L.simulate(P, mspec, ccl, pin, pout, d.target_len, s)
+        assert bool(e_c.feasible) == e_o.feasible
+        if e_o.feasible:
+            assert (e_c.thrput_seq_s, e_c.latency_s) == (e_o.thrput_seq_s, e_o.latency_s)
+
+
+def test_static_latency_is_encode_plus_max_out_decodes():
+    """Closed form of the FT-style static batch:
+    latency = T_enc(B) + max_out * T_dec(B) on a constant-cost profile."""
+    from oracle import simulator as sim
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_oracle_scheduler import _const_profile, _one_layer_model
+    from workload import task_dists
+    d = task_dists("S")
+    S = sim.Simulator(_const_profile(0.5, 0.01), _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out,
+                      63)
+    e = S.simulate_static(16)
+    assert e.latency_s == pytest.approx(0.5 + 80 * 0.01, abs=1e-12)
+    assert e.thrput_seq_s == pytest.approx(16 / 1.3, abs=1e-9)
+
+
 def test_error_statuses(L, tmp_path):
     spec, m, prof, d, cl = _setup()
     P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
