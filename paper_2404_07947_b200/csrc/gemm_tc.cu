@@ -207,7 +207,8 @@ __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"
 template <int BN, int STAGES, int SWAP>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ Wb, int M, int N, int n_wblk,
-                   Work work, EpiParams ep, float* __restrict__ partial, int* __restrict__ counters) {
+                   Work work, EpiParams ep, float* __restrict__ partial, int* __restrict__ counters,
+                   int inkernel_fixup) {
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS =
       (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
       ++ui;
-      if (!u.full) {
+      if (!u.full && inkernel_fixup) {
         // stream-K fixup: the CTA completing the tile's last segment reduces
         const int64_t x0 = (int64_t)u.m * work.nkb;
         const int nseg = sk_owner(work, x0 + work.nkb - 1) - sk_owner(work, x0) + 1;
@@ -366,15 +367,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         if (*s_last) {
           __threadfence();
           const float* base = partial + ((int64_t)u.n * work.tiles_m + u.m) * work.max_segs * (int64_t)(BM * BN);
-          for (int c = c_lo; c < c_hi; ++c) {
-            float acc = 0.f;
-            for (int s = 0; s < nseg; ++s) acc += __ldcg(base + (int64_t)s * BM * BN + (int64_t)c * BM + r);
-            const int tok = u.n * BN + c;
-            if (row_ok && tok < N) {
-              if (SWAP)
-                epi_store(ep, tok, gm, acc);
-              else
-                epi_store(ep, gm, tok, acc);
+          // 16 columns at a time: all loads of a segment issue back to back
+          // (latency overlapped), segments summed in segment order
+          for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+            for (int s = 0; s < nseg; ++s) {
+              const float* src = base + (int64_t)s * BM * BN + (int64_t)c0 * BM + r;
+              float v[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + (int64_t)j * BM);
+#pragma unroll
+              for (int j = 0; j < 16; ++j) acc[j] += v[j];
+            }
+            if (!row_ok) continue;
+            if (SWAP) {
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (u.n * BN + c0 + j < N) epi_store(ep, u.n * BN + c0 + j, gm, acc[j]);
+            } else {
+              epi_store_row16(ep, gm, u.n * BN + c0, N, acc);
             }
           }
           if (threadIdx.x == 128) *cnt = 0;
@@ -424,6 +437,40 @@ Work make_work(int M, int N, int K, int BN, bool streamk) {
   return w;
 }
 
+// Grid-wide stream-K reduction: block (tile, 32-column slice), thread = row;
+// segments summed in segment order (same arithmetic as the in-kernel fixup).
+template <int BN, int SWAP>
+__global__ void __launch_bounds__(128) streamk_reduce_kernel(const float* __restrict__ partial, int M, int N, Work w,
+                                                             EpiParams ep) {
+  const int tile = blockIdx.x, m = tile % w.tiles_m, n = tile / w.tiles_m;
+  const int64_t x0 = (int64_t)m * w.nkb;
+  const int nseg = sk_owner(w, x0 + w.nkb - 1) - sk_owner(w, x0) + 1;
+  if (nseg <= 1) return;  // whole tile: stored by its CTA
+  const int r = threadIdx.x, gm = m * BM + r;
+  const float* base = partial + ((int64_t)n * w.tiles_m + m) * w.max_segs * (int64_t)(BM * BN);
+  for (int c0 = blockIdx.y * 32; c0 < blockIdx.y * 32 + 32; c0 += 16) {
+    float acc[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+    for (int s = 0; s < nseg; ++s) {
+      const float* src = base + (int64_t)s * BM * BN + (int64_t)c0 * BM + r;
+      float v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + (int64_t)j * BM);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] += v[j];
+    }
+    if (gm >= M) continue;
+    if (SWAP) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (n * BN + c0 + j < N) epi_store(ep, n * BN + c0 + j, gm, acc[j]);
+    } else {
+      epi_store_row16(ep, gm, n * BN + c0, N, acc);
+    }
+  }
+}
+
 // Workspace layout: [fixup counters: CNT_CAP ints][partial segments].  The
 // counter region sits at a fixed offset for every shape and token tile so
 // the zero state each fixup leaves behind is where the next launch looks.
@@ -454,8 +501,18 @@ void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wb
     counters = reinterpret_cast<int*>(ws);
     partial = ws + CNT_CAP;
   }
-  gemm_tc_kernel<BN, S, SWAP><<<w.G, GEMM_THREADS, smem, st>>>(tx, Wb, M, N, n_wblk, w, ep, partial, counters);
+  // small token tiles: the last CTA of a split tile reduces in-kernel; wide
+  // tiles (>= 128 columns): a grid-wide reduce kernel spreads the segment sums
+  // over all SMs instead of serialising a whole tile on one CTA's tail
+  const bool inkernel = BN < 128;
+  gemm_tc_kernel<BN, S, SWAP><<<w.G, GEMM_THREADS, smem, st>>>(tx, Wb, M, N, n_wblk, w, ep, partial, counters,
+                                                                  inkernel ? 1 : 0);
   EXG_CHECK_LAUNCH();
+  if (SWAP && !inkernel) {
+    dim3 grid(w.tiles_m * w.tiles_n, BN / 32);
+    streamk_reduce_kernel<BN, SWAP><<<grid, 128, 0, st>>>(partial, M, N, w, ep);
+    EXG_CHECK_LAUNCH();
+  }
 }
 
 __global__ void pack_blocked_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, int64_t rows, int64_t K,

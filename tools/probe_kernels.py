@@ -36,7 +36,7 @@ def gemm(tokens, features, K, decode, mode=0):
     L.check(L.lib().exg_op_pack_weight(W.data_ptr(), W0.data_ptr(), features, K, K, st()))
     out = torch.zeros(tokens, features, device=dev, dtype=torch.float32 if mode in (2, 3) else torch.bfloat16)
     nws = int(L.lib().exg_op_decode_workspace(features, K, tokens)) if decode else 0
-    ws = torch.empty(max(nws, 1), device=dev, dtype=torch.float32)
+    ws = torch.zeros(max(nws, 1), device=dev, dtype=torch.float32)   # fixup counters start at 0
     resid = out.data_ptr() if mode == 2 else None
     split = nws
 
