@@ -76,13 +76,16 @@ exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, c
                                    int32_t max_ctx, float scale, int32_t split_len, int32_t max_splits, float* partial,
                                    void* stream);
 
-/* K4 -- causal prefill attention over packed requests (cu_seqlens [R+1]);
- * request r's tokens sit at positions pos0[r].. of slot[r] and attend to
- * cached keys 0..own position (keys scattered beforehand). */
+/* K4 -- causal prefill attention over packed requests (cu_seqlens [R+1],
+ * T = cu_seqlens[R] tokens, q rows [T][ldq]); request r's tokens sit at
+ * positions pos0[r].. of slot[r] and attend to cached keys 0..own position
+ * (keys scattered beforehand); cache [n_slots][H][max_ctx][dh].  dh = 128
+ * runs on tcgen05 (S and O in TMEM, P rounded to bf16 for P.V); other head
+ * dims on a SIMT kernel with fp32 P. */
 exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, const void* vc,
                                     const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0, int32_t R,
                                     int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh, int32_t max_ctx,
-                                    float scale, void* stream);
+                                    int32_t n_slots, int32_t T, float scale, void* stream);
 
 /* K8 -- out[i] = argmax_v logits[i][v] (fp32 [B][ld]), lowest index on ties;
  * *err_flag (device int32, may be NULL) set to 1 on a NaN. */

@@ -141,7 +141,8 @@ _SIGS = {
     "exg_op_decode_attention": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int64, C.c_int32, C.c_int32,
                                           C.c_int32, C.c_int32, C.c_float, C.c_int32, C.c_int32, _P, _P]),
     "exg_op_prefill_attention": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, C.c_int32, _P,
-                                           C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_float, _P]),
+                                           C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                           C.c_float, _P]),
     "exg_op_argmax": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P]),
     "exg_op_decode_workspace": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
 }

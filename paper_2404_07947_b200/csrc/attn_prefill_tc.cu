@@ -1,0 +1,305 @@
+// K4 prefill attention on the 5th-gen tensor cores (dh = 128).
+//
+// CTA = 128 queries of one (request, head).  Per 128-key tile j:
+//   S_j = Q . K_j^T        tcgen05.mma kind::f16, M=128 N=128 K=128, fp32 in TMEM
+//   P_j = exp(s - m_j)     4 softmax warps, one query row per thread (TMEM -> regs),
+//                          causal mask, online max / sum; P_j -> smem as bf16
+//   O_j = P_j . V_j        tcgen05.mma, A = P (K-major), B = V (MN-major), fp32 in TMEM
+//   o   = o * exp(m_{j-1} - m_j) + O_j   (registers, one row per thread)
+// S and O are double-buffered in TMEM (4 x 128 columns) so the softmax of tile
+// j+1 overlaps the P.V of tile j.  Q, K, V arrive by 2-D TMA (SWIZZLE_128B)
+// straight from the packed qkv buffer and the KV cache.  Scores follow T4(e):
+// fp32(q.k) * fp32(scale); P is rounded to bf16 for the P.V MMA.
+#include "gemm_tc.cuh"
+#include "kernels.cuh"
+
+namespace exg {
+
+namespace {
+constexpr int FQ = 128;          // queries per CTA
+constexpr int FK = 128;          // keys per tile
+constexpr int FD = 128;          // head dim
+constexpr int TILE_BYTES = 128 * 64 * 2;            // one 128-row x 64-col SW128 box
+constexpr int Q_BYTES = 2 * TILE_BYTES;             // [128][128]
+constexpr int KV_BYTES = 2 * TILE_BYTES;            // K or V tile
+constexpr int P_BYTES = 2 * TILE_BYTES;
+constexpr int KV_STAGES = 2;
+constexpr size_t FMHA_SMEM = 1024 + Q_BYTES + KV_STAGES * 2 * KV_BYTES + P_BYTES + 256;
+
+__device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((smem_addr & 0x3FFFF) >> 4);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+struct FmhaParams {
+  const int32_t* cu_seqlens;
+  const int32_t* slot;
+  const int32_t* pos0;
+  int H, max_ctx;
+  float scale_log2;     // fp32(scale) * log2(e)
+  float scale;
+  bf16* out;
+  int64_t ldo;
+};
+
+__global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_constant__ CUtensorMap tmQ,
+                                                              const __grid_constant__ CUtensorMap tmK,
+                                                              const __grid_constant__ CUtensorMap tmV,
+                                                              FmhaParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem;
+  uint8_t* sK = sQ + Q_BYTES;                       // [stage]
+  uint8_t* sV = sK + KV_STAGES * KV_BYTES;          // [stage]
+  uint8_t* sP = sV + KV_STAGES * KV_BYTES;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
+  uint64_t* q_full = bars;              // 1
+  uint64_t* kv_full = bars + 1;         // 2
+  uint64_t* kv_empty = bars + 3;        // 2
+  uint64_t* s_full = bars + 5;          // 2
+  uint64_t* s_free = bars + 7;          // 2
+  uint64_t* p_full = bars + 9;          // 1
+  uint64_t* o_full = bars + 10;         // 2
+  uint64_t* o_free = bars + 12;         // 2
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const int r_req = blockIdx.z, h = blockIdx.y;
+  const int t0 = p.cu_seqlens[r_req], len = p.cu_seqlens[r_req + 1] - t0;
+  const int qb = blockIdx.x * FQ;
+  if (qb >= len) return;
+  const int pos0 = p.pos0[r_req];
+  const int last_key = pos0 + min(len, qb + FQ) - 1;  // inclusive
+  const int ntiles = last_key / FK + 1;
+  const int64_t kv_row0 = ((int64_t)p.slot[r_req] * p.H + h) * p.max_ctx;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmQ);
+    prefetch_tmap(&tmK);
+    prefetch_tmap(&tmV);
+    mbar_init(q_full, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&kv_full[i], 1);
+      mbar_init(&kv_empty[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&o_free[i], 4);
+    }
+    mbar_init(p_full, 4);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_holder, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  // TMEM columns: S buffers at 0 / 128, O buffers at 256 / 384
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(q_full, Q_BYTES);
+      tma_load_2d(sQ, &tmQ, q_full, h * FD, t0 + qb);
+      tma_load_2d(sQ + TILE_BYTES, &tmQ, q_full, h * FD + 64, t0 + qb);
+      for (int j = 0; j < ntiles; ++j) {
+        const int s = j & 1;
+        if (j >= KV_STAGES) mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&kv_full[s], 2 * KV_BYTES);
+        const int row = (int)(kv_row0 + j * FK);
+        tma_load_2d(sK + s * KV_BYTES, &tmK, &kv_full[s], 0, row);
+        tma_load_2d(sK + s * KV_BYTES + TILE_BYTES, &tmK, &kv_full[s], 64, row);
+        tma_load_2d(sV + s * KV_BYTES, &tmV, &kv_full[s], 0, row);
+        tma_load_2d(sV + s * KV_BYTES + TILE_BYTES, &tmV, &kv_full[s], 64, row);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = umma_idesc_bf16(FQ, FK);                   // K-major A and B
+      constexpr uint32_t idesc_o = umma_idesc_bf16(FQ, FD) | (1u << 16);      // B (V) MN-major
+      mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int s = j & 1;
+        mbar_wait(&kv_full[s], (j >> 1) & 1);
+        if (j >= 2) mbar_wait(&s_free[s], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + s * 128;
+        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + s * KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < FD / 16; ++k) {
+          const uint32_t off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
+          umma_bf16(d, umma_desc_sw128(qa + off), umma_desc_sw128(kb + off), idesc_s, k ? 1u : 0u);
+        }
+        umma_commit(&s_full[s]);
+      };
+      issue_s(0);
+      for (int j = 0; j < ntiles; ++j) {
+        if (j + 1 < ntiles) issue_s(j + 1);
+        // O_j = P_j . V_j
+        const int s = j & 1;
+        mbar_wait(p_full, j & 1);
+        if (j >= 2) mbar_wait(&o_free[s], ((j >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + 256 + s * 128;
+        const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + s * KV_BYTES);
+#pragma unroll
+        for (int k = 0; k < FK / 16; ++k) {
+          // A (P, K-major): 64-key blocks of 16 KB, 32 B per 16 keys
+          const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
+          // B (V, MN-major): 16 keys = two 8-key core groups of 1024 B
+          const uint32_t b_off = k * 2048;
+          umma_bf16(d, umma_desc_sw128(pa + a_off), desc_mn_sw128(vb + b_off, TILE_BYTES, 1024), idesc_o,
+                    k ? 1u : 0u);
+        }
+        umma_commit(&o_full[s]);
+        umma_commit(&kv_empty[s]);
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;
+    const int r = q * 32 + lane;                    // query row of the tile = TMEM lane
+    const int qpos = pos0 + qb + r;                  // absolute position of this query
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    float o[FD];
+#pragma unroll
+    for (int d = 0; d < FD; ++d) o[d] = 0.f;
+    float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+    for (int j = 0; j <= ntiles; ++j) {
+      if (j < ntiles) {
+        const int s = j & 1;
+        mbar_wait(&s_full[s], (j >> 1) & 1);
+        tc_fence_after();
+        // pass 1: row max over the tile (masked)
+        const uint32_t sa = tmem + lane_base + s * 128;
+        float mx = -INFINITY;
+        for (int c = 0; c < FK; c += 16) {
+          float v[16];
+          tmem_ld16(sa + c, v);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int kpos = j * FK + c + e;
+            const float sc = (kpos <= qpos) ? v[e] * p.scale : -INFINITY;
+            mx = fmaxf(mx, sc);
+          }
+        }
+        const float m_new = fmaxf(m, mx);
+        const float alpha = (m == -INFINITY) ? 0.f : exp2f((m - m_new) * 1.4426950408889634f);
+        // P_j may overwrite the P buffer once P_{j-1}.V_{j-1} has completed
+        if (j >= 1) mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
+        float sum = 0.f;
+        for (int c = 0; c < FK; c += 16) {
+          float v[16];
+          tmem_ld16(sa + c, v);
+          uint32_t pk[8];
+#pragma unroll
+          for (int e = 0; e < 16; e += 2) {
+            const int kpos = j * FK + c + e;
+            const float p0 = (kpos <= qpos && m_new != -INFINITY)
+                                 ? exp2f((v[e] * p.scale - m_new) * 1.4426950408889634f) : 0.f;
+            const float p1 = (kpos + 1 <= qpos && m_new != -INFINITY)
+                                 ? exp2f((v[e + 1] * p.scale - m_new) * 1.4426950408889634f) : 0.f;
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
+            pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          // row r, keys c..c+15: two 16-byte chunks in the SW128 K-major image
+          uint8_t* blk = sP + (c >> 6) * TILE_BYTES;
+          const int ch = (c & 63) >> 3;
+          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+        l = l * alpha + sum;
+        m = m_new;
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&s_free[s]);
+          mbar_arrive(p_full);
+        }
+        // accumulate O_{j-1} (its rescale factor was alpha_prev)
+        if (j >= 1) {
+          const int so = (j - 1) & 1;
+          const uint32_t oa = tmem + lane_base + 256 + so * 128;
+          tc_fence_after();
+#pragma unroll
+          for (int c = 0; c < FD; c += 16) {
+            float v[16];
+            tmem_ld16(oa + c, v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[c + e] = o[c + e] * alpha_prev + v[e];
+          }
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&o_free[so]);
+        }
+        alpha_prev = alpha;
+      } else {
+        // last tile's P.V
+        const int so = (j - 1) & 1;
+        mbar_wait(&o_full[so], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+        const uint32_t oa = tmem + lane_base + 256 + so * 128;
+#pragma unroll
+        for (int c = 0; c < FD; c += 16) {
+          float v[16];
+          tmem_ld16(oa + c, v);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o[c + e] = o[c + e] * alpha_prev + v[e];
+        }
+      }
+    }
+    if (qb + r < len) {
+      const float inv = 1.f / l;
+      bf16* dst = p.out + (int64_t)(t0 + qb + r) * p.ldo + h * FD;
+#pragma unroll
+      for (int c = 0; c < FD; c += 8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          __nv_bfloat162 b2 = __floats2bfloat162_rn(o[c + e] * inv, o[c + e + 1] * inv);
+          pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+        }
+        *reinterpret_cast<uint4*>(dst + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+}  // namespace
+
+bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
+  if (a.dh != FD) return false;
+  static bool attr = false;
+  if (!attr) {
+    EXG_CUDA(cudaFuncSetAttribute(fmha_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FMHA_SMEM));
+    attr = true;
+  }
+  // Q: the packed qkv buffer [q_rows][ldq] (rows past the last token are
+  // zero-filled by TMA and never stored); K/V: the cache viewed as
+  // [kv_rows = slots*H*max_ctx][dh]
+  FmhaParams p{a.cu_seqlens, a.slot, a.pos0, a.H, a.max_ctx,
+               a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo};
+  const CUtensorMap tq = make_tmap_bf16(a.q, a.q_rows, a.ldq, a.ldq, 128);
+  const CUtensorMap tk = make_tmap_bf16(a.kc, a.kv_rows, FD, FD, 128);
+  const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 128);
+  dim3 grid((a.max_len + FQ - 1) / FQ, a.H, a.R);
+  fmha_prefill_kernel<<<grid, 256, FMHA_SMEM, st>>>(tq, tk, tv, p);
+  EXG_CHECK_LAUNCH();
+  return true;
+}
+
+}  // namespace exg

@@ -374,10 +374,11 @@ exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, c
 exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, const void* vc,
                                     const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0, int32_t R,
                                     int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh, int32_t max_ctx,
-                                    float scale, void* stream) {
+                                    int32_t n_slots, int32_t T, float scale, void* stream) {
   return guarded([&] {
     exg::PrefillAttnArgs a{(const exg::bf16*)q, ldq, (const exg::bf16*)kc, (const exg::bf16*)vc, cu_seqlens, slot,
-                           pos0, R, max_len, (exg::bf16*)out, ldo, H, dh, max_ctx, scale};
+                           pos0, R, max_len, (exg::bf16*)out, ldo, H, dh, max_ctx, scale, (int64_t)T,
+                           (int64_t)n_slots * H * max_ctx};
     exg::prefill_attention(a, (cudaStream_t)stream);
     return EXG_OK;
   });

@@ -319,7 +319,8 @@ void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest) {
   }
   if (attn) {
     PrefillAttnArgs pa{qkv_, 3 * inner, kc(l), vc(l), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,
-                       ctx_, inner, D.H, D.dh, slot_ctx_, scale};
+                       ctx_, inner, D.H, D.dh, slot_ctx_, scale,
+                       (int64_t)eb.T, (int64_t)kv_slots_ * D.H * slot_ctx_};
     const int k = kbegin();
     prefill_attention(pa, st_);
     kend(k, EXG_K_PREFILL_ATTN, 4.0 * D.H * D.dh * eb.attn_pairs);

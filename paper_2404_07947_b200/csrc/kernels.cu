@@ -439,6 +439,7 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
 
 void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st) {
   if (a.R <= 0 || a.max_len <= 0) return;
+  if (prefill_attention_tc(a, st)) return;
   dim3 grid((a.max_len + 31) / 32, a.H, a.R);
   switch (a.dh) {
     case 16: prefill_attn_kernel<16><<<grid, 128, 0, st>>>(a); break;

@@ -80,8 +80,12 @@ struct PrefillAttnArgs {
   int64_t ldo;
   int H, dh, max_ctx;
   float scale;
+  int64_t q_rows;      // rows of the qkv buffer (tokens)
+  int64_t kv_rows;     // slots * H * max_ctx
 };
+// dh = 128: tcgen05 FMHA (attn_prefill_tc.cu); other head dims: SIMT kernel
 void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);
+bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st);
 
 // ---- K8: greedy argmax per row (lowest index wins ties; NaN -> err flag) ---
 void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, int32_t* err_flag, cudaStream_t st);
