@@ -16,22 +16,40 @@
 namespace exg {
 
 namespace {
+// Reads a buffer larger than L2 so every timed repetition starts with the
+// layer's weights and KV cold, as they are inside a real step (each layer's
+// weights are streamed once per iteration).
+__global__ void l2_flush_kernel(const int4* __restrict__ p, int64_t n, int* sink) {
+  int acc = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    acc ^= __ldcs(p + i).x;
+  if (acc == 0x7fffffff) *sink = acc;
+}
+
 struct Timer {
   cudaEvent_t a, b;
   cudaStream_t st;
+  int4* flush = nullptr;
+  int64_t flush_n = 0;
   explicit Timer(cudaStream_t s) : st(s) {
     EXG_CUDA(cudaEventCreate(&a));
     EXG_CUDA(cudaEventCreate(&b));
+    flush_n = (256ll << 20) / sizeof(int4);
+    EXG_CUDA(cudaMalloc(&flush, flush_n * sizeof(int4) + 16));
+    EXG_CUDA(cudaMemsetAsync(flush, 0, flush_n * sizeof(int4) + 16, st));
   }
   ~Timer() {
     cudaEventDestroy(a);
     cudaEventDestroy(b);
+    if (flush) cudaFree(flush);
   }
   template <class F>
   double median(int reps, F&& f) {
     f();  // warm-up
     std::vector<double> v;
     for (int r = 0; r < reps; ++r) {
+      l2_flush_kernel<<<148 * 4, 256, 0, st>>>(flush, flush_n, reinterpret_cast<int*>(flush + flush_n));
+      EXG_CHECK_LAUNCH();
       EXG_CUDA(cudaEventRecord(a, st));
       f();
       EXG_CUDA(cudaEventRecord(b, st));
