@@ -26,6 +26,7 @@ inline uint64_t tid_of(int slot, int kind) { return (uint64_t)slot * 64 + kind; 
 __global__ void embed_decode_kernel(float* __restrict__ x, const int32_t* __restrict__ last_tok,
                                     const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
                                     const bf16* __restrict__ tok, const bf16* __restrict__ pe, int d) {
+  griddep_launch_dependents();
   const int i = blockIdx.x;
   const int64_t id = last_tok[slot[i]];
   const bf16* b = pe + (int64_t)pos[i] * d;

@@ -44,6 +44,12 @@ PFN_encodeTiled_t encode_fn() {
   return fn;
 }
 
+// diagnostics only (exg_diag_gemm_flags): bit 0 = skip the MMAs
+int& gemm_debug_flags() {
+  static int f = 0;
+  return f;
+}
+
 int num_sms() {
   static int n = 0;
   if (!n) {
@@ -198,17 +204,25 @@ struct UnitIter {
   }
 };
 
-constexpr int EPI_WARPS = 8;
-constexpr int GEMM_THREADS = 128 + 32 * EPI_WARPS;
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, %0;" ::"n"(32 * EPI_WARPS) : "memory"); }
+// 8 epilogue warps (two per TMEM lane quarter, each half of the columns).
+// Under PDL the producer streams its first weight blocks before the grid
+// dependency resolves.
+template <int SWAP>
+struct EpiCfg {
+  static constexpr int WARPS = 8;
+  static constexpr int THREADS = 128 + 32 * WARPS;
+};
 
 // SWAP = 1 (decode): A = weights (blocked), B = activations (TMA 2-D).
 // SWAP = 0 (prefill): A = activations (TMA 2-D), B = weights (blocked).
 template <int BN, int STAGES, int SWAP>
-__global__ void __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmX, const bf16* __restrict__ Wb, int M, int N, int n_wblk,
                    Work work, EpiParams ep, float* __restrict__ partial, int* __restrict__ counters,
-                   int inkernel_fixup) {
+                   int inkernel_fixup, int g_dbg) {
+  constexpr int EPI_WARPS = EpiCfg<SWAP>::WARPS;
+  auto epi_bar = [] { asm volatile("bar.sync 1, %0;" ::"n"(32 * EpiCfg<SWAP>::WARPS) : "memory"); };
+  griddep_launch_dependents();
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS =
       (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
@@ -247,37 +261,65 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   Unit u;
   if (warp == 0) {
     if (lane == 0) {
+      // Weights never depend on the previous kernel: the first STAGES weight
+      // loads are issued before griddepcontrol.wait; the activation loads of
+      // those stages follow once the previous grid has completed.
+      auto wbytes_of = [&](int n) {
+        if (SWAP) return A_BYTES;
+        int bytes = 0;
+        for (int rr = 0; rr < BN; rr += BM)
+          if ((n * BN + rr) / BM < n_wblk) bytes += (BN < BM ? BN : BM) * BK * 2;
+        return bytes;
+      };
+      auto issue_w = [&](uint32_t s, int m, int n, int kb) {
+        if (SWAP) {
+          bulk_load(sA + s * A_BYTES, Wb + ((int64_t)m * work.nkb + kb) * BLK_ELEMS, A_BYTES, &full[s]);
+        } else {
+          // weight rows [n*BN, n*BN+BN) = blocks (n*BN)/128 ..; BN = 64 uses half a block
+          for (int rr = 0; rr < BN; rr += BM) {
+            const int blk = (n * BN + rr) / BM;
+            if (blk >= n_wblk) break;
+            const int sub = (n * BN + rr) % BM;
+            bulk_load(sB + s * B_BYTES + rr * BK * 2, Wb + ((int64_t)blk * work.nkb + kb) * BLK_ELEMS + (int64_t)sub * BK,
+                      (uint32_t)((BN < BM ? BN : BM) * BK * 2), &full[s]);
+          }
+        }
+      };
+      auto issue_x = [&](uint32_t s, int m, int n, int kb) {
+        if (SWAP)
+          tma_load_2d(sB + s * B_BYTES, &tmX, &full[s], kb * BK, n * BN);
+        else
+          tma_load_2d(sA + s * A_BYTES, &tmX, &full[s], kb * BK, m * BM);
+      };
+      int pend[STAGES][3];
+      int npend = 0;
+      bool waited = false;
       uint32_t g = 0;
       while (it.next(u)) {
         for (int kb = u.kb0; kb < u.kb1; ++kb, ++g) {
           const uint32_t s = g % STAGES;
           const uint32_t ph = (g / STAGES) & 1;
+          if (!waited && g >= STAGES) {
+            griddep_wait();
+            for (int i = 0; i < npend; ++i) issue_x(i, pend[i][0], pend[i][1], pend[i][2]);
+            waited = true;
+          }
           if (g >= STAGES) mbar_wait(&empty[s], ph ^ 1);
-          if (SWAP) {
-            mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
-            bulk_load(sA + s * A_BYTES, Wb + ((int64_t)u.m * work.nkb + kb) * BLK_ELEMS, A_BYTES, &full[s]);
-            tma_load_2d(sB + s * B_BYTES, &tmX, &full[s], kb * BK, u.n * BN);
+          mbar_arrive_expect_tx(&full[s], wbytes_of(u.n) + (SWAP ? B_BYTES : A_BYTES));
+          issue_w(s, u.m, u.n, kb);
+          if (waited) {
+            issue_x(s, u.m, u.n, kb);
           } else {
-            // weight rows [n*BN, n*BN+BN) = blocks (n*BN)/128 .. ; BN = 64 uses half a block
-            const int row0 = u.n * BN;
-            int bytes = 0;
-            for (int rr = 0; rr < BN; rr += BM) {
-              const int blk = (row0 + rr) / BM;
-              if (blk >= n_wblk) break;
-              bytes += (BN < BM ? BN : BM) * BK * 2;
-            }
-            mbar_arrive_expect_tx(&full[s], A_BYTES + bytes);
-            tma_load_2d(sA + s * A_BYTES, &tmX, &full[s], kb * BK, u.m * BM);
-            for (int rr = 0; rr < BN; rr += BM) {
-              const int blk = (row0 + rr) / BM;
-              if (blk >= n_wblk) break;
-              const int sub = (row0 + rr) % BM;  // 0 or 64 (BN = 64)
-              bulk_load(sB + s * B_BYTES + rr * BK * 2,
-                        Wb + ((int64_t)blk * work.nkb + kb) * BLK_ELEMS + (int64_t)sub * BK,
-                        (uint32_t)((BN < BM ? BN : BM) * BK * 2), &full[s]);
-            }
+            pend[npend][0] = u.m;
+            pend[npend][1] = u.n;
+            pend[npend][2] = kb;
+            ++npend;
           }
         }
+      }
+      if (!waited) {
+        griddep_wait();
+        for (int i = 0; i < npend; ++i) issue_x(i, pend[i][0], pend[i][1], pend[i][2]);
       }
     }
   } else if (warp == 1) {
@@ -294,6 +336,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (g_dbg & 1) {  // diagnostics: memory pipeline only (no MMA)
+            mbar_arrive(&empty[s]);
+            continue;
+          }
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
           const uint32_t b_base = smem_u32(sB + s * B_BYTES);
 #pragma unroll
@@ -310,8 +356,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // 8 epilogue warps: warp w reads TMEM lanes 32*(w%4).. (hardware rule)
     // and one half of the accumulator columns
     const int q = warp & 3;
-    const int half = (warp - 4) >> 2;
-    const int c_lo = half * (BN / 2), c_hi = c_lo + BN / 2;
+    constexpr int PARTS = EPI_WARPS / 4;  // column parts per TMEM lane quarter
+    const int part = (warp - 4) >> 2;
+    const int c_lo = part * (BN / PARTS), c_hi = c_lo + BN / PARTS;
+    griddep_wait();  // outputs / residual may still be in use by the previous kernel
     const int r = q * 32 + lane;
     uint32_t ui = 0;
     while (it.next(u)) {
@@ -404,14 +452,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 }
 
-template <int BN>
+// Ring depth: up to 8 stages within ~200 KB (one CTA per SM).  Measured: a
+// half-SM ring (2 CTAs/SM so the next GEMM co-resides under PDL) loses more
+// weight-stream depth than the overlap gains.
+template <int BN, int SWAP>
 constexpr int stages_for() {
-  return (BN * BK * 2 + A_BYTES) * 8 <= 200 * 1024 ? 8 : (200 * 1024) / (BN * BK * 2 + A_BYTES);
+  constexpr int budget = 200 * 1024;
+  constexpr int per = BN * BK * 2 + A_BYTES;
+  return budget / per > 8 ? 8 : budget / per;
 }
 
-template <int BN>
+template <int BN, int SWAP>
 size_t smem_bytes() {
-  constexpr int S = stages_for<BN>();
+  constexpr int S = stages_for<BN, SWAP>();
   return 1024 + (size_t)S * (A_BYTES + BN * BK * 2) + (2 * S + 4) * 8 + 16;
 }
 
@@ -442,6 +495,7 @@ Work make_work(int M, int N, int K, int BN, bool streamk) {
 template <int BN, int SWAP>
 __global__ void __launch_bounds__(128) streamk_reduce_kernel(const float* __restrict__ partial, int M, int N, Work w,
                                                              EpiParams ep) {
+  griddep_launch_dependents();
   const int tile = blockIdx.x, m = tile % w.tiles_m, n = tile / w.tiles_m;
   const int64_t x0 = (int64_t)m * w.nkb;
   const int nseg = sk_owner(w, x0 + w.nkb - 1) - sk_owner(w, x0) + 1;
@@ -483,9 +537,9 @@ size_t ws_need(const Work& w, int BN) {
 template <int BN, int SWAP>
 void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wblk, const EpiParams& ep, float* ws,
             size_t ws_floats, cudaStream_t st) {
-  constexpr int S = stages_for<BN>();
+  constexpr int S = stages_for<BN, SWAP>();
   static bool attr_set = false;
-  const size_t smem = smem_bytes<BN>();
+  const size_t smem = smem_bytes<BN, SWAP>();
   if (!attr_set) {
     EXG_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, S, SWAP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)smem));
@@ -505,8 +559,20 @@ void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wb
   // tiles (>= 128 columns): a grid-wide reduce kernel spreads the segment sums
   // over all SMs instead of serialising a whole tile on one CTA's tail
   const bool inkernel = BN < 128;
-  gemm_tc_kernel<BN, S, SWAP><<<w.G, GEMM_THREADS, smem, st>>>(tx, Wb, M, N, n_wblk, w, ep, partial, counters,
-                                                                  inkernel ? 1 : 0);
+  // programmatic dependent launch: the kernel may start while the previous
+  // one drains; it prefetches weights, then griddepcontrol.wait()s
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(w.G);
+  cfg.blockDim = dim3(EpiCfg<SWAP>::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  EXG_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, S, SWAP>, tx, Wb, M, N, n_wblk, w, ep, partial, counters,
+                              inkernel ? 1 : 0, gemm_debug_flags()));
   EXG_CHECK_LAUNCH();
   if (SWAP && !inkernel) {
     dim3 grid(w.tiles_m * w.tiles_n, BN / 32);
@@ -590,3 +656,5 @@ void linear(const LinearArgs& a, cudaStream_t st) {
 }
 
 }  // namespace exg
+
+extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }

@@ -50,6 +50,7 @@ void weightgen(bf16* dst, int64_t rows, int64_t cols, int64_t ld, const GenParam
 // ============================================================================
 __global__ void embed_kernel(float* __restrict__ x, const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
                              const bf16* __restrict__ tok, const bf16* __restrict__ pe, int d, int tok_blocked) {
+  griddep_launch_dependents();
   const int t = blockIdx.x;
   const int64_t id = ids[t];
   const bf16* b = pe + (int64_t)pos[t] * d;
@@ -84,6 +85,7 @@ __device__ __forceinline__ float block_sum_256(float v, float* red) {
 __global__ void __launch_bounds__(256) layernorm_kernel(bf16* __restrict__ y, int64_t ldy, const float* __restrict__ x,
                                                         int64_t ldx, const bf16* __restrict__ g,
                                                         const bf16* __restrict__ b, int d, float eps) {
+  griddep_launch_dependents();
   __shared__ float red[8];
   const float* xr = x + (int64_t)blockIdx.x * ldx;
   float s = 0.f;
@@ -160,6 +162,7 @@ struct DecodeCfg {
 
 template <int DH>
 __global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a) {
+  griddep_launch_dependents();
   using C = DecodeCfg<DH>;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* sk = dsm;
@@ -310,6 +313,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a) {
 
 template <int DH>
 __global__ void decode_combine_kernel(DecodeAttnArgs a) {
+  griddep_launch_dependents();
   const int i = blockIdx.x / a.H, h = blockIdx.x % a.H;
   const int nk = a.n_keys[i];
   const int nsplit = (nk + a.split_len - 1) / a.split_len;
@@ -364,6 +368,7 @@ void decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
 // ============================================================================
 template <int DH>
 __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
+  griddep_launch_dependents();
   constexpr int QPB = 32, LPQ = 4, DPL = DH / LPQ, KTILE = 32;
   __shared__ __align__(16) bf16 ks[KTILE][DH];
   __shared__ __align__(16) bf16 vs[KTILE][DH];

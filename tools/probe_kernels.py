@@ -91,10 +91,39 @@ def pattn(R, n, H=40, dh=128):
     print("prefill-attn R=%d n=%d: %8.1f us  %7.1f TFLOP/s" % (R, n, t * 1e6, flops / t / 1e12))
 
 
+def stream_probe():
+    """HBM ceiling of the bulk-copy ring (no MMA): 148..592 CTAs x chunk x stages."""
+    import ctypes
+    f = L.lib().exg_diag_stream_probe
+    f.restype = ctypes.c_int
+    f.argtypes = [ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                  ctypes.c_void_p]
+    buf = torch.zeros(1 << 30, dtype=torch.uint8, device=dev)
+    sink = torch.zeros(1, dtype=torch.int32, device=dev)
+    for total in (1 << 30, 157286400, 52428800):
+        for ctas, chunk, stages in ((148, 16384, 8), (148, 32768, 6), (296, 16384, 6), (444, 16384, 4)):
+            per = (total // ctas) // chunk * chunk
+            t = timeit(lambda: f(buf.data_ptr(), per, ctas, chunk, stages, sink.data_ptr(), st()))
+            print("stream %4d MB ctas=%d chunk=%d stages=%d: %6.1f us %.1f GB/s" %
+                  (total >> 20, ctas, chunk, stages, t * 1e6, per * ctas / t / 1e9))
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "gemm":
         T, N, K = map(int, sys.argv[2:5])
         gemm(T, N, K, sys.argv[5] == "dec", int(sys.argv[6]) if len(sys.argv) > 6 else 0)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "nomma":
+        for flags in (0, 1):
+            L.lib().exg_diag_gemm_flags(flags)
+            print("flags", flags)
+            for B in (16, 64):
+                gemm(B, 15360, 5120, True)
+                gemm(B, 5120, 5120, True, 2)
+                gemm(B, 5120, 20480, True, 2)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "stream":
+        stream_probe()
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "dattn":
         dattn(int(sys.argv[2]), int(sys.argv[3]))
@@ -115,3 +144,4 @@ if __name__ == "__main__":
         dattn(B, c)
     pattn(16, 256)
     pattn(8, 512)
+
