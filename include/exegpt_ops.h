@@ -27,7 +27,8 @@ extern "C" {
  * : (r+row_off)*canon_cols + (c+col_off) of tensor `tensor_id`;
  * gain = 1 for norm gains 1+U(+-0.1), else U(+-sqrt(3)*0.02).  blocked = 1
  * writes the GEMM blocked layout (below) of the [rows][cols] matrix instead
- * (ld ignored, exg_op_blocked_elems(rows, cols) elements, zero padded). */
+ * (ld ignored, exg_op_blocked_elems(rows, cols) elements; the padding of the
+ * last tiles is not written -- zero-fill the destination first). */
 exg_status exg_op_weightgen(void* dst, int64_t rows, int64_t cols, int64_t ld, uint64_t seed, uint64_t tensor_id,
                             int32_t gain, int32_t transposed, int64_t canon_cols, int64_t row_off, int64_t col_off,
                             int32_t blocked, void* stream);

@@ -295,6 +295,18 @@ def rra_schedule(b_e: int, b_d: int, n_d: int) -> exg_schedule:
     return s
 
 
+def make_schedule(strategy: int, b_e: int, b_d: int, stages, n_d: int = 0, b_m: int = 0, n_enc_gpus: int = 0,
+                  tp_degree: int = 1, tp_gpus: int = 0) -> exg_schedule:
+    """A caller-filled multi-stage schedule; stages = [(first_gpu, n_gpus,
+    layer_begin, layer_end), ...] (WAA: encoder stages first)."""
+    s = exg_schedule()
+    s.strategy, s.b_e, s.b_d, s.b_m, s.n_d = strategy, b_e, b_d, b_m, n_d
+    s.tp_degree, s.tp_gpus, s.n_enc_gpus, s.n_stages = tp_degree, tp_gpus, n_enc_gpus, len(stages)
+    for k, (g, ng, l0, l1) in enumerate(stages):
+        s.stage_first_gpu[k], s.stage_n_gpus[k], s.stage_layer_begin[k], s.stage_layer_end[k] = g, ng, l0, l1
+    return s
+
+
 def simulate(prof: Profile, mspec: exg_model_spec, cl: exg_cluster_spec, pin: Pmf, pout: Pmf, target_len: int,
              sched: exg_schedule) -> exg_estimate:
     est = exg_estimate()

@@ -12,12 +12,14 @@
 #include "../../include/exegpt.h"
 #include "../../include/exegpt_ops.h"
 #include "engine.cuh"
+#include "multi.h"
 #include "planner.h"
 #include "profiler.h"
 #include "runner.h"
 
 struct exg_ctx {
-  std::unique_ptr<exg::Engine> engine;
+  std::unique_ptr<exg::Engine> engine;      // single-GPU context
+  std::unique_ptr<exg::MultiCtx> multi;     // n_gpus > 1 emulated on one device
   exg_model_spec spec;
   exg_cluster_spec cluster;
   int rank = 0, world = 1, device = 0;
@@ -137,7 +139,10 @@ exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluste
     c->rank = rank;
     c->world = world;
     c->device = device;
-    c->engine = std::make_unique<exg::Engine>(*spec, device);
+    if (cluster && cluster->n_gpus > 1)
+      c->multi = std::make_unique<exg::MultiCtx>(*spec, device);  // every GPU of a layout emulated on `device`
+    else
+      c->engine = std::make_unique<exg::Engine>(*spec, device);
     *out = c.release();
     return EXG_OK;
   });
@@ -154,6 +159,7 @@ exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profi
   return guarded([&] {
     if (!ctx || !grid || !out) throw std::invalid_argument("null argument");
     auto p = std::make_unique<exg_profile>();
+    if (!ctx->engine) throw std::invalid_argument("profile on a single-GPU context (cluster.n_gpus = 1)");
     exg::profile_layers(*ctx->engine, *grid, &p->p);
     *out = p.release();
     return EXG_OK;
@@ -259,6 +265,13 @@ exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* r
     if (!ctx || !sched || (!reqs && n > 0)) throw std::invalid_argument("null argument");
     if (n < 1) throw std::invalid_argument("empty request batch");
     EXG_CUDA(cudaSetDevice(ctx->device));
+    if (ctx->multi) {
+      int gpus = 0;
+      for (int k = 0; k < sched->n_stages && k < EXG_MAX_STAGES; ++k) gpus += sched->stage_n_gpus[k];
+      if (gpus > ctx->cluster.n_gpus) return fail(EXG_E_INFEASIBLE, "schedule needs more GPUs than the cluster has");
+      ctx->multi->run(*sched, reqs, n, out_tokens, out_latency_s, stats, opts);
+      return EXG_OK;
+    }
     if (sched->strategy != EXG_RRA)
       return fail(EXG_E_INFEASIBLE, "WAA needs >= 2 GPUs (SPEC.md:233); this context has 1");
     if (sched->tp_degree > 1 || sched->n_stages > 1)
@@ -273,8 +286,8 @@ exg_status exg_op_weightgen(void* dst, int64_t rows, int64_t cols, int64_t ld, u
                             int32_t gain, int32_t transposed, int64_t canon_cols, int64_t row_off, int64_t col_off,
                             int32_t blocked, void* stream) {
   return guarded([&] {
-    exg::GenParams g{seed,   tensor_id, gain,    (float)(2.0 * std::sqrt(3.0) * 0.02), 0.2f, transposed, canon_cols,
-                     row_off, col_off,  blocked};
+    exg::GenParams g{seed,    tensor_id, gain,    (float)(2.0 * std::sqrt(3.0) * 0.02), 0.2f, transposed, canon_cols,
+                     row_off, col_off,   blocked, 0};
     exg::weightgen((exg::bf16*)dst, rows, cols, ld, g, (cudaStream_t)stream);
     return EXG_OK;
   });

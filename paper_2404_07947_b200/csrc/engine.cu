@@ -1,14 +1,20 @@
-// Engine: seeded weights, workspace, encode / decode forward passes.
+// Engine: seeded weights, workspace, encode / decode forward passes of one
+// model shard (layers [l0, l1), TP rank of tp).
 //
 // Layer (pre-LN) with the rounding points of T4:
 //   h   = bf16(LN1(x))                 x: fp32 residual
 //   qkv = bf16(h W_qkv + b)            -> K,V scattered into the row's slot
 //   ctx = bf16(attention(q, K, V))     fp32 scores / softmax / P.V
-//   x  += ctx W_o + b_o                fp32 epilogue
+//   x  += ctx W_o + b_o                fp32 (TP: fp32 partials all-reduced, T4(i))
 //   h   = bf16(LN2(x))
 //   f   = bf16(act(h W_1 + b_1))       act in fp32
-//   x  += f W_2 + b_2                  fp32 epilogue
-// final: logits = bf16(LN_f(x)) E^T (fp32), argmax.
+//   x  += f W_2 + b_2                  fp32 (TP: as above)
+// final (last stage): logits = bf16(LN_f(x)) E^T (fp32), argmax.
+//
+// Tensor parallelism (Megatron): rank r of t holds heads
+// [r H/t, (r+1) H/t) of Q, K, V and W_o's matching input rows, and FFN
+// columns [r F/t, (r+1) F/t); the two residual updates of a layer are the
+// layer's two all-reduces.
 #include <cmath>
 #include <cstring>
 
@@ -77,6 +83,13 @@ __global__ void __launch_bounds__(256) argmax_scatter_kernel(const float* __rest
   }
 }
 
+__global__ void add_bias_resid_kernel(float* __restrict__ x, const float* __restrict__ p,
+                                      const bf16* __restrict__ bias, int64_t n, int d) {
+  griddep_launch_dependents();
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    x[i] = x[i] + (p[i] + bf2f(bias[i % d]));
+}
+
 template <typename T>
 T* carve(uint8_t*& p, size_t n) {
   T* r = reinterpret_cast<T*>(p);
@@ -85,7 +98,15 @@ T* carve(uint8_t*& p, size_t n) {
 }
 }  // namespace
 
-Engine::Engine(const exg_model_spec& s, int device) : dev_(device) {
+void add_bias_resid(float* x, const float* p, const bf16* bias, int rows, int d, cudaStream_t st) {
+  const int64_t n = (int64_t)rows * d;
+  if (n <= 0) return;
+  add_bias_resid_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(x, p, bias, n, d);
+  EXG_CHECK_LAUNCH();
+}
+
+Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cudaStream_t stream)
+    : S_(shard), dev_(device) {
   if (s.arch == EXG_ARCH_T5 || s.n_enc_layers != 0) throw std::invalid_argument("encoder-decoder models: not built yet");
   D.arch = s.arch;
   D.L = s.n_dec_layers;
@@ -98,10 +119,23 @@ Engine::Engine(const exg_model_spec& s, int device) : dev_(device) {
   D.max_pos = s.max_pos;
   D.seed = s.weight_seed;
   D.act = s.arch == EXG_ARCH_OPT ? ACT_RELU : ACT_GELU;
+  if (S_.l1 < 0) S_.l1 = D.L;
+  if (S_.l0 < 0 || S_.l1 > D.L || S_.l0 >= S_.l1) throw std::invalid_argument("bad shard layer range");
+  if (S_.tp < 1 || D.H % S_.tp || D.ff % S_.tp || S_.tp_rank < 0 || S_.tp_rank >= S_.tp)
+    throw std::invalid_argument("n_heads and d_ff must be divisible by the TP degree");
+  D.Hl = D.H / S_.tp;
+  D.inner_l = D.Hl * D.dh;
+  D.ffl = D.ff / S_.tp;
   if (D.d % 64 || D.inner % 64 || D.ff % 64) throw std::invalid_argument("d, H*dh, d_ff must be multiples of 64");
+  if (D.inner_l % 8 || D.ffl % 8) throw std::invalid_argument("TP shard widths must be multiples of 8");
   if (D.dh != 16 && D.dh != 64 && D.dh != 128) throw std::invalid_argument("d_head must be 16, 64 or 128");
   EXG_CUDA(cudaSetDevice(dev_));
-  EXG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  if (stream) {
+    st_ = stream;
+  } else {
+    EXG_CUDA(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+    own_stream_ = true;
+  }
   EXG_CUDA(cudaMalloc(&err_, sizeof(int32_t)));
   EXG_CUDA(cudaMemsetAsync(err_, 0, sizeof(int32_t), st_));
   gen_weights();
@@ -110,57 +144,77 @@ Engine::Engine(const exg_model_spec& s, int device) : dev_(device) {
 Engine::~Engine() {
   cudaSetDevice(dev_);
   cudaStreamSynchronize(st_);
-  for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)last_tok_, (void*)err_, (void*)prof_tables_})
+  for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)last_tok_, (void*)err_})
     if (p) cudaFree(p);
   for (cudaEvent_t e : kev_) cudaEventDestroy(e);
-  if (st_) cudaStreamDestroy(st_);
+  if (own_stream_ && st_) cudaStreamDestroy(st_);
 }
 
 void Engine::gen_weights() {
-  const size_t d = D.d, inner = D.inner, ff = D.ff;
+  const size_t d = D.d, il = D.inner_l, fl = D.ffl;
+  const int64_t inner = D.inner, ff = D.ff;
+  const int r = S_.tp_rank;
   auto al = [](size_t n) { return (n * 2 + 255) & ~size_t(255); };
   auto bl = [&](size_t rows, size_t K) { return al((size_t)blocked_elems(rows, K)); };
-  size_t per_layer = al(d) * 4 + bl(3 * inner, d) + al(3 * inner) + bl(d, inner) + al(d) + bl(ff, d) + al(ff) +
-                     bl(d, ff) + al(d);
-  wbytes_ = bl(D.V, d) + al((size_t)D.max_pos * d) + 2 * al(d) + per_layer * D.L;
+  const size_t per_layer =
+      al(d) * 4 + bl(3 * il, d) + al(3 * il) + bl(d, il) + al(d) + bl(fl, d) + al(fl) + bl(d, fl) + al(d);
+  const bool need_tok = S_.embed || S_.head;
+  wbytes_ = (need_tok ? bl(D.V, d) : 0) + (S_.embed ? al((size_t)D.max_pos * d) : 0) + (S_.head ? 2 * al(d) : 0) +
+            per_layer * n_layers();
   EXG_CUDA(cudaMalloc(&wbuf_, wbytes_));
+  EXG_CUDA(cudaMemsetAsync(wbuf_, 0, wbytes_, st_));  // zero padding of the blocked tiles
   uint8_t* p = wbuf_;
   const float c_mat = (float)(2.0 * std::sqrt(3.0) * 0.02);
   const float c_gain = 0.2f;
+  // generate rows x cols of tensor (slot, kind) with canonical index offsets
+  // (row_off, col_off) into dst (plain row-major, or blocked starting at
+  // destination row dst_row0 of a matrix with `cols` columns)
   auto gen = [&](bf16* dst, int64_t rows, int64_t cols, int slot, int kind, int gain, int transposed,
-                 int64_t canon_cols, int blocked = 0) {
-    GenParams g{D.seed, tid_of(slot, kind), gain, c_mat, c_gain, transposed, canon_cols, 0, 0, blocked};
+                 int64_t canon_cols, int blocked = 0, int64_t row_off = 0, int64_t col_off = 0,
+                 int64_t dst_row0 = 0) {
+    GenParams g{D.seed, tid_of(slot, kind), gain, c_mat, c_gain, transposed, canon_cols, row_off, col_off, blocked,
+                dst_row0};
     weightgen(dst, rows, cols, cols, g, st_);
   };
   auto carve_blk = [&](size_t rows, size_t K) { return carve<bf16>(p, (size_t)blocked_elems(rows, K)); };
-  // token embedding in the GEMM blocked layout: it is the A operand of the
-  // tied LM head (decode swap-AB); the embedding gather indexes it directly
-  tok_emb_ = carve_blk(D.V, d);
-  gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d, 1);
-  pos_emb_ = carve<bf16>(p, (size_t)D.max_pos * d);
-  gen(pos_emb_, D.max_pos, d, 0, K_POS, 0, 0, d);
-  lnf_g_ = carve<bf16>(p, d);
-  gen(lnf_g_, 1, d, 0, K_LNFG, 1, 0, d);
-  lnf_b_ = carve<bf16>(p, d);
-  gen(lnf_b_, 1, d, 0, K_LNFB, 0, 0, d);
-  layers_.resize(D.L);
-  for (int l = 0; l < D.L; ++l) {
-    const int s = 1001 + l;
+  if (need_tok) {
+    // token embedding in the GEMM blocked layout: the A operand of the tied
+    // LM head (decode swap-AB); the embedding gather indexes it directly
+    tok_emb_ = carve_blk(D.V, d);
+    gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d, 1);
+  }
+  if (S_.embed) {
+    pos_emb_ = carve<bf16>(p, (size_t)D.max_pos * d);
+    gen(pos_emb_, D.max_pos, d, 0, K_POS, 0, 0, d);
+  }
+  if (S_.head) {
+    lnf_g_ = carve<bf16>(p, d);
+    gen(lnf_g_, 1, d, 0, K_LNFG, 1, 0, d);
+    lnf_b_ = carve<bf16>(p, d);
+    gen(lnf_b_, 1, d, 0, K_LNFB, 0, 0, d);
+  }
+  layers_.resize(n_layers());
+  for (int l = 0; l < n_layers(); ++l) {
+    const int s = 1001 + S_.l0 + l;
     LayerW& w = layers_[l];
     w.ln1_g = carve<bf16>(p, d);  gen(w.ln1_g, 1, d, s, K_LN1G, 1, 0, d);
     w.ln1_b = carve<bf16>(p, d);  gen(w.ln1_b, 1, d, s, K_LN1B, 0, 0, d);
     w.ln2_g = carve<bf16>(p, d);  gen(w.ln2_g, 1, d, s, K_LN2G, 1, 0, d);
     w.ln2_b = carve<bf16>(p, d);  gen(w.ln2_b, 1, d, s, K_LN2B, 0, 0, d);
     // matrices stored W^T [out][in] (K-major for tcgen05) in the blocked,
-    // pre-swizzled GEMM layout; canonical index from W[in][out]
-    w.Wqkv = carve_blk(3 * inner, d);   gen(w.Wqkv, 3 * inner, d, s, K_WQKV, 0, 1, 3 * inner, 1);
-    w.bqkv = carve<bf16>(p, 3 * inner); gen(w.bqkv, 1, 3 * inner, s, K_BQKV, 0, 0, 3 * inner);
-    w.Wo = carve_blk(d, inner);         gen(w.Wo, d, inner, s, K_WO, 0, 1, d, 1);
-    w.bo = carve<bf16>(p, d);           gen(w.bo, 1, d, s, K_BO, 0, 0, d);
-    w.W1 = carve_blk(ff, d);            gen(w.W1, ff, d, s, K_W1, 0, 1, ff, 1);
-    w.b1 = carve<bf16>(p, ff);          gen(w.b1, 1, ff, s, K_B1, 0, 0, ff);
-    w.W2 = carve_blk(d, ff);            gen(w.W2, d, ff, s, K_W2, 0, 1, d, 1);
-    w.b2 = carve<bf16>(p, d);           gen(w.b2, 1, d, s, K_B2, 0, 0, d);
+    // pre-swizzled GEMM layout; canonical index from the unsharded W[in][out]
+    w.Wqkv = carve_blk(3 * il, d);
+    w.bqkv = carve<bf16>(p, 3 * il);
+    for (int sec = 0; sec < 3; ++sec) {  // q, k, v rows of this rank's heads
+      gen(w.Wqkv, il, d, s, K_WQKV, 0, 1, 3 * inner, 1, sec * inner + r * (int64_t)il, 0, sec * (int64_t)il);
+      gen(w.bqkv + sec * il, 1, il, s, K_BQKV, 0, 0, 3 * inner, 0, 0, sec * inner + r * (int64_t)il);
+    }
+    w.Wo = carve_blk(d, il);   gen(w.Wo, d, il, s, K_WO, 0, 1, d, 1, 0, r * (int64_t)il);
+    w.bo = carve<bf16>(p, d);  gen(w.bo, 1, d, s, K_BO, 0, 0, d);
+    w.W1 = carve_blk(fl, d);   gen(w.W1, fl, d, s, K_W1, 0, 1, ff, 1, r * (int64_t)fl, 0);
+    w.b1 = carve<bf16>(p, fl); gen(w.b1, 1, fl, s, K_B1, 0, 0, ff, 0, 0, r * (int64_t)fl);
+    w.W2 = carve_blk(d, fl);   gen(w.W2, d, fl, s, K_W2, 0, 1, d, 1, 0, r * (int64_t)fl);
+    w.b2 = carve<bf16>(p, d);  gen(w.b2, 1, d, s, K_B2, 0, 0, d);
   }
   EXG_CUDA(cudaStreamSynchronize(st_));
 }
@@ -174,23 +228,27 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   cap_rows_ = std::max(max_rows, cap_rows_);
   const size_t T = cap_tokens_, R = cap_rows_;
   size_t sk = 0;
-  for (auto fk : {std::make_pair(3 * D.inner, D.d), std::make_pair(D.d, D.inner), std::make_pair(D.ff, D.d),
-                  std::make_pair(D.d, D.ff), std::make_pair(D.V, D.d)})
+  for (auto fk : {std::make_pair(3 * D.inner_l, D.d), std::make_pair(D.d, D.inner_l), std::make_pair(D.ffl, D.d),
+                  std::make_pair(D.d, D.ffl), std::make_pair(D.V, D.d)})
     sk = std::max(sk, decode_ws_floats(fk.first, fk.second, (int)R));
   splitk_cap_ = sk;
   max_splits_cap_ = (D.max_pos + split_len_ - 1) / split_len_;
-  const size_t parts = R * D.H * (size_t)max_splits_cap_ * (D.dh + 2);
+  const size_t parts = R * D.Hl * (size_t)max_splits_cap_ * (D.dh + 2);
+  const size_t tp_part = S_.tp > 1 ? T * D.d : 0;
+  const size_t logit_rows = S_.head ? R : 0;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
-  const size_t bytes = al(T * D.d * 4) + al(T * D.d * 2) + al(T * 3 * D.inner * 2) + al(T * D.inner * 2) +
-                       al(T * D.ff * 2) + al(R * D.V * 4) + al(sk * 4) + al(parts * 4);
+  const size_t bytes = al(T * D.d * 4) + al(tp_part * 4) + al(T * D.d * 2) + al(T * 3 * D.inner_l * 2) +
+                       al(T * D.inner_l * 2) + al(T * D.ffl * 2) + al(logit_rows * D.V * 4) + al(sk * 4) +
+                       al(parts * 4);
   uint8_t* p;
   EXG_CUDA(cudaMalloc(&p, bytes));
   x_ = carve<float>(p, T * D.d);
+  part_ = tp_part ? carve<float>(p, tp_part) : nullptr;
   h_ = carve<bf16>(p, T * D.d);
-  qkv_ = carve<bf16>(p, T * 3 * D.inner);
-  ctx_ = carve<bf16>(p, T * D.inner);
-  ff_ = carve<bf16>(p, T * D.ff);
-  logits_ = carve<float>(p, R * D.V);
+  qkv_ = carve<bf16>(p, T * 3 * D.inner_l);
+  ctx_ = carve<bf16>(p, T * D.inner_l);
+  ff_ = carve<bf16>(p, T * D.ffl);
+  logits_ = logit_rows ? carve<float>(p, logit_rows * D.V) : nullptr;
   splitk_ws_ = carve<float>(p, sk);
   attn_part_ = carve<float>(p, parts);
   EXG_CUDA(cudaMemsetAsync(x_, 0, bytes, st_));
@@ -198,7 +256,7 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
 
 void Engine::ensure_kv(int slots, int slot_ctx, int layers) {
   if (slot_ctx > D.max_pos) throw std::invalid_argument("slot_ctx exceeds max_pos");
-  if (layers < 0) layers = D.L;
+  if (layers < 0) layers = n_layers();
   if (slots <= kv_slots_ && slot_ctx == slot_ctx_ && layers <= kv_layers_) return;
   EXG_CUDA(cudaStreamSynchronize(st_));
   if (kv_) EXG_CUDA(cudaFree(kv_));
@@ -218,6 +276,7 @@ void Engine::ensure_kv(int slots, int slot_ctx, int layers) {
   }
   EXG_CUDA(cudaMemsetAsync(kv_, 0, bytes, st_));
   EXG_CUDA(cudaMalloc(&last_tok_, sizeof(int32_t) * kv_slots_));
+  EXG_CUDA(cudaMemsetAsync(last_tok_, 0, sizeof(int32_t) * kv_slots_, st_));
 }
 
 void Engine::linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep) {
@@ -235,8 +294,22 @@ void Engine::linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, i
   const int k = kbegin();
   linear(a, st_);
   const double out_b = ep.mode == EPI_RESID ? 8.0 : (ep.mode == EPI_F32 ? 4.0 : 2.0);
-  kend(k, EXG_K_DECODE_GEMM,
-       2.0 * features * K + 2.0 * tokens * K + out_b * tokens * features);
+  kend(k, EXG_K_DECODE_GEMM, 2.0 * features * K + 2.0 * tokens * K + out_b * tokens * features);
+}
+
+void Engine::linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep) {
+  LinearArgs a;
+  a.X = X;
+  a.ldx = ldx;
+  a.Wb = W;
+  a.K = K;
+  ep.tokens = tokens;
+  ep.features = features;
+  a.ep = ep;
+  a.decode = false;
+  const int k = kbegin();
+  linear(a, st_);
+  kend(k, EXG_K_PREFILL_GEMM, 2.0 * tokens * features * K);
 }
 
 int Engine::kbegin() {
@@ -276,21 +349,6 @@ void Engine::collect_kernel_timing(double* t, double* w, int64_t* n) {
   krec_.clear();
 }
 
-void Engine::linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep) {
-  LinearArgs a;
-  a.X = X;
-  a.ldx = ldx;
-  a.Wb = W;
-  a.K = K;
-  ep.tokens = tokens;
-  ep.features = features;
-  a.ep = ep;
-  a.decode = false;
-  const int k = kbegin();
-  linear(a, st_);
-  kend(k, EXG_K_PREFILL_GEMM, 2.0 * tokens * features * K);
-}
-
 static EpiParams epi_bf16(const bf16* bias, bf16* out, int64_t ldo, int act = ACT_NONE) {
   EpiParams e;
   e.mode = act == ACT_NONE ? EPI_BF16 : EPI_BF16_ACT;
@@ -300,68 +358,135 @@ static EpiParams epi_bf16(const bf16* bias, bf16* out, int64_t ldo, int act = AC
   e.ldo = ldo;
   return e;
 }
-static EpiParams epi_resid(const bf16* bias, float* resid, int64_t ldr) {
+
+void Engine::resid_update(bool decode, const bf16* X, int64_t ldx, int tokens, const bf16* W, int K,
+                          const bf16* bias) {
   EpiParams e;
-  e.mode = EPI_RESID;
-  e.bias = bias;
-  e.resid = resid;
-  e.ldr = ldr;
-  return e;
+  if (S_.tp == 1) {
+    e.mode = EPI_RESID;
+    e.bias = bias;
+    e.resid = x_;
+    e.ldr = D.d;
+  } else {
+    e.mode = EPI_F32;
+    e.out_f32 = part_;
+    e.ldo = D.d;
+  }
+  if (decode)
+    linear_dec(X, ldx, tokens, W, D.d, K, e);
+  else
+    linear_pre(X, ldx, tokens, W, D.d, K, e);
+  if (S_.tp > 1) {
+    if (red_) {
+      red_->allreduce_sum(part_, (int64_t)tokens * D.d, st_);
+      add_bias_resid(x_, part_, bias, tokens, D.d, st_);
+    } else {
+      // lockstep TP group on one device: the group sums every rank's part_
+      // (sum_tp_parts) and then calls finish_pending()
+      pend_bias_ = bias;
+      pend_rows_ = tokens;
+    }
+  }
 }
 
-void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest) {
+void Engine::finish_pending() {
+  if (!pend_bias_) return;
+  add_bias_resid(x_, part_, pend_bias_, pend_rows_, D.d, st_);
+  pend_bias_ = nullptr;
+}
+
+void Engine::enc_attn_block(int l, const EncodeBatch& eb) {
   const LayerW& w = layers_[l];
-  const int T = eb.T, d = D.d, inner = D.inner;
+  layer_encode(l, eb, true, false, 1);
+  resid_update(false, ctx_, D.inner_l, eb.T, w.Wo, D.inner_l, w.bo);
+}
+
+void Engine::enc_ffn_block(int l, const EncodeBatch& eb) { layer_encode(l, eb, false, true, 2); }
+
+void Engine::dec_attn_block(int l, const DecodeBatch& db) {
+  const LayerW& w = layers_[l];
+  layer_decode(l, db, true, false, 1);
+  resid_update(true, ctx_, D.inner_l, db.B, w.Wo, D.inner_l, w.bo);
+}
+
+void Engine::dec_ffn_block(int l, const DecodeBatch& db) { layer_decode(l, db, false, true, 2); }
+
+// part 0: the whole layer (attention and / or the rest, for the profiler);
+// part 1: LN1, QKV, KV scatter, attention (up to, excluding, the O-proj);
+// part 2: LN2, FFN1, FFN2 (after the attention residual update).
+void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest, int part) {
+  const LayerW& w = layers_[l];
+  const int T = eb.T, d = D.d, il = D.inner_l;
   const float scale = (float)(1.0 / std::sqrt((double)D.dh));
+  if (part == 2) {
+    layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, T, d, 1e-5f, st_);
+    linear_pre(h_, d, T, w.W1, D.ffl, d, epi_bf16(w.b1, ff_, D.ffl, D.act));
+    resid_update(false, ff_, D.ffl, T, w.W2, D.ffl, w.b2);
+    return;
+  }
+  if (part == 1) attn = rest = true;
   if (rest) {
     layernorm(h_, d, x_, d, w.ln1_g, w.ln1_b, T, d, 1e-5f, st_);
-    linear_pre(h_, d, T, w.Wqkv, 3 * inner, d, epi_bf16(w.bqkv, qkv_, 3 * inner));
-    kv_scatter(kc(l), vc(l), qkv_, eb.tslot, eb.pos, T, D.H, D.dh, slot_ctx_, st_);
+    linear_pre(h_, d, T, w.Wqkv, 3 * il, d, epi_bf16(w.bqkv, qkv_, 3 * il));
+    kv_scatter(kc(l), vc(l), qkv_, eb.tslot, eb.pos, T, D.Hl, D.dh, slot_ctx_, st_);
   }
   if (attn) {
-    PrefillAttnArgs pa{qkv_, 3 * inner, kc(l), vc(l), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,
-                       ctx_, inner, D.H, D.dh, slot_ctx_, scale,
-                       (int64_t)eb.T, (int64_t)kv_slots_ * D.H * slot_ctx_};
+    PrefillAttnArgs pa{qkv_, 3 * il, kc(l), vc(l), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,
+                       ctx_, il, D.Hl, D.dh, slot_ctx_, scale,
+                       (int64_t)eb.T, (int64_t)kv_slots_ * D.Hl * slot_ctx_};
     const int k = kbegin();
     prefill_attention(pa, st_);
-    kend(k, EXG_K_PREFILL_ATTN, 4.0 * D.H * D.dh * eb.attn_pairs);
+    kend(k, EXG_K_PREFILL_ATTN, 4.0 * D.Hl * D.dh * eb.attn_pairs);
   }
+  if (part == 1) return;
   if (rest) {
-    linear_pre(ctx_, inner, T, w.Wo, d, inner, epi_resid(w.bo, x_, d));
+    resid_update(false, ctx_, il, T, w.Wo, il, w.bo);
     layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, T, d, 1e-5f, st_);
-    linear_pre(h_, d, T, w.W1, D.ff, d, epi_bf16(w.b1, ff_, D.ff, D.act));
-    linear_pre(ff_, D.ff, T, w.W2, d, D.ff, epi_resid(w.b2, x_, d));
+    linear_pre(h_, d, T, w.W1, D.ffl, d, epi_bf16(w.b1, ff_, D.ffl, D.act));
+    resid_update(false, ff_, D.ffl, T, w.W2, D.ffl, w.b2);
   }
+}
+
+void Engine::embed_encode(const EncodeBatch& eb) {
+  if (eb.T > cap_tokens_) throw std::invalid_argument("encode batch exceeds workspace");
+  if (S_.embed && eb.T > 0) embed(x_, eb.ids, eb.pos, tok_emb_, pos_emb_, eb.T, D.d, st_, 1);
 }
 
 void Engine::encode(const EncodeBatch& eb) {
   if (eb.T <= 0) return;
-  if (eb.T > cap_tokens_) throw std::invalid_argument("encode batch exceeds workspace");
-  embed(x_, eb.ids, eb.pos, tok_emb_, pos_emb_, eb.T, D.d, st_, 1);
-  for (int l = 0; l < D.L; ++l) layer_encode(l, eb, true, true);
+  if (S_.tp > 1 && !red_) throw std::logic_error("TP shard without a reducer: drive it through a TP group");
+  embed_encode(eb);
+  for (int l = 0; l < n_layers(); ++l) layer_encode(l, eb, true, true);
 }
 
-void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest) {
+void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, int part) {
   const LayerW& w = layers_[l];
-  const int B = db.B, d = D.d, inner = D.inner;
+  const int B = db.B, d = D.d, il = D.inner_l;
   const float scale = (float)(1.0 / std::sqrt((double)D.dh));
+  if (part == 2) {
+    layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, B, d, 1e-5f, st_);
+    linear_dec(h_, d, B, w.W1, D.ffl, d, epi_bf16(w.b1, ff_, D.ffl, D.act));
+    resid_update(true, ff_, D.ffl, B, w.W2, D.ffl, w.b2);
+    return;
+  }
+  if (part == 1) attn = rest = true;
   if (rest) {
     layernorm(h_, d, x_, d, w.ln1_g, w.ln1_b, B, d, 1e-5f, st_);
-    linear_dec(h_, d, B, w.Wqkv, 3 * inner, d, epi_bf16(w.bqkv, qkv_, 3 * inner));
-    kv_scatter(kc(l), vc(l), qkv_, db.slot, db.pos, B, D.H, D.dh, slot_ctx_, st_);
+    linear_dec(h_, d, B, w.Wqkv, 3 * il, d, epi_bf16(w.bqkv, qkv_, 3 * il));
+    kv_scatter(kc(l), vc(l), qkv_, db.slot, db.pos, B, D.Hl, D.dh, slot_ctx_, st_);
   }
   if (attn) {
     DecodeAttnArgs da;
     da.q = qkv_;
-    da.ldq = 3 * inner;
+    da.ldq = 3 * il;
     da.kc = kc(l);
     da.vc = vc(l);
     da.slot = db.slot;
     da.n_keys = db.nkeys;
     da.out = ctx_;
-    da.ldo = inner;
+    da.ldo = il;
     da.B = B;
-    da.H = D.H;
+    da.H = D.Hl;
     da.dh = D.dh;
     da.max_ctx = slot_ctx_;
     da.scale = scale;
@@ -370,45 +495,59 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest) {
     da.partial = attn_part_;
     const int k = kbegin();
     decode_attention(da, st_);
-    kend(k, EXG_K_DECODE_ATTN, db.sum_keys * 2.0 * D.H * D.dh * 2.0 + (double)B * D.H * D.dh * 2.0 * 2.0);
+    kend(k, EXG_K_DECODE_ATTN, db.sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)B * D.Hl * D.dh * 2.0 * 2.0);
   }
+  if (part == 1) return;
   if (rest) {
-    linear_dec(ctx_, inner, B, w.Wo, d, inner, epi_resid(w.bo, x_, d));
+    resid_update(true, ctx_, il, B, w.Wo, il, w.bo);
     layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, B, d, 1e-5f, st_);
-    linear_dec(h_, d, B, w.W1, D.ff, d, epi_bf16(w.b1, ff_, D.ff, D.act));
-    linear_dec(ff_, D.ff, B, w.W2, d, D.ff, epi_resid(w.b2, x_, d));
+    linear_dec(h_, d, B, w.W1, D.ffl, d, epi_bf16(w.b1, ff_, D.ffl, D.act));
+    resid_update(true, ff_, D.ffl, B, w.W2, D.ffl, w.b2);
+  }
+}
+
+void Engine::embed_decode(const DecodeBatch& db) {
+  const int B = db.B;
+  if (B > cap_rows_) throw std::invalid_argument("decode batch exceeds workspace");
+  if (S_.embed && B > 0) {
+    embed_decode_kernel<<<B, 256, 0, st_>>>(x_, last_tok_, db.slot, db.pos, tok_emb_, pos_emb_, D.d);
+    EXG_CHECK_LAUNCH();
   }
 }
 
 void Engine::decode(const DecodeBatch& db) {
-  const int B = db.B;
-  if (B <= 0) return;
-  if (B > cap_rows_) throw std::invalid_argument("decode batch exceeds workspace");
-  embed_decode_kernel<<<B, 256, 0, st_>>>(x_, last_tok_, db.slot, db.pos, tok_emb_, pos_emb_, D.d);
-  EXG_CHECK_LAUNCH();
-  for (int l = 0; l < D.L; ++l) layer_decode(l, db, true, true);
-  layernorm(h_, D.d, x_, D.d, lnf_g_, lnf_b_, B, D.d, 1e-5f, st_);
-  EpiParams e;
-  e.mode = EPI_F32;
-  e.out_f32 = logits_;
-  e.ldo = D.V;
-  linear_dec(h_, D.d, B, tok_emb_, D.V, D.d, e);
-  argmax_scatter_kernel<<<B, 256, 0, st_>>>(logits_, D.V, db.slot, db.out_off, last_tok_, db.out_tokens, err_);
-  EXG_CHECK_LAUNCH();
+  if (db.B <= 0) return;
+  if (S_.tp > 1 && !red_) throw std::logic_error("TP shard without a reducer: drive it through a TP group");
+  embed_decode(db);
+  for (int l = 0; l < n_layers(); ++l) layer_decode(l, db, true, true);
+  head_decode(db);
 }
 
-}  // namespace exg
+void Engine::head_decode(const DecodeBatch& db) {
+  const int B = db.B;
+  if (S_.head && B > 0) {
+    layernorm(h_, D.d, x_, D.d, lnf_g_, lnf_b_, B, D.d, 1e-5f, st_);
+    EpiParams e;
+    e.mode = EPI_F32;
+    e.out_f32 = logits_;
+    e.ldo = D.V;
+    linear_dec(h_, D.d, B, tok_emb_, D.V, D.d, e);
+    argmax_scatter_kernel<<<B, 256, 0, st_>>>(logits_, D.V, db.slot, db.out_off, last_tok_, db.out_tokens, err_);
+    EXG_CHECK_LAUNCH();
+  }
+}
 
-namespace exg {
 namespace {
 __global__ void set_last_tokens_kernel(int32_t* last_tok, const int32_t* rslot, const int32_t* tok, int n) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < n) last_tok[rslot[k]] = tok[k];
 }
 }  // namespace
+
 void set_last_tokens(int32_t* last_tok, const int32_t* rslot, const int32_t* tok, int n, cudaStream_t st) {
   if (n <= 0) return;
   set_last_tokens_kernel<<<(n + 127) / 128, 128, 0, st>>>(last_tok, rslot, tok, n);
   EXG_CHECK_LAUNCH();
 }
+
 }  // namespace exg

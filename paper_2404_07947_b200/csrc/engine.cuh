@@ -1,6 +1,13 @@
-// Device-side model: seeded weights in HBM, activation workspace, KV slot
-// pool, and the encode (prefill) / decode forward passes built from the
-// sm_100a kernels.  One Engine per GPU (rank).
+// Device-side model shard: seeded weights in HBM, activation workspace, KV
+// slot pool, and the encode (prefill) / decode forward passes built from the
+// sm_100a kernels.
+//
+// An Engine holds the layers [l0, l1) of the model, tensor-parallel rank
+// tp_rank of tp (heads and FFN columns split as in Megatron),
+// plus the embeddings if it is a first stage and the final norm + LM head if
+// it is a last stage.  A single-GPU model is the shard {0, L, 1, 0, true,
+// true}.  Pipelines, TP groups and WAA encoder/decoder sets are built from
+// several Engines by the executors (runner.cu, multi.cu).
 #pragma once
 #include <vector>
 
@@ -18,6 +25,22 @@ struct LayerW {
 struct Dims {
   int arch, L, d, H, dh, inner, ff, V, max_pos, act;
   uint64_t seed;
+  // local (tensor-parallel shard) sizes
+  int Hl, inner_l, ffl;
+};
+
+struct EngineShard {
+  int l0 = 0, l1 = -1;        // layer range (l1 = -1: all layers)
+  int tp = 1, tp_rank = 0;    // tensor-parallel degree and rank
+  bool embed = true;          // first stage: token + position embeddings
+  bool head = true;           // last stage: final LayerNorm + tied LM head + argmax
+};
+
+// TP reduction of fp32 partial sums (O-projection / FFN2 outputs, T4(i)).
+struct Reducer {
+  virtual ~Reducer() = default;
+  // in-place sum over the TP group; called by every rank of the group
+  virtual void allreduce_sum(float* buf, int64_t n, cudaStream_t st) = 0;
 };
 
 // Packed encode batch, device arrays (see Engine::encode).
@@ -33,37 +56,65 @@ struct DecodeBatch {
   int B = 0, max_keys = 0;
   double sum_keys = 0;     // sum_i n_keys[i]   (decode-attention work)
   const int32_t *slot = nullptr, *pos = nullptr, *nkeys = nullptr, *out_off = nullptr;
-  int32_t* out_tokens = nullptr;   // device [sum S]
-  float* logits_keep = nullptr;    // optional: logits stay in Engine::logits
+  int32_t* out_tokens = nullptr;   // device [sum S] (last stage)
 };
 
 class Engine {
  public:
-  Engine(const exg_model_spec& spec, int device);
+  // stream == nullptr: the engine creates its own non-blocking stream
+  Engine(const exg_model_spec& spec, int device, const EngineShard& shard = EngineShard(),
+         cudaStream_t stream = nullptr);
   ~Engine();
   Engine(const Engine&) = delete;
 
   const Dims& dims() const { return D; }
+  const EngineShard& shard() const { return S_; }
+  int n_layers() const { return S_.l1 - S_.l0; }
   int device() const { return dev_; }
   cudaStream_t stream() const { return st_; }
+  void set_reducer(Reducer* r) { red_ = r; }
 
   void ensure_workspace(int max_tokens, int max_rows);
   void ensure_kv(int slots, int slot_ctx, int layers = -1);
   int kv_slots() const { return kv_slots_; }
   int slot_ctx() const { return slot_ctx_; }
   int32_t* last_tok() { return last_tok_; }
+  // residual stream x [rows][d] fp32: the stage input (non-first stages) and
+  // output (non-last stages)
+  float* x() { return x_; }
+  // KV cache of local layer l: [slot][Hl][slot_ctx][dh]
+  bf16* kc(int l) const { return kv_ + (size_t)l * 2 * kv_layer_elems(); }
+  bf16* vc(int l) const { return kc(l) + kv_layer_elems(); }
 
-  // prefill of the packed tokens through every layer; writes K/V into slots
+  // prefill of the packed tokens through this shard's layers; writes K/V into
+  // slots.  First stage: embeds eb.ids; otherwise x() holds the input rows.
   void encode(const EncodeBatch& eb);
-  // one decode iteration for B rows: next token ids -> last_tok[slot],
-  // out_tokens[out_off[i]]; logits left in logits() ([B][V] fp32)
+  // one decode iteration for B rows.  First stage embeds last_tok[slot];
+  // last stage: next ids -> last_tok[slot] and out_tokens[out_off[i]],
+  // logits left in logits() ([B][V] fp32).
   void decode(const DecodeBatch& db);
   const float* logits() const { return logits_; }
 
-  // single-layer timing helpers for XProfiler (one encoder / decoder layer)
-  void layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest);
-  void layer_decode(int l, const DecodeBatch& db, bool attn, bool rest);
-  void fill_tables_for_profile();
+  // single-layer helpers: XProfiler timing (part 0: attention and / or the
+  // rest of layer l) and the blocks a lockstep TP group drives (part 1: up
+  // to the attention output; part 2: the FFN)
+  void layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest, int part = 0);
+  void layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, int part = 0);
+
+  // stage pieces, for executors that drive several engines
+  void embed_encode(const EncodeBatch& eb);
+  void embed_decode(const DecodeBatch& db);
+  void head_decode(const DecodeBatch& db);
+  // layer l around its two TP reductions: attention block (LN1 .. O-proj),
+  // FFN block (LN2 .. FFN2).  tp > 1 without a reducer leaves the fp32
+  // partial in part() for the group to sum; finish_pending() then adds it
+  // and the bias to the residual.
+  void enc_attn_block(int l, const EncodeBatch& eb);
+  void enc_ffn_block(int l, const EncodeBatch& eb);
+  void dec_attn_block(int l, const DecodeBatch& db);
+  void dec_ffn_block(int l, const DecodeBatch& db);
+  void finish_pending();
+  float* part() { return part_; }
 
   int32_t* err_flag() { return err_; }
   size_t weight_bytes() const { return wbytes_; }
@@ -86,10 +137,18 @@ class Engine {
   void gen_weights();
   void linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   void linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
+  // residual update x += W.act + b: fused epilogue (tp = 1) or partial ->
+  // TP all-reduce -> add (tp > 1)
+  void resid_update(bool decode, const bf16* X, int64_t ldx, int tokens, const bf16* W, int K, const bf16* bias);
 
   Dims D;
+  EngineShard S_;
   int dev_;
+  bool own_stream_ = false;
   cudaStream_t st_ = nullptr;
+  Reducer* red_ = nullptr;
+  const bf16* pend_bias_ = nullptr;
+  int pend_rows_ = 0;
   uint8_t* wbuf_ = nullptr;
   size_t wbytes_ = 0;
   bf16 *tok_emb_ = nullptr, *pos_emb_ = nullptr, *lnf_g_ = nullptr, *lnf_b_ = nullptr;
@@ -97,6 +156,7 @@ class Engine {
   // workspace
   int cap_tokens_ = 0, cap_rows_ = 0;
   float* x_ = nullptr;
+  float* part_ = nullptr;        // TP partial sums [T][d]
   bf16 *h_ = nullptr, *qkv_ = nullptr, *ctx_ = nullptr, *ff_ = nullptr;
   float* logits_ = nullptr;
   float* splitk_ws_ = nullptr;
@@ -108,12 +168,11 @@ class Engine {
   bf16* kv_ = nullptr;
   int kv_slots_ = 0, slot_ctx_ = 0, kv_layers_ = 0;
   int32_t* last_tok_ = nullptr;
-  // profiler scratch tables
-  int32_t* prof_tables_ = nullptr;
 
-  bf16* kc(int l) const { return kv_ + (size_t)l * 2 * kv_layer_elems(); }
-  bf16* vc(int l) const { return kc(l) + kv_layer_elems(); }
-  size_t kv_layer_elems() const { return (size_t)kv_slots_ * D.H * slot_ctx_ * D.dh; }
+  size_t kv_layer_elems() const { return (size_t)kv_slots_ * D.Hl * slot_ctx_ * D.dh; }
 };
+
+// x[i][:] += p[i][:] + bias   (fp32 residual, bf16 bias), n = rows * d
+void add_bias_resid(float* x, const float* p, const bf16* bias, int rows, int d, cudaStream_t st);
 
 }  // namespace exg

@@ -15,30 +15,25 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t z) {
 }
 
 __global__ void weightgen_kernel(bf16* __restrict__ dst, int64_t rows, int64_t cols, int64_t ld, GenParams p) {
-  // blocked: iterate the zero-padded [rows_p][cols_p] and scatter to the
-  // blocked layout; else the plain row-major [rows][ld]
-  const int64_t rp = p.blocked ? (rows + 127) / 128 * 128 : rows;
-  const int64_t cp = p.blocked ? (cols + 63) / 64 * 64 : cols;
-  const int64_t n = rp * cp;
+  // blocked: scatter rows [dst_row0, dst_row0 + rows) of the blocked layout
+  // (padding is not written: the destination is zero-filled beforehand);
+  // else the plain row-major [rows][ld]
+  const int64_t n = rows * cols;
   const uint64_t key = p.seed ^ (p.tensor_id << 40);
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t r = e / cp, c = e % cp;
-    bf16 out = __float2bfloat16_rn(0.0f);
-    if (r < rows && c < cols) {
-      const int64_t i = p.transposed ? (c + p.col_off) * p.canon_cols + (r + p.row_off)
-                                     : (r + p.row_off) * p.canon_cols + (c + p.col_off);
-      const uint64_t h = splitmix64(key ^ (uint64_t)i);
-      const float u = __fmul_rn((float)(uint32_t)(h >> 40), 5.9604644775390625e-08f);  // * 2^-24, exact
-      const float cen = __fsub_rn(u, 0.5f);                                           // exact
-      const float v = p.gain ? __fadd_rn(1.0f, __fmul_rn(cen, p.c_gain)) : __fmul_rn(cen, p.c_mat);
-      out = __float2bfloat16_rn(v);
-    }
-    dst[p.blocked ? blocked_index(r, c, cols) : r * ld + c] = out;
+    const int64_t r = e / cols, c = e % cols;
+    const int64_t i = p.transposed ? (c + p.col_off) * p.canon_cols + (r + p.row_off)
+                                   : (r + p.row_off) * p.canon_cols + (c + p.col_off);
+    const uint64_t h = splitmix64(key ^ (uint64_t)i);
+    const float u = __fmul_rn((float)(uint32_t)(h >> 40), 5.9604644775390625e-08f);  // * 2^-24, exact
+    const float cen = __fsub_rn(u, 0.5f);                                           // exact
+    const float v = p.gain ? __fadd_rn(1.0f, __fmul_rn(cen, p.c_gain)) : __fmul_rn(cen, p.c_mat);
+    dst[p.blocked ? blocked_index(r + p.dst_row0, c, cols) : r * ld + c] = __float2bfloat16_rn(v);
   }
 }
 
 void weightgen(bf16* dst, int64_t rows, int64_t cols, int64_t ld, const GenParams& p, cudaStream_t st) {
-  const int64_t n = p.blocked ? blocked_elems(rows, cols) : rows * cols;
+  const int64_t n = rows * cols;
   if (n <= 0) return;
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
   weightgen_kernel<<<blocks, 256, 0, st>>>(dst, rows, cols, ld, p);

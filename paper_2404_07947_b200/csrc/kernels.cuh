@@ -21,7 +21,9 @@ struct GenParams {
   int transposed;
   int64_t canon_cols;
   int64_t row_off, col_off;
-  int blocked;         // 1: write the GEMM blocked layout (gemm_tc.cuh), zero padded
+  int blocked;         // 1: write the GEMM blocked layout (gemm_tc.cuh) of a matrix
+                       //    with `cols` columns (padding left as is: zero-fill first)
+  int64_t dst_row0;    // blocked: first destination row
 };
 void weightgen(bf16* dst, int64_t rows, int64_t cols, int64_t ld, const GenParams& p, cudaStream_t st);
 

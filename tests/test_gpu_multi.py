@@ -1,0 +1,112 @@
+"""Multi-GPU layouts of the method on one B200 (every GPU of a layout
+emulated by its own Engine holding exactly that GPU's weight shard and KV):
+
+* RRA over pipeline stages (PP) with P micro-batches;
+* partial tensor parallelism (TP all-reduce of fp32
+  partials in rank order, T4(i));
+* WAA: encoder GPU(s) / decoder GPU(s), KV handoff layer by
+  layer to the owning decoder stage and TP rank, rows merged at iteration
+  boundaries, decoder micro-batches.
+
+Parity bar: greedy ids equal to the oracle's
+bf16-emulating decode (near-ties reported with their margin), logits within
+2e-2; layouts without TP are bit-identical to the single-GPU run (same
+per-row arithmetic, bit-exact transfers)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def env():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2404_07947_b200 as X
+    from paper_2404_07947_b200 import _lib
+    from oracle import transformer as T
+    from workload import MODELS, config1_requests, weight_seed
+    spec = MODELS["tiny"]
+    seed = weight_seed(1)
+    reqs = config1_requests()
+    single = X.Context(spec, seed)
+    multi = X.Context(spec, seed, cluster=X.cluster_spec(8))
+    base_t, _, _, base_l = single.run(X.rra_schedule(4, 8, 6), reqs, dump=range(len(reqs)))
+    ora = T.greedy_kv(T.Weights(spec, seed), reqs, "bf16", record_logits=True)
+    return X, _lib, reqs, single, multi, base_t, base_l, ora
+
+
+def _check_vs_oracle(reqs, toks, logits, ora):
+    worst = 0.0
+    for r, q in enumerate(reqs):
+        for t in range(q.output_len):
+            if toks[r][t] != ora.tokens[r][t]:
+                assert ora.margins[r][t] <= 2 * TOL, "hard mismatch req %d step %d" % (r, t)
+                pytest.fail("near-tie divergence req %d step %d (margin %.3g)" % (r, t, ora.margins[r][t]))
+            worst = max(worst, float(np.abs(logits[r][t] - ora.logits[r][t]).max()))
+    assert worst <= TOL, worst
+
+
+PP_LAYOUTS = {
+    "pp2": [(0, 1, 0, 1), (1, 1, 1, 2)],
+}
+TP_LAYOUTS = {
+    "tp2_then_single": [(0, 2, 0, 1), (2, 1, 1, 2)],     # partial TP: c = 2 GPUs at the front, t = 2
+    "tp4": [(0, 4, 0, 2)],
+    "single_then_tp2": [(0, 1, 0, 1), (1, 2, 1, 2)],
+}
+
+
+@pytest.mark.parametrize("name", list(PP_LAYOUTS))
+def test_rra_pipeline_bit_identical_to_single_gpu(env, name):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    s = L.make_schedule(X.EXG_RRA, 4, 8, PP_LAYOUTS[name], n_d=6)
+    toks, lat, st, lg = multi.run(s, reqs, dump=range(len(reqs)))
+    assert toks == base_t
+    for r in range(len(reqs)):
+        assert np.array_equal(lg[r], base_l[r]), r
+    assert st["out_tokens"] == sum(q.output_len for q in reqs) and np.all(lat > 0)
+
+
+@pytest.mark.parametrize("name", list(TP_LAYOUTS))
+def test_rra_partial_tp_matches_oracle(env, name):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    s = L.make_schedule(X.EXG_RRA, 4, 8, TP_LAYOUTS[name], n_d=6, tp_degree=max(g[1] for g in TP_LAYOUTS[name]))
+    toks, lat, st, lg = multi.run(s, reqs, dump=range(len(reqs)))
+    _check_vs_oracle(reqs, toks, lg, ora)
+
+
+@pytest.mark.parametrize("b_e,b_d,b_m,n_enc,layout", [
+    (2, 8, 0, 1, [(0, 1, 0, 2), (1, 1, 0, 2)]),                     # 1 encoder GPU + 1 decoder GPU
+    (3, 8, 4, 1, [(0, 1, 0, 2), (1, 1, 0, 1), (2, 1, 1, 2)]),      # decoder pipeline, 2 micro-batches
+    (1, 5, 2, 2, [(0, 1, 0, 1), (1, 1, 1, 2), (2, 1, 0, 2)]),      # encoder pipeline of 2
+])
+def test_waa_bit_identical_to_single_gpu(env, b_e, b_d, b_m, n_enc, layout):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    s = L.make_schedule(X.EXG_WAA_C, b_e, b_d, layout, b_m=b_m, n_enc_gpus=n_enc)
+    toks, lat, st, lg = multi.run(s, reqs, dump=range(len(reqs)))
+    assert toks == base_t
+    for r in range(len(reqs)):
+        assert np.array_equal(lg[r], base_l[r]), r
+
+
+def test_waa_with_decoder_tp_matches_oracle(env):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    layout = [(0, 1, 0, 2), (1, 2, 0, 1), (3, 1, 1, 2)]   # enc GPU 0; dec: TP-2 stage + single stage
+    s = L.make_schedule(X.EXG_WAA_C, 2, 8, layout, b_m=4, n_enc_gpus=1, tp_degree=2, tp_gpus=2)
+    toks, lat, st, lg = multi.run(s, reqs, dump=range(len(reqs)))
+    _check_vs_oracle(reqs, toks, lg, ora)
+
+
+def test_layout_validation(env):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    bad = L.make_schedule(X.EXG_RRA, 4, 8, [(0, 1, 0, 1)], n_d=6)          # misses layer 1
+    with pytest.raises(X.ExgError) as ei:
+        multi.run(bad, reqs)
+    assert ei.value.status == 1
+    too_many = L.make_schedule(X.EXG_RRA, 4, 8, [(0, 8, 0, 1), (8, 1, 1, 2)], n_d=6)
+    with pytest.raises(X.ExgError):
+        multi.run(too_many, reqs)
