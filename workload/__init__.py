@@ -69,6 +69,10 @@ MODELS = {
     "gpt3-175b": ModelSpec("gpt3-175b", "gpt3", 0, 96, 12288, 96, 128, 49152, 50257, 2048),
     # PAPER.md:415 (T5 11B: 48 layers = 24 enc + 24 dec, hidden 1024, 128 heads)
     "t5-11b": ModelSpec("t5-11b", "t5", 24, 24, 1024, 128, 128, 65536, 32128, 2048),
+    # encoder-decoder parity cases (T5 architecture at config-1 scale; the
+    # dh=128 one exercises the tensor-core attention paths)
+    "tiny-t5": ModelSpec("tiny-t5", "t5", 2, 2, 64, 4, 16, 256, 512, 64),
+    "small-t5": ModelSpec("small-t5", "t5", 2, 2, 256, 2, 128, 512, 512, 256),
 }
 
 
