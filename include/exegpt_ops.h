@@ -58,7 +58,14 @@ exg_status exg_op_linear(const void* X, int64_t ldx, const void* Wb, int32_t tok
 exg_status exg_op_layernorm(void* y, int64_t ldy, const float* x, int64_t ldx, const void* g, const void* b, int32_t T,
                             int32_t d, float eps, void* stream);
 
-/* K1 -- x fp32 [T][d] = tok_emb[ids[t]] + pos_emb[pos[t]] (bf16 tables). */
+/* T5 RMSNorm (SURVEY.md §8(c) T1 T5 reading): y bf16 [T][d] =
+ * bf16(x rsqrt(mean_j x^2 + eps) g out_scale), fp32 statistics.  out_scale
+ * folds the tied LM head's d^-1/2 into the final norm. */
+exg_status exg_op_rmsnorm(void* y, int64_t ldy, const float* x, int64_t ldx, const void* g, int32_t T, int32_t d,
+                          float eps, float out_scale, void* stream);
+
+/* K1 -- x fp32 [T][d] = tok_emb[ids[t]] + pos_emb[pos[t]] (bf16 tables;
+ * pos_emb NULL: no position term, T5). */
 exg_status exg_op_embed(float* x, const int32_t* ids, const int32_t* pos, const void* tok_emb, const void* pos_emb,
                         int32_t T, int32_t d, void* stream);
 
@@ -71,22 +78,28 @@ exg_status exg_op_kv_scatter(void* kc, void* vc, const void* qkv, const int32_t*
  * out[i][h] = bf16( softmax_j( fp32(q_i,h . K[slot_i][h][j]) * scale ) . V )
  * over j < n_keys[i].  q: bf16 rows of stride ldq (head h at h*dh); out:
  * bf16 [B][ldo].  Keys are split in fixed chunks of split_len; partial: fp32
- * [B][H][max_splits][dh+2] scratch when max_splits > 1. */
+ * [B][H][max_splits][dh+2] scratch when max_splits > 1.  bias (may be NULL):
+ * fp32 additive score bias, key j of row i / head h gets
+ * bias[h*bias_ld + bias_off + j - (n_keys[i]-1)] after the scale (T5 relative
+ * position bias; the query is the newest key). */
 exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, const void* vc, const int32_t* slot,
                                    const int32_t* n_keys, void* out, int64_t ldo, int32_t B, int32_t H, int32_t dh,
                                    int32_t max_ctx, float scale, int32_t split_len, int32_t max_splits, float* partial,
-                                   void* stream);
+                                   const float* bias, int32_t bias_ld, int32_t bias_off, void* stream);
 
 /* K4 -- causal prefill attention over packed requests (cu_seqlens [R+1],
  * T = cu_seqlens[R] tokens, q rows [T][ldq]); request r's tokens sit at
  * positions pos0[r].. of slot[r] and attend to cached keys 0..own position
  * (keys scattered beforehand); cache [n_slots][H][max_ctx][dh].  dh = 128
  * runs on tcgen05 (S and O in TMEM, P rounded to bf16 for P.V); other head
- * dims on a SIMT kernel with fp32 P. */
+ * dims on a SIMT kernel with fp32 P.  causal = 0: every query sees all keys
+ * of its request (T5 encoder).  bias (may be NULL): score(q, k) +=
+ * bias[h*bias_ld + bias_off + kpos - qpos] after the scale. */
 exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, const void* vc,
                                     const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0, int32_t R,
                                     int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh, int32_t max_ctx,
-                                    int32_t n_slots, int32_t T, float scale, void* stream);
+                                    int32_t n_slots, int32_t T, float scale, int32_t causal, const float* bias,
+                                    int32_t bias_ld, int32_t bias_off, void* stream);
 
 /* K8 -- out[i] = argmax_v logits[i][v] (fp32 [B][ld]), lowest index on ties;
  * *err_flag (device int32, may be NULL) set to 1 on a NaN. */

@@ -26,7 +26,10 @@ W_o_x [inner][d]; slot 0: tok_emb, lnf_g (decoder final norm), lnx_g
 Modes as in transformer.py: (i) fp64 naive recompute, (ii) fp64 KV loop,
 (iii) bf16-emulating KV loop (T4 rounding points; RMS output bf16, q/k/v and
 cross K/V bf16, scores fp32(q.k) + fp32 bias, ctx bf16, FFN1 relu fp32 -> bf16,
-residual fp32, logits fp32(h E^T) * 2^-k exact).
+residual fp32, logits fp32(bf16(RMS_f(x) d^-1/2) E^T): the head scale is
+applied to the normed state before its bf16 rounding -- a reading; equal to
+scaling the logits whenever d^-1/2 is a power of two, as for every T5 shape
+here (d = 64, 256, 1024)).
 
 Pins: (i) vs HuggingFace T5ForConditionalGeneration (fp64, same weights);
 (i) == (ii); bucket table vs the published bucket rule on hand cases.
@@ -221,8 +224,8 @@ def greedy_kv(W: T5Weights, requests, mode: str = "bf16", record_logits: bool = 
                 h = R.bf16(rms(x, L["ln2_g"]))
                 f = R.bf16(np.maximum(R.f32(h @ L["W_1"]), 0.0))
                 x = R.f32(x + R.f32(f @ L["W_2"]))
-            hf = R.bf16(rms(x, W.lnf_g))
-            lg = R.f32(R.f32(hf @ W.tok_emb.T) * head_scale)[0]
+            hf = R.bf16(rms(x, W.lnf_g) * head_scale)
+            lg = R.f32(hf @ W.tok_emb.T)[0]
             y = argmax_first(lg)
             out.append(y)
             mg_r.append(top2_margin(lg))

@@ -136,13 +136,15 @@ _SIGS = {
     "exg_op_linear": (C.c_int, [_P, C.c_int64, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                 C.c_int32, _P, _P, C.c_int64, _P, C.c_int64, C.c_int32, _P, C.c_int64, _P]),
     "exg_op_layernorm": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, _P, C.c_int32, C.c_int32, C.c_float, _P]),
+"exg_op_rmsnorm": (C.c_int, [_P, C.c_int64, _P, C.c_int64, _P, C.c_int32, C.c_int32, C.c_float, C.c_float, _P]),
     "exg_op_embed": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, _P]),
     "exg_op_kv_scatter": (C.c_int, [_P, _P, _P, _P, _P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, _P]),
     "exg_op_decode_attention": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int64, C.c_int32, C.c_int32,
-                                          C.c_int32, C.c_int32, C.c_float, C.c_int32, C.c_int32, _P, _P]),
+                                          C.c_int32, C.c_int32, C.c_float, C.c_int32, C.c_int32, _P,
+                                          _P, C.c_int32, C.c_int32, _P]),
     "exg_op_prefill_attention": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, C.c_int32, _P,
                                            C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
-                                           C.c_float, _P]),
+                                           C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, _P]),
     "exg_op_argmax": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P]),
     "exg_op_decode_workspace": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
 }

@@ -49,6 +49,9 @@ struct FmhaParams {
   float scale;
   bf16* out;
   int64_t ldo;
+  int causal;
+  const float* bias;    // T5 relative bias: score += bias[h * bias_ld + bias_off + kpos - qpos]
+  int bias_ld, bias_off;
 };
 
 __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_constant__ CUtensorMap tmQ,
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
   const int qb = blockIdx.x * FQ;
   if (qb >= len) return;
   const int pos0 = p.pos0[r_req];
-  const int last_key = pos0 + min(len, qb + FQ) - 1;  // inclusive
+  const int last_key = p.causal ? pos0 + min(len, qb + FQ) - 1 : pos0 + len - 1;  // inclusive
   const int ntiles = last_key / FK + 1;
   const int64_t kv_row0 = ((int64_t)p.slot[r_req] * p.H + h) * p.max_ctx;
 
@@ -168,6 +171,8 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
     const int q = warp - 4;
     const int r = q * 32 + lane;                    // query row of the tile = TMEM lane
     const int qpos = pos0 + qb + r;                  // absolute position of this query
+    const int kmax = p.causal ? qpos : pos0 + len - 1;  // last key this query sees
+    const float* brow = (p.bias && qb + r < len) ? p.bias + (int64_t)h * p.bias_ld + p.bias_off - qpos : nullptr;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     float o[FD];
 #pragma unroll
@@ -187,7 +192,8 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
             const int kpos = j * FK + c + e;
-            const float sc = (kpos <= qpos) ? v[e] * p.scale : -INFINITY;
+            float sc = (kpos <= kmax) ? __fmul_rn(v[e], p.scale) : -INFINITY;
+            if (brow && kpos <= kmax) sc = __fadd_rn(sc, brow[kpos]);
             mx = fmaxf(mx, sc);
           }
         }
@@ -203,10 +209,15 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
 #pragma unroll
           for (int e = 0; e < 16; e += 2) {
             const int kpos = j * FK + c + e;
-            const float p0 = (kpos <= qpos && m_new != -INFINITY)
-                                 ? exp2f((v[e] * p.scale - m_new) * 1.4426950408889634f) : 0.f;
-            const float p1 = (kpos + 1 <= qpos && m_new != -INFINITY)
-                                 ? exp2f((v[e + 1] * p.scale - m_new) * 1.4426950408889634f) : 0.f;
+            float s0 = __fmul_rn(v[e], p.scale), s1 = __fmul_rn(v[e + 1], p.scale);
+            if (brow) {
+              if (kpos <= kmax) s0 = __fadd_rn(s0, brow[kpos]);
+              if (kpos + 1 <= kmax) s1 = __fadd_rn(s1, brow[kpos + 1]);
+            }
+            const float p0 = (kpos <= kmax && m_new != -INFINITY)
+                                 ? exp2f((s0 - m_new) * 1.4426950408889634f) : 0.f;
+            const float p1 = (kpos + 1 <= kmax && m_new != -INFINITY)
+                                 ? exp2f((s1 - m_new) * 1.4426950408889634f) : 0.f;
             __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
             sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
             pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
@@ -293,7 +304,7 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   // zero-filled by TMA and never stored); K/V: the cache viewed as
   // [kv_rows = slots*H*max_ctx][dh]
   FmhaParams p{a.cu_seqlens, a.slot, a.pos0, a.H, a.max_ctx,
-               a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo};
+               a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo, a.causal, a.bias, a.bias_ld, a.bias_off};
   const CUtensorMap tq = make_tmap_bf16(a.q, a.q_rows, a.ldq, a.ldq, 128);
   const CUtensorMap tk = make_tmap_bf16(a.kc, a.kv_rows, FD, FD, 128);
   const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 128);

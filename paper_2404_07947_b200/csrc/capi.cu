@@ -266,6 +266,8 @@ exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* r
     if (n < 1) throw std::invalid_argument("empty request batch");
     EXG_CUDA(cudaSetDevice(ctx->device));
     if (ctx->multi) {
+      if (ctx->spec.arch == EXG_ARCH_T5)
+        return fail(EXG_E_INFEASIBLE, "encoder-decoder models: multi-GPU layouts are not built yet");
       int gpus = 0;
       for (int k = 0; k < sched->n_stages && k < EXG_MAX_STAGES; ++k) gpus += sched->stage_n_gpus[k];
       if (gpus > ctx->cluster.n_gpus) return fail(EXG_E_INFEASIBLE, "schedule needs more GPUs than the cluster has");
@@ -339,6 +341,14 @@ exg_status exg_op_layernorm(void* y, int64_t ldy, const float* x, int64_t ldx, c
   });
 }
 
+exg_status exg_op_rmsnorm(void* y, int64_t ldy, const float* x, int64_t ldx, const void* g, int32_t T, int32_t d,
+                          float eps, float out_scale, void* stream) {
+  return guarded([&] {
+    exg::rmsnorm((exg::bf16*)y, ldy, x, ldx, (const exg::bf16*)g, T, d, eps, out_scale, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
 exg_status exg_op_embed(float* x, const int32_t* ids, const int32_t* pos, const void* tok_emb, const void* pos_emb,
                         int32_t T, int32_t d, void* stream) {
   return guarded([&] {
@@ -359,7 +369,7 @@ exg_status exg_op_kv_scatter(void* kc, void* vc, const void* qkv, const int32_t*
 exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, const void* vc, const int32_t* slot,
                                    const int32_t* n_keys, void* out, int64_t ldo, int32_t B, int32_t H, int32_t dh,
                                    int32_t max_ctx, float scale, int32_t split_len, int32_t max_splits, float* partial,
-                                   void* stream) {
+                                   const float* bias, int32_t bias_ld, int32_t bias_off, void* stream) {
   return guarded([&] {
     if (max_splits > 1 && !partial) throw std::invalid_argument("max_splits > 1 needs a partial buffer");
     exg::DecodeAttnArgs a;
@@ -379,6 +389,9 @@ exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, c
     a.split_len = split_len;
     a.max_splits = max_splits;
     a.partial = partial;
+    a.bias = bias;
+    a.bias_ld = bias_ld;
+    a.bias_off = bias_off;
     exg::decode_attention(a, (cudaStream_t)stream);
     return EXG_OK;
   });
@@ -387,11 +400,12 @@ exg_status exg_op_decode_attention(const void* q, int64_t ldq, const void* kc, c
 exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, const void* vc,
                                     const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0, int32_t R,
                                     int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh, int32_t max_ctx,
-                                    int32_t n_slots, int32_t T, float scale, void* stream) {
+                                    int32_t n_slots, int32_t T, float scale, int32_t causal, const float* bias,
+                                    int32_t bias_ld, int32_t bias_off, void* stream) {
   return guarded([&] {
     exg::PrefillAttnArgs a{(const exg::bf16*)q, ldq, (const exg::bf16*)kc, (const exg::bf16*)vc, cu_seqlens, slot,
                            pos0, R, max_len, (exg::bf16*)out, ldo, H, dh, max_ctx, scale, (int64_t)T,
-                           (int64_t)n_slots * H * max_ctx};
+                           (int64_t)n_slots * H * max_ctx, causal, bias, bias_ld, bias_off};
     exg::prefill_attention(a, (cudaStream_t)stream);
     return EXG_OK;
   });

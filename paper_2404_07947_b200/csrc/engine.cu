@@ -25,8 +25,29 @@ namespace exg {
 namespace {
 enum Kind {
   K_TOK = 0, K_POS = 1, K_LN1G = 2, K_LN1B = 3, K_WQKV = 4, K_BQKV = 5, K_WO = 6, K_BO = 7, K_LN2G = 8,
-  K_LN2B = 9, K_W1 = 10, K_B1 = 11, K_W2 = 12, K_B2 = 13, K_LNFG = 14, K_LNFB = 15
+  K_LN2B = 9, K_W1 = 10, K_B1 = 11, K_W2 = 12, K_B2 = 13, K_LNFG = 14, K_LNFB = 15,
+  K_RELB = 16, K_WQX = 17, K_WKVX = 18, K_WOX = 19, K_LNXG = 20
 };
+constexpr int T5_BUCKETS = 32, T5_MAX_DIST = 128;
+constexpr float T5_EPS = 1e-6f;
+
+// T5 relative position bucket of rel = key_pos - query_pos (double-precision
+// log, truncation)
+int t5_bucket(int rel, bool bidirectional) {
+  int ret = 0, n = T5_BUCKETS;
+  if (bidirectional) {
+    n /= 2;
+    if (rel > 0) ret += n;
+    rel = std::abs(rel);
+  } else {
+    rel = -std::min(rel, 0);
+  }
+  const int max_exact = n / 2;
+  if (rel < max_exact) return ret + rel;
+  const int large = max_exact + (int)(std::log((double)rel / max_exact) / std::log((double)T5_MAX_DIST / max_exact) *
+                                      (n - max_exact));
+  return ret + std::min(large, n - 1);
+}
 inline uint64_t tid_of(int slot, int kind) { return (uint64_t)slot * 64 + kind; }
 
 __global__ void embed_decode_kernel(float* __restrict__ x, const int32_t* __restrict__ last_tok,
@@ -35,9 +56,11 @@ __global__ void embed_decode_kernel(float* __restrict__ x, const int32_t* __rest
   griddep_launch_dependents();
   const int i = blockIdx.x;
   const int64_t id = last_tok[slot[i]];
-  const bf16* b = pe + (int64_t)pos[i] * d;
-  for (int j = threadIdx.x; j < d; j += blockDim.x)
-    x[(int64_t)i * d + j] = __fadd_rn(bf2f(tok[blocked_index(id, j, d)]), bf2f(b[j]));
+  const bf16* b = pe ? pe + (int64_t)pos[i] * d : nullptr;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const float e = bf2f(tok[blocked_index(id, j, d)]);
+    x[(int64_t)i * d + j] = b ? __fadd_rn(e, bf2f(b[j])) : e;
+  }
 }
 
 // argmax over a logits row, lowest index on ties, result scattered to the
@@ -87,7 +110,7 @@ __global__ void add_bias_resid_kernel(float* __restrict__ x, const float* __rest
                                       const bf16* __restrict__ bias, int64_t n, int d) {
   griddep_launch_dependents();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    x[i] = x[i] + (p[i] + bf2f(bias[i % d]));
+    x[i] = x[i] + (bias ? p[i] + bf2f(bias[i % d]) : p[i]);
 }
 
 template <typename T>
@@ -107,7 +130,14 @@ void add_bias_resid(float* x, const float* p, const bf16* bias, int rows, int d,
 
 Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cudaStream_t stream)
     : S_(shard), dev_(device) {
-  if (s.arch == EXG_ARCH_T5 || s.n_enc_layers != 0) throw std::invalid_argument("encoder-decoder models: not built yet");
+  t5_ = s.arch == EXG_ARCH_T5;
+  if (t5_) {
+    if (s.n_enc_layers != s.n_dec_layers) throw std::invalid_argument("T5: n_enc_layers must equal n_dec_layers");
+    if (shard.tp != 1 || shard.l0 != 0 || (shard.l1 >= 0 && shard.l1 != s.n_dec_layers) || !shard.embed || !shard.head)
+      throw std::invalid_argument("T5: sharded layouts are not built yet (single-GPU engine only)");
+  } else if (s.n_enc_layers != 0) {
+    throw std::invalid_argument("decoder-only architectures have no encoder layers");
+  }
   D.arch = s.arch;
   D.L = s.n_dec_layers;
   D.d = s.d_model;
@@ -118,7 +148,7 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
   D.V = s.vocab;
   D.max_pos = s.max_pos;
   D.seed = s.weight_seed;
-  D.act = s.arch == EXG_ARCH_OPT ? ACT_RELU : ACT_GELU;
+  D.act = (s.arch == EXG_ARCH_OPT || t5_) ? ACT_RELU : ACT_GELU;
   if (S_.l1 < 0) S_.l1 = D.L;
   if (S_.l0 < 0 || S_.l1 > D.L || S_.l0 >= S_.l1) throw std::invalid_argument("bad shard layer range");
   if (S_.tp < 1 || D.H % S_.tp || D.ff % S_.tp || S_.tp_rank < 0 || S_.tp_rank >= S_.tp)
@@ -138,13 +168,17 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
   }
   EXG_CUDA(cudaMalloc(&err_, sizeof(int32_t)));
   EXG_CUDA(cudaMemsetAsync(err_, 0, sizeof(int32_t), st_));
-  gen_weights();
+  if (t5_)
+    gen_weights_t5();
+  else
+    gen_weights();
 }
 
 Engine::~Engine() {
   cudaSetDevice(dev_);
   cudaStreamSynchronize(st_);
-  for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)last_tok_, (void*)err_})
+  for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)xkv_, (void*)last_tok_, (void*)err_,
+                  (void*)enc_bias_})
     if (p) cudaFree(p);
   for (cudaEvent_t e : kev_) cudaEventDestroy(e);
   if (own_stream_ && st_) cudaStreamDestroy(st_);
@@ -219,6 +253,87 @@ void Engine::gen_weights() {
   EXG_CUDA(cudaStreamSynchronize(st_));
 }
 
+// T5: no biases, RMS gains, relative-bias tables at
+// the first encoder / decoder layer slots, encoder final norm = (slot 0, lnx_g)
+void Engine::gen_weights_t5() {
+  const size_t d = D.d, in = D.inner, f = D.ff;
+  auto al = [](size_t n) { return (n * 2 + 255) & ~size_t(255); };
+  auto bl = [&](size_t rows, size_t K) { return al((size_t)blocked_elems(rows, K)); };
+  const size_t enc_layer = al(d) * 2 + bl(3 * in, d) + bl(d, in) + bl(f, d) + bl(d, f);
+  const size_t dec_layer = enc_layer + al(d) + bl(in, d) + bl(2 * in, d) + bl(d, in);
+  wbytes_ = bl(D.V, d) + 2 * al(d) + 2 * al((size_t)T5_BUCKETS * D.H) + D.L * (enc_layer + dec_layer);
+  EXG_CUDA(cudaMalloc(&wbuf_, wbytes_));
+  EXG_CUDA(cudaMemsetAsync(wbuf_, 0, wbytes_, st_));
+  uint8_t* p = wbuf_;
+  const float c_mat = (float)(2.0 * std::sqrt(3.0) * 0.02);
+  const float c_gain = 0.2f;
+  auto gen = [&](bf16* dst, int64_t rows, int64_t cols, int slot, int kind, int gain, int transposed,
+                 int64_t canon_cols, int blocked = 0, int64_t row_off = 0, int64_t col_off = 0,
+                 int64_t dst_row0 = 0) {
+    GenParams g{D.seed, tid_of(slot, kind), gain, c_mat, c_gain, transposed, canon_cols, row_off, col_off, blocked,
+                dst_row0};
+    weightgen(dst, rows, cols, cols, g, st_);
+  };
+  auto carve_blk = [&](size_t rows, size_t K) { return carve<bf16>(p, (size_t)blocked_elems(rows, K)); };
+  auto vec = [&](int slot, int kind, int gain) {
+    bf16* v = carve<bf16>(p, d);
+    gen(v, 1, d, slot, kind, gain, 0, d);
+    return v;
+  };
+  // W^T [out][in] blocked from the canonical W[in][out] (columns col0.. of it)
+  auto mat = [&](int slot, int kind, int64_t out, int64_t K, int64_t canon_cols, int64_t col0 = 0) {
+    bf16* m = carve_blk(out, K);
+    gen(m, out, K, slot, kind, 0, 1, canon_cols, 1, col0, 0);
+    return m;
+  };
+  tok_emb_ = carve_blk(D.V, d);
+  gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d, 1);
+  lnf_g_ = vec(0, K_LNFG, 1);
+  enc_lnf_g_ = vec(0, K_LNXG, 1);
+  enc_rel_ = carve<bf16>(p, (size_t)T5_BUCKETS * D.H);
+  gen(enc_rel_, T5_BUCKETS, D.H, 1, K_RELB, 0, 0, D.H);
+  dec_rel_ = carve<bf16>(p, (size_t)T5_BUCKETS * D.H);
+  gen(dec_rel_, T5_BUCKETS, D.H, 1001, K_RELB, 0, 0, D.H);
+  enc_layers_.resize(D.L);
+  layers_.resize(D.L);
+  for (int side = 0; side < 2; ++side) {
+    for (int l = 0; l < D.L; ++l) {
+      const int s = side ? 1001 + l : 1 + l;
+      LayerW& w = side ? layers_[l] : enc_layers_[l];
+      w.ln1_g = vec(s, K_LN1G, 1);
+      w.ln2_g = vec(s, K_LN2G, 1);
+      w.Wqkv = mat(s, K_WQKV, 3 * in, d, 3 * in);
+      w.Wo = mat(s, K_WO, d, in, d);
+      w.W1 = mat(s, K_W1, f, d, f);
+      w.W2 = mat(s, K_W2, d, f, d);
+      if (side) {
+        w.lnx_g = vec(s, K_LNXG, 1);
+        w.Wqx = mat(s, K_WQX, in, d, in);
+        w.Wkvx = mat(s, K_WKVX, 2 * in, d, 2 * in);
+        w.Wox = mat(s, K_WOX, d, in, d);
+      }
+    }
+  }
+  // fp32 bias tables over every signed distance -(P-1) .. P-1
+  const int P = D.max_pos;
+  bias_ld_ = 2 * P - 1;
+  bias_off_ = P - 1;
+  std::vector<int32_t> bk(2 * (size_t)bias_ld_);
+  for (int j = 0; j < bias_ld_; ++j) {
+    bk[j] = t5_bucket(j - bias_off_, true);
+    bk[bias_ld_ + j] = t5_bucket(j - bias_off_, false);
+  }
+  int32_t* dbk = nullptr;
+  EXG_CUDA(cudaMalloc(&enc_bias_, sizeof(float) * 2 * (size_t)D.Hl * bias_ld_));
+  dec_bias_ = enc_bias_ + (size_t)D.Hl * bias_ld_;
+  EXG_CUDA(cudaMalloc(&dbk, sizeof(int32_t) * bk.size()));
+  EXG_CUDA(cudaMemcpyAsync(dbk, bk.data(), sizeof(int32_t) * bk.size(), cudaMemcpyHostToDevice, st_));
+  rel_bias_table(enc_bias_, enc_rel_, dbk, bias_ld_, D.Hl, D.H, 0, st_);
+  rel_bias_table(dec_bias_, dec_rel_, dbk + bias_ld_, bias_ld_, D.Hl, D.H, 0, st_);
+  EXG_CUDA(cudaStreamSynchronize(st_));
+  EXG_CUDA(cudaFree(dbk));
+}
+
 void Engine::ensure_workspace(int max_tokens, int max_rows) {
   max_tokens = std::max(max_tokens, max_rows);
   if (max_tokens <= cap_tokens_ && max_rows <= cap_rows_) return;
@@ -229,6 +344,7 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   const size_t T = cap_tokens_, R = cap_rows_;
   size_t sk = 0;
   for (auto fk : {std::make_pair(3 * D.inner_l, D.d), std::make_pair(D.d, D.inner_l), std::make_pair(D.ffl, D.d),
+                  std::make_pair(D.inner_l, D.d),
                   std::make_pair(D.d, D.ffl), std::make_pair(D.V, D.d)})
     sk = std::max(sk, decode_ws_floats(fk.first, fk.second, (int)R));
   splitk_cap_ = sk;
@@ -254,27 +370,37 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   EXG_CUDA(cudaMemsetAsync(x_, 0, bytes, st_));
 }
 
-void Engine::ensure_kv(int slots, int slot_ctx, int layers) {
-  if (slot_ctx > D.max_pos) throw std::invalid_argument("slot_ctx exceeds max_pos");
+void Engine::ensure_kv(int slots, int slot_ctx, int layers, int xctx) {
+  if (slot_ctx > D.max_pos || xctx > D.max_pos) throw std::invalid_argument("slot_ctx exceeds max_pos");
+  if (t5_ && xctx < 1) throw std::invalid_argument("encoder-decoder model: cross-attention context xctx must be >= 1");
+  if (!t5_) xctx = 0;
   if (layers < 0) layers = n_layers();
-  if (slots <= kv_slots_ && slot_ctx == slot_ctx_ && layers <= kv_layers_) return;
+  if (slots <= kv_slots_ && slot_ctx == slot_ctx_ && layers <= kv_layers_ && xctx == xctx_) return;
   EXG_CUDA(cudaStreamSynchronize(st_));
   if (kv_) EXG_CUDA(cudaFree(kv_));
+  if (xkv_) EXG_CUDA(cudaFree(xkv_));
   if (last_tok_) EXG_CUDA(cudaFree(last_tok_));
   kv_ = nullptr;
+  xkv_ = nullptr;
   last_tok_ = nullptr;
   kv_slots_ = std::max(slots, 1);
   slot_ctx_ = slot_ctx;
+  xctx_ = xctx;
   kv_layers_ = layers;
   const size_t bytes = (size_t)layers * 2 * kv_layer_elems() * sizeof(bf16);
+  const size_t xbytes = (size_t)layers * 2 * xkv_layer_elems() * sizeof(bf16);
   cudaError_t e = cudaMalloc(&kv_, bytes);
+  if (e == cudaSuccess && xbytes) e = cudaMalloc(&xkv_, xbytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
+    if (kv_) cudaFree(kv_);
+    kv_ = nullptr;
     kv_slots_ = 0;
     kv_layers_ = 0;
     throw std::bad_alloc();
   }
   EXG_CUDA(cudaMemsetAsync(kv_, 0, bytes, st_));
+  if (xbytes) EXG_CUDA(cudaMemsetAsync(xkv_, 0, xbytes, st_));
   EXG_CUDA(cudaMalloc(&last_tok_, sizeof(int32_t) * kv_slots_));
   EXG_CUDA(cudaMemsetAsync(last_tok_, 0, sizeof(int32_t) * kv_slots_, st_));
 }
@@ -415,6 +541,11 @@ void Engine::dec_ffn_block(int l, const DecodeBatch& db) { layer_decode(l, db, f
 // part 1: LN1, QKV, KV scatter, attention (up to, excluding, the O-proj);
 // part 2: LN2, FFN1, FFN2 (after the attention residual update).
 void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest, int part) {
+  if (t5_) {
+    if (part != 0) throw std::logic_error("T5: no TP blocks");
+    enc_layer_t5(l, eb, attn, rest);
+    return;
+  }
   const LayerW& w = layers_[l];
   const int T = eb.T, d = D.d, il = D.inner_l;
   const float scale = (float)(1.0 / std::sqrt((double)D.dh));
@@ -454,12 +585,21 @@ void Engine::embed_encode(const EncodeBatch& eb) {
 
 void Engine::encode(const EncodeBatch& eb) {
   if (eb.T <= 0) return;
+  if (t5_) {
+    encode_t5(eb);
+    return;
+  }
   if (S_.tp > 1 && !red_) throw std::logic_error("TP shard without a reducer: drive it through a TP group");
   embed_encode(eb);
   for (int l = 0; l < n_layers(); ++l) layer_encode(l, eb, true, true);
 }
 
 void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, int part) {
+  if (t5_) {
+    if (part != 0) throw std::logic_error("T5: no TP blocks");
+    dec_layer_t5(l, db, attn, rest);
+    return;
+  }
   const LayerW& w = layers_[l];
   const int B = db.B, d = D.d, il = D.inner_l;
   const float scale = (float)(1.0 / std::sqrt((double)D.dh));
@@ -510,6 +650,7 @@ void Engine::embed_decode(const DecodeBatch& db) {
   const int B = db.B;
   if (B > cap_rows_) throw std::invalid_argument("decode batch exceeds workspace");
   if (S_.embed && B > 0) {
+    // T5: no position embedding (pos_emb_ null)
     embed_decode_kernel<<<B, 256, 0, st_>>>(x_, last_tok_, db.slot, db.pos, tok_emb_, pos_emb_, D.d);
     EXG_CHECK_LAUNCH();
   }
@@ -526,7 +667,10 @@ void Engine::decode(const DecodeBatch& db) {
 void Engine::head_decode(const DecodeBatch& db) {
   const int B = db.B;
   if (S_.head && B > 0) {
-    layernorm(h_, D.d, x_, D.d, lnf_g_, lnf_b_, B, D.d, 1e-5f, st_);
+    if (t5_)  // tied head of T5: logits = (RMS_f(x) d^-1/2) E^T (the scale folded into the norm output)
+      rmsnorm(h_, D.d, x_, D.d, lnf_g_, B, D.d, T5_EPS, (float)(1.0 / std::sqrt((double)D.d)), st_);
+    else
+      layernorm(h_, D.d, x_, D.d, lnf_g_, lnf_b_, B, D.d, 1e-5f, st_);
     EpiParams e;
     e.mode = EPI_F32;
     e.out_f32 = logits_;
@@ -534,6 +678,109 @@ void Engine::head_decode(const DecodeBatch& db) {
     linear_dec(h_, D.d, B, tok_emb_, D.V, D.d, e);
     argmax_scatter_kernel<<<B, 256, 0, st_>>>(logits_, D.V, db.slot, db.out_off, last_tok_, db.out_tokens, err_);
     EXG_CHECK_LAUNCH();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// T5 encoder-decoder (SURVEY.md §8(c) T1 T5 reading; oracle/t5.py)
+//   encoder layer:  h = bf16(RMS(x)); qkv; bidirectional attention + relative
+//                   bias (scale 1); x += ctx W_o; h = bf16(RMS(x));
+//                   x += bf16(relu(h W_1)) W_2
+//   encode phase:   encoder over all n input tokens, e = bf16(RMS_enc(x)),
+//                   cross K/V of every decoder layer = bf16(e W_kv_x) -> xkv
+//   decoder layer:  self-attention (causal relative bias) over the decoder
+//                   KV, cross-attention over xkv, ReLU FFN; no biases.
+// The encoder's own K/V are staged in decoder layer 0's cross cache at the
+// request's slot; the cross K/V projection of layer 0 overwrites them.
+// ---------------------------------------------------------------------------
+void Engine::enc_layer_t5(int l, const EncodeBatch& eb, bool attn, bool rest) {
+  const LayerW& w = enc_layers_[l];
+  const int T = eb.T, d = D.d, il = D.inner_l;
+  if (rest) {
+    rmsnorm(h_, d, x_, d, w.ln1_g, T, d, T5_EPS, 1.f, st_);
+    linear_pre(h_, d, T, w.Wqkv, 3 * il, d, epi_bf16(nullptr, qkv_, 3 * il));
+    kv_scatter(xkc(0), xvc(0), qkv_, eb.tslot, eb.pos, T, D.Hl, D.dh, xctx_, st_);
+  }
+  if (attn) {
+    PrefillAttnArgs pa{qkv_, 3 * il, xkc(0), xvc(0), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,
+                       ctx_, il, D.Hl, D.dh, xctx_, 1.0f,
+                       (int64_t)eb.T, (int64_t)kv_slots_ * D.Hl * xctx_, 0, enc_bias_, bias_ld_, bias_off_};
+    const int k = kbegin();
+    prefill_attention(pa, st_);
+    kend(k, EXG_K_PREFILL_ATTN, 4.0 * D.Hl * D.dh * eb.attn_pairs);
+  }
+  if (rest) {
+    resid_update(false, ctx_, il, T, w.Wo, il, nullptr);
+    rmsnorm(h_, d, x_, d, w.ln2_g, T, d, T5_EPS, 1.f, st_);
+    linear_pre(h_, d, T, w.W1, D.ffl, d, epi_bf16(nullptr, ff_, D.ffl, ACT_RELU));
+    resid_update(false, ff_, D.ffl, T, w.W2, D.ffl, nullptr);
+  }
+}
+
+void Engine::encode_t5(const EncodeBatch& eb) {
+  const int T = eb.T, d = D.d;
+  if (T > cap_tokens_) throw std::invalid_argument("encode batch exceeds workspace");
+  embed(x_, eb.ids, eb.pos, tok_emb_, nullptr, T, d, st_, 1);
+  for (int l = 0; l < D.L; ++l) enc_layer_t5(l, eb, true, true);
+  rmsnorm(h_, d, x_, d, enc_lnf_g_, T, d, T5_EPS, 1.f, st_);
+  // K13: cross K/V of every decoder layer, K at columns [il, 2il) and V at
+  // [2il, 3il) of the qkv buffer, then scattered to the slots
+  for (int l = 0; l < D.L; ++l) cross_kv(l, eb);
+}
+
+void Engine::cross_kv(int l, const EncodeBatch& eb) {
+  const int il = D.inner_l;
+  linear_pre(h_, D.d, eb.T, layers_[l].Wkvx, 2 * il, D.d, epi_bf16(nullptr, qkv_ + il, 3 * il));
+  kv_scatter(xkc(l), xvc(l), qkv_, eb.tslot, eb.pos, eb.T, D.Hl, D.dh, xctx_, st_);
+}
+
+void Engine::dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, int ctx, const DecodeBatch& db,
+                   const int32_t* nkeys, int max_keys, double sum_keys, const float* bias) {
+  DecodeAttnArgs da;
+  da.q = q;
+  da.ldq = ldq;
+  da.kc = kc;
+  da.vc = vc;
+  da.slot = db.slot;
+  da.n_keys = nkeys;
+  da.out = ctx_;
+  da.ldo = D.inner_l;
+  da.B = db.B;
+  da.H = D.Hl;
+  da.dh = D.dh;
+  da.max_ctx = ctx;
+  da.scale = 1.0f;
+  da.split_len = split_len_;
+  da.max_splits = std::max(1, (max_keys + split_len_ - 1) / split_len_);
+  da.partial = attn_part_;
+  da.bias = bias;
+  da.bias_ld = bias_ld_;
+  da.bias_off = bias_off_;
+  const int k = kbegin();
+  decode_attention(da, st_);
+  kend(k, EXG_K_DECODE_ATTN, sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)db.B * D.Hl * D.dh * 2.0 * 2.0);
+}
+
+void Engine::dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest) {
+  const LayerW& w = layers_[l];
+  const int B = db.B, d = D.d, il = D.inner_l;
+  if (rest) {
+    rmsnorm(h_, d, x_, d, w.ln1_g, B, d, T5_EPS, 1.f, st_);
+    linear_dec(h_, d, B, w.Wqkv, 3 * il, d, epi_bf16(nullptr, qkv_, 3 * il));
+    kv_scatter(kc(l), vc(l), qkv_, db.slot, db.pos, B, D.Hl, D.dh, slot_ctx_, st_);
+  }
+  if (attn) dattn(qkv_, 3 * il, kc(l), vc(l), slot_ctx_, db, db.nkeys, db.max_keys, db.sum_keys, dec_bias_);
+  if (rest) {
+    resid_update(true, ctx_, il, B, w.Wo, il, nullptr);
+    rmsnorm(h_, d, x_, d, w.lnx_g, B, d, T5_EPS, 1.f, st_);
+    linear_dec(h_, d, B, w.Wqx, il, d, epi_bf16(nullptr, qkv_, 3 * il));
+  }
+  if (attn) dattn(qkv_, 3 * il, xkc(l), xvc(l), xctx_, db, db.xkeys, db.max_xkeys, db.sum_xkeys, nullptr);
+  if (rest) {
+    resid_update(true, ctx_, il, B, w.Wox, il, nullptr);
+    rmsnorm(h_, d, x_, d, w.ln2_g, B, d, T5_EPS, 1.f, st_);
+    linear_dec(h_, d, B, w.W1, D.ffl, d, epi_bf16(nullptr, ff_, D.ffl, ACT_RELU));
+    resid_update(true, ff_, D.ffl, B, w.W2, D.ffl, nullptr);
   }
 }
 

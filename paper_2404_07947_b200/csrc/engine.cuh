@@ -19,7 +19,10 @@
 namespace exg {
 
 struct LayerW {
-  bf16 *ln1_g, *ln1_b, *Wqkv, *bqkv, *Wo, *bo, *ln2_g, *ln2_b, *W1, *b1, *W2, *b2;
+  bf16 *ln1_g = nullptr, *ln1_b = nullptr, *Wqkv = nullptr, *bqkv = nullptr, *Wo = nullptr, *bo = nullptr;
+  bf16 *ln2_g = nullptr, *ln2_b = nullptr, *W1 = nullptr, *b1 = nullptr, *W2 = nullptr, *b2 = nullptr;
+  // T5 decoder cross-attention: RMS gain, W_q_x^T, W_kv_x^T, W_o_x^T
+  bf16 *lnx_g = nullptr, *Wqx = nullptr, *Wkvx = nullptr, *Wox = nullptr;
 };
 
 struct Dims {
@@ -57,6 +60,10 @@ struct DecodeBatch {
   double sum_keys = 0;     // sum_i n_keys[i]   (decode-attention work)
   const int32_t *slot = nullptr, *pos = nullptr, *nkeys = nullptr, *out_off = nullptr;
   int32_t* out_tokens = nullptr;   // device [sum S] (last stage)
+  // encoder-decoder: cross-attention key counts (= input lengths) per row
+  const int32_t* xkeys = nullptr;
+  int max_xkeys = 0;
+  double sum_xkeys = 0;
 };
 
 class Engine {
@@ -75,7 +82,17 @@ class Engine {
   void set_reducer(Reducer* r) { red_ = r; }
 
   void ensure_workspace(int max_tokens, int max_rows);
-  void ensure_kv(int slots, int slot_ctx, int layers = -1);
+  // decoder self-attention KV (slot_ctx keys per slot); encoder-decoder
+  // models also get the cross K/V cache of every decoder layer (xctx keys)
+  void ensure_kv(int slots, int slot_ctx, int layers = -1, int xctx = 0);
+  // T5-style encoder-decoder: encode = encoder over all
+  // n input tokens + cross K/V projections (K13); decode starts from token 0
+  bool encdec() const { return t5_; }
+  int xctx() const { return xctx_; }
+  bf16* xkc(int l) const { return xkv_ + (size_t)l * 2 * xkv_layer_elems(); }
+  bf16* xvc(int l) const { return xkc(l) + xkv_layer_elems(); }
+  // K13: cross K/V of decoder layer l from the encoder output (bf16 in h)
+  void cross_kv(int l, const EncodeBatch& eb);
   int kv_slots() const { return kv_slots_; }
   int slot_ctx() const { return slot_ctx_; }
   int32_t* last_tok() { return last_tok_; }
@@ -135,6 +152,12 @@ class Engine {
   int kbegin();
   void kend(int idx, int cls, double work);
   void gen_weights();
+  void gen_weights_t5();
+  void encode_t5(const EncodeBatch& eb);
+  void enc_layer_t5(int l, const EncodeBatch& eb, bool attn, bool rest);
+  void dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest);
+  void dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, int ctx, const DecodeBatch& db,
+             const int32_t* nkeys, int max_keys, double sum_keys, const float* bias);
   void linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   void linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   // residual update x += W.act + b: fused epilogue (tp = 1) or partial ->
@@ -153,6 +176,15 @@ class Engine {
   size_t wbytes_ = 0;
   bf16 *tok_emb_ = nullptr, *pos_emb_ = nullptr, *lnf_g_ = nullptr, *lnf_b_ = nullptr;
   std::vector<LayerW> layers_;
+  // encoder-decoder (T5)
+  bool t5_ = false;
+  std::vector<LayerW> enc_layers_;
+  bf16 *enc_lnf_g_ = nullptr, *enc_rel_ = nullptr, *dec_rel_ = nullptr;
+  float *enc_bias_ = nullptr, *dec_bias_ = nullptr;   // fp32 [Hl][2 max_pos - 1], centre max_pos - 1
+  int bias_ld_ = 0, bias_off_ = 0;
+  bf16* xkv_ = nullptr;
+  int xctx_ = 0;
+  size_t xkv_layer_elems() const { return (size_t)kv_slots_ * D.Hl * xctx_ * D.dh; }
   // workspace
   int cap_tokens_ = 0, cap_rows_ = 0;
   float* x_ = nullptr;

@@ -48,10 +48,10 @@ __global__ void embed_kernel(float* __restrict__ x, const int32_t* __restrict__ 
   griddep_launch_dependents();
   const int t = blockIdx.x;
   const int64_t id = ids[t];
-  const bf16* b = pe + (int64_t)pos[t] * d;
+  const bf16* b = pe ? pe + (int64_t)pos[t] * d : nullptr;
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     const bf16 a = tok[tok_blocked ? blocked_index(id, j, d) : id * d + j];
-    x[(int64_t)t * d + j] = __fadd_rn(bf2f(a), bf2f(b[j]));
+    x[(int64_t)t * d + j] = b ? __fadd_rn(bf2f(a), bf2f(b[j])) : bf2f(a);
   }
 }
 
@@ -101,6 +101,46 @@ void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g,
                float eps, cudaStream_t st) {
   if (T <= 0) return;
   layernorm_kernel<<<T, 256, 0, st>>>(y, ldy, x, ldx, g, b, d, eps);
+  EXG_CHECK_LAUNCH();
+}
+
+// T5 RMSNorm: y = bf16(x * rsqrt(mean(x^2) + eps) * g * out_scale)
+__global__ void __launch_bounds__(256) rmsnorm_kernel(bf16* __restrict__ y, int64_t ldy, const float* __restrict__ x,
+                                                      int64_t ldx, const bf16* __restrict__ g, int d, float eps,
+                                                      float out_scale) {
+  griddep_launch_dependents();
+  __shared__ float red[8];
+  const float* xr = x + (int64_t)blockIdx.x * ldx;
+  float q = 0.f;
+  for (int j = threadIdx.x; j < d; j += 256) q += xr[j] * xr[j];
+  const float ms = block_sum_256(q, red) / (float)d;
+  const float rstd = rsqrtf(ms + eps);
+  bf16* yr = y + (int64_t)blockIdx.x * ldy;
+  for (int j = threadIdx.x; j < d; j += 256) yr[j] = f2bf(xr[j] * rstd * bf2f(g[j]) * out_scale);
+}
+
+void rmsnorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, int T, int d, float eps,
+             float out_scale, cudaStream_t st) {
+  if (T <= 0) return;
+  rmsnorm_kernel<<<T, 256, 0, st>>>(y, ldy, x, ldx, g, d, eps, out_scale);
+  EXG_CHECK_LAUNCH();
+}
+
+// fp32 relative-bias table: tab[h][j] = rel[bucket[j]][h0 + h] (bf16 weights,
+// rel is [n_buckets][H_total])
+__global__ void rel_bias_table_kernel(float* __restrict__ tab, const bf16* __restrict__ rel,
+                                      const int32_t* __restrict__ bucket, int n, int Hl, int H_total, int h0) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * Hl) return;
+  const int h = (int)(e / n), j = (int)(e % n);
+  tab[e] = bf2f(rel[(int64_t)bucket[j] * H_total + h0 + h]);
+}
+
+void rel_bias_table(float* tab, const bf16* rel, const int32_t* bucket, int n, int Hl, int H_total, int h0,
+                    cudaStream_t st) {
+  const int64_t tot = (int64_t)n * Hl;
+  if (tot <= 0) return;
+  rel_bias_table_kernel<<<(int)((tot + 255) / 256), 256, 0, st>>>(tab, rel, bucket, n, Hl, H_total, h0);
   EXG_CHECK_LAUNCH();
 }
 
@@ -240,7 +280,9 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a) {
     }
 #pragma unroll
     for (int o2 = 1; o2 < C::LPK; o2 <<= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o2);
-    const float score = valid ? dot * a.scale : -INFINITY;
+    float score = valid ? __fmul_rn(dot, a.scale) : -INFINITY;
+    if (a.bias && valid)  // T5 relative bias of distance key - query (query = newest key)
+      score = __fadd_rn(score, a.bias[(int64_t)h * a.bias_ld + a.bias_off + (k_begin + t * C::KT + key_local) - (nk - 1)]);
     const float tmax = warp_max(score);
     const float m_new = fmaxf(m, tmax);
     const float alpha = (m == -INFINITY) ? 0.f : __expf(m - m_new);
@@ -387,7 +429,8 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
     o[d] = 0.f;
   }
   float m = -INFINITY, l = 0.f;
-  const int last_key = p0 + min(len, qb + QPB) - 1;  // inclusive, for the whole CTA
+  const int last_key = a.causal ? p0 + min(len, qb + QPB) - 1 : p0 + len - 1;  // inclusive, for the whole CTA
+  const float* brow = a.bias ? a.bias + (int64_t)h * a.bias_ld + a.bias_off - my_pos : nullptr;
   for (int kt = 0; kt <= last_key; kt += KTILE) {
     const int nkt = min(KTILE, last_key + 1 - kt);
     __syncthreads();
@@ -410,8 +453,9 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
       }
       dot += __shfl_xor_sync(0xffffffffu, dot, 1);
       dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-      const bool ok = qvalid && j < nkt && (kt + j) <= my_pos;
-      sc[j] = ok ? dot * a.scale : -INFINITY;
+      const bool ok = qvalid && j < nkt && (!a.causal || (kt + j) <= my_pos);
+      sc[j] = ok ? __fmul_rn(dot, a.scale) : -INFINITY;
+      if (brow && ok) sc[j] = __fadd_rn(sc[j], brow[kt + j]);
       tmax = fmaxf(tmax, sc[j]);
     }
     if (tmax == -INFINITY) continue;

@@ -36,6 +36,14 @@ void embed(float* x, const int32_t* ids, const int32_t* pos, const bf16* tok_emb
 void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
                float eps, cudaStream_t st);
 
+// ---- T5 RMSNorm: y = bf16(x rsqrt(mean(x^2) + eps) g out_scale) ----------
+void rmsnorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, int T, int d, float eps,
+             float out_scale, cudaStream_t st);
+// fp32 table tab[h][j] = rel[bucket[j]][h0 + h], h < Hl, j < n (T5 relative
+// attention bias, bucket[] precomputed on the host, T9)
+void rel_bias_table(float* tab, const bf16* rel, const int32_t* bucket, int n, int Hl, int H_total, int h0,
+                    cudaStream_t st);
+
 // ---- K7: scatter the K,V columns of a fused qkv buffer into cache slots -----
 // qkv: [T][3*inner] bf16; token t goes to (slot[t], pos[t]).
 // Cache layout per layer: [slot][H][max_ctx][dh] for K and for V.
@@ -62,6 +70,10 @@ struct DecodeAttnArgs {
   int split_len;
   int max_splits;      // >= ceil(max_i n_keys[i] / split_len)
   float* partial;      // [B][H][max_splits][dh + 2] when max_splits > 1
+  // optional additive score bias (T5 relative position bias): the score of
+  // key k of row i, head h gets bias[h * bias_ld + bias_off + k - (n_keys[i]-1)]
+  const float* bias = nullptr;
+  int bias_ld = 0, bias_off = 0;
 };
 void decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
 
@@ -84,6 +96,11 @@ struct PrefillAttnArgs {
   float scale;
   int64_t q_rows;      // rows of the qkv buffer (tokens)
   int64_t kv_rows;     // slots * H * max_ctx
+  // causal = 0: every query attends to all keys pos0 .. pos0+len-1 of its
+  // request (T5 encoder); bias: score(q, k) += bias[h * bias_ld + bias_off + kpos - qpos]
+  int causal = 1;
+  const float* bias = nullptr;
+  int bias_ld = 0, bias_off = 0;
 };
 // dh = 128: tcgen05 FMHA (attn_prefill_tc.cu); other head dims: SIMT kernel
 void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);

@@ -78,7 +78,7 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
   const int max_enc_tokens = std::max(max_t, max_c);
   const int ctx_cap = max_c;
   const int slots = std::max(max_b, (max_enc_tokens + ctx_cap - 1) / ctx_cap);
-  E.ensure_kv(slots, ctx_cap, 1);
+  E.ensure_kv(slots, ctx_cap, 1, E.encdec() ? ctx_cap : 0);
   E.ensure_workspace(max_enc_tokens, max_b);
   cudaStream_t st = E.stream();
 
@@ -91,7 +91,7 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
     h_slot[t] = t / ctx_cap;
   }
   int32_t* d;
-  const size_t nints = (size_t)3 * n_tok + 4 * (slots + 1);
+  const size_t nints = (size_t)3 * n_tok + 3 * (slots + 1) + 2 * max_b;
   EXG_CUDA(cudaMalloc(&d, nints * sizeof(int32_t)));
   int32_t *d_ids = d, *d_pos = d + n_tok, *d_slot = d + 2 * n_tok;
   int32_t *d_cu = d + 3 * n_tok, *d_rs = d_cu + slots + 1, *d_p0 = d_rs + slots + 1, *d_aux = d_p0 + slots + 1;
@@ -113,7 +113,7 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
   ad = ae;
   ae.t.assign(bs.size(), std::vector<double>(cs.size()));
   ad.t.assign(bs.size(), std::vector<double>(cs.size()));
-  std::vector<int32_t> h_cu(slots + 1), h_nk(max_b);
+  std::vector<int32_t> h_cu(slots + 1), h_nk(2 * max_b);
   for (size_t ib = 0; ib < bs.size(); ++ib) {
     const int b = bs[ib];
     for (size_t ic = 0; ic < cs.size(); ++ic) {
@@ -134,14 +134,20 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
       eb.pos0 = d_p0;
       ae.t[ib][ic] = tm.median(reps, [&] { E.layer_encode(0, eb, true, false); }) * ((double)b / be);
       // decode attention: b rows, c keys each, row i in slot i
-      for (int i = 0; i < b; ++i) h_nk[i] = c;
-      EXG_CUDA(cudaMemcpy(d_aux, h_nk.data(), b * 4, cudaMemcpyHostToDevice));
+      // (encoder-decoder: c keys split between self- and cross-attention,
+      // ceil(c/2) encoder keys -- the simulator's context is S_e + S_d / 2)
+      const int c_self = E.encdec() ? std::max(1, c / 2) : c, c_x = std::max(1, c - c / 2);
+      for (int i = 0; i < b; ++i) h_nk[i] = c_self;
+      for (int i = 0; i < b; ++i) h_nk[max_b + i] = c_x;
+      EXG_CUDA(cudaMemcpy(d_aux, h_nk.data(), 2 * max_b * 4, cudaMemcpyHostToDevice));
       DecodeBatch db;
       db.B = b;
-      db.max_keys = c;
+      db.max_keys = c_self;
       db.slot = d_rs;
       db.pos = d_p0;
       db.nkeys = d_aux;
+      db.xkeys = d_aux + max_b;
+      db.max_xkeys = c_x;
       ad.t[ib][ic] = tm.median(reps, [&] { E.layer_decode(0, db, true, false); });
     }
   }
@@ -157,7 +163,12 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
     eb.pos = d_pos;
     eb.tslot = d_slot;
     re.x.push_back(T);
-    re.t.push_back(tm.median(reps, [&] { E.layer_encode(0, eb, false, true); }));
+    // encoder-decoder: the encode phase also projects the cross K/V of each
+    // decoder layer (K13), charged to the layer
+    re.t.push_back(tm.median(reps, [&] {
+      E.layer_encode(0, eb, false, true);
+      if (E.encdec()) E.cross_kv(0, eb);
+    }));
   }
   // decode rest: input size = batch rows, swept over the batch axis
   for (int b : bs) {
@@ -167,6 +178,8 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
     db.slot = d_rs;
     db.pos = d_p0;
     db.nkeys = d_aux;
+    db.xkeys = d_aux + max_b;
+    db.max_xkeys = 1;
     rd.x.push_back(b);
     rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }));
   }

@@ -91,13 +91,20 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   const Dims& D = E.dims();
   if (s.strategy != EXG_RRA) throw std::invalid_argument("run_rra: strategy is not RRA");
   if (s.b_e < 1 || s.b_d < s.b_e || s.n_d < 1) throw std::invalid_argument("RRA needs 1 <= B_E <= B_D, N_D >= 1");
-  int max_in = 1, max_ctx = 1;
+  // token accounting: decoder-only encode = positions
+  // 0..n-2, decode u consumes x[n-1] / y[u-1] at position n-1+u-1;
+  // encoder-decoder encode = all n tokens, decode u consumes the start token
+  // 0 / y[u-1] at decoder position u-1 and cross-attends to the n encoder keys
+  const bool ed = E.encdec();
+  int max_in = 1, max_ctx = 1, max_out = 1;
   int64_t total_out = 0;
   std::vector<int64_t> base(n + 1, 0);
   for (int r = 0; r < n; ++r) {
     const exg_request& q = reqs[r];
     if (q.input_len < 1 || q.output_len < 1 || !q.input_ids) throw std::invalid_argument("request lengths must be >= 1");
-    if (q.input_len + q.output_len > D.max_pos) throw std::invalid_argument("input_len + output_len > max_pos");
+    if (ed ? std::max(q.input_len, q.output_len) > D.max_pos : q.input_len + q.output_len > D.max_pos)
+      throw std::invalid_argument(ed ? "input_len or output_len > max_pos" : "input_len + output_len > max_pos");
+    max_out = std::max(max_out, q.output_len);
     for (int j = 0; j < q.input_len; ++j)
       if (q.input_ids[j] < 0 || q.input_ids[j] >= D.V) throw std::invalid_argument("token id out of range");
     max_in = std::max(max_in, q.input_len);
@@ -105,18 +112,20 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
     base[r + 1] = base[r] + q.output_len;
   }
   total_out = base[n];
-  const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : max_ctx;
-  if (slot_ctx < max_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
+  const int need_ctx = ed ? max_out : max_ctx;
+  const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : need_ctx;
+  if (slot_ctx < need_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
   const int B_D = s.b_d, B_E = s.b_e;
-  E.ensure_kv(B_D, slot_ctx);
-  E.ensure_workspace(B_E * (max_in - 1), B_D);
+  const int enc_drop = ed ? 0 : 1;   // input tokens the encode phase does not process
+  E.ensure_kv(B_D, slot_ctx, -1, ed ? max_in : 0);
+  E.ensure_workspace(std::max(1, B_E * (max_in - enc_drop)), B_D);
   cudaStream_t st = E.stream();
 
   // device arrays: output tokens, encode tables, decode tables
   int32_t* d_out = nullptr;
   int32_t* d_tab = nullptr;
   const size_t enc_ints = (size_t)3 * B_E * max_in + 3 * (B_E + 1) + 2 * B_E;
-  const size_t dec_ints = (size_t)4 * B_D;
+  const size_t dec_ints = (size_t)5 * B_D;
   const size_t tab_ints = std::max(enc_ints, dec_ints);
   EXG_CUDA(cudaMalloc(&d_out, sizeof(int32_t) * std::max<int64_t>(total_out, 1)));
   EXG_CUDA(cudaMalloc(&d_tab, sizeof(int32_t) * (enc_ints + dec_ints)));
@@ -161,7 +170,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       Staging::Slot& sl = stage.acquire();
       int32_t* h = sl.host;
       int T = 0, maxlen = 0;
-      for (int k = 0; k < admit; ++k) T += reqs[next_req + k].input_len - 1;
+      for (int k = 0; k < admit; ++k) T += reqs[next_req + k].input_len - enc_drop;
       int32_t* ids = h;
       int32_t* pos = ids + T;
       int32_t* tsl = pos + T;
@@ -176,7 +185,8 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         const exg_request& q = reqs[r];
         const int slot = free_slots.back();
         free_slots.pop_back();
-        for (int j = 0; j < q.input_len - 1; ++j, ++t) {
+        const int ne = q.input_len - enc_drop;
+        for (int j = 0; j < ne; ++j, ++t) {
           ids[t] = q.input_ids[j];
           pos[t] = j;
           tsl[t] = slot;
@@ -184,9 +194,9 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         cu[k + 1] = t;
         rsl[k] = slot;
         p0[k] = 0;
-        last[k] = q.input_ids[q.input_len - 1];
-        maxlen = std::max(maxlen, q.input_len - 1);
-        active.push_back(Row{r, slot, q.input_len - 1, 0});
+        last[k] = ed ? 0 : q.input_ids[q.input_len - 1];
+        maxlen = std::max(maxlen, ne);
+        active.push_back(Row{r, slot, ed ? 0 : q.input_len - 1, 0});
         admit_ev[r] = ev_phase;
       }
       const size_t nints = (size_t)3 * T + (admit + 1) + 3 * admit;
@@ -199,8 +209,8 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       eb.R = admit;
       eb.max_len = maxlen;
       for (int k = 0; k < admit; ++k) {
-        const double m = reqs[next_req + k].input_len - 1;
-        eb.attn_pairs += m * (m + 1) / 2;
+        const double m = reqs[next_req + k].input_len - enc_drop;
+        eb.attn_pairs += ed ? m * m : m * (m + 1) / 2;
       }
       eb.ids = d_enc;
       eb.pos = d_enc + T;
@@ -218,18 +228,21 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       const int B = (int)active.size();
       Staging::Slot& sl = stage.acquire();
       int32_t* h = sl.host;
-      int max_keys = 0;
-      double sum_keys = 0;
+      int max_keys = 0, max_xkeys = 0;
+      double sum_keys = 0, sum_xkeys = 0;
       for (int i = 0; i < B; ++i) {
         const Row& rw = active[i];
         h[i] = rw.slot;
         h[B + i] = rw.pos;
         h[2 * B + i] = rw.pos + 1;
         h[3 * B + i] = (int32_t)(base[rw.req] + rw.emitted);
+        h[4 * B + i] = reqs[rw.req].input_len;
         max_keys = std::max(max_keys, rw.pos + 1);
         sum_keys += rw.pos + 1;
+        max_xkeys = std::max(max_xkeys, reqs[rw.req].input_len);
+        sum_xkeys += reqs[rw.req].input_len;
       }
-      EXG_CUDA(cudaMemcpyAsync(d_dec, h, (size_t)4 * B * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      EXG_CUDA(cudaMemcpyAsync(d_dec, h, (size_t)5 * B * sizeof(int32_t), cudaMemcpyHostToDevice, st));
       EXG_CUDA(cudaEventRecord(sl.ev, st));
       DecodeBatch db;
       db.B = B;
@@ -239,6 +252,11 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       db.pos = d_dec + B;
       db.nkeys = d_dec + 2 * B;
       db.out_off = d_dec + 3 * B;
+      if (ed) {
+        db.xkeys = d_dec + 4 * B;
+        db.max_xkeys = max_xkeys;
+        db.sum_xkeys = sum_xkeys;
+      }
       db.out_tokens = d_out;
       E.decode(db);
       if (dumping) {

@@ -144,7 +144,7 @@ def test_decode_attention_parity(L, dh):
     part = torch.zeros(B * H * max_splits * (dh + 2), dtype=torch.float32, device=dev())
     out = torch.zeros((B, H * dh), dtype=torch.bfloat16, device=dev())
     _run(L, "exg_op_decode_attention", ptr(tq), 3 * H * dh, ptr(tK), ptr(tV), ptr(tslot), ptr(tnk), ptr(out),
-         H * dh, B, H, dh, max_ctx, scale, split_len, max_splits, ptr(part), stream())
+         H * dh, B, H, dh, max_ctx, scale, split_len, max_splits, ptr(part), None, 0, 0, stream())
     torch.cuda.synchronize()
     got = to_np(out)
     for i in range(B):
@@ -174,7 +174,7 @@ def test_decode_attention_constant_keys_give_mean(L):
     part = torch.zeros(H * 2 * (dh + 2), dtype=torch.float32, device=dev())
     out = torch.zeros((1, H * dh), dtype=torch.bfloat16, device=dev())
     _run(L, "exg_op_decode_attention", ptr(tq), 3 * H * dh, ptr(tK), ptr(tV), ptr(tslot), ptr(tnk), ptr(out),
-         H * dh, 1, H, dh, max_ctx, 0.088388, 512, 2, ptr(part), stream())
+         H * dh, 1, H, dh, max_ctx, 0.088388, 512, 2, ptr(part), None, 0, 0, stream())
     torch.cuda.synchronize()
     ref = V[0, :, :nk].mean(axis=1).reshape(-1)
     assert np.abs(to_np(out)[0] - ref).max() < 2e-3
@@ -195,7 +195,7 @@ def test_decode_attention_batch_invariant(L):
         tn = torch.from_numpy(nk[rows]).to(dev())
         out = torch.zeros((len(rows), H * dh), dtype=torch.bfloat16, device=dev())
         _run(L, "exg_op_decode_attention", ptr(tq), H * dh, ptr(tK), ptr(tV), ptr(ts), ptr(tn), ptr(out), H * dh,
-             len(rows), H, dh, max_ctx, 0.088388, 512, 2, ptr(part), stream())
+             len(rows), H, dh, max_ctx, 0.088388, 512, 2, ptr(part), None, 0, 0, stream())
         torch.cuda.synchronize()
         return out.cpu()
 
@@ -232,7 +232,7 @@ def test_prefill_attention_parity(L, dh):
     out = torch.zeros((T, H * dh), dtype=torch.bfloat16, device=dev())
     scale = float(np.float32(1 / math.sqrt(dh)))
     _run(L, "exg_op_prefill_attention", ptr(tq), 3 * H * dh, ptr(tK), ptr(tV), ptr(tcu), ptr(tsl), ptr(tp0), R,
-         max(lens), ptr(out), H * dh, H, dh, max_ctx, n_slots, T, scale, stream())
+         max(lens), ptr(out), H * dh, H, dh, max_ctx, n_slots, T, scale, 1, None, 0, 0, stream())
     torch.cuda.synchronize()
     got = to_np(out)
     rel, ab = (2.0 ** -8, 2e-3) if dh != 128 else (2.0 ** -7, 4e-3)

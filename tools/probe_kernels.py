@@ -65,7 +65,7 @@ def dattn(B, c, H=40, dh=128, split_len=512):
     def fn():
         L.check(L.lib().exg_op_decode_attention(q.data_ptr(), 3 * H * dh, kc.data_ptr(), vc.data_ptr(),
                                                 slot.data_ptr(), nk.data_ptr(), out.data_ptr(), H * dh, B, H, dh,
-                                                max_ctx, 0.0883883, split_len, ms, part.data_ptr(), st()))
+                                                max_ctx, 0.0883883, split_len, ms, part.data_ptr(), None, 0, 0, st()))
     t = timeit(fn)
     byts = B * H * (2.0 * c * dh * 2 + 2 * dh * 2)
     print("decode-attn B=%4d c=%5d H=%d: %8.1f us  %7.1f GB/s" % (B, c, H, t * 1e6, byts / t / 1e9))
@@ -85,7 +85,7 @@ def pattn(R, n, H=40, dh=128):
     def fn():
         L.check(L.lib().exg_op_prefill_attention(q.data_ptr(), 3 * H * dh, kc.data_ptr(), vc.data_ptr(),
                                                  cu.data_ptr(), slot.data_ptr(), p0.data_ptr(), R, n, out.data_ptr(),
-                                                 H * dh, H, dh, max_ctx, R, T, 0.0883883, st()))
+                                                 H * dh, H, dh, max_ctx, R, T, 0.0883883, 1, None, 0, 0, st()))
     t = timeit(fn)
     flops = 4.0 * H * dh * R * n * (n + 1) / 2
     print("prefill-attn R=%d n=%d: %8.1f us  %7.1f TFLOP/s" % (R, n, t * 1e6, flops / t / 1e12))
