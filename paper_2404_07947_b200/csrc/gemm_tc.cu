@@ -94,6 +94,46 @@ __device__ __forceinline__ void epi_store(const EpiParams& ep, int tok, int feat
   }
 }
 
+// 16 consecutive tokens t0.. of one feature (decode swap-AB orientation).
+// All global loads (bias, residual) are issued before any store: a per-element
+// read-modify-write would serialise 16 memory round trips, since the compiler
+// cannot prove the stores do not alias the next load.
+__device__ __forceinline__ void epi_store_col16(const EpiParams& ep, int t0, int feat, int N, const float* v) {
+  const int n = min(16, N - t0);
+  const float b = ep.bias ? bf2f(ep.bias[feat]) : 0.f;
+  float x[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    x[j] = v[j];
+    if (ep.bias) x[j] += b;
+  }
+  switch (ep.mode) {
+    case EPI_BF16_ACT:
+#pragma unroll
+      for (int j = 0; j < 16; ++j) x[j] = ep.act == ACT_RELU ? fmaxf(x[j], 0.0f) : (ep.act == ACT_GELU ? gelu_tanh(x[j]) : x[j]);
+      // fall through
+    case EPI_BF16:
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < n) ep.out_bf16[(int64_t)(t0 + j) * ep.ldo + feat] = f2bf(x[j]);
+      break;
+    case EPI_RESID: {
+      float* r = ep.resid + (int64_t)t0 * ep.ldr + feat;
+      float old[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) old[j] = j < n ? r[(int64_t)j * ep.ldr] : 0.f;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < n) r[(int64_t)j * ep.ldr] = old[j] + x[j];
+      break;
+    }
+    default:
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < n) ep.out_f32[(int64_t)(t0 + j) * ep.ldo + feat] = x[j];
+  }
+}
+
 // 16 consecutive features of one token row (prefill orientation), vectorised
 __device__ __forceinline__ void epi_store_row16(const EpiParams& ep, int tok, int f0, int N, const float* v) {
   if (f0 + 16 <= N) {
@@ -114,9 +154,12 @@ __device__ __forceinline__ void epi_store_row16(const EpiParams& ep, int tok, in
     } else if (ep.mode == EPI_RESID) {
       if ((ep.ldr & 3) == 0) {
         float4* r = reinterpret_cast<float4*>(ep.resid + (int64_t)tok * ep.ldr + f0);
+        float4 old[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) old[q] = r[q];   // all loads before any store
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          float4 x = r[q];
+          float4 x = old[q];
           x.x += epi_value(ep, f0 + 4 * q, v[4 * q]);
           x.y += epi_value(ep, f0 + 4 * q + 1, v[4 * q + 1]);
           x.z += epi_value(ep, f0 + 4 * q + 2, v[4 * q + 2]);
@@ -384,13 +427,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
         for (int c = c_lo; c < c_hi; c += 16) {
           float v[16];
           tmem_ld16(taddr + c, v);
-          if (row_ok) {
-#pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              const int tok = u.n * BN + c + j;
-              if (tok < N) epi_store(ep, tok, gm, v[j]);
-            }
-          }
+          if (row_ok && u.n * BN + c < N) epi_store_col16(ep, u.n * BN + c, gm, N, v);
         }
       } else {
         for (int c = c_lo; c < c_hi; c += 16) {
@@ -431,9 +468,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
             }
             if (!row_ok) continue;
             if (SWAP) {
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (u.n * BN + c0 + j < N) epi_store(ep, u.n * BN + c0 + j, gm, acc[j]);
+              if (u.n * BN + c0 < N) epi_store_col16(ep, u.n * BN + c0, gm, N, acc);
             } else {
               epi_store_row16(ep, gm, u.n * BN + c0, N, acc);
             }
@@ -516,9 +551,7 @@ __global__ void __launch_bounds__(128) streamk_reduce_kernel(const float* __rest
     }
     if (gm >= M) continue;
     if (SWAP) {
-#pragma unroll
-      for (int j = 0; j < 16; ++j)
-        if (n * BN + c0 + j < N) epi_store(ep, n * BN + c0 + j, gm, acc[j]);
+      if (n * BN + c0 < N) epi_store_col16(ep, n * BN + c0, gm, N, acc);
     } else {
       epi_store_row16(ep, gm, n * BN + c0, N, acc);
     }

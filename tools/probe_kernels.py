@@ -128,6 +128,9 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "dattn":
         dattn(int(sys.argv[2]), int(sys.argv[3]))
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "pattn":
+        pattn(int(sys.argv[2]), int(sys.argv[3]))
+        sys.exit(0)
     d, ff = 5120, 20480
     for T in (2048, 8192):
         gemm(T, 3 * d, d, False)
