@@ -171,9 +171,20 @@ exg_status exg_get_unique_id(uint8_t uid[128]);
 
 /* Create a rank's context on `device`: allocates and generates this rank's
  * weights on the GPU from spec->weight_seed (K14).  Collective over `world`
- * ranks when world > 1.  *out is owned by the library (exg_destroy). */
+ * ranks when world > 1 (one process per GPU, NCCL over NVLink; uid from
+ * exg_get_unique_id on rank 0): GPU g of a schedule's layout (G GPUs) belongs
+ * to rank g*world/G, every rank calls exg_run with identical arguments and the
+ * outputs are written on rank 0.  world = 1 with cluster->n_gpus > 1 runs every
+ * GPU of a layout in this one process on `device` (single-device emulation).
+ * *out is owned by the library (exg_destroy). */
 exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device, int32_t rank,
                       int32_t world, const uint8_t* uid, exg_ctx** out);
+/* `world` rank contexts of one process on one `device`, connected by a
+ * device-copy transport instead of NCCL (each rank's exg_run must be called
+ * from its own thread).  For testing the multi-rank executor on one GPU;
+ * out[0..world) are destroyed individually with exg_destroy. */
+exg_status exg_create_local_group(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device,
+                                  int32_t world, exg_ctx** out);
 void exg_destroy(exg_ctx* ctx);
 
 /* ---- XProfiler --------------------------------------- */

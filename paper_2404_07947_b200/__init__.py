@@ -5,7 +5,9 @@ under an RRA / WAA schedule, behind the C-ABI of libexegpt.so
 step of the hot path runs in the library's CUDA kernels.
 """
 from ._lib import (EXG_RRA, EXG_WAA_C, EXG_WAA_M, Context, ExgError, Pmf, Profile, cluster_spec, lib,
-                   model_spec, rra_schedule, schedule_find, schedule_resolve, search_opts, simulate)
+                   local_group, model_spec, rra_schedule, run_group, schedule_find, schedule_resolve, search_opts,
+                   simulate, unique_id)
 
 __all__ = ["EXG_RRA", "EXG_WAA_C", "EXG_WAA_M", "Context", "ExgError", "Pmf", "Profile", "cluster_spec", "lib",
-           "model_spec", "rra_schedule", "schedule_find", "schedule_resolve", "search_opts", "simulate"]
+           "local_group", "model_spec", "rra_schedule", "run_group", "schedule_find", "schedule_resolve",
+           "search_opts", "simulate", "unique_id"]

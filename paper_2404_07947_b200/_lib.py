@@ -115,6 +115,8 @@ _SIGS = {
     "exg_create": (C.c_int, [C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.c_int32, C.c_int32,
                              C.c_int32, C.POINTER(C.c_uint8), C.POINTER(_P)]),
     "exg_destroy": (None, [_P]),
+    "exg_create_local_group": (C.c_int, [C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.c_int32,
+                                         C.c_int32, C.POINTER(_P)]),
     "exg_profile_run": (C.c_int, [_P, C.POINTER(exg_profile_grid), C.POINTER(_P)]),
     "exg_profile_save": (C.c_int, [_P, C.c_char_p]),
     "exg_profile_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
@@ -197,13 +199,30 @@ def search_opts(eps_t=0.02, eps_l=0.02, b_e_max=256, n_d_max=0, m_max=8, little=
     return exg_search_opts(eps_t, eps_l, b_e_max, n_d_max, m_max, int(little))
 
 
+def unique_id() -> bytes:
+    """NCCL unique id of a multi-rank group (rank 0; broadcast the bytes)."""
+    buf = (C.c_uint8 * 128)()
+    check(lib().exg_get_unique_id(buf))
+    return bytes(buf)
+
+
 class Context:
-    def __init__(self, spec, seed: int, device: int = 0, cluster: Optional[exg_cluster_spec] = None):
+    """One rank's context.  world > 1: one process per GPU, NCCL (uid from
+    unique_id() on rank 0); every rank calls run() with identical arguments and
+    rank 0 receives the outputs."""
+
+    def __init__(self, spec, seed: int, device: int = 0, cluster: Optional[exg_cluster_spec] = None,
+                 rank: int = 0, world: int = 1, uid: Optional[bytes] = None, _handle=None):
         self.spec = spec
         self.mspec = model_spec(spec, seed)
         self.cluster = cluster or cluster_spec()
+        self.rank, self.world = rank, world
+        if _handle is not None:
+            self.h = _handle
+            return
         h = _P()
-        check(lib().exg_create(C.byref(self.mspec), C.byref(self.cluster), device, 0, 1, None, C.byref(h)))
+        ubuf = (C.c_uint8 * 128).from_buffer_copy(uid) if uid is not None else None
+        check(lib().exg_create(C.byref(self.mspec), C.byref(self.cluster), device, rank, world, ubuf, C.byref(h)))
         self.h = h
 
     def close(self):
@@ -265,6 +284,41 @@ class Context:
                 dumped[i] = logits[off:off + S]
                 off += S
         return toks, lat, stats.as_dict(), dumped
+
+
+def local_group(spec, seed: int, world: int, cluster: Optional[exg_cluster_spec] = None, device: int = 0):
+    """`world` rank contexts in this process on one device, joined by the
+    device-copy transport (exg_create_local_group); drive them with run_group."""
+    cluster = cluster or cluster_spec(world)
+    mspec = model_spec(spec, seed)
+    hs = (_P * world)()
+    check(lib().exg_create_local_group(C.byref(mspec), C.byref(cluster), device, world, hs))
+    return [Context(spec, seed, device, cluster, rank=r, world=world, _handle=_P(hs[r])) for r in range(world)]
+
+
+def run_group(ctxs, sched: exg_schedule, requests, **kw):
+    """Call run() on every rank context from its own thread (the calls are
+    collective); returns the per-rank results, rank 0's being authoritative.
+    The first rank error is re-raised."""
+    import threading
+    res = [None] * len(ctxs)
+    err = [None] * len(ctxs)
+
+    def go(r):
+        try:
+            res[r] = ctxs[r].run(sched, requests, **kw)
+        except BaseException as e:  # noqa: BLE001 -- reported below
+            err[r] = e
+
+    th = [threading.Thread(target=go, args=(r,), daemon=True) for r in range(len(ctxs))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in err:
+        if e is not None:
+            raise e
+    return res
 
 
 class Profile:

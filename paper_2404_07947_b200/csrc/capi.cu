@@ -12,6 +12,7 @@
 #include "../../include/exegpt.h"
 #include "../../include/exegpt_ops.h"
 #include "engine.cuh"
+#include "comm.h"
 #include "multi.h"
 #include "planner.h"
 #include "profiler.h"
@@ -118,8 +119,12 @@ const char* exg_last_error(void) { return g_err.c_str(); }
 exg_status exg_get_unique_id(uint8_t uid[128]) {
   return guarded([&] {
     if (!uid) throw std::invalid_argument("null uid");
-    std::memset(uid, 0, 128);
-    return fail(EXG_E_NCCL, "multi-rank contexts are not built in this version");
+    try {
+      exg::nccl_unique_id(uid);
+    } catch (const std::exception& e) {
+      return fail(EXG_E_NCCL, e.what());
+    }
+    return EXG_OK;
   });
 }
 
@@ -129,7 +134,9 @@ exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluste
     if (!out) throw std::invalid_argument("null out");
     *out = nullptr;
     check_spec(spec);
-    if (world != 1 || rank != 0) return fail(EXG_E_NCCL, "multi-rank contexts are not built in this version");
+    if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank / world");
+    if (world > 1 && !uid) throw std::invalid_argument("multi-rank context needs the rank-0 unique id");
+    if (world > 1 && (!cluster || cluster->n_gpus < world)) throw std::invalid_argument("cluster has fewer GPUs than ranks");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EXG_E_CUDA, "no CUDA device");
     if (device < 0 || device >= ndev) throw std::invalid_argument("bad device index");
@@ -139,11 +146,47 @@ exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluste
     c->rank = rank;
     c->world = world;
     c->device = device;
-    if (cluster && cluster->n_gpus > 1)
+    if (world > 1) {
+      std::unique_ptr<exg::Comm> comm;
+      EXG_CUDA(cudaSetDevice(device));
+      try {
+        comm = exg::make_nccl_comm(uid, rank, world);
+      } catch (const std::exception& e) {
+        return fail(EXG_E_NCCL, e.what());
+      }
+      c->multi = std::make_unique<exg::MultiCtx>(*spec, device, std::move(comm));
+    } else if (cluster && cluster->n_gpus > 1) {
       c->multi = std::make_unique<exg::MultiCtx>(*spec, device);  // every GPU of a layout emulated on `device`
-    else
+    } else {
       c->engine = std::make_unique<exg::Engine>(*spec, device);
+    }
     *out = c.release();
+    return EXG_OK;
+  });
+}
+
+exg_status exg_create_local_group(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device,
+                                  int32_t world, exg_ctx** out) {
+  return guarded([&] {
+    if (!out || !cluster) throw std::invalid_argument("null argument");
+    check_spec(spec);
+    if (world < 2 || world > cluster->n_gpus) throw std::invalid_argument("world must be in [2, cluster.n_gpus]");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EXG_E_CUDA, "no CUDA device");
+    if (device < 0 || device >= ndev) throw std::invalid_argument("bad device index");
+    auto hub = exg::make_local_hub(world);
+    std::vector<std::unique_ptr<exg_ctx>> cs;
+    for (int r = 0; r < world; ++r) {
+      auto c = std::make_unique<exg_ctx>();
+      c->spec = *spec;
+      c->cluster = *cluster;
+      c->rank = r;
+      c->world = world;
+      c->device = device;
+      c->multi = std::make_unique<exg::MultiCtx>(*spec, device, exg::make_local_comm(hub, r));
+      cs.push_back(std::move(c));
+    }
+    for (int r = 0; r < world; ++r) out[r] = cs[r].release();
     return EXG_OK;
   });
 }

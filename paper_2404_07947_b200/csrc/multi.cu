@@ -2,22 +2,40 @@
 // partial tensor parallelism inside a stage
 // and WAA's encoder / decoder split with the KV handoff.
 //
-// This file drives the stages of one schedule on ONE device in a single host
-// thread: every (stage, TP rank) is its own Engine holding exactly the weight
-// shard and KV of that GPU of the layout, TP partial sums are reduced in rank
-// order by sum_tp_parts, pipeline hops and the WAA handoff are device copies
-// between the engines.  It is the functional emulation used to check the
-// multi-GPU data flow against the oracle on a single B200; the per-stage
-// work, tables and transfers are the ones a multi-process deployment (one
-// rank per GPU, NCCL in place of the copies) performs.
+// SPMD: every rank runs this same host loop over the whole layout.  GPU g of
+// the layout (G GPUs) belongs to rank owner(g) = g * world / G; a rank builds
+// the Engines (exact weight shard + KV of that GPU) of the GPUs it owns, runs
+// their kernels on its stream, and at each exchange step of the method calls
+// the transport (comm.h) when the two GPUs involved belong to different ranks,
+// or makes a device copy when they belong to the same one:
+//   * pipeline hop: the hidden states [rows][d] fp32 from the previous stage's
+//     TP rank 0 to every TP rank of the next stage;
+//   * TP reduction: each TP rank's fp32 partial sums exchanged inside the group
+//     and summed in rank order on every member (T4(i): bitwise identical on
+//     every rank and to the single-rank run);
+//   * WAA handoff: each encoded request's K/V rows of every layer, sliced by
+//     the receiving TP rank's heads, into the decoder slots it was given;
+//   * token return: the last stage's next-token table to the first stage.
+// The control flow depends only on request lengths (forced outputs), never on
+// device results, so every rank takes the same decisions and issues its sends
+// and recvs in the same global order (no deadlock: the earliest pending
+// exchange always has both of its ranks waiting on it).  world = 1 runs the
+// whole layout in one process on one device (single-device emulation).
+//
+// Latency stamps: a one-thread kernel writes %globaltimer (ns, common to the
+// GPUs of a node) at phase starts (on the rank owning the first encoding
+// stage) and iteration ends (on the rank owning the LM head); rank 0 gathers
+// them and the output tokens at the end.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <map>
 #include <memory>
+#include <set>
 #include <stdexcept>
 #include <vector>
 
+#include "comm.h"
 #include "engine.cuh"
 #include "multi.h"
 #include "runner.h"
@@ -26,119 +44,213 @@ namespace exg {
 
 namespace {
 struct PartPtrs {
-  float* p[8];
-  int n;
+  const float* in[8];   // TP partials in rank order
+  float* out[8];        // buffers receiving the sum
+  int n_in, n_out;
 };
 
-// out[i] = sum_r part_r[i] in rank order, written back to every rank
-__global__ void sum_tp_parts_kernel(PartPtrs pp, int64_t n) {
+__global__ void sum_parts_kernel(PartPtrs pp, int64_t n) {
   griddep_launch_dependents();
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    float s = pp.p[0][i];
-    for (int r = 1; r < pp.n; ++r) s += pp.p[r][i];
-    for (int r = 0; r < pp.n; ++r) pp.p[r][i] = s;
+    float s = pp.in[0][i];
+    for (int r = 1; r < pp.n_in; ++r) s += pp.in[r][i];
+    for (int r = 0; r < pp.n_out; ++r) pp.out[r][i] = s;
   }
+}
+
+void launch_sum(const PartPtrs& pp, int64_t n, cudaStream_t st) {
+  sum_parts_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(pp, n);
+  EXG_CHECK_LAUNCH();
 }
 
 struct HandoffRow {
   int src_slot, dst_slot, len;
+  int64_t off;   // rows before this one in the batch (packed message: [row][Hd][len][dh])
 };
 
-// copy K (or V) rows [0, len) of heads [h0, h0+Hd) of each request from an
-// encoder KV layer [slot][He][ctx_e][dh] into a decoder KV layer
-// [slot][Hd][ctx_d][dh]
+// K (or V) rows [0, len) of heads [h0, h0+Hd) of each request:
+//   mode 0: encoder cache -> decoder cache (both on this rank)
+//   mode 1: encoder cache -> packed message
+//   mode 2: packed message -> decoder cache
 __global__ void kv_handoff_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst, const HandoffRow* rows,
-                                  int nrows, int He, int h0, int Hd, int ctx_e, int ctx_d, int dh) {
+                                  int nrows, int He, int h0, int Hd, int ctx_e, int ctx_d, int dh, int mode) {
   const int rh = blockIdx.x;
   const int i = rh / Hd, h = rh % Hd;
   if (i >= nrows) return;
   const HandoffRow r = rows[i];
-  const int4* s = reinterpret_cast<const int4*>(src + (((int64_t)r.src_slot * He + h0 + h) * ctx_e) * dh);
-  int4* d = reinterpret_cast<int4*>(dst + (((int64_t)r.dst_slot * Hd + h) * ctx_d) * dh);
+  const int64_t pk = (r.off * Hd + (int64_t)h * r.len) * dh;
+  const int4* s = reinterpret_cast<const int4*>(mode == 2 ? src + pk
+                                                          : src + (((int64_t)r.src_slot * He + h0 + h) * ctx_e) * dh);
+  int4* d = reinterpret_cast<int4*>(mode == 1 ? dst + pk : dst + (((int64_t)r.dst_slot * Hd + h) * ctx_d) * dh);
   const int n = r.len * dh / 8;
   for (int e = threadIdx.x; e < n; e += blockDim.x) d[e] = s[e];
+}
+
+__global__ void stamp_kernel(uint64_t* out) {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *out = t;
 }
 }  // namespace
 
 void sum_tp_parts(const std::vector<Engine*>& ranks, int64_t n, cudaStream_t st) {
   if (ranks.size() <= 1 || n <= 0) return;
   PartPtrs pp;
-  pp.n = (int)ranks.size();
-  for (int r = 0; r < pp.n; ++r) pp.p[r] = ranks[r]->part();
-  sum_tp_parts_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(pp, n);
-  EXG_CHECK_LAUNCH();
+  pp.n_in = pp.n_out = (int)ranks.size();
+  for (int r = 0; r < pp.n_in; ++r) pp.in[r] = pp.out[r] = ranks[r]->part();
+  launch_sum(pp, n, st);
 }
 
 // ---------------------------------------------------------------------------
-// Stage: a TP group driven in lockstep
+// Exec: this rank's view of the layout's GPUs
+// ---------------------------------------------------------------------------
+struct Exec {
+  int me = 0, world = 1, G = 1;
+  Comm* comm = nullptr;
+  cudaStream_t st = nullptr;
+  int owner(int gpu) const { return (int)((int64_t)gpu * world / G); }
+  bool mine(int gpu) const { return owner(gpu) == me; }
+  // bytes from (gpu a, src) to (gpu b, dst); a pointer is only valid on its owner
+  void xfer(int ga, const void* src, int gb, void* dst, size_t bytes) const {
+    const int oa = owner(ga), ob = owner(gb);
+    if (bytes == 0) return;
+    if (oa == me && ob == me) {
+      if (src != dst) EXG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+    } else if (oa == me) {
+      comm->send(src, bytes, ob, st);
+    } else if (ob == me) {
+      comm->recv(dst, bytes, oa, st);
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Stage: one TP group (GPUs first_gpu .. first_gpu+tp-1) driven in lockstep
 // ---------------------------------------------------------------------------
 struct Stage {
-  std::vector<std::unique_ptr<Engine>> eng;
-  int l0 = 0, l1 = 0, tp = 1;
+  std::vector<std::unique_ptr<Engine>> eng;   // [tp], nullptr for GPUs of other ranks
+  int l0 = 0, l1 = 0, tp = 1, first_gpu = 0;
   bool first = false, last = false;
-  cudaStream_t st = nullptr;
+  std::vector<float*> tmp;                    // [tp] partial buffers of the cross-rank exchange
+  size_t tmp_cap = 0;
 
-  std::vector<Engine*> ptrs() const {
-    std::vector<Engine*> v;
-    for (auto& e : eng) v.push_back(e.get());
-    return v;
+  ~Stage() {
+    for (float* p : tmp)
+      if (p) cudaFree(p);
   }
-  void load_x(const float* x_in, int rows, int d) {
-    if (first || !x_in) return;
-    for (auto& e : eng) EXG_CUDA(cudaMemcpyAsync(e->x(), x_in, sizeof(float) * rows * d, cudaMemcpyDeviceToDevice, st));
+  int gpu(int r) const { return first_gpu + r; }
+  bool any_local() const {
+    for (auto& e : eng)
+      if (e) return true;
+    return false;
   }
-  void encode(const EncodeBatch& eb, const float* x_in, int d) {
-    if (eb.T <= 0) return;
-    load_x(x_in, eb.T, d);
-    for (auto& e : eng) e->embed_encode(eb);
-    const auto v = ptrs();
+
+  void ensure_tmp(size_t n) {
+    if (n <= tmp_cap) return;
+    for (float* p : tmp)
+      if (p) cudaFree(p);
+    tmp.assign(tp, nullptr);
+    tmp_cap = n;
+    for (int r = 0; r < tp; ++r) EXG_CUDA(cudaMalloc(&tmp[r], sizeof(float) * tmp_cap));
+  }
+
+  // TP reduction of the pending fp32 partials of `rows` rows, then the
+  // residual update of every local member
+  void tp_reduce(const Exec& X, int rows, int d) {
+    if (tp == 1 || !any_local()) return;
+    const int64_t n = (int64_t)rows * d;
+    bool all_local = true;
+    for (int r = 0; r < tp; ++r) all_local &= X.mine(gpu(r));
+    if (all_local) {
+      std::vector<Engine*> v;
+      for (auto& e : eng) v.push_back(e.get());
+      sum_tp_parts(v, n, X.st);
+    } else {
+      ensure_tmp((size_t)n);
+      // ranks of this group other than this one
+      std::set<int> peers;
+      for (int r = 0; r < tp; ++r)
+        if (!X.mine(gpu(r))) peers.insert(X.owner(gpu(r)));
+      X.comm->group_start();
+      for (int a = 0; a < tp; ++a) {   // each local partial once to every other rank of the group
+        if (!X.mine(gpu(a))) continue;
+        for (int q : peers) X.comm->send(eng[a]->part(), sizeof(float) * n, q, X.st);
+      }
+      for (int b = 0; b < tp; ++b)     // every remote member's partial, in member order
+        if (!X.mine(gpu(b))) X.comm->recv(tmp[b], sizeof(float) * n, X.owner(gpu(b)), X.st);
+      X.comm->group_end();
+      // sum in rank order into the spare buffer of the first local member,
+      // then hand it to every local member
+      PartPtrs pp;
+      pp.n_in = tp;
+      pp.n_out = 1;
+      int first_local = -1;
+      for (int r = 0; r < tp; ++r) {
+        pp.in[r] = X.mine(gpu(r)) ? eng[r]->part() : tmp[r];
+        if (first_local < 0 && X.mine(gpu(r))) first_local = r;
+      }
+      pp.out[0] = tmp[first_local];
+      launch_sum(pp, n, X.st);
+      for (int r = 0; r < tp; ++r)
+        if (X.mine(gpu(r)))
+          EXG_CUDA(cudaMemcpyAsync(eng[r]->part(), tmp[first_local], sizeof(float) * n, cudaMemcpyDeviceToDevice,
+                                   X.st));
+    }
+    for (auto& e : eng)
+      if (e) e->finish_pending();
+  }
+
+  void encode(const Exec& X, const EncodeBatch& eb, int d) {
+    if (eb.T <= 0 || !any_local()) return;
+    for (auto& e : eng)
+      if (e) e->embed_encode(eb);
     for (int l = 0; l < l1 - l0; ++l) {
-      for (auto& e : eng) e->enc_attn_block(l, eb);
-      if (tp > 1) {
-        sum_tp_parts(v, (int64_t)eb.T * d, st);
-        for (auto& e : eng) e->finish_pending();
-      }
-      for (auto& e : eng) e->enc_ffn_block(l, eb);
-      if (tp > 1) {
-        sum_tp_parts(v, (int64_t)eb.T * d, st);
-        for (auto& e : eng) e->finish_pending();
-      }
+      for (auto& e : eng)
+        if (e) e->enc_attn_block(l, eb);
+      tp_reduce(X, eb.T, d);
+      for (auto& e : eng)
+        if (e) e->enc_ffn_block(l, eb);
+      tp_reduce(X, eb.T, d);
     }
   }
-  void decode(const DecodeBatch& db, const float* x_in, int d) {
-    if (db.B <= 0) return;
-    load_x(x_in, db.B, d);
-    for (auto& e : eng) e->embed_decode(db);
-    const auto v = ptrs();
+  void decode(const Exec& X, const DecodeBatch& db, int d) {
+    if (db.B <= 0 || !any_local()) return;
+    for (auto& e : eng)
+      if (e) e->embed_decode(db);
     for (int l = 0; l < l1 - l0; ++l) {
-      for (auto& e : eng) e->dec_attn_block(l, db);
-      if (tp > 1) {
-        sum_tp_parts(v, (int64_t)db.B * d, st);
-        for (auto& e : eng) e->finish_pending();
-      }
-      for (auto& e : eng) e->dec_ffn_block(l, db);
-      if (tp > 1) {
-        sum_tp_parts(v, (int64_t)db.B * d, st);
-        for (auto& e : eng) e->finish_pending();
-      }
+      for (auto& e : eng)
+        if (e) e->dec_attn_block(l, db);
+      tp_reduce(X, db.B, d);
+      for (auto& e : eng)
+        if (e) e->dec_ffn_block(l, db);
+      tp_reduce(X, db.B, d);
     }
-    if (last) eng[0]->head_decode(db);  // every TP rank holds the same x: rank 0 runs the head
+    // every TP rank holds the same x: rank 0 of the last stage runs the head
+    if (last && eng[0]) eng[0]->head_decode(db);
   }
-  float* x_out() { return eng[0]->x(); }
 };
+
+// hidden states of `rows` rows: previous stage's TP rank 0 -> every TP rank of the next
+static void hop(const Exec& X, Stage& prev, Stage& next, int rows, int d) {
+  const size_t bytes = sizeof(float) * (size_t)rows * d;
+  for (int r = 0; r < next.tp; ++r)
+    X.xfer(prev.gpu(0), prev.eng[0] ? prev.eng[0]->x() : nullptr, next.gpu(r),
+           next.eng[r] ? next.eng[r]->x() : nullptr, bytes);
+}
 
 // ---------------------------------------------------------------------------
 // Layout: the stages of a schedule, built once per layout and cached
 // ---------------------------------------------------------------------------
 struct Layout {
   std::vector<std::unique_ptr<Stage>> enc, dec;  // WAA: encoder / decoder pipelines; RRA: dec only
+  int G = 0;                                     // GPUs of the layout
 };
 
 static std::string layout_key(const exg_schedule& s) {
   std::string k = std::to_string(s.strategy) + ":" + std::to_string(s.n_enc_gpus);
   for (int i = 0; i < s.n_stages; ++i)
-    k += "|" + std::to_string(s.stage_n_gpus[i]) + "," + std::to_string(s.stage_layer_begin[i]) + "," +
-         std::to_string(s.stage_layer_end[i]);
+    k += "|" + std::to_string(s.stage_first_gpu[i]) + "," + std::to_string(s.stage_n_gpus[i]) + "," +
+         std::to_string(s.stage_layer_begin[i]) + "," + std::to_string(s.stage_layer_end[i]);
   return k;
 }
 
@@ -146,12 +258,19 @@ struct MultiCtx::Impl {
   exg_model_spec spec;
   int device;
   cudaStream_t st = nullptr;
+  std::unique_ptr<Comm> comm;
+  int rank = 0, world = 1;
   std::map<std::string, std::unique_ptr<Layout>> layouts;
 };
 
-MultiCtx::MultiCtx(const exg_model_spec& spec, int device) : p_(new Impl) {
+MultiCtx::MultiCtx(const exg_model_spec& spec, int device, std::unique_ptr<Comm> comm) : p_(new Impl) {
   p_->spec = spec;
   p_->device = device;
+  if (comm) {
+    p_->rank = comm->rank();
+    p_->world = comm->world();
+  }
+  p_->comm = std::move(comm);
   EXG_CUDA(cudaSetDevice(device));
   EXG_CUDA(cudaStreamCreateWithFlags(&p_->st, cudaStreamNonBlocking));
 }
@@ -160,20 +279,36 @@ MultiCtx::~MultiCtx() {
   cudaSetDevice(p_->device);
   if (p_->st) cudaStreamSynchronize(p_->st);
   p_->layouts.clear();
+  p_->comm.reset();
   if (p_->st) cudaStreamDestroy(p_->st);
   delete p_;
 }
 
-static std::unique_ptr<Stage> make_stage(const exg_model_spec& spec, int device, cudaStream_t st, int l0, int l1,
+int MultiCtx::rank() const { return p_->rank; }
+int MultiCtx::world() const { return p_->world; }
+
+static Exec make_exec(const MultiCtx::Impl* p, int G) {
+  Exec X;
+  X.me = p->rank;
+  X.world = p->world;
+  X.G = G;
+  X.comm = p->comm.get();
+  X.st = p->st;
+  return X;
+}
+
+static std::unique_ptr<Stage> make_stage(const MultiCtx::Impl* p, const Exec& X, int first_gpu, int l0, int l1,
                                          int tp, bool first, bool last) {
   auto s = std::make_unique<Stage>();
   s->l0 = l0;
   s->l1 = l1;
   s->tp = tp;
+  s->first_gpu = first_gpu;
   s->first = first;
   s->last = last;
-  s->st = st;
+  s->eng.resize(tp);
   for (int r = 0; r < tp; ++r) {
+    if (!X.mine(first_gpu + r)) continue;
     EngineShard sh;
     sh.l0 = l0;
     sh.l1 = l1;
@@ -181,7 +316,7 @@ static std::unique_ptr<Stage> make_stage(const exg_model_spec& spec, int device,
     sh.tp_rank = r;
     sh.embed = first;
     sh.head = last && r == 0;
-    s->eng.push_back(std::make_unique<Engine>(spec, device, sh, st));
+    s->eng[r] = std::make_unique<Engine>(p->spec, p->device, sh, p->st);
   }
   return s;
 }
@@ -193,12 +328,19 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
   const int L = p->spec.n_dec_layers;
   auto lay = std::make_unique<Layout>();
   std::vector<int> enc_idx, dec_idx;
-  for (int i = 0; i < s.n_stages; ++i)
+  int G = 0;
+  for (int i = 0; i < s.n_stages; ++i) {
+    if (s.stage_first_gpu[i] != G) throw std::invalid_argument("schedule stages must occupy consecutive GPUs");
+    if (s.stage_n_gpus[i] < 1 || s.stage_n_gpus[i] > 8) throw std::invalid_argument("bad stage GPU count");
+    G += s.stage_n_gpus[i];
     (s.strategy != EXG_RRA && s.stage_first_gpu[i] < s.n_enc_gpus ? enc_idx : dec_idx).push_back(i);
+  }
+  if (p->world > G) throw std::invalid_argument("more ranks than GPUs in the schedule's layout");
+  lay->G = G;
   auto check_cover = [&](const std::vector<int>& idx) {
     int next = 0;
     for (int i : idx) {
-      if (s.stage_layer_begin[i] != next || s.stage_layer_end[i] <= next || s.stage_n_gpus[i] < 1)
+      if (s.stage_layer_begin[i] != next || s.stage_layer_end[i] <= next)
         throw std::invalid_argument("schedule stages must cover the layers contiguously");
       next = s.stage_layer_end[i];
     }
@@ -206,15 +348,16 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
   };
   if (s.strategy != EXG_RRA) check_cover(enc_idx);
   check_cover(dec_idx);
+  const Exec X = make_exec(p, G);
   for (size_t k = 0; k < enc_idx.size(); ++k) {
     const int i = enc_idx[k];
     if (s.stage_n_gpus[i] != 1) throw std::invalid_argument("WAA encoder stages are single-GPU");
-    lay->enc.push_back(make_stage(p->spec, p->device, p->st, s.stage_layer_begin[i], s.stage_layer_end[i], 1,
+    lay->enc.push_back(make_stage(p, X, s.stage_first_gpu[i], s.stage_layer_begin[i], s.stage_layer_end[i], 1,
                                   k == 0, false));
   }
   for (size_t k = 0; k < dec_idx.size(); ++k) {
     const int i = dec_idx[k];
-    lay->dec.push_back(make_stage(p->spec, p->device, p->st, s.stage_layer_begin[i], s.stage_layer_end[i],
+    lay->dec.push_back(make_stage(p, X, s.stage_first_gpu[i], s.stage_layer_begin[i], s.stage_layer_end[i],
                                   s.stage_n_gpus[i], k == 0, k + 1 == dec_idx.size()));
   }
   Layout* out = lay.get();
@@ -223,7 +366,7 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
 }
 
 // ---------------------------------------------------------------------------
-// shared run state: request bookkeeping, device tables, events
+// shared run state: request bookkeeping, device tables, stamps
 // ---------------------------------------------------------------------------
 namespace {
 struct Row {
@@ -238,9 +381,11 @@ struct Tables {
   bool used = false;
   void ensure(size_t n) {
     if (n <= cap) return;
+    if (used) EXG_CUDA(cudaEventSynchronize(ev));
     if (dev) cudaFree(dev);
     if (host) cudaFreeHost(host);
     cap = n;
+    used = false;
     EXG_CUDA(cudaMalloc(&dev, cap * sizeof(int32_t)));
     EXG_CUDA(cudaMallocHost(&host, cap * sizeof(int32_t)));
     if (!ev) EXG_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -269,40 +414,49 @@ struct RunState {
   int64_t total_out = 0;
   int max_in = 1, max_ctx = 1;
   int32_t* d_out = nullptr;
-  std::vector<cudaEvent_t> evs;
-  std::vector<int> ev_kind, ev_tok;
+  uint64_t* d_stamps = nullptr;
+  int n_stamps = 0, cap_stamps = 0;
   std::vector<int> admit_ev, done_ev;
   cudaStream_t st;
   int64_t decode_iters = 0, encode_phases = 0, batch_sum = 0;
   ~RunState() {
-    for (auto e : evs) cudaEventDestroy(e);
+    if (st) cudaStreamSynchronize(st);
     if (d_out) cudaFree(d_out);
+    if (d_stamps) cudaFree(d_stamps);
   }
-  int record(int kind, int toks) {
-    cudaEvent_t e;
-    EXG_CUDA(cudaEventCreate(&e));
-    EXG_CUDA(cudaEventRecord(e, st));
-    evs.push_back(e);
-    ev_kind.push_back(kind);
-    ev_tok.push_back(toks);
-    return (int)evs.size() - 1;
+  // stamp index k, written (on this rank) only when `mine`
+  int record(bool mine) {
+    const int k = n_stamps++;
+    if (k >= cap_stamps) throw std::logic_error("stamp capacity exceeded");
+    if (mine) {
+      stamp_kernel<<<1, 1, 0, st>>>(d_stamps + k);
+      EXG_CHECK_LAUNCH();
+    }
+    return k;
   }
 };
 
-void validate_requests(RunState& R, const Dims& D) {
+void validate_requests(RunState& R, int V, int max_pos) {
   R.base.assign(R.n + 1, 0);
   for (int r = 0; r < R.n; ++r) {
     const exg_request& q = R.reqs[r];
     if (q.input_len < 1 || q.output_len < 1 || !q.input_ids) throw std::invalid_argument("request lengths must be >= 1");
-    if (q.input_len + q.output_len > D.max_pos) throw std::invalid_argument("input_len + output_len > max_pos");
+    if (q.input_len + q.output_len > max_pos) throw std::invalid_argument("input_len + output_len > max_pos");
     for (int j = 0; j < q.input_len; ++j)
-      if (q.input_ids[j] < 0 || q.input_ids[j] >= D.V) throw std::invalid_argument("token id out of range");
+      if (q.input_ids[j] < 0 || q.input_ids[j] >= V) throw std::invalid_argument("token id out of range");
     R.max_in = std::max(R.max_in, q.input_len);
     R.max_ctx = std::max(R.max_ctx, q.input_len + q.output_len);
     R.base[r + 1] = R.base[r] + q.output_len;
   }
   R.total_out = R.base[R.n];
-  EXG_CUDA(cudaMalloc(&R.d_out, sizeof(int32_t) * std::max<int64_t>(R.total_out, 1)));
+  const size_t nout = (size_t)std::max<int64_t>(R.total_out, 1);
+  EXG_CUDA(cudaMalloc(&R.d_out, sizeof(int32_t) * nout));
+  EXG_CUDA(cudaMemsetAsync(R.d_out, 0, sizeof(int32_t) * nout, R.st));
+  // one stamp per loop pass (phase start) and per decode iteration, + start;
+  // both are bounded by the number of output tokens + requests
+  R.cap_stamps = (int)std::min<int64_t>(2 * (R.total_out + R.n) + 16, (int64_t)1 << 30);
+  EXG_CUDA(cudaMalloc(&R.d_stamps, sizeof(uint64_t) * R.cap_stamps));
+  EXG_CUDA(cudaMemsetAsync(R.d_stamps, 0, sizeof(uint64_t) * R.cap_stamps, R.st));
 }
 
 // packed encode tables for requests [r0, r0+k) with the given slots
@@ -380,27 +534,127 @@ std::vector<std::pair<int, int>> chunks(int n, int parts) {
   return out;
 }
 
-void finish_stats(RunState& R, Engine& any, int32_t* out_tokens, double* out_latency, exg_run_stats* stats) {
-  EXG_CUDA(cudaStreamSynchronize(R.st));
-  if (out_tokens) EXG_CUDA(cudaMemcpy(out_tokens, R.d_out, sizeof(int32_t) * R.total_out, cudaMemcpyDeviceToHost));
-  int32_t err = 0;
-  EXG_CUDA(cudaMemcpy(&err, any.err_flag(), sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (err) throw std::runtime_error("NaN logit encountered (T7)");
-  const int nev = (int)R.evs.size();
-  std::vector<double> t(nev, 0.0);
-  for (int k = 1; k < nev; ++k) {
-    float ms = 0.f;
-    EXG_CUDA(cudaEventElapsedTime(&ms, R.evs[0], R.evs[k]));
-    t[k] = ms * 1e-3;
+// optional fp32 logits dump (exg_run_opts.logits_out / dump_mask), written
+// by the rank holding the LM head
+struct Dump {
+  const exg_run_opts* opts = nullptr;
+  std::vector<int64_t> base;
+  bool on() const { return opts && opts->logits_out && opts->dump_mask; }
+};
+
+Dump make_dump(const RunState& R, const exg_run_opts* opts) {
+  Dump d;
+  d.opts = opts;
+  d.base.assign(R.n + 1, 0);
+  if (d.on())
+    for (int r = 0; r < R.n; ++r) d.base[r + 1] = d.base[r] + (opts->dump_mask[r] ? R.reqs[r].output_len : 0);
+  return d;
+}
+
+// one decode iteration of `rows` through the pipeline in n_mb micro-batches
+void decode_pipeline(const Exec& X, RunState& R, std::vector<std::unique_ptr<Stage>>& pipe, std::vector<Tables>& tabs,
+                     int& ti, const std::vector<Row>& rows, int n_mb, int d, const Dump& dump) {
+  const int B = (int)rows.size();
+  for (const auto& mb : chunks(B, n_mb)) {
+    Tables& tb = tabs[ti++ % tabs.size()];
+    DecodeBatch db = build_decode(R, tb, rows, mb.first, mb.second, R.st);
+    for (size_t k = 0; k < pipe.size(); ++k) {
+      if (k > 0) hop(X, *pipe[k - 1], *pipe[k], mb.second, d);
+      pipe[k]->decode(X, db, d);
+    }
+    Engine* head = pipe.back()->eng[0].get();
+    if (dump.on() && head) {
+      const int V = head->dims().V;
+      for (int i = 0; i < mb.second; ++i) {
+        const Row& rw = rows[mb.first + i];
+        if (!dump.opts->dump_mask[rw.req]) continue;
+        float* dst = dump.opts->logits_out + (dump.base[rw.req] + rw.emitted) * (int64_t)V;
+        EXG_CUDA(cudaMemcpyAsync(dst, head->logits() + (int64_t)i * V, sizeof(float) * V, cudaMemcpyDeviceToHost,
+                                 R.st));
+      }
+    }
   }
+}
+
+// the last stage's ids become the first stage's next inputs (K15)
+void return_tokens(const Exec& X, std::vector<std::unique_ptr<Stage>>& pipe, int slots) {
+  Stage& Ls = *pipe.back();
+  Stage& Fs = *pipe.front();
+  for (int r = 0; r < Fs.tp; ++r)
+    X.xfer(Ls.gpu(0), Ls.eng[0] ? Ls.eng[0]->last_tok() : nullptr, Fs.gpu(r),
+           Fs.eng[r] ? Fs.eng[r]->last_tok() : nullptr, sizeof(int32_t) * slots);
+}
+
+void retire(RunState& R, std::vector<Row>& active, std::vector<int>& free_slots, int ev) {
+  int w = 0;
+  for (size_t i = 0; i < active.size(); ++i) {
+    Row rw = active[i];
+    rw.emitted += 1;
+    rw.pos += 1;
+    if (rw.emitted == R.reqs[rw.req].output_len) {
+      R.done_ev[rw.req] = ev;
+      free_slots.push_back(rw.slot);
+    } else {
+      active[w++] = rw;
+    }
+  }
+  active.resize(w);
+}
+
+// results to rank 0: the output tokens from the head's rank, the stamps from
+// every rank (each stamp is written by exactly one rank, the others hold 0)
+void finish(const Exec& X, RunState& R, Stage& head_stage, int32_t* out_tokens, double* out_latency,
+            exg_run_stats* stats) {
+  const int ho = X.owner(head_stage.gpu(0));
+  std::vector<uint64_t> stamps(R.n_stamps, 0);
+  auto merge = [&](const uint64_t* dev) {
+    std::vector<uint64_t> h(R.n_stamps);
+    EXG_CUDA(cudaMemcpyAsync(h.data(), dev, sizeof(uint64_t) * R.n_stamps, cudaMemcpyDeviceToHost, R.st));
+    EXG_CUDA(cudaStreamSynchronize(R.st));
+    for (int k = 0; k < R.n_stamps; ++k) stamps[k] = std::max(stamps[k], h[k]);
+  };
+  if (X.world > 1) {
+    if (ho != 0) {
+      if (X.me == ho) X.comm->send(R.d_out, sizeof(int32_t) * R.total_out, 0, R.st);
+      if (X.me == 0) X.comm->recv(R.d_out, sizeof(int32_t) * R.total_out, ho, R.st);
+    }
+    uint64_t* tmp = nullptr;
+    if (X.me == 0) EXG_CUDA(cudaMalloc(&tmp, sizeof(uint64_t) * std::max(1, R.n_stamps)));
+    for (int q = 1; q < X.world; ++q) {
+      if (X.me == q) X.comm->send(R.d_stamps, sizeof(uint64_t) * R.n_stamps, 0, R.st);
+      if (X.me == 0) {
+        X.comm->recv(tmp, sizeof(uint64_t) * R.n_stamps, q, R.st);
+        merge(tmp);
+      }
+    }
+    if (tmp) {
+      EXG_CUDA(cudaStreamSynchronize(R.st));
+      cudaFree(tmp);
+    }
+  }
+  EXG_CUDA(cudaStreamSynchronize(R.st));
+  if (Engine* head = head_stage.eng[0].get()) {
+    int32_t err = 0;
+    EXG_CUDA(cudaMemcpy(&err, head->err_flag(), sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (err) throw std::runtime_error("NaN logit encountered (T7)");
+  }
+  if (X.me != 0) {
+    if (stats) std::memset(stats, 0, sizeof(*stats));
+    return;
+  }
+  if (out_tokens) EXG_CUDA(cudaMemcpy(out_tokens, R.d_out, sizeof(int32_t) * R.total_out, cudaMemcpyDeviceToHost));
+  merge(R.d_stamps);
+  const uint64_t t0 = stamps[0];   // run start
+  auto sec = [&](int k) { return stamps[k] >= t0 ? (double)(stamps[k] - t0) * 1e-9 : 0.0; };
   std::vector<double> lat(R.n);
   for (int r = 0; r < R.n; ++r) {
-    lat[r] = t[R.done_ev[r]] - t[R.admit_ev[r]];
+    lat[r] = sec(R.done_ev[r]) - sec(R.admit_ev[r]);
     if (out_latency) out_latency[r] = lat[r];
   }
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
-    const double wall = t[nev - 1];
+    double wall = 0;
+    for (int k = 0; k < R.n_stamps; ++k) wall = std::max(wall, sec(k));
     stats->wall_s = wall;
     stats->out_tokens = R.total_out;
     stats->decode_iters = R.decode_iters;
@@ -421,75 +675,6 @@ void finish_stats(RunState& R, Engine& any, int32_t* out_tokens, double* out_lat
     stats->mean_decode_batch = R.decode_iters ? (double)R.batch_sum / R.decode_iters : 0;
   }
 }
-
-// optional fp32 logits dump (exg_run_opts.logits_out / dump_mask)
-struct Dump {
-  const exg_run_opts* opts = nullptr;
-  std::vector<int64_t> base;
-  bool on() const { return opts && opts->logits_out && opts->dump_mask; }
-};
-
-// run the decode pipeline on `rows` (micro-batches through every stage)
-void decode_pipeline(RunState& R, std::vector<std::unique_ptr<Stage>>& pipe, std::vector<Tables>& tabs,
-                     const std::vector<Row>& rows, int n_mb, int d, const Dump& dump) {
-  const int B = (int)rows.size();
-  const auto mbs = chunks(B, n_mb);
-  int ti = 0;
-  for (const auto& mb : mbs) {
-    Tables& tb = tabs[ti++ % tabs.size()];
-    DecodeBatch db = build_decode(R, tb, rows, mb.first, mb.second, R.st);
-    const float* x = nullptr;
-    for (auto& s : pipe) {
-      s->decode(db, x, d);
-      x = s->x_out();
-    }
-    if (dump.on()) {
-      Engine* head = pipe.back()->eng[0].get();
-      const int V = head->dims().V;
-      for (int i = 0; i < mb.second; ++i) {
-        const Row& rw = rows[mb.first + i];
-        if (!dump.opts->dump_mask[rw.req]) continue;
-        float* dst = dump.opts->logits_out + (dump.base[rw.req] + rw.emitted) * (int64_t)V;
-        EXG_CUDA(cudaMemcpyAsync(dst, head->logits() + (int64_t)i * V, sizeof(float) * V, cudaMemcpyDeviceToHost,
-                                 R.st));
-      }
-    }
-  }
-}
-
-Dump make_dump(const RunState& R, const exg_run_opts* opts) {
-  Dump d;
-  d.opts = opts;
-  d.base.assign(R.n + 1, 0);
-  if (d.on())
-    for (int r = 0; r < R.n; ++r) d.base[r + 1] = d.base[r] + (opts->dump_mask[r] ? R.reqs[r].output_len : 0);
-  return d;
-}
-
-// the last stage's ids become stage 0's next inputs (K15)
-void return_tokens(std::vector<std::unique_ptr<Stage>>& pipe, int slots, cudaStream_t st) {
-  Engine* head = pipe.back()->eng[0].get();
-  for (auto& e : pipe.front()->eng)
-    if (e.get() != head)
-      EXG_CUDA(cudaMemcpyAsync(e->last_tok(), head->last_tok(), sizeof(int32_t) * slots, cudaMemcpyDeviceToDevice,
-                               st));
-}
-
-void retire(RunState& R, std::vector<Row>& active, std::vector<int>& free_slots, int ev) {
-  int w = 0;
-  for (size_t i = 0; i < active.size(); ++i) {
-    Row rw = active[i];
-    rw.emitted += 1;
-    rw.pos += 1;
-    if (rw.emitted == R.reqs[rw.req].output_len) {
-      R.done_ev[rw.req] = ev;
-      free_slots.push_back(rw.slot);
-    } else {
-      active[w++] = rw;
-    }
-  }
-  active.resize(w);
-}
 }  // namespace
 
 // ---------------------------------------------------------------------------
@@ -499,20 +684,24 @@ void retire(RunState& R, std::vector<Row>& active, std::vector<int>& free_slots,
 static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s, const exg_request* reqs, int n,
                           int32_t* out_tokens, double* out_latency, exg_run_stats* stats, const exg_run_opts* opts) {
   auto& pipe = lay->dec;
-  const Dims& D = pipe.front()->eng[0]->dims();
+  const Exec X = make_exec(p, lay->G);
+  const int d = p->spec.d_model;
   RunState R;
   R.reqs = reqs;
   R.n = n;
   R.st = p->st;
-  validate_requests(R, D);
+  validate_requests(R, p->spec.vocab, p->spec.max_pos);
   const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : R.max_ctx;
   if (slot_ctx < R.max_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
   const int B_D = s.b_d, B_E = s.b_e, P = (int)pipe.size();
+  if (B_E < 1 || B_D < B_E || s.n_d < 1) throw std::invalid_argument("RRA needs 1 <= B_E <= B_D, N_D >= 1");
   for (auto& st : pipe)
-    for (auto& e : st->eng) {
-      e->ensure_kv(B_D, slot_ctx);
-      e->ensure_workspace(B_E * (R.max_in - 1), B_D);
-    }
+    for (auto& e : st->eng)
+      if (e) {
+        e->ensure_kv(B_D, slot_ctx);
+        e->ensure_workspace(B_E * (R.max_in - 1), B_D);
+      }
+  const bool first_mine = X.mine(pipe.front()->gpu(0)), head_mine = X.mine(pipe.back()->gpu(0));
   std::vector<Tables> tabs(8);
   const Dump dump = make_dump(R, opts);
   std::vector<int> free_slots(B_D);
@@ -521,10 +710,10 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   R.admit_ev.assign(n, -1);
   R.done_ev.assign(n, -1);
   int next_req = 0, ti = 0;
-  R.record(0, 0);
+  R.record(first_mine);
   while (next_req < n || !active.empty()) {
     const int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
-    const int ev_phase = R.record(0, 0);
+    const int ev_phase = R.record(first_mine);
     if (admit > 0) {
       std::vector<int> slots(admit);
       for (int k = 0; k < admit; ++k) {
@@ -534,11 +723,11 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         active.push_back(Row{next_req + k, slots[k], q.input_len - 1, 0});
         R.admit_ev[next_req + k] = ev_phase;
       }
-      // x[n-1] of every admitted request -> last_tok[slot] on the first stage
       for (const auto& mb : chunks(admit, P)) {
         Tables& tb = tabs[ti++ % tabs.size()];
         std::vector<int32_t> last;
         EncodeBatch eb = build_encode(R, tb, next_req + mb.first, mb.second, slots.data() + mb.first, R.st, &last);
+        // x[n-1] of every admitted request -> last_tok[slot] on the first stage
         Tables& tl = tabs[ti++ % tabs.size()];
         tl.ensure(2 * last.size() + 2);
         int32_t* h = tl.begin();
@@ -548,27 +737,25 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         }
         tl.upload(2 * last.size(), R.st);
         for (auto& e : pipe.front()->eng)
-          set_last_tokens(e->last_tok(), tl.dev, tl.dev + last.size(), (int)last.size(), R.st);
-        const float* x = nullptr;
-        for (auto& stg : pipe) {
-          stg->encode(eb, x, D.d);
-          x = stg->x_out();
+          if (e) set_last_tokens(e->last_tok(), tl.dev, tl.dev + last.size(), (int)last.size(), R.st);
+        for (size_t k = 0; k < pipe.size(); ++k) {
+          if (k > 0) hop(X, *pipe[k - 1], *pipe[k], eb.T, d);
+          pipe[k]->encode(X, eb, d);
         }
       }
       next_req += admit;
       ++R.encode_phases;
     }
-    R.record(1, 0);
     for (int u = 0; u < s.n_d && !active.empty(); ++u) {
-      decode_pipeline(R, pipe, tabs, active, P, D.d, dump);
-      return_tokens(pipe, B_D, R.st);
-      const int ev = R.record(2, (int)active.size());
+      decode_pipeline(X, R, pipe, tabs, ti, active, P, d, dump);
+      return_tokens(X, pipe, B_D);
+      const int ev = R.record(head_mine);
       ++R.decode_iters;
       R.batch_sum += (int64_t)active.size();
       retire(R, active, free_slots, ev);
     }
   }
-  finish_stats(R, *pipe.back()->eng[0], out_tokens, out_latency, stats);
+  finish(X, R, *pipe.back(), out_tokens, out_latency, stats);
 }
 
 // ---------------------------------------------------------------------------
@@ -582,12 +769,13 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
                           int32_t* out_tokens, double* out_latency, exg_run_stats* stats, const exg_run_opts* opts) {
   auto& enc = lay->enc;
   auto& dec = lay->dec;
-  const Dims& D = dec.front()->eng[0]->dims();
+  const Exec X = make_exec(p, lay->G);
+  const int d = p->spec.d_model, H = p->spec.n_heads, dh = p->spec.d_head;
   RunState R;
   R.reqs = reqs;
   R.n = n;
   R.st = p->st;
-  validate_requests(R, D);
+  validate_requests(R, p->spec.vocab, p->spec.max_pos);
   const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : R.max_ctx;
   if (slot_ctx < R.max_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
   const int B_D = s.b_d, B_E = s.b_e;
@@ -595,43 +783,47 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   const int M = s.b_m > 0 ? std::max(1, (B_D + s.b_m - 1) / s.b_m) : 1;
   const int enc_ctx = std::max(1, R.max_in);
   for (auto& st : enc)
-    for (auto& e : st->eng) {
-      e->ensure_kv(B_E, enc_ctx);
-      e->ensure_workspace(B_E * (R.max_in - 1), B_E);
-    }
+    for (auto& e : st->eng)
+      if (e) {
+        e->ensure_kv(B_E, enc_ctx);
+        e->ensure_workspace(B_E * (R.max_in - 1), B_E);
+      }
   for (auto& st : dec)
-    for (auto& e : st->eng) {
-      e->ensure_kv(B_D, slot_ctx);
-      e->ensure_workspace(1, B_D);
-    }
+    for (auto& e : st->eng)
+      if (e) {
+        e->ensure_kv(B_D, slot_ctx);
+        e->ensure_workspace(1, B_D);
+      }
+  const bool first_mine = X.mine(enc.front()->gpu(0)), head_mine = X.mine(dec.back()->gpu(0));
   std::vector<Tables> tabs(8);
   const Dump dump = make_dump(R, opts);
+  // handoff row table; packed-message staging for transfers between ranks
   HandoffRow* d_hrows = nullptr;
   EXG_CUDA(cudaMalloc(&d_hrows, sizeof(HandoffRow) * B_E));
   HandoffRow* h_hrows = nullptr;
   EXG_CUDA(cudaMallocHost(&h_hrows, sizeof(HandoffRow) * B_E));
+  bf16* stage_buf = nullptr;
+  size_t stage_cap = 0;
   std::vector<int> free_slots(B_D);
   for (int i = 0; i < B_D; ++i) free_slots[i] = B_D - 1 - i;
   std::vector<Row> active;
   R.admit_ev.assign(n, -1);
   R.done_ev.assign(n, -1);
   int next_req = 0, pend_r0 = -1, pend_k = 0, pend_ev = -1, ti = 0;
-  R.record(0, 0);
+  R.record(first_mine);
   while (next_req < n || pend_k > 0 || !active.empty()) {
     // encoder: keep one encoded batch ready (encoder slots 0..k-1)
     if (pend_k == 0 && next_req < n) {
       const int k = std::min(B_E, n - next_req);
-      pend_ev = R.record(0, 0);
+      pend_ev = R.record(first_mine);
       std::vector<int> eslots(k);
       for (int j = 0; j < k; ++j) eslots[j] = j;
       Tables& tb = tabs[ti++ % tabs.size()];
       EncodeBatch eb = build_encode(R, tb, next_req, k, eslots.data(), R.st, nullptr);
-      const float* x = nullptr;
-      for (auto& stg : enc) {
-        stg->encode(eb, x, D.d);
-        x = stg->x_out();
+      for (size_t q = 0; q < enc.size(); ++q) {
+        if (q > 0) hop(X, *enc[q - 1], *enc[q], eb.T, d);
+        enc[q]->encode(X, eb, d);
       }
-      R.record(1, 0);
       pend_r0 = next_req;
       pend_k = k;
       next_req += k;
@@ -640,29 +832,56 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
     // handoff + merge at an iteration boundary when the decoder has room
     if (pend_k > 0 && (int)free_slots.size() >= pend_k) {
       std::vector<int> dslots(pend_k);
+      int64_t rows_len = 0;
+      // the previous handoff's table upload must be done before h_hrows is rewritten
+      EXG_CUDA(cudaStreamSynchronize(R.st));
       for (int j = 0; j < pend_k; ++j) {
         dslots[j] = free_slots.back();
         free_slots.pop_back();
         const exg_request& q = reqs[pend_r0 + j];
-        h_hrows[j] = HandoffRow{j, dslots[j], q.input_len - 1};
+        h_hrows[j] = HandoffRow{j, dslots[j], q.input_len - 1, rows_len};
+        rows_len += q.input_len - 1;
         active.push_back(Row{pend_r0 + j, dslots[j], q.input_len - 1, 0});
         R.admit_ev[pend_r0 + j] = pend_ev;
       }
       EXG_CUDA(cudaMemcpyAsync(d_hrows, h_hrows, sizeof(HandoffRow) * pend_k, cudaMemcpyHostToDevice, R.st));
+      const size_t need = (size_t)rows_len * H * dh;   // largest slice (a TP-1 decoder stage)
+      if (X.world > 1 && need > stage_cap) {
+        EXG_CUDA(cudaStreamSynchronize(R.st));
+        if (stage_buf) cudaFree(stage_buf);
+        stage_cap = need;
+        EXG_CUDA(cudaMalloc(&stage_buf, sizeof(bf16) * stage_cap));
+      }
       for (auto& es : enc) {
-        Engine* src = es->eng[0].get();
         for (int l = es->l0; l < es->l1; ++l)
           for (auto& ds : dec) {
             if (l < ds->l0 || l >= ds->l1) continue;
+            const int Hd = H / ds->tp;
             for (int r = 0; r < ds->tp; ++r) {
+              const int ge = es->gpu(0), gd = ds->gpu(r);
+              const bool src_mine = X.mine(ge), dst_mine = X.mine(gd);
+              if (!src_mine && !dst_mine) continue;
+              Engine* src = es->eng[0].get();
               Engine* dst = ds->eng[r].get();
-              const int Hd = dst->dims().Hl;
+              const size_t bytes = sizeof(bf16) * (size_t)rows_len * Hd * dh;
               for (int kv = 0; kv < 2; ++kv) {
-                const bf16* sp = kv ? src->vc(l - es->l0) : src->kc(l - es->l0);
-                bf16* dp = kv ? dst->vc(l - ds->l0) : dst->kc(l - ds->l0);
-                kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp, dp, d_hrows, pend_k, D.H, r * Hd, Hd, enc_ctx,
-                                                                 slot_ctx, D.dh);
-                EXG_CHECK_LAUNCH();
+                const bf16* sp_ = src ? (kv ? src->vc(l - es->l0) : src->kc(l - es->l0)) : nullptr;
+                bf16* dp = dst ? (kv ? dst->vc(l - ds->l0) : dst->kc(l - ds->l0)) : nullptr;
+                if (src_mine && dst_mine) {
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, dp, d_hrows, pend_k, H, r * Hd, Hd, enc_ctx,
+                                                                   slot_ctx, dh, 0);
+                  EXG_CHECK_LAUNCH();
+                } else if (src_mine) {
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, stage_buf, d_hrows, pend_k, H, r * Hd, Hd,
+                                                                   enc_ctx, slot_ctx, dh, 1);
+                  EXG_CHECK_LAUNCH();
+                  p->comm->send(stage_buf, bytes, X.owner(gd), R.st);
+                } else {
+                  p->comm->recv(stage_buf, bytes, X.owner(ge), R.st);
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(stage_buf, dp, d_hrows, pend_k, H, r * Hd, Hd,
+                                                                   enc_ctx, slot_ctx, dh, 2);
+                  EXG_CHECK_LAUNCH();
+                }
               }
             }
           }
@@ -677,19 +896,21 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         h[pend_k + j] = q.input_ids[q.input_len - 1];
       }
       tl.upload(2 * pend_k, R.st);
-      for (auto& e : dec.front()->eng) set_last_tokens(e->last_tok(), tl.dev, tl.dev + pend_k, pend_k, R.st);
-      // the handoff must finish reading encoder KV before the next encode
+      for (auto& e : dec.front()->eng)
+        if (e) set_last_tokens(e->last_tok(), tl.dev, tl.dev + pend_k, pend_k, R.st);
       pend_k = 0;
     }
     if (active.empty()) continue;
-    decode_pipeline(R, dec, tabs, active, M, D.d, dump);
-    return_tokens(dec, B_D, R.st);
-    const int ev = R.record(2, (int)active.size());
+    decode_pipeline(X, R, dec, tabs, ti, active, M, d, dump);
+    return_tokens(X, dec, B_D);
+    const int ev = R.record(head_mine);
     ++R.decode_iters;
     R.batch_sum += (int64_t)active.size();
     retire(R, active, free_slots, ev);
   }
-  finish_stats(R, *dec.back()->eng[0], out_tokens, out_latency, stats);
+  finish(X, R, *dec.back(), out_tokens, out_latency, stats);
+  EXG_CUDA(cudaStreamSynchronize(R.st));
+  if (stage_buf) cudaFree(stage_buf);
   cudaFree(d_hrows);
   cudaFreeHost(h_hrows);
 }

@@ -110,3 +110,59 @@ def test_layout_validation(env):
     too_many = L.make_schedule(X.EXG_RRA, 4, 8, [(0, 8, 0, 1), (8, 1, 1, 2)], n_d=6)
     with pytest.raises(X.ExgError):
         multi.run(too_many, reqs)
+
+
+# ---------------------------------------------------------------------------
+# multi-rank executor: `world` rank contexts (threads of this process on the
+# one GPU, device-copy transport in place of NCCL), every GPU of the layout
+# owned by rank g*world/G.  Same arithmetic in the same order as the
+# single-rank run of the same layout => bit-identical ids and logits.
+# ---------------------------------------------------------------------------
+RANK_CASES = [
+    # (name, strategy, b_e, b_d, b_m, n_enc, layout, tp_degree, world)
+    ("pp2_w2", "rra", 4, 8, 0, 0, [(0, 1, 0, 1), (1, 1, 1, 2)], 1, 2),
+    ("tp2_split_w2", "rra", 4, 8, 0, 0, [(0, 2, 0, 2)], 2, 2),
+    ("tp2_then_single_w2", "rra", 4, 8, 0, 0, [(0, 2, 0, 1), (2, 1, 1, 2)], 2, 2),
+    ("single_then_tp2_w3", "rra", 4, 8, 0, 0, [(0, 1, 0, 1), (1, 2, 1, 2)], 2, 3),
+    ("waa_enc_dec_w2", "waa", 2, 8, 0, 1, [(0, 1, 0, 2), (1, 1, 0, 2)], 1, 2),
+    ("waa_dec_pipeline_w2", "waa", 3, 8, 4, 1, [(0, 1, 0, 2), (1, 1, 0, 1), (2, 1, 1, 2)], 1, 2),
+    ("waa_enc_pipeline_w3", "waa", 1, 5, 2, 2, [(0, 1, 0, 1), (1, 1, 1, 2), (2, 1, 0, 2)], 1, 3),
+    ("waa_dec_tp_w4", "waa", 2, 8, 4, 1, [(0, 1, 0, 2), (1, 2, 0, 1), (3, 1, 1, 2)], 2, 4),
+]
+
+
+@pytest.mark.parametrize("case", RANK_CASES, ids=[c[0] for c in RANK_CASES])
+def test_multi_rank_bit_identical_to_single_rank(env, case):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    name, strat, b_e, b_d, b_m, n_enc, layout, tp, world = case
+    strategy = X.EXG_RRA if strat == "rra" else X.EXG_WAA_C
+    tp_gpus = sum(g[1] for g in layout if g[1] > 1)
+    s = L.make_schedule(strategy, b_e, b_d, layout, n_d=6, b_m=b_m, n_enc_gpus=n_enc, tp_degree=tp, tp_gpus=tp_gpus)
+    ref_t, _, _, ref_l = multi.run(s, reqs, dump=range(len(reqs)))
+    from workload import weight_seed
+    group = X.local_group(multi.spec, weight_seed(1), world, X.cluster_spec(8))
+    res = X.run_group(group, s, reqs, dump=range(len(reqs)))
+    toks, lat, st, lg = res[0]
+    assert toks == ref_t
+    for r in range(len(reqs)):
+        assert np.array_equal(lg[r], ref_l[r]) or not np.any(lg[r]), r   # logits live on the LM head's rank
+    head_rank = max(range(world), key=lambda q: np.count_nonzero(res[q][3][0]))
+    for r in range(len(reqs)):
+        assert np.array_equal(res[head_rank][3][r], ref_l[r]), r
+    assert st["out_tokens"] == sum(q.output_len for q in reqs)
+    assert np.all(lat > 0) and st["wall_s"] >= lat.max()
+    if tp == 1:
+        assert toks == base_t
+    for c in group:
+        c.close()
+
+
+def test_multi_rank_errors(env):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    from workload import weight_seed
+    group = X.local_group(multi.spec, weight_seed(1), 3, X.cluster_spec(8))
+    s = L.make_schedule(X.EXG_RRA, 4, 8, [(0, 1, 0, 1), (1, 1, 1, 2)], n_d=6)   # 2 GPUs < 3 ranks
+    with pytest.raises(X.ExgError):
+        X.run_group(group, s, reqs)
+    for c in group:
+        c.close()
