@@ -132,6 +132,27 @@ def cpu_cores():
         return os.cpu_count()
 
 
+# ---- multi-rank host logic (weak scaling: independent replicas) ------------
+def rank_request_seed(rank: int) -> int:
+    """Each rank draws its own requests of the same workload (weak scaling)."""
+    return 0xE6E1_0000 + CONFIG_NO + 1000 * rank
+
+
+def reduce_over_ranks(v: float, op: str, dist=None, device: str = "cuda") -> float:
+    """max / sum of a scalar over the ranks of the default process group."""
+    if dist is None:
+        return v
+    import torch
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def job_throughput(tokens: float, seconds: float, dist=None, device: str = "cuda") -> float:
+    """Whole-job metric: the tokens every rank produced / the slowest rank's time."""
+    return reduce_over_ranks(tokens, "sum", dist, device) / reduce_over_ranks(seconds, "max", dist, device)
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle (CPU, float64, bf16-emulating KV loop) on
     a bounded sample of the workload; rank 0 only."""
@@ -198,18 +219,10 @@ def main():
             dist.barrier()
 
     def max_over_ranks(v):
-        if not dist:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return reduce_over_ranks(v, "max", dist)
 
     def sum_over_ranks(v):
-        if not dist:
-            return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.SUM)
-        return float(t.item())
+        return reduce_over_ranks(v, "sum", dist)
 
     spec = MODELS[MODEL]
     d = task_dists(TASK)
@@ -256,7 +269,7 @@ def main():
             scheds[name] = None
     t_sched = time.perf_counter() - t0
 
-    reqs = make_requests(args.requests, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E1_0000 + CONFIG_NO + 1000 * rank)
+    reqs = make_requests(args.requests, d.pmf_in, d.pmf_out, spec.vocab, rank_request_seed(rank))
     slot_ctx = len(d.pmf_in) + len(d.pmf_out)
     h2d = sum((r.input_len - 1) * 12 + 16 + 16 * r.output_len for r in reqs)
     d2h = sum(4 * r.output_len for r in reqs)
