@@ -309,8 +309,6 @@ exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* r
     if (n < 1) throw std::invalid_argument("empty request batch");
     EXG_CUDA(cudaSetDevice(ctx->device));
     if (ctx->multi) {
-      if (ctx->spec.arch == EXG_ARCH_T5)
-        return fail(EXG_E_INFEASIBLE, "encoder-decoder models: multi-GPU layouts are not built yet");
       int gpus = 0;
       for (int k = 0; k < sched->n_stages && k < EXG_MAX_STAGES; ++k) gpus += sched->stage_n_gpus[k];
       if (gpus > ctx->cluster.n_gpus) return fail(EXG_E_INFEASIBLE, "schedule needs more GPUs than the cluster has");

@@ -133,8 +133,12 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
   t5_ = s.arch == EXG_ARCH_T5;
   if (t5_) {
     if (s.n_enc_layers != s.n_dec_layers) throw std::invalid_argument("T5: n_enc_layers must equal n_dec_layers");
-    if (shard.tp != 1 || shard.l0 != 0 || (shard.l1 >= 0 && shard.l1 != s.n_dec_layers) || !shard.embed || !shard.head)
-      throw std::invalid_argument("T5: sharded layouts are not built yet (single-GPU engine only)");
+    if (shard.tp != 1) throw std::invalid_argument("T5: tensor-parallel shards are not built yet");
+    if (shard.t5_role == 0 &&
+        (shard.l0 != 0 || (shard.l1 >= 0 && shard.l1 != s.n_dec_layers) || !shard.embed || !shard.head))
+      throw std::invalid_argument("T5: pipelines hold encoder and decoder layers on separate WAA GPU sets only");
+    if (shard.t5_role == 1 && shard.head) throw std::invalid_argument("T5 encoder-side shards hold no LM head");
+    if (shard.t5_role < 0 || shard.t5_role > 2) throw std::invalid_argument("bad T5 role");
   } else if (s.n_enc_layers != 0) {
     throw std::invalid_argument("decoder-only architectures have no encoder layers");
   }
@@ -257,11 +261,17 @@ void Engine::gen_weights() {
 // the first encoder / decoder layer slots, encoder final norm = (slot 0, lnx_g)
 void Engine::gen_weights_t5() {
   const size_t d = D.d, in = D.inner, f = D.ff;
+  const int role = S_.t5_role, nl = n_layers();
+  const bool has_enc = role != 2, has_dec = role != 1;
+  const bool enc_last = role == 0 || (role == 1 && S_.enc_last);
+  const int n_xproj = (role == 1 && S_.enc_last) ? D.L : 0;
   auto al = [](size_t n) { return (n * 2 + 255) & ~size_t(255); };
   auto bl = [&](size_t rows, size_t K) { return al((size_t)blocked_elems(rows, K)); };
   const size_t enc_layer = al(d) * 2 + bl(3 * in, d) + bl(d, in) + bl(f, d) + bl(d, f);
   const size_t dec_layer = enc_layer + al(d) + bl(in, d) + bl(2 * in, d) + bl(d, in);
-  wbytes_ = bl(D.V, d) + 2 * al(d) + 2 * al((size_t)T5_BUCKETS * D.H) + D.L * (enc_layer + dec_layer);
+  const bool need_tok = S_.embed || S_.head;
+  wbytes_ = (need_tok ? bl(D.V, d) : 0) + 2 * al(d) + 2 * al((size_t)T5_BUCKETS * D.H) +
+            (has_enc ? nl * enc_layer : 0) + (has_dec ? nl * dec_layer : 0) + n_xproj * bl(2 * in, d);
   EXG_CUDA(cudaMalloc(&wbuf_, wbytes_));
   EXG_CUDA(cudaMemsetAsync(wbuf_, 0, wbytes_, st_));
   uint8_t* p = wbuf_;
@@ -286,19 +296,26 @@ void Engine::gen_weights_t5() {
     gen(m, out, K, slot, kind, 0, 1, canon_cols, 1, col0, 0);
     return m;
   };
-  tok_emb_ = carve_blk(D.V, d);
-  gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d, 1);
-  lnf_g_ = vec(0, K_LNFG, 1);
-  enc_lnf_g_ = vec(0, K_LNXG, 1);
-  enc_rel_ = carve<bf16>(p, (size_t)T5_BUCKETS * D.H);
-  gen(enc_rel_, T5_BUCKETS, D.H, 1, K_RELB, 0, 0, D.H);
-  dec_rel_ = carve<bf16>(p, (size_t)T5_BUCKETS * D.H);
-  gen(dec_rel_, T5_BUCKETS, D.H, 1001, K_RELB, 0, 0, D.H);
-  enc_layers_.resize(D.L);
-  layers_.resize(D.L);
+  if (need_tok) {
+    tok_emb_ = carve_blk(D.V, d);
+    gen(tok_emb_, D.V, d, 0, K_TOK, 0, 0, d, 1);
+  }
+  if (S_.head) lnf_g_ = vec(0, K_LNFG, 1);
+  if (enc_last) enc_lnf_g_ = vec(0, K_LNXG, 1);
+  if (has_enc) {
+    enc_rel_ = carve<bf16>(p, (size_t)T5_BUCKETS * D.H);
+    gen(enc_rel_, T5_BUCKETS, D.H, 1, K_RELB, 0, 0, D.H);
+  }
+  if (has_dec) {
+    dec_rel_ = carve<bf16>(p, (size_t)T5_BUCKETS * D.H);
+    gen(dec_rel_, T5_BUCKETS, D.H, 1001, K_RELB, 0, 0, D.H);
+  }
+  if (has_enc) enc_layers_.resize(nl);
+  if (has_dec) layers_.resize(nl);
   for (int side = 0; side < 2; ++side) {
-    for (int l = 0; l < D.L; ++l) {
-      const int s = side ? 1001 + l : 1 + l;
+    if (side == 0 ? !has_enc : !has_dec) continue;
+    for (int l = 0; l < nl; ++l) {
+      const int s = side ? 1001 + S_.l0 + l : 1 + S_.l0 + l;
       LayerW& w = side ? layers_[l] : enc_layers_[l];
       w.ln1_g = vec(s, K_LN1G, 1);
       w.ln2_g = vec(s, K_LN2G, 1);
@@ -314,6 +331,7 @@ void Engine::gen_weights_t5() {
       }
     }
   }
+  for (int l = 0; l < n_xproj; ++l) xproj_.push_back(mat(1001 + l, K_WKVX, 2 * in, d, 2 * in));
   // fp32 bias tables over every signed distance -(P-1) .. P-1
   const int P = D.max_pos;
   bias_ld_ = 2 * P - 1;
@@ -328,8 +346,8 @@ void Engine::gen_weights_t5() {
   dec_bias_ = enc_bias_ + (size_t)D.Hl * bias_ld_;
   EXG_CUDA(cudaMalloc(&dbk, sizeof(int32_t) * bk.size()));
   EXG_CUDA(cudaMemcpyAsync(dbk, bk.data(), sizeof(int32_t) * bk.size(), cudaMemcpyHostToDevice, st_));
-  rel_bias_table(enc_bias_, enc_rel_, dbk, bias_ld_, D.Hl, D.H, 0, st_);
-  rel_bias_table(dec_bias_, dec_rel_, dbk + bias_ld_, bias_ld_, D.Hl, D.H, 0, st_);
+  if (enc_rel_) rel_bias_table(enc_bias_, enc_rel_, dbk, bias_ld_, D.Hl, D.H, 0, st_);
+  if (dec_rel_) rel_bias_table(dec_bias_, dec_rel_, dbk + bias_ld_, bias_ld_, D.Hl, D.H, 0, st_);
   EXG_CUDA(cudaStreamSynchronize(st_));
   EXG_CUDA(cudaFree(dbk));
 }
@@ -375,6 +393,9 @@ void Engine::ensure_kv(int slots, int slot_ctx, int layers, int xctx) {
   if (t5_ && xctx < 1) throw std::invalid_argument("encoder-decoder model: cross-attention context xctx must be >= 1");
   if (!t5_) xctx = 0;
   if (layers < 0) layers = n_layers();
+  // T5 encoder side: no self-attention cache; cross caches per n_cross_layers
+  const int self_layers = (t5_ && S_.t5_role == 1) ? 0 : layers;
+  const int x_layers = !t5_ ? 0 : (S_.t5_role == 1 ? n_cross_layers() : layers);
   if (slots <= kv_slots_ && slot_ctx == slot_ctx_ && layers <= kv_layers_ && xctx == xctx_) return;
   EXG_CUDA(cudaStreamSynchronize(st_));
   if (kv_) EXG_CUDA(cudaFree(kv_));
@@ -387,9 +408,9 @@ void Engine::ensure_kv(int slots, int slot_ctx, int layers, int xctx) {
   slot_ctx_ = slot_ctx;
   xctx_ = xctx;
   kv_layers_ = layers;
-  const size_t bytes = (size_t)layers * 2 * kv_layer_elems() * sizeof(bf16);
-  const size_t xbytes = (size_t)layers * 2 * xkv_layer_elems() * sizeof(bf16);
-  cudaError_t e = cudaMalloc(&kv_, bytes);
+  const size_t bytes = (size_t)self_layers * 2 * kv_layer_elems() * sizeof(bf16);
+  const size_t xbytes = (size_t)x_layers * 2 * xkv_layer_elems() * sizeof(bf16);
+  cudaError_t e = bytes ? cudaMalloc(&kv_, bytes) : cudaSuccess;
   if (e == cudaSuccess && xbytes) e = cudaMalloc(&xkv_, xbytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
@@ -399,7 +420,7 @@ void Engine::ensure_kv(int slots, int slot_ctx, int layers, int xctx) {
     kv_layers_ = 0;
     throw std::bad_alloc();
   }
-  EXG_CUDA(cudaMemsetAsync(kv_, 0, bytes, st_));
+  if (bytes) EXG_CUDA(cudaMemsetAsync(kv_, 0, bytes, st_));
   if (xbytes) EXG_CUDA(cudaMemsetAsync(xkv_, 0, xbytes, st_));
   EXG_CUDA(cudaMalloc(&last_tok_, sizeof(int32_t) * kv_slots_));
   EXG_CUDA(cudaMemsetAsync(last_tok_, 0, sizeof(int32_t) * kv_slots_, st_));
@@ -658,6 +679,7 @@ void Engine::embed_decode(const DecodeBatch& db) {
 
 void Engine::decode(const DecodeBatch& db) {
   if (db.B <= 0) return;
+  if (t5_ && S_.t5_role == 1) throw std::logic_error("T5 encoder-side shard: no decoder layers");
   if (S_.tp > 1 && !red_) throw std::logic_error("TP shard without a reducer: drive it through a TP group");
   embed_decode(db);
   for (int l = 0; l < n_layers(); ++l) layer_decode(l, db, true, true);
@@ -719,18 +741,21 @@ void Engine::enc_layer_t5(int l, const EncodeBatch& eb, bool attn, bool rest) {
 
 void Engine::encode_t5(const EncodeBatch& eb) {
   const int T = eb.T, d = D.d;
+  if (S_.t5_role == 2) throw std::logic_error("T5 decoder-side shard: no encoder layers");
   if (T > cap_tokens_) throw std::invalid_argument("encode batch exceeds workspace");
-  embed(x_, eb.ids, eb.pos, tok_emb_, nullptr, T, d, st_, 1);
-  for (int l = 0; l < D.L; ++l) enc_layer_t5(l, eb, true, true);
+  if (S_.embed) embed(x_, eb.ids, eb.pos, tok_emb_, nullptr, T, d, st_, 1);
+  for (int l = 0; l < n_layers(); ++l) enc_layer_t5(l, eb, true, true);
+  if (S_.t5_role == 1 && !S_.enc_last) return;   // residual stream x() continues on the next encoder stage
   rmsnorm(h_, d, x_, d, enc_lnf_g_, T, d, T5_EPS, 1.f, st_);
   // K13: cross K/V of every decoder layer, K at columns [il, 2il) and V at
   // [2il, 3il) of the qkv buffer, then scattered to the slots
-  for (int l = 0; l < D.L; ++l) cross_kv(l, eb);
+  for (int l = 0; l < n_cross_layers(); ++l) cross_kv(l, eb);
 }
 
 void Engine::cross_kv(int l, const EncodeBatch& eb) {
   const int il = D.inner_l;
-  linear_pre(h_, D.d, eb.T, layers_[l].Wkvx, 2 * il, D.d, epi_bf16(nullptr, qkv_ + il, 3 * il));
+  const bf16* W = S_.t5_role == 1 ? xproj_[l] : layers_[l].Wkvx;
+  linear_pre(h_, D.d, eb.T, W, 2 * il, D.d, epi_bf16(nullptr, qkv_ + il, 3 * il));
   kv_scatter(xkc(l), xvc(l), qkv_, eb.tslot, eb.pos, eb.T, D.Hl, D.dh, xctx_, st_);
 }
 

@@ -37,6 +37,12 @@ struct EngineShard {
   int tp = 1, tp_rank = 0;    // tensor-parallel degree and rank
   bool embed = true;          // first stage: token + position embeddings
   bool head = true;           // last stage: final LayerNorm + tied LM head + argmax
+  // T5 (tp = 1): 0 = encoder and decoder layers [l0, l1) (single GPU);
+  // 1 = WAA encoder side: encoder layers [l0, l1), and if enc_last the final
+  //     encoder norm + the cross K/V projections of every decoder layer (K13);
+  // 2 = WAA decoder side: decoder layers [l0, l1) with their cross caches
+  int t5_role = 0;
+  bool enc_last = true;
 };
 
 // TP reduction of fp32 partial sums (O-projection / FFN2 outputs, T4(i)).
@@ -88,6 +94,9 @@ class Engine {
   // T5-style encoder-decoder: encode = encoder over all
   // n input tokens + cross K/V projections (K13); decode starts from token 0
   bool encdec() const { return t5_; }
+  int t5_role() const { return S_.t5_role; }
+  // decoder layers whose cross K/V this engine holds (xkc / xvc index range)
+  int n_cross_layers() const { return t5_ ? (S_.t5_role == 1 ? (S_.enc_last ? D.L : 1) : n_layers()) : 0; }
   int xctx() const { return xctx_; }
   bf16* xkc(int l) const { return xkv_ + (size_t)l * 2 * xkv_layer_elems(); }
   bf16* xvc(int l) const { return xkc(l) + xkv_layer_elems(); }
@@ -179,6 +188,7 @@ class Engine {
   // encoder-decoder (T5)
   bool t5_ = false;
   std::vector<LayerW> enc_layers_;
+  std::vector<bf16*> xproj_;   // role 1, enc_last: W_kv_x^T of every decoder layer
   bf16 *enc_lnf_g_ = nullptr, *enc_rel_ = nullptr, *dec_rel_ = nullptr;
   float *enc_bias_ = nullptr, *dec_bias_ = nullptr;   // fp32 [Hl][2 max_pos - 1], centre max_pos - 1
   int bias_ld_ = 0, bias_off_ = 0;

@@ -256,6 +256,18 @@ struct EpiCfg {
   static constexpr int THREADS = 128 + 32 * WARPS;
 };
 
+// diagnostics (exg_diag_gemm_flags bit 2): per-CTA %globaltimer marks
+//   0 entry, 1 setup done, 2 producer past griddepcontrol.wait, 3 first full
+//   stage at the MMA warp, 4 last MMA commit, 5 epilogue done, 6 exit
+__device__ unsigned long long g_gemm_tl[256 * 8];
+__device__ __forceinline__ void tl_mark(int dbg, int k) {
+  if (dbg & 4) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 256) g_gemm_tl[blockIdx.x * 8 + k] = t;
+  }
+}
+
 // SWAP = 1 (decode): A = weights (blocked), B = activations (TMA 2-D).
 // SWAP = 0 (prefill): A = activations (TMA 2-D), B = weights (blocked).
 template <int BN, int STAGES, int SWAP>
@@ -266,6 +278,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
   constexpr int EPI_WARPS = EpiCfg<SWAP>::WARPS;
   auto epi_bar = [] { asm volatile("bar.sync 1, %0;" ::"n"(32 * EpiCfg<SWAP>::WARPS) : "memory"); };
   griddep_launch_dependents();
+  if (threadIdx.x == 0) tl_mark(g_dbg, 0);
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS =
       (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
@@ -298,6 +311,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) tl_mark(g_dbg, 1);
 
   UnitIter it;
   it.init(work, blockIdx.x);
@@ -344,6 +358,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
           const uint32_t ph = (g / STAGES) & 1;
           if (!waited && g >= STAGES) {
             griddep_wait();
+            tl_mark(g_dbg, 2);
             for (int i = 0; i < npend; ++i) issue_x(i, pend[i][0], pend[i][1], pend[i][2]);
             waited = true;
           }
@@ -362,6 +377,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
       }
       if (!waited) {
         griddep_wait();
+        tl_mark(g_dbg, 2);
         for (int i = 0; i < npend; ++i) issue_x(i, pend[i][0], pend[i][1], pend[i][2]);
       }
     }
@@ -379,6 +395,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
           const uint32_t ph = (g / STAGES) & 1;
           mbar_wait(&full[s], ph);
           tc_fence_after();
+          if (g == 0) tl_mark(g_dbg, 3);
           if (g_dbg & 1) {  // diagnostics: memory pipeline only (no MMA)
             mbar_arrive(&empty[s]);
             continue;
@@ -394,6 +411,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
         umma_commit(&tfull[a]);
         ++ui;
       }
+      tl_mark(g_dbg, 4);
     }
   } else if (warp >= 4) {
     // 8 epilogue warps: warp w reads TMEM lanes 32*(w%4).. (hardware rule)
@@ -452,19 +470,26 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
         if (*s_last) {
           __threadfence();
           const float* base = partial + ((int64_t)u.n * work.tiles_m + u.m) * work.max_segs * (int64_t)(BM * BN);
-          // 16 columns at a time: all loads of a segment issue back to back
-          // (latency overlapped), segments summed in segment order
+          // 16 columns at a time; the loads of up to 4 segments issue back to
+          // back (one L2 round trip instead of one per segment), segments
+          // summed in segment order
           for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
             float acc[16];
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-            for (int s = 0; s < nseg; ++s) {
-              const float* src = base + (int64_t)s * BM * BN + (int64_t)c0 * BM + r;
-              float v[16];
+            for (int s0 = 0; s0 < nseg; s0 += 4) {
+              float v[4][16];
 #pragma unroll
-              for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + (int64_t)j * BM);
+              for (int q = 0; q < 4; ++q) {
+                const float* src = base + (int64_t)(s0 + q) * BM * BN + (int64_t)c0 * BM + r;
 #pragma unroll
-              for (int j = 0; j < 16; ++j) acc[j] += v[j];
+                for (int j = 0; j < 16; ++j) v[q][j] = (s0 + q < nseg) ? __ldcg(src + (int64_t)j * BM) : 0.f;
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q)
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (s0 + q < nseg) acc[j] += v[q][j];
             }
             if (!row_ok) continue;
             if (SWAP) {
@@ -478,6 +503,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
         epi_bar();
       }
     }
+    if (threadIdx.x == 128) tl_mark(g_dbg, 5);
   }
   tc_fence_before();
   __syncthreads();
@@ -485,6 +511,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
+  if (threadIdx.x == 0) tl_mark(g_dbg, 6);
 }
 
 // Ring depth: up to 8 stages within ~200 KB (one CTA per SM).  Measured: a
@@ -541,13 +568,19 @@ __global__ void __launch_bounds__(128) streamk_reduce_kernel(const float* __rest
     float acc[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-    for (int s = 0; s < nseg; ++s) {
-      const float* src = base + (int64_t)s * BM * BN + (int64_t)c0 * BM + r;
-      float v[16];
+    for (int s0 = 0; s0 < nseg; s0 += 4) {   // up to 4 segments' loads in flight
+      float v[4][16];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) v[j] = __ldcg(src + (int64_t)j * BM);
+      for (int q = 0; q < 4; ++q) {
+        const float* src = base + (int64_t)(s0 + q) * BM * BN + (int64_t)c0 * BM + r;
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] += v[j];
+        for (int j = 0; j < 16; ++j) v[q][j] = (s0 + q < nseg) ? __ldcg(src + (int64_t)j * BM) : 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (s0 + q < nseg) acc[j] += v[q][j];
     }
     if (gm >= M) continue;
     if (SWAP) {
@@ -691,3 +724,7 @@ void linear(const LinearArgs& a, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
+// per-CTA timeline marks of the last GEMM run with flag bit 2 ([256][8] ns)
+extern "C" int exg_diag_gemm_timeline(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, exg::g_gemm_tl, sizeof(unsigned long long) * 256 * 8) == cudaSuccess ? 0 : 1;
+}

@@ -200,8 +200,13 @@ struct Stage {
       if (e) e->finish_pending();
   }
 
+  bool t5() const { return eng.size() == 1 && eng[0] && eng[0]->encdec(); }
   void encode(const Exec& X, const EncodeBatch& eb, int d) {
     if (eb.T <= 0 || !any_local()) return;
+    if (t5()) {  // T5 stages are single-GPU: the engine runs its whole part of the encode phase
+      eng[0]->encode(eb);
+      return;
+    }
     for (auto& e : eng)
       if (e) e->embed_encode(eb);
     for (int l = 0; l < l1 - l0; ++l) {
@@ -215,6 +220,10 @@ struct Stage {
   }
   void decode(const Exec& X, const DecodeBatch& db, int d) {
     if (db.B <= 0 || !any_local()) return;
+    if (t5()) {
+      eng[0]->decode(db);
+      return;
+    }
     for (auto& e : eng)
       if (e) e->embed_decode(db);
     for (int l = 0; l < l1 - l0; ++l) {
@@ -298,7 +307,7 @@ static Exec make_exec(const MultiCtx::Impl* p, int G) {
 }
 
 static std::unique_ptr<Stage> make_stage(const MultiCtx::Impl* p, const Exec& X, int first_gpu, int l0, int l1,
-                                         int tp, bool first, bool last) {
+                                         int tp, bool first, bool last, int t5_role = 0, bool enc_last = true) {
   auto s = std::make_unique<Stage>();
   s->l0 = l0;
   s->l1 = l1;
@@ -316,6 +325,8 @@ static std::unique_ptr<Stage> make_stage(const MultiCtx::Impl* p, const Exec& X,
     sh.tp_rank = r;
     sh.embed = first;
     sh.head = last && r == 0;
+    sh.t5_role = t5_role;
+    sh.enc_last = enc_last;
     s->eng[r] = std::make_unique<Engine>(p->spec, p->device, sh, p->st);
   }
   return s;
@@ -349,16 +360,20 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
   if (s.strategy != EXG_RRA) check_cover(enc_idx);
   check_cover(dec_idx);
   const Exec X = make_exec(p, G);
+  const bool t5 = p->spec.arch == EXG_ARCH_T5;
+  if (t5 && s.strategy == EXG_RRA)
+    throw std::invalid_argument("T5: multi-GPU layouts run under WAA (encoder / decoder GPU sets) only");
   for (size_t k = 0; k < enc_idx.size(); ++k) {
     const int i = enc_idx[k];
     if (s.stage_n_gpus[i] != 1) throw std::invalid_argument("WAA encoder stages are single-GPU");
     lay->enc.push_back(make_stage(p, X, s.stage_first_gpu[i], s.stage_layer_begin[i], s.stage_layer_end[i], 1,
-                                  k == 0, false));
+                                  k == 0, false, t5 ? 1 : 0, k + 1 == enc_idx.size()));
   }
   for (size_t k = 0; k < dec_idx.size(); ++k) {
     const int i = dec_idx[k];
+    if (t5 && s.stage_n_gpus[i] != 1) throw std::invalid_argument("T5: tensor-parallel stages are not built yet");
     lay->dec.push_back(make_stage(p, X, s.stage_first_gpu[i], s.stage_layer_begin[i], s.stage_layer_end[i],
-                                  s.stage_n_gpus[i], k == 0, k + 1 == dec_idx.size()));
+                                  s.stage_n_gpus[i], k == 0, k + 1 == dec_idx.size(), t5 ? 2 : 0));
   }
   Layout* out = lay.get();
   p->layouts[key] = std::move(lay);
@@ -412,7 +427,8 @@ struct RunState {
   int n;
   std::vector<int64_t> base;
   int64_t total_out = 0;
-  int max_in = 1, max_ctx = 1;
+  int max_in = 1, max_ctx = 1, max_out = 1;
+  bool ed = false;   // encoder-decoder token accounting (T6 for T5)
   int32_t* d_out = nullptr;
   uint64_t* d_stamps = nullptr;
   int n_stamps = 0, cap_stamps = 0;
@@ -441,10 +457,12 @@ void validate_requests(RunState& R, int V, int max_pos) {
   for (int r = 0; r < R.n; ++r) {
     const exg_request& q = R.reqs[r];
     if (q.input_len < 1 || q.output_len < 1 || !q.input_ids) throw std::invalid_argument("request lengths must be >= 1");
-    if (q.input_len + q.output_len > max_pos) throw std::invalid_argument("input_len + output_len > max_pos");
+    if (R.ed ? std::max(q.input_len, q.output_len) > max_pos : q.input_len + q.output_len > max_pos)
+      throw std::invalid_argument(R.ed ? "input_len or output_len > max_pos" : "input_len + output_len > max_pos");
     for (int j = 0; j < q.input_len; ++j)
       if (q.input_ids[j] < 0 || q.input_ids[j] >= V) throw std::invalid_argument("token id out of range");
     R.max_in = std::max(R.max_in, q.input_len);
+    R.max_out = std::max(R.max_out, q.output_len);
     R.max_ctx = std::max(R.max_ctx, q.input_len + q.output_len);
     R.base[r + 1] = R.base[r] + q.output_len;
   }
@@ -462,8 +480,9 @@ void validate_requests(RunState& R, int V, int max_pos) {
 // packed encode tables for requests [r0, r0+k) with the given slots
 EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int* slots, cudaStream_t st,
                          std::vector<int32_t>* last_ids) {
+  const int drop = R.ed ? 0 : 1;   // T6: decoder-only encodes positions 0..n-2, T5 all n tokens
   int T = 0, maxlen = 0;
-  for (int j = 0; j < k; ++j) T += R.reqs[r0 + j].input_len - 1;
+  for (int j = 0; j < k; ++j) T += R.reqs[r0 + j].input_len - drop;
   tb.ensure((size_t)3 * T + 3 * (k + 1) + 8);
   int32_t* h = tb.begin();
   int32_t *ids = h, *pos = ids + T, *tsl = pos + T, *cu = tsl + T, *rsl = cu + k + 1, *p0 = rsl + k;
@@ -472,7 +491,7 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
   EncodeBatch eb;
   for (int j = 0; j < k; ++j) {
     const exg_request& q = R.reqs[r0 + j];
-    for (int p = 0; p < q.input_len - 1; ++p, ++t) {
+    for (int p = 0; p < q.input_len - drop; ++p, ++t) {
       ids[t] = q.input_ids[p];
       pos[t] = p;
       tsl[t] = slots[j];
@@ -480,9 +499,9 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
     cu[j + 1] = t;
     rsl[j] = slots[j];
     p0[j] = 0;
-    maxlen = std::max(maxlen, q.input_len - 1);
-    const double m = q.input_len - 1;
-    eb.attn_pairs += m * (m + 1) / 2;
+    maxlen = std::max(maxlen, q.input_len - drop);
+    const double m = q.input_len - drop;
+    eb.attn_pairs += R.ed ? m * m : m * (m + 1) / 2;
     if (last_ids) last_ids->push_back(q.input_ids[q.input_len - 1]);
   }
   tb.upload((size_t)3 * T + (k + 1) + 2 * k, st);
@@ -500,19 +519,24 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
 
 DecodeBatch build_decode(const RunState& R, Tables& tb, const std::vector<Row>& rows, int i0, int B,
                          cudaStream_t st) {
-  tb.ensure((size_t)4 * B + 8);
+  tb.ensure((size_t)5 * B + 8);
   int32_t* h = tb.begin();
   DecodeBatch db;
   for (int i = 0; i < B; ++i) {
     const Row& rw = rows[i0 + i];
+    const int n_in = R.reqs[rw.req].input_len;
     h[i] = rw.slot;
     h[B + i] = rw.pos;
     h[2 * B + i] = rw.pos + 1;
     h[3 * B + i] = (int32_t)(R.base[rw.req] + rw.emitted);
+    h[4 * B + i] = n_in;
     db.max_keys = std::max(db.max_keys, rw.pos + 1);
     db.sum_keys += rw.pos + 1;
+    db.max_xkeys = std::max(db.max_xkeys, n_in);
+    db.sum_xkeys += n_in;
   }
-  tb.upload((size_t)4 * B, st);
+  tb.upload((size_t)5 * B, st);
+  if (R.ed) db.xkeys = tb.dev + 4 * B;
   db.B = B;
   db.slot = tb.dev;
   db.pos = tb.dev + B;
@@ -775,23 +799,30 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   R.reqs = reqs;
   R.n = n;
   R.st = p->st;
+  R.ed = p->spec.arch == EXG_ARCH_T5;
   validate_requests(R, p->spec.vocab, p->spec.max_pos);
-  const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : R.max_ctx;
-  if (slot_ctx < R.max_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
+  // decoder self-attention context: n-1+S keys (decoder-only) or S (T5)
+  const int need_ctx = R.ed ? R.max_out : R.max_ctx;
+  const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : need_ctx;
+  if (slot_ctx < need_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
   const int B_D = s.b_d, B_E = s.b_e;
   if (B_E < 1 || B_D < B_E) throw std::invalid_argument("WAA needs 1 <= B_E <= B_D");
   const int M = s.b_m > 0 ? std::max(1, (B_D + s.b_m - 1) / s.b_m) : 1;
   const int enc_ctx = std::max(1, R.max_in);
+  const int drop = R.ed ? 0 : 1;
   for (auto& st : enc)
     for (auto& e : st->eng)
       if (e) {
-        e->ensure_kv(B_E, enc_ctx);
-        e->ensure_workspace(B_E * (R.max_in - 1), B_E);
+        if (R.ed)
+          e->ensure_kv(B_E, 1, -1, enc_ctx);   // encoder side: encoder K/V staging + cross K/V of the batch
+        else
+          e->ensure_kv(B_E, enc_ctx);
+        e->ensure_workspace(std::max(1, B_E * (R.max_in - drop)), B_E);
       }
   for (auto& st : dec)
     for (auto& e : st->eng)
       if (e) {
-        e->ensure_kv(B_D, slot_ctx);
+        e->ensure_kv(B_D, slot_ctx, -1, R.ed ? R.max_in : 0);
         e->ensure_workspace(1, B_D);
       }
   const bool first_mine = X.mine(enc.front()->gpu(0)), head_mine = X.mine(dec.back()->gpu(0));
@@ -839,9 +870,10 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         dslots[j] = free_slots.back();
         free_slots.pop_back();
         const exg_request& q = reqs[pend_r0 + j];
-        h_hrows[j] = HandoffRow{j, dslots[j], q.input_len - 1, rows_len};
-        rows_len += q.input_len - 1;
-        active.push_back(Row{pend_r0 + j, dslots[j], q.input_len - 1, 0});
+        // handed-off K/V rows: positions 0..n-2 (decoder-only) / the n cross K/V rows (T5)
+        h_hrows[j] = HandoffRow{j, dslots[j], q.input_len - drop, rows_len};
+        rows_len += q.input_len - drop;
+        active.push_back(Row{pend_r0 + j, dslots[j], R.ed ? 0 : q.input_len - 1, 0});
         R.admit_ev[pend_r0 + j] = pend_ev;
       }
       EXG_CUDA(cudaMemcpyAsync(d_hrows, h_hrows, sizeof(HandoffRow) * pend_k, cudaMemcpyHostToDevice, R.st));
@@ -852,8 +884,12 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         stage_cap = need;
         EXG_CUDA(cudaMalloc(&stage_buf, sizeof(bf16) * stage_cap));
       }
+      // decoder-only: encoder stage es holds the KV of its layers [l0, l1);
+      // T5: the last encoder stage holds the cross K/V of every decoder layer
       for (auto& es : enc) {
-        for (int l = es->l0; l < es->l1; ++l)
+        if (R.ed && es != enc.back()) continue;
+        const int la = R.ed ? 0 : es->l0, lb = R.ed ? p->spec.n_dec_layers : es->l1;
+        for (int l = la; l < lb; ++l)
           for (auto& ds : dec) {
             if (l < ds->l0 || l >= ds->l1) continue;
             const int Hd = H / ds->tp;
@@ -864,22 +900,27 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
               Engine* src = es->eng[0].get();
               Engine* dst = ds->eng[r].get();
               const size_t bytes = sizeof(bf16) * (size_t)rows_len * Hd * dh;
+              const int ctx_d = R.ed ? R.max_in : slot_ctx;
               for (int kv = 0; kv < 2; ++kv) {
-                const bf16* sp_ = src ? (kv ? src->vc(l - es->l0) : src->kc(l - es->l0)) : nullptr;
-                bf16* dp = dst ? (kv ? dst->vc(l - ds->l0) : dst->kc(l - ds->l0)) : nullptr;
+                const bf16* sp_ = nullptr;
+                bf16* dp = nullptr;
+                if (src) sp_ = R.ed ? (kv ? src->xvc(l) : src->xkc(l)) : (kv ? src->vc(l - es->l0) : src->kc(l - es->l0));
+                if (dst)
+                  dp = R.ed ? (kv ? dst->xvc(l - ds->l0) : dst->xkc(l - ds->l0))
+                            : (kv ? dst->vc(l - ds->l0) : dst->kc(l - ds->l0));
                 if (src_mine && dst_mine) {
                   kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, dp, d_hrows, pend_k, H, r * Hd, Hd, enc_ctx,
-                                                                   slot_ctx, dh, 0);
+                                                                   ctx_d, dh, 0);
                   EXG_CHECK_LAUNCH();
                 } else if (src_mine) {
                   kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, stage_buf, d_hrows, pend_k, H, r * Hd, Hd,
-                                                                   enc_ctx, slot_ctx, dh, 1);
+                                                                   enc_ctx, ctx_d, dh, 1);
                   EXG_CHECK_LAUNCH();
                   p->comm->send(stage_buf, bytes, X.owner(gd), R.st);
                 } else {
                   p->comm->recv(stage_buf, bytes, X.owner(ge), R.st);
                   kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(stage_buf, dp, d_hrows, pend_k, H, r * Hd, Hd,
-                                                                   enc_ctx, slot_ctx, dh, 2);
+                                                                   enc_ctx, ctx_d, dh, 2);
                   EXG_CHECK_LAUNCH();
                 }
               }
@@ -893,7 +934,7 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       for (int j = 0; j < pend_k; ++j) {
         const exg_request& q = reqs[pend_r0 + j];
         h[j] = dslots[j];
-        h[pend_k + j] = q.input_ids[q.input_len - 1];
+        h[pend_k + j] = R.ed ? 0 : q.input_ids[q.input_len - 1];   // T5: decoder start token 0
       }
       tl.upload(2 * pend_k, R.st);
       for (auto& e : dec.front()->eng)

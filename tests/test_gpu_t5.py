@@ -7,7 +7,10 @@ T5), checked against oracle/t5.py:
   bias over one and several 512-key splits;
 * end to end through exg_run: greedy ids equal oracle mode (iii) (near-ties
   reported with their margin), logits within 2e-2, for the dh=16 and the
-  dh=128 parity models; batch invariance across RRA schedules (bit-identical).
+  dh=128 parity models; batch invariance across RRA schedules (bit-identical);
+* WAA layouts (config 3 shape): encoder GPU(s) project every decoder layer's
+  cross K/V and hand it off to the decoder GPU(s) -- bit-identical to the
+  single-GPU run, in one process and over 2 / 4 thread ranks.
 """
 import math
 
@@ -173,7 +176,7 @@ def test_t5_batch_invariance(t5env):
         assert np.array_equal(a[3][r], b[3][r]), r
 
 
-def test_t5_multi_gpu_layout_rejected(t5env):
+def test_t5_rra_multi_gpu_layout_rejected(t5env):
     X, spec, reqs, ctx, ora = t5env
     from paper_2404_07947_b200 import _lib
     from workload import weight_seed
@@ -181,3 +184,41 @@ def test_t5_multi_gpu_layout_rejected(t5env):
     s = _lib.make_schedule(X.EXG_RRA, 2, 4, [(0, 1, 0, spec.n_dec_layers)], n_d=2)
     with pytest.raises(X.ExgError):
         multi.run(s, reqs[:2])
+
+
+# WAA for T5 (config 3: encoder GPU(s) + decoder GPU(s)): the last encoder
+# stage projects the cross K/V of every decoder layer (K13) and hands each
+# decoder stage its layers' n cross K/V rows per request (K12).  Same per-row
+# arithmetic as the single-GPU run => bit-identical ids and logits, also with
+# the GPUs split over thread ranks.
+T5_WAA = [
+    # (name, b_e, b_d, b_m, n_enc, layout, world)
+    ("enc1_dec1", 2, 5, 0, 1, [(0, 1, 0, 2), (1, 1, 0, 2)], 1),
+    ("enc1_dec1_w2", 2, 5, 0, 1, [(0, 1, 0, 2), (1, 1, 0, 2)], 2),
+    ("enc2_dec2_mb", 3, 6, 3, 2, [(0, 1, 0, 1), (1, 1, 1, 2), (2, 1, 0, 1), (3, 1, 1, 2)], 1),
+    ("enc2_dec2_mb_w4", 3, 6, 3, 2, [(0, 1, 0, 1), (1, 1, 1, 2), (2, 1, 0, 1), (3, 1, 1, 2)], 4),
+]
+
+
+@pytest.mark.parametrize("case", T5_WAA, ids=[c[0] for c in T5_WAA])
+def test_t5_waa_bit_identical_to_single_gpu(t5env, case):
+    X, spec, reqs, ctx, ora = t5env
+    from paper_2404_07947_b200 import _lib
+    from workload import weight_seed
+    name, b_e, b_d, b_m, n_enc, layout, world = case
+    base_t, _, _, base_l = ctx.run(X.rra_schedule(3, 5, 4), reqs, dump=range(len(reqs)))
+    s = _lib.make_schedule(X.EXG_WAA_C, b_e, b_d, layout, b_m=b_m, n_enc_gpus=n_enc)
+    if world == 1:
+        multi = X.Context(spec, weight_seed(3), cluster=X.cluster_spec(4))
+        toks, lat, st, lg = multi.run(s, reqs, dump=range(len(reqs)))
+        heads = [lg]
+    else:
+        group = X.local_group(spec, weight_seed(3), world, X.cluster_spec(4))
+        res = X.run_group(group, s, reqs, dump=range(len(reqs)))
+        toks, lat, st, lg = res[0]
+        heads = [r[3] for r in res if np.any(r[3][0])]
+    assert toks == base_t
+    assert len(heads) == 1
+    for r in range(len(reqs)):
+        assert np.array_equal(heads[0][r], base_l[r]), r
+    assert st["out_tokens"] == sum(q.output_len for q in reqs) and np.all(lat > 0)
