@@ -132,6 +132,15 @@ def cpu_cores():
         return os.cpu_count()
 
 
+def workload_variance(st):
+    """Table 9: mean single-stage time and its 99th-pctl
+    range (|t - mean|) for encode phases and decode iterations."""
+    def one(m, d):
+        return {"mean_s": m, "p99_range_s": d, "p99_range_pct": 100.0 * d / m if m else None}
+    return {"encoder": one(st["enc_stage_mean_s"], st["enc_stage_p99dev_s"]),
+            "decoder": one(st["dec_stage_mean_s"], st["dec_stage_p99dev_s"])}
+
+
 # ---- multi-rank host logic (weak scaling: independent replicas) ------------
 def rank_request_seed(rank: int) -> int:
     """Each rank draws its own requests of the same workload (weak scaling)."""
@@ -192,6 +201,7 @@ def main():
     ap.add_argument("--little", type=int, default=1,
                     help="1: completion fraction by Little's law (SURVEY.md S3; DESIGN.md), 0: paper's E[1/ceil(S/N_D)]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--dyn", type=float, default=0.1, help="dynamic workload adjustment threshold (0: skip the run)")
     ap.add_argument("--roofline-steps", type=int, default=1, help="extra steps with per-launch kernel events")
     ap.add_argument("--bounds", default="all", choices=["all", "headline"])
     args = ap.parse_args()
@@ -307,6 +317,7 @@ def main():
             launches += st["kernel_launches"]
             lats.append(lat)
             steady.append(st["tok_s_steady"])
+            var_st = st
         if torch.cuda.is_available():
             torch.cuda.nvtx.range_pop()
         barrier()
@@ -346,6 +357,15 @@ def main():
                            "encode_s": st2["encode_s"], "decode_s": st2["decode_s"],
                            "encode_phases": st2["encode_phases"], "decode_iters": st2["decode_iters"],
                            "wall_s": st2["wall_s"], **sla(lat2, L_b)}
+
+    # dynamic workload adjustment on the headline schedule:
+    # one extra run, reported beside the plain one (not part of `value`)
+    dyn = None
+    if args.dyn > 0 and rank == 0:
+        _, lat_d, st_d, _ = ctx.run(sched, reqs, slot_ctx=slot_ctx, dyn_threshold=args.dyn)
+        dyn = {"threshold": args.dyn, "tok_s": st_d["tok_s"], "tok_s_steady": st_d["tok_s_steady"],
+               "mean_encode_batch": st_d["mean_encode_batch"], "mean_decode_batch": st_d["mean_decode_batch"],
+               "variance": workload_variance(st_d), **sla(lat_d, L_head)}
 
     pk = peaks()
     # roofline of the dominant kernel class (time share) + decode attention
@@ -404,6 +424,8 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            "workload_variance": workload_variance(var_st),
+            "dyn_adjust": dyn,
             "bounds": other,
             "setup_s": {"weights": t_weights, "profile": t_prof, "schedule_find_4_bounds": t_sched},
         }

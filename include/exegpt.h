@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EXG_ABI_VERSION 1
+#define EXG_ABI_VERSION 2
 
 typedef enum {
   EXG_OK = 0,
@@ -128,6 +128,12 @@ typedef struct {
   int32_t pin_nccl_algo;      /* reserved for multi-GPU parity runs             */
   int32_t kernel_timing;      /* 1: CUDA events around every launch of the
                                  kernel classes below (roofline evidence)       */
+  double dyn_threshold;       /* > 0: dynamic workload adjustment (PAPER.md:350-354,
+                                 RRA on 1 GPU): each encode batch's token sum
+                                 is kept within +-threshold of B_E x mean
+                                 encoded length, and B_E is raised / lowered by
+                                 one while the decode batch sits below / above
+                                 +-threshold of its running average; 0 = off  */
 } exg_run_opts;
 
 /* Kernel classes timed when exg_run_opts.kernel_timing = 1.  Work is the
@@ -154,6 +160,10 @@ typedef struct {
   double k_time_s[EXG_K_CLASSES];      /* summed launch durations per class        */
   double k_work[EXG_K_CLASSES];        /* summed algorithmic work per class        */
   int64_t k_launches[EXG_K_CLASSES];
+  /* workload variance (Table 9): mean single-stage time and
+   * the 99th percentile of |t - mean| of encode phases and decode iterations */
+  double enc_stage_mean_s, enc_stage_p99dev_s, dec_stage_mean_s, dec_stage_p99dev_s;
+  double mean_encode_batch;            /* requests per encode phase (admissions)  */
 } exg_run_stats;
 
 typedef struct exg_ctx exg_ctx;           /* one per rank: device state + comms */

@@ -86,7 +86,8 @@ class exg_request(C.Structure):
 
 class exg_run_opts(C.Structure):
     _fields_ = [("logits_out", C.POINTER(C.c_float)), ("dump_mask", C.POINTER(C.c_uint8)),
-                ("slot_ctx", C.c_int32), ("pin_nccl_algo", C.c_int32), ("kernel_timing", C.c_int32)]
+                ("slot_ctx", C.c_int32), ("pin_nccl_algo", C.c_int32), ("kernel_timing", C.c_int32),
+                ("dyn_threshold", C.c_double)]
 
 
 K_CLASSES = ["prefill_gemm", "decode_gemm", "decode_attn", "prefill_attn"]
@@ -98,7 +99,10 @@ class exg_run_stats(C.Structure):
                 ("wall_s", C.c_double), ("out_tokens", C.c_int64), ("decode_iters", C.c_int64),
                 ("encode_phases", C.c_int64), ("mean_decode_batch", C.c_double), ("encode_s", C.c_double),
                 ("decode_s", C.c_double), ("kernel_launches", C.c_int64), ("k_time_s", C.c_double * 4),
-                ("k_work", C.c_double * 4), ("k_launches", C.c_int64 * 4)]
+                ("k_work", C.c_double * 4), ("k_launches", C.c_int64 * 4),
+                ("enc_stage_mean_s", C.c_double), ("enc_stage_p99dev_s", C.c_double),
+                ("dec_stage_mean_s", C.c_double), ("dec_stage_p99dev_s", C.c_double),
+                ("mean_encode_batch", C.c_double)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("k_")}
@@ -152,6 +156,7 @@ _SIGS = {
 }
 
 _lib = None
+ABI_VERSION = 2   # include/exegpt.h EXG_ABI_VERSION
 
 
 def lib():
@@ -165,6 +170,8 @@ def lib():
             f = getattr(L, name)
             f.restype = res
             f.argtypes = args
+        if L.exg_abi_version() != ABI_VERSION:
+            raise ImportError("libexegpt.so ABI %d != binding ABI %d: rebuild" % (L.exg_abi_version(), ABI_VERSION))
         _lib = L
     return _lib
 
@@ -246,7 +253,7 @@ class Context:
         return Profile(h)
 
     def run(self, sched: exg_schedule, requests, dump: Optional[Sequence[int]] = None, slot_ctx: int = 0,
-            kernel_timing: bool = False):
+            kernel_timing: bool = False, dyn_threshold: float = 0.0):
         """Returns (tokens per request, latencies [s], stats dict, logits per
         dumped request [S_r][V] or None)."""
         n = len(requests)
@@ -260,7 +267,7 @@ class Context:
         out = np.zeros(total, dtype=np.int32)
         lat = np.zeros(n, dtype=np.float64)
         stats = exg_run_stats()
-        opts = exg_run_opts(None, None, slot_ctx, 0, int(kernel_timing))
+        opts = exg_run_opts(None, None, slot_ctx, 0, int(kernel_timing), float(dyn_threshold))
         logits = None
         if dump is not None:
             mask = np.zeros(n, dtype=np.uint8)

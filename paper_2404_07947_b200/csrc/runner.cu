@@ -157,6 +157,11 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   };
 
   int next_req = 0;
+  const double dyn = opts ? opts->dyn_threshold : 0.0;
+  double mean_enc_tokens = 0, steady_batch_sum = 0;
+  int64_t steady_iters = 0, admitted_phases = 0;
+  for (int r = 0; r < n; ++r) mean_enc_tokens += reqs[r].input_len - enc_drop;
+  mean_enc_tokens /= n;
   int64_t decode_iters = 0, encode_phases = 0, batch_sum = 0;
   const long long launches0 = launch_counter().load();
   E.set_kernel_timing(opts && opts->kernel_timing);
@@ -164,7 +169,30 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   record(0, 0);
   while (next_req < n || !active.empty()) {
     // ---------------- encode phase ----------------
-    const int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
+    int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
+    if (dyn > 0 && admit > 0) {
+      // dynamic workload adjustment: decoder batch below /
+      // above +-dyn of its running average -> admit that many rows more / fewer
+      int be = B_E;
+      if (steady_iters >= 2 * s.n_d && !active.empty()) {
+        const double avg = steady_batch_sum / steady_iters, cur = (double)active.size();
+        if (cur < (1 - dyn) * avg || cur > (1 + dyn) * avg) be = B_E + (int)std::lround(avg - cur);
+      }
+      be = std::max(1, std::min(be, B_D));
+      // encoder workload (token sum) within +-dyn of be x the mean encoded length
+      const int cap = std::min(B_D - (int)active.size(), n - next_req);
+      const double target = be * mean_enc_tokens;
+      double tok = 0;
+      int k = 0;
+      while (k < cap) {
+        const double t = reqs[next_req + k].input_len - enc_drop;
+        if (k >= be && tok >= (1 - dyn) * target) break;
+        if (k >= 1 && tok + t > (1 + dyn) * target) break;
+        tok += t;
+        ++k;
+      }
+      admit = k;
+    }
     const int ev_phase = record(0, 0);
     if (admit > 0) {
       Staging::Slot& sl = stage.acquire();
@@ -221,8 +249,9 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       E.encode(eb);
       next_req += admit;
       ++encode_phases;
+      ++admitted_phases;
     }
-    record(1, 0);
+    record(1, admit);   // tokens field of an encode-end event: requests admitted
     // ---------------- N_D decode iterations ----------------
     for (int u = 0; u < s.n_d && !active.empty(); ++u) {
       const int B = (int)active.size();
@@ -270,6 +299,10 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       const int ev_it = record(2, B);
       ++decode_iters;
       batch_sum += B;
+      if (next_req < n) {   // decode batch average while requests keep arriving (not the drain)
+        steady_batch_sum += B;
+        ++steady_iters;
+      }
       // early termination + stable compaction of the row table
       int w = 0;
       for (int i = 0; i < B; ++i) {
@@ -338,6 +371,32 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
     }
     stats->encode_s = enc;
     stats->decode_s = dec;
+    stats->mean_encode_batch = admitted_phases ? (double)n / admitted_phases : 0;
+    // Table 9: single-stage times of encode phases and
+    // decode iterations inside the steady window, mean and p99 of |t - mean|
+    {
+      const int r0 = std::min(n - 1, (int)std::ceil(0.1 * n));
+      const double w0 = t[admit_ev[r0]], w1 = t[admit_ev[n - 1]];
+      std::vector<double> te, td;
+      for (int k = 1; k < nev; ++k) {
+        if (t[k - 1] < w0 || t[k] > w1) continue;
+        if (ev_kind[k] == 1 && t[k] - t[k - 1] > 0 && ev_kind[k - 1] == 0 && ev_tokens[k] > 0) te.push_back(t[k] - t[k - 1]);
+        if (ev_kind[k] == 2) td.push_back(t[k] - t[k - 1]);
+      }
+      auto spread = [](const std::vector<double>& v, double* mean, double* p99dev) {
+        *mean = *p99dev = 0;
+        if (v.empty()) return;
+        double m = 0;
+        for (double x : v) m += x;
+        m /= v.size();
+        std::vector<double> dv;
+        for (double x : v) dv.push_back(std::fabs(x - m));
+        *mean = m;
+        *p99dev = pct(dv, 0.99);
+      };
+      spread(te, &stats->enc_stage_mean_s, &stats->enc_stage_p99dev_s);
+      spread(td, &stats->dec_stage_mean_s, &stats->dec_stage_p99dev_s);
+    }
     // steady-state window: admission of request ceil(0.1 n) .. admission of
     // the last request
     const int r0 = std::min(n - 1, (int)std::ceil(0.1 * n));

@@ -109,3 +109,20 @@ def test_input_errors(setup):
     bad = X.rra_schedule(4, 2, 1)
     with pytest.raises(X.ExgError):
         ctx.run(bad, reqs)
+
+
+def test_dynamic_workload_adjustment_keeps_results(setup):
+    """the runtime B_E correction changes only which encode
+    phase admits a request; per-request results are batch invariant (T13), so
+    ids and logits are bit-identical to the plain schedule."""
+    X, T, spec, W, reqs, ctx, ora = setup
+    from workload import make_requests, uniform_pmf
+    many = make_requests(40, uniform_pmf(4, 40), uniform_pmf(1, 20), spec.vocab, 77)
+    a = ctx.run(X.rra_schedule(4, 10, 3), many, dump=range(len(many)))
+    b = ctx.run(X.rra_schedule(4, 10, 3), many, dump=range(len(many)), dyn_threshold=0.1)
+    assert a[0] == b[0]
+    for r in range(len(many)):
+        assert np.array_equal(a[3][r], b[3][r]), r
+    st = b[2]
+    assert st["mean_encode_batch"] > 0 and st["dec_stage_mean_s"] > 0 and st["dec_stage_p99dev_s"] >= 0
+    assert a[2]["mean_encode_batch"] == pytest.approx(len(many) / a[2]["encode_phases"])
