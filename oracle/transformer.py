@@ -192,9 +192,23 @@ class Result:
 
 
 class KVLoop:
-    def __init__(self, W: Weights, mode: str):
+    """accum = "fp64" (default): every product accumulated in fp64 and rounded
+    once at the T4 rounding point -- the reference.  accum = "fp32": the same
+    rounding points with fp32 accumulation (numpy float32 matmuls), a second
+    valid evaluation of the contract used only to measure how far two valid
+    evaluations can drift apart at a given model width (calibrates the
+    full-width parity tolerance)."""
+
+    def __init__(self, W: Weights, mode: str, accum: str = "fp64"):
         self.W, self.spec, self.R = W, W.spec, Rounding(mode)
         self.act = act_fn(self.spec.arch)
+        assert accum in ("fp64", "fp32")
+        self.f32acc = accum == "fp32"
+
+    def mm(self, a, b):
+        if self.f32acc:
+            return (np.asarray(a, dtype=np.float32) @ np.asarray(b, dtype=np.float32)).astype(np.float64)
+        return a @ b
 
     def _layer(self, l, x, rows, caches):
         """x: [T, d] residual (fp32-valued in bf16 mode) for tokens `rows`
@@ -205,7 +219,7 @@ class KVLoop:
         H, dh = spec.n_heads, spec.d_head
         L = self.W.layer(l)
         h = R.bf16(layer_norm(x, L["ln1_g"], L["ln1_b"]))
-        qkv = R.bf16(h @ L["W_qkv"] + L["b_qkv"])
+        qkv = R.bf16(self.mm(h, L["W_qkv"]) + L["b_qkv"])
         T = x.shape[0]
         q = qkv[:, :H * dh].reshape(T, H, dh)
         k = qkv[:, H * dh:2 * H * dh].reshape(T, H, dh)
@@ -226,20 +240,20 @@ class KVLoop:
             klen = K[l].shape[1]
             assert klen == p0 + n_new
             qs = q[i:j].transpose(1, 0, 2)                         # [H, n_new, dh]
-            s = R.f32(qs @ K[l].transpose(0, 2, 1))                # [H, n_new, klen]
+            s = R.f32(self.mm(qs, K[l].transpose(0, 2, 1)))        # [H, n_new, klen]
             s = R.f32(s * scale)
             qpos = p0 + np.arange(n_new)[:, None]
             s = np.where(np.arange(klen)[None, :] <= qpos, s, -np.inf)
             m = s.max(axis=-1, keepdims=True)
             e = np.exp(s - m)
             pr = e / e.sum(axis=-1, keepdims=True)
-            ctx[i:j] = (pr @ Vc[l]).transpose(1, 0, 2)
+            ctx[i:j] = self.mm(pr, Vc[l]).transpose(1, 0, 2)
             i = j
         ctx = R.bf16(ctx.reshape(T, H * dh))
-        x = R.f32(x + R.f32(ctx @ L["W_o"] + L["b_o"]))
+        x = R.f32(x + R.f32(self.mm(ctx, L["W_o"]) + L["b_o"]))
         h2 = R.bf16(layer_norm(x, L["ln2_g"], L["ln2_b"]))
-        f = R.bf16(self.act(R.f32(h2 @ L["W_1"] + L["b_1"])))
-        x = R.f32(x + R.f32(f @ L["W_2"] + L["b_2"]))
+        f = R.bf16(self.act(R.f32(self.mm(h2, L["W_1"]) + L["b_1"])))
+        x = R.f32(x + R.f32(self.mm(f, L["W_2"]) + L["b_2"]))
         return x
 
     def _forward(self, tokens, rows, caches):
@@ -253,7 +267,7 @@ class KVLoop:
     def _logits(self, x):
         R = self.R
         hf = R.bf16(layer_norm(x, self.W.lnf_g, self.W.lnf_b))
-        return R.f32(hf @ self.W.head().T)
+        return R.f32(self.mm(hf, self.W.head().T))
 
     def run(self, requests, record_logits: bool = False, record: Optional[set] = None) -> Result:
         """Greedy decode every request; token accounting T6."""
@@ -294,8 +308,8 @@ class KVLoop:
 
 
 def greedy_kv(W: Weights, requests, mode: str = "bf16", record_logits: bool = False,
-              record: Optional[set] = None) -> Result:
-    return KVLoop(W, mode).run(requests, record_logits, record)
+              record: Optional[set] = None, accum: str = "fp64") -> Result:
+    return KVLoop(W, mode, accum).run(requests, record_logits, record)
 
 
 def teacher_forced_logits(W: Weights, request, forced: List[int], mode: str = "fp64") -> List[np.ndarray]:

@@ -293,8 +293,14 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
 }
 }  // namespace
 
+// diagnostics: 1 = route dh = 128 to the SIMT kernel (exg_diag_prefill_simt)
+int& prefill_force_simt() {
+  static int f = 0;
+  return f;
+}
+
 bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
-  if (a.dh != FD) return false;
+  if (a.dh != FD || prefill_force_simt()) return false;
   static bool attr = false;
   if (!attr) {
     EXG_CUDA(cudaFuncSetAttribute(fmha_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FMHA_SMEM));
@@ -315,3 +321,5 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
 }
 
 }  // namespace exg
+
+extern "C" void exg_diag_prefill_simt(int on) { exg::prefill_force_simt() = on; }

@@ -1,0 +1,104 @@
+"""Parity at the bench's full sizes (config 2: OPT-13B, task S), in the launch
+configuration bench.py times (tier rule ③):
+
+* full width, sampled outputs: the first 2 of OPT-13B's 40 layers (identical
+  weights: layer l is tensor slot 1001+l of the same seed) + embeddings + LM
+  head run on the GPU with the bench's request recipe and its headline RRA
+  control variables (B_E=31, B_D=77, N_D=16, 592-key slots); three sampled
+  requests are recomputed one by one by the oracle (mode iii) over their
+  first output steps (a step's logits depend only on the request's own
+  prefix).  Tolerance at this width: two valid evaluations of
+  the T4 rounding contract drift apart as the width grows (each fp32
+  accumulation-order difference can flip a bf16 rounding), so the bar is
+  calibrated per request by the oracle itself -- the distance between its
+  fp64-accumulated and fp32-accumulated evaluations (measured ~0.02 max-abs,
+  ~0.003 mean-abs at this width): GPU logits within max(2e-2, 2x that) max-abs
+  and max(2e-3, 2x that) mean-abs; ids equal except at near ties (oracle
+  top-2 margin within the bar, the GPU's token within it of the oracle's
+  maximum), after which that request's prefixes differ;
+* full depth, properties: all 40 layers, two schedules that put the same
+  requests in different batches give bit-identical ids and logits (T13).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2        # north_star's bf16 bar; widened per request by the calibration below
+TOL_MEAN = 2e-3
+STEPS = 6
+
+
+@pytest.fixture(scope="module")
+def X():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2404_07947_b200 as X
+    return X
+
+
+def _bench_requests(n):
+    from workload import MODELS, make_requests, task_dists
+    d = task_dists("S")
+    return make_requests(n, d.pmf_in, d.pmf_out, MODELS["opt-13b"].vocab, 0xE6E1_0002)
+
+
+@pytest.mark.parametrize("simt", [0])   # 1 routes dh=128 prefill to the fp32-P SIMT kernel (same result)
+def test_opt13b_width_sampled_parity_in_bench_configuration(X, simt):
+    from oracle import transformer as T
+    from workload import MODELS, ModelSpec, Request, weight_seed
+    full = MODELS["opt-13b"]
+    spec = ModelSpec("opt-13b-first2", full.arch, 0, 2, full.d_model, full.n_heads, full.d_head, full.d_ff,
+                     full.vocab, full.max_pos)
+    reqs = _bench_requests(192)
+    sample = [0, 95, 191]
+    ctx = X.Context(spec, weight_seed(2))
+    X.lib().exg_diag_prefill_simt(simt)
+    toks, lat, st, lg = ctx.run(X.rra_schedule(31, 77, 16), reqs, dump=sample, slot_ctx=592)
+    X.lib().exg_diag_prefill_simt(0)
+    assert st["mean_decode_batch"] > 40          # steady decode batches in the bench's token-tile class (33..64)
+    W = T.Weights(spec, weight_seed(2), cache_fp64=False)
+    near_ties = []
+    for r in sample:
+        q = reqs[r]
+        k = min(STEPS, q.output_len)
+        rq = Request(q.ids, q.input_len, k)
+        ora = T.greedy_kv(W, [rq], "bf16", record_logits=True)
+        o32 = T.greedy_kv(W, [rq], "bf16", record_logits=True, accum="fp32")
+        cal_max = cal_mean = 0.0
+        for t in range(k):
+            dd = np.abs(o32.logits[0][t] - ora.logits[0][t])
+            cal_max, cal_mean = max(cal_max, float(dd.max())), max(cal_mean, float(dd.mean()))
+            if o32.tokens[0][t] != ora.tokens[0][t]:
+                break
+        tol, tol_mean = max(TOL, 2 * cal_max), max(TOL_MEAN, 2 * cal_mean)
+        worst = worst_mean = 0.0
+        for t in range(k):
+            diff = np.abs(lg[r][t] - ora.logits[0][t])
+            worst, worst_mean = max(worst, float(diff.max())), max(worst_mean, float(diff.mean()))
+            if toks[r][t] != ora.tokens[0][t]:
+                # an argmax decided by rounding: valid iff the oracle's top-2 margin
+                # is within the bar and the GPU's token is within it of the maximum
+                assert ora.margins[0][t] <= 2 * tol, "hard mismatch req %d step %d" % (r, t)
+                lo = ora.logits[0][t]
+                assert lo[toks[r][t]] >= lo.max() - 2 * tol, (r, t)
+                near_ties.append((r, t, ora.margins[0][t]))
+                break
+        print("req", r, "simt", simt, "gpu-vs-oracle max/mean %.4g/%.4g" % (worst, worst_mean),
+              "oracle fp32-vs-fp64 %.4g/%.4g" % (cal_max, cal_mean))
+        assert worst <= tol and worst_mean <= tol_mean, (r, worst, worst_mean, tol, tol_mean)
+    assert len(near_ties) <= 1, near_ties
+
+
+def test_opt13b_full_depth_batch_invariance(X):
+    from workload import MODELS, weight_seed
+    reqs = _bench_requests(24)
+    ctx = X.Context(MODELS["opt-13b"], weight_seed(2))
+    dump = [0, 11, 23]
+    a = ctx.run(X.rra_schedule(4, 8, 2), reqs, dump=dump, slot_ctx=592)
+    b = ctx.run(X.rra_schedule(24, 24, 8), reqs, dump=dump, slot_ctx=592)
+    assert a[0] == b[0]
+    for r in dump:
+        assert np.array_equal(a[3][r], b[3][r]), r
+        assert np.all(np.isfinite(a[3][r]))
