@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
                                                               const __grid_constant__ CUtensorMap tmV,
                                                               FmhaParams p) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem;
@@ -315,7 +316,7 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   const CUtensorMap tk = make_tmap_bf16(a.kc, a.kv_rows, FD, FD, 128);
   const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 128);
   dim3 grid((a.max_len + FQ - 1) / FQ, a.H, a.R);
-  fmha_prefill_kernel<<<grid, 256, FMHA_SMEM, st>>>(tq, tk, tv, p);
+  launch_pdl(fmha_prefill_kernel, dim3(grid), dim3(256), FMHA_SMEM, st, tq, tk, tv, p);
   EXG_CHECK_LAUNCH();
   return true;
 }

@@ -54,6 +54,7 @@ __global__ void embed_decode_kernel(float* __restrict__ x, const int32_t* __rest
                                     const int32_t* __restrict__ slot, const int32_t* __restrict__ pos,
                                     const bf16* __restrict__ tok, const bf16* __restrict__ pe, int d) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   const int i = blockIdx.x;
   const int64_t id = last_tok[slot[i]];
   const bf16* b = pe ? pe + (int64_t)pos[i] * d : nullptr;
@@ -70,6 +71,8 @@ __global__ void __launch_bounds__(256) argmax_scatter_kernel(const float* __rest
                                                               const int32_t* __restrict__ out_off,
                                                               int32_t* __restrict__ last_tok,
                                                               int32_t* __restrict__ out_tokens, int32_t* err) {
+  griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   __shared__ float sv[256];
   __shared__ int si[256];
   const float* row = logits + (int64_t)blockIdx.x * V;
@@ -109,6 +112,7 @@ __global__ void __launch_bounds__(256) argmax_scatter_kernel(const float* __rest
 __global__ void add_bias_resid_kernel(float* __restrict__ x, const float* __restrict__ p,
                                       const bf16* __restrict__ bias, int64_t n, int d) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     x[i] = x[i] + (bias ? p[i] + bf2f(bias[i % d]) : p[i]);
 }
@@ -124,7 +128,7 @@ T* carve(uint8_t*& p, size_t n) {
 void add_bias_resid(float* x, const float* p, const bf16* bias, int rows, int d, cudaStream_t st) {
   const int64_t n = (int64_t)rows * d;
   if (n <= 0) return;
-  add_bias_resid_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(x, p, bias, n, d);
+  launch_pdl(add_bias_resid_kernel, dim3((int)std::min<int64_t>((n + 255) / 256, 148 * 8)), dim3(256), 0, st, x, p, bias, n, d);
   EXG_CHECK_LAUNCH();
 }
 
@@ -672,7 +676,7 @@ void Engine::embed_decode(const DecodeBatch& db) {
   if (B > cap_rows_) throw std::invalid_argument("decode batch exceeds workspace");
   if (S_.embed && B > 0) {
     // T5: no position embedding (pos_emb_ null)
-    embed_decode_kernel<<<B, 256, 0, st_>>>(x_, last_tok_, db.slot, db.pos, tok_emb_, pos_emb_, D.d);
+    launch_pdl(embed_decode_kernel, dim3(B), dim3(256), 0, st_, x_, last_tok_, db.slot, db.pos, tok_emb_, pos_emb_, D.d);
     EXG_CHECK_LAUNCH();
   }
 }
@@ -698,7 +702,7 @@ void Engine::head_decode(const DecodeBatch& db) {
     e.out_f32 = logits_;
     e.ldo = D.V;
     linear_dec(h_, D.d, B, tok_emb_, D.V, D.d, e);
-    argmax_scatter_kernel<<<B, 256, 0, st_>>>(logits_, D.V, db.slot, db.out_off, last_tok_, db.out_tokens, err_);
+    launch_pdl(argmax_scatter_kernel, dim3(B), dim3(256), 0, st_, logits_, D.V, db.slot, db.out_off, last_tok_, db.out_tokens, err_);
     EXG_CHECK_LAUNCH();
   }
 }

@@ -558,6 +558,7 @@ template <int BN, int SWAP>
 __global__ void __launch_bounds__(128) streamk_reduce_kernel(const float* __restrict__ partial, int M, int N, Work w,
                                                              EpiParams ep) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   const int tile = blockIdx.x, m = tile % w.tiles_m, n = tile / w.tiles_m;
   const int64_t x0 = (int64_t)m * w.nkb;
   const int nseg = sk_owner(w, x0 + w.nkb - 1) - sk_owner(w, x0) + 1;
@@ -642,7 +643,7 @@ void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wb
   EXG_CHECK_LAUNCH();
   if (SWAP && !inkernel) {
     dim3 grid(w.tiles_m * w.tiles_n, BN / 32);
-    streamk_reduce_kernel<BN, SWAP><<<grid, 128, 0, st>>>(partial, M, N, w, ep);
+    launch_pdl(streamk_reduce_kernel<BN, SWAP>, dim3(grid), dim3(128), 0, st, partial, M, N, w, ep);
     EXG_CHECK_LAUNCH();
   }
 }

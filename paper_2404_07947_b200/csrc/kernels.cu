@@ -46,6 +46,7 @@ void weightgen(bf16* dst, int64_t rows, int64_t cols, int64_t ld, const GenParam
 __global__ void embed_kernel(float* __restrict__ x, const int32_t* __restrict__ ids, const int32_t* __restrict__ pos,
                              const bf16* __restrict__ tok, const bf16* __restrict__ pe, int d, int tok_blocked) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   const int t = blockIdx.x;
   const int64_t id = ids[t];
   const bf16* b = pe ? pe + (int64_t)pos[t] * d : nullptr;
@@ -58,7 +59,7 @@ __global__ void embed_kernel(float* __restrict__ x, const int32_t* __restrict__ 
 void embed(float* x, const int32_t* ids, const int32_t* pos, const bf16* tok_emb, const bf16* pos_emb, int T, int d,
            cudaStream_t st, int tok_blocked) {
   if (T <= 0) return;
-  embed_kernel<<<T, 256, 0, st>>>(x, ids, pos, tok_emb, pos_emb, d, tok_blocked);
+  launch_pdl(embed_kernel, dim3(T), dim3(256), 0, st, x, ids, pos, tok_emb, pos_emb, d, tok_blocked);
   EXG_CHECK_LAUNCH();
 }
 
@@ -81,6 +82,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(bf16* __restrict__ y, in
                                                         int64_t ldx, const bf16* __restrict__ g,
                                                         const bf16* __restrict__ b, int d, float eps) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   __shared__ float red[8];
   const float* xr = x + (int64_t)blockIdx.x * ldx;
   float s = 0.f;
@@ -100,7 +102,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(bf16* __restrict__ y, in
 void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
                float eps, cudaStream_t st) {
   if (T <= 0) return;
-  layernorm_kernel<<<T, 256, 0, st>>>(y, ldy, x, ldx, g, b, d, eps);
+  launch_pdl(layernorm_kernel, dim3(T), dim3(256), 0, st, y, ldy, x, ldx, g, b, d, eps);
   EXG_CHECK_LAUNCH();
 }
 
@@ -109,6 +111,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(bf16* __restrict__ y, int6
                                                       int64_t ldx, const bf16* __restrict__ g, int d, float eps,
                                                       float out_scale) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   __shared__ float red[8];
   const float* xr = x + (int64_t)blockIdx.x * ldx;
   float q = 0.f;
@@ -122,7 +125,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(bf16* __restrict__ y, int6
 void rmsnorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, int T, int d, float eps,
              float out_scale, cudaStream_t st) {
   if (T <= 0) return;
-  rmsnorm_kernel<<<T, 256, 0, st>>>(y, ldy, x, ldx, g, d, eps, out_scale);
+  launch_pdl(rmsnorm_kernel, dim3(T), dim3(256), 0, st, y, ldy, x, ldx, g, d, eps, out_scale);
   EXG_CHECK_LAUNCH();
 }
 
@@ -150,6 +153,8 @@ void rel_bias_table(float* tab, const bf16* rel, const int32_t* bucket, int n, i
 __global__ void kv_scatter_kernel(bf16* __restrict__ kc, bf16* __restrict__ vc, const bf16* __restrict__ qkv,
                                   const int32_t* __restrict__ slot, const int32_t* __restrict__ pos, int T, int H,
                                   int dh, int max_ctx) {
+  griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   const int inner = H * dh;
   const int chunks = inner / 8;  // 16-byte chunks per K (or V) row
   const int64_t n = (int64_t)T * 2 * chunks;
@@ -169,7 +174,7 @@ void kv_scatter(bf16* kc, bf16* vc, const bf16* qkv, const int32_t* slot, const 
   if (T <= 0) return;
   const int64_t n = (int64_t)T * 2 * (H * dh / 8);
   const int blocks = (int)std::min<int64_t>((n + 255) / 256, 148 * 16);
-  kv_scatter_kernel<<<blocks, 256, 0, st>>>(kc, vc, qkv, slot, pos, T, H, dh, max_ctx);
+  launch_pdl(kv_scatter_kernel, dim3(blocks), dim3(256), 0, st, kc, vc, qkv, slot, pos, T, H, dh, max_ctx);
   EXG_CHECK_LAUNCH();
 }
 
@@ -198,6 +203,7 @@ struct DecodeCfg {
 template <int DH>
 __global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   using C = DecodeCfg<DH>;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* sk = dsm;
@@ -351,6 +357,7 @@ __global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a) {
 template <int DH>
 __global__ void decode_combine_kernel(DecodeAttnArgs a) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   const int i = blockIdx.x / a.H, h = blockIdx.x % a.H;
   const int nk = a.n_keys[i];
   const int nsplit = (nk + a.split_len - 1) / a.split_len;
@@ -379,10 +386,10 @@ void decode_attention_t(const DecodeAttnArgs& a, cudaStream_t st) {
     attr = true;
   }
   dim3 grid(a.B * a.H, a.max_splits);
-  decode_attn_kernel<DH><<<grid, 128, C::SMEM, st>>>(a);
+  launch_pdl(decode_attn_kernel<DH>, dim3(grid), dim3(128), C::SMEM, st, a);
   EXG_CHECK_LAUNCH();
   if (a.max_splits > 1) {
-    decode_combine_kernel<DH><<<a.B * a.H, DH < 32 ? 32 : DH, 0, st>>>(a);
+    launch_pdl(decode_combine_kernel<DH>, dim3(a.B * a.H), dim3(DH < 32 ? 32 : DH), 0, st, a);
     EXG_CHECK_LAUNCH();
   }
 }
@@ -406,6 +413,7 @@ void decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
 template <int DH>
 __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   constexpr int QPB = 32, LPQ = 4, DPL = DH / LPQ, KTILE = 32;
   __shared__ __align__(16) bf16 ks[KTILE][DH];
   __shared__ __align__(16) bf16 vs[KTILE][DH];
@@ -486,9 +494,9 @@ void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st) {
   if (prefill_attention_tc(a, st)) return;
   dim3 grid((a.max_len + 31) / 32, a.H, a.R);
   switch (a.dh) {
-    case 16: prefill_attn_kernel<16><<<grid, 128, 0, st>>>(a); break;
-    case 64: prefill_attn_kernel<64><<<grid, 128, 0, st>>>(a); break;
-    case 128: prefill_attn_kernel<128><<<grid, 128, 0, st>>>(a); break;
+    case 16: launch_pdl(prefill_attn_kernel<16>, grid, dim3(128), 0, st, a); break;
+    case 64: launch_pdl(prefill_attn_kernel<64>, grid, dim3(128), 0, st, a); break;
+    case 128: launch_pdl(prefill_attn_kernel<128>, grid, dim3(128), 0, st, a); break;
     default: throw CudaError("prefill_attention: unsupported head dim");
   }
   EXG_CHECK_LAUNCH();
@@ -499,6 +507,8 @@ void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st) {
 // ============================================================================
 __global__ void __launch_bounds__(256) argmax_kernel(int32_t* __restrict__ out, const float* __restrict__ logits,
                                                       int64_t ld, int V, int32_t* err) {
+  griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   __shared__ float sv[256];
   __shared__ int si[256];
   const float* row = logits + (int64_t)blockIdx.x * ld;
@@ -533,7 +543,7 @@ __global__ void __launch_bounds__(256) argmax_kernel(int32_t* __restrict__ out, 
 
 void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, int32_t* err_flag, cudaStream_t st) {
   if (B <= 0) return;
-  argmax_kernel<<<B, 256, 0, st>>>(out, logits, ld, V, err_flag);
+  launch_pdl(argmax_kernel, dim3(B), dim3(256), 0, st, out, logits, ld, V, err_flag);
   EXG_CHECK_LAUNCH();
 }
 

@@ -51,6 +51,7 @@ struct PartPtrs {
 
 __global__ void sum_parts_kernel(PartPtrs pp, int64_t n) {
   griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     float s = pp.in[0][i];
     for (int r = 1; r < pp.n_in; ++r) s += pp.in[r][i];
@@ -59,7 +60,7 @@ __global__ void sum_parts_kernel(PartPtrs pp, int64_t n) {
 }
 
 void launch_sum(const PartPtrs& pp, int64_t n, cudaStream_t st) {
-  sum_parts_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 148 * 8), 256, 0, st>>>(pp, n);
+  launch_pdl(sum_parts_kernel, dim3((int)std::min<int64_t>((n + 255) / 256, 148 * 8)), dim3(256), 0, st, pp, n);
   EXG_CHECK_LAUNCH();
 }
 
