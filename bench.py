@@ -40,6 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 TASK = "S"
+COMM_ALPHA_S, COMM_BW = 10e-6, 700e9   # modeled p2p latency / bandwidth per GPU link set
 MODEL = "opt-13b"
 CONFIG_NO = 2
 B_E_MAX = 64
@@ -201,6 +202,8 @@ def main():
     ap.add_argument("--little", type=int, default=1,
                     help="1: completion fraction by Little's law (SURVEY.md S3; DESIGN.md), 0: paper's E[1/ceil(S/N_D)]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plan-gpus", type=lambda v: [int(x) for x in v.split(",") if x], default=[2, 4, 8],
+                    help="cluster sizes for the scheduler's predicted multi-GPU plan")
     ap.add_argument("--dyn", type=float, default=0.1, help="dynamic workload adjustment threshold (0: skip the run)")
     ap.add_argument("--roofline-steps", type=int, default=1, help="extra steps with per-launch kernel events")
     ap.add_argument("--bounds", default="all", choices=["all", "headline"])
@@ -246,7 +249,10 @@ def main():
     ctxs = [1, 32, 64, 128, 192, 256, 320, 384, 448, 512, 592]
     tokens = [1, 16, 64, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768]
     t0 = time.perf_counter()
-    prof = ctx.profile(batch, ctxs, tokens, reps=3)
+    prof = ctx.profile(batch, ctxs, tokens, reps=3, tps=[1, 2, 4, 8])
+    # interconnect tables: alpha-beta model of NVLink 5 / NVSwitch (DESIGN.md
+    # reading; a single-GPU context cannot time them)
+    prof.comm_model(COMM_ALPHA_S, COMM_BW)
     t_prof = time.perf_counter() - t0
     if rank == 0:
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
@@ -367,6 +373,19 @@ def main():
                "mean_encode_batch": st_d["mean_encode_batch"], "mean_decode_batch": st_d["mean_decode_batch"],
                "variance": workload_variance(st_d), **sla(lat_d, L_head)}
 
+    # the scheduler's multi-GPU plan for this workload and bound (predicted by
+    # the XSimulator on the measured per-GPU tables + the modeled interconnect)
+    plan = {}
+    for n in args.plan_gpus:
+        try:
+            cl_n = X.cluster_spec(n, cl.mem_per_gpu_bytes, cl.workspace_bytes)
+            s_n, e_n = X.schedule_find(prof, ctx.mspec, cl_n, pin, pout, d.target_len, L_head * (1 - args.margin),
+                                       X.EXG_RRA | X.EXG_WAA_C, X.search_opts(b_e_max=B_E_MAX, little=args.little))
+            plan[str(n)] = {"predicted_tok_s": e_n.thrput_tok_s, "predicted_latency_s": e_n.latency_s,
+                            "schedule": s_n.as_dict()}
+        except X.ExgError as e:
+            plan[str(n)] = {"infeasible": str(e)}
+
     pk = peaks()
     # roofline of the dominant kernel class (time share) + decode attention
     dom = max(ktime, key=lambda k: ktime[k])
@@ -424,6 +443,8 @@ def main():
                     "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
             "clocks": clk.summary(),
+            "multi_gpu_plan": {"latency_bound_s": L_head, "comm": "modeled: alpha %.0f us, %.0f GB/s" %
+                               (COMM_ALPHA_S * 1e6, COMM_BW / 1e9), "predicted": plan},
             "workload_variance": workload_variance(var_st),
             "dyn_adjust": dyn,
             "bounds": other,

@@ -204,6 +204,13 @@ void exg_destroy(exg_ctx* ctx);
 exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profile** out);
 /* profile-v1 text file ("%.17g" numbers, lossless). */
 exg_status exg_profile_save(const exg_profile* p, const char* path);
+/* Fill the communication tables from an alpha-beta model of the
+ * interconnect, for profiles taken on a single-GPU context (a reading,
+ * DESIGN.md §3): pp_sync(bytes) = alpha + bytes/bw; for every TP degree t > 1
+ * of the profile, tp_sync[t](bytes) = alpha + (t-1)*bytes/bw (each rank
+ * sends its fp32 partial to t-1 peers over its own link).  Byte grid 1 KB ..
+ * 64 GB, factor 4.  Replaces existing tables. */
+exg_status exg_profile_comm_model(exg_profile* p, double alpha_s, double bw_bytes_per_s);
 exg_status exg_profile_load(const char* path, exg_profile** out);
 void exg_profile_free(exg_profile* p);
 

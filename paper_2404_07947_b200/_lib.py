@@ -125,6 +125,7 @@ _SIGS = {
     "exg_profile_save": (C.c_int, [_P, C.c_char_p]),
     "exg_profile_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
     "exg_profile_free": (None, [_P]),
+    "exg_profile_comm_model": (C.c_int, [_P, C.c_double, C.c_double]),
     "exg_simulate": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
                                C.POINTER(exg_pmf), C.c_int32, C.POINTER(exg_schedule), C.POINTER(exg_estimate)]),
     "exg_schedule_resolve": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec),
@@ -243,11 +244,11 @@ class Context:
         except Exception:
             pass
 
-    def profile(self, batch, ctx, tokens, reps: int = 3) -> "Profile":
-        arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.int32)) for a in (batch, ctx, tokens, [1])]
+    def profile(self, batch, ctx, tokens, reps: int = 3, tps=(1,)) -> "Profile":
+        arrs = [np.ascontiguousarray(np.asarray(a, dtype=np.int32)) for a in (batch, ctx, tokens, tps)]
         ptr = lambda a: a.ctypes.data_as(C.POINTER(C.c_int32))
         g = exg_profile_grid(len(arrs[0]), ptr(arrs[0]), len(arrs[1]), ptr(arrs[1]), len(arrs[2]), ptr(arrs[2]),
-                             1, ptr(arrs[3]), reps)
+                             len(arrs[3]), ptr(arrs[3]), reps)
         h = _P()
         check(lib().exg_profile_run(self.h, C.byref(g), C.byref(h)))
         return Profile(h)
@@ -340,6 +341,10 @@ class Profile:
 
     def save(self, path: str):
         check(lib().exg_profile_save(self.h, path.encode()))
+
+    def comm_model(self, alpha_s: float, bw_bytes_per_s: float):
+        """Fill tp_sync / pp_sync from an alpha-beta interconnect model."""
+        check(lib().exg_profile_comm_model(self.h, alpha_s, bw_bytes_per_s))
 
     def __del__(self):
         try:

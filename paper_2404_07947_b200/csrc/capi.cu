@@ -203,7 +203,7 @@ exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profi
     if (!ctx || !grid || !out) throw std::invalid_argument("null argument");
     auto p = std::make_unique<exg_profile>();
     if (!ctx->engine) throw std::invalid_argument("profile on a single-GPU context (cluster.n_gpus = 1)");
-    exg::profile_layers(*ctx->engine, *grid, &p->p);
+    exg::profile_layers(*ctx->engine, ctx->spec, *grid, &p->p);
     *out = p.release();
     return EXG_OK;
   });
@@ -215,6 +215,31 @@ exg_status exg_profile_save(const exg_profile* p, const char* path) {
     std::ofstream f(path);
     if (!f) throw std::invalid_argument(std::string("cannot open ") + path);
     f << p->p.dumps();
+    return EXG_OK;
+  });
+}
+
+exg_status exg_profile_comm_model(exg_profile* p, double alpha_s, double bw_bytes_per_s) {
+  return guarded([&] {
+    if (!p) throw std::invalid_argument("null profile");
+    if (!(alpha_s >= 0) || !(bw_bytes_per_s > 0)) throw std::invalid_argument("bad alpha / bandwidth");
+    exg::plan::Table1D pp;
+    for (double b = 1024.0; b <= 64.0 * (1ull << 30); b *= 4.0) {
+      pp.x.push_back(b);
+      pp.t.push_back(alpha_s + b / bw_bytes_per_s);
+    }
+    p->p.pp_sync = pp;
+    p->p.has_pp = true;
+    p->p.tp_sync.clear();
+    for (int t : p->p.tps) {
+      if (t <= 1) continue;
+      exg::plan::Table1D tb;
+      for (double b : pp.x) {
+        tb.x.push_back(b);
+        tb.t.push_back(alpha_s + (t - 1) * b / bw_bytes_per_s);
+      }
+      p->p.tp_sync[t] = tb;
+    }
     return EXG_OK;
   });
 }

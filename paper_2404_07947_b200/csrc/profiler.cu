@@ -64,8 +64,8 @@ struct Timer {
 };
 }  // namespace
 
-void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
-  if (g.n_batch < 1 || g.n_ctx < 1 || g.n_tokens < 1) throw std::invalid_argument("empty profile grid");
+// attention and "rest" tables of one layer of engine E under key t
+static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profile& P) {
   const Dims& D = E.dims();
   const int reps = std::max(1, g.reps);
   std::vector<int> bs(g.batch, g.batch + g.n_batch), cs(g.ctx, g.ctx + g.n_ctx), ts(g.tokens, g.tokens + g.n_tokens);
@@ -104,9 +104,6 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
   EXG_CUDA(cudaMemcpy(d_p0, h_p0.data(), (slots + 1) * 4, cudaMemcpyHostToDevice));
 
   Timer tm(st);
-  plan::Profile& P = *out;
-  P = plan::Profile();
-  P.tps = {1};
   plan::Table2D ae, ad;
   ae.b.assign(bs.begin(), bs.end());
   ae.c.assign(cs.begin(), cs.end());
@@ -151,8 +148,8 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
       ad.t[ib][ic] = tm.median(reps, [&] { E.layer_decode(0, db, true, false); });
     }
   }
-  P.attn[{"enc", 1}] = ae;
-  P.attn[{"dec", 1}] = ad;
+  P.attn[{"enc", t}] = ae;
+  P.attn[{"dec", t}] = ad;
   plan::Table1D re, rd;
   for (int T : ts) {
     EncodeBatch eb;
@@ -183,10 +180,44 @@ void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out) {
     rd.x.push_back(b);
     rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }));
   }
-  P.rest[{"enc", 1}] = re;
-  P.rest[{"dec", 1}] = rd;
+  P.rest[{"enc", t}] = re;
+  P.rest[{"dec", t}] = rd;
   EXG_CUDA(cudaStreamSynchronize(st));
   cudaFree(d);
+}
+
+// Every requested TP degree t ("all possible parallel
+// configurations"): t = 1 times the context's own layer 0; t > 1 builds a
+// one-layer shard engine of TP rank 0 (H/t heads, d_ff/t FFN columns -- the
+// per-GPU work of a TP group) and times it the same way.  The all-reduce
+// itself is the tp_sync table (exg_profile_comm_model / a multi-rank profile).
+void profile_layers(Engine& E, const exg_model_spec& spec, const exg_profile_grid& g, plan::Profile* out) {
+  if (g.n_batch < 1 || g.n_ctx < 1 || g.n_tokens < 1) throw std::invalid_argument("empty profile grid");
+  std::vector<int> tps;
+  for (int i = 0; i < g.n_tp; ++i) tps.push_back(g.tp[i]);
+  if (tps.empty()) tps.push_back(1);
+  for (size_t i = 0; i < tps.size(); ++i)
+    if (tps[i] < 1 || (i && tps[i] <= tps[i - 1])) throw std::invalid_argument("grid TP degrees must be increasing");
+  plan::Profile& P = *out;
+  P = plan::Profile();
+  for (int t : tps) {
+    if (t == 1) {
+      profile_one(E, 1, g, P);
+    } else {
+      if (E.encdec()) throw std::invalid_argument("T5: tensor-parallel profiles are not built yet");
+      if (spec.n_heads % t || spec.d_ff % t) throw std::invalid_argument("TP degree must divide n_heads and d_ff");
+      EngineShard sh;
+      sh.l0 = 0;
+      sh.l1 = 1;
+      sh.tp = t;
+      sh.tp_rank = 0;
+      sh.embed = false;
+      sh.head = false;
+      Engine shard(spec, E.device(), sh);
+      profile_one(shard, t, g, P);
+    }
+    P.tps.push_back(t);
+  }
 }
 
 }  // namespace exg

@@ -5,5 +5,5 @@
 #include "planner.h"
 
 namespace exg {
-void profile_layers(Engine& E, const exg_profile_grid& g, plan::Profile* out);
+void profile_layers(Engine& E, const exg_model_spec& spec, const exg_profile_grid& g, plan::Profile* out);
 }

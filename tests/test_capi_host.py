@@ -193,3 +193,26 @@ def test_error_statuses(L, tmp_path):
     open(bad, "w").write("profile-v1\ntp 1 1\nbogus\n")
     with pytest.raises(L.ExgError):
         L.Profile.load(bad)
+
+
+def test_profile_comm_model_tables(L, tmp_path):
+    """exg_profile_comm_model: pp_sync = alpha + bytes/bw, tp_sync[t] = alpha +
+    (t-1) bytes/bw for every t > 1 of the profile (DESIGN.md §3 reading)."""
+    from oracle import simulator as sim
+    spec, m, prof, d, cl = _setup("G", "opt-66b", 8)
+    P, *_ = _c_objects(L, spec, prof, d, cl, tmp_path)
+    alpha, bw = 12e-6, 450e9
+    P.comm_model(alpha, bw)
+    path = str(tmp_path / "cm.txt")
+    P.save(path)
+    Q = sim.Profile.loads(open(path).read())
+    xs = Q.pp_sync.x
+    assert xs[0] == 1024.0 and xs[-1] == 64.0 * 2 ** 30
+    for x, t in zip(xs, Q.pp_sync.t):
+        assert t == alpha + x / bw
+    for tp in prof.tps:
+        if tp > 1:
+            for x, t in zip(Q.tp_sync[tp].x, Q.tp_sync[tp].t):
+                assert t == alpha + (tp - 1) * x / bw
+    with pytest.raises(L.ExgError):
+        P.comm_model(alpha, 0.0)

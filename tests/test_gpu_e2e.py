@@ -126,3 +126,20 @@ def test_dynamic_workload_adjustment_keeps_results(setup):
     st = b[2]
     assert st["mean_encode_batch"] > 0 and st["dec_stage_mean_s"] > 0 and st["dec_stage_p99dev_s"] >= 0
     assert a[2]["mean_encode_batch"] == pytest.approx(len(many) / a[2]["encode_phases"])
+
+
+def test_profile_tp_shards(setup, tmp_path):
+    """XProfiler over TP degrees: t > 1 times a one-layer shard
+    of TP rank 0; every requested degree gets attention and rest tables."""
+    X, T, spec, W, reqs, ctx, ora = setup
+    from oracle import simulator as sim
+    prof = ctx.profile([1, 4, 8], [16, 48], [16, 64, 256], reps=1, tps=[1, 2, 4])
+    path = str(tmp_path / "p.txt")
+    prof.comm_model(10e-6, 700e9)
+    prof.save(path)
+    P = sim.Profile.loads(open(path).read())
+    assert P.tps == [1, 2, 4]
+    for t in (1, 2, 4):
+        for ph in ("enc", "dec"):
+            assert np.all(np.array(P.attn[(ph, t)].t) > 0) and np.all(np.array(P.rest[(ph, t)].t) > 0)
+    assert 2 in P.tp_sync and 4 in P.tp_sync and P.pp_sync is not None
