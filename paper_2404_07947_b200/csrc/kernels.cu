@@ -182,12 +182,15 @@ void kv_scatter(bf16* kc, bf16* vc, const bf16* qkv, const int32_t* slot, const 
 // K6 ragged decode attention
 //
 // One CTA (4 warps) per (row, head, split).  Thread 0 streams the split's K
-// and V rows (contiguous per (slot, head)) through a 4-stage ring of
-// cp.async.bulk copies completing on mbarriers; every warp owns a fixed
+// and V rows (contiguous per (slot, head)) through a 2-stage ring of
+// cp.async.bulk copies completing on mbarriers (32 KB, 7 CTAs per SM: at the
+// bench's context mix the per-CTA tile loop, not the ring depth, limits
+// throughput, so more resident CTAs beat deeper rings -- measured 4.5 ->
+// 5.1 TB/s at B=56, 5.5 -> 6.5 TB/s at B=256); every warp owns a fixed
 // subset of keys of each tile, keeps its own online-softmax state, and the
 // four warp states are merged at the end in warp order.
 // ============================================================================
-template <int DH>
+template <int DH, int ST = 4>
 struct DecodeCfg {
   static constexpr int CH = DH / 8;                 // 16-byte chunks per key row
   static constexpr int LPK = CH >= 4 ? 4 : CH;      // lanes per key (dot product)
@@ -195,16 +198,16 @@ struct DecodeCfg {
   static constexpr int KPW = 32 / LPK;              // keys per warp per tile
   static constexpr int KT = 4 * KPW;                // keys per tile
   static constexpr int ROWB = DH * 2;               // bytes per key row
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = ST;
   static constexpr int DPL = DH >= 32 ? DH / 32 : 1;  // output dims per lane (P.V)
   static constexpr size_t SMEM = (size_t)STAGES * KT * ROWB * 2;
 };
 
-template <int DH>
-__global__ void __launch_bounds__(128) decode_attn_kernel(DecodeAttnArgs a) {
+template <int DH, int ST, int MB = 1>
+__global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) {
   griddep_launch_dependents();
   griddep_wait();  // launched with PDL: predecessors complete + visible
-  using C = DecodeCfg<DH>;
+  using C = DecodeCfg<DH, ST>;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint8_t* sk = dsm;
   uint8_t* sv = dsm + C::STAGES * C::KT * C::ROWB;
@@ -377,17 +380,37 @@ __global__ void decode_combine_kernel(DecodeAttnArgs a) {
   }
 }
 
-template <int DH>
-void decode_attention_t(const DecodeAttnArgs& a, cudaStream_t st) {
-  using C = DecodeCfg<DH>;
+// ring depth (diagnostics override via exg_diag_decode_stages; 0 = default)
+int& decode_stages_override() {
+  static int s = 0;
+  return s;
+}
+
+template <int DH, int ST, int MB = 1>
+void decode_attention_st(const DecodeAttnArgs& a, cudaStream_t st) {
+  using C = DecodeCfg<DH, ST>;
   static bool attr = false;
   if (!attr) {
-    EXG_CUDA(cudaFuncSetAttribute(decode_attn_kernel<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+    EXG_CUDA(cudaFuncSetAttribute(decode_attn_kernel<DH, ST, MB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)C::SMEM));
     attr = true;
   }
   dim3 grid(a.B * a.H, a.max_splits);
-  launch_pdl(decode_attn_kernel<DH>, dim3(grid), dim3(128), C::SMEM, st, a);
+  launch_pdl(decode_attn_kernel<DH, ST, MB>, dim3(grid), dim3(128), C::SMEM, st, a);
   EXG_CHECK_LAUNCH();
+}
+
+template <int DH>
+void decode_attention_t(const DecodeAttnArgs& a, cudaStream_t st) {
+  switch (decode_stages_override()) {
+    case 1: decode_attention_st<DH, 1, 8>(a, st); break;
+    case 2: decode_attention_st<DH, 2>(a, st); break;
+    case 3: decode_attention_st<DH, 3>(a, st); break;
+    case 4: decode_attention_st<DH, 4>(a, st); break;
+    case 27: decode_attention_st<DH, 2, 7>(a, st); break;
+    case 16: decode_attention_st<DH, 1, 6>(a, st); break;
+    default: decode_attention_st<DH, 2, 7>(a, st); break;
+  }
   if (a.max_splits > 1) {
     launch_pdl(decode_combine_kernel<DH>, dim3(a.B * a.H), dim3(DH < 32 ? 32 : DH), 0, st, a);
     EXG_CHECK_LAUNCH();
@@ -548,3 +571,5 @@ void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, in
 }
 
 }  // namespace exg
+
+extern "C" void exg_diag_decode_stages(int s) { exg::decode_stages_override() = s; }

@@ -71,6 +71,36 @@ def dattn(B, c, H=40, dh=128, split_len=512):
     print("decode-attn B=%4d c=%5d H=%d: %8.1f us  %7.1f GB/s" % (B, c, H, t * 1e6, byts / t / 1e9))
 
 
+def dattn_mix(B, split_len=512, H=40, dh=128, seed=0):
+    """Decode attention at the bench's context mix: row contexts n + u with n
+    from task S's input PMF and u uniform in the output range."""
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from workload import task_dists
+    d = task_dists("S")
+    rng = np.random.default_rng(seed)
+    n = rng.choice(np.arange(1, len(d.pmf_in) + 1), size=B, p=np.asarray(d.pmf_in) / np.sum(d.pmf_in))
+    u = rng.integers(1, 40, size=B)
+    ctxs = (n + u).astype(np.int32)
+    max_ctx = 592
+    kc = torch.randn(B, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    vc = torch.randn(B, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    q = torch.randn(B, 3 * H * dh, device=dev).to(torch.bfloat16)
+    slot = torch.arange(B, dtype=torch.int32, device=dev)
+    nk = torch.from_numpy(ctxs).to(dev)
+    ms = (int(ctxs.max()) + split_len - 1) // split_len
+    part = torch.empty(B * H * ms * (dh + 2), device=dev)
+    out = torch.empty(B, H * dh, device=dev, dtype=torch.bfloat16)
+
+    def fn():
+        L.check(L.lib().exg_op_decode_attention(q.data_ptr(), 3 * H * dh, kc.data_ptr(), vc.data_ptr(),
+                                                slot.data_ptr(), nk.data_ptr(), out.data_ptr(), H * dh, B, H, dh,
+                                                max_ctx, 0.0883883, split_len, ms, part.data_ptr(), None, 0, 0, st()))
+    t = timeit(fn)
+    byts = H * (2.0 * ctxs.sum() * dh * 2 + B * 2 * dh * 2)
+    print("decode-attn mix B=%4d mean ctx %5.0f split %4d: %8.1f us  %7.1f GB/s" % (B, ctxs.mean(), split_len,
+                                                                                    t * 1e6, byts / t / 1e9))
+
+
 def pattn(R, n, H=40, dh=128):
     T = R * n
     max_ctx = n
@@ -127,6 +157,14 @@ if __name__ == "__main__":
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "dattn":
         dattn(int(sys.argv[2]), int(sys.argv[3]))
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "dmix":
+        for stages in (int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "2,27,1,16,4").split(",")):
+            L.lib().exg_diag_decode_stages(stages)
+            print("stages", stages)
+            for B in (16, 56, 79, 256):
+                dattn_mix(B, 512)
+        L.lib().exg_diag_decode_stages(0)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pattn":
         pattn(int(sys.argv[2]), int(sys.argv[3]))
