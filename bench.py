@@ -41,6 +41,9 @@ sys.path.insert(0, ROOT)
 
 TASK = "S"
 COMM_ALPHA_S, COMM_BW = 10e-6, 700e9   # modeled p2p latency / bandwidth per GPU link set
+METRIC = "output tokens/s under latency bound (BASELINE.json; 70th-pctl bound headline)"
+WORKLOAD = ("config 2: OPT-13B (seeded random init), task S (in 256+-252<=512, out 32+-13<=80, p99 63), "
+            "RRA on 1xB200 per rank")
 MODEL = "opt-13b"
 CONFIG_NO = 2
 B_E_MAX = 64
@@ -179,11 +182,11 @@ def run_reference(args, rank, world):
     value = float(np.mean(vals))
     sample = ("1 task-S request (64 input tokens, 4 output tokens) through the first 2 of 40 OPT-13B layers "
               "(same seeded weights) + embeddings + LM head, oracle mode (iii); tokens/s scaled by 2/40")
-    out = {"metric": "output tokens/s under latency bound", "value": value, "unit": "output tokens/s",
+    out = {"metric": METRIC, "value": value, "unit": "output tokens/s",
            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "config 2: OPT-13B, task S, RRA on 1xB200 (oracle sample)"},
+           "config": {"workload": WORKLOAD, "oracle_sample": "first 2 of 40 layers, scaled by 2/40"},
            "cpu_baseline": {"value": value, "unit": "output tokens/s", "cores": cpu_cores(), "kind": "oracle",
                             "sample": sample},
            "e2e": {"value": value, "unit": "output tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -421,12 +424,11 @@ def main():
 
     if rank == 0:
         out = {
-            "metric": "output tokens/s under latency bound (BASELINE.json; 70th-pctl bound headline)",
+            "metric": METRIC,
             "value": value, "unit": "output tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dev_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "config 2: OPT-13B (seeded random init), task S (in 256+-252<=512, "
-                                   "out 32+-13<=80, p99 63), RRA on 1xB200 per rank",
+            "config": {"workload": WORKLOAD,
                        "requests_per_step": args.requests, "latency_bound_s": L_head,
                        "bound_rule": "70th pctl of static-batch latencies (PAPER.md:490)",
                        "schedule": sched.as_dict(), "predicted_tok_s": est.thrput_tok_s,
