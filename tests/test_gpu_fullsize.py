@@ -102,3 +102,42 @@ def test_opt13b_full_depth_batch_invariance(X):
     for r in dump:
         assert np.array_equal(a[3][r], b[3][r]), r
         assert np.all(np.isfinite(a[3][r]))
+
+
+# ---------------------------------------------------------------------------
+# configs 4 and 5 at their models' full width: one layer of OPT-66B under WAA
+# with a TP-2 decoder group, one layer of GPT-3 175B under RRA with TP 8 --
+# every GPU of the layout emulated on this device with exactly its shard --
+# vs the oracle (calibrated bar as above) on short requests
+# ---------------------------------------------------------------------------
+def _width_case(X, model, layout, strategy, b_e, b_d, tp, n_enc, n_gpus):
+    from oracle import transformer as T
+    from workload import MODELS, ModelSpec, make_requests, uniform_pmf, weight_seed
+    full = MODELS[model]
+    spec = ModelSpec(model + "-1layer", full.arch, 0, 1, full.d_model, full.n_heads, full.d_head, full.d_ff,
+                     full.vocab, full.max_pos)
+    reqs = make_requests(4, uniform_pmf(24, 48), uniform_pmf(2, 3), full.vocab, 0xE6E10004)
+    from paper_2404_07947_b200 import _lib
+    ctx = X.Context(spec, weight_seed(4), cluster=X.cluster_spec(n_gpus))
+    tp_gpus = sum(g[1] for g in layout if g[1] > 1)
+    s = _lib.make_schedule(strategy, b_e, b_d, layout, n_d=2, b_m=0, n_enc_gpus=n_enc, tp_degree=tp, tp_gpus=tp_gpus)
+    toks, lat, st, lg = ctx.run(s, reqs, dump=range(len(reqs)))
+    W = T.Weights(spec, weight_seed(4), cache_fp64=False)
+    ora = T.greedy_kv(W, reqs, "bf16", record_logits=True)
+    o32 = T.greedy_kv(W, reqs, "bf16", record_logits=True, accum="fp32")
+    for r, q in enumerate(reqs):
+        cal = max(float(np.abs(o32.logits[r][t] - ora.logits[r][t]).max()) for t in range(q.output_len))
+        tol = max(TOL, 2 * cal)
+        for t in range(q.output_len):
+            assert np.abs(lg[r][t] - ora.logits[r][t]).max() <= tol, (model, r, t, tol)
+            if toks[r][t] != ora.tokens[r][t]:
+                assert ora.margins[r][t] <= 2 * tol, (model, r, t)
+                break
+
+
+def test_config4_opt66b_width_waa_tp2(X):
+    _width_case(X, "opt-66b", [(0, 1, 0, 1), (1, 2, 0, 1)], X.EXG_WAA_C, 2, 4, 2, 1, 3)
+
+
+def test_config5_gpt3_width_rra_tp8(X):
+    _width_case(X, "gpt3-175b", [(0, 8, 0, 1)], X.EXG_RRA, 2, 4, 8, 0, 8)
