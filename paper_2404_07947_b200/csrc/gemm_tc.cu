@@ -21,6 +21,8 @@
 
 #include <mutex>
 
+#include <vector>
+
 #include "gemm_tc.cuh"
 
 namespace exg {
@@ -48,6 +50,20 @@ PFN_encodeTiled_t encode_fn() {
 int& gemm_debug_flags() {
   static int f = 0;
   return f;
+}
+
+// g_dbg kernel argument: the flags, plus the launch sequence number when
+// span recording (bit 4) is on
+int& gemm_span_seq() {
+  static int n = 0;
+  return n;
+}
+int gemm_dbg_arg(bool decode) {
+  const int f = gemm_debug_flags();
+  if (!(f & 16)) return f;
+  if (!decode || gemm_span_seq() >= 4096) return f & ~16;   // decode launches only, first 4096
+  const int seq = gemm_span_seq()++;
+  return (f & 0xff) | (seq << 8);
 }
 
 int num_sms() {
@@ -260,6 +276,9 @@ struct EpiCfg {
 //   0 entry, 1 setup done, 2 producer past griddepcontrol.wait, 3 first full
 //   stage at the MMA warp, 4 last MMA commit, 5 epilogue done, 6 exit
 __device__ unsigned long long g_gemm_tl[256 * 8];
+// flag bit 4: in-situ launch spans -- earliest CTA entry / latest CTA exit of
+// launch number (g_dbg >> 8) & 4095 (exg_diag_gemm_spans)
+__device__ unsigned long long g_span_start[4096], g_span_end[4096], g_span_dep[4096];
 __device__ __forceinline__ void tl_mark(int dbg, int k) {
   if (dbg & 4) {
     unsigned long long t;
@@ -279,6 +298,11 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
   auto epi_bar = [] { asm volatile("bar.sync 1, %0;" ::"n"(32 * EpiCfg<SWAP>::WARPS) : "memory"); };
   griddep_launch_dependents();
   if (threadIdx.x == 0) tl_mark(g_dbg, 0);
+  if ((g_dbg & 16) && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMin(&g_span_start[(g_dbg >> 8) & 4095], t);
+  }
   constexpr int B_BYTES = BN * BK * 2;
   constexpr uint32_t TMEM_COLS =
       (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
@@ -359,6 +383,11 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
           if (!waited && g >= STAGES) {
             griddep_wait();
             tl_mark(g_dbg, 2);
+            if (g_dbg & 16) {
+              unsigned long long t;
+              asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+              atomicMin(&g_span_dep[(g_dbg >> 8) & 4095], t);
+            }
             for (int i = 0; i < npend; ++i) issue_x(i, pend[i][0], pend[i][1], pend[i][2]);
             waited = true;
           }
@@ -378,6 +407,11 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
       if (!waited) {
         griddep_wait();
         tl_mark(g_dbg, 2);
+        if (g_dbg & 16) {
+          unsigned long long t;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+          atomicMin(&g_span_dep[(g_dbg >> 8) & 4095], t);
+        }
         for (int i = 0; i < npend; ++i) issue_x(i, pend[i][0], pend[i][1], pend[i][2]);
       }
     }
@@ -512,6 +546,11 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
     tmem_dealloc(tmem, TMEM_COLS);
   }
   if (threadIdx.x == 0) tl_mark(g_dbg, 6);
+  if ((g_dbg & 16) && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    atomicMax(&g_span_end[(g_dbg >> 8) & 4095], t);
+  }
 }
 
 // Ring depth: up to 8 stages within ~200 KB (one CTA per SM).  Measured: a
@@ -639,7 +678,7 @@ void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wb
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   EXG_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, S, SWAP>, tx, Wb, M, N, n_wblk, w, ep, partial, counters,
-                              inkernel ? 1 : 0, gemm_debug_flags()));
+                              inkernel ? 1 : 0, gemm_dbg_arg(SWAP)));
   EXG_CHECK_LAUNCH();
   if (SWAP && !inkernel) {
     dim3 grid(w.tiles_m * w.tiles_n, BN / 32);
@@ -725,6 +764,21 @@ void linear(const LinearArgs& a, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
+// span recording: reset clears the arrays and the launch counter; read copies
+// min(n, 4096) spans (ns) and returns the number of launches recorded
+extern "C" int exg_diag_gemm_spans_reset() {
+  std::vector<unsigned long long> lo(4096, ~0ull), hi(4096, 0ull);
+  exg::gemm_span_seq() = 0;
+  if (cudaMemcpyToSymbol(exg::g_span_start, lo.data(), sizeof(unsigned long long) * 4096) != cudaSuccess) return 1;
+  if (cudaMemcpyToSymbol(exg::g_span_dep, lo.data(), sizeof(unsigned long long) * 4096) != cudaSuccess) return 1;
+  return cudaMemcpyToSymbol(exg::g_span_end, hi.data(), sizeof(unsigned long long) * 4096) == cudaSuccess ? 0 : 1;
+}
+extern "C" int exg_diag_gemm_spans(unsigned long long* start, unsigned long long* end, unsigned long long* dep) {
+  cudaMemcpyFromSymbol(dep, exg::g_span_dep, sizeof(unsigned long long) * 4096);
+  cudaMemcpyFromSymbol(start, exg::g_span_start, sizeof(unsigned long long) * 4096);
+  cudaMemcpyFromSymbol(end, exg::g_span_end, sizeof(unsigned long long) * 4096);
+  return exg::gemm_span_seq();
+}
 // per-CTA timeline marks of the last GEMM run with flag bit 2 ([256][8] ns)
 extern "C" int exg_diag_gemm_timeline(unsigned long long* out) {
   return cudaMemcpyFromSymbol(out, exg::g_gemm_tl, sizeof(unsigned long long) * 256 * 8) == cudaSuccess ? 0 : 1;

@@ -99,9 +99,99 @@ __global__ void __launch_bounds__(256) layernorm_kernel(bf16* __restrict__ y, in
   for (int j = threadIdx.x; j < d; j += 256) yr[j] = f2bf((xr[j] - mean) * rstd * bf2f(g[j]) + bf2f(b[j]));
 }
 
+// Row held in registers (NV float4 per thread): one global read of x, the
+// statistics from registers -- the decode-time LayerNorm is latency-bound
+// (a few dozen rows), so one load round trip instead of three matters.
+// RMS = 1: T5 RMSNorm with output scale (b unused).
+template <int NV, int RMS>
+__global__ void __launch_bounds__(256) norm_reg_kernel(bf16* __restrict__ y, int64_t ldy, const float* __restrict__ x,
+                                                       int64_t ldx, const bf16* __restrict__ g,
+                                                       const bf16* __restrict__ b, int d, float eps, float out_scale) {
+  griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
+  __shared__ float red[8];
+  const float4* xr = reinterpret_cast<const float4*>(x + (int64_t)blockIdx.x * ldx);
+  const int n4 = d >> 2;
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = threadIdx.x + k * 256;
+    v[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    s += RMS ? (v[k].x * v[k].x + v[k].y * v[k].y) + (v[k].z * v[k].z + v[k].w * v[k].w)
+             : (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+  float mean = 0.f, rstd;
+  if (RMS) {
+    rstd = rsqrtf(block_sum_256(s, red) / (float)d + eps);
+  } else {
+    mean = block_sum_256(s, red) / (float)d;
+    float q = 0.f;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      if (threadIdx.x + k * 256 >= n4) continue;
+      const float a = v[k].x - mean, bb = v[k].y - mean, c = v[k].z - mean, e = v[k].w - mean;
+      q += (a * a + bb * bb) + (c * c + e * e);
+    }
+    rstd = rsqrtf(block_sum_256(q, red) / (float)d + eps);
+  }
+  bf16* yr = y + (int64_t)blockIdx.x * ldy;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = threadIdx.x + k * 256;
+    if (i >= n4) continue;
+    const uint2 gr = reinterpret_cast<const uint2*>(g)[i];
+    const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gr.x));
+    const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gr.y));
+    float o0, o1, o2, o3;
+    if (RMS) {
+      o0 = v[k].x * rstd * g01.x * out_scale;
+      o1 = v[k].y * rstd * g01.y * out_scale;
+      o2 = v[k].z * rstd * g23.x * out_scale;
+      o3 = v[k].w * rstd * g23.y * out_scale;
+    } else {
+      const uint2 br = reinterpret_cast<const uint2*>(b)[i];
+      const float2 b01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.x));
+      const float2 b23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.y));
+      o0 = (v[k].x - mean) * rstd * g01.x + b01.x;
+      o1 = (v[k].y - mean) * rstd * g01.y + b01.y;
+      o2 = (v[k].z - mean) * rstd * g23.x + b23.x;
+      o3 = (v[k].w - mean) * rstd * g23.y + b23.y;
+    }
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(o0, o1), p1 = __floats2bfloat162_rn(o2, o3);
+    uint2 out;
+    out.x = *reinterpret_cast<uint32_t*>(&p0);
+    out.y = *reinterpret_cast<uint32_t*>(&p1);
+    reinterpret_cast<uint2*>(yr)[i] = out;
+  }
+}
+
+// dispatch: register-resident rows up to d = 16384 (x, y row strides and d
+// multiples of 4 floats / bf16), the strided kernels otherwise
+template <int RMS>
+static bool norm_reg(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
+                     float eps, float out_scale, cudaStream_t st) {
+  if ((d & 3) || (ldx & 3) || (ldy & 3) || d > 16384) return false;
+  const int nv = (d / 4 + 255) / 256;
+  auto go = [&](auto kern) {
+    launch_pdl(kern, dim3(T), dim3(256), 0, st, y, ldy, x, ldx, g, b, d, eps, out_scale);
+    EXG_CHECK_LAUNCH();
+  };
+  if (nv <= 1) go(norm_reg_kernel<1, RMS>);
+  else if (nv <= 2) go(norm_reg_kernel<2, RMS>);
+  else if (nv <= 4) go(norm_reg_kernel<4, RMS>);
+  else if (nv <= 5) go(norm_reg_kernel<5, RMS>);
+  else if (nv <= 8) go(norm_reg_kernel<8, RMS>);
+  else if (nv <= 9) go(norm_reg_kernel<9, RMS>);
+  else if (nv <= 12) go(norm_reg_kernel<12, RMS>);
+  else go(norm_reg_kernel<16, RMS>);
+  return true;
+}
+
 void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
                float eps, cudaStream_t st) {
   if (T <= 0) return;
+  if (norm_reg<0>(y, ldy, x, ldx, g, b, T, d, eps, 1.f, st)) return;
   launch_pdl(layernorm_kernel, dim3(T), dim3(256), 0, st, y, ldy, x, ldx, g, b, d, eps);
   EXG_CHECK_LAUNCH();
 }
@@ -125,6 +215,7 @@ __global__ void __launch_bounds__(256) rmsnorm_kernel(bf16* __restrict__ y, int6
 void rmsnorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, int T, int d, float eps,
              float out_scale, cudaStream_t st) {
   if (T <= 0) return;
+  if (norm_reg<1>(y, ldy, x, ldx, g, nullptr, T, d, eps, out_scale, st)) return;
   launch_pdl(rmsnorm_kernel, dim3(T), dim3(256), 0, st, y, ldy, x, ldx, g, d, eps, out_scale);
   EXG_CHECK_LAUNCH();
 }
