@@ -9,6 +9,7 @@
 // engine stream, median kept.  TP degree 1 on a single-GPU context (TP>1
 // all-reduce and PP send timings need a multi-rank context).
 #include <algorithm>
+#include <chrono>
 #include <vector>
 
 #include "profiler.h"
@@ -151,6 +152,40 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
   P.attn[{"enc", t}] = ae;
   P.attn[{"dec", t}] = ad;
   plan::Table1D re, rd;
+  // decode rest (timed before the encode heater below: memory-bound decode
+  // iterations run between encode phases at the recovered clock): input
+  // size = batch rows, swept over the batch axis
+  for (int b : bs) {
+    DecodeBatch db;
+    db.B = b;
+    db.max_keys = 1;
+    db.slot = d_rs;
+    db.pos = d_p0;
+    db.nkeys = d_aux;
+    db.xkeys = d_aux + max_b;
+    db.max_xkeys = 1;
+    rd.x.push_back(b);
+    rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }));
+  }
+  // Sustained-load state (reading): a real encode phase runs
+  // back-to-back prefill GEMMs for ~0.1-0.3 s, long enough for the power
+  // limiter to settle the SM clock below its boost; bring the GPU there
+  // before timing the "rest" tables (compute-bound prefill GEMMs follow the
+  // clock).  Runs the largest encode point for >= 0.5 s.
+  {
+    EncodeBatch hb;
+    hb.T = ts.back();
+    hb.R = 1;
+    hb.max_len = hb.T;
+    hb.ids = d_ids;
+    hb.pos = d_pos;
+    hb.tslot = d_slot;
+    const auto t0 = std::chrono::steady_clock::now();
+    while (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < 0.5) {
+      for (int k = 0; k < 4; ++k) E.layer_encode(0, hb, false, true);
+      EXG_CUDA(cudaStreamSynchronize(st));
+    }
+  }
   for (int T : ts) {
     EncodeBatch eb;
     eb.T = T;
@@ -166,19 +201,6 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
       E.layer_encode(0, eb, false, true);
       if (E.encdec()) E.cross_kv(0, eb);
     }));
-  }
-  // decode rest: input size = batch rows, swept over the batch axis
-  for (int b : bs) {
-    DecodeBatch db;
-    db.B = b;
-    db.max_keys = 1;
-    db.slot = d_rs;
-    db.pos = d_p0;
-    db.nkeys = d_aux;
-    db.xkeys = d_aux + max_b;
-    db.max_xkeys = 1;
-    rd.x.push_back(b);
-    rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }));
   }
   P.rest[{"enc", t}] = re;
   P.rest[{"dec", t}] = rd;
