@@ -441,6 +441,7 @@ def main():
             "roofline": roof(dom),
             "roofline_decode_attn": roof("decode_attn"),
             "roofline_decode_gemm": roof("decode_gemm"),
+            "roofline_prefill_attn": roof("prefill_attn"),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "output tokens/s", "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h},
