@@ -52,6 +52,12 @@ int& gemm_debug_flags() {
   return f;
 }
 
+// diagnostics: stream-K CTA count cap (0 = one per SM)
+int& gemm_sk_ctas() {
+  static int n = 0;
+  return n;
+}
+
 // g_dbg kernel argument: the flags, plus the launch sequence number when
 // span recording (bit 4) is on
 int& gemm_span_seq() {
@@ -580,7 +586,8 @@ Work make_work(int M, int N, int K, int BN, bool streamk) {
   const int sms = num_sms();
   if (streamk) {
     w.dp = 0;
-    w.G = (int)std::min<int64_t>(sms, w.I);
+    const int cap = gemm_sk_ctas() > 0 ? std::min(gemm_sk_ctas(), sms) : sms;
+    w.G = (int)std::min<int64_t>(cap, w.I);
     const int64_t per = w.I / w.G;  // >= 1
     w.max_segs = (int)((w.nkb + per - 1) / per) + 2;
   } else {
@@ -764,6 +771,7 @@ void linear(const LinearArgs& a, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
+extern "C" void exg_diag_gemm_sk_ctas(int n) { exg::gemm_sk_ctas() = n; }
 // span recording: reset clears the arrays and the launch counter; read copies
 // min(n, 4096) spans (ns) and returns the number of launches recorded
 extern "C" int exg_diag_gemm_spans_reset() {

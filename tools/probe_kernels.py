@@ -158,6 +158,17 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "dattn":
         dattn(int(sys.argv[2]), int(sys.argv[3]))
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "skctas":
+        for cap in (148, 120, 100, 74):
+            L.lib().exg_diag_gemm_sk_ctas(cap)
+            print("stream-K CTAs", cap)
+            for T in (16, 64):
+                gemm(T, 15360, 5120, True)
+                gemm(T, 5120, 5120, True, 2)
+                gemm(T, 20480, 5120, True)
+                gemm(T, 5120, 20480, True, 2)
+        L.lib().exg_diag_gemm_sk_ctas(0)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "dmix":
         for stages in (int(x) for x in (sys.argv[2] if len(sys.argv) > 2 else "2,27,1,16,4").split(",")):
             L.lib().exg_diag_decode_stages(stages)
