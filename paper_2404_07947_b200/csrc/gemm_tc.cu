@@ -52,6 +52,12 @@ int& gemm_debug_flags() {
   return f;
 }
 
+// prefill raster: A slab (MB) kept L2-resident per group (diagnostics override)
+int64_t& gemm_slab_mb() {
+  static int64_t mb = 32;
+  return mb;
+}
+
 // diagnostics: stream-K CTA count cap (0 = one per SM)
 int& gemm_sk_ctas() {
   static int n = 0;
@@ -582,7 +588,7 @@ Work make_work(int M, int N, int K, int BN, bool streamk) {
   w.nkb = (K + BK - 1) / BK;
   w.I = (int64_t)w.tiles_m * w.nkb;
   // raster group: m-tiles whose A slab is ~32 MB (kept L2-resident)
-  w.gm = (int)std::max<int64_t>(1, std::min<int64_t>(w.tiles_m, (32ll << 20) / ((int64_t)BM * K * 2)));
+  w.gm = (int)std::max<int64_t>(1, std::min<int64_t>(w.tiles_m, (gemm_slab_mb() << 20) / ((int64_t)BM * K * 2)));
   const int sms = num_sms();
   if (streamk) {
     w.dp = 0;
@@ -772,6 +778,7 @@ void linear(const LinearArgs& a, cudaStream_t st) {
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
 extern "C" void exg_diag_gemm_sk_ctas(int n) { exg::gemm_sk_ctas() = n; }
+extern "C" void exg_diag_gemm_slab_mb(int mb) { exg::gemm_slab_mb() = mb; }
 // span recording: reset clears the arrays and the launch counter; read copies
 // min(n, 4096) spans (ns) and returns the number of launches recorded
 extern "C" int exg_diag_gemm_spans_reset() {

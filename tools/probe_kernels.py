@@ -158,6 +158,16 @@ if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "dattn":
         dattn(int(sys.argv[2]), int(sys.argv[3]))
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "slab":
+        for mb in (16, 32, 48, 64, 96):
+            L.lib().exg_diag_gemm_slab_mb(mb)
+            print("A slab MB", mb)
+            for T in (4096, 8192, 16384):
+                gemm(T, 15360, 5120, False)
+                gemm(T, 20480, 5120, False)
+                gemm(T, 5120, 20480, False, 2)
+        L.lib().exg_diag_gemm_slab_mb(32)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "skctas":
         for cap in (148, 120, 100, 74):
             L.lib().exg_diag_gemm_sk_ctas(cap)
