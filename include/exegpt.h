@@ -189,6 +189,12 @@ exg_status exg_get_unique_id(uint8_t uid[128]);
  * *out is owned by the library (exg_destroy). */
 exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device, int32_t rank,
                       int32_t world, const uint8_t* uid, exg_ctx** out);
+/* One rank owning every GPU of a layout on `device`, with a one-rank NCCL
+ * communicator through which every exchange of the layout (pipeline hops,
+ * token return, packed WAA handoff messages) is sent to itself -- runs the
+ * NCCL transport on a single GPU (transport test). */
+exg_status exg_create_nccl_loopback(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device,
+                                    exg_ctx** out);
 /* `world` rank contexts of one process on one `device`, connected by a
  * device-copy transport instead of NCCL (each rank's exg_run must be called
  * from its own thread).  For testing the multi-rank executor on one GPU;

@@ -5,9 +5,9 @@ under an RRA / WAA schedule, behind the C-ABI of libexegpt.so
 step of the hot path runs in the library's CUDA kernels.
 """
 from ._lib import (EXG_RRA, EXG_WAA_C, EXG_WAA_M, Context, ExgError, Pmf, Profile, cluster_spec, lib,
-                   local_group, model_spec, rra_schedule, run_group, schedule_find, schedule_resolve, search_opts,
-                   simulate, unique_id)
+                   local_group, model_spec, nccl_loopback, rra_schedule, run_group, schedule_find,
+                   schedule_resolve, search_opts, simulate, unique_id)
 
 __all__ = ["EXG_RRA", "EXG_WAA_C", "EXG_WAA_M", "Context", "ExgError", "Pmf", "Profile", "cluster_spec", "lib",
-           "local_group", "model_spec", "rra_schedule", "run_group", "schedule_find", "schedule_resolve",
+           "local_group", "model_spec", "nccl_loopback", "rra_schedule", "run_group", "schedule_find", "schedule_resolve",
            "search_opts", "simulate", "unique_id"]

@@ -121,6 +121,8 @@ _SIGS = {
     "exg_destroy": (None, [_P]),
     "exg_create_local_group": (C.c_int, [C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.c_int32,
                                          C.c_int32, C.POINTER(_P)]),
+    "exg_create_nccl_loopback": (C.c_int, [C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.c_int32,
+                                           C.POINTER(_P)]),
     "exg_profile_run": (C.c_int, [_P, C.POINTER(exg_profile_grid), C.POINTER(_P)]),
     "exg_profile_save": (C.c_int, [_P, C.c_char_p]),
     "exg_profile_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
@@ -302,6 +304,15 @@ def local_group(spec, seed: int, world: int, cluster: Optional[exg_cluster_spec]
     hs = (_P * world)()
     check(lib().exg_create_local_group(C.byref(mspec), C.byref(cluster), device, world, hs))
     return [Context(spec, seed, device, cluster, rank=r, world=world, _handle=_P(hs[r])) for r in range(world)]
+
+
+def nccl_loopback(spec, seed: int, cluster: Optional[exg_cluster_spec] = None, device: int = 0) -> Context:
+    """One-rank context whose layout exchanges all go through NCCL (send /
+    recv to self): the NCCL transport on a single GPU."""
+    cluster = cluster or cluster_spec(8)
+    h = _P()
+    check(lib().exg_create_nccl_loopback(C.byref(model_spec(spec, seed)), C.byref(cluster), device, C.byref(h)))
+    return Context(spec, seed, device, cluster, _handle=h)
 
 
 def run_group(ctxs, sched: exg_schedule, requests, **kw):

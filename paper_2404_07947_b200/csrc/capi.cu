@@ -165,6 +165,34 @@ exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluste
   });
 }
 
+exg_status exg_create_nccl_loopback(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device,
+                                    exg_ctx** out) {
+  return guarded([&] {
+    if (!out || !cluster) throw std::invalid_argument("null argument");
+    *out = nullptr;
+    check_spec(spec);
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EXG_E_CUDA, "no CUDA device");
+    if (device < 0 || device >= ndev) throw std::invalid_argument("bad device index");
+    EXG_CUDA(cudaSetDevice(device));
+    std::unique_ptr<exg::Comm> comm;
+    try {
+      uint8_t uid[128];
+      exg::nccl_unique_id(uid);
+      comm = exg::make_nccl_comm(uid, 0, 1);
+    } catch (const std::exception& e) {
+      return fail(EXG_E_NCCL, e.what());
+    }
+    auto c = std::make_unique<exg_ctx>();
+    c->spec = *spec;
+    c->cluster = *cluster;
+    c->device = device;
+    c->multi = std::make_unique<exg::MultiCtx>(*spec, device, std::move(comm));
+    *out = c.release();
+    return EXG_OK;
+  });
+}
+
 exg_status exg_create_local_group(const exg_model_spec* spec, const exg_cluster_spec* cluster, int32_t device,
                                   int32_t world, exg_ctx** out) {
   return guarded([&] {

@@ -109,6 +109,9 @@ struct Exec {
   int me = 0, world = 1, G = 1;
   Comm* comm = nullptr;
   cudaStream_t st = nullptr;
+  // one-rank NCCL loopback (transport test): exchanges between this rank's
+  // own GPUs still go through ncclSend / ncclRecv to self
+  bool loop = false;
   int owner(int gpu) const { return (int)((int64_t)gpu * world / G); }
   bool mine(int gpu) const { return owner(gpu) == me; }
   // bytes from (gpu a, src) to (gpu b, dst); a pointer is only valid on its owner
@@ -116,7 +119,15 @@ struct Exec {
     const int oa = owner(ga), ob = owner(gb);
     if (bytes == 0) return;
     if (oa == me && ob == me) {
-      if (src != dst) EXG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+      if (src == dst) return;
+      if (loop) {
+        comm->group_start();
+        comm->send(src, bytes, me, st);
+        comm->recv(dst, bytes, me, st);
+        comm->group_end();
+      } else {
+        EXG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+      }
     } else if (oa == me) {
       comm->send(src, bytes, ob, st);
     } else if (ob == me) {
@@ -270,6 +281,7 @@ struct MultiCtx::Impl {
   cudaStream_t st = nullptr;
   std::unique_ptr<Comm> comm;
   int rank = 0, world = 1;
+  bool loopback = false;   // a one-rank communicator: route local exchanges through it
   std::map<std::string, std::unique_ptr<Layout>> layouts;
 };
 
@@ -279,6 +291,7 @@ MultiCtx::MultiCtx(const exg_model_spec& spec, int device, std::unique_ptr<Comm>
   if (comm) {
     p_->rank = comm->rank();
     p_->world = comm->world();
+    p_->loopback = comm->world() == 1;
   }
   p_->comm = std::move(comm);
   EXG_CUDA(cudaSetDevice(device));
@@ -304,6 +317,7 @@ static Exec make_exec(const MultiCtx::Impl* p, int G) {
   X.G = G;
   X.comm = p->comm.get();
   X.st = p->st;
+  X.loop = p->loopback;
   return X;
 }
 
@@ -879,11 +893,12 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       }
       EXG_CUDA(cudaMemcpyAsync(d_hrows, h_hrows, sizeof(HandoffRow) * pend_k, cudaMemcpyHostToDevice, R.st));
       const size_t need = (size_t)rows_len * H * dh;   // largest slice (a TP-1 decoder stage)
-      if (X.world > 1 && need > stage_cap) {
+      if ((X.world > 1 || X.loop) && need > stage_cap) {
         EXG_CUDA(cudaStreamSynchronize(R.st));
         if (stage_buf) cudaFree(stage_buf);
         stage_cap = need;
-        EXG_CUDA(cudaMalloc(&stage_buf, sizeof(bf16) * stage_cap));
+        // loopback: a second half receives the message sent from the first
+        EXG_CUDA(cudaMalloc(&stage_buf, sizeof(bf16) * stage_cap * (X.loop ? 2 : 1)));
       }
       // decoder-only: encoder stage es holds the KV of its layers [l0, l1);
       // T5: the last encoder stage holds the cross K/V of every decoder layer
@@ -909,7 +924,18 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
                 if (dst)
                   dp = R.ed ? (kv ? dst->xvc(l - ds->l0) : dst->xkc(l - ds->l0))
                             : (kv ? dst->vc(l - ds->l0) : dst->kc(l - ds->l0));
-                if (src_mine && dst_mine) {
+                if (src_mine && dst_mine && X.loop) {
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, stage_buf, d_hrows, pend_k, H, r * Hd, Hd,
+                                                                   enc_ctx, ctx_d, dh, 1);
+                  EXG_CHECK_LAUNCH();
+                  p->comm->group_start();
+                  p->comm->send(stage_buf, bytes, X.me, R.st);
+                  p->comm->recv(stage_buf + stage_cap, bytes, X.me, R.st);
+                  p->comm->group_end();
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(stage_buf + stage_cap, dp, d_hrows, pend_k, H,
+                                                                   r * Hd, Hd, enc_ctx, ctx_d, dh, 2);
+                  EXG_CHECK_LAUNCH();
+                } else if (src_mine && dst_mine) {
                   kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, dp, d_hrows, pend_k, H, r * Hd, Hd, enc_ctx,
                                                                    ctx_d, dh, 0);
                   EXG_CHECK_LAUNCH();

@@ -166,3 +166,32 @@ def test_multi_rank_errors(env):
         X.run_group(group, s, reqs)
     for c in group:
         c.close()
+
+
+# NCCL transport on one GPU: a one-rank communicator through which every
+# exchange of the layout is sent to itself (ncclSend / ncclRecv in a group),
+# bit-identical to the device-copy path
+NCCL_CASES = [
+    ("pp2", "rra", 4, 8, 0, 0, [(0, 1, 0, 1), (1, 1, 1, 2)], 1),
+    ("tp2_then_single", "rra", 4, 8, 0, 0, [(0, 2, 0, 1), (2, 1, 1, 2)], 2),
+    ("waa_dec_pipeline", "waa", 3, 8, 4, 1, [(0, 1, 0, 2), (1, 1, 0, 1), (2, 1, 1, 2)], 1),
+    ("waa_dec_tp", "waa", 2, 8, 4, 1, [(0, 1, 0, 2), (1, 2, 0, 1), (3, 1, 1, 2)], 2),
+]
+
+
+@pytest.mark.parametrize("case", NCCL_CASES, ids=[c[0] for c in NCCL_CASES])
+def test_nccl_loopback_bit_identical(env, case):
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    name, strat, b_e, b_d, b_m, n_enc, layout, tp = case
+    strategy = X.EXG_RRA if strat == "rra" else X.EXG_WAA_C
+    tp_gpus = sum(g[1] for g in layout if g[1] > 1)
+    s = L.make_schedule(strategy, b_e, b_d, layout, n_d=6, b_m=b_m, n_enc_gpus=n_enc, tp_degree=tp, tp_gpus=tp_gpus)
+    ref_t, _, _, ref_l = multi.run(s, reqs, dump=range(len(reqs)))
+    from workload import weight_seed
+    nc = X.nccl_loopback(multi.spec, weight_seed(1), X.cluster_spec(8))
+    toks, lat, st, lg = nc.run(s, reqs, dump=range(len(reqs)))
+    assert toks == ref_t
+    for r in range(len(reqs)):
+        assert np.array_equal(lg[r], ref_l[r]), r
+    assert np.all(lat > 0)
+    nc.close()
