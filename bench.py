@@ -166,6 +166,93 @@ def job_throughput(tokens: float, seconds: float, dist=None, device: str = "cuda
     return reduce_over_ranks(tokens, "sum", dist, device) / reduce_over_ranks(seconds, "max", dist, device)
 
 
+def static_bounds(X, prof, mspec, cl, pin, pout, target_len):
+    """Latency bounds: 10/30/70th percentiles of the FT-style static-batch
+    latencies B = 4, 8, ... on the profile."""
+    from paper_2404_07947_b200._lib import exg_schedule
+    stat = []
+    for B in range(4, 1025, 4):
+        s = exg_schedule()
+        s.strategy, s.b_e = 8, B
+        e = X.simulate(prof, mspec, cl, pin, pout, target_len, s)
+        if not e.feasible:
+            break
+        stat.append(e.latency_s)
+    p10, p30, p70 = (float(np.percentile(stat, q)) for q in (10, 30, 70))
+    return [("p10", p10), ("p30", p30), ("p70", p70), ("inf", math.inf)]
+
+
+def run_layout(args, rank, world, local):
+    """--layout plan (opt-in): the scheduler's N-GPU schedule for the p70
+    bound run as ONE job over the N ranks -- NCCL between processes, GPU g of
+    the layout on rank g*N/G (multi.cu).  Rank 0 profiles and plans; the
+    schedule and the NCCL id are broadcast; every rank runs the same requests."""
+    import torch
+    import torch.distributed as dist
+    import paper_2404_07947_b200 as X
+    from paper_2404_07947_b200._lib import exg_schedule
+    from workload import MODELS, make_requests, task_dists, weight_seed
+    spec = MODELS[MODEL]
+    d = task_dists(TASK)
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    free, total = torch.cuda.mem_get_info(local)
+    pin, pout = X.Pmf(d.pmf_in), X.Pmf(d.pmf_out)
+    box = [None, None]
+    if rank == 0:
+        ctx1 = X.Context(spec, weight_seed(CONFIG_NO), device=local,
+                         cluster=X.cluster_spec(1, total - (6 << 30), 8 << 30))
+        prof = ctx1.profile([1, 2, 4, 8, 16, 32, 48, 64, 96, 128, 160, 192, 224, 256, 320, 384, 448, 512],
+                            [1, 32, 64, 128, 192, 256, 320, 384, 448, 512, 592],
+                            [1, 16, 64, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768], reps=3, tps=[1, 2, 4, 8])
+        prof.comm_model(COMM_ALPHA_S, COMM_BW)
+        L_head = dict(static_bounds(X, prof, ctx1.mspec, ctx1.cluster, pin, pout, d.target_len))["p70"]
+        cl_n = X.cluster_spec(world, ctx1.cluster.mem_per_gpu_bytes, ctx1.cluster.workspace_bytes)
+        s, e = X.schedule_find(prof, ctx1.mspec, cl_n, pin, pout, d.target_len, L_head * (1 - args.margin),
+                               X.EXG_RRA | X.EXG_WAA_C, X.search_opts(b_e_max=B_E_MAX, little=args.little))
+        box = [{"sched": bytes(s), "bound": L_head, "pred": e.thrput_tok_s}, X.unique_id()]
+        ctx1.close()
+        del ctx1
+        torch.cuda.empty_cache()
+    dist.broadcast_object_list(box, src=0)
+    plan, uid = box
+    s = exg_schedule.from_buffer_copy(plan["sched"])
+    ctx = X.Context(spec, weight_seed(CONFIG_NO), device=local,
+                    cluster=X.cluster_spec(world, total - (6 << 30), 8 << 30), rank=rank, world=world, uid=uid)
+    reqs = make_requests(args.requests, d.pmf_in, d.pmf_out, spec.vocab, rank_request_seed(0))
+    slot_ctx = len(d.pmf_in) + len(d.pmf_out)
+    for _ in range(args.warmup):
+        ctx.run(s, reqs, slot_ctx=slot_ctx)
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall, toks, lats = 0.0, 0, []
+    th0 = time.perf_counter()
+    for _ in range(args.steps):
+        _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx)
+        wall += st["wall_s"]
+        toks += st["out_tokens"]
+        lats.append(lat)
+    torch.cuda.synchronize()
+    dist.barrier()
+    host = time.perf_counter() - th0
+    if rank == 0:   # stamps and outputs are gathered on rank 0 (one job, not replicas)
+        lat = lats[-1]
+        print(json.dumps({
+            "metric": METRIC, "value": toks / wall, "unit": "output tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD.replace("on 1xB200 per rank", "as one job"), "layout": "plan",
+                       "latency_bound_s": plan["bound"], "schedule": s.as_dict(), "predicted_tok_s": plan["pred"],
+                       "requests_per_step": args.requests},
+            "e2e": {"value": toks / host, "unit": "output tokens/s", "h2d_bytes_per_step": None,
+                    "d2h_bytes_per_step": None},
+            "sla": {"p99_latency_s": float(np.percentile(lat, 99)), "max_latency_s": float(np.max(lat)),
+                    "sla_a_met": bool(np.percentile(lat, 99) <= plan["bound"])}}))
+    ctx.close()
+    dist.destroy_process_group()
+
+
 def run_reference(args, rank, world):
     """--impl reference: the oracle (CPU, float64, bf16-emulating KV loop) on
     a bounded sample of the workload; rank 0 only."""
@@ -206,6 +293,8 @@ def main():
     ap.add_argument("--little", type=int, default=1,
                     help="1: completion fraction by Little's law (SURVEY.md S3; DESIGN.md), 0: paper's E[1/ceil(S/N_D)]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--layout", default="replicas", choices=["replicas", "plan"],
+                    help="N > 1: independent replicas (default) or the scheduler's N-GPU layout as one NCCL job")
     ap.add_argument("--plan-gpus", type=lambda v: [int(x) for x in v.split(",") if x], default=[2, 4, 8],
                     help="cluster sizes for the scheduler's predicted multi-GPU plan")
     ap.add_argument("--dyn", type=float, default=0.1, help="dynamic workload adjustment threshold (0: skip the run)")
@@ -218,6 +307,9 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.layout == "plan" and world > 1:
+        run_layout(args, rank, world, local)
         return
 
     import torch
@@ -263,18 +355,8 @@ def main():
         prof.save(os.path.join(ROOT, "gpurun_out", "profile_opt13b.txt"))
     cl = ctx.cluster
     pin, pout = X.Pmf(d.pmf_in), X.Pmf(d.pmf_out)
-    from paper_2404_07947_b200._lib import exg_schedule
     # static-batch latency sweep -> bounds
-    stat = []
-    for B in range(4, 1025, 4):
-        s = exg_schedule()
-        s.strategy, s.b_e = 8, B
-        e = X.simulate(prof, ctx.mspec, cl, pin, pout, d.target_len, s)
-        if not e.feasible:
-            break
-        stat.append(e.latency_s)
-    p10, p30, p70 = (float(np.percentile(stat, q)) for q in (10, 30, 70))
-    bounds = [("p10", p10), ("p30", p30), ("p70", p70), ("inf", math.inf)]
+    bounds = static_bounds(X, prof, ctx.mspec, cl, pin, pout, d.target_len)
     scheds = {}
     t0 = time.perf_counter()
     for name, L_b in bounds:
