@@ -182,7 +182,7 @@ def schedule_find(S: sim.Simulator, L_b: float, strategy_mask: int, opts: Search
     n_d_max = opts.n_d_max if opts.n_d_max > 0 else S.max_out
     best = None   # (key, Found)
     total_evals = 0
-    for strat in (sim.RRA, sim.WAA_C):
+    for strat in (sim.RRA, sim.WAA_C, sim.WAA_M):
         if not (strategy_mask & strat):
             continue
         if strat != sim.RRA and N < 2:
@@ -197,8 +197,8 @@ def schedule_find(S: sim.Simulator, L_b: float, strategy_mask: int, opts: Search
                         return S.rra_schedule(x1, n_d_max + 1 - x2, t, c)
                     b2 = n_d_max
                 else:
-                    def mk(x1, x2, t=t, c=c):
-                        return S.waa_schedule(x1, opts.m_max + 1 - x2, t, c)
+                    def mk(x1, x2, t=t, c=c, strat=strat):
+                        return S.waa_schedule(x1, opts.m_max + 1 - x2, t, c, strat)
                     b2 = opts.m_max
 
                 def perf_fn(x1, x2, mk=mk):

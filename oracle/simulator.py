@@ -405,21 +405,33 @@ class Simulator:
         return Estimate(thr, thr * self.s_d, lat)
 
     # -- WAA (S7) -----------------------------------------------------------
-    def waa_split(self, b_e: int, b_d: int) -> int:
+    def waa_split(self, b_e: int, b_d: int, strat: int = WAA_C) -> int:
+        """Encoder GPUs out of N.  WAA-C (S7): proportional to the encoder /
+        decoder compute per iteration.  WAA-M (reading): so the
+        per-GPU memory of the two sides is equal -- M_E = weights + B_E max_in
+        KV rows, M_D = weights + B_D (max_in + max_out) KV rows, n_enc =
+        round(N M_E / (M_E + M_D))."""
         N = self.cl.n_gpus
-        C_E = self.n_layers * self.layer_enc(1, b_e)
-        C_D = self.n_layers * self.layer_dec(1, b_d)
-        n_enc = int(math.floor(N * C_E / (C_E + C_D) + 0.5))
+        if strat == WAA_M:
+            kv = self.kv_bytes_per_token_layer()
+            W = self.n_layers * self.layer_bytes() + self.emb_bytes()
+            M_E = W + (b_e * self.max_in * self.n_layers) * kv
+            M_D = W + (b_d * (self.max_in + self.max_out) * self.n_layers) * kv
+            n_enc = int(math.floor(N * M_E / (M_E + M_D) + 0.5))
+        else:
+            C_E = self.n_layers * self.layer_enc(1, b_e)
+            C_D = self.n_layers * self.layer_dec(1, b_d)
+            n_enc = int(math.floor(N * C_E / (C_E + C_D) + 0.5))
         return min(max(n_enc, 1), N - 1)
 
-    def waa_schedule(self, b_e: int, M: int, t: int, c: int) -> Optional[Schedule]:
+    def waa_schedule(self, b_e: int, M: int, t: int, c: int, strat: int = WAA_C) -> Optional[Schedule]:
         if self.cl.n_gpus < 2:
             return None
         b_d = seqdist.waa_b_d(b_e, self.s_d)
         M = min(M, b_d)
         b_m = -(-b_d // M)
         try:
-            n_enc = self.waa_split(b_e, b_d)
+            n_enc = self.waa_split(b_e, b_d, strat)
         except OutOfHull:
             return None
         n_dec = self.cl.n_gpus - n_enc
@@ -427,7 +439,7 @@ class Simulator:
             return None
         enc = stage_layout(n_enc, 1, 0, self.n_layers, 0)
         dec = stage_layout(n_dec, t, c, self.n_layers, n_enc)
-        return Schedule(WAA_C, b_e, b_d, b_m, 0, t, c, n_enc, enc + dec)
+        return Schedule(strat, b_e, b_d, b_m, 0, t, c, n_enc, enc + dec)
 
     def simulate_waa(self, s: Schedule) -> Estimate:
         enc = [st for st in s.stages if st[0] < s.n_enc_gpus]

@@ -316,8 +316,9 @@ exg_status exg_schedule_resolve(const exg_profile* p, const exg_model_spec* spec
     if (sched->strategy == EXG_RRA) {
       if (sched->b_e < 1 || sched->n_d < 1) throw std::invalid_argument("RRA needs b_e >= 1, n_d >= 1");
       s = S.rra_schedule(sched->b_e, sched->n_d, std::max(1, sched->tp_degree), sched->tp_gpus);
-    } else if (sched->strategy == EXG_WAA_C) {
-      s = S.waa_schedule(sched->b_e, std::max(1, m_count), std::max(1, sched->tp_degree), sched->tp_gpus);
+    } else if (sched->strategy == EXG_WAA_C || sched->strategy == EXG_WAA_M) {
+      s = S.waa_schedule(sched->b_e, std::max(1, m_count), std::max(1, sched->tp_degree), sched->tp_gpus,
+                         sched->strategy);
       if (!s.valid) return fail(EXG_E_INFEASIBLE, "WAA needs >= 2 GPUs and tp_gpus <= decoder GPUs");
     } else {
       throw std::invalid_argument("unknown strategy");

@@ -352,15 +352,26 @@ Sched Simulator::rra_schedule(int b_e, int n_d, int t, int c) {
   return s;
 }
 
-int Simulator::waa_split(int b_e, int b_d) {
+// WAA-C: compute-proportional; WAA-M: equal per-GPU memory
+// (mirror of oracle/simulator.py waa_split, same expression order)
+int Simulator::waa_split(int b_e, int b_d, int strat) {
   const int N = cl.n_gpus;
-  const double C_E = n_layers * layer_enc(1, b_e);
-  const double C_D = n_layers * layer_dec(1, b_d);
-  const int n_enc = (int)std::floor(N * C_E / (C_E + C_D) + 0.5);
+  int n_enc;
+  if (strat == EXG_WAA_M) {
+    const double kv = kv_bytes_per_token_layer();
+    const double W = n_layers * layer_bytes() + emb_bytes();
+    const double mem_e = W + (double)((int64_t)b_e * max_in * n_layers) * kv;
+    const double mem_d = W + (double)((int64_t)b_d * (max_in + max_out) * n_layers) * kv;
+    n_enc = (int)std::floor(N * mem_e / (mem_e + mem_d) + 0.5);
+  } else {
+    const double C_E = n_layers * layer_enc(1, b_e);
+    const double C_D = n_layers * layer_dec(1, b_d);
+    n_enc = (int)std::floor(N * C_E / (C_E + C_D) + 0.5);
+  }
   return std::min(std::max(n_enc, 1), N - 1);
 }
 
-Sched Simulator::waa_schedule(int b_e, int M, int t, int c) {
+Sched Simulator::waa_schedule(int b_e, int M, int t, int c, int strat) {
   Sched s;
   s.valid = false;
   if (cl.n_gpus < 2) return s;
@@ -369,14 +380,14 @@ Sched Simulator::waa_schedule(int b_e, int M, int t, int c) {
   const int b_m = (b_d + M - 1) / M;
   int n_enc;
   try {
-    n_enc = waa_split(b_e, b_d);
+    n_enc = waa_split(b_e, b_d, strat);
   } catch (const OutOfHull&) {
     return s;
   }
   const int n_dec = cl.n_gpus - n_enc;
   if (c > n_dec) return s;
   s.valid = true;
-  s.strategy = EXG_WAA_C;
+  s.strategy = strat;
   s.b_e = b_e;
   s.b_d = b_d;
   s.b_m = b_m;
@@ -610,7 +621,7 @@ bool schedule_find(Simulator& S, double L_b, uint32_t mask, const exg_search_opt
   double k_thr = 0, k_lat = 0;
   int k_rest[5] = {0, 0, 0, 0, 0};
   int64_t total_evals = 0;
-  const int strats[2] = {EXG_RRA, EXG_WAA_C};
+  const int strats[3] = {EXG_RRA, EXG_WAA_C, EXG_WAA_M};
   for (int strat : strats) {
     if (!(mask & (uint32_t)strat)) continue;
     if (strat != EXG_RRA && N < 2) continue;
@@ -624,7 +635,7 @@ bool schedule_find(Simulator& S, double L_b, uint32_t mask, const exg_search_opt
       for (int c : cs) {
         auto mk = [&](int x1, int x2) {
           return strat == EXG_RRA ? S.rra_schedule(x1, n_d_max + 1 - x2, t, c)
-                                  : S.waa_schedule(x1, o.m_max + 1 - x2, t, c);
+                                  : S.waa_schedule(x1, o.m_max + 1 - x2, t, c, strat);
         };
         const int b2 = strat == EXG_RRA ? n_d_max : o.m_max;
         auto perf_fn = [&](int x1, int x2) -> Perf {

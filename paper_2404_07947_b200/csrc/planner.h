@@ -73,7 +73,7 @@ class Simulator {
   Simulator(const Profile& p, const exg_model_spec& m, const exg_cluster_spec& cl, std::vector<double> pmf_in,
             std::vector<double> pmf_out, int target_len, bool use_little);
   Sched rra_schedule(int b_e, int n_d, int t, int c);
-  Sched waa_schedule(int b_e, int M, int t, int c);
+  Sched waa_schedule(int b_e, int M, int t, int c, int strat = EXG_WAA_C);
   Est simulate(const Sched& s);
   Est simulate_static(int B);
   double layer_enc(int t, double b);
@@ -98,7 +98,7 @@ class Simulator {
   double layer_bytes() const;
   double emb_bytes() const;
   double kv_bytes_per_token_layer() const;
-  int waa_split(int b_e, int b_d);
+  int waa_split(int b_e, int b_d, int strat = EXG_WAA_C);
   Est simulate_rra(const Sched& s);
   Est simulate_waa(const Sched& s);
 };

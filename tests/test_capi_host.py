@@ -121,7 +121,8 @@ def test_simulate_pipeline_bit_identical(L, tmp_path, n_gpus, t, c):
 
 
 @pytest.mark.parametrize("task,model,n_gpus,mask", [("S", "opt-13b", 1, 1), ("S", "opt-13b", 4, 3),
-                                                    ("G", "opt-66b", 8, 3), ("C1", "gpt3-175b", 8, 3)])
+                                                    ("G", "opt-66b", 8, 3), ("C1", "gpt3-175b", 8, 3),
+                                                    ("G", "opt-66b", 4, 7), ("C1", "gpt3-175b", 8, 4)])
 def test_schedule_find_bit_identical(L, tmp_path, task, model, n_gpus, mask):
     from oracle import bnb, simulator as sim
     spec, m, prof, d, cl = _setup(task, model, n_gpus)

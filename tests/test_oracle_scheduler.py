@@ -282,3 +282,24 @@ def test_schedule_find_bound_relaxation_trend():
         assert f.estimate.thrput_seq_s >= prev * (1 - 0.02)
         prev = f.estimate.thrput_seq_s
     assert prev > 0
+
+
+def test_waa_m_split_balances_memory():
+    """WAA-M (DESIGN.md reading): the encoder GPU count makes the
+    per-GPU memory of the two sides as equal as any neighbouring split."""
+    m = sim.SimModel.from_spec(MODELS["opt-66b"])
+    d = task_dists("G")
+    S = sim.Simulator(_synthetic_profile(m), m, sim.SimCluster(8, 180e9, 4e9), d.pmf_in, d.pmf_out, d.target_len)
+    kv = S.kv_bytes_per_token_layer()
+    W = S.n_layers * S.layer_bytes() + S.emb_bytes()
+    for b_e in (1, 4, 16, 64):
+        b_d = b_e * 192
+        me = W + b_e * S.max_in * S.n_layers * kv
+        md = W + b_d * (S.max_in + S.max_out) * S.n_layers * kv
+        n = S.waa_split(b_e, b_d, sim.WAA_M)
+        gap = lambda k: abs(me / k - md / (8 - k))
+        for k in (n - 1, n + 1):
+            if 1 <= k <= 7:
+                assert gap(n) <= gap(k) * (1 + 1e-12), (b_e, n, k)
+        s = S.waa_schedule(b_e, 2, 1, 0, sim.WAA_M)
+        assert s.strategy == sim.WAA_M and s.n_enc_gpus == n
