@@ -138,9 +138,6 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
   if (t5_) {
     if (s.n_enc_layers != s.n_dec_layers) throw std::invalid_argument("T5: n_enc_layers must equal n_dec_layers");
     if (shard.tp != 1) throw std::invalid_argument("T5: tensor-parallel shards are not built yet");
-    if (shard.t5_role == 0 &&
-        (shard.l0 != 0 || (shard.l1 >= 0 && shard.l1 != s.n_dec_layers) || !shard.embed || !shard.head))
-      throw std::invalid_argument("T5: pipelines hold encoder and decoder layers on separate WAA GPU sets only");
     if (shard.t5_role == 1 && shard.head) throw std::invalid_argument("T5 encoder-side shards hold no LM head");
     if (shard.t5_role < 0 || shard.t5_role > 2) throw std::invalid_argument("bad T5 role");
   } else if (s.n_enc_layers != 0) {
@@ -267,7 +264,7 @@ void Engine::gen_weights_t5() {
   const size_t d = D.d, in = D.inner, f = D.ff;
   const int role = S_.t5_role, nl = n_layers();
   const bool has_enc = role != 2, has_dec = role != 1;
-  const bool enc_last = role == 0 || (role == 1 && S_.enc_last);
+  const bool enc_last = role != 2 && S_.enc_last;   // holds the encoder's final norm
   const int n_xproj = (role == 1 && S_.enc_last) ? D.L : 0;
   auto al = [](size_t n) { return (n * 2 + 255) & ~size_t(255); };
   auto bl = [&](size_t rows, size_t K) { return al((size_t)blocked_elems(rows, K)); };
@@ -743,16 +740,25 @@ void Engine::enc_layer_t5(int l, const EncodeBatch& eb, bool attn, bool rest) {
   }
 }
 
+// the encode phase of this shard: its encoder layers, then (last encoder
+// shard) the final norm -> h() and the cross K/V it holds.  A non-last shard of
+// an RRA pipeline (role 0) gets the encoder output broadcast into h() by the
+// executor and then runs cross_kv_all() for its decoder layers.
 void Engine::encode_t5(const EncodeBatch& eb) {
   const int T = eb.T, d = D.d;
   if (S_.t5_role == 2) throw std::logic_error("T5 decoder-side shard: no encoder layers");
   if (T > cap_tokens_) throw std::invalid_argument("encode batch exceeds workspace");
   if (S_.embed) embed(x_, eb.ids, eb.pos, tok_emb_, nullptr, T, d, st_, 1);
   for (int l = 0; l < n_layers(); ++l) enc_layer_t5(l, eb, true, true);
-  if (S_.t5_role == 1 && !S_.enc_last) return;   // residual stream x() continues on the next encoder stage
+  if (!S_.enc_last) return;   // the residual stream x() continues on the next stage
   rmsnorm(h_, d, x_, d, enc_lnf_g_, T, d, T5_EPS, 1.f, st_);
-  // K13: cross K/V of every decoder layer, K at columns [il, 2il) and V at
-  // [2il, 3il) of the qkv buffer, then scattered to the slots
+  cross_kv_all(eb);
+}
+
+// K13: cross K/V of every decoder layer held here from the encoder output in
+// h(): K at columns [il, 2il) and V at [2il, 3il) of the qkv buffer, then
+// scattered to the slots
+void Engine::cross_kv_all(const EncodeBatch& eb) {
   for (int l = 0; l < n_cross_layers(); ++l) cross_kv(l, eb);
 }
 

@@ -100,8 +100,11 @@ class Engine {
   int xctx() const { return xctx_; }
   bf16* xkc(int l) const { return xkv_ + (size_t)l * 2 * xkv_layer_elems(); }
   bf16* xvc(int l) const { return xkc(l) + xkv_layer_elems(); }
-  // K13: cross K/V of decoder layer l from the encoder output (bf16 in h)
+  // K13: cross K/V of decoder layer l (all layers held: cross_kv_all) from
+  // the encoder output (bf16 in h())
   void cross_kv(int l, const EncodeBatch& eb);
+  void cross_kv_all(const EncodeBatch& eb);
+  bf16* h() { return h_; }
   int kv_slots() const { return kv_slots_; }
   int slot_ctx() const { return slot_ctx_; }
   int32_t* last_tok() { return last_tok_; }

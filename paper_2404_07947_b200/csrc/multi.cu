@@ -376,8 +376,6 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
   check_cover(dec_idx);
   const Exec X = make_exec(p, G);
   const bool t5 = p->spec.arch == EXG_ARCH_T5;
-  if (t5 && s.strategy == EXG_RRA)
-    throw std::invalid_argument("T5: multi-GPU layouts run under WAA (encoder / decoder GPU sets) only");
   for (size_t k = 0; k < enc_idx.size(); ++k) {
     const int i = enc_idx[k];
     if (s.stage_n_gpus[i] != 1) throw std::invalid_argument("WAA encoder stages are single-GPU");
@@ -387,8 +385,11 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
   for (size_t k = 0; k < dec_idx.size(); ++k) {
     const int i = dec_idx[k];
     if (t5 && s.stage_n_gpus[i] != 1) throw std::invalid_argument("T5: tensor-parallel stages are not built yet");
+    // T5 under RRA: each stage holds encoder and decoder layers [l0, l1) (role 0)
+    const bool rra = s.strategy == EXG_RRA;
     lay->dec.push_back(make_stage(p, X, s.stage_first_gpu[i], s.stage_layer_begin[i], s.stage_layer_end[i],
-                                  s.stage_n_gpus[i], k == 0, k + 1 == dec_idx.size(), t5 ? 2 : 0));
+                                  s.stage_n_gpus[i], k == 0, k + 1 == dec_idx.size(), t5 ? (rra ? 0 : 2) : 0,
+                                  k + 1 == dec_idx.size()));
   }
   Layout* out = lay.get();
   p->layouts[key] = std::move(lay);
@@ -517,7 +518,7 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
     maxlen = std::max(maxlen, q.input_len - drop);
     const double m = q.input_len - drop;
     eb.attn_pairs += R.ed ? m * m : m * (m + 1) / 2;
-    if (last_ids) last_ids->push_back(q.input_ids[q.input_len - 1]);
+    if (last_ids) last_ids->push_back(R.ed ? 0 : q.input_ids[q.input_len - 1]);   // T5: decoder start token
   }
   tb.upload((size_t)3 * T + (k + 1) + 2 * k, st);
   eb.T = T;
@@ -729,16 +730,19 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   R.reqs = reqs;
   R.n = n;
   R.st = p->st;
+  R.ed = p->spec.arch == EXG_ARCH_T5;
   validate_requests(R, p->spec.vocab, p->spec.max_pos);
-  const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : R.max_ctx;
-  if (slot_ctx < R.max_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
+  const int need_ctx = R.ed ? R.max_out : R.max_ctx;
+  const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : need_ctx;
+  if (slot_ctx < need_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
   const int B_D = s.b_d, B_E = s.b_e, P = (int)pipe.size();
   if (B_E < 1 || B_D < B_E || s.n_d < 1) throw std::invalid_argument("RRA needs 1 <= B_E <= B_D, N_D >= 1");
+  const int drop = R.ed ? 0 : 1;
   for (auto& st : pipe)
     for (auto& e : st->eng)
       if (e) {
-        e->ensure_kv(B_D, slot_ctx);
-        e->ensure_workspace(B_E * (R.max_in - 1), B_D);
+        e->ensure_kv(B_D, slot_ctx, -1, R.ed ? R.max_in : 0);
+        e->ensure_workspace(std::max(1, B_E * (R.max_in - drop)), B_D);
       }
   const bool first_mine = X.mine(pipe.front()->gpu(0)), head_mine = X.mine(pipe.back()->gpu(0));
   std::vector<Tables> tabs(8);
@@ -759,7 +763,7 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         slots[k] = free_slots.back();
         free_slots.pop_back();
         const exg_request& q = reqs[next_req + k];
-        active.push_back(Row{next_req + k, slots[k], q.input_len - 1, 0});
+        active.push_back(Row{next_req + k, slots[k], R.ed ? 0 : q.input_len - 1, 0});
         R.admit_ev[next_req + k] = ev_phase;
       }
       for (const auto& mb : chunks(admit, P)) {
@@ -780,6 +784,17 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         for (size_t k = 0; k < pipe.size(); ++k) {
           if (k > 0) hop(X, *pipe[k - 1], *pipe[k], eb.T, d);
           pipe[k]->encode(X, eb, d);
+        }
+        if (R.ed && P > 1) {
+          // T5: the encoder output (bf16 [T][d], last stage) to every other
+          // stage, which projects the cross K/V of its own decoder layers
+          Stage& Ls = *pipe.back();
+          for (int k = 0; k + 1 < P; ++k) {
+            Stage& S_k = *pipe[k];
+            X.xfer(Ls.gpu(0), Ls.eng[0] ? Ls.eng[0]->h() : nullptr, S_k.gpu(0), S_k.eng[0] ? S_k.eng[0]->h() : nullptr,
+                   sizeof(bf16) * (size_t)eb.T * d);
+            if (S_k.eng[0]) S_k.eng[0]->cross_kv_all(eb);
+          }
         }
       }
       next_req += admit;

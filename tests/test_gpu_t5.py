@@ -176,14 +176,27 @@ def test_t5_batch_invariance(t5env):
         assert np.array_equal(a[3][r], b[3][r]), r
 
 
-def test_t5_rra_multi_gpu_layout_rejected(t5env):
+@pytest.mark.parametrize("transport", ["one_rank", "two_ranks", "nccl_loopback"])
+def test_t5_rra_pipeline_bit_identical(t5env, transport):
+    """RRA over 2 pipeline stages, each holding encoder and decoder layers
+    [l0, l1): the encoder output is broadcast from the last stage so every
+    stage projects the cross K/V of its own decoder layers."""
     X, spec, reqs, ctx, ora = t5env
     from paper_2404_07947_b200 import _lib
     from workload import weight_seed
-    multi = X.Context(spec, weight_seed(3), cluster=X.cluster_spec(2))
-    s = _lib.make_schedule(X.EXG_RRA, 2, 4, [(0, 1, 0, spec.n_dec_layers)], n_d=2)
-    with pytest.raises(X.ExgError):
-        multi.run(s, reqs[:2])
+    base_t, _, _, base_l = ctx.run(X.rra_schedule(3, 5, 4), reqs, dump=range(len(reqs)))
+    s = _lib.make_schedule(X.EXG_RRA, 3, 5, [(0, 1, 0, 1), (1, 1, 1, 2)], n_d=4)
+    if transport == "one_rank":
+        res = [X.Context(spec, weight_seed(3), cluster=X.cluster_spec(2)).run(s, reqs, dump=range(len(reqs)))]
+    elif transport == "two_ranks":
+        res = X.run_group(X.local_group(spec, weight_seed(3), 2, X.cluster_spec(2)), s, reqs, dump=range(len(reqs)))
+    else:
+        res = [X.nccl_loopback(spec, weight_seed(3), X.cluster_spec(2)).run(s, reqs, dump=range(len(reqs)))]
+    assert res[0][0] == base_t
+    head = [r[3] for r in res if np.any(r[3][0])]
+    assert len(head) == 1
+    for r in range(len(reqs)):
+        assert np.array_equal(head[0][r], base_l[r]), r
 
 
 # WAA for T5 (config 3: encoder GPU(s) + decoder GPU(s)): the last encoder
