@@ -141,3 +141,27 @@ def test_config4_opt66b_width_waa_tp2(X):
 
 def test_config5_gpt3_width_rra_tp8(X):
     _width_case(X, "gpt3-175b", [(0, 8, 0, 1)], X.EXG_RRA, 2, 4, 8, 0, 8)
+
+
+def test_config3_t5_11b_width_parity(X):
+    """T5-11B width (d = 1024, 128 heads x 128, d_ff = 65536; one encoder and
+    one decoder layer, identical weights) on task-T-shaped requests vs
+    oracle/t5.py mode (iii), under RRA and under the 2-GPU WAA layout of config 3."""
+    from oracle import t5 as T5
+    from paper_2404_07947_b200 import _lib
+    from workload import MODELS, ModelSpec, make_requests, uniform_pmf, weight_seed
+    full = MODELS["t5-11b"]
+    spec = ModelSpec("t5-11b-1+1", "t5", 1, 1, full.d_model, full.n_heads, full.d_head, full.d_ff, full.vocab,
+                     full.max_pos)
+    reqs = make_requests(4, uniform_pmf(40, 150), uniform_pmf(2, 4), full.vocab, 0xE6E10005)
+    ora = T5.greedy_kv(T5.T5Weights(spec, weight_seed(3)), reqs, "bf16", record_logits=True)
+    runs = [X.Context(spec, weight_seed(3)).run(X.rra_schedule(2, 4, 2), reqs, dump=range(len(reqs)))]
+    s = _lib.make_schedule(X.EXG_WAA_C, 2, 4, [(0, 1, 0, 1), (1, 1, 0, 1)], n_enc_gpus=1)
+    runs.append(X.Context(spec, weight_seed(3), cluster=X.cluster_spec(2)).run(s, reqs, dump=range(len(reqs))))
+    for toks, lat, st, lg in runs:
+        for r, q in enumerate(reqs):
+            for t in range(q.output_len):
+                assert np.abs(lg[r][t] - ora.logits[r][t]).max() <= TOL, (r, t)
+                if toks[r][t] != ora.tokens[r][t]:
+                    assert ora.margins[r][t] <= 2 * TOL, (r, t)
+                    break
