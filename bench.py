@@ -173,13 +173,68 @@ def static_bounds(X, prof, mspec, cl, pin, pout, target_len):
     stat = []
     for B in range(4, 1025, 4):
         s = exg_schedule()
-        s.strategy, s.b_e = 8, B
+        s.strategy, s.b_e = X.EXG_STATIC, B
         e = X.simulate(prof, mspec, cl, pin, pout, target_len, s)
         if not e.feasible:
             break
         stat.append(e.latency_s)
     p10, p30, p70 = (float(np.percentile(stat, q)) for q in (10, 30, 70))
     return [("p10", p10), ("p30", p30), ("p70", p70), ("inf", math.inf)]
+
+
+def static_pick(X, prof, mspec, cl, pin, pout, target_len, L_b):
+    """The FT-style static batch size for a bound: the simulated
+    max-throughput B whose static latency (max-length output)
+    is within L_b; None if even B = 1 misses it."""
+    from paper_2404_07947_b200._lib import exg_schedule
+    best = None
+    for B in range(1, 1025):
+        s = exg_schedule()
+        s.strategy, s.b_e = X.EXG_STATIC, B
+        e = X.simulate(prof, mspec, cl, pin, pout, target_len, s)
+        if not e.feasible:
+            break
+        if e.latency_s <= L_b and (best is None or e.thrput_tok_s > best[1].thrput_tok_s):
+            best = (B, e)
+    return best
+
+
+def in_runner_baselines(args, X, ctx, prof, cl, pin, pout, d, bounds, scheds, reqs, slot_ctx, sla):
+    """the paper's comparison points run on the same
+    kernels, requests and bounds -- FT-style static batches (PAPER.md:112:
+    fixed batch, no early termination; B = the simulated best static batch
+    within the bound) and ORCA-style iteration-level admission (PAPER.md:116:
+    new requests join every iteration = RRA with N_D = 1, B_E / B_D picked by
+    Algorithm 1 with N_D^max = 1) -- beside the ExeGPT schedule (RRA,
+    Algorithm 1).  Ratios are measured tokens/s; a leg whose run misses the
+    bound (SLA-(b)) is reported with sla_b_met false."""
+    res = {}
+    for name, L_b in bounds:
+        row = {"latency_bound_s": L_b}
+        legs = {}
+        if scheds.get(name):
+            legs["exegpt"] = (scheds[name][0], scheds[name][1].thrput_tok_s)
+        pick = static_pick(X, prof, ctx.mspec, cl, pin, pout, d.target_len, L_b * (1 - args.margin))
+        if pick:
+            legs["ft_static"] = (X.static_schedule(pick[0]), pick[1].thrput_tok_s)
+        try:
+            so, eo = X.schedule_find(prof, ctx.mspec, cl, pin, pout, d.target_len, L_b * (1 - args.margin),
+                                     X.EXG_RRA, X.search_opts(b_e_max=B_E_MAX, n_d_max=1, little=args.little))
+            legs["orca_style"] = (so, eo.thrput_tok_s)
+        except X.ExgError:
+            pass
+        for leg, (sch, pred) in legs.items():
+            _, lat, st, _ = ctx.run(sch, reqs, slot_ctx=slot_ctx)
+            row[leg] = {"schedule": sch.as_dict(), "predicted_tok_s": pred, "tok_s": st["tok_s"],
+                        "mean_decode_batch": st["mean_decode_batch"], "decode_iters": st["decode_iters"],
+                        "encode_phases": st["encode_phases"], "wall_s": st["wall_s"], **sla(lat, L_b, reqs)}
+        for leg in ("ft_static", "orca_style"):
+            if "exegpt" in row and leg in row:
+                row["exegpt_over_" + leg.split("_")[0]] = row["exegpt"]["tok_s"] / row[leg]["tok_s"]
+            elif "exegpt" in row:
+                row["exegpt_over_" + leg.split("_")[0]] = None   # the baseline has no batch within the bound
+        res[name] = row
+    return res
 
 
 def run_layout(args, rank, world, local):
@@ -300,6 +355,8 @@ def main():
     ap.add_argument("--dyn", type=float, default=0.1, help="dynamic workload adjustment threshold (0: skip the run)")
     ap.add_argument("--roofline-steps", type=int, default=1, help="extra steps with per-launch kernel events")
     ap.add_argument("--bounds", default="all", choices=["all", "headline"])
+    ap.add_argument("--baseline-requests", type=int, default=512,
+                    help="requests per in-runner baseline run (FT static / ORCA-style / ExeGPT); 0: skip")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -376,13 +433,14 @@ def main():
     h2d = sum((r.input_len - 1) * 12 + 16 + 16 * r.output_len for r in reqs)
     d2h = sum(4 * r.output_len for r in reqs)
 
-    def sla(lat, L_b):
+    def sla(lat, L_b, rq=None):
         # SLA-(b) (the paper's main definition): a
         # sequence of the 99th-percentile length completes within L_B -- checked
         # on every request whose output is at most that long; SLA-(a): 99 % of
         # all requests complete within L_B.
-        upto = [lat[i] for i, r in enumerate(reqs) if r.output_len <= d.target_len]
-        at = [lat[i] for i, r in enumerate(reqs) if r.output_len == d.target_len]
+        rq = reqs if rq is None else rq
+        upto = [lat[i] for i, r in enumerate(rq) if r.output_len <= d.target_len]
+        at = [lat[i] for i, r in enumerate(rq) if r.output_len == d.target_len]
         return {"sla_b_met": bool(max(upto) < L_b), "sla_a_met": bool(np.percentile(lat, 99) <= L_b),
                 "max_latency_upto_p99_len_s": float(max(upto)),
                 "max_latency_at_p99_len_s": float(max(at)) if at else None, "p99_latency_s": float(np.percentile(lat, 99))}
@@ -459,6 +517,12 @@ def main():
                "mean_encode_batch": st_d["mean_encode_batch"], "mean_decode_batch": st_d["mean_decode_batch"],
                "variance": workload_variance(st_d), **sla(lat_d, L_head)}
 
+    # in-runner baselines (NEXT-4) on the first --baseline-requests requests
+    base = None
+    if args.baseline_requests > 0 and rank == 0:
+        base = in_runner_baselines(args, X, ctx, prof, cl, pin, pout, d, bounds, scheds,
+                                   reqs[:args.baseline_requests], slot_ctx, sla)
+
     # the scheduler's multi-GPU plan for this workload and bound (predicted by
     # the XSimulator on the measured per-GPU tables + the modeled interconnect)
     plan = {}
@@ -533,6 +597,11 @@ def main():
                                (COMM_ALPHA_S * 1e6, COMM_BW / 1e9), "predicted": plan},
             "workload_variance": workload_variance(var_st),
             "dyn_adjust": dyn,
+            "in_runner_baselines": base and {"requests": min(args.baseline_requests, args.requests),
+                                             "rule": "same kernels / requests / bounds; FT static = best "
+                                                     "simulated static batch within the bound (PAPER.md:112), "
+                                                     "ORCA-style = RRA N_D=1 (PAPER.md:116)",
+                                             "per_bound": base},
             "bounds": other,
             "setup_s": {"weights": t_weights, "profile": t_prof, "schedule_find_4_bounds": t_sched},
         }

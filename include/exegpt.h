@@ -44,8 +44,10 @@ typedef enum { EXG_ARCH_OPT = 0, EXG_ARCH_GPT3 = 1, EXG_ARCH_T5 = 2 } exg_arch; 
 typedef enum { EXG_BF16 = 0, EXG_FP32 = 1 } exg_dtype;
 /* bitmask of scheduling policies.  EXG_STATIC is the
  * FasterTransformer-style static batch (fixed batch, no early
- * termination) used only by exg_simulate, to derive latency bounds by the
- * paper's recipe; b_e = the static batch size. */
+ * termination): exg_simulate estimates it to derive latency bounds by the
+ * paper's recipe, and exg_run executes it on one GPU as the
+ * in-runner baseline; b_e = the static batch size.
+ * It is never chosen by exg_schedule_find. */
 typedef enum { EXG_RRA = 1, EXG_WAA_C = 2, EXG_WAA_M = 4, EXG_STATIC = 8 } exg_strategy;
 
 /* Model shape (Table 1) plus the weight seed of the
@@ -244,7 +246,12 @@ exg_status exg_schedule_find(const exg_profile* p, const exg_model_spec* spec, c
  * out_tokens: int32 [sum output_len] in request order (prefix-sum offsets);
  * out_latency_s: [n], from the start of the encode phase that admitted the
  * request to the end of the iteration that emitted its last token.
- * Greedy decoding, token accounting SURVEY.md §8(c) T6.  Collective. */
+ * Greedy decoding, token accounting SURVEY.md §8(c) T6.  Collective.
+ * sched->strategy == EXG_STATIC (one GPU): batches of b_e requests admitted
+ * only when the previous batch has drained; finished rows keep being
+ * computed until the batch's longest output is done and every
+ * request of the batch completes at that iteration (its latency ends there).
+ * Tokens are identical to RRA's (greedy, per-request; T13). */
 exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* reqs, int32_t n, int32_t* out_tokens,
                    double* out_latency_s, exg_run_stats* stats, const exg_run_opts* opts);
 

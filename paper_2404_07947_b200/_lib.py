@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libexegpt.so")
 
 EXG_OK, EXG_E_INPUT, EXG_E_INFEASIBLE, EXG_E_CUDA, EXG_E_NCCL, EXG_E_OOM, EXG_E_INTERNAL = range(7)
 EXG_ARCH_OPT, EXG_ARCH_GPT3, EXG_ARCH_T5 = 0, 1, 2
-EXG_RRA, EXG_WAA_C, EXG_WAA_M = 1, 2, 4
+EXG_RRA, EXG_WAA_C, EXG_WAA_M, EXG_STATIC = 1, 2, 4, 8
 MAX_STAGES = 8
 
 STATUS_NAMES = {0: "EXG_OK", 1: "EXG_E_INPUT", 2: "EXG_E_INFEASIBLE", 3: "EXG_E_CUDA", 4: "EXG_E_NCCL",
@@ -369,6 +369,16 @@ def rra_schedule(b_e: int, b_d: int, n_d: int) -> exg_schedule:
     """A caller-filled single-GPU RRA schedule (config 1 style)."""
     s = exg_schedule()
     s.strategy, s.b_e, s.b_d, s.n_d, s.tp_degree, s.tp_gpus = EXG_RRA, b_e, b_d, n_d, 1, 0
+    s.n_stages = 1
+    s.stage_first_gpu[0], s.stage_n_gpus[0], s.stage_layer_begin[0], s.stage_layer_end[0] = 0, 1, 0, 0
+    return s
+
+
+def static_schedule(b: int) -> exg_schedule:
+    """FasterTransformer-style static batch of b requests on one GPU
+    (the in-runner baseline)."""
+    s = exg_schedule()
+    s.strategy, s.b_e, s.b_d, s.n_d, s.tp_degree, s.tp_gpus = EXG_STATIC, b, b, 0, 1, 0
     s.n_stages = 1
     s.stage_first_gpu[0], s.stage_n_gpus[0], s.stage_layer_begin[0], s.stage_layer_end[0] = 0, 1, 0, 0
     return s

@@ -1,21 +1,38 @@
 // K4 prefill attention on the 5th-gen tensor cores (dh = 128).
 //
-// CTA = 128 queries of one (request, head).  Per 128-key tile j:
+// Persistent: one CTA per SM walks the work items (128 queries of one
+// (request, head)) -- longest causal items first, item id strided by the grid
+// -- so TMEM allocation, barrier set-up and the first Q / K / V loads of an
+// item overlap the previous item's softmax and P.V.  Per 128-key tile j:
 //   S_j = Q . K_j^T        tcgen05.mma kind::f16, M=128 N=128 K=128, fp32 in TMEM
 //   P_j = exp(s - m_j)     4 softmax warps, one query row per thread (TMEM -> regs),
 //                          causal mask, online max / sum; P_j -> smem as bf16
 //   O_j = P_j . V_j        tcgen05.mma, A = P (K-major), B = V (MN-major), fp32 in TMEM
 //   o   = o * exp(m_{j-1} - m_j) + O_j   (registers, one row per thread)
 // S and O are double-buffered in TMEM (4 x 128 columns) so the softmax of tile
-// j+1 overlaps the P.V of tile j.  Q, K, V arrive by 2-D TMA (SWIZZLE_128B)
-// straight from the packed qkv buffer and the KV cache.  Scores follow T4(e):
-// fp32(q.k) * fp32(scale); P is rounded to bf16 for the P.V MMA.
+// j+1 overlaps the P.V of tile j; Q is double-buffered in shared memory so the
+// next item's Q lands while the current one finishes.  Buffer indices and
+// mbarrier phases run on per-CTA counters across items.  Q, K, V arrive by
+// 2-D TMA (SWIZZLE_128B) straight from the packed qkv buffer and the KV cache.
+// Scores follow T4(e): fp32(q.k) * fp32(scale); P is rounded to bf16 for the
+// P.V MMA.  The arithmetic per query row is the same as a
+// one-item-per-CTA launch: results do not depend on the item order.
 #include "gemm_tc.cuh"
 #include "kernels.cuh"
 
 namespace exg {
 
 namespace {
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    EXG_CUDA(cudaGetDevice(&dev));
+    EXG_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
 constexpr int FQ = 128;          // queries per CTA
 constexpr int FK = 128;          // keys per tile
 constexpr int FD = 128;          // head dim
@@ -24,7 +41,9 @@ constexpr int Q_BYTES = 2 * TILE_BYTES;             // [128][128]
 constexpr int KV_BYTES = 2 * TILE_BYTES;            // K or V tile
 constexpr int P_BYTES = 2 * TILE_BYTES;
 constexpr int KV_STAGES = 2;
-constexpr size_t FMHA_SMEM = 1024 + Q_BYTES + KV_STAGES * 2 * KV_BYTES + P_BYTES + 256;
+constexpr int Q_STAGES = 2;
+constexpr size_t FMHA_SMEM = 1024 + Q_STAGES * Q_BYTES + KV_STAGES * 2 * KV_BYTES + P_BYTES + 256;
+static_assert(FMHA_SMEM <= 232448, "FMHA shared memory over the sm_100 per-CTA limit");
 
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -44,7 +63,7 @@ struct FmhaParams {
   const int32_t* cu_seqlens;
   const int32_t* slot;
   const int32_t* pos0;
-  int H, max_ctx;
+  int H, max_ctx, R, QT;   // QT = query tiles of the longest request
   float scale_log2;     // fp32(scale) * log2(e)
   float scale;
   bf16* out;
@@ -54,45 +73,63 @@ struct FmhaParams {
   int bias_ld, bias_off;
 };
 
+// Work item `id` -> (request, head, query tile); false if the tile is past
+// the request's length.  Query tiles are enumerated last-first (the causal
+// cost of a tile grows with its index), so the grid stride deals the
+// expensive items out first.
+struct Item {
+  int r, h, qb, t0, len, pos0, ntiles;
+  int64_t kv_row0;
+};
+__device__ __forceinline__ bool item_of(const FmhaParams& p, int id, Item& it) {
+  const int rh = p.R * p.H;
+  const int qt = p.QT - 1 - id / rh;
+  const int rem = id % rh;
+  it.r = rem / p.H;
+  it.h = rem % p.H;
+  it.t0 = p.cu_seqlens[it.r];
+  it.len = p.cu_seqlens[it.r + 1] - it.t0;
+  it.qb = qt * FQ;
+  if (it.qb >= it.len) return false;
+  it.pos0 = p.pos0[it.r];
+  const int last_key = p.causal ? it.pos0 + min(it.len, it.qb + FQ) - 1 : it.pos0 + it.len - 1;  // inclusive
+  it.ntiles = last_key / FK + 1;
+  it.kv_row0 = ((int64_t)p.slot[it.r] * p.H + it.h) * p.max_ctx;
+  return true;
+}
+
 __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV,
                                                               FmhaParams p) {
   griddep_launch_dependents();
-  griddep_wait();  // launched with PDL: predecessors complete + visible
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sQ = smem;
-  uint8_t* sK = sQ + Q_BYTES;                       // [stage]
-  uint8_t* sV = sK + KV_STAGES * KV_BYTES;          // [stage]
+  uint8_t* sQ = smem;                               // [q stage]
+  uint8_t* sK = sQ + Q_STAGES * Q_BYTES;            // [kv stage]
+  uint8_t* sV = sK + KV_STAGES * KV_BYTES;          // [kv stage]
   uint8_t* sP = sV + KV_STAGES * KV_BYTES;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sP + P_BYTES);
-  uint64_t* q_full = bars;              // 1
-  uint64_t* kv_full = bars + 1;         // 2
-  uint64_t* kv_empty = bars + 3;        // 2
-  uint64_t* s_full = bars + 5;          // 2
-  uint64_t* s_free = bars + 7;          // 2
-  uint64_t* p_full = bars + 9;          // 1
-  uint64_t* o_full = bars + 10;         // 2
-  uint64_t* o_free = bars + 12;         // 2
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 14);
+  uint64_t* q_full = bars;              // 2
+  uint64_t* q_empty = bars + 2;         // 2
+  uint64_t* kv_full = bars + 4;         // 2
+  uint64_t* kv_empty = bars + 6;        // 2
+  uint64_t* s_full = bars + 8;          // 2
+  uint64_t* s_free = bars + 10;         // 2
+  uint64_t* p_full = bars + 12;         // 1
+  uint64_t* o_full = bars + 13;         // 2
+  uint64_t* o_free = bars + 15;         // 2
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
 
-  const int r_req = blockIdx.z, h = blockIdx.y;
-  const int t0 = p.cu_seqlens[r_req], len = p.cu_seqlens[r_req + 1] - t0;
-  const int qb = blockIdx.x * FQ;
-  if (qb >= len) return;
-  const int pos0 = p.pos0[r_req];
-  const int last_key = p.causal ? pos0 + min(len, qb + FQ) - 1 : pos0 + len - 1;  // inclusive
-  const int ntiles = last_key / FK + 1;
-  const int64_t kv_row0 = ((int64_t)p.slot[r_req] * p.H + h) * p.max_ctx;
-
+  const int n_items = p.QT * p.R * p.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmQ);
     prefetch_tmap(&tmK);
     prefetch_tmap(&tmV);
-    mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
+      mbar_init(&q_full[i], 1);
+      mbar_init(&q_empty[i], 1);
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
@@ -109,140 +146,185 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
   // TMEM columns: S buffers at 0 / 128, O buffers at 256 / 384
+  griddep_wait();  // launched with PDL: predecessors complete + visible
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, Q_BYTES);
-      tma_load_2d(sQ, &tmQ, q_full, h * FD, t0 + qb);
-      tma_load_2d(sQ + TILE_BYTES, &tmQ, q_full, h * FD + 64, t0 + qb);
-      for (int j = 0; j < ntiles; ++j) {
-        const int s = j & 1;
-        if (j >= KV_STAGES) mbar_wait(&kv_empty[s], ((j >> 1) & 1) ^ 1);
-        mbar_arrive_expect_tx(&kv_full[s], 2 * KV_BYTES);
-        const int row = (int)(kv_row0 + j * FK);
-        tma_load_2d(sK + s * KV_BYTES, &tmK, &kv_full[s], 0, row);
-        tma_load_2d(sK + s * KV_BYTES + TILE_BYTES, &tmK, &kv_full[s], 64, row);
-        tma_load_2d(sV + s * KV_BYTES, &tmV, &kv_full[s], 0, row);
-        tma_load_2d(sV + s * KV_BYTES + TILE_BYTES, &tmV, &kv_full[s], 64, row);
+      uint32_t nq = 0, g = 0;   // items loaded, K/V tiles loaded by this CTA
+      for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
+        Item it;
+        if (!item_of(p, id, it)) continue;
+        const int qs = nq & 1;
+        if (nq >= Q_STAGES) mbar_wait(&q_empty[qs], ((nq >> 1) & 1) ^ 1);
+        mbar_arrive_expect_tx(&q_full[qs], Q_BYTES);
+        tma_load_2d(sQ + qs * Q_BYTES, &tmQ, &q_full[qs], it.h * FD, it.t0 + it.qb);
+        tma_load_2d(sQ + qs * Q_BYTES + TILE_BYTES, &tmQ, &q_full[qs], it.h * FD + 64, it.t0 + it.qb);
+        ++nq;
+        for (int j = 0; j < it.ntiles; ++j, ++g) {
+          const int s = g & 1;
+          if (g >= KV_STAGES) mbar_wait(&kv_empty[s], ((g >> 1) & 1) ^ 1);
+          mbar_arrive_expect_tx(&kv_full[s], 2 * KV_BYTES);
+          const int row = (int)(it.kv_row0 + j * FK);
+          tma_load_2d(sK + s * KV_BYTES, &tmK, &kv_full[s], 0, row);
+          tma_load_2d(sK + s * KV_BYTES + TILE_BYTES, &tmK, &kv_full[s], 64, row);
+          tma_load_2d(sV + s * KV_BYTES, &tmV, &kv_full[s], 0, row);
+          tma_load_2d(sV + s * KV_BYTES + TILE_BYTES, &tmV, &kv_full[s], 64, row);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(FQ, FK);                   // K-major A and B
       constexpr uint32_t idesc_o = umma_idesc_bf16(FQ, FD) | (1u << 16);      // B (V) MN-major
-      mbar_wait(q_full, 0);
-      auto issue_s = [&](int j) {
-        const int s = j & 1;
-        mbar_wait(&kv_full[s], (j >> 1) & 1);
-        if (j >= 2) mbar_wait(&s_free[s], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + s * 128;
-        const uint32_t qa = smem_u32(sQ), kb = smem_u32(sK + s * KV_BYTES);
+      uint32_t nq = 0, base = 0;   // items, tiles before the current item
+      for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
+        Item it;
+        if (!item_of(p, id, it)) continue;
+        const int qs = nq & 1;
+        mbar_wait(&q_full[qs], (nq >> 1) & 1);
+        auto issue_s = [&](int j) {
+          const uint32_t gj = base + j;
+          const int s = gj & 1;
+          mbar_wait(&kv_full[s], (gj >> 1) & 1);
+          if (gj >= 2) mbar_wait(&s_free[s], ((gj >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + s * 128;
+          const uint32_t qa = smem_u32(sQ + qs * Q_BYTES), kb = smem_u32(sK + s * KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < FD / 16; ++k) {
-          const uint32_t off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
-          umma_bf16(d, umma_desc_sw128(qa + off), umma_desc_sw128(kb + off), idesc_s, k ? 1u : 0u);
-        }
-        umma_commit(&s_full[s]);
-      };
-      issue_s(0);
-      for (int j = 0; j < ntiles; ++j) {
-        if (j + 1 < ntiles) issue_s(j + 1);
-        // O_j = P_j . V_j
-        const int s = j & 1;
-        mbar_wait(p_full, j & 1);
-        if (j >= 2) mbar_wait(&o_free[s], ((j >> 1) & 1) ^ 1);
-        tc_fence_after();
-        const uint32_t d = tmem + 256 + s * 128;
-        const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + s * KV_BYTES);
+          for (int k = 0; k < FD / 16; ++k) {
+            const uint32_t off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
+            umma_bf16(d, umma_desc_sw128(qa + off), umma_desc_sw128(kb + off), idesc_s, k ? 1u : 0u);
+          }
+          umma_commit(&s_full[s]);
+          if (j == it.ntiles - 1) umma_commit(&q_empty[qs]);   // last read of this Q
+        };
+        issue_s(0);
+        for (int j = 0; j < it.ntiles; ++j) {
+          if (j + 1 < it.ntiles) issue_s(j + 1);
+          // O_j = P_j . V_j
+          const uint32_t gj = base + j;
+          const int s = gj & 1;
+          mbar_wait(p_full, gj & 1);
+          if (gj >= 2) mbar_wait(&o_free[s], ((gj >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t d = tmem + 256 + s * 128;
+          const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + s * KV_BYTES);
 #pragma unroll
-        for (int k = 0; k < FK / 16; ++k) {
-          // A (P, K-major): 64-key blocks of 16 KB, 32 B per 16 keys
-          const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
-          // B (V, MN-major): 16 keys = two 8-key core groups of 1024 B
-          const uint32_t b_off = k * 2048;
-          umma_bf16(d, umma_desc_sw128(pa + a_off), desc_mn_sw128(vb + b_off, TILE_BYTES, 1024), idesc_o,
-                    k ? 1u : 0u);
+          for (int k = 0; k < FK / 16; ++k) {
+            // A (P, K-major): 64-key blocks of 16 KB, 32 B per 16 keys
+            const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
+            // B (V, MN-major): 16 keys = two 8-key core groups of 1024 B
+            const uint32_t b_off = k * 2048;
+            umma_bf16(d, umma_desc_sw128(pa + a_off), desc_mn_sw128(vb + b_off, TILE_BYTES, 1024), idesc_o,
+                      k ? 1u : 0u);
+          }
+          umma_commit(&o_full[s]);
+          umma_commit(&kv_empty[s]);
         }
-        umma_commit(&o_full[s]);
-        umma_commit(&kv_empty[s]);
+        base += it.ntiles;
+        ++nq;
       }
     }
   } else if (warp >= 4) {
     const int q = warp - 4;
     const int r = q * 32 + lane;                    // query row of the tile = TMEM lane
-    const int qpos = pos0 + qb + r;                  // absolute position of this query
-    const int kmax = p.causal ? qpos : pos0 + len - 1;  // last key this query sees
-    const float* brow = (p.bias && qb + r < len) ? p.bias + (int64_t)h * p.bias_ld + p.bias_off - qpos : nullptr;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    float o[FD];
+    uint32_t base = 0;
+    for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
+      Item it;
+      if (!item_of(p, id, it)) continue;
+      const int qpos = it.pos0 + it.qb + r;                  // absolute position of this query
+      const int kmax = p.causal ? qpos : it.pos0 + it.len - 1;  // last key this query sees
+      const float* brow =
+          (p.bias && it.qb + r < it.len) ? p.bias + (int64_t)it.h * p.bias_ld + p.bias_off - qpos : nullptr;
+      float o[FD];
 #pragma unroll
-    for (int d = 0; d < FD; ++d) o[d] = 0.f;
-    float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
-    for (int j = 0; j <= ntiles; ++j) {
-      if (j < ntiles) {
-        const int s = j & 1;
-        mbar_wait(&s_full[s], (j >> 1) & 1);
-        tc_fence_after();
-        // pass 1: row max over the tile (masked)
-        const uint32_t sa = tmem + lane_base + s * 128;
-        float mx = -INFINITY;
-        for (int c = 0; c < FK; c += 16) {
-          float v[16];
-          tmem_ld16(sa + c, v);
-#pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int kpos = j * FK + c + e;
-            float sc = (kpos <= kmax) ? __fmul_rn(v[e], p.scale) : -INFINITY;
-            if (brow && kpos <= kmax) sc = __fadd_rn(sc, brow[kpos]);
-            mx = fmaxf(mx, sc);
-          }
-        }
-        const float m_new = fmaxf(m, mx);
-        const float alpha = (m == -INFINITY) ? 0.f : exp2f((m - m_new) * 1.4426950408889634f);
-        // P_j may overwrite the P buffer once P_{j-1}.V_{j-1} has completed
-        if (j >= 1) mbar_wait(&o_full[(j - 1) & 1], ((j - 1) >> 1) & 1);
-        float sum = 0.f;
-        for (int c = 0; c < FK; c += 16) {
-          float v[16];
-          tmem_ld16(sa + c, v);
-          uint32_t pk[8];
-#pragma unroll
-          for (int e = 0; e < 16; e += 2) {
-            const int kpos = j * FK + c + e;
-            float s0 = __fmul_rn(v[e], p.scale), s1 = __fmul_rn(v[e + 1], p.scale);
-            if (brow) {
-              if (kpos <= kmax) s0 = __fadd_rn(s0, brow[kpos]);
-              if (kpos + 1 <= kmax) s1 = __fadd_rn(s1, brow[kpos + 1]);
-            }
-            const float p0 = (kpos <= kmax && m_new != -INFINITY)
-                                 ? exp2f((s0 - m_new) * 1.4426950408889634f) : 0.f;
-            const float p1 = (kpos + 1 <= kmax && m_new != -INFINITY)
-                                 ? exp2f((s1 - m_new) * 1.4426950408889634f) : 0.f;
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-            sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
-            pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
-          }
-          // row r, keys c..c+15: two 16-byte chunks in the SW128 K-major image
-          uint8_t* blk = sP + (c >> 6) * TILE_BYTES;
-          const int ch = (c & 63) >> 3;
-          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-        }
-        l = l * alpha + sum;
-        m = m_new;
-        fence_proxy_async_smem();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(&s_free[s]);
-          mbar_arrive(p_full);
-        }
-        // accumulate O_{j-1} (its rescale factor was alpha_prev)
-        if (j >= 1) {
-          const int so = (j - 1) & 1;
-          const uint32_t oa = tmem + lane_base + 256 + so * 128;
+      for (int d = 0; d < FD; ++d) o[d] = 0.f;
+      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
+      for (int j = 0; j <= it.ntiles; ++j) {
+        const uint32_t gj = base + j;
+        if (j < it.ntiles) {
+          const int s = gj & 1;
+          mbar_wait(&s_full[s], (gj >> 1) & 1);
           tc_fence_after();
+          // pass 1: row max over the tile (masked)
+          const uint32_t sa = tmem + lane_base + s * 128;
+          float mx = -INFINITY;
+          for (int c = 0; c < FK; c += 16) {
+            float v[16];
+            tmem_ld16(sa + c, v);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const int kpos = j * FK + c + e;
+              float sc = (kpos <= kmax) ? __fmul_rn(v[e], p.scale) : -INFINITY;
+              if (brow && kpos <= kmax) sc = __fadd_rn(sc, brow[kpos]);
+              mx = fmaxf(mx, sc);
+            }
+          }
+          const float m_new = fmaxf(m, mx);
+          const float alpha = (m == -INFINITY) ? 0.f : exp2f((m - m_new) * 1.4426950408889634f);
+          // P_j may overwrite the P buffer once the previous P.V has completed
+          // (within the item; the previous item's last P.V was awaited below)
+          if (j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
+          float sum = 0.f;
+          for (int c = 0; c < FK; c += 16) {
+            float v[16];
+            tmem_ld16(sa + c, v);
+            uint32_t pk[8];
+#pragma unroll
+            for (int e = 0; e < 16; e += 2) {
+              const int kpos = j * FK + c + e;
+              float s0 = __fmul_rn(v[e], p.scale), s1 = __fmul_rn(v[e + 1], p.scale);
+              if (brow) {
+                if (kpos <= kmax) s0 = __fadd_rn(s0, brow[kpos]);
+                if (kpos + 1 <= kmax) s1 = __fadd_rn(s1, brow[kpos + 1]);
+              }
+              const float p0 = (kpos <= kmax && m_new != -INFINITY)
+                                   ? exp2f((s0 - m_new) * 1.4426950408889634f) : 0.f;
+              const float p1 = (kpos + 1 <= kmax && m_new != -INFINITY)
+                                   ? exp2f((s1 - m_new) * 1.4426950408889634f) : 0.f;
+              __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+              sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
+              pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+            }
+            // row r, keys c..c+15: two 16-byte chunks in the SW128 K-major image
+            uint8_t* blk = sP + (c >> 6) * TILE_BYTES;
+            const int ch = (c & 63) >> 3;
+            *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
+          l = l * alpha + sum;
+          m = m_new;
+          fence_proxy_async_smem();
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(&s_free[s]);
+            mbar_arrive(p_full);
+          }
+          // accumulate O_{j-1} (its rescale factor was alpha_prev)
+          if (j >= 1) {
+            const int so = (gj - 1) & 1;
+            const uint32_t oa = tmem + lane_base + 256 + so * 128;
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < FD; c += 16) {
+              float v[16];
+              tmem_ld16(oa + c, v);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) o[c + e] = o[c + e] * alpha_prev + v[e];
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&o_free[so]);
+          }
+          alpha_prev = alpha;
+        } else {
+          // last tile's P.V
+          const int so = (gj - 1) & 1;
+          mbar_wait(&o_full[so], ((gj - 1) >> 1) & 1);
+          tc_fence_after();
+          const uint32_t oa = tmem + lane_base + 256 + so * 128;
 #pragma unroll
           for (int c = 0; c < FD; c += 16) {
             float v[16];
@@ -254,34 +336,21 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
           __syncwarp();
           if (lane == 0) mbar_arrive(&o_free[so]);
         }
-        alpha_prev = alpha;
-      } else {
-        // last tile's P.V
-        const int so = (j - 1) & 1;
-        mbar_wait(&o_full[so], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-        const uint32_t oa = tmem + lane_base + 256 + so * 128;
-#pragma unroll
-        for (int c = 0; c < FD; c += 16) {
-          float v[16];
-          tmem_ld16(oa + c, v);
-#pragma unroll
-          for (int e = 0; e < 16; ++e) o[c + e] = o[c + e] * alpha_prev + v[e];
-        }
       }
-    }
-    if (qb + r < len) {
-      const float inv = 1.f / l;
-      bf16* dst = p.out + (int64_t)(t0 + qb + r) * p.ldo + h * FD;
+      base += it.ntiles;
+      if (it.qb + r < it.len) {
+        const float inv = 1.f / l;
+        bf16* dst = p.out + (int64_t)(it.t0 + it.qb + r) * p.ldo + it.h * FD;
 #pragma unroll
-      for (int c = 0; c < FD; c += 8) {
-        uint32_t pk[4];
+        for (int c = 0; c < FD; c += 8) {
+          uint32_t pk[4];
 #pragma unroll
-        for (int e = 0; e < 8; e += 2) {
-          __nv_bfloat162 b2 = __floats2bfloat162_rn(o[c + e] * inv, o[c + e + 1] * inv);
-          pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+          for (int e = 0; e < 8; e += 2) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(o[c + e] * inv, o[c + e + 1] * inv);
+            pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
+          }
+          *reinterpret_cast<uint4*>(dst + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         }
-        *reinterpret_cast<uint4*>(dst + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
       }
     }
   }
@@ -310,12 +379,16 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   // Q: the packed qkv buffer [q_rows][ldq] (rows past the last token are
   // zero-filled by TMA and never stored); K/V: the cache viewed as
   // [kv_rows = slots*H*max_ctx][dh]
-  FmhaParams p{a.cu_seqlens, a.slot, a.pos0, a.H, a.max_ctx,
+  const int QT = (a.max_len + FQ - 1) / FQ;
+  FmhaParams p{a.cu_seqlens, a.slot, a.pos0, a.H, a.max_ctx, a.R, QT,
                a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo, a.causal, a.bias, a.bias_ld, a.bias_off};
+  const int n_items = QT * a.R * a.H;
+  if (n_items <= 0) return true;
   const CUtensorMap tq = make_tmap_bf16(a.q, a.q_rows, a.ldq, a.ldq, 128);
   const CUtensorMap tk = make_tmap_bf16(a.kc, a.kv_rows, FD, FD, 128);
   const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 128);
-  dim3 grid((a.max_len + FQ - 1) / FQ, a.H, a.R);
+  // persistent grid: one CTA per SM (227 KB of shared memory, 512 TMEM columns)
+  const int grid = std::min(n_items, sm_count());
   launch_pdl(fmha_prefill_kernel, dim3(grid), dim3(256), FMHA_SMEM, st, tq, tk, tv, p);
   EXG_CHECK_LAUNCH();
   return true;

@@ -369,7 +369,7 @@ exg_status exg_run(exg_ctx* ctx, const exg_schedule* sched, const exg_request* r
       ctx->multi->run(*sched, reqs, n, out_tokens, out_latency_s, stats, opts);
       return EXG_OK;
     }
-    if (sched->strategy != EXG_RRA)
+    if (sched->strategy != EXG_RRA && sched->strategy != EXG_STATIC)
       return fail(EXG_E_INFEASIBLE, "WAA needs >= 2 GPUs (SPEC.md:233); this context has 1");
     if (sched->tp_degree > 1 || sched->n_stages > 1)
       return fail(EXG_E_INFEASIBLE, "schedule needs more GPUs than this context has");

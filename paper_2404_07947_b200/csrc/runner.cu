@@ -9,6 +9,14 @@
 // row table simply omits the finished rows.  When no requests remain the
 // decode phases drain without encoding.
 //
+// FasterTransformer-style static batch (EXG_STATIC, the in-runner baseline
+// of SURVEY.md §8(f) NEXT-4): b_e requests are admitted only
+// when the previous batch has finished, encoded together, and decoded with a
+// fixed batch -- completed queries are not early-terminated, they keep being
+// computed (the "white boxes" of PAPER.md:112) until the batch's longest
+// output is done; the batch's results return together at that iteration
+// (latency of every request = batch start .. batch end).
+//
 // The host never waits on the GPU inside the loop: row tables go through a
 // ring of pinned staging buffers recycled by events, tokens are written by
 // the argmax kernel straight into a device output array, and times come from
@@ -59,6 +67,7 @@ struct Staging {
 
 struct Row {
   int req, slot, pos, emitted;
+  bool live = true;   // false: finished, still computed by the static batch
 };
 
 struct EventPool {
@@ -89,8 +98,10 @@ double pct(std::vector<double> v, double q) {
 void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, int32_t* out_tokens,
              double* out_latency, exg_run_stats* stats, const exg_run_opts* opts) {
   const Dims& D = E.dims();
-  if (s.strategy != EXG_RRA) throw std::invalid_argument("run_rra: strategy is not RRA");
-  if (s.b_e < 1 || s.b_d < s.b_e || s.n_d < 1) throw std::invalid_argument("RRA needs 1 <= B_E <= B_D, N_D >= 1");
+  const bool ft = s.strategy == EXG_STATIC;
+  if (s.strategy != EXG_RRA && !ft) throw std::invalid_argument("run_rra: strategy is not RRA or STATIC");
+  if (ft ? s.b_e < 1 : (s.b_e < 1 || s.b_d < s.b_e || s.n_d < 1))
+    throw std::invalid_argument(ft ? "static batch needs b_e >= 1" : "RRA needs 1 <= B_E <= B_D, N_D >= 1");
   // token accounting: decoder-only encode = positions
   // 0..n-2, decode u consumes x[n-1] / y[u-1] at position n-1+u-1;
   // encoder-decoder encode = all n tokens, decode u consumes the start token
@@ -115,7 +126,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   const int need_ctx = ed ? max_out : max_ctx;
   const int slot_ctx = (opts && opts->slot_ctx > 0) ? opts->slot_ctx : need_ctx;
   if (slot_ctx < need_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
-  const int B_D = s.b_d, B_E = s.b_e;
+  const int B_D = ft ? s.b_e : s.b_d, B_E = s.b_e;
   const int enc_drop = ed ? 0 : 1;   // input tokens the encode phase does not process
   E.ensure_kv(B_D, slot_ctx, -1, ed ? max_in : 0);
   E.ensure_workspace(std::max(1, B_E * (max_in - enc_drop)), B_D);
@@ -127,7 +138,8 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   const size_t enc_ints = (size_t)3 * B_E * max_in + 3 * (B_E + 1) + 2 * B_E;
   const size_t dec_ints = (size_t)5 * B_D;
   const size_t tab_ints = std::max(enc_ints, dec_ints);
-  EXG_CUDA(cudaMalloc(&d_out, sizeof(int32_t) * std::max<int64_t>(total_out, 1)));
+  // + B_D scratch entries: the tokens of finished rows a static batch still computes
+  EXG_CUDA(cudaMalloc(&d_out, sizeof(int32_t) * (total_out + B_D)));
   EXG_CUDA(cudaMalloc(&d_tab, sizeof(int32_t) * (enc_ints + dec_ints)));
   int32_t* d_enc = d_tab;
   int32_t* d_dec = d_tab + enc_ints;
@@ -157,7 +169,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   };
 
   int next_req = 0;
-  const double dyn = opts ? opts->dyn_threshold : 0.0;
+  const double dyn = (opts && !ft) ? opts->dyn_threshold : 0.0;
   double mean_enc_tokens = 0, steady_batch_sum = 0;
   int64_t steady_iters = 0, admitted_phases = 0;
   for (int r = 0; r < n; ++r) mean_enc_tokens += reqs[r].input_len - enc_drop;
@@ -170,6 +182,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   while (next_req < n || !active.empty()) {
     // ---------------- encode phase ----------------
     int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
+    if (ft && !active.empty()) admit = 0;   // static batch: no admission until it has drained
     if (dyn > 0 && admit > 0) {
       // dynamic workload adjustment: decoder batch below /
       // above +-dyn of its running average -> admit that many rows more / fewer
@@ -253,21 +266,26 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
     }
     record(1, admit);   // tokens field of an encode-end event: requests admitted
     // ---------------- N_D decode iterations ----------------
-    for (int u = 0; u < s.n_d && !active.empty(); ++u) {
+    for (int u = 0; (ft || u < s.n_d) && !active.empty(); ++u) {
       const int B = (int)active.size();
       Staging::Slot& sl = stage.acquire();
       int32_t* h = sl.host;
       int max_keys = 0, max_xkeys = 0;
       double sum_keys = 0, sum_xkeys = 0;
+      int live = 0;
       for (int i = 0; i < B; ++i) {
         const Row& rw = active[i];
+        // a finished row of a static batch keeps decoding past its length:
+        // its position is clamped inside its own slot, its token goes to scratch
+        const int pos = rw.live ? rw.pos : std::min({rw.pos, slot_ctx - 1, D.max_pos - 1});
+        live += rw.live;
         h[i] = rw.slot;
-        h[B + i] = rw.pos;
-        h[2 * B + i] = rw.pos + 1;
-        h[3 * B + i] = (int32_t)(base[rw.req] + rw.emitted);
+        h[B + i] = pos;
+        h[2 * B + i] = pos + 1;
+        h[3 * B + i] = rw.live ? (int32_t)(base[rw.req] + rw.emitted) : (int32_t)(total_out + i);
         h[4 * B + i] = reqs[rw.req].input_len;
-        max_keys = std::max(max_keys, rw.pos + 1);
-        sum_keys += rw.pos + 1;
+        max_keys = std::max(max_keys, pos + 1);
+        sum_keys += pos + 1;
         max_xkeys = std::max(max_xkeys, reqs[rw.req].input_len);
         sum_xkeys += reqs[rw.req].input_len;
       }
@@ -291,12 +309,12 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       if (dumping) {
         for (int i = 0; i < B; ++i) {
           const Row& rw = active[i];
-          if (!opts->dump_mask[rw.req]) continue;
+          if (!rw.live || !opts->dump_mask[rw.req]) continue;
           float* dst = opts->logits_out + (dump_base[rw.req] + rw.emitted) * (int64_t)D.V;
           EXG_CUDA(cudaMemcpyAsync(dst, E.logits() + (int64_t)i * D.V, sizeof(float) * D.V, cudaMemcpyDeviceToHost, st));
         }
       }
-      const int ev_it = record(2, B);
+      const int ev_it = record(2, live);
       ++decode_iters;
       batch_sum += B;
       if (next_req < n) {   // decode batch average while requests keep arriving (not the drain)
@@ -305,6 +323,22 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       }
       // early termination + stable compaction of the row table
       int w = 0;
+      if (ft) {
+        int alive = 0;
+        for (Row& rw : active) {
+          rw.pos += 1;
+          if (rw.live && ++rw.emitted == reqs[rw.req].output_len) rw.live = false;
+          alive += rw.live;
+        }
+        if (alive == 0) {   // the batch is done: every result returns at this iteration
+          for (const Row& rw : active) {
+            done_ev[rw.req] = ev_it;
+            free_slots.push_back(rw.slot);
+          }
+          active.clear();
+        }
+        continue;
+      }
       for (int i = 0; i < B; ++i) {
         Row rw = active[i];
         rw.emitted += 1;

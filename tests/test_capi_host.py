@@ -217,3 +217,32 @@ def test_profile_comm_model_tables(L, tmp_path):
                 assert t == alpha + (tp - 1) * x / bw
     with pytest.raises(L.ExgError):
         P.comm_model(alpha, 0.0)
+
+
+def test_in_runner_baseline_picks(L, tmp_path):
+    """bench.py's NEXT-4 legs: the FT static batch is the simulated
+    max-throughput B within the bound (checked against a brute-force scan of
+    the oracle simulator), and the ORCA-style schedule (Algorithm 1 with
+    N_D^max = 1) admits every iteration."""
+    import bench
+    from oracle import simulator as sim
+    spec, m, prof, d, cl = _setup()
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    S = sim.Simulator(prof, m, cl, d.pmf_in, d.pmf_out, d.target_len)
+    lats = [S.simulate_static(B) for B in (1, 8, 64)]
+    orca = 0
+    for L_b in [e.latency_s * 1.01 for e in lats if e.feasible]:
+        B, e = bench.static_pick(L, P, mspec, ccl, pin, pout, d.target_len, L_b)
+        brute = [(S.simulate_static(b).thrput_tok_s, -b) for b in range(1, 1025)
+                 if S.simulate_static(b).feasible and S.simulate_static(b).latency_s <= L_b]
+        assert (e.thrput_tok_s, -B) == max(brute)
+        assert e.latency_s <= L_b
+        try:
+            s, _ = L.schedule_find(P, mspec, ccl, pin, pout, d.target_len, L_b, L.EXG_RRA,
+                                   L.search_opts(n_d_max=1, b_e_max=64))
+        except L.ExgError:      # iteration-level admission can miss a tight bound
+            continue
+        assert s.n_d == 1
+        orca += 1
+    assert orca >= 1
+    assert bench.static_pick(L, P, mspec, ccl, pin, pout, d.target_len, 1e-9) is None

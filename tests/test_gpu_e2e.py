@@ -143,3 +143,39 @@ def test_profile_tp_shards(setup, tmp_path):
         for ph in ("enc", "dec"):
             assert np.all(np.array(P.attn[(ph, t)].t) > 0) and np.all(np.array(P.rest[(ph, t)].t) > 0)
     assert 2 in P.tp_sync and 4 in P.tp_sync and P.pp_sync is not None
+
+
+def test_static_batch_baseline(setup):
+    """FT-style static batch (EXG_STATIC; SURVEY.md §8(f)
+    NEXT-4): finished rows keep being computed until the batch's longest
+    output is done.  Per-request results are batch invariant (T13), so ids
+    and logits are bit-identical to the RRA run; every request of a batch
+    completes at the same iteration."""
+    X, T, spec, W, reqs, ctx, ora = setup
+    base_t, _, _, base_l = ctx.run(X.rra_schedule(4, 8, 6), reqs, dump=range(len(reqs)))
+    for b in (1, 3, 8):
+        toks, lat, st, lg = ctx.run(X.static_schedule(b), reqs, dump=range(len(reqs)))
+        assert toks == base_t
+        for r in range(len(reqs)):
+            assert np.array_equal(lg[r], base_l[r]), (b, r)
+        batches = [list(range(k, min(k + b, len(reqs)))) for k in range(0, len(reqs), b)]
+        assert st["encode_phases"] == len(batches)
+        assert st["decode_iters"] == sum(max(reqs[r].output_len for r in g) for g in batches)
+        assert st["mean_decode_batch"] == pytest.approx(
+            sum(len(g) * max(reqs[r].output_len for r in g) for g in batches) / st["decode_iters"])
+        for g in batches:
+            assert len({float(lat[r]) for r in g}) == 1, (b, g)
+        assert np.all(lat > 0)
+    # a finished row whose position runs past its slot / max_pos keeps being
+    # computed (clamped inside its own slot) without touching its batch-mates
+    from workload import Request
+    rng = np.random.default_rng(1)
+    two = [Request(rng.integers(0, 512, 60).astype(np.int32), 60, 4),
+           Request(rng.integers(0, 512, 8).astype(np.int32), 8, 24)]
+    ref_t, _, _, ref_l = ctx.run(X.rra_schedule(1, 1, 2), two, dump=range(2))
+    toks, _, st, lg = ctx.run(X.static_schedule(2), two, dump=range(2))
+    assert toks == ref_t and st["decode_iters"] == 24
+    for r in range(2):
+        assert np.array_equal(lg[r], ref_l[r]), r
+    with pytest.raises(X.ExgError):
+        ctx.run(X.static_schedule(0), reqs)

@@ -1,0 +1,10 @@
+# FMHA persistent-kernel A/B + parity: prefill attention probes (old build vs new),
+# GPU kernel / T5 / e2e tests
+mkdir -p gpurun_out
+echo "== old" > gpurun_out/fmha_ab.txt
+EXG_PROBE_LIB=$PWD/tools/_old/libexegpt.so timeout 300 python tools/probe_kernels.py pmix >> gpurun_out/fmha_ab.txt 2>&1
+echo "== new" >> gpurun_out/fmha_ab.txt
+timeout 300 python tools/probe_kernels.py pmix >> gpurun_out/fmha_ab.txt 2>&1
+timeout 1200 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_t5.py tests/test_gpu_e2e.py -m gpu -x -q > gpurun_out/pytest_fmha.log 2>&1; echo "pytest rc $?"
+tail -3 gpurun_out/pytest_fmha.log
+cat gpurun_out/fmha_ab.txt

@@ -11,6 +11,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2404_07947_b200 import _lib as L  # noqa: E402
+L.LIB_PATH = os.environ.get("EXG_PROBE_LIB", L.LIB_PATH)   # A/B against another build
 
 dev = torch.device("cuda:0")
 st = lambda: torch.cuda.current_stream().cuda_stream
@@ -121,6 +122,30 @@ def pattn(R, n, H=40, dh=128):
     print("prefill-attn R=%d n=%d: %8.1f us  %7.1f TFLOP/s" % (R, n, t * 1e6, flops / t / 1e12))
 
 
+def pattn_mix(R, H=40, dh=128, seed=0):
+    """Prefill attention at the task-S input-length mix (R requests)."""
+    from workload import make_requests, task_dists
+    d = task_dists("S")
+    lens = [max(1, r.input_len - 1) for r in make_requests(R, d.pmf_in, d.pmf_out, 50272, 0xE6E10002 + seed)]
+    T, max_ctx = sum(lens), max(lens)
+    kc = torch.randn(R, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    vc = torch.randn(R, H, max_ctx, dh, device=dev).to(torch.bfloat16)
+    q = torch.randn(T, 3 * H * dh, device=dev).to(torch.bfloat16)
+    cu = torch.tensor([0] + list(np.cumsum(lens)), dtype=torch.int32, device=dev)
+    slot = torch.arange(R, dtype=torch.int32, device=dev)
+    p0 = torch.zeros(R, dtype=torch.int32, device=dev)
+    out = torch.empty(T, H * dh, device=dev, dtype=torch.bfloat16)
+
+    def fn():
+        L.check(L.lib().exg_op_prefill_attention(q.data_ptr(), 3 * H * dh, kc.data_ptr(), vc.data_ptr(),
+                                                 cu.data_ptr(), slot.data_ptr(), p0.data_ptr(), R, max_ctx,
+                                                 out.data_ptr(), H * dh, H, dh, max_ctx, R, T, 0.0883883, 1, None, 0,
+                                                 0, st()))
+    t = timeit(fn)
+    flops = sum(4.0 * H * dh * n * (n + 1) / 2 for n in lens)
+    print("prefill-attn mix R=%d mean n %.0f: %8.1f us  %7.1f TFLOP/s" % (R, T / R, t * 1e6, flops / t / 1e12))
+
+
 def stream_probe():
     """HBM ceiling of the bulk-copy ring (no MMA): 148..592 CTAs x chunk x stages."""
     import ctypes
@@ -186,6 +211,12 @@ if __name__ == "__main__":
             for B in (16, 56, 79, 256):
                 dattn_mix(B, 512)
         L.lib().exg_diag_decode_stages(0)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "pmix":
+        for R in (8, 32, 52, 64):
+            pattn_mix(R)
+        for R, n in ((16, 256), (16, 512), (8, 1024), (64, 128)):
+            pattn(R, n)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pattn":
         pattn(int(sys.argv[2]), int(sys.argv[3]))
