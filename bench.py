@@ -217,19 +217,23 @@ def in_runner_baselines(args, X, ctx, prof, cl, pin, pout, d, bounds, scheds, re
         pick = static_pick(X, prof, ctx.mspec, cl, pin, pout, d.target_len, L_b * (1 - args.margin))
         if pick:
             legs["ft_static"] = (X.static_schedule(pick[0]), pick[1].thrput_tok_s)
+        else:
+            row["ft_static"] = {"infeasible": "no static batch within the bound on the profile"}
         try:
             so, eo = X.schedule_find(prof, ctx.mspec, cl, pin, pout, d.target_len, L_b * (1 - args.margin),
                                      X.EXG_RRA, X.search_opts(b_e_max=B_E_MAX, n_d_max=1, little=args.little))
             legs["orca_style"] = (so, eo.thrput_tok_s)
-        except X.ExgError:
-            pass
+        except X.ExgError as e:
+            # an encode every iteration puts each request behind O(S) encode
+            # phases: no N_D = 1 schedule meets a finite bound on task S
+            row["orca_style"] = {"infeasible": str(e)}
         for leg, (sch, pred) in legs.items():
             _, lat, st, _ = ctx.run(sch, reqs, slot_ctx=slot_ctx)
             row[leg] = {"schedule": sch.as_dict(), "predicted_tok_s": pred, "tok_s": st["tok_s"],
                         "mean_decode_batch": st["mean_decode_batch"], "decode_iters": st["decode_iters"],
                         "encode_phases": st["encode_phases"], "wall_s": st["wall_s"], **sla(lat, L_b, reqs)}
         for leg in ("ft_static", "orca_style"):
-            if "exegpt" in row and leg in row:
+            if "exegpt" in row and "tok_s" in row.get(leg, {}):
                 row["exegpt_over_" + leg.split("_")[0]] = row["exegpt"]["tok_s"] / row[leg]["tok_s"]
             elif "exegpt" in row:
                 row["exegpt_over_" + leg.split("_")[0]] = None   # the baseline has no batch within the bound

@@ -5,10 +5,13 @@
 // -- so TMEM allocation, barrier set-up and the first Q / K / V loads of an
 // item overlap the previous item's softmax and P.V.  Per 128-key tile j:
 //   S_j = Q . K_j^T        tcgen05.mma kind::f16, M=128 N=128 K=128, fp32 in TMEM
-//   P_j = exp(s - m_j)     4 softmax warps, one query row per thread (TMEM -> regs),
-//                          causal mask, online max / sum; P_j -> smem as bf16
+//   P_j = exp(s - m_j)     8 softmax warps: one query row per thread pair, each
+//                          thread of the pair exponentiates one 64-key half of
+//                          the tile (both take the row max over all 128 keys,
+//                          so no exchange per tile); online max / half sums;
+//                          P_j -> smem as bf16
 //   O_j = P_j . V_j        tcgen05.mma, A = P (K-major), B = V (MN-major), fp32 in TMEM
-//   o   = o * exp(m_{j-1} - m_j) + O_j   (registers, one row per thread)
+//   o   = o * exp(m_{j-1} - m_j) + O_j   (registers, one 64-dim half per thread)
 // S and O are double-buffered in TMEM (4 x 128 columns) so the softmax of tile
 // j+1 overlaps the P.V of tile j; Q is double-buffered in shared memory so the
 // next item's Q lands while the current one finishes.  Buffer indices and
@@ -42,7 +45,8 @@ constexpr int KV_BYTES = 2 * TILE_BYTES;            // K or V tile
 constexpr int P_BYTES = 2 * TILE_BYTES;
 constexpr int KV_STAGES = 2;
 constexpr int Q_STAGES = 2;
-constexpr size_t FMHA_SMEM = 1024 + Q_STAGES * Q_BYTES + KV_STAGES * 2 * KV_BYTES + P_BYTES + 256;
+constexpr int SM_WARPS = 8;      // softmax warps (two per TMEM lane quarter)
+constexpr size_t FMHA_SMEM = 1024 + Q_STAGES * Q_BYTES + KV_STAGES * 2 * KV_BYTES + P_BYTES + 256 + 2 * FQ * 4;
 static_assert(FMHA_SMEM <= 232448, "FMHA shared memory over the sm_100 per-CTA limit");
 
 __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t smem_addr, uint32_t lbo, uint32_t sbo) {
@@ -98,7 +102,7 @@ __device__ __forceinline__ bool item_of(const FmhaParams& p, int id, Item& it) {
   return true;
 }
 
-__global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_constant__ CUtensorMap tmQ,
+__global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV,
                                                               FmhaParams p) {
@@ -120,6 +124,7 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
   uint64_t* o_full = bars + 13;         // 2
   uint64_t* o_free = bars + 15;         // 2
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
+  float* lx = reinterpret_cast<float*>(sP + P_BYTES + 256);   // [2][FQ] row-sum halves
 
   const int n_items = p.QT * p.R * p.H;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -133,11 +138,11 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
       mbar_init(&kv_full[i], 1);
       mbar_init(&kv_empty[i], 1);
       mbar_init(&s_full[i], 1);
-      mbar_init(&s_free[i], 4);
+      mbar_init(&s_free[i], SM_WARPS);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_free[i], 4);
+      mbar_init(&o_free[i], SM_WARPS);
     }
-    mbar_init(p_full, 4);
+    mbar_init(p_full, SM_WARPS);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_holder, 512);
@@ -226,9 +231,11 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
       }
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;
+    // warp w reads TMEM lanes 32*(w%4).. (hardware rule); hf = key / dim half
+    const int q = warp & 3, hf = (warp - 4) >> 2;
     const int r = q * 32 + lane;                    // query row of the tile = TMEM lane
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    auto pair_bar = [q] { asm volatile("bar.sync %0, 64;" ::"r"(1 + q) : "memory"); };
     uint32_t base = 0;
     for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
       Item it;
@@ -237,9 +244,10 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
       const int kmax = p.causal ? qpos : it.pos0 + it.len - 1;  // last key this query sees
       const float* brow =
           (p.bias && it.qb + r < it.len) ? p.bias + (int64_t)it.h * p.bias_ld + p.bias_off - qpos : nullptr;
-      float o[FD];
+      constexpr int HD = FD / 2;                      // output dims / keys per half
+      float o[HD];
 #pragma unroll
-      for (int d = 0; d < FD; ++d) o[d] = 0.f;
+      for (int d = 0; d < HD; ++d) o[d] = 0.f;
       float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
       for (int j = 0; j <= it.ntiles; ++j) {
         const uint32_t gj = base + j;
@@ -247,49 +255,49 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
           const int s = gj & 1;
           mbar_wait(&s_full[s], (gj >> 1) & 1);
           tc_fence_after();
-          // pass 1: row max over the tile (masked)
-          const uint32_t sa = tmem + lane_base + s * 128;
+          // pass 1: this half's 64 scores (scaled, biased, masked) into
+          // registers and their max; the row max over the tile is the max of
+          // the two halves' (exchanged through shared memory)
+          const uint32_t sa = tmem + lane_base + s * 128 + hf * HD;
+          const int k0 = j * FK + hf * HD;
+          float sc[HD];
           float mx = -INFINITY;
-          for (int c = 0; c < FK; c += 16) {
-            float v[16];
-            tmem_ld16(sa + c, v);
+#pragma unroll
+          for (int c = 0; c < HD; c += 16) {
+            tmem_ld16(sa + c, sc + c);
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              const int kpos = j * FK + c + e;
-              float sc = (kpos <= kmax) ? __fmul_rn(v[e], p.scale) : -INFINITY;
-              if (brow && kpos <= kmax) sc = __fadd_rn(sc, brow[kpos]);
-              mx = fmaxf(mx, sc);
+              const int kpos = k0 + c + e;
+              float x = (kpos <= kmax) ? __fmul_rn(sc[c + e], p.scale) : -INFINITY;
+              if (brow && kpos <= kmax) x = __fadd_rn(x, brow[kpos]);
+              sc[c + e] = x;
+              mx = fmaxf(mx, x);
             }
           }
+          lx[hf * FQ + r] = mx;
+          pair_bar();
+          mx = fmaxf(lx[r], lx[FQ + r]);
+          pair_bar();   // both halves have read lx before it is written again
           const float m_new = fmaxf(m, mx);
           const float alpha = (m == -INFINITY) ? 0.f : exp2f((m - m_new) * 1.4426950408889634f);
           // P_j may overwrite the P buffer once the previous P.V has completed
           // (within the item; the previous item's last P.V was awaited below)
           if (j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
           float sum = 0.f;
-          for (int c = 0; c < FK; c += 16) {
-            float v[16];
-            tmem_ld16(sa + c, v);
+#pragma unroll
+          for (int c = 0; c < HD; c += 16) {
             uint32_t pk[8];
 #pragma unroll
             for (int e = 0; e < 16; e += 2) {
-              const int kpos = j * FK + c + e;
-              float s0 = __fmul_rn(v[e], p.scale), s1 = __fmul_rn(v[e + 1], p.scale);
-              if (brow) {
-                if (kpos <= kmax) s0 = __fadd_rn(s0, brow[kpos]);
-                if (kpos + 1 <= kmax) s1 = __fadd_rn(s1, brow[kpos + 1]);
-              }
-              const float p0 = (kpos <= kmax && m_new != -INFINITY)
-                                   ? exp2f((s0 - m_new) * 1.4426950408889634f) : 0.f;
-              const float p1 = (kpos + 1 <= kmax && m_new != -INFINITY)
-                                   ? exp2f((s1 - m_new) * 1.4426950408889634f) : 0.f;
+              const float p0 = (m_new != -INFINITY) ? exp2f((sc[c + e] - m_new) * 1.4426950408889634f) : 0.f;
+              const float p1 = (m_new != -INFINITY) ? exp2f((sc[c + e + 1] - m_new) * 1.4426950408889634f) : 0.f;
               __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
               sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
               pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
             }
-            // row r, keys c..c+15: two 16-byte chunks in the SW128 K-major image
-            uint8_t* blk = sP + (c >> 6) * TILE_BYTES;
-            const int ch = (c & 63) >> 3;
+            // row r, keys hf*64+c..+15: two 16-byte chunks in the SW128 K-major image
+            uint8_t* blk = sP + hf * TILE_BYTES;
+            const int ch = c >> 3;
             *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
             *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
           }
@@ -305,10 +313,10 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
           // accumulate O_{j-1} (its rescale factor was alpha_prev)
           if (j >= 1) {
             const int so = (gj - 1) & 1;
-            const uint32_t oa = tmem + lane_base + 256 + so * 128;
+            const uint32_t oa = tmem + lane_base + 256 + so * 128 + hf * HD;
             tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < FD; c += 16) {
+            for (int c = 0; c < HD; c += 16) {
               float v[16];
               tmem_ld16(oa + c, v);
 #pragma unroll
@@ -324,9 +332,9 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
           const int so = (gj - 1) & 1;
           mbar_wait(&o_full[so], ((gj - 1) >> 1) & 1);
           tc_fence_after();
-          const uint32_t oa = tmem + lane_base + 256 + so * 128;
+          const uint32_t oa = tmem + lane_base + 256 + so * 128 + hf * HD;
 #pragma unroll
-          for (int c = 0; c < FD; c += 16) {
+          for (int c = 0; c < HD; c += 16) {
             float v[16];
             tmem_ld16(oa + c, v);
 #pragma unroll
@@ -338,11 +346,16 @@ __global__ void __launch_bounds__(256, 1) fmha_prefill_kernel(const __grid_const
         }
       }
       base += it.ntiles;
+      // row sum = the two halves' sums (low half + high half)
+      lx[hf * FQ + r] = l;
+      pair_bar();
+      const float lt = lx[r] + lx[FQ + r];
+      pair_bar();   // both halves have read lx before the next item writes it
       if (it.qb + r < it.len) {
-        const float inv = 1.f / l;
-        bf16* dst = p.out + (int64_t)(it.t0 + it.qb + r) * p.ldo + it.h * FD;
+        const float inv = 1.f / lt;
+        bf16* dst = p.out + (int64_t)(it.t0 + it.qb + r) * p.ldo + it.h * FD + hf * HD;
 #pragma unroll
-        for (int c = 0; c < FD; c += 8) {
+        for (int c = 0; c < HD; c += 8) {
           uint32_t pk[4];
 #pragma unroll
           for (int e = 0; e < 8; e += 2) {
@@ -389,7 +402,7 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 128);
   // persistent grid: one CTA per SM (227 KB of shared memory, 512 TMEM columns)
   const int grid = std::min(n_items, sm_count());
-  launch_pdl(fmha_prefill_kernel, dim3(grid), dim3(256), FMHA_SMEM, st, tq, tk, tv, p);
+  launch_pdl(fmha_prefill_kernel, dim3(grid), dim3(128 + 32 * SM_WARPS), FMHA_SMEM, st, tq, tk, tv, p);
   EXG_CHECK_LAUNCH();
   return true;
 }
