@@ -59,6 +59,14 @@ __device__ __forceinline__ uint64_t desc_mn_sw128(uint32_t smem_addr, uint32_t l
   return d;
 }
 
+// 2^x on the SFU (flush-to-zero: a P below 2^-126 is 0 either way once
+// rounded into the row sum)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -263,14 +271,20 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
           float sc[HD];
           float mx = -INFINITY;
 #pragma unroll
-          for (int c = 0; c < HD; c += 16) {
-            tmem_ld16(sa + c, sc + c);
+          for (int c = 0; c < HD; c += 16) tmem_ld16(sa + c, sc + c);
+          if (k0 + HD - 1 <= kmax && !brow) {      // no key of this half is masked
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              const int kpos = k0 + c + e;
-              float x = (kpos <= kmax) ? __fmul_rn(sc[c + e], p.scale) : -INFINITY;
+            for (int e = 0; e < HD; ++e) {
+              sc[e] = __fmul_rn(sc[e], p.scale);
+              mx = fmaxf(mx, sc[e]);
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < HD; ++e) {
+              const int kpos = k0 + e;
+              float x = (kpos <= kmax) ? __fmul_rn(sc[e], p.scale) : -INFINITY;
               if (brow && kpos <= kmax) x = __fadd_rn(x, brow[kpos]);
-              sc[c + e] = x;
+              sc[e] = x;
               mx = fmaxf(mx, x);
             }
           }
@@ -279,7 +293,9 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
           mx = fmaxf(lx[r], lx[FQ + r]);
           pair_bar();   // both halves have read lx before it is written again
           const float m_new = fmaxf(m, mx);
-          const float alpha = (m == -INFINITY) ? 0.f : exp2f((m - m_new) * 1.4426950408889634f);
+          const float alpha = (m == -INFINITY) ? 0.f : ex2((m - m_new) * 1.4426950408889634f);
+          // p = 2^(s log2 e - m log2 e): one FFMA + one SFU op per score
+          const float nml = (m_new == -INFINITY) ? 0.f : -m_new * 1.4426950408889634f;
           // P_j may overwrite the P buffer once the previous P.V has completed
           // (within the item; the previous item's last P.V was awaited below)
           if (j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
@@ -289,8 +305,8 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
             uint32_t pk[8];
 #pragma unroll
             for (int e = 0; e < 16; e += 2) {
-              const float p0 = (m_new != -INFINITY) ? exp2f((sc[c + e] - m_new) * 1.4426950408889634f) : 0.f;
-              const float p1 = (m_new != -INFINITY) ? exp2f((sc[c + e + 1] - m_new) * 1.4426950408889634f) : 0.f;
+              const float p0 = ex2(fmaf(sc[c + e], 1.4426950408889634f, nml));
+              const float p1 = ex2(fmaf(sc[c + e + 1], 1.4426950408889634f, nml));
               __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
               sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
               pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
