@@ -46,7 +46,8 @@ PFN_encodeTiled_t encode_fn() {
   return fn;
 }
 
-// diagnostics only (exg_diag_gemm_flags): bit 0 = skip the MMAs
+// diagnostics only (exg_diag_gemm_flags): bit 0 = skip the MMAs, bit 6 = prefill on
+// the 1-CTA kernel instead of CTA pairs
 int& gemm_debug_flags() {
   static int f = 0;
   return f;
@@ -700,6 +701,256 @@ void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wb
   }
 }
 
+// ============================================================================
+// Prefill GEMM on CTA pairs (tcgen05 cta_group::2).  A cluster of two CTAs on
+// one TPC computes a 256-token x 256-feature tile with one M=256 N=256 MMA
+// per 16-wide K step issued by the leader CTA: each CTA stages its own 128
+// tokens of A and its own 128 features of W per 64-wide k-block (32 KB per
+// stage instead of the 48 KB a 1-CTA 128x256 tile needs, so the per-SM L2 ->
+// shared-memory stream drops by a third), and each holds its 128 rows x 256
+// columns of the fp32 accumulator in its own TMEM (double-buffered, 512
+// columns).  Both CTAs' TMA loads complete on the leader's `full` barrier; the
+// leader's commits arrive on both CTAs' `empty` / `tfull` barriers
+// (multicast); both CTAs' epilogue warps release a TMEM buffer on the
+// leader's `tempty`.  Weights stream as verbatim 16 KB blocks of the blocked
+// layout (a 2-D TMA box of 128 rows x 128 B, no swizzle: the block already
+// is the SWIZZLE_128B shared-memory image).  Per output element the K loop,
+// MMA K steps and epilogue are those of the 1-CTA kernel.
+// ============================================================================
+constexpr int P2_STAGES = 6;
+// shared::cluster address of this shared variable's copy in the leader CTA (rank 0)
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(smem_u32(p)));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* smem_dst, const CUtensorMap* tmap, uint64_t* bar, int32_t c0,
+                                                 int32_t c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(leader_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this offset in both CTAs once the issued MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(leader_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  const long long t0 = clock64();
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (clock64() - t0 > 8000000000LL) {
+      printf("exg: pair mbarrier wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<0>::THREADS, 1)
+    gemm_pair_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmW, int M, int N,
+                     int nkb, int tiles_m, int tiles_n, int gm_group, EpiParams ep) {
+  constexpr int EPI_WARPS = EpiCfg<0>::WARPS;
+  constexpr int TN = 256;                     // features per pair tile (= tokens per pair tile)
+  constexpr int HALF = 16384;                 // one CTA's A or B share of a k-block
+  constexpr uint32_t TMEM_COLS = 512;
+  griddep_launch_dependents();
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + P2_STAGES * HALF;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + P2_STAGES * HALF);
+  uint64_t* empty = full + P2_STAGES;
+  uint64_t* tfull = empty + P2_STAGES;   // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t rank = cluster_rank();
+  const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmX);
+    prefetch_tmap(&tmW);
+    for (int s = 0; s < P2_STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 2 * EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync_all();   // barriers initialised and TMEM allocated in both CTAs
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  const int tiles = tiles_m * tiles_n;
+  auto tile_mn = [&](int t, int& m, int& n) {
+    // grouped raster: gm_group m-tiles (an L2-resident slab of A) sweep all n-tiles
+    const int per_group = gm_group * tiles_n;
+    const int g = t / per_group, within = t % per_group;
+    const int gm_count = min(gm_group, tiles_m - g * gm_group);
+    m = g * gm_group + within % gm_count;
+    n = within / gm_count;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      griddep_wait();   // activations are the previous kernel's output
+      uint32_t g = 0;
+      for (int t = cid; t < tiles; t += ncl) {
+        int m, n;
+        tile_mn(t, m, n);
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const uint32_t s = g % P2_STAGES;
+          const uint32_t ph = (g / P2_STAGES) & 1;
+          if (g >= P2_STAGES) mbar_wait(&empty[s], ph ^ 1);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 4 * HALF);
+          tma_load_2d_pair(sA + s * HALF, &tmX, &full[s], kb * BK, m * TN + (int)rank * BM);
+          tma_load_2d_pair(sB + s * HALF, &tmW, &full[s], 0, ((n * 2 + (int)rank) * nkb + kb) * BM);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(2 * BM, TN);
+      uint32_t g = 0, ui = 0;
+      for (int t = cid; t < tiles; t += ncl, ++ui) {
+        const uint32_t a = ui & 1;
+        if (ui >= 2) mbar_wait_cluster(&tempty[a], ((ui >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + a * TN;
+        for (int kb = 0; kb < nkb; ++kb, ++g) {
+          const uint32_t s = g % P2_STAGES;
+          mbar_wait(&full[s], (g / P2_STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * HALF), b_base = smem_u32(sB + s * HALF);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(d, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                           (kb || k) ? 1u : 0u);
+          umma_commit_pair(&empty[s]);
+        }
+        umma_commit_pair(&tfull[a]);
+      }
+    }
+  } else if (warp >= 4) {
+    // warp w reads TMEM lanes 32*(w%4).. and one half of the 256 columns
+    const int q = warp & 3;
+    const int part = (warp - 4) >> 2;
+    const int c_lo = part * (TN / 2), c_hi = c_lo + TN / 2;
+    griddep_wait();   // outputs / residual may still be in use by the previous kernel
+    const int r = q * 32 + lane;
+    uint32_t ui = 0;
+    for (int t = cid; t < tiles; t += ncl, ++ui) {
+      int m, n;
+      tile_mn(t, m, n);
+      const uint32_t a = ui & 1;
+      mbar_wait(&tfull[a], (ui >> 1) & 1);
+      tc_fence_after();
+      const int gm = m * TN + (int)rank * BM + r;
+      const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * TN;
+      for (int c = c_lo; c < c_hi; c += 16) {
+        float v[16];
+        tmem_ld16(taddr + c, v);
+        if (gm < M && n * TN + c < N) epi_store_row16(ep, gm, n * TN + c, N, v);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_leader(&tempty[a]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();   // both CTAs done with TMEM and with each other's shared memory
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
+}
+
+constexpr size_t P2_SMEM = 1024 + (size_t)P2_STAGES * 2 * 16384 + (2 * P2_STAGES + 4) * 8 + 16;
+
+// weights (blocked layout) as a 2-D tensor of 128-byte rows: block (nb, kb) is
+// rows [(nb*nkb + kb)*128, +128), copied verbatim (no swizzle)
+CUtensorMap make_tmap_blocked(const bf16* Wb, int64_t n_wblk, int64_t nkb) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {(cuuint64_t)BK, (cuuint64_t)(n_wblk * nkb * BM)};
+  cuuint64_t strides[1] = {(cuuint64_t)BK * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)BM};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<bf16*>(Wb), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (blocked weights) failed " + std::to_string((int)r));
+  return m;
+}
+
+void launch_pair(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wblk, const EpiParams& ep,
+                 cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    EXG_CUDA(cudaFuncSetAttribute(gemm_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P2_SMEM));
+    attr_set = true;
+  }
+  const int nkb = (K + BK - 1) / BK;
+  const int tiles_m = (M + 255) / 256, tiles_n = (N + 255) / 256;
+  const int gm = (int)std::max<int64_t>(1, std::min<int64_t>(tiles_m, (gemm_slab_mb() << 20) / ((int64_t)256 * K * 2)));
+  const int clusters = std::min(num_sms() / 2, tiles_m * tiles_n);
+  const CUtensorMap tw = make_tmap_blocked(Wb, n_wblk, nkb);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(2 * clusters);
+  cfg.blockDim = dim3(EpiCfg<0>::THREADS);
+  cfg.dynamicSmemBytes = P2_SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  EXG_CUDA(cudaLaunchKernelEx(&cfg, gemm_pair_kernel, tx, tw, M, N, nkb, tiles_m, tiles_n, gm, ep));
+  EXG_CHECK_LAUNCH();
+}
+
 __global__ void pack_blocked_kernel(bf16* __restrict__ dst, const bf16* __restrict__ src, int64_t rows, int64_t K,
                                     int64_t ld) {
   const int64_t rp = (rows + 127) / 128 * 128, kp = (K + 63) / 64 * 64;
@@ -765,6 +1016,12 @@ void linear(const LinearArgs& a, cudaStream_t st) {
   } else {
     const int BN = a.bn ? a.bn : (features > 128 ? 256 : (features > 64 ? 128 : 64));
     const CUtensorMap tx = make_tmap_bf16(a.X, tokens, a.K, a.ldx, BM);
+    // CTA pairs (cta_group::2) for the wide prefill GEMMs; diagnostics flag
+    // bit 6 forces the 1-CTA kernel
+    if (BN == 256 && !(gemm_debug_flags() & 64)) {
+      launch_pair(tx, a.Wb, tokens, features, a.K, n_wblk, a.ep, st);
+      return;
+    }
     switch (BN) {
       case 64: launch<64, 0>(tx, a.Wb, tokens, features, a.K, n_wblk, a.ep, nullptr, 0, st); break;
       case 128: launch<128, 0>(tx, a.Wb, tokens, features, a.K, n_wblk, a.ep, nullptr, 0, st); break;

@@ -52,6 +52,52 @@ def gemm(tokens, features, K, decode, mode=0):
           ("dec" if decode else "pre", tokens, features, K, split, t * 1e6, flops / t / 1e12, byts / t / 1e9))
 
 
+def pgemm_ab(tokens, features, K, mode=0, reps_sus=0):
+    """Prefill GEMM: CTA-pair kernel vs the 1-CTA kernel (diagnostics flag
+    bit 6): time both, and compare their outputs bit for bit."""
+    X = torch.randn(tokens, K, device=dev).to(torch.bfloat16)
+    W0 = (torch.randn(features, K, device=dev) * 0.02).to(torch.bfloat16)
+    W = torch.empty(int(L.lib().exg_op_blocked_elems(features, K)), dtype=torch.bfloat16, device=dev)
+    L.check(L.lib().exg_op_pack_weight(W.data_ptr(), W0.data_ptr(), features, K, K, st()))
+    bias = (torch.randn(features, device=dev) * 0.1).to(torch.bfloat16)
+    outs = {}
+    for flag in (64, 0):
+        L.lib().exg_diag_gemm_flags(flag)
+        out = torch.zeros(tokens, features, device=dev, dtype=torch.float32 if mode in (2, 3) else torch.bfloat16)
+        resid = out.data_ptr() if mode == 2 else None
+
+        def fn():
+            L.check(L.lib().exg_op_linear(X.data_ptr(), K, W.data_ptr(), tokens, features, K, mode, 1,
+                                          bias.data_ptr(), out.data_ptr(), features, resid, features, 0, None, 0,
+                                          st()))
+        if mode == 2:
+            out.zero_()
+        fn()
+        torch.cuda.synchronize()
+        outs[flag] = out.clone()
+        t = timeit(fn)
+        flops = 2.0 * tokens * features * K
+        line = "pgemm %s T=%5d N=%5d K=%5d mode %d: %8.1f us %7.1f TFLOP/s" % (
+            "1cta" if flag else "pair", tokens, features, K, mode, t * 1e6, flops / t / 1e12)
+        if reps_sus:
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps_sus):
+                fn()
+            b.record()
+            torch.cuda.synchronize()
+            ts = a.elapsed_time(b) * 1e-3 / reps_sus
+            line += "  sustained x%d: %8.1f us %7.1f TFLOP/s" % (reps_sus, ts * 1e6, flops / ts / 1e12)
+        print(line, flush=True)
+    L.lib().exg_diag_gemm_flags(0)
+    if mode == 2:
+        print("   (resid mode: accumulated over different rep counts, not compared)")
+    else:
+        same = torch.equal(outs[0], outs[64])
+        print("   pair == 1cta bitwise:", same, " max |diff|", float((outs[0].float() - outs[64].float()).abs().max()))
+
+
 def dattn(B, c, H=40, dh=128, split_len=512):
     max_ctx = ((c + 63) // 64) * 64
     kc = torch.randn(B, H, max_ctx, dh, device=dev).to(torch.bfloat16)
@@ -211,6 +257,16 @@ if __name__ == "__main__":
             for B in (16, 56, 79, 256):
                 dattn_mix(B, 512)
         L.lib().exg_diag_decode_stages(0)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "pgemm":
+        d, ff = 5120, 20480
+        for T in (12544, 8192, 300):
+            pgemm_ab(T, 3 * d, d, 0, 200 if T == 12544 else 0)
+            pgemm_ab(T, d, d, 0)
+            pgemm_ab(T, ff, d, 1 if False else 0, 100 if T == 12544 else 0)
+            pgemm_ab(T, d, ff, 0)
+        pgemm_ab(1000, 300, 512, 0)
+        pgemm_ab(777, 1024, 5120, 2)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pmix":
         for R in (8, 32, 52, 64):
