@@ -635,10 +635,14 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
   if (rest) {
     layernorm(h_, d, x_, d, w.ln1_g, w.ln1_b, B, d, 1e-5f, st_);
     linear_dec(h_, d, B, w.Wqkv, 3 * il, d, epi_bf16(w.bqkv, qkv_, 3 * il));
-    kv_scatter(kc(l), vc(l), qkv_, db.slot, db.pos, B, D.Hl, D.dh, slot_ctx_, st_);
   }
   if (attn) {
+    // K7 fused: the attention kernel appends the new token's K / V (from the
+    // qkv buffer) to the cache at position n_keys - 1
     DecodeAttnArgs da;
+    da.knew = qkv_ + il;
+    da.vnew = qkv_ + 2 * il;
+    da.ldnew = 3 * il;
     da.q = qkv_;
     da.ldq = 3 * il;
     da.kc = kc(l);
@@ -657,7 +661,8 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
     da.partial = attn_part_;
     const int k = kbegin();
     decode_attention(da, st_);
-    kend(k, EXG_K_DECODE_ATTN, db.sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)B * D.Hl * D.dh * 2.0 * 2.0);
+    kend(k, EXG_K_DECODE_ATTN, db.sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)B * D.Hl * D.dh * 2.0 * 2.0 +
+                                   (double)B * 2.0 * D.Hl * D.dh * 2.0);
   }
   if (part == 1) return;
   if (rest) {
@@ -770,8 +775,13 @@ void Engine::cross_kv(int l, const EncodeBatch& eb) {
 }
 
 void Engine::dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, int ctx, const DecodeBatch& db,
-                   const int32_t* nkeys, int max_keys, double sum_keys, const float* bias) {
+                   const int32_t* nkeys, int max_keys, double sum_keys, const float* bias, bool append) {
   DecodeAttnArgs da;
+  if (append) {   // fused KV append of the new token (K7): K / V follow q in the qkv buffer
+    da.knew = q + D.inner_l;
+    da.vnew = q + 2 * D.inner_l;
+    da.ldnew = ldq;
+  }
   da.q = q;
   da.ldq = ldq;
   da.kc = kc;
@@ -793,7 +803,8 @@ void Engine::dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, i
   da.bias_off = bias_off_;
   const int k = kbegin();
   decode_attention(da, st_);
-  kend(k, EXG_K_DECODE_ATTN, sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)db.B * D.Hl * D.dh * 2.0 * 2.0);
+  kend(k, EXG_K_DECODE_ATTN, sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)db.B * D.Hl * D.dh * 2.0 * 2.0 +
+                                (append ? (double)db.B * 2.0 * D.Hl * D.dh * 2.0 : 0.0));
 }
 
 void Engine::dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest) {
@@ -802,9 +813,9 @@ void Engine::dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest) {
   if (rest) {
     rmsnorm(h_, d, x_, d, w.ln1_g, B, d, T5_EPS, 1.f, st_);
     linear_dec(h_, d, B, w.Wqkv, 3 * il, d, epi_bf16(nullptr, qkv_, 3 * il));
-    kv_scatter(kc(l), vc(l), qkv_, db.slot, db.pos, B, D.Hl, D.dh, slot_ctx_, st_);
   }
-  if (attn) dattn(qkv_, 3 * il, kc(l), vc(l), slot_ctx_, db, db.nkeys, db.max_keys, db.sum_keys, dec_bias_);
+  // the self-attention appends the new token's K / V to the cache itself
+  if (attn) dattn(qkv_, 3 * il, kc(l), vc(l), slot_ctx_, db, db.nkeys, db.max_keys, db.sum_keys, dec_bias_, true);
   if (rest) {
     resid_update(true, ctx_, il, B, w.Wo, il, nullptr);
     rmsnorm(h_, d, x_, d, w.lnx_g, B, d, T5_EPS, 1.f, st_);

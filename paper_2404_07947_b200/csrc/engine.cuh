@@ -169,7 +169,7 @@ class Engine {
   void enc_layer_t5(int l, const EncodeBatch& eb, bool attn, bool rest);
   void dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest);
   void dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, int ctx, const DecodeBatch& db,
-             const int32_t* nkeys, int max_keys, double sum_keys, const float* bias);
+             const int32_t* nkeys, int max_keys, double sum_keys, const float* bias, bool append = false);
   void linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   void linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   // residual update x += W.act + b: fused epilogue (tp = 1) or partial ->

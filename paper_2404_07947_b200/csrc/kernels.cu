@@ -325,6 +325,18 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
     fence_barrier_init();
   }
   if (tid < DH) qs[tid] = bf2f(a.q[(int64_t)i * a.ldq + h * DH + tid]);
+  // fused KV append: this split holds the new key nk-1 -> write its K / V row
+  // to the cache, and patch it into its shared-memory tile after the bulk copy
+  // of that tile (which may carry the stale cache row) has landed
+  const int r_new = nk - 1 - k_begin;
+  const bool app = a.knew != nullptr && r_new < n;
+  int4 new_chunk = make_int4(0, 0, 0, 0);
+  if (app && tid < 2 * C::CH) {
+    const int which = tid / C::CH, c = tid % C::CH;
+    new_chunk = *reinterpret_cast<const int4*>((which ? a.vnew : a.knew) + (int64_t)i * a.ldnew + h * DH + c * 8);
+    bf16* dst = const_cast<bf16*>(which ? vbase : kbase) + (int64_t)r_new * DH + c * 8;
+    *reinterpret_cast<int4*>(dst) = new_chunk;
+  }
   __syncthreads();
 
   auto issue = [&](int t) {
@@ -359,6 +371,15 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
   for (int t = 0; t < ntiles; ++t) {
     const int s = t % C::STAGES;
     mbar_wait(&bar[s], (t / C::STAGES) & 1);
+    if (app && t == r_new / C::KT) {   // CTA-uniform
+      if (tid < 2 * C::CH) {
+        const int which = tid / C::CH, c = tid % C::CH;
+        uint8_t* row = (which ? sv : sk) + s * C::KT * C::ROWB + (r_new % C::KT) * C::ROWB;
+        *reinterpret_cast<int4*>(row + c * 16) = new_chunk;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before the stage is refilled by a bulk copy
+      }
+      __syncthreads();
+    }
     const int nkt = min(C::KT, n - t * C::KT);
     const uint8_t* krow = sk + s * C::KT * C::ROWB;
     const uint8_t* vrow = sv + s * C::KT * C::ROWB;

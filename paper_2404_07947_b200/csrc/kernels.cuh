@@ -74,6 +74,13 @@ struct DecodeAttnArgs {
   // key k of row i, head h gets bias[h * bias_ld + bias_off + k - (n_keys[i]-1)]
   const float* bias = nullptr;
   int bias_ld = 0, bias_off = 0;
+  // optional fused KV append (K7): the new token of row i -- key n_keys[i]-1
+  // -- is read from knew / vnew [B][ldnew] (head h at h * dh) instead of the
+  // cache, and written to the cache at that position by the CTA whose split
+  // holds it (the cache need not contain it before the launch)
+  const bf16* knew = nullptr;
+  const bf16* vnew = nullptr;
+  int64_t ldnew = 0;
 };
 void decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
 

@@ -101,6 +101,42 @@ def test_linear_strided_operands(L):
         assert np.all(out.cpu().numpy()[:, features:] == 0)
 
 
+@pytest.mark.parametrize("tokens,features,K", [(300, 300, 320), (777, 1024, 5120), (256, 512, 64), (1, 260, 128),
+                                               (513, 2560, 960)])
+def test_prefill_pair_kernel_matches_single_cta(L, tokens, features, K):
+    """The CTA-pair prefill GEMM (cta_group::2, M=256 tiles) computes every
+    output element with the same K order and MMA K steps as the 1-CTA kernel
+    (diagnostics flag bit 6): outputs are bit-identical, ragged token and
+    feature tails included, in every epilogue mode."""
+    rng = np.random.default_rng(tokens + features + K)
+    tX = bf16_tensor(bf16_round_np(rng.standard_normal((tokens, K)) * 0.5))
+    tWb = blocked(L, bf16_tensor(bf16_round_np(rng.standard_normal((features, K)) * 0.05)))
+    tb = bf16_tensor(bf16_round_np(rng.standard_normal(features) * 0.1))
+    r0 = torch.from_numpy(rng.standard_normal((tokens, features)).astype(np.float32)).to(dev())
+    try:
+        for mode, act in ((0, 0), (1, 1), (1, 2), (2, 0), (3, 0)):
+            outs = []
+            for flag in (0, 64):
+                L.lib().exg_diag_gemm_flags(flag)
+                if mode in (0, 1):
+                    out = torch.zeros((tokens, features), dtype=torch.bfloat16, device=dev())
+                    _run(L, "exg_op_linear", ptr(tX), K, ptr(tWb), tokens, features, K, mode, act, ptr(tb), ptr(out),
+                         features, None, 0, 0, None, 0, stream())
+                elif mode == 2:
+                    out = r0.clone()
+                    _run(L, "exg_op_linear", ptr(tX), K, ptr(tWb), tokens, features, K, 2, 0, ptr(tb), None, 0,
+                         ptr(out), features, 0, None, 0, stream())
+                else:
+                    out = torch.zeros((tokens, features), dtype=torch.float32, device=dev())
+                    _run(L, "exg_op_linear", ptr(tX), K, ptr(tWb), tokens, features, K, 3, 0, ptr(tb), ptr(out),
+                         features, None, 0, 0, None, 0, stream())
+                torch.cuda.synchronize()
+                outs.append(out)
+            assert torch.equal(outs[0], outs[1]), (mode, act)
+    finally:
+        L.lib().exg_diag_gemm_flags(0)
+
+
 def test_decode_gemm_batch_invariant(L):
     """T13: a token row's decode-GEMM bits do not depend on its batch-mates
     or its row position (tokens ride the MMA N axis)."""
