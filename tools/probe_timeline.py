@@ -13,6 +13,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2404_07947_b200 import _lib as L  # noqa: E402
+L.LIB_PATH = os.environ.get("EXG_PROBE_LIB", L.LIB_PATH)   # A/B against another build
 
 dev = torch.device("cuda:0")
 st = lambda: torch.cuda.current_stream().cuda_stream
