@@ -527,6 +527,18 @@ def main():
         base = in_runner_baselines(args, X, ctx, prof, cl, pin, pout, d, bounds, scheds,
                                    reqs[:args.baseline_requests], slot_ctx, sla)
 
+    def memory_gb(prof_, cl_, sch):
+        """Per-GPU model / KV-cache GB of a schedule (exg_schedule_memory;
+        the memory-overhead accounting of PAPER.md:548-560)."""
+        w, kv = X.schedule_memory(prof_, ctx.mspec, cl_, pin, pout, sch)
+        return {"model_gb": [round(x / 1e9, 2) for x in w], "kv_gb": [round(x / 1e9, 2) for x in kv]}
+
+    memory = {"headline_rra": memory_gb(prof, cl, sched)}
+    if base:
+        for name, row in base.items():
+            if "schedule" in row.get("ft_static", {}):
+                memory["ft_static_" + name] = memory_gb(prof, cl, X.static_schedule(row["ft_static"]["schedule"]["b_e"]))
+
     # the scheduler's multi-GPU plan for this workload and bound (predicted by
     # the XSimulator on the measured per-GPU tables + the modeled interconnect)
     plan = {}
@@ -536,7 +548,7 @@ def main():
             s_n, e_n = X.schedule_find(prof, ctx.mspec, cl_n, pin, pout, d.target_len, L_head * (1 - args.margin),
                                        X.EXG_RRA | X.EXG_WAA_C, X.search_opts(b_e_max=B_E_MAX, little=args.little))
             plan[str(n)] = {"predicted_tok_s": e_n.thrput_tok_s, "predicted_latency_s": e_n.latency_s,
-                            "schedule": s_n.as_dict()}
+                            "schedule": s_n.as_dict(), "memory": memory_gb(prof, cl_n, s_n)}
         except X.ExgError as e:
             plan[str(n)] = {"infeasible": str(e)}
 
@@ -601,6 +613,7 @@ def main():
                                (COMM_ALPHA_S * 1e6, COMM_BW / 1e9), "predicted": plan},
             "workload_variance": workload_variance(var_st),
             "dyn_adjust": dyn,
+            "memory": memory,
             "in_runner_baselines": base and {"requests": min(args.baseline_requests, args.requests),
                                              "rule": "same kernels / requests / bounds; FT static = best "
                                                      "simulated static batch within the bound (PAPER.md:112), "

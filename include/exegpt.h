@@ -228,6 +228,16 @@ void exg_profile_free(exg_profile* p);
 exg_status exg_simulate(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
                         const exg_pmf* in, const exg_pmf* out_len, int32_t target_len, const exg_schedule* sched,
                         exg_estimate* est);
+/* Memory-overhead accounting: the model bytes and KV-cache
+ * bytes each GPU of the schedule's layout holds under the simulator's memory
+ * model (weight shard + embeddings on the first / last stage of each side;
+ * KV slots sized at max_in + max_out rows per decode row -- B_D for RRA / WAA
+ * decoder stages, B for EXG_STATIC -- and max_in per encode row on WAA
+ * encoder stages).  weight_bytes / kv_bytes: caller-owned double
+ * [cluster->n_gpus]; GPUs outside the layout get 0.  Pure host. */
+exg_status exg_schedule_memory(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                               const exg_pmf* in, const exg_pmf* out_len, const exg_schedule* sched,
+                               double* weight_bytes, double* kv_bytes);
 /* Resolve derived fields (B_D, B_m, stage layout) of a schedule given by its
  * control variables (strategy, b_e, n_d | b_m-count, tp_degree, tp_gpus). */
 exg_status exg_schedule_resolve(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,

@@ -194,7 +194,7 @@ class SimCluster:
     workspace_bytes: float = 0.0
 
 
-RRA, WAA_C, WAA_M = 1, 2, 4
+RRA, WAA_C, WAA_M, STATIC = 1, 2, 4, 8
 
 
 @dataclass
@@ -353,6 +353,35 @@ class Simulator:
 
     def kv_bytes_per_token_layer(self) -> float:
         return 2.0 * self.m.inner * 2.0
+
+    def memory(self, s: Schedule):
+        """Per-GPU (model bytes, KV-cache bytes) of a schedule under the
+        memory model of mem_ok (weight shard, embeddings on the first / last
+        stage of each side, KV slots at kv_rows x ctx for the stage's layers):
+        the memory-overhead accounting of PAPER.md:548-560 (WAA holds more
+        model copies and less KV than RRA / FT).  Lists of length n_gpus."""
+        w = [0.0] * self.cl.n_gpus
+        kv = [0.0] * self.cl.n_gpus
+
+        def account(stages, rows, ctx):
+            P = len(stages)
+            for k, (g0, ng, l0, l1) in enumerate(stages):
+                b = (l1 - l0) * self.layer_bytes() / ng
+                if k == 0 or k == P - 1:
+                    b += self.emb_bytes()
+                c = rows * ctx * (l1 - l0) * self.kv_bytes_per_token_layer() / ng
+                for g in range(g0, min(g0 + ng, self.cl.n_gpus)):
+                    w[g] += b
+                    kv[g] += c
+
+        if s.strategy == STATIC:
+            account(stage_layout(self.cl.n_gpus, 1, 0, self.n_layers), s.b_e, self.max_in + self.max_out)
+        elif s.strategy == RRA:
+            account(s.stages, s.b_d, self.max_in + self.max_out)
+        else:
+            account([st for st in s.stages if st[0] < s.n_enc_gpus], s.b_e, self.max_in)
+            account([st for st in s.stages if st[0] >= s.n_enc_gpus], s.b_d, self.max_in + self.max_out)
+        return w, kv
 
     def mem_ok(self, stages, kv_rows: int, ctx: int) -> bool:
         P = len(stages)

@@ -6,8 +6,8 @@ step of the hot path runs in the library's CUDA kernels.
 """
 from ._lib import (EXG_RRA, EXG_STATIC, EXG_WAA_C, EXG_WAA_M, Context, ExgError, Pmf, Profile, cluster_spec, lib,
                    local_group, model_spec, nccl_loopback, rra_schedule, run_group, schedule_find,
-                   schedule_resolve, search_opts, simulate, static_schedule, unique_id)
+                   schedule_memory, schedule_resolve, search_opts, simulate, static_schedule, unique_id)
 
 __all__ = ["EXG_RRA", "EXG_STATIC", "EXG_WAA_C", "EXG_WAA_M", "Context", "ExgError", "Pmf", "Profile", "cluster_spec", "lib",
-           "local_group", "model_spec", "nccl_loopback", "rra_schedule", "run_group", "schedule_find", "schedule_resolve",
+           "local_group", "model_spec", "nccl_loopback", "rra_schedule", "run_group", "schedule_find", "schedule_memory", "schedule_resolve",
            "search_opts", "simulate", "static_schedule", "unique_id"]

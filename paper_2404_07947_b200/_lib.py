@@ -130,6 +130,9 @@ _SIGS = {
     "exg_profile_comm_model": (C.c_int, [_P, C.c_double, C.c_double]),
     "exg_simulate": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
                                C.POINTER(exg_pmf), C.c_int32, C.POINTER(exg_schedule), C.POINTER(exg_estimate)]),
+    "exg_schedule_memory": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
+                                      C.POINTER(exg_pmf), C.POINTER(exg_schedule), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_double)]),
     "exg_schedule_resolve": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec),
                                        C.POINTER(exg_pmf), C.POINTER(exg_pmf), C.c_int32, C.POINTER(exg_schedule)]),
     "exg_schedule_find": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
@@ -402,6 +405,16 @@ def simulate(prof: Profile, mspec: exg_model_spec, cl: exg_cluster_spec, pin: Pm
     check(lib().exg_simulate(prof.h, C.byref(mspec), C.byref(cl), C.byref(pin.c), C.byref(pout.c), target_len,
                              C.byref(sched), C.byref(est)))
     return est
+
+
+def schedule_memory(prof: Profile, mspec, cl, pin: Pmf, pout: Pmf, sched: exg_schedule):
+    """Per-GPU (model bytes, KV-cache bytes) lists of a schedule
+    (exg_schedule_memory, PAPER.md:548-560)."""
+    n = int(cl.n_gpus)
+    w, kv = (C.c_double * n)(), (C.c_double * n)()
+    check(lib().exg_schedule_memory(prof.h, C.byref(mspec), C.byref(cl), C.byref(pin.c), C.byref(pout.c),
+                                    C.byref(sched), w, kv))
+    return list(w), list(kv)
 
 
 def schedule_resolve(prof: Profile, mspec, cl, pin: Pmf, pout: Pmf, sched: exg_schedule, m_count: int = 1):

@@ -306,6 +306,31 @@ exg_status exg_simulate(const exg_profile* p, const exg_model_spec* spec, const 
   });
 }
 
+exg_status exg_schedule_memory(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
+                               const exg_pmf* in, const exg_pmf* out_len, const exg_schedule* sched,
+                               double* weight_bytes, double* kv_bytes) {
+  return guarded([&] {
+    if (!p || !cluster || !sched || !weight_bytes || !kv_bytes) throw std::invalid_argument("null argument");
+    check_spec(spec);
+    exg::plan::Simulator S(p->p, *spec, *cluster, pmf_vec(in), pmf_vec(out_len), 1, false);
+    exg::plan::Sched s;
+    if (sched->strategy == EXG_STATIC) {
+      if (sched->b_e < 1) throw std::invalid_argument("static batch b_e < 1");
+      s.strategy = EXG_STATIC;
+      s.b_e = sched->b_e;
+    } else {
+      s = from_c(sched);
+    }
+    std::vector<double> w, kv;
+    S.memory(s, w, kv);
+    for (int g = 0; g < cluster->n_gpus; ++g) {
+      weight_bytes[g] = w[g];
+      kv_bytes[g] = kv[g];
+    }
+    return EXG_OK;
+  });
+}
+
 exg_status exg_schedule_resolve(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
                                 const exg_pmf* in, const exg_pmf* out_len, int32_t m_count, exg_schedule* sched) {
   return guarded([&] {

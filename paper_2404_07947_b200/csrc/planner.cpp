@@ -340,6 +340,41 @@ bool Simulator::mem_ok(const std::vector<Stage>& st, int64_t kv_rows, int64_t ct
   return true;
 }
 
+// Memory-overhead accounting: the weight shard (+ the
+// embeddings on the first / last stage of each side) and the KV slots
+// (kv_rows x ctx for the stage's layers) each GPU holds -- mem_ok's model,
+// summed per GPU.  RRA / STATIC: B_D (B) rows of max_in + max_out; WAA:
+// encoder stages B_E rows of max_in, decoder stages B_D rows of max_in +
+// max_out.
+void Simulator::memory(const Sched& s, std::vector<double>& w, std::vector<double>& kv) {
+  w.assign(cl.n_gpus, 0.0);
+  kv.assign(cl.n_gpus, 0.0);
+  auto account = [&](const std::vector<Stage>& st, int64_t rows, int64_t ctx) {
+    const int P = (int)st.size();
+    for (int k = 0; k < P; ++k) {
+      const Stage& g = st[k];
+      const int64_t nl = g.layer_end - g.layer_begin;
+      double b = nl * layer_bytes() / g.n_gpus;
+      if (k == 0 || k == P - 1) b += emb_bytes();
+      const double c = (double)(rows * ctx * nl) * kv_bytes_per_token_layer() / g.n_gpus;
+      for (int i = g.first_gpu; i < std::min(g.first_gpu + g.n_gpus, cl.n_gpus); ++i) {
+        w[i] += b;
+        kv[i] += c;
+      }
+    }
+  };
+  if (s.strategy == EXG_STATIC) {
+    account(stage_layout(cl.n_gpus, 1, 0, n_layers, 0), s.b_e, (int64_t)max_in + max_out);
+  } else if (s.strategy == EXG_RRA) {
+    account(s.stages, s.b_d, (int64_t)max_in + max_out);
+  } else {
+    std::vector<Stage> enc, dec;
+    for (const Stage& st : s.stages) (st.first_gpu < s.n_enc_gpus ? enc : dec).push_back(st);
+    account(enc, s.b_e, max_in);
+    account(dec, s.b_d, (int64_t)max_in + max_out);
+  }
+}
+
 Sched Simulator::rra_schedule(int b_e, int n_d, int t, int c) {
   Sched s;
   s.strategy = EXG_RRA;

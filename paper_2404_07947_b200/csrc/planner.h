@@ -80,6 +80,8 @@ class Simulator {
   double layer_dec(int t, double b);
   std::vector<double> stage_times(const std::vector<Stage>& st, bool enc, double b);
   bool mem_ok(const std::vector<Stage>& st, int64_t kv_rows, int64_t ctx);
+  // per-GPU model / KV-cache bytes of a schedule (mem_ok's memory model)
+  void memory(const Sched& s, std::vector<double>& w, std::vector<double>& kv);
 
   const Profile& p;
   exg_model_spec m;

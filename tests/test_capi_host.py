@@ -246,3 +246,60 @@ def test_in_runner_baseline_picks(L, tmp_path):
         orca += 1
     assert orca >= 1
     assert bench.static_pick(L, P, mspec, ccl, pin, pout, d.target_len, 1e-9) is None
+
+
+@pytest.mark.parametrize("n_gpus,t,c", [(1, 1, 0), (4, 1, 0), (8, 2, 4), (8, 4, 8)])
+def test_schedule_memory(L, tmp_path, n_gpus, t, c):
+    """Memory-overhead accounting: C++ bit-identical to
+    the oracle; pinned to closed forms -- summed over GPUs the model bytes
+    are L x layer (x 2 for WAA's two sides) + the embeddings on every GPU of
+    the first / last stage and the KV bytes are rows x ctx x L x (2 H dh 2 B); a
+    schedule is memory-feasible exactly when every GPU's model + KV +
+    workspace fits (mem_ok).  Embeddings are replicated on each GPU of a
+    TP end stage."""
+    from oracle import simulator as sim
+    spec, m, prof, d, cl = _setup("G", "opt-66b", n_gpus)
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    S = sim.Simulator(prof, m, cl, d.pmf_in, d.pmf_out, d.target_len)
+    kvb = 2 * spec.n_heads * spec.d_head * 2
+    Lyr = S.n_layers
+    cases = []
+    for b_e, n_d in [(8, 10), (3, 480)]:
+        s_o = S.rra_schedule(b_e, n_d, t, c)
+        s_c = L.rra_schedule(b_e, 0, n_d)
+        s_c.tp_degree, s_c.tp_gpus = t, c
+        L.schedule_resolve(P, mspec, ccl, pin, pout, s_c)
+        cases.append((s_o, s_c, s_o.b_d, S.max_in + S.max_out, None))
+    if n_gpus > 1:
+        for b_e, M in [(4, 3), (8, 8)]:
+            s_o = S.waa_schedule(b_e, M, 1, 0)
+            s_c = L.exg_schedule()
+            s_c.strategy, s_c.b_e = 2, b_e
+            L.schedule_resolve(P, mspec, ccl, pin, pout, s_c, M)
+            cases.append((s_o, s_c, None, None, s_o))
+    st_c = L.static_schedule(16)
+    st_o = sim.Schedule(sim.STATIC, 16, 16, 0, 0, 1, 0, 0, [])
+    cases.append((st_o, st_c, 16, S.max_in + S.max_out, None))
+    for s_o, s_c, rows, ctx, waa in cases:
+        w_o, kv_o = S.memory(s_o)
+        w_c, kv_c = L.schedule_memory(P, mspec, ccl, pin, pout, s_c)
+        assert (w_c, kv_c) == (w_o, kv_o)
+        stages = s_o.stages if s_o.strategy != sim.STATIC else sim.stage_layout(n_gpus, 1, 0, Lyr)
+        def end_gpus(side):   # the embeddings sit, replicated, on every GPU of a side's first / last stage
+            return side[0][1] if len(side) == 1 else side[0][1] + side[-1][1]
+
+        if waa is None:
+            ends = end_gpus(stages)
+            assert sum(w_o) == pytest.approx(Lyr * S.layer_bytes() + ends * S.emb_bytes(), rel=1e-12)
+            assert sum(kv_o) == pytest.approx(rows * ctx * Lyr * kvb, rel=1e-12)
+            ok = S.mem_ok(stages, rows, ctx)
+        else:
+            enc = [x for x in waa.stages if x[0] < waa.n_enc_gpus]
+            dec = [x for x in waa.stages if x[0] >= waa.n_enc_gpus]
+            ends = end_gpus(enc) + end_gpus(dec)
+            assert sum(w_o) == pytest.approx(2 * Lyr * S.layer_bytes() + ends * S.emb_bytes(), rel=1e-12)
+            assert sum(kv_o) == pytest.approx((waa.b_e * S.max_in + waa.b_d * (S.max_in + S.max_out)) * Lyr * kvb,
+                                              rel=1e-12)
+            ok = S.mem_ok(enc, waa.b_e, S.max_in) and S.mem_ok(dec, waa.b_d, S.max_in + S.max_out)
+        fits = all(w + k + cl.workspace_bytes <= cl.mem_per_gpu_bytes for w, k in zip(w_o, kv_o) if w > 0)
+        assert fits == ok

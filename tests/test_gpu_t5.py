@@ -176,6 +176,24 @@ def test_t5_batch_invariance(t5env):
         assert np.array_equal(a[3][r], b[3][r]), r
 
 
+def test_t5_static_batch_baseline(t5env):
+    """FT-style static batch (EXG_STATIC) on the encoder-decoder: finished
+    rows keep decoding at clamped decoder positions inside their own slots;
+    ids and logits are bit-identical to the RRA run (T13), decode iterations
+    = sum over batches of the batch's longest output."""
+    X, spec, reqs, ctx, ora = t5env
+    a = ctx.run(X.rra_schedule(3, 5, 4), reqs, dump=range(len(reqs)))
+    b = 3
+    toks, lat, st, lg = ctx.run(X.static_schedule(b), reqs, dump=range(len(reqs)))
+    assert toks == a[0]
+    for r in range(len(reqs)):
+        assert np.array_equal(lg[r], a[3][r]), r
+    groups = [range(k, min(k + b, len(reqs))) for k in range(0, len(reqs), b)]
+    assert st["decode_iters"] == sum(max(reqs[r].output_len for r in g) for g in groups)
+    for g in groups:
+        assert len({float(lat[r]) for r in g}) == 1
+
+
 @pytest.mark.parametrize("transport", ["one_rank", "two_ranks", "nccl_loopback"])
 def test_t5_rra_pipeline_bit_identical(t5env, transport):
     """RRA over 2 pipeline stages, each holding encoder and decoder layers
