@@ -367,7 +367,7 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
                   std::make_pair(D.d, D.ffl), std::make_pair(D.V, D.d)})
     sk = std::max(sk, decode_ws_floats(fk.first, fk.second, (int)R));
   splitk_cap_ = sk;
-  max_splits_cap_ = (D.max_pos + split_len_ - 1) / split_len_;
+  max_splits_cap_ = (D.max_pos + 127) / 128;   // any split length >= 128 (diagnostics override)
   const size_t parts = R * D.Hl * (size_t)max_splits_cap_ * (D.dh + 2);
   const size_t tp_part = S_.tp > 1 ? T * D.d : 0;
   const size_t logit_rows = S_.head ? R : 0;
@@ -656,8 +656,9 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
     da.dh = D.dh;
     da.max_ctx = slot_ctx_;
     da.scale = scale;
-    da.split_len = split_len_;
-    da.max_splits = std::max(1, (db.max_keys + split_len_ - 1) / split_len_);
+    const int sl = split_len();
+    da.split_len = sl;
+    da.max_splits = std::max(1, (db.max_keys + sl - 1) / sl);
     da.partial = attn_part_;
     const int k = kbegin();
     decode_attention(da, st_);
@@ -795,8 +796,9 @@ void Engine::dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, i
   da.dh = D.dh;
   da.max_ctx = ctx;
   da.scale = 1.0f;
-  da.split_len = split_len_;
-  da.max_splits = std::max(1, (max_keys + split_len_ - 1) / split_len_);
+  const int sl = split_len();
+  da.split_len = sl;
+  da.max_splits = std::max(1, (max_keys + sl - 1) / sl);
   da.partial = attn_part_;
   da.bias = bias;
   da.bias_ld = bias_ld_;

@@ -492,6 +492,13 @@ __global__ void decode_combine_kernel(DecodeAttnArgs a) {
   }
 }
 
+// decode-attention key split length (diagnostics override via
+// exg_diag_decode_split; 0 = the engine's default); >= 128
+int& decode_split_override() {
+  static int s = 0;
+  return s;
+}
+
 // ring depth (diagnostics override via exg_diag_decode_stages; 0 = default)
 int& decode_stages_override() {
   static int s = 0;
@@ -685,3 +692,4 @@ void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, in
 }  // namespace exg
 
 extern "C" void exg_diag_decode_stages(int s) { exg::decode_stages_override() = s; }
+extern "C" void exg_diag_decode_split(int s) { exg::decode_split_override() = s >= 128 ? s : 0; }

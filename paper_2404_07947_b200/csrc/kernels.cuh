@@ -83,6 +83,7 @@ struct DecodeAttnArgs {
   int64_t ldnew = 0;
 };
 void decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
+int& decode_split_override();   // diagnostics: key split length (0 = default)
 
 // ---- K4: causal prefill attention over packed variable-length requests -----
 // Token t of request r (cu_seqlens[r] <= t < cu_seqlens[r+1]) sits at

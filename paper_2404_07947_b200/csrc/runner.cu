@@ -155,6 +155,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   for (int i = 0; i < B_D; ++i) free_slots[i] = B_D - 1 - i;
   std::vector<Row> active;
   active.reserve(B_D);
+  std::vector<int> order;   // decode-table row -> active row
   std::vector<int> admit_ev(n, -1), done_ev(n, -1);
   std::vector<cudaEvent_t> evs;
   std::vector<int> ev_kind;        // 0 = phase start, 1 = encode end, 2 = iteration end
@@ -273,11 +274,25 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       int max_keys = 0, max_xkeys = 0;
       double sum_keys = 0, sum_xkeys = 0;
       int live = 0;
-      for (int i = 0; i < B; ++i) {
-        const Row& rw = active[i];
+      // rows in decreasing attention length: the decode-attention grid is
+      // dispatched in row order, so the longest rows start first and the
+      // launch's tail is made of short rows (per-row results do not depend on
+      // the row order, T13)
+      auto row_pos = [&](const Row& rw) {
         // a finished row of a static batch keeps decoding past its length:
         // its position is clamped inside its own slot, its token goes to scratch
-        const int pos = rw.live ? rw.pos : std::min({rw.pos, slot_ctx - 1, D.max_pos - 1});
+        return rw.live ? rw.pos : std::min({rw.pos, slot_ctx - 1, D.max_pos - 1});
+      };
+      order.resize(B);
+      for (int i = 0; i < B; ++i) order[i] = i;
+      std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+        const int kx = row_pos(active[x]) + (ed ? reqs[active[x].req].input_len : 0);
+        const int ky = row_pos(active[y]) + (ed ? reqs[active[y].req].input_len : 0);
+        return kx > ky;
+      });
+      for (int i = 0; i < B; ++i) {
+        const Row& rw = active[order[i]];
+        const int pos = row_pos(rw);
         live += rw.live;
         h[i] = rw.slot;
         h[B + i] = pos;
@@ -308,7 +323,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       E.decode(db);
       if (dumping) {
         for (int i = 0; i < B; ++i) {
-          const Row& rw = active[i];
+          const Row& rw = active[order[i]];
           if (!rw.live || !opts->dump_mask[rw.req]) continue;
           float* dst = opts->logits_out + (dump_base[rw.req] + rw.emitted) * (int64_t)D.V;
           EXG_CUDA(cudaMemcpyAsync(dst, E.logits() + (int64_t)i * D.V, sizeof(float) * D.V, cudaMemcpyDeviceToHost, st));
