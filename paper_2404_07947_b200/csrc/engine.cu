@@ -580,8 +580,23 @@ void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest, in
   if (part == 1) attn = rest = true;
   if (rest) {
     layernorm(h_, d, x_, d, w.ln1_g, w.ln1_b, T, d, 1e-5f, st_);
-    linear_pre(h_, d, T, w.Wqkv, 3 * il, d, epi_bf16(w.bqkv, qkv_, 3 * il));
-    kv_scatter(kc(l), vc(l), qkv_, eb.tslot, eb.pos, T, D.Hl, D.dh, slot_ctx_, st_);
+    // K7 fused into the QKV GEMM epilogue: K / V rows go straight into the
+    // cache at (tslot, pos); qkv_ keeps Q (the FMHA's A operand)
+    EpiParams e = epi_bf16(w.bqkv, qkv_, 3 * il);
+    e.kv_k = kc(l);
+    e.kv_v = vc(l);
+    e.kv_slot = eb.tslot;
+    e.kv_pos = eb.pos;
+    e.kv_inner = il;
+    e.kv_H = D.Hl;
+    e.kv_dh = D.dh;
+    e.kv_ctx = slot_ctx_;
+    if (D.dh % 16 == 0 && (3 * il) % 8 == 0) {
+      linear_pre(h_, d, T, w.Wqkv, 3 * il, d, e);
+    } else {
+      linear_pre(h_, d, T, w.Wqkv, 3 * il, d, epi_bf16(w.bqkv, qkv_, 3 * il));
+      kv_scatter(kc(l), vc(l), qkv_, eb.tslot, eb.pos, T, D.Hl, D.dh, slot_ctx_, st_);
+    }
   }
   if (attn) {
     PrefillAttnArgs pa{qkv_, 3 * il, kc(l), vc(l), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,

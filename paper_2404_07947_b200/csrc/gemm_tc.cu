@@ -175,6 +175,18 @@ __device__ __forceinline__ void epi_store_row16(const EpiParams& ep, int tok, in
               __floats2bfloat162_rn(epi_value(ep, f0 + 2 * j, v[2 * j]), epi_value(ep, f0 + 2 * j + 1, v[2 * j + 1]));
           pk[j] = *reinterpret_cast<uint32_t*>(&h2);
         }
+        if (ep.kv_k && f0 >= ep.kv_inner) {
+          // K / V columns: straight into the cache row (slot, head, pos); the
+          // 16 features lie in one head (dh % 16 == 0)
+          const int which = (f0 - ep.kv_inner) / ep.kv_inner, hd = (f0 - ep.kv_inner) % ep.kv_inner;
+          const int h = hd / ep.kv_dh, j = hd % ep.kv_dh;
+          bf16* base = which ? ep.kv_v : ep.kv_k;
+          uint4* dst = reinterpret_cast<uint4*>(
+              base + (((int64_t)ep.kv_slot[tok] * ep.kv_H + h) * ep.kv_ctx + ep.kv_pos[tok]) * ep.kv_dh + j);
+          dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          return;
+        }
         uint4* dst = reinterpret_cast<uint4*>(ep.out_bf16 + (int64_t)tok * ep.ldo + f0);
         dst[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
         dst[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);

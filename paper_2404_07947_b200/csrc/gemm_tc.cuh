@@ -32,6 +32,15 @@ struct EpiParams {
   float* resid = nullptr;
   int64_t ldr = 0;
   int tokens = 0, features = 0;
+  // prefill QKV (EPI_BF16, row orientation): also store output features
+  // [kv_inner, 3 kv_inner) -- K then V -- of token t into the KV cache at
+  // (kv_slot[t], head, kv_pos[t]) (K7 fused into the producing GEMM); the
+  // qkv output then holds Q only
+  bf16* kv_k = nullptr;
+  bf16* kv_v = nullptr;
+  const int32_t* kv_slot = nullptr;
+  const int32_t* kv_pos = nullptr;
+  int kv_inner = 0, kv_H = 0, kv_dh = 0, kv_ctx = 0;
 };
 
 // ---- blocked weight layout ---------------------------------------------------
