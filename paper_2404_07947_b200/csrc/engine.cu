@@ -374,7 +374,7 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
   const size_t bytes = al(T * D.d * 4) + al(tp_part * 4) + al(T * D.d * 2) + al(T * 3 * D.inner_l * 2) +
                        al(T * D.inner_l * 2) + al(T * D.ffl * 2) + al(logit_rows * D.V * 4) + al(sk * 4) +
-                       al(parts * 4);
+                       al(parts * 4) + al(R * D.Hl * 4);
   uint8_t* p;
   EXG_CUDA(cudaMalloc(&p, bytes));
   x_ = carve<float>(p, T * D.d);
@@ -386,6 +386,7 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   logits_ = logit_rows ? carve<float>(p, logit_rows * D.V) : nullptr;
   splitk_ws_ = carve<float>(p, sk);
   attn_part_ = carve<float>(p, parts);
+  attn_cnt_ = carve<int32_t>(p, R * D.Hl);   // split-merge counters: zero, left at zero by each merge
   EXG_CUDA(cudaMemsetAsync(x_, 0, bytes, st_));
 }
 
@@ -675,6 +676,7 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
     da.split_len = sl;
     da.max_splits = std::max(1, (db.max_keys + sl - 1) / sl);
     da.partial = attn_part_;
+    da.counters = attn_cnt_;
     const int k = kbegin();
     decode_attention(da, st_);
     kend(k, EXG_K_DECODE_ATTN, db.sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)B * D.Hl * D.dh * 2.0 * 2.0 +
@@ -815,6 +817,7 @@ void Engine::dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, i
   da.split_len = sl;
   da.max_splits = std::max(1, (max_keys + sl - 1) / sl);
   da.partial = attn_part_;
+  da.counters = attn_cnt_;
   da.bias = bias;
   da.bias_ld = bias_ld_;
   da.bias_off = bias_off_;

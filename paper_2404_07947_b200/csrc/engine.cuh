@@ -207,6 +207,7 @@ class Engine {
   float* splitk_ws_ = nullptr;
   size_t splitk_cap_ = 0;
   float* attn_part_ = nullptr;
+  int32_t* attn_cnt_ = nullptr;
   int split_len_ = 512, max_splits_cap_ = 0;
   int split_len() const { return decode_split_override() ? decode_split_override() : split_len_; }
   int32_t* err_ = nullptr;

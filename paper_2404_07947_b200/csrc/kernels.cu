@@ -467,6 +467,32 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
       pp[2 + tid] = O;
     }
   }
+  if (nsplit > 1 && a.counters) {
+    // the last split CTA of this (row, head) merges the splits in split order
+    // -- the arithmetic of decode_combine_kernel, without its launch
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = (atomicAdd(&a.counters[(int64_t)i * a.H + h], 1) == nsplit - 1);
+    __syncthreads();
+    if (s_last) {
+      __threadfence();
+      const float* base = a.partial + ((int64_t)i * a.H + h) * a.max_splits * (DH + 2);
+      float M = -INFINITY;
+      for (int s2 = 0; s2 < nsplit; ++s2) M = fmaxf(M, __ldcg(base + s2 * (DH + 2)));
+      if (tid < DH) {
+        float L = 0.f, O = 0.f;
+        for (int s2 = 0; s2 < nsplit; ++s2) {
+          const float* pp = base + s2 * (DH + 2);
+          const float c = __expf(__ldcg(pp) - M);
+          L += __ldcg(pp + 1) * c;
+          O += __ldcg(pp + 2 + tid) * c;
+        }
+        a.out[(int64_t)i * a.ldo + h * DH + tid] = f2bf(O / L);
+      }
+      if (tid == 0) a.counters[(int64_t)i * a.H + h] = 0;
+    }
+  }
 }
 
 template <int DH>
@@ -530,14 +556,23 @@ void decode_attention_t(const DecodeAttnArgs& a, cudaStream_t st) {
     case 16: decode_attention_st<DH, 1, 6>(a, st); break;
     default: decode_attention_st<DH, 2, 7>(a, st); break;
   }
-  if (a.max_splits > 1) {
+  if (a.max_splits > 1 && !a.counters) {
     launch_pdl(decode_combine_kernel<DH>, dim3(a.B * a.H), dim3(DH < 32 ? 32 : DH), 0, st, a);
     EXG_CHECK_LAUNCH();
   }
 }
 
-void decode_attention(const DecodeAttnArgs& a, cudaStream_t st) {
-  if (a.B <= 0) return;
+// diagnostics (exg_diag_decode_merge): 1 = merge splits in the separate
+// combine kernel even when counters are given
+int& decode_force_combine() {
+  static int f = 0;
+  return f;
+}
+
+void decode_attention(const DecodeAttnArgs& a_in, cudaStream_t st) {
+  if (a_in.B <= 0) return;
+  DecodeAttnArgs a = a_in;
+  if (decode_force_combine()) a.counters = nullptr;
   switch (a.dh) {
     case 16: decode_attention_t<16>(a, st); break;
     case 64: decode_attention_t<64>(a, st); break;
@@ -693,3 +728,4 @@ void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, in
 
 extern "C" void exg_diag_decode_stages(int s) { exg::decode_stages_override() = s; }
 extern "C" void exg_diag_decode_split(int s) { exg::decode_split_override() = s >= 128 ? s : 0; }
+extern "C" void exg_diag_decode_merge(int force_combine) { exg::decode_force_combine() = force_combine; }

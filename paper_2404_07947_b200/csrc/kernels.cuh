@@ -70,6 +70,9 @@ struct DecodeAttnArgs {
   int split_len;
   int max_splits;      // >= ceil(max_i n_keys[i] / split_len)
   float* partial;      // [B][H][max_splits][dh + 2] when max_splits > 1
+  // optional [B][H] zeroed counters: the last split CTA of a (row, head)
+  // merges the splits in-kernel (no combine launch); null -> combine kernel
+  int32_t* counters = nullptr;
   // optional additive score bias (T5 relative position bias): the score of
   // key k of row i, head h gets bias[h * bias_ld + bias_off + k - (n_keys[i]-1)]
   const float* bias = nullptr;

@@ -179,3 +179,40 @@ def test_static_batch_baseline(setup):
         assert np.array_equal(lg[r], ref_l[r]), r
     with pytest.raises(X.ExgError):
         ctx.run(X.static_schedule(0), reqs)
+
+
+def test_long_context_split_merge():
+    """Rows longer than one 512-key attention split: the
+    decode attention's last split CTA merges the splits in-kernel; ids and
+    logits are bit-identical to the separate combine kernel (diagnostics
+    switch) and match the oracle's bf16-emulating KV loop."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2404_07947_b200 as X
+    from oracle import transformer as T
+    from workload import ModelSpec, Request
+    spec = ModelSpec("long-ctx", "opt", 0, 2, 256, 2, 128, 1024, 512, 1100)
+    seed = 0xE6E0_0077
+    rng = np.random.default_rng(5)
+    reqs = [Request(rng.integers(0, 512, n).astype(np.int32), n, s)
+            for n, s in ((700, 6), (505, 12), (1030, 3), (40, 5))]
+    ctx = X.Context(spec, seed)
+    a = ctx.run(X.rra_schedule(2, 4, 4), reqs, dump=range(len(reqs)))
+    X.lib().exg_diag_decode_merge(1)
+    try:
+        b = ctx.run(X.rra_schedule(2, 4, 4), reqs, dump=range(len(reqs)))
+    finally:
+        X.lib().exg_diag_decode_merge(0)
+    assert a[0] == b[0]
+    for r in range(len(reqs)):
+        assert np.array_equal(a[3][r], b[3][r]), r
+    ora = T.greedy_kv(T.Weights(spec, seed), reqs, "bf16", record_logits=True)
+    worst = 0.0
+    for r, q in enumerate(reqs):
+        for t in range(q.output_len):
+            if a[0][r][t] != ora.tokens[r][t]:
+                assert ora.margins[r][t] <= 2 * TOL, (r, t)
+                break
+            worst = max(worst, float(np.abs(a[3][r][t] - ora.logits[r][t]).max()))
+    assert worst <= TOL, worst
+    ctx.close()
