@@ -603,6 +603,7 @@ def main():
             "roofline": roof(dom),
             "roofline_decode_attn": roof("decode_attn"),
             "roofline_decode_gemm": roof("decode_gemm"),
+            "roofline_prefill_gemm": roof("prefill_gemm"),
             "roofline_prefill_attn": roof("prefill_attn"),
             "cpu_baseline": cpu,
             "e2e": {"value": e2e, "unit": "output tokens/s", "h2d_bytes_per_step": h2d,
