@@ -12,8 +12,18 @@ Rules the paper leaves open (listed in DESIGN.md):
    upp.thrput + eps_T < T*.
 Perf evaluations are memoised; `evals` counts distinct points.
 
+Outer loops: strategy x TP degree t x applied GPUs c, and
+for WAA also the decoder micro-batch count M: like the TP degree, M is not a
+monotone variable on its own (with weight-streaming-bound decode stages the
+per-stage time hardly shrinks with B_m, so the fill F grows with M and
+latency rises with M), so it is fixed per run of Algorithm 1, which then
+searches B_E (reading S9').  RRA searches (B_E, N_D) in one run.
+
 Pins: equals exhaustive argmax on strictly monotone grids; upper-corner
-shortcut in <= 2 evaluations; infeasible lower corner.
+shortcut in <= 2 evaluations; infeasible lower corner
+(tests/test_oracle_scheduler.py); schedule_find equals the exhaustive
+optimum over strategy x t x c x (x1, x2) on 1/2/4-GPU problems with the
+memory-limited B_E^max active (tests/test_oracle_pins.py).
 """
 from __future__ import annotations
 
@@ -195,11 +205,13 @@ def schedule_find(S: sim.Simulator, L_b: float, strategy_mask: int, opts: Search
                 if strat == sim.RRA:
                     def mk(x1, x2, t=t, c=c):
                         return S.rra_schedule(x1, n_d_max + 1 - x2, t, c)
-                    b2 = n_d_max
+                    x2_ranges = [(1, n_d_max)]
                 else:
                     def mk(x1, x2, t=t, c=c, strat=strat):
                         return S.waa_schedule(x1, opts.m_max + 1 - x2, t, c, strat)
-                    b2 = opts.m_max
+                    # the micro-batch count is an outer variable like the TP
+                    # degree: not monotone (DESIGN.md reading)
+                    x2_ranges = [(x2, x2) for x2 in range(1, opts.m_max + 1)]
 
                 def perf_fn(x1, x2, mk=mk):
                     s = mk(x1, x2)
@@ -207,24 +219,25 @@ def schedule_find(S: sim.Simulator, L_b: float, strategy_mask: int, opts: Search
                         return Perf(INF, INF)
                     return _perf_of(S.simulate(s))
 
-                # B_E^max: largest B_E feasible at the least memory-hungry x2 (= 1)
-                b1 = 0
-                for be in range(1, opts.b_e_max + 1):
-                    if math.isfinite(perf_fn(be, 1).latency):
-                        b1 = be
-                    else:
-                        break
-                if b1 == 0:
-                    continue
-                r = branch_and_bound(1, b1, 1, b2, perf_fn, L_b, opts.eps_t_frac, opts.eps_l_frac)
-                total_evals += r.evals + b1
-                if r.x is None:
-                    continue
-                sch = mk(*r.x)
-                est = S.simulate(sch)
-                key = (-est.thrput_seq_s, est.latency_s, strat, t, c, r.x[0], r.x[1])
-                if best is None or key < best[0]:
-                    best = (key, Found(sch, est, 0))
+                for a2, b2 in x2_ranges:
+                    # B_E^max: largest B_E feasible at the least memory-hungry x2
+                    b1 = 0
+                    for be in range(1, opts.b_e_max + 1):
+                        if math.isfinite(perf_fn(be, a2).latency):
+                            b1 = be
+                        else:
+                            break
+                    if b1 == 0:
+                        continue
+                    r = branch_and_bound(1, b1, a2, b2, perf_fn, L_b, opts.eps_t_frac, opts.eps_l_frac)
+                    total_evals += r.evals + b1
+                    if r.x is None:
+                        continue
+                    sch = mk(*r.x)
+                    est = S.simulate(sch)
+                    key = (-est.thrput_seq_s, est.latency_s, strat, t, c, r.x[0], r.x[1])
+                    if best is None or key < best[0]:
+                        best = (key, Found(sch, est, 0))
     if best is None:
         return None
     best[1].evals = total_evals

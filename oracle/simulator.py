@@ -15,8 +15,13 @@ Readings (listed in DESIGN.md):
   stage proportional to GPUs per stage, remainder one per stage from the front.
 
 Pins: Table 8 rows 3-4 identities (RRA P=1), Fig. 4 "7" and "3 2/3" (WAA
-pipeline), pipeline algebra == FIFO event loop; beyond these the timeline is
-**parity unpinned** against the paper (Fig. 4a is missing).
+pipeline), pipeline algebra == FIFO event loop (tests/test_oracle_scheduler.py);
+simulate_waa vs Table 8 row 1 + Table 9's WAA decoder stage, vs an independent
+WAA event loop (throughput equal; latency bracketed, equal for M = 1 with a
+draining decoder), the handoff term; waa_split through SPEC.md:235-237 and the
+mirror invariant; interp2 on hand values and bilinear closed forms
+(tests/test_oracle_pins.py).  The RRA P > 1 timeline is pinned only by the
+pipeline algebra identities (Fig. 4a is missing from PAPER.md).
 """
 from __future__ import annotations
 

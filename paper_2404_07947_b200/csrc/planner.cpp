@@ -672,43 +672,53 @@ bool schedule_find(Simulator& S, double L_b, uint32_t mask, const exg_search_opt
           return strat == EXG_RRA ? S.rra_schedule(x1, n_d_max + 1 - x2, t, c)
                                   : S.waa_schedule(x1, o.m_max + 1 - x2, t, c, strat);
         };
-        const int b2 = strat == EXG_RRA ? n_d_max : o.m_max;
+        // x2 ranges: RRA searches N_D inside Algorithm 1; for WAA the
+        // micro-batch count is an outer variable like the TP degree
+        // -- it is not monotone (DESIGN.md reading)
+        std::vector<std::pair<int, int>> x2r;
+        if (strat == EXG_RRA)
+          x2r.push_back({1, n_d_max});
+        else
+          for (int x2 = 1; x2 <= o.m_max; ++x2) x2r.push_back({x2, x2});
         auto perf_fn = [&](int x1, int x2) -> Perf {
           Sched s = mk(x1, x2);
           if (!s.valid) return Perf{INF, INF};
           return perf_of(S.simulate(s));
         };
-        int b1 = 0;
-        for (int be = 1; be <= o.b_e_max; ++be) {
-          if (std::isfinite(perf_fn(be, 1).latency))
-            b1 = be;
-          else
-            break;
-        }
-        if (b1 == 0) continue;
-        BnBResult r = branch_and_bound(1, b1, 1, b2, perf_fn, L_b, o.eps_t_frac, o.eps_l_frac);
-        total_evals += r.evals + b1;
-        if (!r.found) continue;
-        Sched sch = mk(r.x1, r.x2);
-        Est est = S.simulate(sch);
-        const double nthr = -est.thr;
-        const int rest[5] = {strat, t, c, r.x1, r.x2};
-        bool better = !have;
-        if (have) {
-          if (nthr != k_thr)
-            better = nthr < k_thr;
-          else if (est.lat != k_lat)
-            better = est.lat < k_lat;
-          else
-            better = std::lexicographical_compare(rest, rest + 5, k_rest, k_rest + 5);
-        }
-        if (better) {
-          have = true;
-          k_thr = nthr;
-          k_lat = est.lat;
-          std::copy(rest, rest + 5, k_rest);
-          out->sched = sch;
-          out->est = est;
+        for (const auto& ab2 : x2r) {
+          const int a2 = ab2.first, b2 = ab2.second;
+          int b1 = 0;
+          for (int be = 1; be <= o.b_e_max; ++be) {
+            if (std::isfinite(perf_fn(be, a2).latency))
+              b1 = be;
+            else
+              break;
+          }
+          if (b1 == 0) continue;
+          BnBResult r = branch_and_bound(1, b1, a2, b2, perf_fn, L_b, o.eps_t_frac, o.eps_l_frac);
+          total_evals += r.evals + b1;
+          if (!r.found) continue;
+          Sched sch = mk(r.x1, r.x2);
+          Est est = S.simulate(sch);
+          const double nthr = -est.thr;
+          const int rest[5] = {strat, t, c, r.x1, r.x2};
+          bool better = !have;
+          if (have) {
+            if (nthr != k_thr)
+              better = nthr < k_thr;
+            else if (est.lat != k_lat)
+              better = est.lat < k_lat;
+            else
+              better = std::lexicographical_compare(rest, rest + 5, k_rest, k_rest + 5);
+          }
+          if (better) {
+            have = true;
+            k_thr = nthr;
+            k_lat = est.lat;
+            std::copy(rest, rest + 5, k_rest);
+            out->sched = sch;
+            out->est = est;
+          }
         }
       }
     }

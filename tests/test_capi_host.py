@@ -303,3 +303,39 @@ def test_schedule_memory(L, tmp_path, n_gpus, t, c):
             ok = S.mem_ok(enc, waa.b_e, S.max_in) and S.mem_ok(dec, waa.b_d, S.max_in + S.max_out)
         fits = all(w + k + cl.workspace_bytes <= cl.mem_per_gpu_bytes for w, k in zip(w_o, kv_o) if w > 0)
         assert fits == ok
+
+
+@pytest.mark.parametrize("n_gpus", [2, 4])
+def test_schedule_find_bit_identical_on_exhaustive_pin_problems(L, tmp_path, n_gpus):
+    """The small problems on which tests/test_oracle_pins.py pins the
+    oracle's schedule_find to the exhaustive optimum: the C++ planner returns
+    the same schedule, estimate and evaluation count (S15)."""
+    import sys
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from test_oracle_pins import _small_problem
+    from oracle import bnb
+    from workload import MODELS
+    S = _small_problem(n_gpus)
+    path = str(tmp_path / "p.txt")
+    S.p.save(path)
+    P = L.Profile.load(path)
+    spec = MODELS["opt-13b"]
+    import dataclasses
+    spec = dataclasses.replace(spec, n_dec_layers=S.m.n_dec_layers, n_heads=S.m.n_heads)
+    mspec = L.model_spec(spec, 1)
+    ccl = L.cluster_spec(S.cl.n_gpus, S.cl.mem_per_gpu_bytes, S.cl.workspace_bytes)
+    pin, pout = L.Pmf(S.pmf_in), L.Pmf(S.pmf_out)
+    opts = bnb.SearchOpts(eps_t_frac=0.0, eps_l_frac=0.0, b_e_max=12, m_max=4)
+    copts = L.search_opts(eps_t=0.0, eps_l=0.0, b_e_max=12, m_max=4)
+    for L_b in (0.005, 0.0103, 0.02, 0.05, math.inf):
+        f = bnb.schedule_find(S, L_b, 7, opts)
+        if f is None:
+            with pytest.raises(L.ExgError):
+                L.schedule_find(P, mspec, ccl, pin, pout, S.target_len, L_b, 7, copts)
+            continue
+        s, est = L.schedule_find(P, mspec, ccl, pin, pout, S.target_len, L_b, 7, copts)
+        assert (s.strategy, s.b_e, s.b_d, s.b_m, s.n_d, s.tp_degree, s.tp_gpus, s.n_enc_gpus) == (
+            f.schedule.strategy, f.schedule.b_e, f.schedule.b_d, f.schedule.b_m, f.schedule.n_d,
+            f.schedule.tp_degree, f.schedule.tp_gpus, f.schedule.n_enc_gpus)
+        assert est.thrput_seq_s == f.estimate.thrput_seq_s and est.latency_s == f.estimate.latency_s
+        assert est.perf_evals == f.evals
