@@ -130,12 +130,14 @@ typedef struct {
   int32_t pin_nccl_algo;      /* reserved for multi-GPU parity runs             */
   int32_t kernel_timing;      /* 1: CUDA events around every launch of the
                                  kernel classes below (roofline evidence)       */
-  double dyn_threshold;       /* > 0: dynamic workload adjustment (PAPER.md:350-354,
-                                 RRA on 1 GPU): each encode batch's token sum
-                                 is kept within +-threshold of B_E x mean
-                                 encoded length, and B_E is raised / lowered by
-                                 one while the decode batch sits below / above
-                                 +-threshold of its running average; 0 = off  */
+  double dyn_threshold;       /* > 0: dynamic workload adjustment:
+                                 while the decode batch sits outside
+                                 +-threshold of its running average, the next
+                                 encode batch targets B_E' = B_E + round(avg -
+                                 current) rows (clamped to [1, B_D]); its token
+                                 sum is kept within +-threshold of B_E' x the
+                                 mean encoded length and never above B_E x the
+                                 longest input (the encode workspace); 0 = off */
 } exg_run_opts;
 
 /* Kernel classes timed when exg_run_opts.kernel_timing = 1.  Work is the

@@ -188,15 +188,18 @@ class Result:
     margins: List[List[float]] = field(default_factory=list)
 
 
-def greedy_kv(W: T5Weights, requests, mode: str = "bf16", record_logits: bool = False) -> Result:
+def greedy_kv(W: T5Weights, requests, mode: str = "bf16", record_logits: bool = False,
+              forced: Optional[List[List[int]]] = None) -> Result:
     """(ii)/(iii): encoder once per request, cross K/V projected once (K13),
-    decoder self-attention KV cache, one token per decode iteration."""
+    decoder self-attention KV cache, one token per decode iteration.
+    forced[r]: decode inputs forced to these tokens (teacher forcing on
+    another run's output) instead of the greedy ids."""
     R = Rounding(mode)
     spec = W.spec
     H, dh, inner, d = spec.n_heads, spec.d_head, spec.inner, spec.d_model
     head_scale = d ** -0.5
     toks, logs, margins = [], [], []
-    for q in requests:
+    for qi, q in enumerate(requests):
         enc = encoder_forward(W, q.ids, R)
         n = enc.shape[0]
         cross = []
@@ -231,7 +234,7 @@ def greedy_kv(W: T5Weights, requests, mode: str = "bf16", record_logits: bool = 
             mg_r.append(top2_margin(lg))
             if record_logits:
                 lg_r.append(lg)
-            cur = y
+            cur = y if forced is None else forced[qi][t]
         toks.append(out)
         logs.append(lg_r)
         margins.append(mg_r)

@@ -312,12 +312,13 @@ def greedy_kv(W: Weights, requests, mode: str = "bf16", record_logits: bool = Fa
     return KVLoop(W, mode, accum).run(requests, record_logits, record)
 
 
-def teacher_forced_logits(W: Weights, request, forced: List[int], mode: str = "fp64") -> List[np.ndarray]:
+def teacher_forced_logits(W: Weights, request, forced: List[int], mode: str = "fp64",
+                          accum: str = "fp64") -> List[np.ndarray]:
     """Logits of every decode step when the decode inputs are forced to
     `forced` (the tokens some other run emitted): used to compare a run's
-    logits with mode (ii) on that run's own prefix."""
-    from workload import Request
-    loop = KVLoop(W, mode)
+    logits with mode (ii) on that run's own prefix, and to keep checking a
+    run past a near-tie divergence (tests/parity.py)."""
+    loop = KVLoop(W, mode, accum)
     nL, H, dh = W.spec.n_dec_layers, W.spec.n_heads, W.spec.d_head
     caches = {0: ([np.zeros((H, 0, dh)) for _ in range(nL)], [np.zeros((H, 0, dh)) for _ in range(nL)])}
     n = request.input_len

@@ -191,9 +191,12 @@ def check(status: int):
 ARCH_OF = {"opt": EXG_ARCH_OPT, "gpt3": EXG_ARCH_GPT3, "t5": EXG_ARCH_T5}
 
 
-def model_spec(spec, seed: int) -> exg_model_spec:
+EXG_BF16, EXG_FP32 = 0, 1
+
+
+def model_spec(spec, seed: int, dtype: int = EXG_BF16) -> exg_model_spec:
     return exg_model_spec(ARCH_OF[spec.arch], spec.n_enc_layers, spec.n_dec_layers, spec.d_model, spec.n_heads,
-                          spec.d_head, spec.d_ff, spec.vocab, spec.max_pos, 0, seed)
+                          spec.d_head, spec.d_ff, spec.vocab, spec.max_pos, dtype, seed)
 
 
 def cluster_spec(n_gpus: int = 1, mem_per_gpu: float = 180e9, workspace: float = 6e9) -> exg_cluster_spec:
@@ -225,9 +228,9 @@ class Context:
     rank 0 receives the outputs."""
 
     def __init__(self, spec, seed: int, device: int = 0, cluster: Optional[exg_cluster_spec] = None,
-                 rank: int = 0, world: int = 1, uid: Optional[bytes] = None, _handle=None):
+                 rank: int = 0, world: int = 1, uid: Optional[bytes] = None, _handle=None, dtype: int = EXG_BF16):
         self.spec = spec
-        self.mspec = model_spec(spec, seed)
+        self.mspec = model_spec(spec, seed, dtype)
         self.cluster = cluster or cluster_spec()
         self.rank, self.world = rank, world
         if _handle is not None:

@@ -73,6 +73,16 @@ void check_spec(const exg_model_spec* s) {
   if (s->n_dec_layers < 1 || s->d_model < 1 || s->n_heads < 1 || s->d_head < 1 || s->d_ff < 1 || s->vocab < 2 ||
       s->max_pos < 2)
     throw std::invalid_argument("invalid model spec");
+  if (s->dtype != EXG_BF16 && s->dtype != EXG_FP32) throw std::invalid_argument("unknown dtype");
+}
+
+// the fp32 parity path covers decoder-only models on a
+// single-GPU context
+void check_fp32_scope(const exg_model_spec* s, const exg_cluster_spec* cluster, int world) {
+  if (s->dtype != EXG_FP32) return;
+  if (s->arch == EXG_ARCH_T5) throw std::invalid_argument("EXG_FP32: encoder-decoder models run bf16 only");
+  if (world > 1 || (cluster && cluster->n_gpus > 1))
+    throw std::invalid_argument("EXG_FP32: single-GPU contexts only (cluster.n_gpus = 1, world = 1)");
 }
 
 void to_c(const exg::plan::Sched& s, exg_schedule* o) {
@@ -134,6 +144,7 @@ exg_status exg_create(const exg_model_spec* spec, const exg_cluster_spec* cluste
     if (!out) throw std::invalid_argument("null out");
     *out = nullptr;
     check_spec(spec);
+    check_fp32_scope(spec, cluster, world);
     if (world < 1 || rank < 0 || rank >= world) throw std::invalid_argument("bad rank / world");
     if (world > 1 && !uid) throw std::invalid_argument("multi-rank context needs the rank-0 unique id");
     if (world > 1 && (!cluster || cluster->n_gpus < world)) throw std::invalid_argument("cluster has fewer GPUs than ranks");
@@ -171,6 +182,7 @@ exg_status exg_create_nccl_loopback(const exg_model_spec* spec, const exg_cluste
     if (!out || !cluster) throw std::invalid_argument("null argument");
     *out = nullptr;
     check_spec(spec);
+    check_fp32_scope(spec, cluster, 2);
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EXG_E_CUDA, "no CUDA device");
     if (device < 0 || device >= ndev) throw std::invalid_argument("bad device index");
@@ -198,6 +210,7 @@ exg_status exg_create_local_group(const exg_model_spec* spec, const exg_cluster_
   return guarded([&] {
     if (!out || !cluster) throw std::invalid_argument("null argument");
     check_spec(spec);
+    check_fp32_scope(spec, cluster, world);
     if (world < 2 || world > cluster->n_gpus) throw std::invalid_argument("world must be in [2, cluster.n_gpus]");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(EXG_E_CUDA, "no CUDA device");
@@ -231,6 +244,7 @@ exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profi
     if (!ctx || !grid || !out) throw std::invalid_argument("null argument");
     auto p = std::make_unique<exg_profile>();
     if (!ctx->engine) throw std::invalid_argument("profile on a single-GPU context (cluster.n_gpus = 1)");
+    if (ctx->spec.dtype != EXG_BF16) throw std::invalid_argument("the profiler times the bf16 path");
     exg::profile_layers(*ctx->engine, ctx->spec, *grid, &p->p);
     *out = p.release();
     return EXG_OK;

@@ -154,6 +154,11 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
   D.max_pos = s.max_pos;
   D.seed = s.weight_seed;
   D.act = (s.arch == EXG_ARCH_OPT || t5_) ? ACT_RELU : ACT_GELU;
+  if (s.dtype != EXG_BF16 && s.dtype != EXG_FP32) throw std::invalid_argument("unknown dtype");
+  D.f32 = s.dtype == EXG_FP32;
+  if (D.f32 && (t5_ || shard.tp != 1 || !shard.embed || !shard.head || shard.l0 != 0 ||
+                (shard.l1 >= 0 && shard.l1 != s.n_dec_layers)))
+    throw std::invalid_argument("the fp32 path runs decoder-only models on one GPU (whole model, no TP / PP)");
   if (S_.l1 < 0) S_.l1 = D.L;
   if (S_.l0 < 0 || S_.l1 > D.L || S_.l0 >= S_.l1) throw std::invalid_argument("bad shard layer range");
   if (S_.tp < 1 || D.H % S_.tp || D.ff % S_.tp || S_.tp_rank < 0 || S_.tp_rank >= S_.tp)
@@ -372,9 +377,12 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   const size_t tp_part = S_.tp > 1 ? T * D.d : 0;
   const size_t logit_rows = S_.head ? R : 0;
   auto al = [](size_t b) { return (b + 255) & ~size_t(255); };
+  const size_t f32_act = D.f32 ? al(T * D.d * 4) + al(T * 3 * D.inner_l * 4) + al(T * D.inner_l * 4) +
+                                     al(T * D.ffl * 4)
+                               : 0;
   const size_t bytes = al(T * D.d * 4) + al(tp_part * 4) + al(T * D.d * 2) + al(T * 3 * D.inner_l * 2) +
                        al(T * D.inner_l * 2) + al(T * D.ffl * 2) + al(logit_rows * D.V * 4) + al(sk * 4) +
-                       al(parts * 4) + al(R * D.Hl * 4);
+                       al(parts * 4) + al(R * D.Hl * 4) + f32_act;
   uint8_t* p;
   EXG_CUDA(cudaMalloc(&p, bytes));
   x_ = carve<float>(p, T * D.d);
@@ -387,6 +395,12 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   splitk_ws_ = carve<float>(p, sk);
   attn_part_ = carve<float>(p, parts);
   attn_cnt_ = carve<int32_t>(p, R * D.Hl);   // split-merge counters: zero, left at zero by each merge
+  if (D.f32) {
+    hf_ = carve<float>(p, T * D.d);
+    qkvf_ = carve<float>(p, T * 3 * D.inner_l);
+    ctxf_ = carve<float>(p, T * D.inner_l);
+    fff_ = carve<float>(p, T * D.ffl);
+  }
   EXG_CUDA(cudaMemsetAsync(x_, 0, bytes, st_));
 }
 
@@ -410,7 +424,7 @@ void Engine::ensure_kv(int slots, int slot_ctx, int layers, int xctx) {
   slot_ctx_ = slot_ctx;
   xctx_ = xctx;
   kv_layers_ = layers;
-  const size_t bytes = (size_t)self_layers * 2 * kv_layer_elems() * sizeof(bf16);
+  const size_t bytes = (size_t)self_layers * 2 * kv_layer_elems() * (D.f32 ? sizeof(float) : sizeof(bf16));
   const size_t xbytes = (size_t)x_layers * 2 * xkv_layer_elems() * sizeof(bf16);
   cudaError_t e = bytes ? cudaMalloc(&kv_, bytes) : cudaSuccess;
   if (e == cudaSuccess && xbytes) e = cudaMalloc(&xkv_, xbytes);
@@ -623,6 +637,10 @@ void Engine::embed_encode(const EncodeBatch& eb) {
 
 void Engine::encode(const EncodeBatch& eb) {
   if (eb.T <= 0) return;
+  if (D.f32) {
+    encode_f32(eb);
+    return;
+  }
   if (t5_) {
     encode_t5(eb);
     return;
@@ -703,6 +721,10 @@ void Engine::embed_decode(const DecodeBatch& db) {
 
 void Engine::decode(const DecodeBatch& db) {
   if (db.B <= 0) return;
+  if (D.f32) {
+    decode_f32(db);
+    return;
+  }
   if (t5_ && S_.t5_role == 1) throw std::logic_error("T5 encoder-side shard: no decoder layers");
   if (S_.tp > 1 && !red_) throw std::logic_error("TP shard without a reducer: drive it through a TP group");
   embed_decode(db);
@@ -725,6 +747,42 @@ void Engine::head_decode(const DecodeBatch& db) {
     launch_pdl(argmax_scatter_kernel, dim3(B), dim3(256), 0, st_, logits_, D.V, db.slot, db.out_off, last_tok_, db.out_tokens, err_);
     EXG_CHECK_LAUNCH();
   }
+}
+
+// ---------------------------------------------------------------------------
+// fp32 parity path (fp32_path.cu): the layer of the file
+// header with every rounding point of T4 removed -- fp32 norm output, q/k/v,
+// KV cache, context, FFN activation and logits; FFMA contractions.
+// ---------------------------------------------------------------------------
+void Engine::layer_f32(int l, int rows, const int32_t* slot, const int32_t* pos) {
+  const LayerW& w = layers_[l];
+  const int d = D.d, il = D.inner_l;
+  const float scale = (float)(1.0 / std::sqrt((double)D.dh));
+  layernorm_f32(hf_, d, x_, d, w.ln1_g, w.ln1_b, rows, d, 1e-5f, st_);
+  linear_f32(hf_, d, w.Wqkv, rows, 3 * il, d, w.bqkv, EPI_F32, ACT_NONE, qkvf_, 3 * il, st_);
+  // K7: the rows' K / V into their slots, then causal attention over keys
+  // 0..pos of each row's slot
+  kv_scatter_f32(kcf(l), vcf(l), qkvf_, 3 * il, il, slot, pos, rows, D.Hl, D.dh, slot_ctx_, st_);
+  attention_f32(qkvf_, 3 * il, kcf(l), vcf(l), slot, pos, rows, D.Hl, D.dh, slot_ctx_, scale, ctxf_, il, st_);
+  linear_f32(ctxf_, il, w.Wo, rows, d, il, w.bo, EPI_RESID, ACT_NONE, x_, d, st_);
+  layernorm_f32(hf_, d, x_, d, w.ln2_g, w.ln2_b, rows, d, 1e-5f, st_);
+  linear_f32(hf_, d, w.W1, rows, D.ffl, d, w.b1, EPI_BF16_ACT, D.act, fff_, D.ffl, st_);
+  linear_f32(fff_, D.ffl, w.W2, rows, d, D.ffl, w.b2, EPI_RESID, ACT_NONE, x_, d, st_);
+}
+
+void Engine::encode_f32(const EncodeBatch& eb) {
+  embed_encode(eb);
+  for (int l = 0; l < n_layers(); ++l) layer_f32(l, eb.T, eb.tslot, eb.pos);
+}
+
+void Engine::decode_f32(const DecodeBatch& db) {
+  embed_decode(db);
+  for (int l = 0; l < n_layers(); ++l) layer_f32(l, db.B, db.slot, db.pos);
+  layernorm_f32(hf_, D.d, x_, D.d, lnf_g_, lnf_b_, db.B, D.d, 1e-5f, st_);
+  linear_f32(hf_, D.d, tok_emb_, db.B, D.V, D.d, nullptr, EPI_F32, ACT_NONE, logits_, D.V, st_);
+  launch_pdl(argmax_scatter_kernel, dim3(db.B), dim3(256), 0, st_, logits_, D.V, db.slot, db.out_off, last_tok_,
+             db.out_tokens, err_);
+  EXG_CHECK_LAUNCH();
 }
 
 // ---------------------------------------------------------------------------

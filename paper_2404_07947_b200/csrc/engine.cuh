@@ -27,6 +27,7 @@ struct LayerW {
 
 struct Dims {
   int arch, L, d, H, dh, inner, ff, V, max_pos, act;
+  bool f32 = false;   // fp32 parity path (fp32_path.cu)
   uint64_t seed;
   // local (tensor-parallel shard) sizes
   int Hl, inner_l, ffl;
@@ -111,9 +112,13 @@ class Engine {
   // residual stream x [rows][d] fp32: the stage input (non-first stages) and
   // output (non-last stages)
   float* x() { return x_; }
-  // KV cache of local layer l: [slot][Hl][slot_ctx][dh]
+  // KV cache of local layer l: [slot][Hl][slot_ctx][dh] (bf16; fp32 on the
+  // fp32 path: kcf / vcf)
   bf16* kc(int l) const { return kv_ + (size_t)l * 2 * kv_layer_elems(); }
   bf16* vc(int l) const { return kc(l) + kv_layer_elems(); }
+  float* kcf(int l) const { return reinterpret_cast<float*>(kv_) + (size_t)l * 2 * kv_layer_elems(); }
+  float* vcf(int l) const { return kcf(l) + kv_layer_elems(); }
+  bool fp32() const { return D.f32; }
 
   // prefill of the packed tokens through this shard's layers; writes K/V into
   // slots.  First stage: embeds eb.ids; otherwise x() holds the input rows.
@@ -166,6 +171,10 @@ class Engine {
   void gen_weights();
   void gen_weights_t5();
   void encode_t5(const EncodeBatch& eb);
+  // fp32 parity path: the same layer, every intermediate in fp32
+  void encode_f32(const EncodeBatch& eb);
+  void decode_f32(const DecodeBatch& db);
+  void layer_f32(int l, int rows, const int32_t* slot, const int32_t* pos);
   void enc_layer_t5(int l, const EncodeBatch& eb, bool attn, bool rest);
   void dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest);
   void dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, int ctx, const DecodeBatch& db,
@@ -204,6 +213,8 @@ class Engine {
   float* part_ = nullptr;        // TP partial sums [T][d]
   bf16 *h_ = nullptr, *qkv_ = nullptr, *ctx_ = nullptr, *ff_ = nullptr;
   float* logits_ = nullptr;
+  // fp32 path activations: norm output, q|k|v, attention context, FFN1 output
+  float *hf_ = nullptr, *qkvf_ = nullptr, *ctxf_ = nullptr, *fff_ = nullptr;
   float* splitk_ws_ = nullptr;
   size_t splitk_cap_ = 0;
   float* attn_part_ = nullptr;

@@ -117,6 +117,23 @@ struct PrefillAttnArgs {
 void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);
 bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st);
 
+// ---- fp32 parity path (fp32_path.cu) -------------------
+// y = LN(x) * g + b in fp32 (biased variance, eps)
+void layernorm_f32(float* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
+                   float eps, cudaStream_t st);
+// FFMA GEMM: out[t][f] (=, += for EPI_RESID) X[t][:] . W[f][:] + bias[f] with W
+// the blocked bf16 [F][K] layout; mode EPI_F32 | EPI_BF16_ACT (fp32 act(.)) |
+// EPI_RESID
+void linear_f32(const float* X, int64_t ldx, const bf16* Wb, int T, int F, int K, const bf16* bias, int mode, int act,
+                float* out, int64_t ldo, cudaStream_t st);
+// K, V columns [inner, 3 inner) of qkv row t -> fp32 cache (slot[t], h, pos[t])
+void kv_scatter_f32(float* kc, float* vc, const float* qkv, int64_t ldqkv, int inner, const int32_t* slot,
+                    const int32_t* pos, int T, int H, int dh, int ctx, cudaStream_t st);
+// row i attends over keys 0..pos[i] of slot[i] (causal), fp32 softmax with expf
+void attention_f32(const float* q, int64_t ldq, const float* kc, const float* vc, const int32_t* slot,
+                   const int32_t* pos, int rows, int H, int dh, int ctx, float scale, float* out, int64_t ldo,
+                   cudaStream_t st);
+
 // ---- K8: greedy argmax per row (lowest index wins ties; NaN -> err flag) ---
 void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, int32_t* err_flag, cudaStream_t st);
 

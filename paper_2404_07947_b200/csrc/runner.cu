@@ -25,6 +25,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <memory>
 #include <numeric>
 #include <stdexcept>
 #include <vector>
@@ -128,21 +129,34 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   if (slot_ctx < need_ctx) throw std::invalid_argument("slot_ctx smaller than a request's input+output length");
   const int B_D = ft ? s.b_e : s.b_d, B_E = s.b_e;
   const int enc_drop = ed ? 0 : 1;   // input tokens the encode phase does not process
+  const double dyn = (opts && !ft) ? opts->dyn_threshold : 0.0;
+  // encode-phase capacity: B_E rows of at most max_in - enc_drop tokens.  The
+  // dynamic adjustment may admit up to B_D rows, but never more tokens than
+  // this (its token target is clamped to enc_tok_cap below)
+  const int enc_tok_cap = std::max(1, B_E * (max_in - enc_drop));
+  const int enc_row_cap = dyn > 0 ? B_D : B_E;
   E.ensure_kv(B_D, slot_ctx, -1, ed ? max_in : 0);
-  E.ensure_workspace(std::max(1, B_E * (max_in - enc_drop)), B_D);
+  E.ensure_workspace(enc_tok_cap, B_D);
   cudaStream_t st = E.stream();
 
-  // device arrays: output tokens, encode tables, decode tables
-  int32_t* d_out = nullptr;
-  int32_t* d_tab = nullptr;
-  const size_t enc_ints = (size_t)3 * B_E * max_in + 3 * (B_E + 1) + 2 * B_E;
+  // device arrays: output tokens, encode tables, decode tables (freed on
+  // every exit path)
+  struct DevFree {
+    void operator()(int32_t* p) const { cudaFree(p); }
+  };
+  const size_t enc_ints = (size_t)3 * enc_tok_cap + 3 * ((size_t)enc_row_cap + 1) + 2 * (size_t)enc_row_cap;
   const size_t dec_ints = (size_t)5 * B_D;
   const size_t tab_ints = std::max(enc_ints, dec_ints);
+  int32_t* raw = nullptr;
   // + B_D scratch entries: the tokens of finished rows a static batch still computes
-  EXG_CUDA(cudaMalloc(&d_out, sizeof(int32_t) * (total_out + B_D)));
-  EXG_CUDA(cudaMalloc(&d_tab, sizeof(int32_t) * (enc_ints + dec_ints)));
-  int32_t* d_enc = d_tab;
-  int32_t* d_dec = d_tab + enc_ints;
+  EXG_CUDA(cudaMalloc(&raw, sizeof(int32_t) * (total_out + B_D)));
+  std::unique_ptr<int32_t, DevFree> d_out_own(raw);
+  raw = nullptr;
+  EXG_CUDA(cudaMalloc(&raw, sizeof(int32_t) * (enc_ints + dec_ints)));
+  std::unique_ptr<int32_t, DevFree> d_tab_own(raw);
+  int32_t* d_out = d_out_own.get();
+  int32_t* d_enc = d_tab_own.get();
+  int32_t* d_dec = d_enc + enc_ints;
   Staging stage(64, tab_ints);
   EventPool evp;
   std::vector<float> dump_host;
@@ -170,7 +184,6 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   };
 
   int next_req = 0;
-  const double dyn = (opts && !ft) ? opts->dyn_threshold : 0.0;
   double mean_enc_tokens = 0, steady_batch_sum = 0;
   int64_t steady_iters = 0, admitted_phases = 0;
   for (int r = 0; r < n; ++r) mean_enc_tokens += reqs[r].input_len - enc_drop;
@@ -202,6 +215,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         const double t = reqs[next_req + k].input_len - enc_drop;
         if (k >= be && tok >= (1 - dyn) * target) break;
         if (k >= 1 && tok + t > (1 + dyn) * target) break;
+        if (k >= 1 && tok + t > enc_tok_cap) break;   // workspace / staging capacity
         tok += t;
         ++k;
       }
@@ -372,8 +386,8 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   int32_t err = 0;
   EXG_CUDA(cudaMemcpy(&err, E.err_flag(), sizeof(int32_t), cudaMemcpyDeviceToHost));
   if (out_tokens) EXG_CUDA(cudaMemcpy(out_tokens, d_out, sizeof(int32_t) * total_out, cudaMemcpyDeviceToHost));
-  cudaFree(d_out);
-  cudaFree(d_tab);
+  d_out_own.reset();
+  d_tab_own.reset();
   if (err) throw std::runtime_error("NaN logit encountered (T7)");
 
   // ---------------- timing ----------------

@@ -17,3 +17,16 @@ def pytest_configure(config):
 def tiny_spec():
     from workload import MODELS
     return MODELS["tiny"]
+
+
+def pytest_terminal_summary(terminalreporter, exitstatus, config):
+    """Near-tie divergences are reported, never passed
+    silently: every one recorded by tests/parity.py is listed here."""
+    try:
+        from parity import NEAR_TIES
+    except ImportError:
+        return
+    if NEAR_TIES:
+        terminalreporter.section("near-tie divergences (T4a)")
+        for label, r, t, m in NEAR_TIES:
+            terminalreporter.write_line("%s: request %d step %d, oracle top-2 margin %.3g" % (label, r, t, m))

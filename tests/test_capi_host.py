@@ -339,3 +339,17 @@ def test_schedule_find_bit_identical_on_exhaustive_pin_problems(L, tmp_path, n_g
             f.schedule.tp_degree, f.schedule.tp_gpus, f.schedule.n_enc_gpus)
         assert est.thrput_seq_s == f.estimate.thrput_seq_s and est.latency_s == f.estimate.latency_s
         assert est.perf_evals == f.evals
+
+
+def test_dtype_contract_without_gpu(L):
+    """exg_create validates the dtype before touching a device: an unknown
+    dtype, or EXG_FP32 outside the fp32 path's scope (encoder-decoder model,
+    multi-GPU context), returns EXG_E_INPUT -- never a silent bf16 run
+    (ADVICE r1)."""
+    import ctypes as C
+    from workload import MODELS
+    for spec_name, dtype, ngpu in (("tiny", 7, 1), ("tiny-t5", 1, 1), ("tiny", 1, 2)):
+        ms = L.model_spec(MODELS[spec_name], 1, dtype)
+        h = C.c_void_p()
+        st = L.lib().exg_create(C.byref(ms), C.byref(L.cluster_spec(ngpu)), 0, 0, 1, None, C.byref(h))
+        assert st == L.EXG_E_INPUT, (spec_name, dtype, ngpu, st)

@@ -14,6 +14,8 @@ configs[0]) -- SURVEY.md §8(c) T4/T4a:
 import numpy as np
 import pytest
 
+from parity import compare_free_running, decoder_only_tf
+
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
@@ -39,15 +41,9 @@ def setup():
 def test_config1_ids_and_logits(setup):
     X, T, spec, W, reqs, ctx, ora = setup
     toks, lat, stats, logits = ctx.run(X.rra_schedule(4, 8, 6), reqs, dump=range(len(reqs)))
-    worst = 0.0
-    for r, q in enumerate(reqs):
-        for t in range(q.output_len):
-            if toks[r][t] != ora.tokens[r][t]:
-                m = ora.margins[r][t]
-                assert m <= 2 * TOL, "hard mismatch req %d step %d margin %.4g" % (r, t, m)
-                pytest.fail("near-tie divergence req %d step %d (margin %.3g)" % (r, t, m))
-            worst = max(worst, float(np.abs(logits[r][t] - ora.logits[r][t]).max()))
-    assert worst <= TOL, worst
+    # config 1's weight seed keeps every oracle margin >= 1e-3 (T4a fixture
+    # choice), so no near tie is allowed here
+    compare_free_running("config1", toks, logits, ora, TOL, decoder_only_tf(W, reqs), max_near_ties=0)
     assert stats["out_tokens"] == sum(q.output_len for q in reqs)
     assert stats["encode_phases"] >= 2 and stats["decode_iters"] >= max(q.output_len for q in reqs)
     assert np.all(lat > 0)
@@ -86,15 +82,7 @@ def test_single_token_input_and_long_requests(setup):
              Request(rng.integers(0, 512, 2).astype(np.int32), 2, 1)]
     o = T.greedy_kv(W, extra, "bf16", record_logits=True)
     toks, _, _, lg = ctx.run(X.rra_schedule(2, 3, 4), extra, dump=range(3))
-    for r in range(3):
-        n_ok = 0
-        for t in range(extra[r].output_len):
-            if toks[r][t] != o.tokens[r][t]:
-                assert o.margins[r][t] <= 2 * TOL
-                break
-            assert np.abs(lg[r][t] - o.logits[r][t]).max() <= TOL
-            n_ok += 1
-        assert n_ok >= 1
+    compare_free_running("edge-lengths", toks, lg, o, TOL, decoder_only_tf(W, extra), max_near_ties=1)
 
 
 def test_input_errors(setup):
@@ -206,13 +194,23 @@ def test_long_context_split_merge():
     assert a[0] == b[0]
     for r in range(len(reqs)):
         assert np.array_equal(a[3][r], b[3][r]), r
-    ora = T.greedy_kv(T.Weights(spec, seed), reqs, "bf16", record_logits=True)
-    worst = 0.0
-    for r, q in enumerate(reqs):
-        for t in range(q.output_len):
-            if a[0][r][t] != ora.tokens[r][t]:
-                assert ora.margins[r][t] <= 2 * TOL, (r, t)
-                break
-            worst = max(worst, float(np.abs(a[3][r][t] - ora.logits[r][t]).max()))
-    assert worst <= TOL, worst
+    Wl = T.Weights(spec, seed)
+    ora = T.greedy_kv(Wl, reqs, "bf16", record_logits=True)
+    compare_free_running("long-ctx", a[0], a[3], ora, TOL, decoder_only_tf(Wl, reqs), max_near_ties=1)
     ctx.close()
+
+
+def test_dynamic_adjustment_narrow_inputs_stays_in_capacity(setup):
+    """with every input the same length, the dynamic
+    adjustment admits more than B_E rows (B_E' up to B_D); the encode tables
+    and workspace are sized for that, the token sum never exceeds B_E x the
+    longest input, and results stay bit-identical to the plain schedule."""
+    X, T, spec, W, reqs, ctx, ora = setup
+    from workload import make_requests, uniform_pmf
+    same = make_requests(40, uniform_pmf(20, 20), uniform_pmf(1, 12), spec.vocab, 91)
+    a = ctx.run(X.rra_schedule(4, 10, 3), same, dump=range(len(same)))
+    b = ctx.run(X.rra_schedule(4, 10, 3), same, dump=range(len(same)), dyn_threshold=0.1)
+    assert a[0] == b[0]
+    for r in range(len(same)):
+        assert np.array_equal(a[3][r], b[3][r]), r
+    assert b[2]["encode_phases"] >= len(same) // 10
