@@ -47,6 +47,10 @@ WORKLOAD = ("config 2: OPT-13B (seeded random init), task S (in 256+-252<=512, o
 MODEL = "opt-13b"
 CONFIG_NO = 2
 B_E_MAX = 64
+# XProfiler sweep axes: batch, context, tokens
+PROFILE_BATCH = [1, 2, 4, 8, 16, 32, 48, 64, 96, 128, 160, 192, 224, 256, 320, 384, 448, 512]
+PROFILE_CTX = [1, 32, 64, 128, 192, 256, 320, 384, 448, 512, 592]
+PROFILE_TOKENS = [1, 16, 64, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768]
 
 
 def peaks():
@@ -105,28 +109,148 @@ class Clocks:
 
 # ----------------------------------------------------------------------------
 # CPU baseline: the oracle as it stands (test infrastructure) on a bounded
-# sample of the same workload.
+# sample of the same workload -- a measured per-layer cost model of oracle
+# mode (iii)'s batched KV loop (SURVEY.md §8(d) "Oracle timing").
 # ----------------------------------------------------------------------------
-def oracle_sample_setup(n_layers_sample=2):
-    from oracle import transformer as T
-    from workload import MODELS, ModelSpec, Request, make_requests, task_dists, weight_seed
-    full = MODELS[MODEL]
-    spec = ModelSpec(full.name + "-first%dlayers" % n_layers_sample, full.arch, 0, n_layers_sample, full.d_model,
-                     full.n_heads, full.d_head, full.d_ff, full.vocab, full.max_pos)
-    W = T.Weights(spec, weight_seed(CONFIG_NO), cache_fp64=False)
-    for l in range(n_layers_sample):
-        W.layer(l)                                  # generate outside the timed region
-    d = task_dists(TASK)
-    r = make_requests(1, d.pmf_in, d.pmf_out, full.vocab, 0xE6E1_0000 + CONFIG_NO)[0]
-    req = Request(r.ids[:64], min(64, r.input_len), 4)
-    return T, W, req, full.n_dec_layers / n_layers_sample
+CPU_REQUESTS = 32
 
 
-def oracle_sample_step(T, W, req, scale):
+class OracleCostModel:
+    """Oracle mode (iii) (oracle/transformer.py KVLoop, bf16-emulating, fp64
+    accumulation) running CPU_REQUESTS task-S requests batched exactly as
+    KVLoop.run does -- one encode forward over every request's input tokens,
+    then decode iterations over the still-active rows -- through all L = 40
+    OPT-13B layers.  Every layer has the same shapes, so the run's time is
+
+        L * [enc(T_E) + sum_u dec(b_u)] + sum_u head(b_u)
+
+    with b_u the rows alive at iteration u.  enc / dec / head are measured on
+    the host with the oracle's own functions (KVLoop._layer on layer 0,
+    KVLoop._logits): enc per encoded token on a packed sample of requests,
+    dec and head at two batch sizes (linear in b).  Weight generation is
+    outside the timed region (a CPU server holds its weights)."""
+
+    def __init__(self, n_enc_sample=4):
+        from oracle import transformer as T
+        from workload import MODELS, ModelSpec, make_requests, task_dists, weight_seed
+        full = MODELS[MODEL]
+        self.L = full.n_dec_layers
+        spec = ModelSpec(full.name + "-layer0", full.arch, 0, 1, full.d_model, full.n_heads, full.d_head,
+                         full.d_ff, full.vocab, full.max_pos)
+        self.T = T
+        self.W = T.Weights(spec, weight_seed(CONFIG_NO), cache_fp64=False)
+        self.W.layer(0)                                     # generated outside the timed region
+        d = task_dists(TASK)
+        self.reqs = make_requests(CPU_REQUESTS, d.pmf_in, d.pmf_out, full.vocab, 0xE6E1_0000 + CONFIG_NO)
+        self.loop = T.KVLoop(self.W, "bf16")
+        self.sample = self.reqs[:n_enc_sample]
+        H, dh = spec.n_heads, spec.d_head
+        toks, rows = [], []
+        for r, q in enumerate(self.sample):
+            for p in range(q.input_len - 1):
+                toks.append(int(q.ids[p]))
+                rows.append((r, p))
+        self.enc_rows, self.enc_toks = rows, np.array(toks)
+        self.mk = lambda: {r: ([np.zeros((H, 0, dh))], [np.zeros((H, 0, dh))]) for r in range(len(self.sample))}
+        self.base_caches = self.mk()
+        x = self.loop._forward(self.enc_toks, rows, self.base_caches)     # caches for the decode measurement
+        del x
+
+    def _dec_caches(self, b):
+        return {i: ([self.base_caches[i % len(self.sample)][0][0].copy()],
+                    [self.base_caches[i % len(self.sample)][1][0].copy()]) for i in range(b)}
+
+    def measure(self, b_lo=8, b_hi=CPU_REQUESTS):
+        """One bounded sample: returns (modeled tok/s, modeled seconds, measured CPU seconds, detail)."""
+        loop, W = self.loop, self.W
+        t_all = time.perf_counter()
+        # encode: layer 0 over the sample's packed input tokens
+        pos = np.array([p for _, p in self.enc_rows])
+        x = loop.R.f32(W.emb_rows(self.enc_toks) + W.pos_emb[pos])
+        t0 = time.perf_counter()
+        loop._layer(0, x, self.enc_rows, self.mk())
+        c_enc = (time.perf_counter() - t0) / len(self.enc_rows)
+        dec, head = {}, {}
+        for b in (b_lo, b_hi):
+            caches = self._dec_caches(b)
+            rows = [(i, self.sample[i % len(self.sample)].input_len - 1) for i in range(b)]
+            toks = np.array([int(self.sample[i % len(self.sample)].ids[-1]) for i in range(b)])
+            xd = loop.R.f32(W.emb_rows(toks) + W.pos_emb[np.array([p for _, p in rows])])
+            t0 = time.perf_counter()
+            xo = loop._layer(0, xd, rows, caches)
+            dec[b] = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            loop._logits(xo)
+            head[b] = time.perf_counter() - t0
+        lin = lambda f, b: f[b_lo] + (f[b_hi] - f[b_lo]) * (b - b_lo) / (b_hi - b_lo)
+        T_E = sum(q.input_len - 1 for q in self.reqs)
+        S = [q.output_len for q in self.reqs]
+        b_u = [sum(1 for s in S if s >= u) for u in range(1, max(S) + 1)]
+        t_model = self.L * (c_enc * T_E + sum(lin(dec, b) for b in b_u)) + sum(lin(head, b) for b in b_u)
+        cpu_s = time.perf_counter() - t_all
+        detail = {"enc_s_per_token_layer": c_enc, "dec_layer_s": {str(k): v for k, v in dec.items()},
+                  "head_s": {str(k): v for k, v in head.items()}, "encode_tokens": T_E, "decode_iters": len(b_u),
+                  "modeled_run_s": t_model}
+        return sum(S) / t_model, t_model, cpu_s, detail
+
+
+def cpu_info():
+    """Host description for the CPU baseline: lscpu model, usable cores, BLAS
+    library and its thread count."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    blas = []
+    try:
+        import threadpoolctl
+        np.ones((64, 64)) @ np.ones((64, 64))
+        blas = [{"api": i.get("internal_api"), "threads": i.get("num_threads"), "version": i.get("version")}
+                for i in threadpoolctl.threadpool_info()]
+    except Exception:
+        pass
+    return {"cpu_model": model, "cores": cpu_cores(), "blas": blas}
+
+
+def cpu_baseline_block(cm: "OracleCostModel", value, model_s, cpu_s, detail):
+    info = cpu_info()
+    threads = max([b["threads"] or 0 for b in info["blas"]] or [1])
+    return {"value": value, "unit": "output tokens/s", "cores": threads or info["cores"], "kind": "oracle",
+            "sample": ("per-layer cost model of oracle mode (iii)'s batched KV loop over %d task-S requests "
+                       "(%d encode tokens, %d decode iterations) through all %d OPT-13B layers + LM head: "
+                       "layer-0 encode / decode / head measured on the host (%.1f s of CPU work), modeled run "
+                       "%.0f s" % (CPU_REQUESTS, detail["encode_tokens"], detail["decode_iters"], cm.L, cpu_s,
+                                   model_s)),
+            "host": info, "measured": detail}
+
+
+def scheduler_wall_times(X, prof, ctx, cl, pin, pout, d, L_b, args):
+    """exg_schedule_find (C++) vs oracle/bnb.schedule_find (Python) on the
+    same profile-v1 file, bound and options; also checks they agree (S15)."""
+    import tempfile
+    from oracle import bnb, simulator as sim
+    from workload import MODELS
+    with tempfile.TemporaryDirectory() as tmp:
+        path = os.path.join(tmp, "p.txt")
+        prof.save(path)
+        P = sim.Profile.load(path)
+    S = sim.Simulator(P, sim.SimModel.from_spec(MODELS[MODEL]), sim.SimCluster(cl.n_gpus, cl.mem_per_gpu_bytes,
+                                                                             cl.workspace_bytes),
+                      d.pmf_in, d.pmf_out, d.target_len, use_little_fraction=bool(args.little))
     t0 = time.perf_counter()
-    T.greedy_kv(W, [req], "bf16")
-    dt = time.perf_counter() - t0
-    return req.output_len / (dt * scale), dt
+    s_c, e_c = X.schedule_find(prof, ctx.mspec, cl, pin, pout, d.target_len, L_b * (1 - args.margin), X.EXG_RRA,
+                               X.search_opts(b_e_max=B_E_MAX, little=args.little))
+    t_c = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    f = bnb.schedule_find(S, L_b * (1 - args.margin), sim.RRA, bnb.SearchOpts(b_e_max=B_E_MAX,
+                                                                              use_little_fraction=bool(args.little)))
+    t_py = time.perf_counter() - t0
+    same = f is not None and (f.schedule.b_e, f.schedule.n_d, f.estimate.thrput_seq_s) == (
+        s_c.b_e, s_c.n_d, e_c.thrput_seq_s)
+    return {"cpp": t_c, "python_oracle": t_py, "evals": int(e_c.perf_evals), "identical_choice": bool(same)}
 
 
 def cpu_cores():
@@ -261,9 +385,7 @@ def run_layout(args, rank, world, local):
     if rank == 0:
         ctx1 = X.Context(spec, weight_seed(CONFIG_NO), device=local,
                          cluster=X.cluster_spec(1, total - (6 << 30), 8 << 30))
-        prof = ctx1.profile([1, 2, 4, 8, 16, 32, 48, 64, 96, 128, 160, 192, 224, 256, 320, 384, 448, 512],
-                            [1, 32, 64, 128, 192, 256, 320, 384, 448, 512, 592],
-                            [1, 16, 64, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768], reps=3, tps=[1, 2, 4, 8])
+        prof = ctx1.profile(PROFILE_BATCH, PROFILE_CTX, PROFILE_TOKENS, reps=3, tps=[1, 2, 4, 8])
         prof.comm_model(COMM_ALPHA_S, COMM_BW)
         L_head = dict(static_bounds(X, prof, ctx1.mspec, ctx1.cluster, pin, pout, d.target_len))["p70"]
         cl_n = X.cluster_spec(world, ctx1.cluster.mem_per_gpu_bytes, ctx1.cluster.workspace_bytes)
@@ -313,28 +435,28 @@ def run_layout(args, rank, world, local):
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle (CPU, float64, bf16-emulating KV loop) on
-    a bounded sample of the workload; rank 0 only."""
+    """--impl reference: the oracle (CPU, float64, bf16-emulating KV loop)
+    timed by its per-layer cost model on a bounded sample per step (see
+    OracleCostModel); rank 0 only."""
     if rank != 0:
         return
-    T, W, req, scale = oracle_sample_setup()
+    cm = OracleCostModel()
     for _ in range(args.warmup):
-        oracle_sample_step(T, W, req, scale)
-    vals, times = [], []
+        cm.measure()
+    vals, times, last = [], [], None
     for _ in range(args.steps):
-        v, dt = oracle_sample_step(T, W, req, scale)
+        v, model_s, cpu_s, detail = cm.measure()
         vals.append(v)
-        times.append(dt)
+        times.append(model_s)
+        last = (v, model_s, cpu_s, detail)
     value = float(np.mean(vals))
-    sample = ("1 task-S request (64 input tokens, 4 output tokens) through the first 2 of 40 OPT-13B layers "
-              "(same seeded weights) + embeddings + LM head, oracle mode (iii); tokens/s scaled by 2/40")
+    cpu = cpu_baseline_block(cm, value, *last[1:])
     out = {"metric": METRIC, "value": value, "unit": "output tokens/s",
            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * float(np.mean(times)), "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "oracle_sample": "first 2 of 40 layers, scaled by 2/40"},
-           "cpu_baseline": {"value": value, "unit": "output tokens/s", "cores": cpu_cores(), "kind": "oracle",
-                            "sample": sample},
+           "config": {"workload": WORKLOAD, "oracle_sample": cpu["sample"]},
+           "cpu_baseline": cpu,
            "e2e": {"value": value, "unit": "output tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
 
@@ -402,11 +524,8 @@ def main():
                     cluster=X.cluster_spec(1, total - (6 << 30), 8 << 30))
     t_weights = time.perf_counter() - t_setup
     # XProfiler sweep
-    batch = [1, 2, 4, 8, 16, 32, 48, 64, 96, 128, 160, 192, 224, 256, 320, 384, 448, 512]
-    ctxs = [1, 32, 64, 128, 192, 256, 320, 384, 448, 512, 592]
-    tokens = [1, 16, 64, 256, 512, 1024, 2048, 4096, 8192, 16384, 32768]
     t0 = time.perf_counter()
-    prof = ctx.profile(batch, ctxs, tokens, reps=3, tps=[1, 2, 4, 8])
+    prof = ctx.profile(PROFILE_BATCH, PROFILE_CTX, PROFILE_TOKENS, reps=3, tps=[1, 2, 4, 8])
     # interconnect tables: alpha-beta model of NVLink 5 / NVSwitch (DESIGN.md
     # reading; a single-GPU context cannot time them)
     prof.comm_model(COMM_ALPHA_S, COMM_BW)
@@ -578,12 +697,11 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        T, W, req, scale = oracle_sample_setup()
-        v, dt = oracle_sample_step(T, W, req, scale)
-        cpu = {"value": v, "unit": "output tokens/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": "1 task-S request (64 in, 4 out) through the first 2 of 40 OPT-13B layers + "
-                         "embeddings + LM head, oracle mode (iii) on the host; tokens/s scaled by 2/40 "
-                         "(%.1f s of CPU work)" % dt}
+        cm = OracleCostModel()
+        cpu = cpu_baseline_block(cm, *cm.measure())
+        # scheduler wall time, Python oracle vs the C++ planner, on the same
+        # profile file and bound (PAPER.md:637 reports 3 s - 5 min for its own)
+        cpu["schedule_find_s"] = scheduler_wall_times(X, prof, ctx, cl, pin, pout, d, L_head, args)
 
     if rank == 0:
         out = {

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EXG_ABI_VERSION 2
+#define EXG_ABI_VERSION 3
 
 typedef enum {
   EXG_OK = 0,
@@ -138,6 +138,16 @@ typedef struct {
                                  sum is kept within +-threshold of B_E' x the
                                  mean encoded length and never above B_E x the
                                  longest input (the encode workspace); 0 = off */
+  /* optional per-stage trace (single-GPU runs; simulator-fidelity and Table 9
+   * analyses): one record of 5 doubles per encode phase that admitted
+   * requests and per decode iteration, in time order --
+   *   {kind (1 encode, 2 decode), start [s from the run's first event],
+   *    duration [s], rows (admitted requests | decode batch),
+   *    work (encoded tokens | sum of attention keys)};
+   * at most trace_cap records are written (their count is
+   * exg_run_stats.trace_records). */
+  double* trace_out;
+  int32_t trace_cap;
 } exg_run_opts;
 
 /* Kernel classes timed when exg_run_opts.kernel_timing = 1.  Work is the
@@ -168,6 +178,7 @@ typedef struct {
    * the 99th percentile of |t - mean| of encode phases and decode iterations */
   double enc_stage_mean_s, enc_stage_p99dev_s, dec_stage_mean_s, dec_stage_p99dev_s;
   double mean_encode_batch;            /* requests per encode phase (admissions)  */
+  int64_t trace_records;               /* records written to exg_run_opts.trace_out */
 } exg_run_stats;
 
 typedef struct exg_ctx exg_ctx;           /* one per rank: device state + comms */

@@ -67,9 +67,30 @@ def dec_slot(l: int) -> int:
     return 1001 + l
 
 
+_CHUNK = 1 << 22
+
+
 def gen_values(seed: int, tid: int, n: int, kind: str, start: int = 0) -> np.ndarray:
     """n consecutive values (indices start..start+n-1) of tensor `tid`, as
-    float32 arrays holding bf16-exact values."""
+    float32 arrays holding bf16-exact values.  Large tensors are generated in
+    index chunks on a thread pool (every value depends on its own index only,
+    so the result is the same array)."""
+    if n > 2 * _CHUNK:
+        import concurrent.futures as cf
+        import os
+        out = np.empty(n, np.float32)
+
+        def job(s):
+            e = min(n, s + _CHUNK)
+            out[s:e] = _gen_values(seed, tid, e - s, kind, start + s)
+
+        with cf.ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1))) as ex:
+            list(ex.map(job, range(0, n, _CHUNK)))
+        return out
+    return _gen_values(seed, tid, n, kind, start)
+
+
+def _gen_values(seed: int, tid: int, n: int, kind: str, start: int) -> np.ndarray:
     i = np.arange(start, start + n, dtype=np.uint64)
     key = np.uint64(seed) ^ (np.uint64(tid) << np.uint64(40))
     h = splitmix64(key ^ i)

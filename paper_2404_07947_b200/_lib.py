@@ -87,7 +87,7 @@ class exg_request(C.Structure):
 class exg_run_opts(C.Structure):
     _fields_ = [("logits_out", C.POINTER(C.c_float)), ("dump_mask", C.POINTER(C.c_uint8)),
                 ("slot_ctx", C.c_int32), ("pin_nccl_algo", C.c_int32), ("kernel_timing", C.c_int32),
-                ("dyn_threshold", C.c_double)]
+                ("dyn_threshold", C.c_double), ("trace_out", C.POINTER(C.c_double)), ("trace_cap", C.c_int32)]
 
 
 K_CLASSES = ["prefill_gemm", "decode_gemm", "decode_attn", "prefill_attn"]
@@ -102,7 +102,7 @@ class exg_run_stats(C.Structure):
                 ("k_work", C.c_double * 4), ("k_launches", C.c_int64 * 4),
                 ("enc_stage_mean_s", C.c_double), ("enc_stage_p99dev_s", C.c_double),
                 ("dec_stage_mean_s", C.c_double), ("dec_stage_p99dev_s", C.c_double),
-                ("mean_encode_batch", C.c_double)]
+                ("mean_encode_batch", C.c_double), ("trace_records", C.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("k_")}
@@ -162,7 +162,7 @@ _SIGS = {
 }
 
 _lib = None
-ABI_VERSION = 2   # include/exegpt.h EXG_ABI_VERSION
+ABI_VERSION = 3   # include/exegpt.h EXG_ABI_VERSION
 
 
 def lib():
@@ -262,9 +262,10 @@ class Context:
         return Profile(h)
 
     def run(self, sched: exg_schedule, requests, dump: Optional[Sequence[int]] = None, slot_ctx: int = 0,
-            kernel_timing: bool = False, dyn_threshold: float = 0.0):
+            kernel_timing: bool = False, dyn_threshold: float = 0.0, trace: Optional[list] = None):
         """Returns (tokens per request, latencies [s], stats dict, logits per
-        dumped request [S_r][V] or None)."""
+        dumped request [S_r][V] or None).  trace: a list that receives the
+        per-stage records [kind, start, duration, rows, work] (exegpt.h)."""
         n = len(requests)
         keep = []
         reqs = (exg_request * n)()
@@ -277,6 +278,12 @@ class Context:
         lat = np.zeros(n, dtype=np.float64)
         stats = exg_run_stats()
         opts = exg_run_opts(None, None, slot_ctx, 0, int(kernel_timing), float(dyn_threshold))
+        tbuf = None
+        if trace is not None:
+            cap = 8 * (n + 16) + 4 * total
+            tbuf = np.zeros((cap, 5), dtype=np.float64)
+            opts.trace_out = tbuf.ctypes.data_as(C.POINTER(C.c_double))
+            opts.trace_cap = cap
         logits = None
         if dump is not None:
             mask = np.zeros(n, dtype=np.uint8)
@@ -288,6 +295,8 @@ class Context:
             opts.dump_mask = mask.ctypes.data_as(C.POINTER(C.c_uint8))
         check(lib().exg_run(self.h, C.byref(sched), reqs, n, out.ctypes.data_as(C.POINTER(C.c_int32)),
                             lat.ctypes.data_as(C.POINTER(C.c_double)), C.byref(stats), C.byref(opts)))
+        if trace is not None:
+            trace.extend(tbuf[:int(stats.trace_records)].tolist())
         toks, off = [], 0
         for r in requests:
             toks.append(out[off:off + r.output_len].tolist())

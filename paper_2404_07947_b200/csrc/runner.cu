@@ -174,14 +174,19 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   std::vector<cudaEvent_t> evs;
   std::vector<int> ev_kind;        // 0 = phase start, 1 = encode end, 2 = iteration end
   std::vector<int> ev_tokens;      // tokens emitted by the iteration ending at this event
+  std::vector<int> ev_rows;        // trace: decode batch of the iteration ending here
+  std::vector<double> ev_work;     // trace: encoded tokens / attention keys of the stage ending here
   auto record = [&](int kind, int toks) {
     cudaEvent_t e = evp.get();
     EXG_CUDA(cudaEventRecord(e, st));
     evs.push_back(e);
     ev_kind.push_back(kind);
     ev_tokens.push_back(toks);
+    ev_rows.push_back(0);
+    ev_work.push_back(0.0);
     return (int)evs.size() - 1;
   };
+  int enc_T = 0;
 
   int next_req = 0;
   double mean_enc_tokens = 0, steady_batch_sum = 0;
@@ -275,11 +280,16 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       eb.rslot = eb.cu + admit + 1;
       eb.pos0 = eb.rslot + admit;
       E.encode(eb);
+      enc_T = T;
       next_req += admit;
       ++encode_phases;
       ++admitted_phases;
     }
-    record(1, admit);   // tokens field of an encode-end event: requests admitted
+    {
+      const int k_end = record(1, admit);   // tokens field of an encode-end event: requests admitted
+      ev_rows[k_end] = admit;
+      ev_work[k_end] = admit > 0 ? enc_T : 0;
+    }
     // ---------------- N_D decode iterations ----------------
     for (int u = 0; (ft || u < s.n_d) && !active.empty(); ++u) {
       const int B = (int)active.size();
@@ -344,6 +354,8 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         }
       }
       const int ev_it = record(2, live);
+      ev_rows[ev_it] = B;
+      ev_work[ev_it] = sum_keys;
       ++decode_iters;
       batch_sum += B;
       if (next_req < n) {   // decode batch average while requests keep arriving (not the drain)
@@ -408,8 +420,22 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   int64_t kn[EXG_K_CLASSES] = {0};
   E.collect_kernel_timing(kt, kw, kn);
   E.set_kernel_timing(false);
+  int64_t n_trace = 0;
+  if (opts && opts->trace_out && opts->trace_cap > 0) {
+    for (int k = 1; k < nev && n_trace < opts->trace_cap; ++k) {
+      const bool enc = ev_kind[k] == 1 && ev_rows[k] > 0, dec = ev_kind[k] == 2;
+      if (!enc && !dec) continue;
+      double* rec = opts->trace_out + 5 * n_trace++;
+      rec[0] = enc ? 1 : 2;
+      rec[1] = t[k - 1];
+      rec[2] = t[k] - t[k - 1];
+      rec[3] = ev_rows[k];
+      rec[4] = ev_work[k];
+    }
+  }
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
+    stats->trace_records = n_trace;
     stats->kernel_launches = launches;
     for (int c = 0; c < EXG_K_CLASSES; ++c) {
       stats->k_time_s[c] = kt[c];

@@ -85,17 +85,112 @@ def test_opt13b_width_sampled_parity_in_bench_configuration(X, simt):
     assert len(near_ties) <= 1, near_ties
 
 
-def test_opt13b_full_depth_batch_invariance(X):
+@pytest.fixture(scope="module")
+def full_depth(X):
+    """All 40 layers of OPT-13B on 24 task-S requests under two schedules
+    that put the requests in different batches."""
     from workload import MODELS, weight_seed
     reqs = _bench_requests(24)
     ctx = X.Context(MODELS["opt-13b"], weight_seed(2))
     dump = [0, 11, 23]
     a = ctx.run(X.rra_schedule(4, 8, 2), reqs, dump=dump, slot_ctx=592)
     b = ctx.run(X.rra_schedule(24, 24, 8), reqs, dump=dump, slot_ctx=592)
+    ctx.close()
+    return reqs, dump, a, b
+
+
+def test_opt13b_full_depth_batch_invariance(full_depth):
+    reqs, dump, a, b = full_depth
     assert a[0] == b[0]
     for r in dump:
         assert np.array_equal(a[3][r], b[3][r]), r
         assert np.all(np.isfinite(a[3][r]))
+
+
+def _teacher_forced_layerwise(spec, seed, reqs, forced, accums=("fp64", "fp32")):
+    """Oracle mode (iii) logits of every decode step of each request with the
+    decode inputs forced to forced[r] (the GPU's own tokens), for each
+    accumulation in `accums`.  One causal forward over each whole sequence
+    x[0..n-1] + forced[0..S-2] -- the decode step t's logits are those of the
+    row at position n-1+t (a row depends only on its own prefix) -- run layer
+    by layer: each layer's weights are generated (T3), used for every
+    sequence and both accumulations, then dropped, so a 40-layer OPT-13B
+    never has to sit in host memory."""
+    from oracle import transformer as T
+    W = T.Weights(spec, seed, cache_fp64=False)
+    toks, rows, out_rows = [], [], []
+    for r, q in enumerate(reqs):
+        seq = [int(v) for v in q.ids] + [int(v) for v in forced[r][:q.output_len - 1]]
+        for p, v in enumerate(seq):
+            if p >= q.input_len - 1:
+                out_rows.append(len(toks))
+            toks.append(v)
+            rows.append((r, p))
+    res = {}
+    loops = {a: T.KVLoop(W, "bf16", a) for a in accums}
+    H, dh, nL = spec.n_heads, spec.d_head, spec.n_dec_layers
+    caches = {a: {r: ([None] * nL, [None] * nL) for r in range(len(reqs))} for a in accums}
+    for a in accums:
+        for r in range(len(reqs)):
+            for l in range(nL):
+                caches[a][r][0][l] = np.zeros((H, 0, dh))
+                caches[a][r][1][l] = np.zeros((H, 0, dh))
+    R = loops[accums[0]].R
+    pos = np.array([p for _, p in rows])
+    x0 = R.f32(W.emb_rows(np.array(toks)) + W.pos_emb[pos])
+    xs = {a: x0.copy() for a in accums}
+    for l in range(nL):
+        for a in accums:
+            xs[a] = loops[a]._layer(l, xs[a], rows, caches[a])
+            for r in range(len(reqs)):      # keys of earlier layers are not needed again
+                caches[a][r][0][l] = caches[a][r][1][l] = None
+        W._layers.pop(l, None)
+    for a in accums:
+        lg = loops[a]._logits(xs[a][out_rows])
+        k, res[a] = 0, []
+        for q in reqs:
+            res[a].append([lg[k + t] for t in range(q.output_len)])
+            k += q.output_len
+    return res
+
+
+def test_opt13b_full_depth_vs_oracle(full_depth):
+    """All 40 layers of OPT-13B (the bench's model, task-S requests) vs oracle
+    mode (iii) on two sampled requests, weights regenerated per layer:
+    the oracle is teacher-forced on the GPU's tokens (so a near tie early on
+    does not end the comparison); every step's GPU id must be the oracle's
+    argmax or a recorded near tie, and every step's logits lie within the
+    calibrated bar max(2e-2, 2 x the oracle's own fp32-vs-fp64 accumulation
+    spread at this depth) -- DESIGN.md §9."""
+    from oracle import transformer as T
+    from workload import MODELS, Request, weight_seed
+    reqs, dump, a, _ = full_depth
+    sample = dump[:2]
+    steps = 8
+    sreqs = [Request(reqs[r].ids, reqs[r].input_len, min(steps, reqs[r].output_len)) for r in sample]
+    forced = [a[0][r][:sreqs[i].output_len] for i, r in enumerate(sample)]
+    tf = _teacher_forced_layerwise(MODELS["opt-13b"], weight_seed(2), sreqs, forced)
+    ev = []
+    for i, r in enumerate(sample):
+        ora, o32 = tf["fp64"][i], tf["fp32"][i]
+        cal = max(float(np.abs(o32[t] - ora[t]).max()) for t in range(len(ora)))
+        tol = max(TOL, 2 * cal)
+        worst = 0.0
+        for t in range(len(ora)):
+            worst = max(worst, float(np.abs(a[3][r][t] - ora[t]).max()))
+            y, yo = a[0][r][t], int(np.argmax(ora[t]))
+            if y != yo:
+                m = float(np.sort(ora[t])[-1] - np.sort(ora[t])[-2])
+                assert m <= 2 * tol, "hard mismatch req %d step %d (margin %.4g)" % (r, t, m)
+                assert ora[t][y] >= ora[t].max() - 2 * tol
+                ev.append(("opt13b-40L req %d" % r, 0, t, m))
+                print("NEAR-TIE opt13b 40 layers: request %d step %d margin %.3g" % (r, t, m))
+        print("OPT-13B 40 layers req %d (n=%d): gpu-vs-oracle max %.4g, oracle fp32-vs-fp64 %.4g, bar %.4g"
+              % (r, reqs[r].input_len, worst, cal, tol))
+        assert worst <= tol, (r, worst, tol)
+    from parity import NEAR_TIES
+    NEAR_TIES.extend(ev)
+    assert len(ev) <= 2
 
 
 # ---------------------------------------------------------------------------

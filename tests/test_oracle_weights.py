@@ -43,3 +43,15 @@ def test_distinct_tensors_decorrelated():
     a = wg.gen_values(7, wg.tensor_id(1001, "W_o"), 50000, "W_o").astype(np.float64)
     b = wg.gen_values(7, wg.tensor_id(1002, "W_o"), 50000, "W_o").astype(np.float64)
     assert abs(np.corrcoef(a, b)[0, 1]) < 0.02
+
+
+def test_chunked_generation_is_the_same_array(monkeypatch):
+    """gen_values splits large tensors into index chunks on a thread pool;
+    every value depends on its own index only, so the array is unchanged."""
+    import numpy as np
+    from oracle import weights as wgen
+    ref = wgen._gen_values(7, 12345, 100_003, "W_1", 17)
+    monkeypatch.setattr(wgen, "_CHUNK", 1000)
+    assert np.array_equal(wgen.gen_values(7, 12345, 100_003, "W_1", 17), ref)
+    ref_g = wgen._gen_values(7, 99, 50_001, "ln1_g", 0)
+    assert np.array_equal(wgen.gen_values(7, 99, 50_001, "ln1_g"), ref_g)
