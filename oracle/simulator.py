@@ -8,6 +8,8 @@ Readings (listed in DESIGN.md):
   the last (=> infeasible);
 * layer time = attn + rest + k * tp_sync, k = 2 all-reduces per layer
   (PAPER.md:109; 3 for a T5 decoder layer), messages in fp32 (T4(i));
+* decode stage time of the last stage + head(b): final norm, LM head and
+  argmax once per iteration (profile table `head`, when present);
 * RRA timeline via the pipeline algebra F/Pi (S6), P micro-batches;
 * WAA timeline (S7): throughput = B_E / max(T_E, T_D); latency =
   T_E^trav + T_handoff + T_E + (S-1) Pi + F;
@@ -62,6 +64,7 @@ class Profile:
     rest: Dict[Tuple[str, int], Table1D] = field(default_factory=dict)
     tp_sync: Dict[int, Table1D] = field(default_factory=dict)
     pp_sync: Optional[Table1D] = None
+    head: Optional[Table1D] = None     # decode head (final norm + LM head + argmax) vs batch
 
     def save(self, path: str):
         with open(path, "w") as f:
@@ -87,6 +90,10 @@ class Profile:
             out.append("pp_sync %d" % len(self.pp_sync.x))
             out.append(" ".join(g(v) for v in self.pp_sync.x))
             out.append(" ".join(g(v) for v in self.pp_sync.t))
+        if self.head is not None:
+            out.append("head %d" % len(self.head.x))
+            out.append(" ".join(g(v) for v in self.head.x))
+            out.append(" ".join(g(v) for v in self.head.t))
         out.append("end")
         return "\n".join(out) + "\n"
 
@@ -127,6 +134,10 @@ class Profile:
                 n = int(nxt())
                 x = [float(nxt()) for _ in range(n)]
                 p.pp_sync = Table1D(x, [float(nxt()) for _ in range(n)])
+            elif kw == "head":
+                n = int(nxt())
+                x = [float(nxt()) for _ in range(n)]
+                p.head = Table1D(x, [float(nxt()) for _ in range(n)])
             else:
                 raise ValueError("bad keyword %r" % kw)
 
@@ -336,6 +347,10 @@ class Simulator:
             if k < P - 1:
                 toks = b * self.s_e if phase == "enc" else b
                 v += self._pp_sync(toks * self.m.d_model * 2.0)
+            if phase == "dec" and k == P - 1 and self.p.head is not None:
+                # the decode head (final norm + LM head + argmax) runs once per
+                # iteration on the last stage (DESIGN.md reading)
+                v += interp1(self.p.head.x, self.p.head.t, b)
             out.append(v)
         return out
 

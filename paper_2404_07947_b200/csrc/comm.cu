@@ -34,7 +34,35 @@ class NcclComm final : public Comm {
     EXG_NCCL(ncclCommInitRank(&comm_, world, id, rank));
   }
   ~NcclComm() override {
+    for (auto& kv : sub_)
+      if (kv.second) ncclCommDestroy(kv.second);
     if (comm_) ncclCommDestroy(comm_);
+  }
+  void prepare_groups(const std::vector<std::vector<int>>& groups) override {
+    for (const auto& g : groups) {
+      if (g.size() < 2 || sub_.count(g)) continue;
+      bool member = false;
+      for (int r : g) member |= r == rank_;
+      // every rank takes part in the split; non-members get no communicator
+      ncclComm_t c = nullptr;
+      EXG_NCCL(ncclCommSplit(comm_, member ? split_color(g) : NCCL_SPLIT_NOCOLOR, rank_, &c, nullptr));
+      sub_[g] = c;
+    }
+  }
+  bool has_allreduce() const override { return true; }
+  void allreduce_sum(float* buf, size_t n, const std::vector<int>& group, cudaStream_t st) override {
+    auto it = sub_.find(group);
+    if (it == sub_.end() || !it->second) throw std::logic_error("NCCL: TP group was not prepared");
+    EXG_NCCL(ncclAllReduce(buf, buf, n, ncclFloat32, ncclSum, it->second, st));
+  }
+  void check_async() override {
+    auto one = [](ncclComm_t c) {
+      ncclResult_t a = ncclSuccess;
+      if (c && ncclCommGetAsyncError(c, &a) == ncclSuccess && a != ncclSuccess && a != ncclInProgress)
+        throw std::runtime_error(std::string("NCCL async error: ") + ncclGetErrorString(a));
+    };
+    one(comm_);
+    for (auto& kv : sub_) one(kv.second);
   }
   int rank() const override { return rank_; }
   int world() const override { return world_; }
@@ -48,8 +76,15 @@ class NcclComm final : public Comm {
   }
 
  private:
+  // the same color on every member: a hash of the member list
+  static int split_color(const std::vector<int>& g) {
+    uint32_t h = 2166136261u;
+    for (int r : g) h = (h ^ (uint32_t)r) * 16777619u;
+    return (int)(h & 0x3fffffff);
+  }
   ncclComm_t comm_ = nullptr;
   int rank_, world_;
+  std::map<std::vector<int>, ncclComm_t> sub_;
 };
 }  // namespace
 

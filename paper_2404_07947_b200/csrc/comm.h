@@ -20,6 +20,8 @@
 #include <cstddef>
 #include <cstdint>
 #include <memory>
+#include <stdexcept>
+#include <vector>
 
 namespace exg {
 
@@ -31,6 +33,21 @@ struct Comm {
   virtual void group_end() = 0;
   virtual void send(const void* buf, size_t bytes, int peer, cudaStream_t st) = 0;
   virtual void recv(void* buf, size_t bytes, int peer, cudaStream_t st) = 0;
+  // Collective over ALL ranks, identical arguments on every rank: set up the
+  // sub-communicators of these rank groups (each ascending, >= 2 ranks) --
+  // the TP groups of a layout.  NCCL: ncclCommSplit.
+  virtual void prepare_groups(const std::vector<std::vector<int>>& groups) { (void)groups; }
+  // Native in-place fp32 sum over a prepared group (called by every member,
+  // on its stream).  Transports without one (has_allreduce() false) leave
+  // the caller to exchange the partials with send / recv.
+  virtual bool has_allreduce() const { return false; }
+  virtual void allreduce_sum(float* buf, size_t n, const std::vector<int>& group, cudaStream_t st) {
+    (void)buf, (void)n, (void)group, (void)st;
+    throw std::logic_error("transport has no native all-reduce");
+  }
+  // Surface asynchronous transport errors (NCCL: ncclCommGetAsyncError of the
+  // communicator and its sub-communicators); throws on error.
+  virtual void check_async() {}
 };
 
 // NCCL communicator over `world` processes (uid from nccl_unique_id on rank 0)

@@ -105,13 +105,61 @@ void sum_tp_parts(const std::vector<Engine*>& ranks, int64_t n, cudaStream_t st)
 // ---------------------------------------------------------------------------
 // Exec: this rank's view of the layout's GPUs
 // ---------------------------------------------------------------------------
+// Staging ring of a transfer direction between ranks: the compute stream
+// and the communication stream hand buffers to each other through events, so
+// a pipeline hop / token return / KV-handoff message travels on the comm
+// stream while the compute stream goes on with the next micro-batch
+// ("overlapping communication with computation").
+struct XferRing {
+  static constexpr int N = 4;
+  void* buf[N] = {};
+  cudaEvent_t ready[N] = {}, done[N] = {};
+  bool used[N] = {};
+  size_t cap = 0;
+  int next = 0;
+  ~XferRing() { release(); }
+  void release() {
+    for (int i = 0; i < N; ++i) {
+      if (done[i]) cudaEventSynchronize(done[i]);
+      if (buf[i]) cudaFree(buf[i]);
+      if (ready[i]) cudaEventDestroy(ready[i]);
+      if (done[i]) cudaEventDestroy(done[i]);
+      buf[i] = nullptr;
+      ready[i] = done[i] = nullptr;
+      used[i] = false;
+    }
+    cap = 0;
+  }
+  int acquire(size_t bytes) {
+    if (bytes > cap) {
+      release();
+      cap = bytes;
+      for (int i = 0; i < N; ++i) {
+        EXG_CUDA(cudaMalloc(&buf[i], cap));
+        EXG_CUDA(cudaEventCreateWithFlags(&ready[i], cudaEventDisableTiming));
+        EXG_CUDA(cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming));
+      }
+    }
+    const int s = next;
+    next = (next + 1) % N;
+    return s;
+  }
+};
+
 struct Exec {
   int me = 0, world = 1, G = 1;
   Comm* comm = nullptr;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;    // compute stream
+  cudaStream_t cst = nullptr;   // communication stream (exchanges between ranks)
+  XferRing* tx = nullptr;       // send staging
+  XferRing* rx = nullptr;       // receive staging
   // one-rank NCCL loopback (transport test): exchanges between this rank's
   // own GPUs still go through ncclSend / ncclRecv to self
   bool loop = false;
+  // parity mode (exg_run_opts.pin_nccl_algo): TP partial sums exchanged and
+  // summed in member order on every rank (bitwise the one-rank sum) instead
+  // of the transport's all-reduce
+  bool pin = false;
   int owner(int gpu) const { return (int)((int64_t)gpu * world / G); }
   bool mine(int gpu) const { return owner(gpu) == me; }
   // bytes from (gpu a, src) to (gpu b, dst); a pointer is only valid on its owner
@@ -129,10 +177,42 @@ struct Exec {
         EXG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
       }
     } else if (oa == me) {
-      comm->send(src, bytes, ob, st);
+      send_async(src, bytes, ob);
     } else if (ob == me) {
-      comm->recv(dst, bytes, oa, st);
+      recv_async(dst, bytes, oa);
     }
+  }
+  // comm stream waits for the compute stream / compute stream for the comm stream
+  void fork() const {
+    EXG_CUDA(cudaEventRecord(ev_fork, st));
+    EXG_CUDA(cudaStreamWaitEvent(cst, ev_fork, 0));
+  }
+  void join() const {
+    EXG_CUDA(cudaEventRecord(ev_join, cst));
+    EXG_CUDA(cudaStreamWaitEvent(st, ev_join, 0));
+  }
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  // src (ready on the compute stream) -> peer, through a send staging buffer
+  void send_async(const void* src, size_t bytes, int peer) const {
+    const int s = tx->acquire(bytes);
+    if (tx->used[s]) EXG_CUDA(cudaStreamWaitEvent(st, tx->done[s], 0));   // its previous send is out
+    EXG_CUDA(cudaMemcpyAsync(tx->buf[s], src, bytes, cudaMemcpyDeviceToDevice, st));
+    EXG_CUDA(cudaEventRecord(tx->ready[s], st));
+    EXG_CUDA(cudaStreamWaitEvent(cst, tx->ready[s], 0));
+    comm->send(tx->buf[s], bytes, peer, cst);
+    EXG_CUDA(cudaEventRecord(tx->done[s], cst));
+    tx->used[s] = true;
+  }
+  // peer -> dst (usable on the compute stream afterwards), through a receive staging buffer
+  void recv_async(void* dst, size_t bytes, int peer) const {
+    const int s = rx->acquire(bytes);
+    if (rx->used[s]) EXG_CUDA(cudaStreamWaitEvent(cst, rx->done[s], 0));   // its previous copy-out is done
+    comm->recv(rx->buf[s], bytes, peer, cst);
+    EXG_CUDA(cudaEventRecord(rx->ready[s], cst));
+    EXG_CUDA(cudaStreamWaitEvent(st, rx->ready[s], 0));
+    EXG_CUDA(cudaMemcpyAsync(dst, rx->buf[s], bytes, cudaMemcpyDeviceToDevice, st));
+    EXG_CUDA(cudaEventRecord(rx->done[s], st));
+    rx->used[s] = true;
   }
 };
 
@@ -168,29 +248,65 @@ struct Stage {
 
   // TP reduction of the pending fp32 partials of `rows` rows, then the
   // residual update of every local member
+  // owner ranks of this TP group (ascending)
+  std::vector<int> ranks(const Exec& X) const {
+    std::vector<int> g;
+    for (int r = 0; r < tp; ++r)
+      if (g.empty() || g.back() != X.owner(gpu(r))) g.push_back(X.owner(gpu(r)));
+    return g;
+  }
+
   void tp_reduce(const Exec& X, int rows, int d) {
     if (tp == 1 || !any_local()) return;
     const int64_t n = (int64_t)rows * d;
     bool all_local = true;
     for (int r = 0; r < tp; ++r) all_local &= X.mine(gpu(r));
+    std::vector<int> group;
+    if (!all_local && !X.pin) group = ranks(X);   // the TP sub-communicator's ranks
     if (all_local) {
       std::vector<Engine*> v;
       for (auto& e : eng) v.push_back(e.get());
       sum_tp_parts(v, n, X.st);
+    } else if (!X.pin && X.comm->has_allreduce()) {
+      // the local members' partials summed in member order, all-reduced over
+      // the group's ranks (NCCL all-reduce in fp32 on the TP
+      // sub-communicator, T4(i)), and handed to the other local members
+      int first_local = -1;
+      PartPtrs pp;
+      pp.n_in = 0;
+      for (int r = 0; r < tp; ++r)
+        if (X.mine(gpu(r))) {
+          if (first_local < 0) first_local = r;
+          pp.in[pp.n_in++] = eng[r]->part();
+        }
+      float* buf = eng[first_local]->part();
+      if (pp.n_in > 1) {
+        pp.n_out = 1;
+        pp.out[0] = buf;
+        launch_sum(pp, n, X.st);
+      }
+      X.comm->allreduce_sum(buf, (size_t)n, group, X.st);
+      for (int r = first_local + 1; r < tp; ++r)
+        if (X.mine(gpu(r)))
+          EXG_CUDA(cudaMemcpyAsync(eng[r]->part(), buf, sizeof(float) * n, cudaMemcpyDeviceToDevice, X.st));
     } else {
       ensure_tmp((size_t)n);
       // ranks of this group other than this one
       std::set<int> peers;
       for (int r = 0; r < tp; ++r)
         if (!X.mine(gpu(r))) peers.insert(X.owner(gpu(r)));
+      // the main communicator's operations all run on the communication
+      // stream, ordered against the compute stream by events
+      X.fork();
       X.comm->group_start();
       for (int a = 0; a < tp; ++a) {   // each local partial once to every other rank of the group
         if (!X.mine(gpu(a))) continue;
-        for (int q : peers) X.comm->send(eng[a]->part(), sizeof(float) * n, q, X.st);
+        for (int q : peers) X.comm->send(eng[a]->part(), sizeof(float) * n, q, X.cst);
       }
       for (int b = 0; b < tp; ++b)     // every remote member's partial, in member order
-        if (!X.mine(gpu(b))) X.comm->recv(tmp[b], sizeof(float) * n, X.owner(gpu(b)), X.st);
+        if (!X.mine(gpu(b))) X.comm->recv(tmp[b], sizeof(float) * n, X.owner(gpu(b)), X.cst);
       X.comm->group_end();
+      X.join();
       // sum in rank order into the spare buffer of the first local member,
       // then hand it to every local member
       PartPtrs pp;
@@ -278,7 +394,10 @@ static std::string layout_key(const exg_schedule& s) {
 struct MultiCtx::Impl {
   exg_model_spec spec;
   int device;
-  cudaStream_t st = nullptr;
+  cudaStream_t st = nullptr;    // compute
+  cudaStream_t cst = nullptr;   // exchanges with other ranks (PAPER.md:176 overlap)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  XferRing tx, rx;
   std::unique_ptr<Comm> comm;
   int rank = 0, world = 1;
   bool loopback = false;   // a one-rank communicator: route local exchanges through it
@@ -296,28 +415,43 @@ MultiCtx::MultiCtx(const exg_model_spec& spec, int device, std::unique_ptr<Comm>
   p_->comm = std::move(comm);
   EXG_CUDA(cudaSetDevice(device));
   EXG_CUDA(cudaStreamCreateWithFlags(&p_->st, cudaStreamNonBlocking));
+  EXG_CUDA(cudaStreamCreateWithFlags(&p_->cst, cudaStreamNonBlocking));
+  EXG_CUDA(cudaEventCreateWithFlags(&p_->ev_fork, cudaEventDisableTiming));
+  EXG_CUDA(cudaEventCreateWithFlags(&p_->ev_join, cudaEventDisableTiming));
 }
 
 MultiCtx::~MultiCtx() {
   cudaSetDevice(p_->device);
   if (p_->st) cudaStreamSynchronize(p_->st);
+  if (p_->cst) cudaStreamSynchronize(p_->cst);
   p_->layouts.clear();
+  p_->tx.release();
+  p_->rx.release();
   p_->comm.reset();
+  if (p_->ev_fork) cudaEventDestroy(p_->ev_fork);
+  if (p_->ev_join) cudaEventDestroy(p_->ev_join);
   if (p_->st) cudaStreamDestroy(p_->st);
+  if (p_->cst) cudaStreamDestroy(p_->cst);
   delete p_;
 }
 
 int MultiCtx::rank() const { return p_->rank; }
 int MultiCtx::world() const { return p_->world; }
 
-static Exec make_exec(const MultiCtx::Impl* p, int G) {
+static Exec make_exec(MultiCtx::Impl* p, int G, const exg_run_opts* opts = nullptr) {
   Exec X;
   X.me = p->rank;
   X.world = p->world;
   X.G = G;
   X.comm = p->comm.get();
   X.st = p->st;
+  X.cst = p->cst;
+  X.tx = &p->tx;
+  X.rx = &p->rx;
+  X.ev_fork = p->ev_fork;
+  X.ev_join = p->ev_join;
   X.loop = p->loopback;
+  X.pin = opts && opts->pin_nccl_algo;
   return X;
 }
 
@@ -390,6 +524,18 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
     lay->dec.push_back(make_stage(p, X, s.stage_first_gpu[i], s.stage_layer_begin[i], s.stage_layer_end[i],
                                   s.stage_n_gpus[i], k == 0, k + 1 == dec_idx.size(), t5 ? (rra ? 0 : 2) : 0,
                                   k + 1 == dec_idx.size()));
+  }
+  // TP sub-communicators (collective: every rank builds the same layout at
+  // the same point of the run)
+  if (p->world > 1 && p->comm) {
+    std::vector<std::vector<int>> groups;
+    for (auto* side : {&lay->enc, &lay->dec})
+      for (auto& st : *side)
+        if (st->tp > 1) {
+          std::vector<int> g = st->ranks(X);
+          if (g.size() > 1) groups.push_back(g);
+        }
+    p->comm->prepare_groups(groups);
   }
   Layout* out = lay.get();
   p->layouts[key] = std::move(lay);
@@ -654,23 +800,29 @@ void finish(const Exec& X, RunState& R, Stage& head_stage, int32_t* out_tokens, 
     for (int k = 0; k < R.n_stamps; ++k) stamps[k] = std::max(stamps[k], h[k]);
   };
   if (X.world > 1) {
+    // results to rank 0 over the main communicator, on its stream (cst)
+    X.fork();
     if (ho != 0) {
-      if (X.me == ho) X.comm->send(R.d_out, sizeof(int32_t) * R.total_out, 0, R.st);
-      if (X.me == 0) X.comm->recv(R.d_out, sizeof(int32_t) * R.total_out, ho, R.st);
+      if (X.me == ho) X.comm->send(R.d_out, sizeof(int32_t) * R.total_out, 0, X.cst);
+      if (X.me == 0) X.comm->recv(R.d_out, sizeof(int32_t) * R.total_out, ho, X.cst);
     }
     uint64_t* tmp = nullptr;
     if (X.me == 0) EXG_CUDA(cudaMalloc(&tmp, sizeof(uint64_t) * std::max(1, R.n_stamps)));
     for (int q = 1; q < X.world; ++q) {
-      if (X.me == q) X.comm->send(R.d_stamps, sizeof(uint64_t) * R.n_stamps, 0, R.st);
+      if (X.me == q) X.comm->send(R.d_stamps, sizeof(uint64_t) * R.n_stamps, 0, X.cst);
       if (X.me == 0) {
-        X.comm->recv(tmp, sizeof(uint64_t) * R.n_stamps, q, R.st);
+        X.comm->recv(tmp, sizeof(uint64_t) * R.n_stamps, q, X.cst);
+        X.join();
         merge(tmp);
       }
     }
+    X.join();
+    EXG_CUDA(cudaStreamSynchronize(X.cst));
     if (tmp) {
       EXG_CUDA(cudaStreamSynchronize(R.st));
       cudaFree(tmp);
     }
+    X.comm->check_async();
   }
   EXG_CUDA(cudaStreamSynchronize(R.st));
   if (Engine* head = head_stage.eng[0].get()) {
@@ -724,7 +876,7 @@ void finish(const Exec& X, RunState& R, Stage& head_stage, int32_t* out_tokens, 
 static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s, const exg_request* reqs, int n,
                           int32_t* out_tokens, double* out_latency, exg_run_stats* stats, const exg_run_opts* opts) {
   auto& pipe = lay->dec;
-  const Exec X = make_exec(p, lay->G);
+  const Exec X = make_exec(p, lay->G, opts);
   const int d = p->spec.d_model;
   RunState R;
   R.reqs = reqs;
@@ -823,7 +975,7 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
                           int32_t* out_tokens, double* out_latency, exg_run_stats* stats, const exg_run_opts* opts) {
   auto& enc = lay->enc;
   auto& dec = lay->dec;
-  const Exec X = make_exec(p, lay->G);
+  const Exec X = make_exec(p, lay->G, opts);
   const int d = p->spec.d_model, H = p->spec.n_heads, dh = p->spec.d_head;
   RunState R;
   R.reqs = reqs;
@@ -858,12 +1010,21 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   const bool first_mine = X.mine(enc.front()->gpu(0)), head_mine = X.mine(dec.back()->gpu(0));
   std::vector<Tables> tabs(8);
   const Dump dump = make_dump(R, opts);
-  // handoff row table; packed-message staging for transfers between ranks
-  HandoffRow* d_hrows = nullptr;
-  EXG_CUDA(cudaMalloc(&d_hrows, sizeof(HandoffRow) * B_E));
-  HandoffRow* h_hrows = nullptr;
-  EXG_CUDA(cudaMallocHost(&h_hrows, sizeof(HandoffRow) * B_E));
-  bf16* stage_buf = nullptr;
+  // handoff row tables: a ring of pinned host / device pairs recycled by
+  // events (no host synchronisation per handoff); packed-message staging
+  // for transfers between ranks goes through the exchange rings of Exec
+  constexpr int HR = 4;
+  HandoffRow* d_hrows[HR] = {};
+  HandoffRow* h_hrows[HR] = {};
+  cudaEvent_t hr_ev[HR] = {};
+  bool hr_used[HR] = {};
+  int hr_next = 0;
+  for (int i = 0; i < HR; ++i) {
+    EXG_CUDA(cudaMalloc(&d_hrows[i], sizeof(HandoffRow) * B_E));
+    EXG_CUDA(cudaMallocHost(&h_hrows[i], sizeof(HandoffRow) * B_E));
+    EXG_CUDA(cudaEventCreateWithFlags(&hr_ev[i], cudaEventDisableTiming));
+  }
+  bf16* stage_buf = nullptr;   // loopback transport: both halves of a self-message
   size_t stage_cap = 0;
   std::vector<int> free_slots(B_D);
   for (int i = 0; i < B_D; ++i) free_slots[i] = B_D - 1 - i;
@@ -894,26 +1055,32 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
     if (pend_k > 0 && (int)free_slots.size() >= pend_k) {
       std::vector<int> dslots(pend_k);
       int64_t rows_len = 0;
-      // the previous handoff's table upload must be done before h_hrows is rewritten
-      EXG_CUDA(cudaStreamSynchronize(R.st));
+      // a row table slot is rewritten only once its previous upload is done
+      const int hs = hr_next;
+      hr_next = (hr_next + 1) % HR;
+      if (hr_used[hs]) EXG_CUDA(cudaEventSynchronize(hr_ev[hs]));
+      HandoffRow* hrow_h = h_hrows[hs];
+      HandoffRow* hrow_d = d_hrows[hs];
       for (int j = 0; j < pend_k; ++j) {
         dslots[j] = free_slots.back();
         free_slots.pop_back();
         const exg_request& q = reqs[pend_r0 + j];
         // handed-off K/V rows: positions 0..n-2 (decoder-only) / the n cross K/V rows (T5)
-        h_hrows[j] = HandoffRow{j, dslots[j], q.input_len - drop, rows_len};
+        hrow_h[j] = HandoffRow{j, dslots[j], q.input_len - drop, rows_len};
         rows_len += q.input_len - drop;
         active.push_back(Row{pend_r0 + j, dslots[j], R.ed ? 0 : q.input_len - 1, 0});
         R.admit_ev[pend_r0 + j] = pend_ev;
       }
-      EXG_CUDA(cudaMemcpyAsync(d_hrows, h_hrows, sizeof(HandoffRow) * pend_k, cudaMemcpyHostToDevice, R.st));
+      EXG_CUDA(cudaMemcpyAsync(hrow_d, hrow_h, sizeof(HandoffRow) * pend_k, cudaMemcpyHostToDevice, R.st));
+      EXG_CUDA(cudaEventRecord(hr_ev[hs], R.st));
+      hr_used[hs] = true;
       const size_t need = (size_t)rows_len * H * dh;   // largest slice (a TP-1 decoder stage)
-      if ((X.world > 1 || X.loop) && need > stage_cap) {
+      if (X.loop && need > stage_cap) {
         EXG_CUDA(cudaStreamSynchronize(R.st));
         if (stage_buf) cudaFree(stage_buf);
         stage_cap = need;
         // loopback: a second half receives the message sent from the first
-        EXG_CUDA(cudaMalloc(&stage_buf, sizeof(bf16) * stage_cap * (X.loop ? 2 : 1)));
+        EXG_CUDA(cudaMalloc(&stage_buf, sizeof(bf16) * stage_cap * 2));
       }
       // decoder-only: encoder stage es holds the KV of its layers [l0, l1);
       // T5: the last encoder stage holds the cross K/V of every decoder layer
@@ -940,30 +1107,47 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
                   dp = R.ed ? (kv ? dst->xvc(l - ds->l0) : dst->xkc(l - ds->l0))
                             : (kv ? dst->vc(l - ds->l0) : dst->kc(l - ds->l0));
                 if (src_mine && dst_mine && X.loop) {
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, stage_buf, d_hrows, pend_k, H, r * Hd, Hd,
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, stage_buf, hrow_d, pend_k, H, r * Hd, Hd,
                                                                    enc_ctx, ctx_d, dh, 1);
                   EXG_CHECK_LAUNCH();
                   p->comm->group_start();
                   p->comm->send(stage_buf, bytes, X.me, R.st);
                   p->comm->recv(stage_buf + stage_cap, bytes, X.me, R.st);
                   p->comm->group_end();
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(stage_buf + stage_cap, dp, d_hrows, pend_k, H,
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(stage_buf + stage_cap, dp, hrow_d, pend_k, H,
                                                                    r * Hd, Hd, enc_ctx, ctx_d, dh, 2);
                   EXG_CHECK_LAUNCH();
                 } else if (src_mine && dst_mine) {
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, dp, d_hrows, pend_k, H, r * Hd, Hd, enc_ctx,
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, dp, hrow_d, pend_k, H, r * Hd, Hd, enc_ctx,
                                                                    ctx_d, dh, 0);
                   EXG_CHECK_LAUNCH();
                 } else if (src_mine) {
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, stage_buf, d_hrows, pend_k, H, r * Hd, Hd,
-                                                                   enc_ctx, ctx_d, dh, 1);
+                  // pack into a send staging buffer (compute stream), send on the
+                  // comm stream: the encoder rank goes on with the next batch
+                  const int sl = X.tx->acquire(bytes);
+                  if (X.tx->used[sl]) EXG_CUDA(cudaStreamWaitEvent(R.st, X.tx->done[sl], 0));
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, static_cast<bf16*>(X.tx->buf[sl]), hrow_d,
+                                                                   pend_k, H, r * Hd, Hd, enc_ctx, ctx_d, dh, 1);
                   EXG_CHECK_LAUNCH();
-                  p->comm->send(stage_buf, bytes, X.owner(gd), R.st);
+                  EXG_CUDA(cudaEventRecord(X.tx->ready[sl], R.st));
+                  EXG_CUDA(cudaStreamWaitEvent(X.cst, X.tx->ready[sl], 0));
+                  p->comm->send(X.tx->buf[sl], bytes, X.owner(gd), X.cst);
+                  EXG_CUDA(cudaEventRecord(X.tx->done[sl], X.cst));
+                  X.tx->used[sl] = true;
                 } else {
-                  p->comm->recv(stage_buf, bytes, X.owner(ge), R.st);
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(stage_buf, dp, d_hrows, pend_k, H, r * Hd, Hd,
-                                                                   enc_ctx, ctx_d, dh, 2);
+                  // receive on the comm stream (overlapping the decoder's running
+                  // iteration), unpack on the compute stream
+                  const int sl = X.rx->acquire(bytes);
+                  if (X.rx->used[sl]) EXG_CUDA(cudaStreamWaitEvent(X.cst, X.rx->done[sl], 0));
+                  p->comm->recv(X.rx->buf[sl], bytes, X.owner(ge), X.cst);
+                  EXG_CUDA(cudaEventRecord(X.rx->ready[sl], X.cst));
+                  EXG_CUDA(cudaStreamWaitEvent(R.st, X.rx->ready[sl], 0));
+                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(static_cast<const bf16*>(X.rx->buf[sl]), dp,
+                                                                   hrow_d, pend_k, H, r * Hd, Hd, enc_ctx, ctx_d, dh,
+                                                                   2);
                   EXG_CHECK_LAUNCH();
+                  EXG_CUDA(cudaEventRecord(X.rx->done[sl], R.st));
+                  X.rx->used[sl] = true;
                 }
               }
             }
@@ -994,8 +1178,11 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   finish(X, R, *dec.back(), out_tokens, out_latency, stats);
   EXG_CUDA(cudaStreamSynchronize(R.st));
   if (stage_buf) cudaFree(stage_buf);
-  cudaFree(d_hrows);
-  cudaFreeHost(h_hrows);
+  for (int i = 0; i < HR; ++i) {
+    cudaFree(d_hrows[i]);
+    cudaFreeHost(h_hrows[i]);
+    cudaEventDestroy(hr_ev[i]);
+  }
 }
 
 void MultiCtx::run(const exg_schedule& s, const exg_request* reqs, int n, int32_t* out_tokens, double* out_latency,

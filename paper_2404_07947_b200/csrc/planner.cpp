@@ -66,6 +66,13 @@ std::string Profile::dumps() const {
     for (size_t i = 0; i < pp_sync.t.size(); ++i) o << (i ? " " : "") << g17(pp_sync.t[i]);
     o << "\n";
   }
+  if (has_head) {
+    o << "head " << head.x.size() << "\n";
+    for (size_t i = 0; i < head.x.size(); ++i) o << (i ? " " : "") << g17(head.x[i]);
+    o << "\n";
+    for (size_t i = 0; i < head.t.size(); ++i) o << (i ? " " : "") << g17(head.t[i]);
+    o << "\n";
+  }
   o << "end\n";
   return o.str();
 }
@@ -121,6 +128,11 @@ Profile Profile::loads(const std::string& text) {
       for (int i = 0; i < m; ++i) p.pp_sync.x.push_back(num());
       for (int i = 0; i < m; ++i) p.pp_sync.t.push_back(num());
       p.has_pp = true;
+    } else if (kw == "head") {
+      int m = integer();
+      for (int i = 0; i < m; ++i) p.head.x.push_back(num());
+      for (int i = 0; i < m; ++i) p.head.t.push_back(num());
+      p.has_head = true;
     } else {
       throw std::invalid_argument("profile-v1: bad keyword '" + kw + "'");
     }
@@ -303,6 +315,8 @@ std::vector<double> Simulator::stage_times(const std::vector<Stage>& st, bool en
       const double toks = enc ? b * s_e : b;
       v += pp_sync(toks * m.d_model * 2.0);
     }
+    // the decode head runs once per iteration on the last stage
+    if (!enc && k == P - 1 && p.has_head) v += interp1(p.head.x, p.head.t, b);
     out.push_back(v);
   }
   return out;

@@ -31,6 +31,8 @@ struct Profile {
   std::map<int, Table1D> tp_sync;
   Table1D pp_sync;
   bool has_pp = false;
+  Table1D head;            // decode head (final norm + LM head + argmax) vs batch
+  bool has_head = false;
   std::string dumps() const;
   static Profile loads(const std::string& text);
 };

@@ -44,20 +44,25 @@ struct Timer {
     cudaEventDestroy(b);
     if (flush) cudaFree(flush);
   }
+  // median over `reps` of (time of `burst` back-to-back runs of f) / burst,
+  // L2 flushed before each rep.  burst = 1: one cold run (attention tables);
+  // burst > 1: the layer as it runs inside a step -- consecutive layers
+  // chained under PDL, the clock in its sustained state (the "rest" tables;
+  // a large model's layer weights exceed L2, so repeats stream from HBM)
   template <class F>
-  double median(int reps, F&& f) {
+  double median(int reps, F&& f, int burst = 1) {
     f();  // warm-up
     std::vector<double> v;
     for (int r = 0; r < reps; ++r) {
       l2_flush_kernel<<<148 * 4, 256, 0, st>>>(flush, flush_n, reinterpret_cast<int*>(flush + flush_n));
       EXG_CHECK_LAUNCH();
       EXG_CUDA(cudaEventRecord(a, st));
-      f();
+      for (int k = 0; k < burst; ++k) f();
       EXG_CUDA(cudaEventRecord(b, st));
       EXG_CUDA(cudaEventSynchronize(b));
       float ms = 0;
       EXG_CUDA(cudaEventElapsedTime(&ms, a, b));
-      v.push_back(ms * 1e-3);
+      v.push_back(ms * 1e-3 / burst);
     }
     std::sort(v.begin(), v.end());
     return v[v.size() / 2];
@@ -65,7 +70,10 @@ struct Timer {
 };
 }  // namespace
 
-// attention and "rest" tables of one layer of engine E under key t
+constexpr int kBurst = 8, kBurstEnc = 4;
+
+// attention and "rest" tables of one layer of engine E under key t (+ the
+// decode head table when E holds the LM head and t = 1)
 static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profile& P) {
   const Dims& D = E.dims();
   const int reps = std::max(1, g.reps);
@@ -165,7 +173,32 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
     db.xkeys = d_aux + max_b;
     db.max_xkeys = 1;
     rd.x.push_back(b);
-    rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }));
+    rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }, kBurst));
+  }
+  // head of a decode iteration on the last stage (final norm + tied LM head +
+  // argmax), per decode batch: the model-level part of an iteration that the
+  // per-layer tables do not hold (DESIGN.md reading)
+  plan::Table1D hd;
+  if (t == 1 && E.shard().head) {
+    std::vector<int32_t> h_off(max_b);
+    for (int i = 0; i < max_b; ++i) h_off[i] = i;
+    int32_t* d_tok = nullptr;
+    EXG_CUDA(cudaMalloc(&d_tok, sizeof(int32_t) * 2 * max_b));
+    EXG_CUDA(cudaMemcpy(d_tok, h_off.data(), max_b * 4, cudaMemcpyHostToDevice));
+    for (int b : bs) {
+      DecodeBatch db;
+      db.B = b;
+      db.max_keys = 1;
+      db.slot = d_rs;
+      db.pos = d_p0;
+      db.nkeys = d_aux;
+      db.out_off = d_tok;
+      db.out_tokens = d_tok + max_b;   // scratch: the argmax writes ids there
+      hd.x.push_back(b);
+      hd.t.push_back(tm.median(reps, [&] { E.head_decode(db); }, kBurst));
+    }
+    EXG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_tok);
   }
   // Sustained-load state (reading): a real encode phase runs
   // back-to-back prefill GEMMs for ~0.1-0.3 s, long enough for the power
@@ -200,10 +233,14 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
     re.t.push_back(tm.median(reps, [&] {
       E.layer_encode(0, eb, false, true);
       if (E.encdec()) E.cross_kv(0, eb);
-    }));
+    }, kBurstEnc));
   }
   P.rest[{"enc", t}] = re;
   P.rest[{"dec", t}] = rd;
+  if (!hd.x.empty()) {
+    P.head = hd;
+    P.has_head = true;
+  }
   EXG_CUDA(cudaStreamSynchronize(st));
   cudaFree(d);
 }

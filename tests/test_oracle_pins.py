@@ -368,3 +368,34 @@ def test_schedule_find_equals_exhaustive(n_gpus):
         assert got.estimate.thrput_seq_s == pytest.approx(ex[2].thrput_seq_s, rel=1e-12), (L_b, got.schedule, ex[1])
         n_match += 1
     assert n_match >= 3
+
+
+# ======================================================== decode head term ==
+def test_head_table_charged_once_per_iteration_on_the_last_stage():
+    """The profile's `head` table (final norm + LM head + argmax per decode
+    iteration) adds head(b) to the decode stage time of the last stage only:
+    RRA P = 1 latency / cycle grow by exactly sum_u head(b_u) (closed form on a
+    constant-cost profile), and profile-v1 round-trips it."""
+    from test_oracle_scheduler import _const_profile, _one_layer_model
+    d = task_dists("S")
+    p0 = _const_profile(0.5, 0.01)
+    p1 = sim.Profile.loads(p0.dumps())
+    p1.head = sim.Table1D([1.0, 1000.0], [0.002, 0.002 + 999 * 1e-5])
+    assert sim.Profile.loads(p1.dumps()).dumps() == p1.dumps()
+    S0 = sim.Simulator(p0, _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
+    S1 = sim.Simulator(p1, _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
+    s = S0.rra_schedule(16, 8, 1, 0)
+    e0, e1 = S0.simulate(s), S1.simulate(s)
+    pu, f = S0.pu(8)
+    bu = seqdist.rra_iteration_batches(s.b_d, pu)
+    head = [0.002 + (b - 1) * 1e-5 for b in bu]
+    T0, T1 = s.b_e / e0.thrput_seq_s, s.b_e / e1.thrput_seq_s
+    assert T1 - T0 == pytest.approx(sum(head), rel=1e-9)
+    # latency of the 63-token query: ceil(63/8) = 8 cycles, the last one to r = 7
+    assert e1.latency_s - e0.latency_s == pytest.approx(7 * sum(head) + sum(head[:7]), rel=1e-9)
+    # pipelines: only the last stage carries it
+    st = sim.stage_layout(4, 1, 0, 8)
+    t0 = S0.stage_times(st, "dec", 16.0)
+    t1 = S1.stage_times(st, "dec", 16.0)
+    assert t1[:3] == t0[:3] and t1[3] - t0[3] == pytest.approx(0.002 + 15 * 1e-5, rel=1e-12)
+    assert S1.stage_times(st, "enc", 16.0) == S0.stage_times(st, "enc", 16.0)

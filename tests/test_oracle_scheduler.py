@@ -264,6 +264,8 @@ def _synthetic_profile(model, tps=(1, 2, 4, 8)):
         if t > 1:
             p.tp_sync[t] = sim.Table1D([0, 1e6, 1e9, 1e12], [1e-5, 1.2e-5, 1.5e-3, 1.5])
     p.pp_sync = sim.Table1D([0, 1e6, 1e9, 1e12, 1e15], [8e-6, 1e-5, 1.3e-3, 1.3, 1300.0])
+    vbytes = model.vocab * d * 2
+    p.head = sim.Table1D(bs, [4e-6 + max(vbytes / 6e12, b * 2 * model.vocab * d / 1.2e15) for b in bs])
     return p
 
 

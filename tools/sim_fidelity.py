@@ -59,6 +59,7 @@ def main():
         tr = []
         _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx, trace=tr)
         tr = np.array(tr)
+        np.save(os.path.join(ROOT, "gpurun_out", "sim_trace_%s.npy" % name), tr)
         enc, dec = tr[tr[:, 0] == 1], tr[tr[:, 0] == 2]
 
         def pred_enc(rows, toks):
@@ -69,7 +70,8 @@ def main():
         def pred_dec(rows, keys):
             a = sim.interp2(P.attn[("dec", 1)], rows, keys / rows)
             r = sim.interp1(P.rest[("dec", 1)].x, P.rest[("dec", 1)].t, rows)
-            return L * (a + r)
+            h = sim.interp1(P.head.x, P.head.t, rows) if P.head is not None else 0.0
+            return L * (a + r) + h
 
         pe = np.array([pred_enc(r[3], r[4]) for r in enc])
         pd = np.array([pred_dec(r[3], r[4]) for r in dec])
