@@ -65,6 +65,7 @@ class Profile:
     tp_sync: Dict[int, Table1D] = field(default_factory=dict)
     pp_sync: Optional[Table1D] = None
     head: Optional[Table1D] = None     # decode head (final norm + LM head + argmax) vs batch
+    switch: Optional[Table1D] = None   # extra time of the first decode iteration after an encode phase
 
     def save(self, path: str):
         with open(path, "w") as f:
@@ -94,6 +95,10 @@ class Profile:
             out.append("head %d" % len(self.head.x))
             out.append(" ".join(g(v) for v in self.head.x))
             out.append(" ".join(g(v) for v in self.head.t))
+        if self.switch is not None:
+            out.append("switch %d" % len(self.switch.x))
+            out.append(" ".join(g(v) for v in self.switch.x))
+            out.append(" ".join(g(v) for v in self.switch.t))
         out.append("end")
         return "\n".join(out) + "\n"
 
@@ -138,6 +143,10 @@ class Profile:
                 n = int(nxt())
                 x = [float(nxt()) for _ in range(n)]
                 p.head = Table1D(x, [float(nxt()) for _ in range(n)])
+            elif kw == "switch":
+                n = int(nxt())
+                x = [float(nxt()) for _ in range(n)]
+                p.switch = Table1D(x, [float(nxt()) for _ in range(n)])
             else:
                 raise ValueError("bad keyword %r" % kw)
 
@@ -309,6 +318,12 @@ class Simulator:
         self.s_d = seqdist.pmf_mean(self.pmf_out)
         self.max_in, self.max_out = len(self.pmf_in), len(self.pmf_out)
         self.ctx_mean = self.s_e + self.s_d / 2.0          # S5 decode-attention context
+        # encode-attention lookup length: the RMS input length (a request's
+        # attention cost grows as n^2; DESIGN.md reading)
+        m2 = 0.0
+        for k in range(1, len(self.pmf_in) + 1):
+            m2 += float(k) * float(k) * float(self.pmf_in[k - 1])
+        self.s_e_rms = math.sqrt(m2)
         self.use_little = use_little_fraction
         self.n_layers = model.n_dec_layers                   # decoder-only: every layer runs both phases
         self.k_dec = 3 if model.arch == "t5" else 2
@@ -327,7 +342,7 @@ class Simulator:
 
     def layer_enc(self, t: int, b: float) -> float:
         toks = b * self.s_e
-        a = interp2(self.p.attn[("enc", t)], b, self.s_e)
+        a = interp2(self.p.attn[("enc", t)], b, self.s_e_rms)
         tb = self.p.rest[("enc", t)]
         r = interp1(tb.x, tb.t, toks)
         return a + r + 2 * self._tp_sync(t, toks * self.m.d_model * 4.0)
@@ -434,6 +449,12 @@ class Simulator:
             Pi, Fu = [], []
             for u in range(s.n_d):
                 tu = self.stage_times(s.stages, "dec", bu[u] / P)
+                if u == 0 and self.p.switch is not None:
+                    # the phase's first decode iteration follows an encode phase:
+                    # its extra time (profile `switch`), each stage its layer share
+                    w = interp1(self.p.switch.x, self.p.switch.t, bu[0] / P)
+                    for k in range(P):
+                        tu[k] = tu[k] + w * float(s.stages[k][3] - s.stages[k][2]) / self.n_layers
                 Pi.append(period(tu, P))
                 Fu.append(fill(tu, P))
         except OutOfHull:
@@ -524,9 +545,12 @@ class Simulator:
         try:
             t_enc = self.stage_times(st, "enc", float(B))
             t_dec = self.stage_times(st, "dec", float(B))
+            lat = fill(t_enc, 1) + self.max_out * fill(t_dec, 1)
+            if self.p.switch is not None:
+                # the first decode iteration follows the encode phase
+                lat += interp1(self.p.switch.x, self.p.switch.t, float(B))
         except OutOfHull:
             return Estimate(0.0, 0.0, INF, False)
-        lat = fill(t_enc, 1) + self.max_out * fill(t_dec, 1)
         thr = B / lat
         return Estimate(thr, thr * self.s_d, lat)
 

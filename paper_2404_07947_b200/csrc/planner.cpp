@@ -73,6 +73,13 @@ std::string Profile::dumps() const {
     for (size_t i = 0; i < head.t.size(); ++i) o << (i ? " " : "") << g17(head.t[i]);
     o << "\n";
   }
+  if (has_sw) {
+    o << "switch " << sw.x.size() << "\n";
+    for (size_t i = 0; i < sw.x.size(); ++i) o << (i ? " " : "") << g17(sw.x[i]);
+    o << "\n";
+    for (size_t i = 0; i < sw.t.size(); ++i) o << (i ? " " : "") << g17(sw.t[i]);
+    o << "\n";
+  }
   o << "end\n";
   return o.str();
 }
@@ -133,6 +140,11 @@ Profile Profile::loads(const std::string& text) {
       for (int i = 0; i < m; ++i) p.head.x.push_back(num());
       for (int i = 0; i < m; ++i) p.head.t.push_back(num());
       p.has_head = true;
+    } else if (kw == "switch") {
+      int m = integer();
+      for (int i = 0; i < m; ++i) p.sw.x.push_back(num());
+      for (int i = 0; i < m; ++i) p.sw.t.push_back(num());
+      p.has_sw = true;
     } else {
       throw std::invalid_argument("profile-v1: bad keyword '" + kw + "'");
     }
@@ -269,6 +281,13 @@ Simulator::Simulator(const Profile& p_, const exg_model_spec& m_, const exg_clus
   max_in = (int)pmf_in.size();
   max_out = (int)pmf_out.size();
   ctx_mean = s_e + s_d / 2.0;
+  // RMS input length: the encode-attention lookup length (its per-request
+  // cost grows as n^2, so b requests of this length cost sum_i n_i^2)
+  {
+    double m2 = 0.0;
+    for (size_t k = 1; k <= pmf_in.size(); ++k) m2 += (double)k * (double)k * pmf_in[k - 1];
+    s_e_rms = std::sqrt(m2);
+  }
   n_layers = m.n_dec_layers;
   k_dec = m.arch == EXG_ARCH_T5 ? 3 : 2;
 }
@@ -290,7 +309,7 @@ double Simulator::layer_enc(int t, double b) {
   auto ia = p.attn.find({"enc", t});
   auto ir = p.rest.find({"enc", t});
   if (ia == p.attn.end() || ir == p.rest.end()) throw OutOfHull{};
-  const double a = interp2(ia->second, b, s_e);
+  const double a = interp2(ia->second, b, s_e_rms);
   const double r = interp1(ir->second.x, ir->second.t, toks);
   return a + r + 2 * tp_sync(t, toks * m.d_model * 4.0);
 }
@@ -462,6 +481,13 @@ Est Simulator::simulate_rra(const Sched& s) {
     std::vector<double> bu = rra_iteration_batches(s.b_d, pf.first);
     for (int u = 0; u < s.n_d; ++u) {
       std::vector<double> tu = stage_times(s.stages, false, bu[u] / P);
+      if (u == 0 && p.has_sw) {
+        // the first decode iteration of a phase follows an encode phase: its
+        // extra time (profile table `switch`), each stage its layer share
+        const double w = interp1(p.sw.x, p.sw.t, bu[0] / P);
+        for (int k = 0; k < P; ++k)
+          tu[k] = tu[k] + w * (double)(s.stages[k].layer_end - s.stages[k].layer_begin) / n_layers;
+      }
       Pi.push_back(period(tu, P));
       Fu.push_back(fill(tu, P));
     }
@@ -517,6 +543,7 @@ Est Simulator::simulate_static(int B) {
     const std::vector<double> t_enc = stage_times(st, true, (double)B);
     const std::vector<double> t_dec = stage_times(st, false, (double)B);
     lat = fill(t_enc, 1) + max_out * fill(t_dec, 1);
+    if (p.has_sw) lat += interp1(p.sw.x, p.sw.t, (double)B);
   } catch (const OutOfHull&) {
     return bad;
   }

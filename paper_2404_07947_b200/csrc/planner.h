@@ -33,6 +33,8 @@ struct Profile {
   bool has_pp = false;
   Table1D head;            // decode head (final norm + LM head + argmax) vs batch
   bool has_head = false;
+  Table1D sw;              // extra time of the first decode iteration after an encode phase vs batch
+  bool has_sw = false;
   std::string dumps() const;
   static Profile loads(const std::string& text);
 };
@@ -90,7 +92,7 @@ class Simulator {
   exg_cluster_spec cl;
   std::vector<double> pmf_in, pmf_out;
   int target_len;
-  double s_e, s_d, ctx_mean;
+  double s_e, s_d, ctx_mean, s_e_rms;
   int max_in, max_out, n_layers, k_dec;
   bool use_little;
 

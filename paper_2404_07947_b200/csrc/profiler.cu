@@ -10,6 +10,8 @@
 // all-reduce and PP send timings need a multi-rank context).
 #include <algorithm>
 #include <chrono>
+#include <cmath>
+#include <thread>
 #include <vector>
 
 #include "profiler.h"
@@ -63,6 +65,34 @@ struct Timer {
       float ms = 0;
       EXG_CUDA(cudaEventElapsedTime(&ms, a, b));
       v.push_back(ms * 1e-3 / burst);
+    }
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  }
+  // the clock's sustained (power-capped) state of a long phase: f back to
+  // back for >= warm_s unmeasured, then >= meas_s timed (no host sync in
+  // between); median over reps
+  template <class F>
+  double sustained(int reps, F&& f, double warm_s = 0.05, double meas_s = 0.05) {
+    EXG_CUDA(cudaEventRecord(a, st));
+    f();
+    EXG_CUDA(cudaEventRecord(b, st));
+    EXG_CUDA(cudaEventSynchronize(b));
+    float ms1 = 0;
+    EXG_CUDA(cudaEventElapsedTime(&ms1, a, b));
+    const double t1 = std::max(1e-6, ms1 * 1e-3);
+    const int kw = (int)std::min(4000.0, std::ceil(warm_s / t1));
+    const int k = (int)std::max(2.0, std::min(4000.0, std::ceil(meas_s / t1)));
+    std::vector<double> v;
+    for (int r = 0; r < reps; ++r) {
+      for (int i = 0; i < kw; ++i) f();
+      EXG_CUDA(cudaEventRecord(a, st));
+      for (int i = 0; i < k; ++i) f();
+      EXG_CUDA(cudaEventRecord(b, st));
+      EXG_CUDA(cudaEventSynchronize(b));
+      float ms = 0;
+      EXG_CUDA(cudaEventElapsedTime(&ms, a, b));
+      v.push_back(ms * 1e-3 / k);
     }
     std::sort(v.begin(), v.end());
     return v[v.size() / 2];
@@ -230,16 +260,94 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
     re.x.push_back(T);
     // encoder-decoder: the encode phase also projects the cross K/V of each
     // decoder layer (K13), charged to the layer
-    re.t.push_back(tm.median(reps, [&] {
+    // a real encode phase is 0.1-0.3 s of back-to-back prefill GEMMs: the
+    // clock is the power-capped sustained one (DESIGN.md reading)
+    re.t.push_back(tm.sustained(reps, [&] {
       E.layer_encode(0, eb, false, true);
       if (E.encdec()) E.cross_kv(0, eb);
-    }, kBurstEnc));
+    }));
+  }
+  // encode -> decode switch: the first decode iteration after an encode
+  // phase runs while the clock recovers from the power cap.  Per decode
+  // batch: a full iteration's decode layers (layer 0's weights and KV, L
+  // times) + the head, right after a sustained encode burst, minus the same
+  // sequence at the recovered clock
+  plan::Table1D swt;
+  if (t == 1) {
+    const int n_sw = E.dims().L;
+    const int c_sw = cs[cs.size() / 2] < ctx_cap ? cs[cs.size() / 2] : ctx_cap;
+    std::vector<int32_t> h_k(2 * max_b);
+    for (int i = 0; i < max_b; ++i) h_k[i] = c_sw, h_k[max_b + i] = std::max(1, c_sw / 2);
+    EXG_CUDA(cudaMemcpy(d_aux, h_k.data(), 2 * max_b * 4, cudaMemcpyHostToDevice));
+    int32_t* d_tok = nullptr;
+    EXG_CUDA(cudaMalloc(&d_tok, sizeof(int32_t) * 2 * max_b));
+    std::vector<int32_t> h_off(max_b);
+    for (int i = 0; i < max_b; ++i) h_off[i] = i;
+    EXG_CUDA(cudaMemcpy(d_tok, h_off.data(), max_b * 4, cudaMemcpyHostToDevice));
+    EncodeBatch hb;
+    hb.T = ts.back();
+    hb.R = 1;
+    hb.max_len = hb.T;
+    hb.ids = d_ids;
+    hb.pos = d_pos;
+    hb.tslot = d_slot;
+    cudaEvent_t e0, e1, e2, e3;
+    for (cudaEvent_t* e : {&e0, &e1, &e2, &e3}) EXG_CUDA(cudaEventCreate(e));
+    for (int b : bs) {
+      DecodeBatch db;
+      db.B = b;
+      db.max_keys = c_sw;
+      db.sum_keys = (double)b * c_sw;
+      db.slot = d_rs;
+      db.pos = d_p0;
+      db.nkeys = d_aux;
+      db.xkeys = d_aux + max_b;
+      db.max_xkeys = std::max(1, c_sw / 2);
+      db.out_off = d_tok;
+      db.out_tokens = d_tok + max_b;
+      auto iteration = [&] {
+        for (int l = 0; l < n_sw; ++l) E.layer_decode(0, db, true, true);
+        if (E.shard().head) E.head_decode(db);
+      };
+      std::vector<double> dv;
+      for (int r = 0; r < reps; ++r) {
+        const auto h0 = std::chrono::steady_clock::now();   // sustained encode, then the iteration
+        while (std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count() < 0.06) {
+          for (int k = 0; k < 2; ++k) E.layer_encode(0, hb, false, true);
+          EXG_CUDA(cudaStreamSynchronize(st));
+        }
+        for (int k = 0; k < 2; ++k) E.layer_encode(0, hb, false, true);   // still running when the iteration is queued
+        EXG_CUDA(cudaEventRecord(e0, st));
+        iteration();
+        EXG_CUDA(cudaEventRecord(e1, st));
+        EXG_CUDA(cudaEventSynchronize(e1));
+        std::this_thread::sleep_for(std::chrono::milliseconds(60));   // clock recovers
+        EXG_CUDA(cudaEventRecord(e2, st));
+        iteration();
+        EXG_CUDA(cudaEventRecord(e3, st));
+        EXG_CUDA(cudaEventSynchronize(e3));
+        float ms_a = 0, ms_b = 0;
+        EXG_CUDA(cudaEventElapsedTime(&ms_a, e0, e1));
+        EXG_CUDA(cudaEventElapsedTime(&ms_b, e2, e3));
+        dv.push_back(std::max(0.0, (ms_a - ms_b) * 1e-3));
+      }
+      std::sort(dv.begin(), dv.end());
+      swt.x.push_back(b);
+      swt.t.push_back(dv[dv.size() / 2]);
+    }
+    for (cudaEvent_t e : {e0, e1, e2, e3}) cudaEventDestroy(e);
+    EXG_CUDA(cudaStreamSynchronize(st));
+    cudaFree(d_tok);
   }
   P.rest[{"enc", t}] = re;
   P.rest[{"dec", t}] = rd;
   if (!hd.x.empty()) {
     P.head = hd;
     P.has_head = true;
+  }
+  if (!swt.x.empty()) {
+    P.sw = swt;
+    P.has_sw = true;
   }
   EXG_CUDA(cudaStreamSynchronize(st));
   cudaFree(d);

@@ -399,3 +399,35 @@ def test_head_table_charged_once_per_iteration_on_the_last_stage():
     t1 = S1.stage_times(st, "dec", 16.0)
     assert t1[:3] == t0[:3] and t1[3] - t0[3] == pytest.approx(0.002 + 15 * 1e-5, rel=1e-12)
     assert S1.stage_times(st, "enc", 16.0) == S0.stage_times(st, "enc", 16.0)
+
+
+def test_switch_table_and_rms_attention_length():
+    """Encode -> decode switch (profile `switch`): the phase's first decode
+    iteration carries switch(b_1) once per RRA cycle (closed form at P = 1);
+    the static batch carries it once.  Encode attention is looked up at the
+    RMS input length sqrt(E[n^2]) (closed form on a table linear in c^2)."""
+    from test_oracle_scheduler import _const_profile, _one_layer_model
+    d = task_dists("S")
+    p0 = _const_profile(0.5, 0.01)
+    p1 = sim.Profile.loads(p0.dumps())
+    p1.switch = sim.Table1D([1.0, 1000.0], [0.003, 0.003 + 999 * 2e-6])
+    assert sim.Profile.loads(p1.dumps()).dumps() == p1.dumps()
+    S0 = sim.Simulator(p0, _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
+    S1 = sim.Simulator(p1, _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
+    s = S0.rra_schedule(16, 8, 1, 0)
+    e0, e1 = S0.simulate(s), S1.simulate(s)
+    w = 0.003 + (s.b_d - 1) * 2e-6                         # b_1 = B_D
+    assert s.b_e / e1.thrput_seq_s - s.b_e / e0.thrput_seq_s == pytest.approx(w, rel=1e-9)
+    assert e1.latency_s - e0.latency_s == pytest.approx(8 * w, rel=1e-9)    # 8 cycles of the 63-token query
+    st0, st1 = S0.simulate_static(8), S1.simulate_static(8)
+    assert st1.latency_s - st0.latency_s == pytest.approx(0.003 + 7 * 2e-6, rel=1e-9)
+    # RMS length: an attention table t = c^2 (per request) makes the encode
+    # attention term b * E[n^2]
+    p2 = sim.Profile.loads(p0.dumps())
+    cs = [float(c) for c in range(1, 600, 7)]
+    p2.attn[("enc", 1)] = sim.Table2D([1.0, 4096.0], cs, [[c * c for c in cs], [4096 * c * c for c in cs]])
+    S2 = sim.Simulator(p2, _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
+    e_n2 = sum(float(k * k) * float(d.pmf_in[k - 1]) for k in range(1, len(d.pmf_in) + 1))
+    a = S2.layer_enc(1, 1.0) - S0.layer_enc(1, 1.0)
+    assert a == pytest.approx(e_n2, rel=2e-3)           # piecewise-linear table of c^2
+    assert e_n2 > 1.25 * S2.s_e ** 2                     # task S: RMS length ~1.14 x the mean
