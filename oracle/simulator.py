@@ -65,7 +65,7 @@ class Profile:
     tp_sync: Dict[int, Table1D] = field(default_factory=dict)
     pp_sync: Optional[Table1D] = None
     head: Optional[Table1D] = None     # decode head (final norm + LM head + argmax) vs batch
-    switch: Optional[Table1D] = None   # extra time of the first decode iteration after an encode phase
+    switch: Optional[Table2D] = None   # cumulative extra time of the first k decode iterations after an encode phase [b][k]
 
     def save(self, path: str):
         with open(path, "w") as f:
@@ -96,9 +96,10 @@ class Profile:
             out.append(" ".join(g(v) for v in self.head.x))
             out.append(" ".join(g(v) for v in self.head.t))
         if self.switch is not None:
-            out.append("switch %d" % len(self.switch.x))
-            out.append(" ".join(g(v) for v in self.switch.x))
-            out.append(" ".join(g(v) for v in self.switch.t))
+            out.append("switch %d %d" % (len(self.switch.b), len(self.switch.c)))
+            out.append(" ".join(g(v) for v in self.switch.b))
+            out.append(" ".join(g(v) for v in self.switch.c))
+            out.append(" ".join(g(v) for row in self.switch.t for v in row))
         out.append("end")
         return "\n".join(out) + "\n"
 
@@ -144,9 +145,10 @@ class Profile:
                 x = [float(nxt()) for _ in range(n)]
                 p.head = Table1D(x, [float(nxt()) for _ in range(n)])
             elif kw == "switch":
-                n = int(nxt())
-                x = [float(nxt()) for _ in range(n)]
-                p.switch = Table1D(x, [float(nxt()) for _ in range(n)])
+                nb, nc = int(nxt()), int(nxt())
+                b = [float(nxt()) for _ in range(nb)]
+                c = [float(nxt()) for _ in range(nc)]
+                p.switch = Table2D(b, c, [[float(nxt()) for _ in range(nc)] for _ in range(nb)])
             else:
                 raise ValueError("bad keyword %r" % kw)
 
@@ -450,9 +452,12 @@ class Simulator:
             for u in range(s.n_d):
                 tu = self.stage_times(s.stages, "dec", bu[u] / P)
                 if u == 0 and self.p.switch is not None:
-                    # the phase's first decode iteration follows an encode phase:
-                    # its extra time (profile `switch`), each stage its layer share
-                    w = interp1(self.p.switch.x, self.p.switch.t, bu[0] / P)
+                    # the phase's decode iterations follow an encode phase: the
+                    # clock recovers from the power cap over the first few; their
+                    # cumulative extra time (profile `switch` at k = min(N_D,
+                    # k_max)) is charged to the first iteration, each stage its
+                    # layer share (DESIGN.md reading)
+                    w = interp2(self.p.switch, bu[0] / P, min(float(s.n_d), self.p.switch.c[-1]))
                     for k in range(P):
                         tu[k] = tu[k] + w * float(s.stages[k][3] - s.stages[k][2]) / self.n_layers
                 Pi.append(period(tu, P))
@@ -547,8 +552,8 @@ class Simulator:
             t_dec = self.stage_times(st, "dec", float(B))
             lat = fill(t_enc, 1) + self.max_out * fill(t_dec, 1)
             if self.p.switch is not None:
-                # the first decode iteration follows the encode phase
-                lat += interp1(self.p.switch.x, self.p.switch.t, float(B))
+                # the decode iterations follow the encode phase (clock recovery)
+                lat += interp2(self.p.switch, float(B), min(float(self.max_out), self.p.switch.c[-1]))
         except OutOfHull:
             return Estimate(0.0, 0.0, INF, False)
         thr = B / lat

@@ -74,10 +74,17 @@ std::string Profile::dumps() const {
     o << "\n";
   }
   if (has_sw) {
-    o << "switch " << sw.x.size() << "\n";
-    for (size_t i = 0; i < sw.x.size(); ++i) o << (i ? " " : "") << g17(sw.x[i]);
+    o << "switch " << sw.b.size() << " " << sw.c.size() << "\n";
+    for (size_t i = 0; i < sw.b.size(); ++i) o << (i ? " " : "") << g17(sw.b[i]);
     o << "\n";
-    for (size_t i = 0; i < sw.t.size(); ++i) o << (i ? " " : "") << g17(sw.t[i]);
+    for (size_t i = 0; i < sw.c.size(); ++i) o << (i ? " " : "") << g17(sw.c[i]);
+    o << "\n";
+    bool first = true;
+    for (const auto& row : sw.t)
+      for (double v : row) {
+        o << (first ? "" : " ") << g17(v);
+        first = false;
+      }
     o << "\n";
   }
   o << "end\n";
@@ -141,9 +148,12 @@ Profile Profile::loads(const std::string& text) {
       for (int i = 0; i < m; ++i) p.head.t.push_back(num());
       p.has_head = true;
     } else if (kw == "switch") {
-      int m = integer();
-      for (int i = 0; i < m; ++i) p.sw.x.push_back(num());
-      for (int i = 0; i < m; ++i) p.sw.t.push_back(num());
+      int nb = integer(), nk = integer();
+      for (int i = 0; i < nb; ++i) p.sw.b.push_back(num());
+      for (int i = 0; i < nk; ++i) p.sw.c.push_back(num());
+      p.sw.t.assign(nb, std::vector<double>(nk));
+      for (int i = 0; i < nb; ++i)
+        for (int j = 0; j < nk; ++j) p.sw.t[i][j] = num();
       p.has_sw = true;
     } else {
       throw std::invalid_argument("profile-v1: bad keyword '" + kw + "'");
@@ -482,9 +492,11 @@ Est Simulator::simulate_rra(const Sched& s) {
     for (int u = 0; u < s.n_d; ++u) {
       std::vector<double> tu = stage_times(s.stages, false, bu[u] / P);
       if (u == 0 && p.has_sw) {
-        // the first decode iteration of a phase follows an encode phase: its
-        // extra time (profile table `switch`), each stage its layer share
-        const double w = interp1(p.sw.x, p.sw.t, bu[0] / P);
+        // the phase's decode iterations follow an encode phase: the clock
+        // recovers from the power cap over the first few of them; their
+        // cumulative extra time (profile table `switch` at k = min(N_D, k_max))
+        // is charged to the first iteration, each stage its layer share
+        const double w = interp2(p.sw, bu[0] / P, std::min((double)s.n_d, p.sw.c.back()));
         for (int k = 0; k < P; ++k)
           tu[k] = tu[k] + w * (double)(s.stages[k].layer_end - s.stages[k].layer_begin) / n_layers;
       }
@@ -543,7 +555,7 @@ Est Simulator::simulate_static(int B) {
     const std::vector<double> t_enc = stage_times(st, true, (double)B);
     const std::vector<double> t_dec = stage_times(st, false, (double)B);
     lat = fill(t_enc, 1) + max_out * fill(t_dec, 1);
-    if (p.has_sw) lat += interp1(p.sw.x, p.sw.t, (double)B);
+    if (p.has_sw) lat += interp2(p.sw, (double)B, std::min((double)max_out, p.sw.c.back()));
   } catch (const OutOfHull&) {
     return bad;
   }

@@ -33,8 +33,8 @@ struct Profile {
   bool has_pp = false;
   Table1D head;            // decode head (final norm + LM head + argmax) vs batch
   bool has_head = false;
-  Table1D sw;              // extra time of the first decode iteration after an encode phase vs batch
-  bool has_sw = false;
+  Table2D sw;              // encode -> decode switch: cumulative extra time of the first k
+  bool has_sw = false;     // decode iterations after an encode phase, [batch][k]
   std::string dumps() const;
   static Profile loads(const std::string& text);
 };

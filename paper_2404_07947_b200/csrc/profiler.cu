@@ -267,12 +267,13 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
       if (E.encdec()) E.cross_kv(0, eb);
     }));
   }
-  // encode -> decode switch: the first decode iteration after an encode
-  // phase runs while the clock recovers from the power cap.  Per decode
-  // batch: a full iteration's decode layers (layer 0's weights and KV, L
-  // times) + the head, right after a sustained encode burst, minus the same
-  // sequence at the recovered clock
-  plan::Table1D swt;
+  // encode -> decode switch: after an encode phase the clock recovers from
+  // the power cap over the first decode iterations.  Per decode batch b (a
+  // subset of the batch axis, its ends included): k = 1..16 back-to-back
+  // iterations (L decode layers of layer 0's weights and KV + the head) right
+  // after a sustained encode burst, minus the same at the recovered clock;
+  // the table holds the cumulative extra time of the first k iterations
+  plan::Table2D swt;
   if (t == 1) {
     const int n_sw = E.dims().L;
     const int c_sw = cs[cs.size() / 2] < ctx_cap ? cs[cs.size() / 2] : ctx_cap;
@@ -291,9 +292,16 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
     hb.ids = d_ids;
     hb.pos = d_pos;
     hb.tslot = d_slot;
-    cudaEvent_t e0, e1, e2, e3;
-    for (cudaEvent_t* e : {&e0, &e1, &e2, &e3}) EXG_CUDA(cudaEventCreate(e));
-    for (int b : bs) {
+    const std::vector<int> ks = {1, 2, 4, 8, 16};
+    const int KMAX = ks.back();
+    std::vector<cudaEvent_t> ev(2 * (KMAX + 1));
+    for (auto& e : ev) EXG_CUDA(cudaEventCreate(&e));
+    std::vector<int> bsw;
+    for (size_t i = 0; i < bs.size(); i += 3) bsw.push_back(bs[i]);
+    if (bsw.back() != bs.back()) bsw.push_back(bs.back());
+    swt.b.assign(bsw.begin(), bsw.end());
+    swt.c.assign(ks.begin(), ks.end());
+    for (int b : bsw) {
       DecodeBatch db;
       db.B = b;
       db.max_keys = c_sw;
@@ -305,37 +313,42 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
       db.max_xkeys = std::max(1, c_sw / 2);
       db.out_off = d_tok;
       db.out_tokens = d_tok + max_b;
-      auto iteration = [&] {
-        for (int l = 0; l < n_sw; ++l) E.layer_decode(0, db, true, true);
-        if (E.shard().head) E.head_decode(db);
+      auto run_k = [&](cudaEvent_t* e) {
+        EXG_CUDA(cudaEventRecord(e[0], st));
+        for (int k = 1; k <= KMAX; ++k) {
+          for (int l = 0; l < n_sw; ++l) E.layer_decode(0, db, true, true);
+          if (E.shard().head) E.head_decode(db);
+          EXG_CUDA(cudaEventRecord(e[k], st));
+        }
+        EXG_CUDA(cudaEventSynchronize(e[KMAX]));
       };
-      std::vector<double> dv;
-      for (int r = 0; r < reps; ++r) {
-        const auto h0 = std::chrono::steady_clock::now();   // sustained encode, then the iteration
+      std::vector<std::vector<double>> ex(ks.size());
+      for (int r = 0; r < std::max(2, reps - 1); ++r) {
+        const auto h0 = std::chrono::steady_clock::now();   // sustained encode ...
         while (std::chrono::duration<double>(std::chrono::steady_clock::now() - h0).count() < 0.06) {
           for (int k = 0; k < 2; ++k) E.layer_encode(0, hb, false, true);
           EXG_CUDA(cudaStreamSynchronize(st));
         }
-        for (int k = 0; k < 2; ++k) E.layer_encode(0, hb, false, true);   // still running when the iteration is queued
-        EXG_CUDA(cudaEventRecord(e0, st));
-        iteration();
-        EXG_CUDA(cudaEventRecord(e1, st));
-        EXG_CUDA(cudaEventSynchronize(e1));
-        std::this_thread::sleep_for(std::chrono::milliseconds(60));   // clock recovers
-        EXG_CUDA(cudaEventRecord(e2, st));
-        iteration();
-        EXG_CUDA(cudaEventRecord(e3, st));
-        EXG_CUDA(cudaEventSynchronize(e3));
-        float ms_a = 0, ms_b = 0;
-        EXG_CUDA(cudaEventElapsedTime(&ms_a, e0, e1));
-        EXG_CUDA(cudaEventElapsedTime(&ms_b, e2, e3));
-        dv.push_back(std::max(0.0, (ms_a - ms_b) * 1e-3));
+        for (int k = 0; k < 2; ++k) E.layer_encode(0, hb, false, true);   // ... still running when decode is queued
+        run_k(ev.data());
+        std::this_thread::sleep_for(std::chrono::milliseconds(80));       // the clock recovers
+        run_k(ev.data() + KMAX + 1);
+        for (size_t j = 0; j < ks.size(); ++j) {
+          float ma = 0, mb = 0;
+          EXG_CUDA(cudaEventElapsedTime(&ma, ev[0], ev[ks[j]]));
+          EXG_CUDA(cudaEventElapsedTime(&mb, ev[KMAX + 1], ev[KMAX + 1 + ks[j]]));
+          ex[j].push_back(std::max(0.0, (ma - mb) * 1e-3));
+        }
       }
-      std::sort(dv.begin(), dv.end());
-      swt.x.push_back(b);
-      swt.t.push_back(dv[dv.size() / 2]);
+      std::vector<double> row;
+      for (auto& v : ex) {
+        std::sort(v.begin(), v.end());
+        row.push_back(v[v.size() / 2]);
+      }
+      for (size_t j = 1; j < row.size(); ++j) row[j] = std::max(row[j], row[j - 1]);   // cumulative: non-decreasing
+      swt.t.push_back(row);
     }
-    for (cudaEvent_t e : {e0, e1, e2, e3}) cudaEventDestroy(e);
+    for (auto& e : ev) cudaEventDestroy(e);
     EXG_CUDA(cudaStreamSynchronize(st));
     cudaFree(d_tok);
   }
@@ -345,7 +358,7 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
     P.head = hd;
     P.has_head = true;
   }
-  if (!swt.x.empty()) {
+  if (!swt.b.empty()) {
     P.sw = swt;
     P.has_sw = true;
   }

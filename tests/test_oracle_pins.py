@@ -410,17 +410,22 @@ def test_switch_table_and_rms_attention_length():
     d = task_dists("S")
     p0 = _const_profile(0.5, 0.01)
     p1 = sim.Profile.loads(p0.dumps())
-    p1.switch = sim.Table1D([1.0, 1000.0], [0.003, 0.003 + 999 * 2e-6])
+    # cumulative extra time of the first k decode iterations: 0.003 + 2e-6 (b-1)
+    # per iteration for k <= 8, flat beyond (the clock has recovered)
+    ks = [1.0, 2.0, 4.0, 8.0, 16.0]
+    p1.switch = sim.Table2D([1.0, 1000.0], ks, [[(0.003 + (b - 1) * 2e-6) * min(k, 8.0) for k in ks]
+                                                for b in (1.0, 1000.0)])
     assert sim.Profile.loads(p1.dumps()).dumps() == p1.dumps()
     S0 = sim.Simulator(p0, _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
     S1 = sim.Simulator(p1, _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
-    s = S0.rra_schedule(16, 8, 1, 0)
-    e0, e1 = S0.simulate(s), S1.simulate(s)
-    w = 0.003 + (s.b_d - 1) * 2e-6                         # b_1 = B_D
-    assert s.b_e / e1.thrput_seq_s - s.b_e / e0.thrput_seq_s == pytest.approx(w, rel=1e-9)
-    assert e1.latency_s - e0.latency_s == pytest.approx(8 * w, rel=1e-9)    # 8 cycles of the 63-token query
+    for n_d, k in ((8, 8.0), (4, 4.0), (30, 8.0)):
+        s = S0.rra_schedule(16, n_d, 1, 0)
+        e0, e1 = S0.simulate(s), S1.simulate(s)
+        w = (0.003 + (s.b_d - 1) * 2e-6) * k                # b_1 = B_D, k = min(N_D, table)
+        assert s.b_e / e1.thrput_seq_s - s.b_e / e0.thrput_seq_s == pytest.approx(w, rel=1e-9)
+        assert e1.latency_s - e0.latency_s == pytest.approx(-(-63 // n_d) * w, rel=1e-9)   # one per cycle
     st0, st1 = S0.simulate_static(8), S1.simulate_static(8)
-    assert st1.latency_s - st0.latency_s == pytest.approx(0.003 + 7 * 2e-6, rel=1e-9)
+    assert st1.latency_s - st0.latency_s == pytest.approx((0.003 + 7 * 2e-6) * 8, rel=1e-9)
     # RMS length: an attention table t = c^2 (per request) makes the encode
     # attention term b * E[n^2]
     p2 = sim.Profile.loads(p0.dumps())

@@ -266,7 +266,8 @@ def _synthetic_profile(model, tps=(1, 2, 4, 8)):
     p.pp_sync = sim.Table1D([0, 1e6, 1e9, 1e12, 1e15], [8e-6, 1e-5, 1.3e-3, 1.3, 1300.0])
     vbytes = model.vocab * d * 2
     p.head = sim.Table1D(bs, [4e-6 + max(vbytes / 6e12, b * 2 * model.vocab * d / 1.2e15) for b in bs])
-    p.switch = sim.Table1D(bs, [1e-4 * (1 + b / 512.0) / 3 for b in bs])
+    ks = [1, 2, 4, 8, 16, 32]
+    p.switch = sim.Table2D(bs, ks, [[1e-4 * (1 + b / 512.0) * min(k, 8) / 3 for k in ks] for b in bs])
     return p
 
 
