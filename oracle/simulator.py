@@ -222,6 +222,7 @@ class SimCluster:
 
 
 RRA, WAA_C, WAA_M, STATIC = 1, 2, 4, 8
+Z99 = 2.3263478740408408   # standard normal 0.99 quantile (RRA latency buffer)
 
 
 @dataclass
@@ -326,6 +327,8 @@ class Simulator:
         for k in range(1, len(self.pmf_in) + 1):
             m2 += float(k) * float(k) * float(self.pmf_in[k - 1])
         self.s_e_rms = math.sqrt(m2)
+        var = m2 - self.s_e * self.s_e                       # input-length variance
+        self.s_e_sd = math.sqrt(var if var > 0.0 else 0.0)
         self.use_little = use_little_fraction
         self.n_layers = model.n_dec_layers                   # decoder-only: every layer runs both phases
         self.k_dec = 3 if model.arch == "t5" else 2
@@ -477,6 +480,17 @@ class Simulator:
         for u in range(r - 1):
             lat += Pi[u]
         lat += Fu[r - 1]
+        # buffer time: the encoder workload of the query's q
+        # encode phases varies with the input lengths (Table 9);
+        # its 99th-percentile excess, z99 sqrt(q B_E) sigma_in tokens spread
+        # over the q phases, at the profile's encode cost (DESIGN.md reading)
+        if self.s_e_sd > 0.0:
+            db = Z99 * self.s_e_sd * math.sqrt(q * s.b_e) / (q * self.s_e)
+            try:
+                T_buf = fill(self.stage_times(s.stages, "enc", (s.b_e + db) / P), P)
+            except OutOfHull:
+                return Estimate(0.0, 0.0, INF, False)
+            lat += q * (T_buf - T_encph)
         return Estimate(thr, thr * self.s_d, lat)
 
     # -- WAA (S7) -----------------------------------------------------------

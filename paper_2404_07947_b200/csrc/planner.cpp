@@ -17,6 +17,8 @@ namespace plan {
 
 static const double INF = std::numeric_limits<double>::infinity();
 
+static constexpr double Z99 = 2.3263478740408408;   // standard normal 0.99 quantile (RRA latency buffer)
+
 // ---------------------------------------------------------------- profile --
 static std::string g17(double v) {
   char buf[64];
@@ -297,6 +299,8 @@ Simulator::Simulator(const Profile& p_, const exg_model_spec& m_, const exg_clus
     double m2 = 0.0;
     for (size_t k = 1; k <= pmf_in.size(); ++k) m2 += (double)k * (double)k * pmf_in[k - 1];
     s_e_rms = std::sqrt(m2);
+    const double var = m2 - s_e * s_e;   // input-length variance
+    s_e_sd = std::sqrt(var > 0.0 ? var : 0.0);
   }
   n_layers = m.n_dec_layers;
   k_dec = m.arch == EXG_ARCH_T5 ? 3 : 2;
@@ -517,6 +521,19 @@ Est Simulator::simulate_rra(const Sched& s) {
   double lat = (q - 1) * T_cyc + T_encph;
   for (int u = 0; u < r - 1; ++u) lat += Pi[u];
   lat += Fu[r - 1];
+  // buffer time: the 99th-percentile excess of the encoder
+  // workload over the query's q encode phases, z99 sqrt(q B_E) sigma_in
+  // tokens spread over the q phases, at the profile's encode cost
+  if (s_e_sd > 0.0) {
+    const double db = Z99 * s_e_sd * std::sqrt((double)(q * s.b_e)) / (q * s_e);
+    double T_buf;
+    try {
+      T_buf = fill(stage_times(s.stages, true, (s.b_e + db) / P), P);
+    } catch (const OutOfHull&) {
+      return bad;
+    }
+    lat += q * (T_buf - T_encph);
+  }
   return Est{thr, thr * s_d, lat, true};
 }
 

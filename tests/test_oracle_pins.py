@@ -436,3 +436,37 @@ def test_switch_table_and_rms_attention_length():
     a = S2.layer_enc(1, 1.0) - S0.layer_enc(1, 1.0)
     assert a == pytest.approx(e_n2, rel=2e-3)           # piecewise-linear table of c^2
     assert e_n2 > 1.25 * S2.s_e ** 2                     # task S: RMS length ~1.14 x the mean
+
+
+def test_rra_latency_buffer_closed_form():
+    """RRA latency buffer (PAPER.md:397 reading): on a profile whose encode
+    layer time is linear in tokens (slope a per token per layer) the latency
+    grows by exactly L a z99 sqrt(q B_E) sigma_in -- the 99th-percentile excess
+    of the encoder workload over the query's q phases -- and throughput is
+    unchanged; sigma_in is the input PMF's standard deviation."""
+    from test_oracle_scheduler import _one_layer_model
+    d = task_dists("S")
+    a = 2e-6
+
+    def prof(slope):
+        p = sim.Profile([1])
+        p.attn[("enc", 1)] = sim.Table2D([1, 4096], [1, 4096], [[0.0, 0.0], [0.0, 0.0]])
+        p.attn[("dec", 1)] = sim.Table2D([1, 4096], [1, 4096], [[0.0, 0.0], [0.0, 0.0]])
+        p.rest[("enc", 1)] = sim.Table1D([0.0, 1e9], [0.01, 0.01 + slope * 1e9])
+        p.rest[("dec", 1)] = sim.Table1D([1, 1e9], [0.01, 0.01])
+        p.pp_sync = sim.Table1D([0, 1e15], [0.0, 0.0])
+        return p
+    S = sim.Simulator(prof(a), _one_layer_model(), sim.SimCluster(1, 1e30), d.pmf_in, d.pmf_out, 63)
+    mean = sum(k * d.pmf_in[k - 1] for k in range(1, len(d.pmf_in) + 1))
+    sd = math.sqrt(sum((k - mean) ** 2 * d.pmf_in[k - 1] for k in range(1, len(d.pmf_in) + 1)))
+    assert S.s_e_sd == pytest.approx(sd, rel=1e-9)
+    for b_e, n_d in ((16, 8), (40, 32), (60, 63)):
+        s = S.rra_schedule(b_e, n_d, 1, 0)
+        e = S.simulate(s)
+        q = -(-63 // n_d)
+        T_enc = 0.01 + a * b_e * mean
+        T_dec = 0.01
+        r = 1 + (63 - 1) % n_d
+        lat0 = (q - 1) * (T_enc + n_d * T_dec) + T_enc + r * T_dec
+        assert e.latency_s - lat0 == pytest.approx(a * sim.Z99 * math.sqrt(q * b_e) * sd, rel=1e-6)
+        assert e.thrput_seq_s == pytest.approx(b_e / (T_enc + n_d * T_dec), rel=1e-12)

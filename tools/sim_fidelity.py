@@ -23,7 +23,7 @@ import bench  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--requests", type=int, default=1024)
-    ap.add_argument("--margin", type=float, default=0.15)
+    ap.add_argument("--margins", default="0.15", help="comma-separated latency margins to run")
     ap.add_argument("--little", type=int, default=1)
     ap.add_argument("--bounds", default="p10,p30,p70,inf")
     args = ap.parse_args()
@@ -52,14 +52,14 @@ def main():
     L = m.n_dec_layers
     out = {"bounds": {}}
     ctx.run(X.rra_schedule(8, 16, 8), reqs[:64], slot_ctx=slot_ctx)   # warm-up
-    for name in args.bounds.split(","):
+    for name, margin in [(b, float(m)) for b in args.bounds.split(",") for m in args.margins.split(",")]:
         L_b = bounds[name]
-        s, e = X.schedule_find(prof, ctx.mspec, cl, pin, pout, d.target_len, L_b * (1 - args.margin), X.EXG_RRA,
+        s, e = X.schedule_find(prof, ctx.mspec, cl, pin, pout, d.target_len, L_b * (1 - margin), X.EXG_RRA,
                                X.search_opts(b_e_max=bench.B_E_MAX, little=args.little))
         tr = []
         _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx, trace=tr)
         tr = np.array(tr)
-        np.save(os.path.join(ROOT, "gpurun_out", "sim_trace_%s.npy" % name), tr)
+        np.save(os.path.join(ROOT, "gpurun_out", "sim_trace_%s_m%g.npy" % (name, margin)), tr)
         enc, dec = tr[tr[:, 0] == 1], tr[tr[:, 0] == 2]
 
         def pred_enc(rows, toks):
@@ -87,7 +87,7 @@ def main():
         bu = sq.rra_iteration_batches(sim_s.b_d, pu)
         upto = [lat[i] for i, r in enumerate(reqs) if r.output_len <= d.target_len]
         row = {
-            "latency_bound_s": L_b, "schedule": sched,
+            "latency_bound_s": L_b, "margin": margin, "schedule": sched,
             "predicted": {"tok_s": e.thrput_tok_s, "latency_s": e.latency_s, "b_d": sim_s.b_d,
                           "mean_b_u": float(np.mean(bu)), "T_enc_s": pred_enc(s.b_e, s.b_e * S.s_e),
                           "T_dec_mean_s": float(np.mean([pred_dec(b, b * S.ctx_mean) for b in bu]))},
@@ -103,8 +103,9 @@ def main():
                                 "p99_residual_pct_after_profile_model": float(100 * np.percentile(resid, 99) / dec[:, 2].mean())},
             "decode_gap_s_mean": float(np.mean(np.diff(dec[:, 1]) - dec[:-1, 2])) if len(dec) > 1 else None,
         }
-        out["bounds"][name] = row
-        print(name, json.dumps(row))
+        row["sla_b_met"] = bool(max(upto) < L_b)
+        out["bounds"]["%s_m%g" % (name, margin)] = row
+        print(name, margin, json.dumps(row))
         sys.stdout.flush()
     json.dump(out, open(os.path.join(ROOT, "gpurun_out", "sim_fidelity.json"), "w"), indent=1)
 
