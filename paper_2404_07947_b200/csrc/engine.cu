@@ -159,6 +159,7 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
   if (D.f32 && (t5_ || shard.tp != 1 || !shard.embed || !shard.head || shard.l0 != 0 ||
                 (shard.l1 >= 0 && shard.l1 != s.n_dec_layers)))
     throw std::invalid_argument("the fp32 path runs decoder-only models on one GPU (whole model, no TP / PP)");
+  defer_ = !t5_ && !D.f32 && shard.tp == 1 && s.d_model % 4 == 0 && s.d_model <= 16384 && deferred_enabled();
   if (S_.l1 < 0) S_.l1 = D.L;
   if (S_.l0 < 0 || S_.l1 > D.L || S_.l0 >= S_.l1) throw std::invalid_argument("bad shard layer range");
   if (S_.tp < 1 || D.H % S_.tp || D.ff % S_.tp || S_.tp_rank < 0 || S_.tp_rank >= S_.tp)
@@ -380,9 +381,11 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   const size_t f32_act = D.f32 ? al(T * D.d * 4) + al(T * 3 * D.inner_l * 4) + al(T * D.inner_l * 4) +
                                      al(T * D.ffl * 4)
                                : 0;
+  const size_t dq = defer_ ? deferred_floats(3 * D.inner_l, D.d, (int)R) : 0;
+  const size_t dr = defer_ ? std::max(deferred_floats(D.d, D.inner_l, (int)R), deferred_floats(D.d, D.ffl, (int)R)) : 0;
   const size_t bytes = al(T * D.d * 4) + al(tp_part * 4) + al(T * D.d * 2) + al(T * 3 * D.inner_l * 2) +
                        al(T * D.inner_l * 2) + al(T * D.ffl * 2) + al(logit_rows * D.V * 4) + al(sk * 4) +
-                       al(parts * 4) + al(R * D.Hl * 4) + f32_act;
+                       al(parts * 4) + al(R * D.Hl * 4) + f32_act + al(dq * 4) + al(dr * 4);
   uint8_t* p;
   EXG_CUDA(cudaMalloc(&p, bytes));
   x_ = carve<float>(p, T * D.d);
@@ -395,6 +398,9 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   splitk_ws_ = carve<float>(p, sk);
   attn_part_ = carve<float>(p, parts);
   attn_cnt_ = carve<int32_t>(p, R * D.Hl);   // split-merge counters: zero, left at zero by each merge
+  defer_qkv_ = dq ? carve<float>(p, dq) : nullptr;
+  defer_res_ = dr ? carve<float>(p, dr) : nullptr;
+  pend_res_ = PendingResid();
   if (D.f32) {
     hf_ = carve<float>(p, T * D.d);
     qkvf_ = carve<float>(p, T * 3 * D.inner_l);
@@ -666,19 +672,29 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
     return;
   }
   if (part == 1) attn = rest = true;
+  const bool defer = defer_ && part == 0;
   if (rest) {
-    layernorm(h_, d, x_, d, w.ln1_g, w.ln1_b, B, d, 1e-5f, st_);
-    linear_dec(h_, d, B, w.Wqkv, 3 * il, d, epi_bf16(w.bqkv, qkv_, 3 * il));
+    ln_decode(w.ln1_g, w.ln1_b, B);
+    EpiParams e = epi_bf16(w.bqkv, qkv_, 3 * il);
+    if (defer) e.defer_out = defer_qkv_;   // q / k / v summed by the attention kernel
+    linear_dec(h_, d, B, w.Wqkv, 3 * il, d, e);
   }
   if (attn) {
     // K7 fused: the attention kernel appends the new token's K / V (from the
-    // qkv buffer) to the cache at position n_keys - 1
+    // qkv buffer, or the deferred QKV segments) to the cache at position
+    // n_keys - 1
     DecodeAttnArgs da;
     da.knew = qkv_ + il;
     da.vnew = qkv_ + 2 * il;
     da.ldnew = 3 * il;
     da.q = qkv_;
     da.ldq = 3 * il;
+    if (defer) {
+      da.qkv_part = defer_qkv_;
+      da.qkv_si = decode_seg_info(3 * il, d);
+      da.qkv_bias = w.bqkv;
+      da.qkv_inner = il;
+    }
     da.kc = kc(l);
     da.vc = vc(l);
     da.slot = db.slot;
@@ -702,15 +718,45 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
   }
   if (part == 1) return;
   if (rest) {
-    resid_update(true, ctx_, il, B, w.Wo, il, w.bo);
-    layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, B, d, 1e-5f, st_);
+    if (defer) {
+      // O-projection: segments only; the residual update + LN2 in one kernel
+      EpiParams e;
+      e.mode = EPI_RESID;
+      e.defer_out = defer_res_;
+      linear_dec(ctx_, il, B, w.Wo, d, il, e);
+      pend_res_ = PendingResid{defer_res_, decode_seg_info(d, il), w.bo};
+    } else {
+      resid_update(true, ctx_, il, B, w.Wo, il, w.bo);
+    }
+    ln_decode(w.ln2_g, w.ln2_b, B);
     linear_dec(h_, d, B, w.W1, D.ffl, d, epi_bf16(w.b1, ff_, D.ffl, D.act));
-    resid_update(true, ff_, D.ffl, B, w.W2, D.ffl, w.b2);
+    // FFN2 deferred when a LayerNorm of this engine follows (the next layer's
+    // LN1 or the final norm); a non-last pipeline stage hands x on as is
+    if (defer && (l + 1 < n_layers() || S_.head)) {
+      EpiParams e;
+      e.mode = EPI_RESID;
+      e.defer_out = defer_res_;
+      linear_dec(ff_, D.ffl, B, w.W2, d, D.ffl, e);
+      pend_res_ = PendingResid{defer_res_, decode_seg_info(d, D.ffl), w.b2};
+    } else {
+      resid_update(true, ff_, D.ffl, B, w.W2, D.ffl, w.b2);
+    }
   }
+}
+
+void Engine::ln_decode(const bf16* g, const bf16* b, int rows) {
+  if (pend_res_.P) {
+    const PendingResid pr = pend_res_;
+    pend_res_ = PendingResid();
+    if (layernorm_deferred(h_, D.d, x_, D.d, pr.P, pr.si, pr.bias, g, b, rows, D.d, 1e-5f, st_)) return;
+    throw std::logic_error("deferred LayerNorm: unsupported shape");
+  }
+  layernorm(h_, D.d, x_, D.d, g, b, rows, D.d, 1e-5f, st_);
 }
 
 void Engine::embed_decode(const DecodeBatch& db) {
   const int B = db.B;
+  pend_res_ = PendingResid();   // a new iteration's residual stream starts here
   if (B > cap_rows_) throw std::invalid_argument("decode batch exceeds workspace");
   if (S_.embed && B > 0) {
     // T5: no position embedding (pos_emb_ null)
@@ -738,7 +784,7 @@ void Engine::head_decode(const DecodeBatch& db) {
     if (t5_)  // tied head of T5: logits = (RMS_f(x) d^-1/2) E^T (the scale folded into the norm output)
       rmsnorm(h_, D.d, x_, D.d, lnf_g_, B, D.d, T5_EPS, (float)(1.0 / std::sqrt((double)D.d)), st_);
     else
-      layernorm(h_, D.d, x_, D.d, lnf_g_, lnf_b_, B, D.d, 1e-5f, st_);
+      ln_decode(lnf_g_, lnf_b_, B);
     EpiParams e;
     e.mode = EPI_F32;
     e.out_f32 = logits_;

@@ -215,6 +215,18 @@ class Engine {
   float* logits_ = nullptr;
   // fp32 path activations: norm output, q|k|v, attention context, FFN1 output
   float *hf_ = nullptr, *qkvf_ = nullptr, *ctxf_ = nullptr, *fff_ = nullptr;
+  // deferred stream-K reductions of the decode GEMMs (gemm_tc.cuh): QKV
+  // segments summed by the decode attention, O-projection / FFN2 segments by
+  // the following LayerNorm (decoder-only, tp = 1, bf16)
+  bool defer_ = false;
+  float *defer_qkv_ = nullptr, *defer_res_ = nullptr;
+  struct PendingResid {
+    const float* P = nullptr;
+    SegInfo si;
+    const bf16* bias = nullptr;
+  } pend_res_;
+  // LayerNorm of x into h_, folding a pending deferred residual update first
+  void ln_decode(const bf16* g, const bf16* b, int rows);
   float* splitk_ws_ = nullptr;
   size_t splitk_cap_ = 0;
   float* attn_part_ = nullptr;

@@ -490,7 +490,20 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
       const bool row_ok = gm < M;
       float* pp = nullptr;
-      if (!u.full) {
+      if (SWAP && ep.defer_out) {
+        // deferred reduction: the raw segment, [seg][token][feature]
+        // (a warp's 32 features of one token are one 128-byte line)
+        float* dst = ep.defer_out + ((int64_t)u.seg * N) * M + gm;
+        for (int c = c_lo; c < c_hi; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
+          const int t0 = u.n * BN + c;
+          if (row_ok)
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (t0 + j < N) dst[(int64_t)(t0 + j) * M] = v[j];
+        }
+      } else if (!u.full) {
         // fp32 partial segment, column-major [BN][128] per (chunk, tile, seg)
         pp = partial + (((int64_t)u.n * work.tiles_m + u.m) * work.max_segs + u.seg) * (int64_t)(BM * BN);
         for (int c = c_lo; c < c_hi; c += 16) {
@@ -517,7 +530,7 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
       ++ui;
-      if (!u.full && inkernel_fixup) {
+      if (!u.full && inkernel_fixup && !(SWAP && ep.defer_out)) {
         // stream-K fixup: the CTA completing the tile's last segment reduces
         const int64_t x0 = (int64_t)u.m * work.nkb;
         const int nseg = sk_owner(work, x0 + work.nkb - 1) - sk_owner(work, x0) + 1;
@@ -706,7 +719,7 @@ void launch(const CUtensorMap& tx, const bf16* Wb, int M, int N, int K, int n_wb
   EXG_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, S, SWAP>, tx, Wb, M, N, n_wblk, w, ep, partial, counters,
                               inkernel ? 1 : 0, gemm_dbg_arg(SWAP)));
   EXG_CHECK_LAUNCH();
-  if (SWAP && !inkernel) {
+  if (SWAP && !inkernel && !ep.defer_out) {
     dim3 grid(w.tiles_m * w.tiles_n, BN / 32);
     launch_pdl(streamk_reduce_kernel<BN, SWAP>, dim3(grid), dim3(128), 0, st, partial, M, N, w, ep);
     EXG_CHECK_LAUNCH();
@@ -995,6 +1008,25 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
+bool& deferred_enabled() {
+  static bool on = true;
+  return on;
+}
+
+SegInfo decode_seg_info(int features, int K) {
+  const Work w = make_work(features, 1, K, 32, true);   // the cut does not depend on tokens / BN
+  SegInfo s;
+  s.nkb = w.nkb;
+  s.G = w.G;
+  s.I = w.I;
+  return s;
+}
+
+size_t deferred_floats(int features, int K, int tokens) {
+  const Work w = make_work(features, 1, K, 32, true);
+  return (size_t)(w.max_segs) * tokens * features;
+}
+
 int decode_bn(int tokens) {
   if (tokens <= 32) return 32;
   if (tokens <= 64) return 64;
@@ -1046,6 +1078,8 @@ void linear(const LinearArgs& a, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
+// deferred stream-K reductions for engines created after the call (1 = on, default)
+extern "C" void exg_diag_deferred(int on) { exg::deferred_enabled() = on != 0; }
 extern "C" void exg_diag_gemm_sk_ctas(int n) { exg::gemm_sk_ctas() = n; }
 extern "C" void exg_diag_gemm_slab_mb(int mb) { exg::gemm_slab_mb() = mb; }
 // span recording: reset clears the arrays and the launch counter; read copies

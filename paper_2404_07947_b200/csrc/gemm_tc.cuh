@@ -41,7 +41,33 @@ struct EpiParams {
   const int32_t* kv_slot = nullptr;
   const int32_t* kv_pos = nullptr;
   int kv_inner = 0, kv_H = 0, kv_dh = 0, kv_ctx = 0;
+  // decode (swap-AB) only -- deferred stream-K reduction: every work unit
+  // stores its raw fp32 accumulator segment to defer_out[seg][token][feature]
+  // (seg = the unit's segment index within its 128-feature tile) and the
+  // kernel ends there: no partial round trip, counters or fixup tail.  The
+  // consumer kernel sums a feature's segments in segment order, adds the
+  // bias and applies the epilogue (seg_count / SegInfo below) -- the same
+  // arithmetic as the in-kernel fixup, so results are bit-identical.
+  float* defer_out = nullptr;
 };
+
+// Stream-K cut of a decode GEMM's weight shape (tiles of 128 features x 64-k
+// blocks over G CTAs): a function of the weight shape only (T13).  Feature
+// tile m has seg_count(m) segments, summed in order by the consumer of a
+// deferred reduction.
+struct SegInfo {
+  int nkb = 0, G = 0;
+  int64_t I = 0;   // tiles_m * nkb
+};
+__host__ __device__ inline int seg_count(const SegInfo& s, int m) {
+  const int64_t x0 = (int64_t)m * s.nkb, x1 = x0 + s.nkb - 1;
+  auto owner = [&](int64_t x) { return (int)(((x + 1) * s.G + s.I - 1) / s.I) - 1; };
+  return owner(x1) - owner(x0) + 1;
+}
+SegInfo decode_seg_info(int features, int K);
+bool& deferred_enabled();   // diagnostics switch (exg_diag_deferred)
+// floats a deferred decode GEMM writes: max segments x tokens x features
+size_t deferred_floats(int features, int K, int tokens);
 
 // ---- blocked weight layout ---------------------------------------------------
 inline int64_t blocked_elems(int64_t rows, int64_t K) {

@@ -188,6 +188,110 @@ static bool norm_reg(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf
   return true;
 }
 
+// Deferred stream-K reduction folded into the LayerNorm (decode, tp = 1):
+// x[row] += (sum_seg P[seg][row][:] + bias) -- the residual update of the
+// preceding O-projection / FFN2, whose GEMM stored only its raw segments --
+// written back to x, then the LayerNorm of norm_reg_kernel on the updated row
+// (same arithmetic, bit-identical to the in-kernel fixup + LayerNorm).
+template <int NV>
+__global__ void __launch_bounds__(256) resid_reduce_ln_kernel(bf16* __restrict__ y, int64_t ldy, float* __restrict__ x,
+                                                              int64_t ldx, const float* __restrict__ P, int tokens,
+                                                              SegInfo si, const bf16* __restrict__ rbias,
+                                                              const bf16* __restrict__ g, const bf16* __restrict__ b,
+                                                              int d, float eps) {
+  griddep_launch_dependents();
+  griddep_wait();  // launched with PDL: predecessors complete + visible
+  __shared__ float red[8];
+  const int row = blockIdx.x;
+  float4* xr = reinterpret_cast<float4*>(x + (int64_t)row * ldx);
+  const int n4 = d >> 2;
+  float4 v[NV];
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = threadIdx.x + k * 256;
+    if (i < n4) {
+      const int f0 = 4 * i;
+      const int ns = seg_count(si, f0 >> 7);
+      const float4* p = reinterpret_cast<const float4*>(P + (int64_t)row * d + f0);
+      const int64_t segstride4 = (int64_t)tokens * d / 4;
+      float4 acc = __ldcg(p);
+      for (int sg = 1; sg < ns; ++sg) {
+        const float4 q = __ldcg(p + sg * segstride4);
+        acc.x += q.x;
+        acc.y += q.y;
+        acc.z += q.z;
+        acc.w += q.w;
+      }
+      if (rbias) {
+        const uint2 br = reinterpret_cast<const uint2*>(rbias)[i];
+        const float2 b01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.x));
+        const float2 b23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.y));
+        acc.x += b01.x;
+        acc.y += b01.y;
+        acc.z += b23.x;
+        acc.w += b23.y;
+      }
+      const float4 old = xr[i];
+      v[k] = make_float4(old.x + acc.x, old.y + acc.y, old.z + acc.z, old.w + acc.w);
+      xr[i] = v[k];
+    } else {
+      v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    s += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+  }
+  const float mean = block_sum_256(s, red) / (float)d;
+  float q = 0.f;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    if (threadIdx.x + k * 256 >= n4) continue;
+    const float a = v[k].x - mean, bb = v[k].y - mean, c = v[k].z - mean, e = v[k].w - mean;
+    q += (a * a + bb * bb) + (c * c + e * e);
+  }
+  const float rstd = rsqrtf(block_sum_256(q, red) / (float)d + eps);
+  bf16* yr = y + (int64_t)row * ldy;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = threadIdx.x + k * 256;
+    if (i >= n4) continue;
+    const uint2 gr = reinterpret_cast<const uint2*>(g)[i];
+    const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gr.x));
+    const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gr.y));
+    const uint2 br = reinterpret_cast<const uint2*>(b)[i];
+    const float2 b01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.x));
+    const float2 b23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.y));
+    const float o0 = (v[k].x - mean) * rstd * g01.x + b01.x;
+    const float o1 = (v[k].y - mean) * rstd * g01.y + b01.y;
+    const float o2 = (v[k].z - mean) * rstd * g23.x + b23.x;
+    const float o3 = (v[k].w - mean) * rstd * g23.y + b23.y;
+    __nv_bfloat162 p0 = __floats2bfloat162_rn(o0, o1), p1 = __floats2bfloat162_rn(o2, o3);
+    uint2 out;
+    out.x = *reinterpret_cast<uint32_t*>(&p0);
+    out.y = *reinterpret_cast<uint32_t*>(&p1);
+    reinterpret_cast<uint2*>(yr)[i] = out;
+  }
+}
+
+bool layernorm_deferred(bf16* y, int64_t ldy, float* x, int64_t ldx, const float* P, const SegInfo& si,
+                        const bf16* rbias, const bf16* g, const bf16* b, int T, int d, float eps, cudaStream_t st) {
+  if ((d & 3) || (ldx & 3) || (ldy & 3) || d > 16384) return false;
+  if (T <= 0) return true;
+  const int nv = (d / 4 + 255) / 256;
+  auto go = [&](auto kern) {
+    launch_pdl(kern, dim3(T), dim3(256), 0, st, y, ldy, x, ldx, P, T, si, rbias, g, b, d, eps);
+    EXG_CHECK_LAUNCH();
+  };
+  if (nv <= 1) go(resid_reduce_ln_kernel<1>);
+  else if (nv <= 2) go(resid_reduce_ln_kernel<2>);
+  else if (nv <= 4) go(resid_reduce_ln_kernel<4>);
+  else if (nv <= 5) go(resid_reduce_ln_kernel<5>);
+  else if (nv <= 8) go(resid_reduce_ln_kernel<8>);
+  else if (nv <= 9) go(resid_reduce_ln_kernel<9>);
+  else if (nv <= 12) go(resid_reduce_ln_kernel<12>);
+  else go(resid_reduce_ln_kernel<16>);
+  return true;
+}
+
 void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
                float eps, cudaStream_t st) {
   if (T <= 0) return;
@@ -294,6 +398,19 @@ struct DecodeCfg {
   static constexpr size_t SMEM = (size_t)STAGES * KT * ROWB * 2;
 };
 
+// feature f of row i of a deferred QKV GEMM: its segments summed in order +
+// bias (the in-kernel fixup's arithmetic), before the bf16 rounding point
+__device__ __forceinline__ float deferred_qkv(const DecodeAttnArgs& a, int i, int f) {
+  const int ns = seg_count(a.qkv_si, f >> 7);
+  const int64_t F = 3LL * a.qkv_inner;
+  const float* p = a.qkv_part + (int64_t)i * F + f;
+  const int64_t ss = (int64_t)a.B * F;
+  float acc = __ldcg(p);
+  for (int sg = 1; sg < ns; ++sg) acc += __ldcg(p + sg * ss);
+  if (a.qkv_bias) acc += bf2f(a.qkv_bias[f]);
+  return acc;
+}
+
 template <int DH, int ST, int MB = 1>
 __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) {
   griddep_launch_dependents();
@@ -324,16 +441,28 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
     fence_barrier_init();
   }
-  if (tid < DH) qs[tid] = bf2f(a.q[(int64_t)i * a.ldq + h * DH + tid]);
+  if (tid < DH)
+    qs[tid] = a.qkv_part ? bf2f(f2bf(deferred_qkv(a, i, h * DH + tid))) : bf2f(a.q[(int64_t)i * a.ldq + h * DH + tid]);
   // fused KV append: this split holds the new key nk-1 -> write its K / V row
   // to the cache, and patch it into its shared-memory tile after the bulk copy
   // of that tile (which may carry the stale cache row) has landed
   const int r_new = nk - 1 - k_begin;
-  const bool app = a.knew != nullptr && r_new < n;
+  const bool app = (a.knew != nullptr || a.qkv_part != nullptr) && r_new < n;
   int4 new_chunk = make_int4(0, 0, 0, 0);
   if (app && tid < 2 * C::CH) {
     const int which = tid / C::CH, c = tid % C::CH;
-    new_chunk = *reinterpret_cast<const int4*>((which ? a.vnew : a.knew) + (int64_t)i * a.ldnew + h * DH + c * 8);
+    if (a.qkv_part) {
+      const int f0 = (1 + which) * a.qkv_inner + h * DH + c * 8;
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(deferred_qkv(a, i, f0 + 2 * e), deferred_qkv(a, i, f0 + 2 * e + 1));
+        w[e] = *reinterpret_cast<uint32_t*>(&h2);
+      }
+      new_chunk = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+    } else {
+      new_chunk = *reinterpret_cast<const int4*>((which ? a.vnew : a.knew) + (int64_t)i * a.ldnew + h * DH + c * 8);
+    }
     bf16* dst = const_cast<bf16*>(which ? vbase : kbase) + (int64_t)r_new * DH + c * 8;
     *reinterpret_cast<int4*>(dst) = new_chunk;
   }

@@ -3,6 +3,7 @@
 // attention, K4 prefill attention, K8 argmax, K9 row compaction.
 #pragma once
 #include "common.cuh"
+#include "gemm_tc.cuh"
 
 namespace exg {
 
@@ -35,6 +36,11 @@ void embed(float* x, const int32_t* ids, const int32_t* pos, const bf16* tok_emb
 // ---- K2: y = bf16(LN(x) * g + b), fp32 statistics, eps 1e-5 ----------------
 void layernorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, const bf16* b, int T, int d,
                float eps, cudaStream_t st);
+// the same after folding a deferred residual GEMM (gemm_tc.cuh SegInfo):
+// x += sum_seg P[seg][row][:] + rbias, written back, then LN.  Returns false
+// (nothing launched) when the shape needs the strided kernels.
+bool layernorm_deferred(bf16* y, int64_t ldy, float* x, int64_t ldx, const float* P, const SegInfo& si,
+                        const bf16* rbias, const bf16* g, const bf16* b, int T, int d, float eps, cudaStream_t st);
 
 // ---- T5 RMSNorm: y = bf16(x rsqrt(mean(x^2) + eps) g out_scale) ----------
 void rmsnorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, int T, int d, float eps,
@@ -84,6 +90,13 @@ struct DecodeAttnArgs {
   const bf16* knew = nullptr;
   const bf16* vnew = nullptr;
   int64_t ldnew = 0;
+  // deferred QKV reduction (gemm_tc.cuh): when qkv_part is set, q / knew /
+  // vnew of row i are bf16(sum_seg qkv_part[seg][i][f] + qkv_bias[f]) with f
+  // = h*dh + j, inner + h*dh + j, 2 inner + h*dh + j (q, knew, vnew ignored)
+  const float* qkv_part = nullptr;
+  SegInfo qkv_si;
+  const bf16* qkv_bias = nullptr;
+  int qkv_inner = 0;
 };
 void decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
 int& decode_split_override();   // diagnostics: key split length (0 = default)

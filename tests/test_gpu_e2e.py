@@ -214,3 +214,31 @@ def test_dynamic_adjustment_narrow_inputs_stays_in_capacity(setup):
     for r in range(len(same)):
         assert np.array_equal(a[3][r], b[3][r]), r
     assert b[2]["encode_phases"] >= len(same) // 10
+
+
+@pytest.mark.parametrize("n_req,b_d", [(24, 20), (160, 150)])
+def test_deferred_stream_k_reduction_bit_identical(n_req, b_d):
+    """Deferred stream-K reduction of the decode GEMMs (QKV segments summed
+    in the attention kernel, O-projection / FFN2 segments in the following
+    LayerNorm; gemm_tc.cuh) is the in-kernel fixup's arithmetic moved to the
+    consumer: ids and logits bit-identical to the fixup path, on a model wide
+    enough that every weight tile is split across CTAs (3-6 segments), at
+    decode batches on the BN = 32 / 64 and BN = 256 token tiles."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2404_07947_b200 as X
+    from workload import ModelSpec, make_requests, uniform_pmf
+    spec = ModelSpec("defer-w2048", "opt", 0, 2, 2048, 16, 128, 8192, 4096, 512)
+    reqs = make_requests(n_req, uniform_pmf(8, 64), uniform_pmf(2, 12), spec.vocab, 0xD3F)
+    outs = []
+    for on in (0, 1):
+        X.lib().exg_diag_deferred(on)
+        try:
+            ctx = X.Context(spec, 0xE6E0_0D3F)
+            outs.append(ctx.run(X.rra_schedule(min(n_req, b_d), b_d, 4), reqs, dump=range(len(reqs))))
+            ctx.close()
+        finally:
+            X.lib().exg_diag_deferred(1)
+    assert outs[0][0] == outs[1][0]
+    for r in range(len(reqs)):
+        assert np.array_equal(outs[0][3][r], outs[1][3][r]), r
