@@ -469,8 +469,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--requests", type=int, default=1024, help="requests per step")
-    ap.add_argument("--margin", type=float, default=0.15,
-                    help="latency margin for stage-time variance and the simulator's measured 7-13%% optimism")
+    ap.add_argument("--margin", type=float, default=0.03,
+                    help="latency margin on top of the simulator's buffer time (its measured latency error is "
+                         "within +-3%% on this workload, tools/sim_fidelity.py)")
     ap.add_argument("--little", type=int, default=1,
                     help="1: completion fraction by Little's law (SURVEY.md S3; DESIGN.md), 0: paper's E[1/ceil(S/N_D)]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
