@@ -127,7 +127,10 @@ typedef struct {
   float* logits_out;          /* optional fp32 [sum dumped output_len][vocab]   */
   const uint8_t* dump_mask;   /* optional [n]: 1 = dump this request's logits   */
   int32_t slot_ctx;           /* KV slot length; 0 -> max(input_len+output_len) */
-  int32_t pin_nccl_algo;      /* reserved for multi-GPU parity runs             */
+  int32_t pin_nccl_algo;      /* 1: TP partial sums exchanged and summed in member
+                                 order on every rank (bitwise the one-rank sum,
+                                 batch invariant, T13) instead of the NCCL
+                                 all-reduce on the TP sub-communicator        */
   int32_t kernel_timing;      /* 1: CUDA events around every launch of the
                                  kernel classes below (roofline evidence)       */
   double dyn_threshold;       /* > 0: dynamic workload adjustment:
@@ -219,10 +222,18 @@ exg_status exg_create_local_group(const exg_model_spec* spec, const exg_cluster_
 void exg_destroy(exg_ctx* ctx);
 
 /* ---- XProfiler --------------------------------------- */
-/* Times one encoder layer and one decoder layer on the real kernels:
- * attention over (batch x ctx) and the rest of the layer over tokens, per
- * TP degree, plus TP all-reduce and PP send costs.  Collective. */
+/* Single-GPU context: times one encoder layer and one decoder layer on the
+ * real kernels -- attention over (batch x ctx) and the rest of the layer over
+ * tokens per TP degree (a TP-rank-0 shard for t > 1), the decode head
+ * (final norm + LM head + argmax) and the encode->decode switch per batch.
+ * Multi-rank context (world > 1, collective, every rank calls it): the
+ * interconnect tables PAPER.md:154 names -- tp_sync[t] = fp32 all-reduce
+ * over ranks [0, t) for each grid TP degree t <= world, pp_sync = one hop rank
+ * 0 -> rank 1 (ping-pong / 2), 1 KB .. 1 GB; rank 0's tables are
+ * authoritative.  Merge them into a layer profile with exg_profile_copy_comm. */
 exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profile** out);
+/* Replace dst's tp_sync / pp_sync tables with src's (a multi-rank profile). */
+exg_status exg_profile_copy_comm(exg_profile* dst, const exg_profile* src);
 /* profile-v1 text file ("%.17g" numbers, lossless). */
 exg_status exg_profile_save(const exg_profile* p, const char* path);
 /* Fill the communication tables from an alpha-beta model of the

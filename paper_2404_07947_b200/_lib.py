@@ -128,6 +128,7 @@ _SIGS = {
     "exg_profile_load": (C.c_int, [C.c_char_p, C.POINTER(_P)]),
     "exg_profile_free": (None, [_P]),
     "exg_profile_comm_model": (C.c_int, [_P, C.c_double, C.c_double]),
+    "exg_profile_copy_comm": (C.c_int, [_P, _P]),
     "exg_simulate": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
                                C.POINTER(exg_pmf), C.c_int32, C.POINTER(exg_schedule), C.POINTER(exg_estimate)]),
     "exg_schedule_memory": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
@@ -262,7 +263,8 @@ class Context:
         return Profile(h)
 
     def run(self, sched: exg_schedule, requests, dump: Optional[Sequence[int]] = None, slot_ctx: int = 0,
-            kernel_timing: bool = False, dyn_threshold: float = 0.0, trace: Optional[list] = None):
+            kernel_timing: bool = False, dyn_threshold: float = 0.0, trace: Optional[list] = None,
+            pin_nccl_algo: bool = False):
         """Returns (tokens per request, latencies [s], stats dict, logits per
         dumped request [S_r][V] or None).  trace: a list that receives the
         per-stage records [kind, start, duration, rows, work] (exegpt.h)."""
@@ -277,7 +279,7 @@ class Context:
         out = np.zeros(total, dtype=np.int32)
         lat = np.zeros(n, dtype=np.float64)
         stats = exg_run_stats()
-        opts = exg_run_opts(None, None, slot_ctx, 0, int(kernel_timing), float(dyn_threshold))
+        opts = exg_run_opts(None, None, slot_ctx, int(pin_nccl_algo), int(kernel_timing), float(dyn_threshold))
         tbuf = None
         if trace is not None:
             cap = 8 * (n + 16) + 4 * total
@@ -371,6 +373,10 @@ class Profile:
     def comm_model(self, alpha_s: float, bw_bytes_per_s: float):
         """Fill tp_sync / pp_sync from an alpha-beta interconnect model."""
         check(lib().exg_profile_comm_model(self.h, alpha_s, bw_bytes_per_s))
+
+    def copy_comm(self, other: "Profile"):
+        """tp_sync / pp_sync tables from a multi-rank profile (exg_profile_copy_comm)."""
+        check(lib().exg_profile_copy_comm(self.h, other.h))
 
     def __del__(self):
         try:

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <memory>
 #include <new>
 #include <sstream>
@@ -243,7 +244,28 @@ exg_status exg_profile_run(exg_ctx* ctx, const exg_profile_grid* grid, exg_profi
   return guarded([&] {
     if (!ctx || !grid || !out) throw std::invalid_argument("null argument");
     auto p = std::make_unique<exg_profile>();
-    if (!ctx->engine) throw std::invalid_argument("profile on a single-GPU context (cluster.n_gpus = 1)");
+    if (ctx->multi && ctx->world > 1) {
+      // multi-rank context: the interconnect tables, collective
+      std::vector<int> tps;
+      for (int i = 0; i < grid->n_tp; ++i) tps.push_back(grid->tp[i]);
+      std::map<int, std::pair<std::vector<double>, std::vector<double>>> tp;
+      std::vector<double> px, pt;
+      ctx->multi->profile_comm(tps, grid->reps, &tp, &px, &pt);
+      p->p.tps.push_back(1);
+      for (auto& kv : tp) {
+        p->p.tps.push_back(kv.first);
+        exg::plan::Table1D tb;
+        tb.x = kv.second.first;
+        tb.t = kv.second.second;
+        p->p.tp_sync[kv.first] = tb;
+      }
+      p->p.pp_sync.x = px;
+      p->p.pp_sync.t = pt;
+      p->p.has_pp = true;
+      *out = p.release();
+      return EXG_OK;
+    }
+    if (!ctx->engine) throw std::invalid_argument("layer profile on a single-GPU context (cluster.n_gpus = 1)");
     if (ctx->spec.dtype != EXG_BF16) throw std::invalid_argument("the profiler times the bf16 path");
     exg::profile_layers(*ctx->engine, ctx->spec, *grid, &p->p);
     *out = p.release();
@@ -282,6 +304,17 @@ exg_status exg_profile_comm_model(exg_profile* p, double alpha_s, double bw_byte
       }
       p->p.tp_sync[t] = tb;
     }
+    return EXG_OK;
+  });
+}
+
+exg_status exg_profile_copy_comm(exg_profile* dst, const exg_profile* src) {
+  return guarded([&] {
+    if (!dst || !src) throw std::invalid_argument("null profile");
+    if (!src->p.has_pp && src->p.tp_sync.empty()) throw std::invalid_argument("source profile has no interconnect tables");
+    dst->p.tp_sync = src->p.tp_sync;
+    dst->p.pp_sync = src->p.pp_sync;
+    dst->p.has_pp = src->p.has_pp;
     return EXG_OK;
   });
 }

@@ -1185,6 +1185,110 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   }
 }
 
+void MultiCtx::profile_comm(const std::vector<int>& tps, int reps,
+                            std::map<int, std::pair<std::vector<double>, std::vector<double>>>* tp,
+                            std::vector<double>* pp_x, std::vector<double>* pp_t) {
+  Impl* p = p_;
+  if (!p->comm || p->world < 2) throw std::invalid_argument("profile_comm needs a multi-rank context (world > 1)");
+  EXG_CUDA(cudaSetDevice(p->device));
+  const int me = p->rank, world = p->world;
+  reps = std::max(1, reps);
+  std::vector<double> bytes;
+  for (double b = 1024.0; b <= (double)(1u << 30); b *= 4.0) bytes.push_back(b);
+  const size_t cap = (size_t)bytes.back();
+  void* buf = nullptr;
+  void* buf2 = nullptr;
+  EXG_CUDA(cudaMalloc(&buf, cap));
+  EXG_CUDA(cudaMalloc(&buf2, cap));
+  EXG_CUDA(cudaMemset(buf, 0, cap));
+  cudaEvent_t a, b;
+  EXG_CUDA(cudaEventCreate(&a));
+  EXG_CUDA(cudaEventCreate(&b));
+  auto median_of = [&](std::vector<double> v) {
+    std::sort(v.begin(), v.end());
+    return v[v.size() / 2];
+  };
+  cudaStream_t st = p->cst;   // the main communicator's stream
+  try {
+    // TP all-reduce tables: every t <= world, ranks [0, t)
+    std::vector<std::vector<int>> groups;
+    for (int t : tps)
+      if (t > 1 && t <= world) {
+        std::vector<int> g;
+        for (int r = 0; r < t; ++r) g.push_back(r);
+        groups.push_back(g);
+      }
+    p->comm->prepare_groups(groups);   // collective over all ranks
+    for (const auto& g : groups) {
+      const int t = (int)g.size();
+      const bool member = me < t;
+      std::vector<double> ts;
+      for (double nb : bytes) {
+        const size_t n = (size_t)nb / sizeof(float);
+        std::vector<double> v;
+        for (int r = 0; r <= reps; ++r) {   // r = 0: warm-up
+          if (!member) continue;
+          EXG_CUDA(cudaEventRecord(a, p->st));
+          if (p->comm->has_allreduce()) {
+            p->comm->allreduce_sum(static_cast<float*>(buf), n, g, p->st);
+          } else {   // exchange of the partials (the transport's TP reduction)
+            p->comm->group_start();
+            for (int q : g)
+              if (q != me) p->comm->send(buf, n * sizeof(float), q, st);
+            for (int q : g)
+              if (q != me) p->comm->recv(buf2, n * sizeof(float), q, st);
+            p->comm->group_end();
+            EXG_CUDA(cudaEventRecord(p->ev_join, st));
+            EXG_CUDA(cudaStreamWaitEvent(p->st, p->ev_join, 0));
+          }
+          EXG_CUDA(cudaEventRecord(b, p->st));
+          EXG_CUDA(cudaEventSynchronize(b));
+          float ms = 0;
+          EXG_CUDA(cudaEventElapsedTime(&ms, a, b));
+          if (r > 0) v.push_back(ms * 1e-3);
+        }
+        ts.push_back(member ? median_of(v) : 0.0);
+      }
+      (*tp)[t] = {bytes, ts};
+    }
+    // pipeline hop: ping-pong rank 0 <-> rank 1, half the round trip
+    pp_x->assign(bytes.begin(), bytes.end());
+    pp_t->clear();
+    for (double nb : bytes) {
+      const size_t n = (size_t)nb;
+      std::vector<double> v;
+      for (int r = 0; r <= reps; ++r) {
+        if (me > 1) continue;
+        EXG_CUDA(cudaEventRecord(a, st));
+        if (me == 0) {
+          p->comm->send(buf, n, 1, st);
+          p->comm->recv(buf2, n, 1, st);
+        } else {
+          p->comm->recv(buf2, n, 0, st);
+          p->comm->send(buf2, n, 0, st);
+        }
+        EXG_CUDA(cudaEventRecord(b, st));
+        EXG_CUDA(cudaEventSynchronize(b));
+        float ms = 0;
+        EXG_CUDA(cudaEventElapsedTime(&ms, a, b));
+        if (r > 0) v.push_back(ms * 1e-3 / 2);
+      }
+      pp_t->push_back(me <= 1 ? median_of(v) : 0.0);
+    }
+    p->comm->check_async();
+  } catch (...) {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(buf);
+    cudaFree(buf2);
+    throw;
+  }
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(buf);
+  cudaFree(buf2);
+}
+
 void MultiCtx::run(const exg_schedule& s, const exg_request* reqs, int n, int32_t* out_tokens, double* out_latency,
                    exg_run_stats* stats, const exg_run_opts* opts) {
   EXG_CUDA(cudaSetDevice(p_->device));

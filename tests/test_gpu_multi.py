@@ -195,3 +195,53 @@ def test_nccl_loopback_bit_identical(env, case):
         assert np.array_equal(lg[r], ref_l[r]), r
     assert np.all(lat > 0)
     nc.close()
+
+
+def test_profile_comm_tables_on_a_rank_group():
+    """XProfiler's interconnect tables on a multi-rank context:
+    every rank calls exg_profile_run (collective); tp_sync[t] for t <= world
+    and pp_sync come back on the byte grid 1 KB .. 1 GB, positive and
+    growing with the message; exg_profile_copy_comm merges them into a layer
+    profile, which the simulator then reads (here over the thread-rank
+    transport: device copies standing in for NVLink)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import threading
+    import paper_2404_07947_b200 as X
+    from oracle import simulator as sim
+    from workload import MODELS, weight_seed
+    spec = MODELS["tiny"]
+    ctxs = X.local_group(spec, weight_seed(1), 4)
+    res, err = [None] * 4, [None] * 4
+
+    def go(r):
+        try:
+            res[r] = ctxs[r].profile([1], [1], [1], reps=2, tps=[1, 2, 4])
+        except BaseException as e:  # noqa: BLE001
+            err[r] = e
+    th = [threading.Thread(target=go, args=(r,)) for r in range(4)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert all(e is None for e in err), err
+    import tempfile, os
+    with tempfile.TemporaryDirectory() as tmp:
+        res[0].save(os.path.join(tmp, "c.txt"))
+        P = sim.Profile.load(os.path.join(tmp, "c.txt"))
+        assert set(P.tp_sync) == {2, 4}
+        for t in (2, 4):
+            ts = P.tp_sync[t].t
+            assert P.tp_sync[t].x[0] == 1024.0 and P.tp_sync[t].x[-1] == float(1 << 30)
+            assert all(v > 0 for v in ts) and ts[-1] > 10 * ts[0]
+        assert all(v > 0 for v in P.pp_sync.t) and P.pp_sync.t[-1] > 10 * P.pp_sync.t[0]
+        single = X.Context(spec, weight_seed(1))
+        lay = single.profile([1, 4], [16, 48], [16, 64], reps=1, tps=[1, 2, 4])
+        lay.copy_comm(res[0])
+        lay.save(os.path.join(tmp, "m.txt"))
+        M = sim.Profile.load(os.path.join(tmp, "m.txt"))
+        assert M.tp_sync[2].t == P.tp_sync[2].t and M.pp_sync.t == P.pp_sync.t
+        assert ("dec", 4) in M.rest
+        single.close()
+    for c in ctxs:
+        c.close()
