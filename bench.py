@@ -19,9 +19,10 @@ termination, until the batch drains).  Procedure:
   5. headline bound (70th pctl): W warm-up + K timed steps, with per-launch
      kernel timing (roofline); the other bounds: one run each.
 
-With N > 1 (torchrun) every rank runs an independent replica on its own
-request stream (weak scaling): the method's multi-GPU layouts (PP / partial
-TP / WAA) are not built yet, so there is no collective in the data path.
+With N > 1 (torchrun) the default is config 4 (OPT-66B, task G) under the
+scheduler's N-GPU plan -- RRA / WAA with partial TP, pipeline hops, KV
+handoff and TP all-reduce over NCCL -- as one job (run_layout); `--layout
+replicas` runs independent config-2 replicas instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -365,71 +366,132 @@ def in_runner_baselines(args, X, ctx, prof, cl, pin, pout, d, bounds, scheds, re
     return res
 
 
+MULTI_MODEL, MULTI_TASK, MULTI_CONFIG_NO = "opt-66b", "G", 4
+MULTI_WORKLOAD = ("config 4: OPT-66B (seeded random init), task G (in 64+-23<=128, out 184+-102<=480, p99 417), "
+                  "the scheduler's N-GPU plan (RRA | WAA-C | WAA-M x partial TP) as one NCCL job")
+
+
+def multi_plans(X, prof, mspec, cl_n, pin, pout, target_len, margin, little):
+    """Config 4's plans on an N-GPU cluster: the static-batch
+    bounds of the paper's recipe, the scheduler's overall pick
+    over RRA | WAA-C | WAA-M x TP degree x applied GPUs at the 70th-percentile
+    bound, and the forced WAA plan with partial TP of degree 2.
+    Pure host (the C-ABI planner); returns a dict of schedules (bytes) and
+    estimates."""
+    bounds = static_bounds(X, prof, mspec, cl_n, pin, pout, target_len)
+    L_b = dict(bounds)["p70"]
+    out = {"bounds": bounds, "latency_bound_s": L_b}
+    opts = X.search_opts(b_e_max=B_E_MAX, little=little)
+    for name, mask, o in (("pick", X.EXG_RRA | X.EXG_WAA_C | X.EXG_WAA_M, opts),
+                          ("waa_tp2", X.EXG_WAA_C | X.EXG_WAA_M, X.search_opts(b_e_max=B_E_MAX, little=little, tp_only=2))):
+        try:
+            s, e = X.schedule_find(prof, mspec, cl_n, pin, pout, target_len, L_b * (1 - margin), mask, o)
+            out[name] = {"sched": bytes(s), "schedule": s.as_dict(), "predicted_tok_s": e.thrput_tok_s,
+                         "predicted_latency_s": e.latency_s}
+        except X.ExgError as err:
+            out[name] = {"infeasible": str(err)}
+    return out
+
+
 def run_layout(args, rank, world, local):
-    """--layout plan (opt-in): the scheduler's N-GPU schedule for the p70
-    bound run as ONE job over the N ranks -- NCCL between processes, GPU g of
-    the layout on rank g*N/G (multi.cu).  Rank 0 profiles and plans; the
-    schedule and the NCCL id are broadcast; every rank runs the same requests."""
+    """N > 1 (torchrun): config 4 -- OPT-66B on task G -- as ONE job over the N
+    ranks (one process per GPU, NCCL): GPU g of the layout on rank g*N/G
+    (multi.cu).  (1) rank 0's NCCL id is broadcast and every rank creates
+    the multi-rank context; (2) XProfiler's interconnect tables are measured
+    collectively (TP all-reduce over NCCL sub-communicators, PP hop); (3)
+    rank 0 profiles the layer tables on a one-GPU context of the full model,
+    merges the measured interconnect tables, derives the bounds and plans;
+    (4) every rank runs the scheduler's pick (W + K steps, device time from
+    the gathered stamps, max over ranks by construction) and, once, the forced
+    WAA TP-2 plan."""
     import torch
     import torch.distributed as dist
     import paper_2404_07947_b200 as X
     from paper_2404_07947_b200._lib import exg_schedule
     from workload import MODELS, make_requests, task_dists, weight_seed
-    spec = MODELS[MODEL]
-    d = task_dists(TASK)
+    spec = MODELS[args.multi_model]
+    d = task_dists(args.multi_task)
+    seed = weight_seed(MULTI_CONFIG_NO)
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     free, total = torch.cuda.mem_get_info(local)
+    mem, ws = total - (6 << 30), 8 << 30
     pin, pout = X.Pmf(d.pmf_in), X.Pmf(d.pmf_out)
-    box = [None, None]
+    box = [X.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(box, src=0)
+    ctx = X.Context(spec, seed, device=local, cluster=X.cluster_spec(world, mem, ws), rank=rank, world=world,
+                    uid=box[0])
+    tps = [t for t in (1, 2, 4, 8) if t <= world and spec.n_heads % t == 0]
+    comm_prof = ctx.profile([1], [1], [1], reps=5, tps=tps)           # collective
+    plan = [None]
     if rank == 0:
-        ctx1 = X.Context(spec, weight_seed(CONFIG_NO), device=local,
-                         cluster=X.cluster_spec(1, total - (6 << 30), 8 << 30))
-        prof = ctx1.profile(PROFILE_BATCH, PROFILE_CTX, PROFILE_TOKENS, reps=3, tps=[1, 2, 4, 8])
-        prof.comm_model(COMM_ALPHA_S, COMM_BW)
-        L_head = dict(static_bounds(X, prof, ctx1.mspec, ctx1.cluster, pin, pout, d.target_len))["p70"]
-        cl_n = X.cluster_spec(world, ctx1.cluster.mem_per_gpu_bytes, ctx1.cluster.workspace_bytes)
-        s, e = X.schedule_find(prof, ctx1.mspec, cl_n, pin, pout, d.target_len, L_head * (1 - args.margin),
-                               X.EXG_RRA | X.EXG_WAA_C, X.search_opts(b_e_max=B_E_MAX, little=args.little))
-        box = [{"sched": bytes(s), "bound": L_head, "pred": e.thrput_tok_s}, X.unique_id()]
+        ctx1 = X.Context(spec, seed, device=local, cluster=X.cluster_spec(1, mem, ws))
+        prof = ctx1.profile(PROFILE_BATCH, PROFILE_CTX, PROFILE_TOKENS, reps=3, tps=tps)
+        prof.copy_comm(comm_prof)
+        os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
+        prof.save(os.path.join(ROOT, "gpurun_out", "profile_multi.txt"))
+        plan[0] = multi_plans(X, prof, ctx1.mspec, X.cluster_spec(world, mem, ws), pin, pout, d.target_len,
+                              args.margin, args.little)
         ctx1.close()
         del ctx1
         torch.cuda.empty_cache()
-    dist.broadcast_object_list(box, src=0)
-    plan, uid = box
-    s = exg_schedule.from_buffer_copy(plan["sched"])
-    ctx = X.Context(spec, weight_seed(CONFIG_NO), device=local,
-                    cluster=X.cluster_spec(world, total - (6 << 30), 8 << 30), rank=rank, world=world, uid=uid)
-    reqs = make_requests(args.requests, d.pmf_in, d.pmf_out, spec.vocab, rank_request_seed(0))
+    dist.broadcast_object_list(plan, src=0)
+    plan = plan[0]
+    if "sched" not in plan["pick"]:
+        if rank == 0:
+            print(json.dumps({"metric": METRIC, "value": None, "n_gpus": world, "unavailable":
+                              "no schedule meets the bound: " + plan["pick"].get("infeasible", "")}))
+        ctx.close()
+        dist.destroy_process_group()
+        return
+    s = exg_schedule.from_buffer_copy(plan["pick"]["sched"])
+    L_b = plan["latency_bound_s"]
+    reqs = make_requests(args.requests, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E1_0000 + MULTI_CONFIG_NO)
     slot_ctx = len(d.pmf_in) + len(d.pmf_out)
+    h2d = sum((r.input_len - 1) * 12 + 16 + 16 * r.output_len for r in reqs)
+    d2h = sum(4 * r.output_len for r in reqs)
     for _ in range(args.warmup):
         ctx.run(s, reqs, slot_ctx=slot_ctx)
     torch.cuda.synchronize()
     dist.barrier()
-    wall, toks, lats = 0.0, 0, []
+    wall, toks, lat = 0.0, 0, None
     th0 = time.perf_counter()
-    for _ in range(args.steps):
-        _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx)
-        wall += st["wall_s"]
-        toks += st["out_tokens"]
-        lats.append(lat)
-    torch.cuda.synchronize()
-    dist.barrier()
-    host = time.perf_counter() - th0
-    if rank == 0:   # stamps and outputs are gathered on rank 0 (one job, not replicas)
-        lat = lats[-1]
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx)
+            wall += st["wall_s"]     # rank 0: stamps of every rank on one clock
+            toks += st["out_tokens"]
+        torch.cuda.synchronize()
+        dist.barrier()
+        host = time.perf_counter() - th0
+    wall = reduce_over_ranks(wall, "max", dist)
+    host = reduce_over_ranks(host, "max", dist)
+    forced = None
+    if "sched" in plan["waa_tp2"]:
+        sw = exg_schedule.from_buffer_copy(plan["waa_tp2"]["sched"])
+        _, lat_w, st_w, _ = ctx.run(sw, reqs, slot_ctx=slot_ctx)
+        forced = {"schedule": plan["waa_tp2"]["schedule"], "predicted_tok_s": plan["waa_tp2"]["predicted_tok_s"],
+                  "tok_s": st_w["tok_s"], "p99_latency_s": float(np.percentile(lat_w, 99)) if rank == 0 else None}
+    else:
+        forced = plan["waa_tp2"]
+    if rank == 0:
+        upto = [lat[i] for i, r in enumerate(reqs) if r.output_len <= d.target_len]
         print(json.dumps({
             "metric": METRIC, "value": toks / wall, "unit": "output tokens/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic",
-            "config": {"workload": WORKLOAD.replace("on 1xB200 per rank", "as one job"), "layout": "plan",
-                       "latency_bound_s": plan["bound"], "schedule": s.as_dict(), "predicted_tok_s": plan["pred"],
-                       "requests_per_step": args.requests},
-            "e2e": {"value": toks / host, "unit": "output tokens/s", "h2d_bytes_per_step": None,
-                    "d2h_bytes_per_step": None},
-            "sla": {"p99_latency_s": float(np.percentile(lat, 99)), "max_latency_s": float(np.max(lat)),
-                    "sla_a_met": bool(np.percentile(lat, 99) <= plan["bound"])}}))
+            "config": {"workload": MULTI_WORKLOAD, "layout": "plan", "latency_bound_s": L_b,
+                       "bound_rule": "70th pctl of static-batch latencies (PAPER.md:490)",
+                       "schedule": plan["pick"]["schedule"], "predicted_tok_s": plan["pick"]["predicted_tok_s"],
+                       "predicted_latency_s": plan["pick"]["predicted_latency_s"], "requests_per_step": args.requests,
+                       "parallelism": "plan over %d GPUs (one NCCL job)" % world},
+            "e2e": {"value": toks / host, "unit": "output tokens/s", "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h},
+            "sla": {"sla_b_met": bool(max(upto) < L_b), "sla_a_met": bool(np.percentile(lat, 99) <= L_b),
+                    "max_latency_upto_p99_len_s": float(max(upto)), "p99_latency_s": float(np.percentile(lat, 99))},
+            "forced_waa_tp2": forced, "clocks": clk.summary(),
+            "comm": "measured: XProfiler tp_sync / pp_sync on this job's NCCL communicators"}))
     ctx.close()
     dist.destroy_process_group()
 
@@ -475,8 +537,11 @@ def main():
     ap.add_argument("--little", type=int, default=1,
                     help="1: completion fraction by Little's law (SURVEY.md S3; DESIGN.md), 0: paper's E[1/ceil(S/N_D)]")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--layout", default="replicas", choices=["replicas", "plan"],
-                    help="N > 1: independent replicas (default) or the scheduler's N-GPU layout as one NCCL job")
+    ap.add_argument("--layout", default="plan", choices=["replicas", "plan"],
+                    help="N > 1: config 4 under the scheduler's N-GPU plan as one NCCL job (default), or "
+                         "independent config-2 replicas")
+    ap.add_argument("--multi-model", default=MULTI_MODEL)
+    ap.add_argument("--multi-task", default=MULTI_TASK)
     ap.add_argument("--plan-gpus", type=lambda v: [int(x) for x in v.split(",") if x], default=[2, 4, 8],
                     help="cluster sizes for the scheduler's predicted multi-GPU plan")
     ap.add_argument("--dyn", type=float, default=0.1, help="dynamic workload adjustment threshold (0: skip the run)")

@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EXG_ABI_VERSION 3
+#define EXG_ABI_VERSION 4
 
 typedef enum {
   EXG_OK = 0,
@@ -105,6 +105,8 @@ typedef struct {
   double eps_t_frac, eps_l_frac;
   int32_t b_e_max, n_d_max, m_max;
   int32_t use_little_fraction;
+  int32_t tp_degree_only;     /* > 0: search only this TP degree (a forced partial-TP
+                                 plan, e.g. config 4's WAA with t = 2); 0 = all   */
 } exg_search_opts;
 
 /* XProfiler sweep axes. */

@@ -169,6 +169,7 @@ class SearchOpts:
     n_d_max: int = 0          # 0 -> max output length
     m_max: int = 8
     use_little_fraction: bool = False
+    tp_degree_only: int = 0   # > 0: only this TP degree (a forced partial-TP plan)
 
 
 @dataclass
@@ -199,6 +200,8 @@ def schedule_find(S: sim.Simulator, L_b: float, strategy_mask: int, opts: Search
             continue
         for t in (1, 2, 4, 8):
             if t > N or H % t != 0:
+                continue
+            if opts.tp_degree_only > 0 and t != opts.tp_degree_only:
                 continue
             cs = [0] if t == 1 else list(range(t, N + 1, t))
             for c in cs:

@@ -71,7 +71,8 @@ class exg_estimate(C.Structure):
 
 class exg_search_opts(C.Structure):
     _fields_ = [("eps_t_frac", C.c_double), ("eps_l_frac", C.c_double), ("b_e_max", C.c_int32),
-                ("n_d_max", C.c_int32), ("m_max", C.c_int32), ("use_little_fraction", C.c_int32)]
+                ("n_d_max", C.c_int32), ("m_max", C.c_int32), ("use_little_fraction", C.c_int32),
+                ("tp_degree_only", C.c_int32)]
 
 
 class exg_profile_grid(C.Structure):
@@ -163,7 +164,7 @@ _SIGS = {
 }
 
 _lib = None
-ABI_VERSION = 3   # include/exegpt.h EXG_ABI_VERSION
+ABI_VERSION = 4   # include/exegpt.h EXG_ABI_VERSION
 
 
 def lib():
@@ -212,8 +213,9 @@ class Pmf:
         self.c = exg_pmf(len(self.arr), self.arr.ctypes.data_as(C.POINTER(C.c_double)))
 
 
-def search_opts(eps_t=0.02, eps_l=0.02, b_e_max=256, n_d_max=0, m_max=8, little=False) -> exg_search_opts:
-    return exg_search_opts(eps_t, eps_l, b_e_max, n_d_max, m_max, int(little))
+def search_opts(eps_t=0.02, eps_l=0.02, b_e_max=256, n_d_max=0, m_max=8, little=False,
+                tp_only=0) -> exg_search_opts:
+    return exg_search_opts(eps_t, eps_l, b_e_max, n_d_max, m_max, int(little), int(tp_only))
 
 
 def unique_id() -> bytes:

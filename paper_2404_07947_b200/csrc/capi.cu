@@ -409,7 +409,7 @@ exg_status exg_schedule_find(const exg_profile* p, const exg_model_spec* spec, c
     check_spec(spec);
     if (!(strategy_mask & (EXG_RRA | EXG_WAA_C | EXG_WAA_M))) throw std::invalid_argument("unknown strategy");
     if (target_len < 1) throw std::invalid_argument("target_len < 1");
-    exg_search_opts o{0.02, 0.02, 256, 0, 8, 0};
+    exg_search_opts o{0.02, 0.02, 256, 0, 8, 0, 0};
     if (opts) o = *opts;
     exg::plan::Simulator S(p->p, *spec, *cluster, pmf_vec(in), pmf_vec(out_len), target_len,
                            o.use_little_fraction != 0);

@@ -732,6 +732,7 @@ bool schedule_find(Simulator& S, double L_b, uint32_t mask, const exg_search_opt
     if (strat != EXG_RRA && N < 2) continue;
     for (int t : {1, 2, 4, 8}) {
       if (t > N || H % t != 0) continue;
+      if (o.tp_degree_only > 0 && t != o.tp_degree_only) continue;
       std::vector<int> cs;
       if (t == 1)
         cs.push_back(0);

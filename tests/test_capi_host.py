@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(L):
     assert len(names) >= 20
     for n in sorted(names):
         assert hasattr(lib, n), n
-    assert L.lib().exg_abi_version() == L.ABI_VERSION == 3
+    assert L.lib().exg_abi_version() == L.ABI_VERSION == 4
 
 
 def _setup(task="S", model="opt-13b", n_gpus=1, mem=180e9, ws=4e9):
