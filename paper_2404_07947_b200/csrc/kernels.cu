@@ -405,8 +405,16 @@ __device__ __forceinline__ float deferred_qkv(const DecodeAttnArgs& a, int i, in
   const int64_t F = 3LL * a.qkv_inner;
   const float* p = a.qkv_part + (int64_t)i * F + f;
   const int64_t ss = (int64_t)a.B * F;
-  float acc = __ldcg(p);
-  for (int sg = 1; sg < ns; ++sg) acc += __ldcg(p + sg * ss);
+  // up to 8 segment loads in flight, summed in segment order
+  float acc = 0.f;
+  for (int s0 = 0; s0 < ns; s0 += 8) {
+    float v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = s0 + q < ns ? __ldcg(p + (s0 + q) * ss) : 0.f;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (s0 + q < ns) acc = (s0 + q == 0) ? v[q] : acc + v[q];
+  }
   if (a.qkv_bias) acc += bf2f(a.qkv_bias[f]);
   return acc;
 }
@@ -441,25 +449,28 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
     fence_barrier_init();
   }
-  if (tid < DH)
-    qs[tid] = a.qkv_part ? bf2f(f2bf(deferred_qkv(a, i, h * DH + tid))) : bf2f(a.q[(int64_t)i * a.ldq + h * DH + tid]);
   // fused KV append: this split holds the new key nk-1 -> write its K / V row
   // to the cache, and patch it into its shared-memory tile after the bulk copy
   // of that tile (which may carry the stale cache row) has landed
   const int r_new = nk - 1 - k_begin;
   const bool app = (a.knew != nullptr || a.qkv_part != nullptr) && r_new < n;
+  __shared__ __align__(16) bf16 kvn[2][DH];   // deferred QKV: the new K / V rows
+  if (a.qkv_part) {
+    // q, and (appending CTA) the new K / V rows: each thread sums the
+    // segments of a few features, rounded at the T4(d) point
+    if (tid < DH) qs[tid] = bf2f(f2bf(deferred_qkv(a, i, h * DH + tid)));
+    if (app)
+      for (int e = tid; e < 2 * DH; e += 128)
+        kvn[e / DH][e % DH] = f2bf(deferred_qkv(a, i, (1 + e / DH) * a.qkv_inner + h * DH + e % DH));
+    __syncthreads();
+  } else if (tid < DH) {
+    qs[tid] = bf2f(a.q[(int64_t)i * a.ldq + h * DH + tid]);
+  }
   int4 new_chunk = make_int4(0, 0, 0, 0);
   if (app && tid < 2 * C::CH) {
     const int which = tid / C::CH, c = tid % C::CH;
     if (a.qkv_part) {
-      const int f0 = (1 + which) * a.qkv_inner + h * DH + c * 8;
-      uint32_t w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        __nv_bfloat162 h2 = __floats2bfloat162_rn(deferred_qkv(a, i, f0 + 2 * e), deferred_qkv(a, i, f0 + 2 * e + 1));
-        w[e] = *reinterpret_cast<uint32_t*>(&h2);
-      }
-      new_chunk = make_int4((int)w[0], (int)w[1], (int)w[2], (int)w[3]);
+      new_chunk = *reinterpret_cast<const int4*>(&kvn[which][c * 8]);
     } else {
       new_chunk = *reinterpret_cast<const int4*>((which ? a.vnew : a.knew) + (int64_t)i * a.ldnew + h * DH + c * 8);
     }
