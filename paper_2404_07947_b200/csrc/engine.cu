@@ -159,7 +159,7 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
   if (D.f32 && (t5_ || shard.tp != 1 || !shard.embed || !shard.head || shard.l0 != 0 ||
                 (shard.l1 >= 0 && shard.l1 != s.n_dec_layers)))
     throw std::invalid_argument("the fp32 path runs decoder-only models on one GPU (whole model, no TP / PP)");
-  defer_ = !t5_ && !D.f32 && shard.tp == 1 && s.d_model % 4 == 0 && s.d_model <= 16384 && deferred_enabled();
+  defer_ = (!t5_ && !D.f32 && shard.tp == 1 && s.d_model % 4 == 0 && s.d_model <= 16384) ? deferred_enabled() : 0;
   if (S_.l1 < 0) S_.l1 = D.L;
   if (S_.l0 < 0 || S_.l1 > D.L || S_.l0 >= S_.l1) throw std::invalid_argument("bad shard layer range");
   if (S_.tp < 1 || D.H % S_.tp || D.ff % S_.tp || S_.tp_rank < 0 || S_.tp_rank >= S_.tp)
@@ -381,8 +381,10 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
   const size_t f32_act = D.f32 ? al(T * D.d * 4) + al(T * 3 * D.inner_l * 4) + al(T * D.inner_l * 4) +
                                      al(T * D.ffl * 4)
                                : 0;
-  const size_t dq = defer_ ? deferred_floats(3 * D.inner_l, D.d, (int)R) : 0;
-  const size_t dr = defer_ ? std::max(deferred_floats(D.d, D.inner_l, (int)R), deferred_floats(D.d, D.ffl, (int)R)) : 0;
+  const size_t dq = (defer_ & DEFER_QKV) ? deferred_floats(3 * D.inner_l, D.d, (int)R) : 0;
+  const size_t dr = (defer_ & DEFER_RESID)
+                        ? std::max(deferred_floats(D.d, D.inner_l, (int)R), deferred_floats(D.d, D.ffl, (int)R))
+                        : 0;
   const size_t bytes = al(T * D.d * 4) + al(tp_part * 4) + al(T * D.d * 2) + al(T * 3 * D.inner_l * 2) +
                        al(T * D.inner_l * 2) + al(T * D.ffl * 2) + al(logit_rows * D.V * 4) + al(sk * 4) +
                        al(parts * 4) + al(R * D.Hl * 4) + f32_act + al(dq * 4) + al(dr * 4);
@@ -672,11 +674,11 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
     return;
   }
   if (part == 1) attn = rest = true;
-  const bool defer = defer_ && part == 0;
+  const bool defer_qkv = (defer_ & DEFER_QKV) && part == 0, defer = (defer_ & DEFER_RESID) && part == 0;
   if (rest) {
     ln_decode(w.ln1_g, w.ln1_b, B);
     EpiParams e = epi_bf16(w.bqkv, qkv_, 3 * il);
-    if (defer) e.defer_out = defer_qkv_;   // q / k / v summed by the attention kernel
+    if (defer_qkv) e.defer_out = defer_qkv_;   // q / k / v summed by the attention kernel
     linear_dec(h_, d, B, w.Wqkv, 3 * il, d, e);
   }
   if (attn) {
@@ -689,7 +691,7 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
     da.ldnew = 3 * il;
     da.q = qkv_;
     da.ldq = 3 * il;
-    if (defer) {
+    if (defer_qkv) {
       da.qkv_part = defer_qkv_;
       da.qkv_si = decode_seg_info(3 * il, d);
       da.qkv_bias = w.bqkv;

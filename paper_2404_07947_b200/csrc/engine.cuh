@@ -218,7 +218,7 @@ class Engine {
   // deferred stream-K reductions of the decode GEMMs (gemm_tc.cuh): QKV
   // segments summed by the decode attention, O-projection / FFN2 segments by
   // the following LayerNorm (decoder-only, tp = 1, bf16)
-  bool defer_ = false;
+  int defer_ = 0;   // DEFER_QKV | DEFER_RESID
   float *defer_qkv_ = nullptr, *defer_res_ = nullptr;
   struct PendingResid {
     const float* P = nullptr;

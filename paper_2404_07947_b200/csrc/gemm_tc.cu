@@ -1008,8 +1008,8 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
-bool& deferred_enabled() {
-  static bool on = true;
+int& deferred_enabled() {
+  static int on = DEFER_DEFAULT;
   return on;
 }
 
@@ -1078,8 +1078,10 @@ void linear(const LinearArgs& a, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
-// deferred stream-K reductions for engines created after the call (1 = on, default)
-extern "C" void exg_diag_deferred(int on) { exg::deferred_enabled() = on != 0; }
+// deferred stream-K reductions for engines created after the call: bit 0 =
+// QKV (summed by the decode attention), bit 1 = O-projection / FFN2 (summed by
+// the following LayerNorm); -1 restores the default
+extern "C" void exg_diag_deferred(int mask) { exg::deferred_enabled() = mask < 0 ? exg::DEFER_DEFAULT : mask; }
 extern "C" void exg_diag_gemm_sk_ctas(int n) { exg::gemm_sk_ctas() = n; }
 extern "C" void exg_diag_gemm_slab_mb(int mb) { exg::gemm_slab_mb() = mb; }
 // span recording: reset clears the arrays and the launch counter; read copies

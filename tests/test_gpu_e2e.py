@@ -231,14 +231,15 @@ def test_deferred_stream_k_reduction_bit_identical(n_req, b_d):
     spec = ModelSpec("defer-w2048", "opt", 0, 2, 2048, 16, 128, 8192, 4096, 512)
     reqs = make_requests(n_req, uniform_pmf(8, 64), uniform_pmf(2, 12), spec.vocab, 0xD3F)
     outs = []
-    for on in (0, 1):
-        X.lib().exg_diag_deferred(on)
+    for mask in (0, 1, 2, 3):   # none / QKV / O-proj + FFN2 / all
+        X.lib().exg_diag_deferred(mask)
         try:
             ctx = X.Context(spec, 0xE6E0_0D3F)
             outs.append(ctx.run(X.rra_schedule(min(n_req, b_d), b_d, 4), reqs, dump=range(len(reqs))))
             ctx.close()
         finally:
-            X.lib().exg_diag_deferred(1)
-    assert outs[0][0] == outs[1][0]
-    for r in range(len(reqs)):
-        assert np.array_equal(outs[0][3][r], outs[1][3][r]), r
+            X.lib().exg_diag_deferred(-1)
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        for r in range(len(reqs)):
+            assert np.array_equal(o[3][r], outs[0][3][r]), r

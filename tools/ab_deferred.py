@@ -17,21 +17,22 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 spec = MODELS["opt-13b"]
 d = task_dists("S")
 reqs = make_requests(n, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E10002)
+MODES = [int(x) for x in os.environ.get("EXG_DEFER_MODES", "0,2,3").split(",")]
 ctxs = {}
-for on in (0, 1):
+for on in MODES:
     X.lib().exg_diag_deferred(on)
     ctxs[on] = X.Context(spec, weight_seed(2))
-X.lib().exg_diag_deferred(1)
+X.lib().exg_diag_deferred(-1)
 sched = X.rra_schedule(56, 83, 32)
 toks = {}
 for r in range(reps):
-    for on in (0, 1):
+    for on in MODES:
         t, lat, st, _ = ctxs[on].run(sched, reqs, slot_ctx=592)
         toks[on] = t
         print("deferred %d rep %d tok_s %.1f decode_s %.4f encode_s %.4f iters %d" % (
             on, r, st["tok_s"], st["decode_s"], st["encode_s"], st["decode_iters"]))
         sys.stdout.flush()
-print("tokens identical:", toks[0] == toks[1])
-for on in (0, 1):
+print("tokens identical:", all(toks[m] == toks[MODES[0]] for m in MODES))
+for on in MODES:
     _, _, st, _ = ctxs[on].run(sched, reqs, slot_ctx=592, kernel_timing=True)
     print("deferred %d kernels: %s" % (on, {k: (round(v["time_s"], 4), v["launches"]) for k, v in st["kernels"].items()}))
