@@ -65,7 +65,10 @@ __host__ __device__ inline int seg_count(const SegInfo& s, int m) {
   return owner(x1) - owner(x0) + 1;
 }
 SegInfo decode_seg_info(int features, int K);
-constexpr int DEFER_QKV = 1, DEFER_RESID = 2, DEFER_DEFAULT = DEFER_QKV | DEFER_RESID;
+constexpr int DEFER_QKV = 1, DEFER_RESID = 2;
+// default: the residual GEMMs only -- A/B on OPT-13B (tools/ab_deferred.py): the
+// deferred QKV sums cost the attention kernel more than they save the GEMM
+constexpr int DEFER_DEFAULT = DEFER_RESID;
 int& deferred_enabled();    // mask of deferred decode GEMMs (exg_diag_deferred)
 // floats a deferred decode GEMM writes: max segments x tokens x features
 size_t deferred_floats(int features, int K, int tokens);
