@@ -135,7 +135,8 @@ typedef struct {
                                  all-reduce on the TP sub-communicator        */
   int32_t kernel_timing;      /* 1: CUDA events around every launch of the
                                  kernel classes below (roofline evidence)       */
-  double dyn_threshold;       /* > 0: dynamic workload adjustment:
+  double dyn_threshold;       /* > 0: dynamic workload adjustment (
+                                 RRA on one GPU and WAA layouts):
                                  while the decode batch sits outside
                                  +-threshold of its running average, the next
                                  encode batch targets B_E' = B_E + round(avg -

@@ -595,6 +595,10 @@ struct RunState {
   uint64_t* d_stamps = nullptr;
   int n_stamps = 0, cap_stamps = 0;
   std::vector<int> admit_ev, done_ev;
+  // Table 9 single-stage times: encode batches (start /
+  // end stamps) and decode iterations (end stamps, consecutive)
+  std::vector<int> enc_start_ev, enc_end_ev, iter_ev;
+  std::vector<int64_t> iter_tokens;   // tokens emitted by the iteration ending at iter_ev[k]
   cudaStream_t st;
   int64_t decode_iters = 0, encode_phases = 0, batch_sum = 0;
   ~RunState() {
@@ -865,6 +869,41 @@ void finish(const Exec& X, RunState& R, Stage& head_stage, int32_t* out_tokens, 
     stats->lat_p99_s = pct(0.99);
     stats->lat_max_s = s.back();
     stats->mean_decode_batch = R.decode_iters ? (double)R.batch_sum / R.decode_iters : 0;
+    stats->mean_encode_batch = R.encode_phases ? (double)R.n / R.encode_phases : 0;
+    // steady window: admission of request ceil(0.1 n) .. admission of the last
+    const int r0 = std::min(R.n - 1, (int)std::ceil(0.1 * R.n));
+    const double w0 = sec(R.admit_ev[r0]), w1 = sec(R.admit_ev[R.n - 1]);
+    auto spread = [&](const std::vector<double>& v, double* mean, double* p99dev) {
+      *mean = *p99dev = 0;
+      if (v.empty()) return;
+      double m = 0;
+      for (double x : v) m += x;
+      m /= v.size();
+      std::vector<double> dv;
+      for (double x : v) dv.push_back(std::fabs(x - m));
+      std::sort(dv.begin(), dv.end());
+      const double rr = 0.99 * (dv.size() - 1);
+      const size_t lo = (size_t)std::floor(rr), hi = (size_t)std::ceil(rr);
+      *mean = m;
+      *p99dev = dv[lo] + (rr - lo) * (dv[hi] - dv[lo]);
+    };
+    std::vector<double> te, td;
+    for (size_t k = 0; k < R.enc_start_ev.size() && k < R.enc_end_ev.size(); ++k) {
+      const double a = sec(R.enc_start_ev[k]), b = sec(R.enc_end_ev[k]);
+      if (a >= w0 && b <= w1 && b > a) te.push_back(b - a);
+    }
+    for (size_t k = 1; k < R.iter_ev.size(); ++k) {
+      const double a = sec(R.iter_ev[k - 1]), b = sec(R.iter_ev[k]);
+      if (a >= w0 && b <= w1 && b > a) td.push_back(b - a);
+    }
+    spread(te, &stats->enc_stage_mean_s, &stats->enc_stage_p99dev_s);
+    spread(td, &stats->dec_stage_mean_s, &stats->dec_stage_p99dev_s);
+    int64_t toks = 0;
+    for (size_t k = 0; k < R.iter_ev.size(); ++k) {
+      const double t = sec(R.iter_ev[k]);
+      if (t > w0 && t <= w1) toks += R.iter_tokens[k];
+    }
+    stats->tok_s_steady = w1 > w0 ? toks / (w1 - w0) : stats->tok_s;
   }
 }
 }  // namespace
@@ -909,6 +948,7 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   while (next_req < n || !active.empty()) {
     const int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
     const int ev_phase = R.record(first_mine);
+    if (admit > 0) R.enc_start_ev.push_back(ev_phase);
     if (admit > 0) {
       std::vector<int> slots(admit);
       for (int k = 0; k < admit; ++k) {
@@ -951,11 +991,14 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       }
       next_req += admit;
       ++R.encode_phases;
+      R.enc_end_ev.push_back(R.record(head_mine));
     }
     for (int u = 0; u < s.n_d && !active.empty(); ++u) {
       decode_pipeline(X, R, pipe, tabs, ti, active, P, d, dump);
       return_tokens(X, pipe, B_D);
       const int ev = R.record(head_mine);
+      R.iter_ev.push_back(ev);
+      R.iter_tokens.push_back((int64_t)active.size());
       ++R.decode_iters;
       R.batch_sum += (int64_t)active.size();
       retire(R, active, free_slots, ev);
@@ -992,14 +1035,23 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   const int M = s.b_m > 0 ? std::max(1, (B_D + s.b_m - 1) / s.b_m) : 1;
   const int enc_ctx = std::max(1, R.max_in);
   const int drop = R.ed ? 0 : 1;
+  const double dyn = opts ? opts->dyn_threshold : 0.0;
+  // encoder capacity: 2 B_E rows under dynamic adjustment, never more tokens
+  // than B_E of the longest input
+  const int enc_rows = dyn > 0 ? std::min(2 * B_E, B_D) : B_E;
+  const int enc_tok_cap = std::max(1, B_E * (R.max_in - drop));
+  double mean_enc_tokens = 0, steady_batch_sum = 0;
+  int64_t steady_iters = 0;
+  for (int r = 0; r < n; ++r) mean_enc_tokens += reqs[r].input_len - drop;
+  mean_enc_tokens /= std::max(1, n);
   for (auto& st : enc)
     for (auto& e : st->eng)
       if (e) {
         if (R.ed)
-          e->ensure_kv(B_E, 1, -1, enc_ctx);   // encoder side: encoder K/V staging + cross K/V of the batch
+          e->ensure_kv(enc_rows, 1, -1, enc_ctx);   // encoder side: encoder K/V staging + cross K/V of the batch
         else
-          e->ensure_kv(B_E, enc_ctx);
-        e->ensure_workspace(std::max(1, B_E * (R.max_in - drop)), B_E);
+          e->ensure_kv(enc_rows, enc_ctx);
+        e->ensure_workspace(enc_tok_cap, enc_rows);
       }
   for (auto& st : dec)
     for (auto& e : st->eng)
@@ -1020,8 +1072,8 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   bool hr_used[HR] = {};
   int hr_next = 0;
   for (int i = 0; i < HR; ++i) {
-    EXG_CUDA(cudaMalloc(&d_hrows[i], sizeof(HandoffRow) * B_E));
-    EXG_CUDA(cudaMallocHost(&h_hrows[i], sizeof(HandoffRow) * B_E));
+    EXG_CUDA(cudaMalloc(&d_hrows[i], sizeof(HandoffRow) * enc_rows));
+    EXG_CUDA(cudaMallocHost(&h_hrows[i], sizeof(HandoffRow) * enc_rows));
     EXG_CUDA(cudaEventCreateWithFlags(&hr_ev[i], cudaEventDisableTiming));
   }
   bf16* stage_buf = nullptr;   // loopback transport: both halves of a self-message
@@ -1036,8 +1088,34 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   while (next_req < n || pend_k > 0 || !active.empty()) {
     // encoder: keep one encoded batch ready (encoder slots 0..k-1)
     if (pend_k == 0 && next_req < n) {
-      const int k = std::min(B_E, n - next_req);
+      int k = std::min(B_E, n - next_req);
+      if (dyn > 0) {
+        // dynamic workload adjustment: "a long encoding
+        // stage can miss the handover ... uneven decoding batches": the
+        // encoder batch's token sum is kept within +-dyn of B_E' x the mean
+        // encoded length, B_E' = B_E + round(avg - current decode batch) while
+        // the decode batch is outside +-dyn of its running average
+        int be = B_E;
+        if (steady_iters >= 2 && !active.empty()) {
+          const double avg = steady_batch_sum / steady_iters, cur = (double)active.size();
+          if (cur < (1 - dyn) * avg || cur > (1 + dyn) * avg) be = B_E + (int)std::lround(avg - cur);
+        }
+        be = std::max(1, std::min(be, enc_rows));
+        const int cap = std::min(enc_rows, n - next_req);
+        const double target = be * mean_enc_tokens;
+        double tok = 0;
+        k = 0;
+        while (k < cap) {
+          const double t = reqs[next_req + k].input_len - drop;
+          if (k >= be && tok >= (1 - dyn) * target) break;
+          if (k >= 1 && tok + t > (1 + dyn) * target) break;
+          if (k >= 1 && tok + t > enc_tok_cap) break;   // encoder workspace
+          tok += t;
+          ++k;
+        }
+      }
       pend_ev = R.record(first_mine);
+      R.enc_start_ev.push_back(pend_ev);
       std::vector<int> eslots(k);
       for (int j = 0; j < k; ++j) eslots[j] = j;
       Tables& tb = tabs[ti++ % tabs.size()];
@@ -1050,6 +1128,7 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       pend_k = k;
       next_req += k;
       ++R.encode_phases;
+      R.enc_end_ev.push_back(R.record(X.mine(enc.back()->gpu(0))));
     }
     // handoff + merge at an iteration boundary when the decoder has room
     if (pend_k > 0 && (int)free_slots.size() >= pend_k) {
@@ -1171,8 +1250,14 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
     decode_pipeline(X, R, dec, tabs, ti, active, M, d, dump);
     return_tokens(X, dec, B_D);
     const int ev = R.record(head_mine);
+    R.iter_ev.push_back(ev);
+    R.iter_tokens.push_back((int64_t)active.size());
     ++R.decode_iters;
     R.batch_sum += (int64_t)active.size();
+    if (next_req < n) {   // decode batch average while requests keep arriving
+      steady_batch_sum += (double)active.size();
+      ++steady_iters;
+    }
     retire(R, active, free_slots, ev);
   }
   finish(X, R, *dec.back(), out_tokens, out_latency, stats);

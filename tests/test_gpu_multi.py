@@ -245,3 +245,24 @@ def test_profile_comm_tables_on_a_rank_group():
         single.close()
     for c in ctxs:
         c.close()
+
+
+def test_waa_dynamic_adjustment_and_stage_variance(env):
+    """NEXT-1 under WAA: the encoder batch follows the
+    decode batch's drift and the token-sum window; results stay bit-identical
+    (batch invariance, T13) and the run reports Table 9's single-stage
+    statistics for the encoder and the decoder."""
+    X, L, reqs, single, multi, base_t, base_l, ora = env
+    from workload import make_requests, uniform_pmf
+    many = make_requests(48, uniform_pmf(4, 40), uniform_pmf(1, 20), 512, 78)
+    layout = [(0, 1, 0, 2), (1, 1, 0, 1), (2, 1, 1, 2)]
+    s = L.make_schedule(X.EXG_WAA_C, 3, 12, layout, b_m=6, n_enc_gpus=1)
+    a = multi.run(s, many, dump=range(len(many)))
+    b = multi.run(s, many, dump=range(len(many)), dyn_threshold=0.1)
+    assert a[0] == b[0]
+    for r in range(len(many)):
+        assert np.array_equal(a[3][r], b[3][r]), r
+    for st in (a[2], b[2]):
+        assert st["dec_stage_mean_s"] > 0 and st["enc_stage_mean_s"] > 0
+        assert st["dec_stage_p99dev_s"] >= 0 and st["mean_encode_batch"] > 0 and st["tok_s_steady"] > 0
+    assert a[2]["mean_encode_batch"] == pytest.approx(3.0, rel=0.05)
