@@ -255,6 +255,16 @@ void exg_profile_free(exg_profile* p);
 exg_status exg_simulate(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
                         const exg_pmf* in, const exg_pmf* out_len, int32_t target_len, const exg_schedule* sched,
                         exg_estimate* est);
+/* The profile's time of one single-GPU stage holding `n_layers` layers
+ * (PAPER.md:150-154 tables): phase 0 = an encode phase of `rows` requests and
+ * `work` encoded tokens, n_layers x (attn(rows, work/rows) + rest(work));
+ * phase 1 = a decode iteration of `rows` rows attending to `work` keys in
+ * total, n_layers x (attn(rows, work/rows) + rest(rows)) + head(rows).
+ * Used to separate the workload-driven part of measured stage times from
+ * the rest (Table 9 analysis).  Pure host. */
+exg_status exg_profile_stage_time(const exg_profile* p, int32_t phase, int32_t tp_degree, int32_t n_layers,
+                                  double rows, double work, double* seconds);
+
 /* Memory-overhead accounting: the model bytes and KV-cache
  * bytes each GPU of the schedule's layout holds under the simulator's memory
  * model (weight shard + embeddings on the first / last stage of each side;

@@ -130,6 +130,8 @@ _SIGS = {
     "exg_profile_free": (None, [_P]),
     "exg_profile_comm_model": (C.c_int, [_P, C.c_double, C.c_double]),
     "exg_profile_copy_comm": (C.c_int, [_P, _P]),
+    "exg_profile_stage_time": (C.c_int, [_P, C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                                         C.POINTER(C.c_double)]),
     "exg_simulate": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
                                C.POINTER(exg_pmf), C.c_int32, C.POINTER(exg_schedule), C.POINTER(exg_estimate)]),
     "exg_schedule_memory": (C.c_int, [_P, C.POINTER(exg_model_spec), C.POINTER(exg_cluster_spec), C.POINTER(exg_pmf),
@@ -375,6 +377,13 @@ class Profile:
     def comm_model(self, alpha_s: float, bw_bytes_per_s: float):
         """Fill tp_sync / pp_sync from an alpha-beta interconnect model."""
         check(lib().exg_profile_comm_model(self.h, alpha_s, bw_bytes_per_s))
+
+    def stage_time(self, phase: int, rows: float, work: float, n_layers: int, tp: int = 1) -> float:
+        """exg_profile_stage_time: the profile's time of one encode phase (0) /
+        decode iteration (1) of a single-GPU stage."""
+        out = C.c_double()
+        check(lib().exg_profile_stage_time(self.h, phase, tp, n_layers, float(rows), float(work), C.byref(out)))
+        return out.value
 
     def copy_comm(self, other: "Profile"):
         """tp_sync / pp_sync tables from a multi-rank profile (exg_profile_copy_comm)."""

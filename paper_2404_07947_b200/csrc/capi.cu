@@ -353,6 +353,25 @@ exg_status exg_simulate(const exg_profile* p, const exg_model_spec* spec, const 
   });
 }
 
+exg_status exg_profile_stage_time(const exg_profile* p, int32_t phase, int32_t tp_degree, int32_t n_layers,
+                                  double rows, double work, double* seconds) {
+  return guarded([&] {
+    if (!p || !seconds) throw std::invalid_argument("null argument");
+    if (phase != 0 && phase != 1) throw std::invalid_argument("phase must be 0 (encode) or 1 (decode)");
+    if (!(rows > 0) || !(work > 0) || n_layers < 1) throw std::invalid_argument("rows, work, n_layers must be > 0");
+    const std::string ph = phase ? "dec" : "enc";
+    auto ia = p->p.attn.find({ph, tp_degree});
+    auto ir = p->p.rest.find({ph, tp_degree});
+    if (ia == p->p.attn.end() || ir == p->p.rest.end()) throw std::invalid_argument("profile has no such table");
+    const double a = exg::plan::interp2(ia->second, rows, work / rows);
+    const double r = exg::plan::interp1(ir->second.x, ir->second.t, phase ? rows : work);
+    double t = n_layers * (a + r);
+    if (phase && p->p.has_head) t += exg::plan::interp1(p->p.head.x, p->p.head.t, rows);
+    *seconds = t;
+    return EXG_OK;
+  });
+}
+
 exg_status exg_schedule_memory(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
                                const exg_pmf* in, const exg_pmf* out_len, const exg_schedule* sched,
                                double* weight_bytes, double* kv_bytes) {

@@ -353,3 +353,23 @@ def test_dtype_contract_without_gpu(L):
         h = C.c_void_p()
         st = L.lib().exg_create(C.byref(ms), C.byref(L.cluster_spec(ngpu)), 0, 0, 1, None, C.byref(h))
         assert st == L.EXG_E_INPUT, (spec_name, dtype, ngpu, st)
+
+
+def test_profile_stage_time_matches_simulator_lookups(L, tmp_path):
+    """exg_profile_stage_time = n_layers x (attention + rest) (+ head for a
+    decode iteration), the XSimulator's per-layer lookups (oracle)."""
+    from oracle import simulator as sim
+    spec, m, prof, d, cl = _setup()
+    P, *_ = _c_objects(L, spec, prof, d, cl, tmp_path)
+    for rows, work in ((4.0, 1000.0), (37.0, 9000.5), (200.0, 51000.0)):
+        enc = P.stage_time(0, rows, work, 40)
+        ref = 40 * (sim.interp2(prof.attn[("enc", 1)], rows, work / rows) +
+                    sim.interp1(prof.rest[("enc", 1)].x, prof.rest[("enc", 1)].t, work))
+        assert enc == pytest.approx(ref, rel=1e-12)
+        dec = P.stage_time(1, rows, work, 40)
+        ref = 40 * (sim.interp2(prof.attn[("dec", 1)], rows, work / rows) +
+                    sim.interp1(prof.rest[("dec", 1)].x, prof.rest[("dec", 1)].t, rows)) + \
+            sim.interp1(prof.head.x, prof.head.t, rows)
+        assert dec == pytest.approx(ref, rel=1e-12)
+    with pytest.raises(L.ExgError):
+        P.stage_time(2, 1.0, 1.0, 1)
