@@ -10,10 +10,17 @@
 //                          the tile (both take the row max over all 128 keys,
 //                          so no exchange per tile); online max / half sums;
 //                          P_j -> smem as bf16
-//   O_j = P_j . V_j        tcgen05.mma, A = P (K-major), B = V (MN-major), fp32 in TMEM
-//   o   = o * exp(m_{j-1} - m_j) + O_j   (registers, one 64-dim half per thread)
-// S and O are double-buffered in TMEM (4 x 128 columns) so the softmax of tile
-// j+1 overlaps the P.V of tile j; Q is double-buffered in shared memory so the
+//   O  += P_j . V_j        tcgen05.mma, A = P (K-major), B = V (MN-major), fp32,
+//                          accumulated in TMEM across the item's tiles
+// Lazy rescaling: P_j is exponentiated against the row's running reference
+// max m_ref, which moves (and O in TMEM is rescaled by the softmax warps) only
+// when a tile's max exceeds it by more than 8 in log2 units -- so p <= 2^8 and
+// the fp32 O / row sums stay far from overflow; mathematically the same
+// softmax (the final 1/l uses the same reference).  About a quarter of the
+// exponentials run as a degree-3 polynomial on the FMA pipe (relative error
+// 1.9e-4, far below P's bf16 rounding) beside the SFU ex2.
+// S is double-buffered in TMEM (2 x 128 columns) so the softmax of tile j+1
+// overlaps the P.V of tile j; Q is double-buffered in shared memory so the
 // next item's Q lands while the current one finishes.  Buffer indices and
 // mbarrier phases run on per-CTA counters across items.  Q, K, V arrive by
 // 2-D TMA (SWIZZLE_128B) straight from the packed qkv buffer and the KV cache.
@@ -66,6 +73,33 @@ __device__ __forceinline__ float ex2(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
+
+// 2^x on the FMA pipe: Cody-Waite split x = i + f, f in [0, 1), degree-3
+// polynomial for 2^f (max relative error 1.9e-4), i added to the exponent
+// field; 0 below 2^-126 like ex2.approx.ftz
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float xi = floorf(x);
+  const float f = x - xi;
+  float p = fmaf(f, 0.07619732618331909f, 0.22820299863815308f);
+  p = fmaf(p, f, 0.6952236294746399f);
+  p = fmaf(p, f, 1.0f);
+  const int e = (int)xi;
+  return e < -126 ? 0.f : __int_as_float(__float_as_int(p) + (e << 23));
+}
+
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const float* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(taddr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])), "r"(__float_as_uint(v[3])),
+      "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])), "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])),
+      "r"(__float_as_uint(v[8])), "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])), "r"(__float_as_uint(v[15]))
+      : "memory");
+}
+
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -129,8 +163,8 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
   uint64_t* s_full = bars + 8;          // 2
   uint64_t* s_free = bars + 10;         // 2
   uint64_t* p_full = bars + 12;         // 1
-  uint64_t* o_full = bars + 13;         // 2
-  uint64_t* o_free = bars + 15;         // 2
+  uint64_t* o_full = bars + 13;         // 2: P.V of a tile done (parity by tile)
+  uint64_t* o_free = bars + 15;         // 2: (unused slot kept for the layout)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
   float* lx = reinterpret_cast<float*>(sP + P_BYTES + 256);   // [2][FQ] row-sum halves
 
@@ -214,13 +248,14 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
         issue_s(0);
         for (int j = 0; j < it.ntiles; ++j) {
           if (j + 1 < it.ntiles) issue_s(j + 1);
-          // O_j = P_j . V_j
+          // O += P_j . V_j (one TMEM accumulator per item; the softmax warps
+          // signal p_full after any lazy rescale of O and, for an item's
+          // first tile, after reading out the previous item's O)
           const uint32_t gj = base + j;
           const int s = gj & 1;
           mbar_wait(p_full, gj & 1);
-          if (gj >= 2) mbar_wait(&o_free[s], ((gj >> 1) & 1) ^ 1);
           tc_fence_after();
-          const uint32_t d = tmem + 256 + s * 128;
+          const uint32_t d = tmem + 256;
           const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + s * KV_BYTES);
 #pragma unroll
           for (int k = 0; k < FK / 16; ++k) {
@@ -229,9 +264,9 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
             // B (V, MN-major): 16 keys = two 8-key core groups of 1024 B
             const uint32_t b_off = k * 2048;
             umma_bf16(d, umma_desc_sw128(pa + a_off), desc_mn_sw128(vb + b_off, TILE_BYTES, 1024), idesc_o,
-                      k ? 1u : 0u);
+                      (j || k) ? 1u : 0u);
           }
-          umma_commit(&o_full[s]);
+          umma_commit(&o_full[gj & 1]);
           umma_commit(&kv_empty[s]);
         }
         base += it.ntiles;
@@ -253,134 +288,129 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
       const float* brow =
           (p.bias && it.qb + r < it.len) ? p.bias + (int64_t)it.h * p.bias_ld + p.bias_off - qpos : nullptr;
       constexpr int HD = FD / 2;                      // output dims / keys per half
-      float o[HD];
-#pragma unroll
-      for (int d = 0; d < HD; ++d) o[d] = 0.f;
-      float m = -INFINITY, l = 0.f, alpha_prev = 0.f;
-      for (int j = 0; j <= it.ntiles; ++j) {
+      constexpr float LOG2E = 1.4426950408889634f;
+      constexpr float RESCALE_LOG2 = 8.f;             // move m_ref when a tile max exceeds it by > 2^8
+      float m = -INFINITY, l = 0.f;                   // m: reference max the P's are taken against
+      const uint32_t oa = tmem + lane_base + 256 + hf * HD;
+      for (int j = 0; j < it.ntiles; ++j) {
         const uint32_t gj = base + j;
-        if (j < it.ntiles) {
-          const int s = gj & 1;
-          mbar_wait(&s_full[s], (gj >> 1) & 1);
-          tc_fence_after();
-          // pass 1: this half's 64 scores (scaled, biased, masked) into
-          // registers and their max; the row max over the tile is the max of
-          // the two halves' (exchanged through shared memory)
-          const uint32_t sa = tmem + lane_base + s * 128 + hf * HD;
-          const int k0 = j * FK + hf * HD;
-          float sc[HD];
-          float mx = -INFINITY;
+        const int s = gj & 1;
+        mbar_wait(&s_full[s], (gj >> 1) & 1);
+        tc_fence_after();
+        // pass 1: this half's 64 scores (scaled, biased, masked) into
+        // registers and their max; the row max over the tile is the max of
+        // the two halves' (exchanged through shared memory)
+        const uint32_t sa = tmem + lane_base + s * 128 + hf * HD;
+        const int k0 = j * FK + hf * HD;
+        float sc[HD];
+        float mx = -INFINITY;
 #pragma unroll
-          for (int c = 0; c < HD; c += 16) tmem_ld16(sa + c, sc + c);
-          if (k0 + HD - 1 <= kmax && !brow) {      // no key of this half is masked
+        for (int c = 0; c < HD; c += 16) tmem_ld16(sa + c, sc + c);
+        if (k0 + HD - 1 <= kmax && !brow) {      // no key of this half is masked
 #pragma unroll
-            for (int e = 0; e < HD; ++e) {
-              sc[e] = __fmul_rn(sc[e], p.scale);
-              mx = fmaxf(mx, sc[e]);
-            }
-          } else {
-#pragma unroll
-            for (int e = 0; e < HD; ++e) {
-              const int kpos = k0 + e;
-              float x = (kpos <= kmax) ? __fmul_rn(sc[e], p.scale) : -INFINITY;
-              if (brow && kpos <= kmax) x = __fadd_rn(x, brow[kpos]);
-              sc[e] = x;
-              mx = fmaxf(mx, x);
-            }
+          for (int e = 0; e < HD; ++e) {
+            sc[e] = __fmul_rn(sc[e], p.scale);
+            mx = fmaxf(mx, sc[e]);
           }
-          lx[hf * FQ + r] = mx;
-          pair_bar();
-          mx = fmaxf(lx[r], lx[FQ + r]);
-          pair_bar();   // both halves have read lx before it is written again
+        } else {
+#pragma unroll
+          for (int e = 0; e < HD; ++e) {
+            const int kpos = k0 + e;
+            float x = (kpos <= kmax) ? __fmul_rn(sc[e], p.scale) : -INFINITY;
+            if (brow && kpos <= kmax) x = __fadd_rn(x, brow[kpos]);
+            sc[e] = x;
+            mx = fmaxf(mx, x);
+          }
+        }
+        lx[hf * FQ + r] = mx;
+        pair_bar();
+        mx = fmaxf(lx[r], lx[FQ + r]);
+        pair_bar();   // both halves have read lx before it is written again
+        // the previous tile's P.V has completed: P may be overwritten and O read
+        if (j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
+        // lazy rescale: the reference max moves only when this tile's max
+        // exceeds it by more than 2^RESCALE_LOG2 (the pair takes the same decision)
+        if (m == -INFINITY || (mx - m) * LOG2E > RESCALE_LOG2) {
           const float m_new = fmaxf(m, mx);
-          const float alpha = (m == -INFINITY) ? 0.f : ex2((m - m_new) * 1.4426950408889634f);
-          // p = 2^(s log2 e - m log2 e): one FFMA + one SFU op per score
-          const float nml = (m_new == -INFINITY) ? 0.f : -m_new * 1.4426950408889634f;
-          // P_j may overwrite the P buffer once the previous P.V has completed
-          // (within the item; the previous item's last P.V was awaited below)
-          if (j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
-          float sum = 0.f;
-#pragma unroll
-          for (int c = 0; c < HD; c += 16) {
-            uint32_t pk[8];
-#pragma unroll
-            for (int e = 0; e < 16; e += 2) {
-              const float p0 = ex2(fmaf(sc[c + e], 1.4426950408889634f, nml));
-              const float p1 = ex2(fmaf(sc[c + e + 1], 1.4426950408889634f, nml));
-              __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-              sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
-              pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
-            }
-            // row r, keys hf*64+c..+15: two 16-byte chunks in the SW128 K-major image
-            uint8_t* blk = sP + hf * TILE_BYTES;
-            const int ch = c >> 3;
-            *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-            *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
-          }
-          l = l * alpha + sum;
-          m = m_new;
-          fence_proxy_async_smem();
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(&s_free[s]);
-            mbar_arrive(p_full);
-          }
-          // accumulate O_{j-1} (its rescale factor was alpha_prev)
-          if (j >= 1) {
-            const int so = (gj - 1) & 1;
-            const uint32_t oa = tmem + lane_base + 256 + so * 128 + hf * HD;
+          if (j >= 1 && m != -INFINITY) {
+            const float alpha = ex2((m - m_new) * LOG2E);
             tc_fence_after();
 #pragma unroll
             for (int c = 0; c < HD; c += 16) {
               float v[16];
               tmem_ld16(oa + c, v);
 #pragma unroll
-              for (int e = 0; e < 16; ++e) o[c + e] = o[c + e] * alpha_prev + v[e];
+              for (int e = 0; e < 16; ++e) v[e] *= alpha;
+              tmem_st16(oa + c, v);
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&o_free[so]);
+            tmem_st_wait();
+            l *= alpha;
           }
-          alpha_prev = alpha;
-        } else {
-          // last tile's P.V
-          const int so = (gj - 1) & 1;
-          mbar_wait(&o_full[so], ((gj - 1) >> 1) & 1);
-          tc_fence_after();
-          const uint32_t oa = tmem + lane_base + 256 + so * 128 + hf * HD;
+          m = m_new;
+        }
+        // p = 2^(s log2 e - m log2 e): one FFMA + an SFU op (or, for a quarter
+        // of the keys, the FMA-pipe polynomial) per score
+        const float nml = (m == -INFINITY) ? 0.f : -m * LOG2E;
+        float sum = 0.f;
 #pragma unroll
-          for (int c = 0; c < HD; c += 16) {
-            float v[16];
-            tmem_ld16(oa + c, v);
+        for (int c = 0; c < HD; c += 16) {
+          uint32_t pk[8];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) o[c + e] = o[c + e] * alpha_prev + v[e];
+          for (int e = 0; e < 16; e += 2) {
+            const float a0 = fmaf(sc[c + e], LOG2E, nml), a1 = fmaf(sc[c + e + 1], LOG2E, nml);
+            const float p0 = ex2(a0);
+            const float p1 = (e % 4 == 2) ? ex2_poly(a1) : ex2(a1);
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
+            sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
+            pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&o_free[so]);
+          // row r, keys hf*64+c..+15: two 16-byte chunks in the SW128 K-major image
+          uint8_t* blk = sP + hf * TILE_BYTES;
+          const int ch = c >> 3;
+          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        }
+        l += sum;
+        fence_proxy_async_smem();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&s_free[s]);
+          mbar_arrive(p_full);
         }
       }
+      // the item's last P.V, then O out of TMEM: normalised by the row sum
+      {
+        const uint32_t gl = base + it.ntiles - 1;
+        mbar_wait(&o_full[gl & 1], (gl >> 1) & 1);
+      }
+      tc_fence_after();
       base += it.ntiles;
       // row sum = the two halves' sums (low half + high half)
       lx[hf * FQ + r] = l;
       pair_bar();
       const float lt = lx[r] + lx[FQ + r];
       pair_bar();   // both halves have read lx before the next item writes it
-      if (it.qb + r < it.len) {
-        const float inv = 1.f / lt;
-        bf16* dst = p.out + (int64_t)(it.t0 + it.qb + r) * p.ldo + it.h * FD + hf * HD;
+      const float inv = 1.f / lt;
+      bf16* dst = p.out + (int64_t)(it.t0 + it.qb + r) * p.ldo + it.h * FD + hf * HD;
 #pragma unroll
-        for (int c = 0; c < HD; c += 8) {
-          uint32_t pk[4];
+      for (int c = 0; c < HD; c += 16) {
+        float v[16];
+        tmem_ld16(oa + c, v);
+        if (it.qb + r < it.len) {
+          uint32_t pk[8];
 #pragma unroll
-          for (int e = 0; e < 8; e += 2) {
-            __nv_bfloat162 b2 = __floats2bfloat162_rn(o[c + e] * inv, o[c + e + 1] * inv);
+          for (int e = 0; e < 16; e += 2) {
+            __nv_bfloat162 b2 = __floats2bfloat162_rn(v[e] * inv, v[e + 1] * inv);
             pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
           }
           *reinterpret_cast<uint4*>(dst + c) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          *reinterpret_cast<uint4*>(dst + c + 8) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
       }
+      // O has been read: the next item's first P.V may overwrite it (it is
+      // issued after this CTA's softmax warps signal the next p_full)
+      tc_fence_before();
     }
   }
   tc_fence_before();
