@@ -845,6 +845,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(EpiCfg<0>::THREADS, 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
   }
   tc_fence_before();
+  __syncthreads();      // the CTA's own view of the allocation (racecheck does not model barrier.cluster)
   cluster_sync_all();   // barriers initialised and TMEM allocated in both CTAs
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
