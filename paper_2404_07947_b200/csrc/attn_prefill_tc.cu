@@ -223,31 +223,47 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
     if (lane == 0) {
       constexpr uint32_t idesc_s = umma_idesc_bf16(FQ, FK);                   // K-major A and B
       constexpr uint32_t idesc_o = umma_idesc_bf16(FQ, FD) | (1u << 16);      // B (V) MN-major
-      uint32_t nq = 0, base = 0;   // items, tiles before the current item
-      for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
-        Item it;
-        if (!item_of(p, id, it)) continue;
-        const int qs = nq & 1;
-        mbar_wait(&q_full[qs], (nq >> 1) & 1);
-        auto issue_s = [&](int j) {
-          const uint32_t gj = base + j;
-          const int s = gj & 1;
-          mbar_wait(&kv_full[s], (gj >> 1) & 1);
-          if (gj >= 2) mbar_wait(&s_free[s], ((gj >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t d = tmem + s * 128;
-          const uint32_t qa = smem_u32(sQ + qs * Q_BYTES), kb = smem_u32(sK + s * KV_BYTES);
+      // S_j of (item, its Q stage, global tile index gj)
+      auto issue_s = [&](const Item& it, int qs, uint32_t gj, bool last) {
+        const int s = gj & 1;
+        mbar_wait(&kv_full[s], (gj >> 1) & 1);
+        if (gj >= 2) mbar_wait(&s_free[s], ((gj >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + s * 128;
+        const uint32_t qa = smem_u32(sQ + qs * Q_BYTES), kb = smem_u32(sK + s * KV_BYTES);
 #pragma unroll
-          for (int k = 0; k < FD / 16; ++k) {
-            const uint32_t off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
-            umma_bf16(d, umma_desc_sw128(qa + off), umma_desc_sw128(kb + off), idesc_s, k ? 1u : 0u);
+        for (int k = 0; k < FD / 16; ++k) {
+          const uint32_t off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
+          umma_bf16(d, umma_desc_sw128(qa + off), umma_desc_sw128(kb + off), idesc_s, k ? 1u : 0u);
+        }
+        umma_commit(&s_full[s]);
+        if (last) umma_commit(&q_empty[qs]);   // last read of this Q
+      };
+      auto next_item = [&](int from, Item& it) {
+        for (int id = from; id < n_items; id += gridDim.x)
+          if (item_of(p, id, it)) return id;
+        return n_items;
+      };
+      uint32_t nq = 0, base = 0;   // items, tiles before the current item
+      Item cur, nxt;
+      int id = next_item(blockIdx.x, cur);
+      if (id < n_items) {
+        mbar_wait(&q_full[0], 0);
+        issue_s(cur, 0, 0, cur.ntiles == 1);
+      }
+      while (id < n_items) {
+        const int qs = nq & 1;
+        const int id_next = next_item(id + gridDim.x, nxt);
+        for (int j = 0; j < cur.ntiles; ++j) {
+          if (j + 1 < cur.ntiles) {
+            issue_s(cur, qs, base + j + 1, j + 2 == cur.ntiles);
+          } else if (id_next < n_items) {
+            // look ahead: the next item's first S while this item's last
+            // softmax and epilogue run
+            const uint32_t nqn = nq + 1;
+            mbar_wait(&q_full[nqn & 1], (nqn >> 1) & 1);
+            issue_s(nxt, nqn & 1, base + cur.ntiles, nxt.ntiles == 1);
           }
-          umma_commit(&s_full[s]);
-          if (j == it.ntiles - 1) umma_commit(&q_empty[qs]);   // last read of this Q
-        };
-        issue_s(0);
-        for (int j = 0; j < it.ntiles; ++j) {
-          if (j + 1 < it.ntiles) issue_s(j + 1);
           // O += P_j . V_j (one TMEM accumulator per item; the softmax warps
           // signal p_full after any lazy rescale of O and, for an item's
           // first tile, after reading out the previous item's O)
@@ -269,8 +285,10 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
           umma_commit(&o_full[gj & 1]);
           umma_commit(&kv_empty[s]);
         }
-        base += it.ntiles;
+        base += cur.ntiles;
         ++nq;
+        id = id_next;
+        cur = nxt;
       }
     }
   } else if (warp >= 4) {
@@ -329,25 +347,27 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
         // the previous tile's P.V has completed: P may be overwritten and O read
         if (j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
         // lazy rescale: the reference max moves only when this tile's max
-        // exceeds it by more than 2^RESCALE_LOG2 (the pair takes the same decision)
-        if (m == -INFINITY || (mx - m) * LOG2E > RESCALE_LOG2) {
-          const float m_new = fmaxf(m, mx);
-          if (j >= 1 && m != -INFINITY) {
-            const float alpha = ex2((m - m_new) * LOG2E);
-            tc_fence_after();
+        // exceeds it by more than 2^RESCALE_LOG2 (both threads of a row take the
+        // same decision); the TMEM accesses are warp-collective, so a warp
+        // rescales when any of its rows must (alpha = 1 for the others)
+        const bool move = m == -INFINITY || (mx - m) * LOG2E > RESCALE_LOG2;
+        const float m_new = move ? fmaxf(m, mx) : m;
+        const bool resc = move && j >= 1 && m != -INFINITY;
+        if (__any_sync(0xffffffffu, resc)) {
+          const float alpha = resc ? ex2((m - m_new) * LOG2E) : 1.f;
+          tc_fence_after();
 #pragma unroll
-            for (int c = 0; c < HD; c += 16) {
-              float v[16];
-              tmem_ld16(oa + c, v);
+          for (int c = 0; c < HD; c += 16) {
+            float v[16];
+            tmem_ld16(oa + c, v);
 #pragma unroll
-              for (int e = 0; e < 16; ++e) v[e] *= alpha;
-              tmem_st16(oa + c, v);
-            }
-            tmem_st_wait();
-            l *= alpha;
+            for (int e = 0; e < 16; ++e) v[e] *= alpha;
+            tmem_st16(oa + c, v);
           }
-          m = m_new;
+          tmem_st_wait();
+          l *= alpha;
         }
+        m = m_new;
         // p = 2^(s log2 e - m log2 e): one FFMA + an SFU op (or, for a quarter
         // of the keys, the FMA-pipe polynomial) per score
         const float nml = (m == -INFINITY) ? 0.f : -m * LOG2E;
