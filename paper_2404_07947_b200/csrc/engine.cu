@@ -160,6 +160,7 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
                 (shard.l1 >= 0 && shard.l1 != s.n_dec_layers)))
     throw std::invalid_argument("the fp32 path runs decoder-only models on one GPU (whole model, no TP / PP)");
   defer_ = (!t5_ && !D.f32 && shard.tp == 1 && s.d_model % 4 == 0 && s.d_model <= 16384) ? deferred_enabled() : 0;
+  chain_ = !t5_ && !D.f32 && shard.tp == 1 && s.d_model % 4 == 0 && s.d_model <= 16384 && chain_enabled();
   if (S_.l1 < 0) S_.l1 = D.L;
   if (S_.l0 < 0 || S_.l1 > D.L || S_.l0 >= S_.l1) throw std::invalid_argument("bad shard layer range");
   if (S_.tp < 1 || D.H % S_.tp || D.ff % S_.tp || S_.tp_rank < 0 || S_.tp_rank >= S_.tp)
@@ -189,7 +190,7 @@ Engine::~Engine() {
   cudaSetDevice(dev_);
   cudaStreamSynchronize(st_);
   for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)xkv_, (void*)last_tok_, (void*)err_,
-                  (void*)enc_bias_})
+                  (void*)enc_bias_, (void*)chain_ws_, (void*)chain_sync_})
     if (p) cudaFree(p);
   for (cudaEvent_t e : kev_) cudaEventDestroy(e);
   if (own_stream_ && st_) cudaStreamDestroy(st_);
@@ -410,6 +411,25 @@ void Engine::ensure_workspace(int max_tokens, int max_rows) {
     fff_ = carve<float>(p, T * D.ffl);
   }
   EXG_CUDA(cudaMemsetAsync(x_, 0, bytes, st_));
+  if (chain_) {
+    // decode chain workspace: the largest need over the token tiles up to R
+    size_t need = 0;
+    for (int t : {32, 64, 128, 256, (int)R}) {
+      if (t > (int)R && t != 32) continue;
+      need = std::max(need, chain_ws_floats(chain_spec(0, std::min<int>(t, (int)R), n_layers() > 1 ? 1 : -1)));
+    }
+    if (need > chain_ws_cap_) {
+      if (chain_ws_) EXG_CUDA(cudaFree(chain_ws_));
+      EXG_CUDA(cudaMalloc(&chain_ws_, need * sizeof(float)));
+      EXG_CUDA(cudaMemsetAsync(chain_ws_, 0, need * sizeof(float), st_));   // fixup counters start at 0
+      chain_ws_cap_ = need;
+    }
+    if (!chain_sync_) {
+      EXG_CUDA(cudaMalloc(&chain_sync_, 16 * sizeof(unsigned)));
+      EXG_CUDA(cudaMemsetAsync(chain_sync_, 0, 16 * sizeof(unsigned), st_));
+      chain_epoch_ = 0;
+    }
+  }
 }
 
 void Engine::ensure_kv(int slots, int slot_ctx, int layers, int xctx) {
@@ -667,6 +687,14 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
   const LayerW& w = layers_[l];
   const int B = db.B, d = D.d, il = D.inner_l;
   const float scale = (float)(1.0 / std::sqrt((double)D.dh));
+  if (chain_ && part == 0) {
+    // one layer's work as the chained decode runs it: the attention, then one
+    // chain launch (O-proj .. FFN2 and this layer's LN1 + QKV in place of the
+    // next layer's)
+    if (attn) dec_attention(l, db);
+    if (rest) dec_rest_chain(l, db, l);
+    return;
+  }
   if (part == 2) {
     layernorm(h_, d, x_, d, w.ln2_g, w.ln2_b, B, d, 1e-5f, st_);
     linear_dec(h_, d, B, w.W1, D.ffl, d, epi_bf16(w.b1, ff_, D.ffl, D.act));
@@ -746,6 +774,89 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
   }
 }
 
+ChainSpec Engine::chain_spec(int l, int B, int next_l) const {
+  const LayerW& w = layers_[l];
+  const int d = D.d, il = D.inner_l;
+  ChainSpec c;
+  c.tokens = B;
+  c.d = d;
+  c.x = x_;
+  c.h = h_;
+  c.eps = 1e-5f;
+  auto resid = [&](const bf16* bias) {
+    EpiParams e;
+    e.mode = EPI_RESID;
+    e.bias = bias;
+    e.resid = x_;
+    e.ldr = d;
+    return e;
+  };
+  c.ph[0].X = ctx_, c.ph[0].ldx = il, c.ph[0].Wb = w.Wo, c.ph[0].features = d, c.ph[0].K = il;
+  c.ph[0].ep = resid(w.bo);
+  c.ph[0].ln_after = 0;
+  c.ln_g[0] = w.ln2_g, c.ln_b[0] = w.ln2_b;
+  c.ph[1].X = h_, c.ph[1].ldx = d, c.ph[1].Wb = w.W1, c.ph[1].features = D.ffl, c.ph[1].K = d;
+  c.ph[1].ep = epi_bf16(w.b1, ff_, D.ffl, D.act);
+  c.ph[2].X = ff_, c.ph[2].ldx = D.ffl, c.ph[2].Wb = w.W2, c.ph[2].features = d, c.ph[2].K = D.ffl;
+  c.ph[2].ep = resid(w.b2);
+  c.n = 3;
+  if (next_l >= 0) {
+    const LayerW& nx = layers_[next_l];
+    c.ph[2].ln_after = 1;
+    c.ln_g[1] = nx.ln1_g, c.ln_b[1] = nx.ln1_b;
+    c.ph[3].X = h_, c.ph[3].ldx = d, c.ph[3].Wb = nx.Wqkv, c.ph[3].features = 3 * il, c.ph[3].K = d;
+    c.ph[3].ep = epi_bf16(nx.bqkv, qkv_, 3 * il);
+    c.n = 4;
+  }
+  return c;
+}
+
+void Engine::dec_rest_chain(int l, const DecodeBatch& db, int next_l) {
+  ChainSpec c = chain_spec(l, db.B, next_l);
+  c.ws = chain_ws_;
+  c.ws_floats = chain_ws_cap_;
+  c.sync = chain_sync_;
+  c.epoch = ++chain_epoch_;
+  double bytes = 0;
+  for (int q = 0; q < c.n; ++q) {
+    const double out_b = c.ph[q].ep.mode == EPI_RESID ? 8.0 : 2.0;
+    bytes += 2.0 * c.ph[q].features * c.ph[q].K + 2.0 * db.B * c.ph[q].K + out_b * db.B * c.ph[q].features;
+  }
+  const int k = kbegin();
+  decode_chain(c, st_);
+  kend(k, EXG_K_DECODE_GEMM, bytes);
+}
+
+void Engine::dec_attention(int l, const DecodeBatch& db) {
+  const int B = db.B, il = D.inner_l;
+  DecodeAttnArgs da;
+  da.knew = qkv_ + il;
+  da.vnew = qkv_ + 2 * il;
+  da.ldnew = 3 * il;
+  da.q = qkv_;
+  da.ldq = 3 * il;
+  da.kc = kc(l);
+  da.vc = vc(l);
+  da.slot = db.slot;
+  da.n_keys = db.nkeys;
+  da.out = ctx_;
+  da.ldo = il;
+  da.B = B;
+  da.H = D.Hl;
+  da.dh = D.dh;
+  da.max_ctx = slot_ctx_;
+  da.scale = (float)(1.0 / std::sqrt((double)D.dh));
+  const int sl = split_len();
+  da.split_len = sl;
+  da.max_splits = std::max(1, (db.max_keys + sl - 1) / sl);
+  da.partial = attn_part_;
+  da.counters = attn_cnt_;
+  const int k = kbegin();
+  decode_attention(da, st_);
+  kend(k, EXG_K_DECODE_ATTN, db.sum_keys * 2.0 * D.Hl * D.dh * 2.0 + (double)B * D.Hl * D.dh * 2.0 * 2.0 +
+                                 (double)B * 2.0 * D.Hl * D.dh * 2.0);
+}
+
 void Engine::ln_decode(const bf16* g, const bf16* b, int rows) {
   if (pend_res_.P) {
     const PendingResid pr = pend_res_;
@@ -776,7 +887,19 @@ void Engine::decode(const DecodeBatch& db) {
   if (t5_ && S_.t5_role == 1) throw std::logic_error("T5 encoder-side shard: no decoder layers");
   if (S_.tp > 1 && !red_) throw std::logic_error("TP shard without a reducer: drive it through a TP group");
   embed_decode(db);
-  for (int l = 0; l < n_layers(); ++l) layer_decode(l, db, true, true);
+  if (chain_) {
+    // layer 0's LN1 + QKV, then per layer: the attention and one chain launch
+    // (O-proj, LN2, FFN1, FFN2 and the next layer's LN1 + QKV)
+    const LayerW& w0 = layers_[0];
+    layernorm(h_, D.d, x_, D.d, w0.ln1_g, w0.ln1_b, db.B, D.d, 1e-5f, st_);
+    linear_dec(h_, D.d, db.B, w0.Wqkv, 3 * D.inner_l, D.d, epi_bf16(w0.bqkv, qkv_, 3 * D.inner_l));
+    for (int l = 0; l < n_layers(); ++l) {
+      dec_attention(l, db);
+      dec_rest_chain(l, db, l + 1 < n_layers() ? l + 1 : -1);
+    }
+  } else {
+    for (int l = 0; l < n_layers(); ++l) layer_decode(l, db, true, true);
+  }
   head_decode(db);
 }
 

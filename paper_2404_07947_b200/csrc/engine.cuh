@@ -227,6 +227,17 @@ class Engine {
   } pend_res_;
   // LayerNorm of x into h_, folding a pending deferred residual update first
   void ln_decode(const bf16* g, const bf16* b, int rows);
+  // decode GEMM chain (gemm_tc.cuh decode_chain): one launch per layer for
+  // O-proj, LN2, FFN1, FFN2 (+ LN1 and QKV of layer next_l when >= 0);
+  // decoder-only, tp = 1, bf16
+  bool chain_ = false;
+  float* chain_ws_ = nullptr;
+  size_t chain_ws_cap_ = 0;
+  unsigned* chain_sync_ = nullptr;
+  unsigned chain_epoch_ = 0;
+  void dec_attention(int l, const DecodeBatch& db);
+  void dec_rest_chain(int l, const DecodeBatch& db, int next_l);
+  ChainSpec chain_spec(int l, int B, int next_l) const;
   float* splitk_ws_ = nullptr;
   size_t splitk_cap_ = 0;
   float* attn_part_ = nullptr;

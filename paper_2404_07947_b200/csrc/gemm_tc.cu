@@ -591,6 +591,401 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
   }
 }
 
+// ============================================================================
+// Decode GEMM chain (one persistent launch per decoder layer): the
+// O-projection (+ residual), LN2, FFN1 (+ act), FFN2 (+ residual) and -- when
+// another layer follows -- that layer's LN1 and QKV, between two decode
+// attention launches.  Every GEMM phase keeps its own stream-K cut (Work of
+// its weight shape, G_p = min(#SMs, I_p)), epilogues and in-kernel fixups --
+// the arithmetic of the separate launches, so results are bit-identical --
+// but the weight stream never stops at a phase boundary: the producer keeps
+// issuing the next phase's weight blocks into the ring while that phase's
+// activations are not ready yet (their TMA loads are queued and issued once
+// the phase's inputs are complete), and the epilogue warps overlap a phase's
+// fixups / LayerNorm with the next phase's mainloop.  Readiness between
+// phases is a grid-wide counter per phase in global memory (every CTA adds
+// one when its epilogue has finished the phase; LN phases add a second
+// counter), monotonic across launches (targets grid x epoch).
+// ============================================================================
+constexpr int CHAIN_MAX = 4;
+struct ChainPhase {
+  const bf16* Wb;
+  Work w;
+  EpiParams ep;
+  float* partial;
+  int* counters;
+  int M, N, n_wblk;
+  int ln_after;          // LayerNorm of x into h once this phase is complete (index into ln[]), -1: none
+};
+struct ChainLN {
+  const bf16 *g, *b;
+};
+struct ChainArgs {
+  int n;
+  ChainPhase ph[CHAIN_MAX];
+  ChainLN ln[2];
+  float* x;
+  bf16* h;
+  int d;
+  float eps;
+  unsigned* sync;        // [2 * CHAIN_MAX]: done[p], ln_done[p]
+  unsigned epoch;        // this launch's number (>= 1): counters reach grid * epoch
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// spin until *p reaches target (wrap-around compare); traps after ~4 s
+__device__ __forceinline__ void wait_counter(const unsigned* p, unsigned target) {
+  if ((int)(ld_acquire_u32(p) - target) >= 0) return;
+  const long long t0 = clock64();
+  while ((int)(ld_acquire_u32(p) - target) < 0) {
+    __nanosleep(128);
+    if (clock64() - t0 > 8000000000LL) {
+      printf("exg: chain counter wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+}
+
+struct ChainIter {
+  const ChainArgs* a;
+  UnitIter it;
+  int p;
+  __device__ void init(const ChainArgs* args) {
+    a = args;
+    p = 0;
+    it.init(a->ph[0].w, blockIdx.x);
+  }
+  // next unit of this CTA; phase index in *ph.  Returns false at the end.
+  __device__ bool next(Unit& u, int* ph) {
+    while (p < a->n) {
+      if ((int)blockIdx.x < a->ph[p].w.G && it.next(u)) {
+        *ph = p;
+        return true;
+      }
+      if (++p < a->n) it.init(a->ph[p].w, blockIdx.x);
+    }
+    return false;
+  }
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
+    decode_chain_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
+                        const __grid_constant__ CUtensorMap tm2, const __grid_constant__ CUtensorMap tm3,
+                        const __grid_constant__ ChainArgs ca) {
+  constexpr int EPI_WARPS = EpiCfg<1>::WARPS;
+  auto epi_bar = [] { asm volatile("bar.sync 1, %0;" ::"n"(32 * EpiCfg<1>::WARPS) : "memory"); };
+  griddep_launch_dependents();
+  constexpr int B_BYTES = BN * BK * 2;
+  constexpr uint32_t TMEM_COLS =
+      (2 * BN <= 32) ? 32 : (2 * BN <= 64 ? 64 : (2 * BN <= 128 ? 128 : (2 * BN <= 256 ? 256 : 512)));
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;      // [2]
+  uint64_t* tempty = tfull + 2;          // [2]
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_holder + 1);
+  float* red = reinterpret_cast<float*>(s_last + 1) + 2;   // [8] LayerNorm partial sums
+
+  const CUtensorMap* tms[CHAIN_MAX] = {&tm0, &tm1, &tm2, &tm3};
+  const unsigned G = gridDim.x;
+  unsigned* done = ca.sync;
+  unsigned* ln_done = ca.sync + CHAIN_MAX;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp == 0 && lane == 0) {
+    for (int q = 0; q < ca.n; ++q) prefetch_tmap(tms[q]);
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
+    }
+    for (int a2 = 0; a2 < 2; ++a2) {
+      mbar_init(&tfull[a2], 1);
+      mbar_init(&tempty[a2], EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_holder, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  // the inputs of phase q are complete: q = 0 -> the previous kernel (PDL);
+  // else the previous phase (or the LayerNorm that follows it) on every CTA
+  auto inputs_ready = [&](int q) {
+    if (q == 0) {
+      griddep_wait();
+    } else {
+      const int pq = q - 1;
+      wait_counter(ca.ph[pq].ln_after >= 0 ? &ln_done[pq] : &done[pq], G * ca.epoch);
+    }
+    fence_proxy_async_global();   // generic-proxy writes of other CTAs -> this CTA's TMA reads
+  };
+
+  ChainIter it;
+  it.init(&ca);
+  Unit u;
+  int ph;
+  if (warp == 0) {
+    if (lane == 0) {
+      // weight blocks stream ahead of their activations: a stage's activation
+      // load waits in a FIFO until its phase's inputs are ready
+      int pend_s[STAGES], pend_ph[STAGES], pend_n[STAGES], pend_kb[STAGES];
+      int ph_head = 0, ph_tail = 0;
+      int ready = -1;   // highest phase whose inputs are known ready
+      auto flush = [&](bool block) {
+        while (ph_head != ph_tail) {
+          const int k = ph_head % STAGES;
+          const int q = pend_ph[k];
+          if (q > ready) {
+            if (!block) return;
+            inputs_ready(q);
+            ready = q;
+          }
+          tma_load_2d(sB + pend_s[k] * B_BYTES, tms[q], &full[pend_s[k]], pend_kb[k] * BK, pend_n[k] * BN);
+          ++ph_head;
+        }
+      };
+      uint32_t g = 0;
+      while (it.next(u, &ph)) {
+        const ChainPhase& P = ca.ph[ph];
+        for (int kb = u.kb0; kb < u.kb1; ++kb, ++g) {
+          const uint32_t s = g % STAGES;
+          const uint32_t par = (g / STAGES) & 1;
+          if (g >= STAGES) {
+            // a stage is reused only after the MMA consumed it, which needs
+            // its activation: queued loads of older stages go out first
+            if (ph_tail - ph_head == STAGES) flush(true);
+            mbar_wait(&empty[s], par ^ 1);
+          }
+          mbar_arrive_expect_tx(&full[s], A_BYTES + B_BYTES);
+          bulk_load(sA + s * A_BYTES, P.Wb + ((int64_t)u.m * P.w.nkb + kb) * BLK_ELEMS, A_BYTES, &full[s]);
+          if (ph <= ready && ph_head == ph_tail) {
+            tma_load_2d(sB + s * B_BYTES, tms[ph], &full[s], kb * BK, u.n * BN);
+          } else {
+            const int k = ph_tail % STAGES;
+            pend_s[k] = s, pend_ph[k] = ph, pend_n[k] = u.n, pend_kb[k] = kb;
+            ++ph_tail;
+            flush(false);
+          }
+        }
+      }
+      flush(true);
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
+      uint32_t g = 0, ui = 0;
+      while (it.next(u, &ph)) {
+        const uint32_t a2 = ui & 1;
+        if (ui >= 2) mbar_wait(&tempty[a2], ((ui >> 1) & 1) ^ 1);
+        tc_fence_after();
+        const uint32_t dtm = tmem + a2 * BN;
+        for (int kb = u.kb0; kb < u.kb1; ++kb, ++g) {
+          const uint32_t s = g % STAGES;
+          mbar_wait(&full[s], (g / STAGES) & 1);
+          tc_fence_after();
+          const uint32_t a_base = smem_u32(sA + s * A_BYTES);
+          const uint32_t b_base = smem_u32(sB + s * B_BYTES);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(dtm, umma_desc_sw128(a_base + k * 32), umma_desc_sw128(b_base + k * 32), idesc,
+                      (kb != u.kb0 || k) ? 1u : 0u);
+          umma_commit(&empty[s]);
+        }
+        umma_commit(&tfull[a2]);
+        ++ui;
+      }
+    }
+  } else if (warp >= 4) {
+    const int q4 = warp & 3;
+    constexpr int PARTS = EPI_WARPS / 4;
+    const int part = (warp - 4) >> 2;
+    const int c_lo = part * (BN / PARTS), c_hi = c_lo + BN / PARTS;
+    const int et = threadIdx.x - 128;      // 0..255 within the epilogue group
+    const int r = q4 * 32 + lane;
+    griddep_wait();   // outputs / residual may still be in use by the previous kernel
+    uint32_t ui = 0;
+    int cur = -1;     // phase whose units this group is storing
+    // end of phase q for this CTA: publish, then the LayerNorm rows of this CTA
+    auto finish_phase = [&](int q) {
+      __threadfence();
+      epi_bar();
+      if (et == 0) red_release_add(&done[q], 1u);
+      const int li = ca.ph[q].ln_after;
+      if (li < 0) {
+        // every counter advances by one per CTA per launch (targets grid x epoch)
+        if (et == 0) red_release_add(&ln_done[q], 1u);
+        return;
+      }
+      // LayerNorm of x into h (rows blockIdx.x, +G, ..): the arithmetic of
+      // norm_reg_kernel (256 threads, fp32 statistics, two block sums)
+      if (et == 0) wait_counter(&done[q], G * ca.epoch);
+      epi_bar();
+      const int rows = ca.ph[q].ep.tokens;
+      const int d = ca.d, n4 = d >> 2;
+      const int nv = (n4 + 255) / 256;
+      for (int row = blockIdx.x; row < rows; row += G) {
+        const float4* xr = reinterpret_cast<const float4*>(ca.x + (int64_t)row * d);
+        float4 v[16];
+        float sm = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if (k >= nv) break;
+          const int i = et + k * 256;
+          v[k] = i < n4 ? __ldcg(xr + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+          sm += (v[k].x + v[k].y) + (v[k].z + v[k].w);
+        }
+        auto block_sum = [&](float val) {
+          val = warp_sum(val);
+          epi_bar();
+          if (lane == 0) red[et >> 5] = val;
+          epi_bar();
+          float t = 0.f;
+#pragma unroll
+          for (int w2 = 0; w2 < 8; ++w2) t += red[w2];
+          return t;
+        };
+        const float mean = block_sum(sm) / (float)d;
+        float qq = 0.f;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if (k >= nv) break;
+          if (et + k * 256 >= n4) continue;
+          const float a0 = v[k].x - mean, b0 = v[k].y - mean, c0 = v[k].z - mean, e0 = v[k].w - mean;
+          qq += (a0 * a0 + b0 * b0) + (c0 * c0 + e0 * e0);
+        }
+        const float rstd = rsqrtf(block_sum(qq) / (float)d + ca.eps);
+        bf16* yr = ca.h + (int64_t)row * d;
+        const ChainLN& L = ca.ln[li];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          if (k >= nv) break;
+          const int i = et + k * 256;
+          if (i >= n4) continue;
+          const uint2 gr = reinterpret_cast<const uint2*>(L.g)[i];
+          const float2 g01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gr.x));
+          const float2 g23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&gr.y));
+          const uint2 br = reinterpret_cast<const uint2*>(L.b)[i];
+          const float2 b01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.x));
+          const float2 b23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&br.y));
+          const float o0 = (v[k].x - mean) * rstd * g01.x + b01.x;
+          const float o1 = (v[k].y - mean) * rstd * g01.y + b01.y;
+          const float o2 = (v[k].z - mean) * rstd * g23.x + b23.x;
+          const float o3 = (v[k].w - mean) * rstd * g23.y + b23.y;
+          __nv_bfloat162 p0 = __floats2bfloat162_rn(o0, o1), p1 = __floats2bfloat162_rn(o2, o3);
+          uint2 outv;
+          outv.x = *reinterpret_cast<uint32_t*>(&p0);
+          outv.y = *reinterpret_cast<uint32_t*>(&p1);
+          reinterpret_cast<uint2*>(yr)[i] = outv;
+        }
+      }
+      __threadfence();
+      epi_bar();
+      if (et == 0) red_release_add(&ln_done[q], 1u);
+    };
+    while (it.next(u, &ph)) {
+      while (cur < ph) {   // phases before this unit's are complete on this CTA
+        if (cur >= 0) finish_phase(cur);
+        ++cur;
+      }
+      const ChainPhase& P = ca.ph[ph];
+      const EpiParams& ep = P.ep;
+      const uint32_t a2 = ui & 1;
+      mbar_wait(&tfull[a2], (ui >> 1) & 1);
+      tc_fence_after();
+      const int gm = u.m * BM + r;
+      const uint32_t taddr = tmem + ((uint32_t)(q4 * 32) << 16) + a2 * BN;
+      const bool row_ok = gm < P.M;
+      if (!u.full) {
+        float* pp = P.partial + (((int64_t)u.n * P.w.tiles_m + u.m) * P.w.max_segs + u.seg) * (int64_t)(BM * BN);
+        for (int c = c_lo; c < c_hi; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pp[(int64_t)(c + j) * BM + r] = v[j];
+        }
+      } else {
+        for (int c = c_lo; c < c_hi; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + c, v);
+          if (row_ok && u.n * BN + c < P.N) epi_store_col16(ep, u.n * BN + c, gm, P.N, v);
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[a2]);
+      ++ui;
+      if (!u.full) {
+        // stream-K fixup: the CTA completing the tile's last segment reduces
+        const int64_t x0 = (int64_t)u.m * P.w.nkb;
+        const int nseg = sk_owner(P.w, x0 + P.w.nkb - 1) - sk_owner(P.w, x0) + 1;
+        int* cnt = P.counters + (u.n * P.w.tiles_m + u.m);
+        __threadfence();
+        epi_bar();
+        if (et == 0) *s_last = (atomicAdd(cnt, 1) == nseg - 1);
+        epi_bar();
+        if (*s_last) {
+          __threadfence();
+          const float* base = P.partial + ((int64_t)u.n * P.w.tiles_m + u.m) * P.w.max_segs * (int64_t)(BM * BN);
+          for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+            float acc[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+            for (int s0 = 0; s0 < nseg; s0 += 4) {
+              float v[4][16];
+#pragma unroll
+              for (int qv = 0; qv < 4; ++qv) {
+                const float* src = base + (int64_t)(s0 + qv) * BM * BN + (int64_t)c0 * BM + r;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) v[qv][j] = (s0 + qv < nseg) ? __ldcg(src + (int64_t)j * BM) : 0.f;
+              }
+#pragma unroll
+              for (int qv = 0; qv < 4; ++qv)
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                  if (s0 + qv < nseg) acc[j] += v[qv][j];
+            }
+            if (!row_ok) continue;
+            if (u.n * BN + c0 < P.N) epi_store_col16(ep, u.n * BN + c0, gm, P.N, acc);
+          }
+          if (et == 0) *cnt = 0;
+        }
+        epi_bar();
+      }
+    }
+    // the remaining phases (including ones with no units on this CTA)
+    while (cur < ca.n) {
+      if (cur >= 0) finish_phase(cur);
+      ++cur;
+    }
+    // counters of the phases this launch does not have
+    if (et == 0)
+      for (int q = ca.n; q < CHAIN_MAX; ++q) {
+        red_release_add(&done[q], 1u);
+        red_release_add(&ln_done[q], 1u);
+      }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
 // Ring depth: up to 8 stages within ~200 KB (one CTA per SM).  Measured: a
 // half-SM ring (2 CTAs/SM so the next GEMM co-resides under PDL) loses more
 // weight-stream depth than the overlap gains.
@@ -1009,6 +1404,11 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
+bool& chain_enabled() {
+  static bool on = true;
+  return on;
+}
+
 int& deferred_enabled() {
   static int on = DEFER_DEFAULT;
   return on;
@@ -1076,9 +1476,89 @@ void linear(const LinearArgs& a, cudaStream_t st) {
   }
 }
 
+size_t chain_ws_floats(const ChainSpec& c) {
+  const int BN = decode_bn(c.tokens);
+  size_t total = 0;
+  for (int q = 0; q < c.n; ++q) total += ws_need(make_work(c.ph[q].features, c.tokens, c.ph[q].K, BN, true), BN);
+  return total;
+}
+
+namespace {
+template <int BN>
+void launch_chain(const ChainSpec& c, cudaStream_t st) {
+  constexpr int S = stages_for<BN, 1>();
+  const size_t smem = smem_bytes<BN, 1>() + 64;
+  static bool attr_set = false;
+  if (!attr_set) {
+    EXG_CUDA(cudaFuncSetAttribute(decode_chain_kernel<BN, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_set = true;
+  }
+  ChainArgs a = {};
+  a.n = c.n;
+  CUtensorMap tm[CHAIN_MAX];
+  float* ws = c.ws;
+  size_t used = 0;
+  for (int q = 0; q < CHAIN_MAX; ++q) {
+    const int qq = q < c.n ? q : c.n - 1;   // unused maps: any valid one
+    tm[q] = make_tmap_bf16(c.ph[qq].X, c.tokens, c.ph[qq].K, c.ph[qq].ldx, BN);
+  }
+  for (int q = 0; q < c.n; ++q) {
+    ChainPhase& P = a.ph[q];
+    P.Wb = c.ph[q].Wb;
+    P.M = c.ph[q].features;
+    P.N = c.tokens;
+    P.n_wblk = (P.M + BM - 1) / BM;
+    P.w = make_work(P.M, c.tokens, c.ph[q].K, BN, true);
+    P.ep = c.ph[q].ep;
+    P.ep.tokens = c.tokens;
+    P.ep.features = P.M;
+    P.ln_after = c.ph[q].ln_after;
+    const size_t need = ws_need(P.w, BN);
+    if ((size_t)P.w.tiles_n * P.w.tiles_m > CNT_CAP) throw CudaError("decode chain: too many tiles for the counter region");
+    if (used + need > c.ws_floats) throw CudaError("decode chain workspace too small");
+    P.counters = reinterpret_cast<int*>(ws + used);
+    P.partial = ws + used + CNT_CAP;
+    used += need;
+  }
+  for (int i = 0; i < 2; ++i) a.ln[i] = ChainLN{c.ln_g[i], c.ln_b[i]};
+  a.x = c.x;
+  a.h = c.h;
+  a.d = c.d;
+  a.eps = c.eps;
+  a.sync = c.sync;
+  a.epoch = c.epoch;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms());
+  cfg.blockDim = dim3(EpiCfg<1>::THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  EXG_CUDA(cudaLaunchKernelEx(&cfg, decode_chain_kernel<BN, S>, tm[0], tm[1], tm[2], tm[3], a));
+  EXG_CHECK_LAUNCH();
+}
+}  // namespace
+
+void decode_chain(const ChainSpec& c, cudaStream_t st) {
+  if (c.n < 1 || c.n > CHAIN_MAX) throw CudaError("decode chain: 1..4 phases");
+  if (c.tokens <= 0) return;
+  if ((c.d & 3) || c.d > 16384) throw CudaError("decode chain: LayerNorm width");
+  switch (decode_bn(c.tokens)) {
+    case 32: launch_chain<32>(c, st); break;
+    case 64: launch_chain<64>(c, st); break;
+    case 128: launch_chain<128>(c, st); break;
+    default: launch_chain<256>(c, st); break;
+  }
+}
+
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
+// decode GEMM chain for engines created after the call (1 = on, default; 0 = separate launches)
+extern "C" void exg_diag_chain(int on) { exg::chain_enabled() = on != 0; }
 // deferred stream-K reductions for engines created after the call: bit 0 =
 // QKV (summed by the decode attention), bit 1 = O-projection / FFN2 (summed by
 // the following LayerNorm); -1 restores the default

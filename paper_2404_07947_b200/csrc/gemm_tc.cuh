@@ -70,6 +70,7 @@ constexpr int DEFER_QKV = 1, DEFER_RESID = 2;
 // deferred QKV sums cost the attention kernel more than they save the GEMM
 constexpr int DEFER_DEFAULT = DEFER_RESID;
 int& deferred_enabled();    // mask of deferred decode GEMMs (exg_diag_deferred)
+bool& chain_enabled();      // decode GEMM chain (exg_diag_chain)
 // floats a deferred decode GEMM writes: max segments x tokens x features
 size_t deferred_floats(int features, int K, int tokens);
 
@@ -111,5 +112,35 @@ struct LinearArgs {
 void linear(const LinearArgs& a, cudaStream_t st);
 
 int decode_bn(int tokens);
+
+// Decode GEMM chain (gemm_tc.cu decode_chain_kernel): up to 4 decode GEMMs
+// (same token count) in one persistent launch, each with its own stream-K
+// cut, epilogue and in-kernel fixup -- bit-identical to separate launches --
+// with an optional LayerNorm of x into h after a phase (ln_after = index
+// into ln_g / ln_b).  Phase q's activations X must be complete once phase
+// q-1 (and its LayerNorm) is; phase 0 waits for the previous kernel (PDL).
+struct ChainSpec {
+  struct Phase {
+    const bf16* X = nullptr;
+    int64_t ldx = 0;
+    const bf16* Wb = nullptr;
+    int features = 0, K = 0;
+    EpiParams ep;
+    int ln_after = -1;
+  } ph[4];
+  int n = 0, tokens = 0;
+  const bf16* ln_g[2] = {nullptr, nullptr};
+  const bf16* ln_b[2] = {nullptr, nullptr};
+  float* x = nullptr;      // fp32 residual [tokens][d] (the LayerNorm input)
+  bf16* h = nullptr;       // bf16 [tokens][d] (the LayerNorm output)
+  int d = 0;
+  float eps = 1e-5f;
+  float* ws = nullptr;     // chain_ws_floats() floats, zero-initialised once
+  size_t ws_floats = 0;
+  unsigned* sync = nullptr;   // 8 zero-initialised counters, owned by the caller
+  unsigned epoch = 0;         // 1, 2, ... per launch on the same sync counters
+};
+size_t chain_ws_floats(const ChainSpec& c);
+void decode_chain(const ChainSpec& c, cudaStream_t st);
 
 }  // namespace exg

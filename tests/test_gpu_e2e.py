@@ -231,6 +231,7 @@ def test_deferred_stream_k_reduction_bit_identical(n_req, b_d):
     spec = ModelSpec("defer-w2048", "opt", 0, 2, 2048, 16, 128, 8192, 4096, 512)
     reqs = make_requests(n_req, uniform_pmf(8, 64), uniform_pmf(2, 12), spec.vocab, 0xD3F)
     outs = []
+    X.lib().exg_diag_chain(0)   # the per-kernel decode path carries the deferred reductions
     for mask in (0, 1, 2, 3):   # none / QKV / O-proj + FFN2 / all
         X.lib().exg_diag_deferred(mask)
         try:
@@ -239,6 +240,37 @@ def test_deferred_stream_k_reduction_bit_identical(n_req, b_d):
             ctx.close()
         finally:
             X.lib().exg_diag_deferred(-1)
+    X.lib().exg_diag_chain(1)
+    for o in outs[1:]:
+        assert o[0] == outs[0][0]
+        for r in range(len(reqs)):
+            assert np.array_equal(o[3][r], outs[0][3][r]), r
+
+
+@pytest.mark.parametrize("n_req,b_d,n_layers", [(24, 20, 3), (160, 150, 2), (9, 9, 1)])
+def test_decode_chain_bit_identical(n_req, b_d, n_layers):
+    """The decode GEMM chain (one persistent launch per layer for O-proj,
+    LN2, FFN1, FFN2 and the next layer's LN1 + QKV; gemm_tc.cu) keeps every
+    GEMM's stream-K cut, epilogue and fixup and the LayerNorm's arithmetic:
+    ids and logits bit-identical to the separate launches, with split tiles
+    (width 2048), every token tile class, 1-3 layers (chains with and
+    without the next layer's QKV), repeated launches on the same counters."""
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2404_07947_b200 as X
+    from workload import ModelSpec, make_requests, uniform_pmf
+    spec = ModelSpec("chain-w2048", "gpt3", 0, n_layers, 2048, 16, 128, 8192, 4096, 512)
+    reqs = make_requests(n_req, uniform_pmf(8, 64), uniform_pmf(2, 12), spec.vocab, 0xC4A1)
+    outs = []
+    for on in (0, 1):
+        X.lib().exg_diag_chain(on)
+        try:
+            ctx = X.Context(spec, 0xE6E0_0C4A)
+            outs.append(ctx.run(X.rra_schedule(min(n_req, b_d), b_d, 4), reqs, dump=range(len(reqs))))
+            outs.append(ctx.run(X.rra_schedule(min(n_req, b_d), b_d, 4), reqs, dump=range(len(reqs))))
+            ctx.close()
+        finally:
+            X.lib().exg_diag_chain(1)
     for o in outs[1:]:
         assert o[0] == outs[0][0]
         for r in range(len(reqs)):

@@ -17,12 +17,15 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 spec = MODELS["opt-13b"]
 d = task_dists("S")
 reqs = make_requests(n, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E10002)
-MODES = [int(x) for x in os.environ.get("EXG_DEFER_MODES", "0,2,3").split(",")]
+# modes: 0..3 = deferred mask with the per-kernel decode path; 10 = decode GEMM chain
+MODES = [int(x) for x in os.environ.get("EXG_DEFER_MODES", "2,10").split(",")]
 ctxs = {}
 for on in MODES:
-    X.lib().exg_diag_deferred(on)
+    X.lib().exg_diag_chain(1 if on == 10 else 0)
+    X.lib().exg_diag_deferred(on if on < 10 else -1)
     ctxs[on] = X.Context(spec, weight_seed(2))
 X.lib().exg_diag_deferred(-1)
+X.lib().exg_diag_chain(1)
 sched = X.rra_schedule(56, 83, 32)
 toks = {}
 for r in range(reps):
