@@ -1476,10 +1476,15 @@ void linear(const LinearArgs& a, cudaStream_t st) {
   }
 }
 
+// chain workspace: [CHAIN_MAX counter regions of CNT_CAP ints][partials of
+// phase 0][partials of phase 1]..  The counter regions sit at fixed offsets
+// for every token tile (the partials' layout changes with BN), so the zero
+// state the fixups leave behind is where the next launch looks
 size_t chain_ws_floats(const ChainSpec& c) {
   const int BN = decode_bn(c.tokens);
-  size_t total = 0;
-  for (int q = 0; q < c.n; ++q) total += ws_need(make_work(c.ph[q].features, c.tokens, c.ph[q].K, BN, true), BN);
+  size_t total = (size_t)CHAIN_MAX * CNT_CAP;
+  for (int q = 0; q < c.n; ++q)
+    total += ws_need(make_work(c.ph[q].features, c.tokens, c.ph[q].K, BN, true), BN) - CNT_CAP;
   return total;
 }
 
@@ -1497,7 +1502,7 @@ void launch_chain(const ChainSpec& c, cudaStream_t st) {
   a.n = c.n;
   CUtensorMap tm[CHAIN_MAX];
   float* ws = c.ws;
-  size_t used = 0;
+  size_t used = (size_t)CHAIN_MAX * CNT_CAP;
   for (int q = 0; q < CHAIN_MAX; ++q) {
     const int qq = q < c.n ? q : c.n - 1;   // unused maps: any valid one
     tm[q] = make_tmap_bf16(c.ph[qq].X, c.tokens, c.ph[qq].K, c.ph[qq].ldx, BN);
@@ -1513,11 +1518,11 @@ void launch_chain(const ChainSpec& c, cudaStream_t st) {
     P.ep.tokens = c.tokens;
     P.ep.features = P.M;
     P.ln_after = c.ph[q].ln_after;
-    const size_t need = ws_need(P.w, BN);
+    const size_t need = ws_need(P.w, BN) - CNT_CAP;   // partials
     if ((size_t)P.w.tiles_n * P.w.tiles_m > CNT_CAP) throw CudaError("decode chain: too many tiles for the counter region");
     if (used + need > c.ws_floats) throw CudaError("decode chain workspace too small");
-    P.counters = reinterpret_cast<int*>(ws + used);
-    P.partial = ws + used + CNT_CAP;
+    P.counters = reinterpret_cast<int*>(ws + (size_t)q * CNT_CAP);
+    P.partial = ws + used;
     used += need;
   }
   for (int i = 0; i < 2; ++i) a.ln[i] = ChainLN{c.ln_g[i], c.ln_b[i]};
