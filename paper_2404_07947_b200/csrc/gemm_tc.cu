@@ -676,6 +676,20 @@ struct ChainIter {
   }
 };
 
+// diagnostics (exg_diag_chain_timeline): per-CTA %globaltimer marks of the
+// last chain launch -- [0] entry, [1+q] producer: inputs of phase q ready,
+// [5+q] epilogue: phase q finished on this CTA, [9+q] LayerNorm after q done,
+// [13] producer: last load issued, [14] epilogue exit
+__device__ unsigned long long g_chain_tl[256 * 16];
+__device__ int g_chain_tl_on;
+__device__ __forceinline__ void chain_mark(int k) {
+  if (g_chain_tl_on) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (blockIdx.x < 256) g_chain_tl[blockIdx.x * 16 + k] = t;
+  }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
     decode_chain_kernel(const __grid_constant__ CUtensorMap tm0, const __grid_constant__ CUtensorMap tm1,
@@ -721,6 +735,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  if (threadIdx.x == 0) chain_mark(0);
 
   // the inputs of phase q are complete: q = 0 -> the previous kernel (PDL);
   // else the previous phase (or the LayerNorm that follows it) on every CTA
@@ -732,6 +747,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
       wait_counter(ca.ph[pq].ln_after >= 0 ? &ln_done[pq] : &done[pq], G * ca.epoch);
     }
     fence_proxy_async_global();   // generic-proxy writes of other CTAs -> this CTA's TMA reads
+    chain_mark(1 + q);
   };
 
   ChainIter it;
@@ -783,6 +799,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
         }
       }
       flush(true);
+      chain_mark(13);
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -824,6 +841,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
       __threadfence();
       epi_bar();
       if (et == 0) red_release_add(&done[q], 1u);
+      if (et == 0) chain_mark(5 + q);
       const int li = ca.ph[q].ln_after;
       if (li < 0) {
         // every counter advances by one per CTA per launch (targets grid x epoch)
@@ -895,6 +913,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
       __threadfence();
       epi_bar();
       if (et == 0) red_release_add(&ln_done[q], 1u);
+      if (et == 0) chain_mark(9 + q);
     };
     while (it.next(u, &ph)) {
       while (cur < ph) {   // phases before this unit's are complete on this CTA
@@ -971,6 +990,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
       if (cur >= 0) finish_phase(cur);
       ++cur;
     }
+    if (et == 0) chain_mark(14);
     // counters of the phases this launch does not have
     if (et == 0)
       for (int q = ca.n; q < CHAIN_MAX; ++q) {
@@ -1562,6 +1582,11 @@ void decode_chain(const ChainSpec& c, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
+extern "C" int exg_diag_chain_timeline(int on, unsigned long long* out) {
+  if (on >= 0) cudaMemcpyToSymbol(exg::g_chain_tl_on, &on, sizeof(int));
+  if (out) return cudaMemcpyFromSymbol(out, exg::g_chain_tl, sizeof(unsigned long long) * 256 * 16) == cudaSuccess ? 0 : 1;
+  return 0;
+}
 // decode GEMM chain for engines created after the call (1 = on, default; 0 = separate launches)
 extern "C" void exg_diag_chain(int on) { exg::chain_enabled() = on != 0; }
 // deferred stream-K reductions for engines created after the call: bit 0 =
