@@ -680,13 +680,13 @@ struct ChainIter {
 // last chain launch -- [0] entry, [1+q] producer: inputs of phase q ready,
 // [5+q] epilogue: phase q finished on this CTA, [9+q] LayerNorm after q done,
 // [13] producer: last load issued, [14] epilogue exit
-__device__ unsigned long long g_chain_tl[256 * 16];
+__device__ unsigned long long g_chain_tl[256 * 32];
 __device__ int g_chain_tl_on;
 __device__ __forceinline__ void chain_mark(int k) {
   if (g_chain_tl_on) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    if (blockIdx.x < 256) g_chain_tl[blockIdx.x * 16 + k] = t;
+    if (blockIdx.x < 256) g_chain_tl[blockIdx.x * 32 + k] = t;
   }
 }
 
@@ -805,6 +805,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_bf16(BM, BN);
       uint32_t g = 0, ui = 0;
+      int last_ph = -1;
       while (it.next(u, &ph)) {
         const uint32_t a2 = ui & 1;
         if (ui >= 2) mbar_wait(&tempty[a2], ((ui >> 1) & 1) ^ 1);
@@ -814,6 +815,11 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
           const uint32_t s = g % STAGES;
           mbar_wait(&full[s], (g / STAGES) & 1);
           tc_fence_after();
+          if (ph != last_ph) {
+            if (last_ph >= 0) chain_mark(20 + last_ph);
+            chain_mark(16 + ph);
+            last_ph = ph;
+          }
           const uint32_t a_base = smem_u32(sA + s * A_BYTES);
           const uint32_t b_base = smem_u32(sB + s * B_BYTES);
 #pragma unroll
@@ -825,6 +831,7 @@ __global__ void __launch_bounds__(EpiCfg<1>::THREADS, 1)
         umma_commit(&tfull[a2]);
         ++ui;
       }
+      if (last_ph >= 0) chain_mark(20 + last_ph);
     }
   } else if (warp >= 4) {
     const int q4 = warp & 3;
@@ -1424,8 +1431,13 @@ CUtensorMap make_tmap_bf16(const void* base, int64_t rows, int64_t cols, int64_t
   return m;
 }
 
+// off by default: measured on OPT-13B task S (tools/ab_deferred.py, mode 10)
+// the chain is slower than PDL-chained separate launches (decode phase 3.65 vs
+// 2.99 s): a one-phase chain launch is ~7 us slower than exg_op_linear and a
+// phase boundary costs as much as a kernel boundary (the fixup tail and the
+// grid-wide readiness wait are still serial); kept as an option
 bool& chain_enabled() {
-  static bool on = true;
+  static bool on = false;
   return on;
 }
 
@@ -1582,12 +1594,43 @@ void decode_chain(const ChainSpec& c, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_gemm_flags(int flags) { exg::gemm_debug_flags() = flags; }
+// one-phase chain (EPI_BF16, no bias) for A/B against exg_op_linear
+extern "C" int exg_diag_chain_gemm(const void* X, int64_t ldx, const void* Wb, int tokens, int features, int K,
+                                   void* out, int64_t ldo, float* ws, int64_t ws_floats, unsigned* sync,
+                                   unsigned epoch, int n_rep, void* stream) {
+  try {
+    exg::ChainSpec c;
+    c.n = std::max(1, std::min(4, n_rep));
+    for (int q = 0; q < c.n; ++q) {
+      c.ph[q].X = (const exg::bf16*)X;
+      c.ph[q].ldx = ldx;
+      c.ph[q].Wb = (const exg::bf16*)Wb;
+      c.ph[q].features = features;
+      c.ph[q].K = K;
+      c.ph[q].ep.mode = exg::EPI_BF16;
+      c.ph[q].ep.out_bf16 = (exg::bf16*)out;
+      c.ph[q].ep.ldo = ldo;
+    }
+    c.tokens = tokens;
+    c.d = 4;
+    c.ws = ws;
+    c.ws_floats = (size_t)ws_floats;
+    c.sync = sync;
+    c.epoch = epoch;
+    if (!ws) return (int)exg::chain_ws_floats(c);
+    exg::decode_chain(c, (cudaStream_t)stream);
+    return 0;
+  } catch (...) {
+    return -1;
+  }
+}
+
 extern "C" int exg_diag_chain_timeline(int on, unsigned long long* out) {
   if (on >= 0) cudaMemcpyToSymbol(exg::g_chain_tl_on, &on, sizeof(int));
-  if (out) return cudaMemcpyFromSymbol(out, exg::g_chain_tl, sizeof(unsigned long long) * 256 * 16) == cudaSuccess ? 0 : 1;
+  if (out) return cudaMemcpyFromSymbol(out, exg::g_chain_tl, sizeof(unsigned long long) * 256 * 32) == cudaSuccess ? 0 : 1;
   return 0;
 }
-// decode GEMM chain for engines created after the call (1 = on, default; 0 = separate launches)
+// decode GEMM chain for engines created after the call (1 = on; 0 = separate launches, default)
 extern "C" void exg_diag_chain(int on) { exg::chain_enabled() = on != 0; }
 // deferred stream-K reductions for engines created after the call: bit 0 =
 // QKV (summed by the decode attention), bit 1 = O-projection / FFN2 (summed by

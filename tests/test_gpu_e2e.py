@@ -240,7 +240,6 @@ def test_deferred_stream_k_reduction_bit_identical(n_req, b_d):
             ctx.close()
         finally:
             X.lib().exg_diag_deferred(-1)
-    X.lib().exg_diag_chain(1)
     for o in outs[1:]:
         assert o[0] == outs[0][0]
         for r in range(len(reqs)):
@@ -270,7 +269,7 @@ def test_decode_chain_bit_identical(n_req, b_d, n_layers):
             outs.append(ctx.run(X.rra_schedule(min(n_req, b_d), b_d, 4), reqs, dump=range(len(reqs))))
             ctx.close()
         finally:
-            X.lib().exg_diag_chain(1)
+            X.lib().exg_diag_chain(0)
     for o in outs[1:]:
         assert o[0] == outs[0][0]
         for r in range(len(reqs)):

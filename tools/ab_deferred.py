@@ -25,7 +25,7 @@ for on in MODES:
     X.lib().exg_diag_deferred(on if on < 10 else -1)
     ctxs[on] = X.Context(spec, weight_seed(2))
 X.lib().exg_diag_deferred(-1)
-X.lib().exg_diag_chain(1)
+X.lib().exg_diag_chain(0)
 sched = X.rra_schedule(56, 83, 32)
 toks = {}
 for r in range(reps):

@@ -21,12 +21,14 @@ lib.exg_diag_chain_timeline.argtypes = [C.c_int, C.c_void_p]
 ctx.run(X.rra_schedule(B, B, 8), reqs)
 lib.exg_diag_chain_timeline(1, None)
 ctx.run(X.rra_schedule(B, B, 8), reqs)
-tl = np.zeros(256 * 16, dtype=np.uint64)
+tl = np.zeros(256 * 32, dtype=np.uint64)
 lib.exg_diag_chain_timeline(0, tl.ctypes.data)
-tl = tl.reshape(256, 16)[:148].astype(np.float64)
+tl = tl.reshape(256, 32)[:148].astype(np.float64)
 t0 = tl[:, 0].min()
 names = {0: "entry", 1: "in0", 2: "in1", 3: "in2", 4: "in3", 5: "fin0", 6: "fin1", 7: "fin2", 8: "fin3",
-         9: "ln0", 10: "ln1", 11: "ln2", 12: "ln3", 13: "prod_end", 14: "epi_exit"}
+         9: "ln0", 10: "ln1", 11: "ln2", 12: "ln3", 13: "prod_end", 14: "epi_exit",
+         16: "mma0_first", 17: "mma1_first", 18: "mma2_first", 19: "mma3_first",
+         20: "mma0_last", 21: "mma1_last", 22: "mma2_last", 23: "mma3_last"}
 for k, nm in names.items():
     v = tl[:, k]
     v = v[v > 0]
