@@ -440,36 +440,53 @@ def run_layout(args, rank, world, local):
     d = task_dists(args.multi_task)
     seed = weight_seed(MULTI_CONFIG_NO)
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist = None   # one-GPU dry run of this path (--layout plan without torchrun)
     free, total = torch.cuda.mem_get_info(local)
     mem, ws = total - (6 << 30), 8 << 30
     pin, pout = X.Pmf(d.pmf_in), X.Pmf(d.pmf_out)
-    box = [X.unique_id() if rank == 0 else None]
-    dist.broadcast_object_list(box, src=0)
-    ctx = X.Context(spec, seed, device=local, cluster=X.cluster_spec(world, mem, ws), rank=rank, world=world,
-                    uid=box[0])
-    tps = [t for t in (1, 2, 4, 8) if t <= world and spec.n_heads % t == 0]
-    comm_prof = ctx.profile([1], [1], [1], reps=5, tps=tps)           # collective
-    plan = [None]
+
+    def bcast(obj):
+        box = [obj]
+        if dist:
+            dist.broadcast_object_list(box, src=0)
+        return box[0]
+
+    uid = bcast(X.unique_id() if rank == 0 and world > 1 else None)
+    tps = [t for t in (1, 2, 4, 8) if t <= max(world, 1) and spec.n_heads % t == 0]
+    comm_prof = None
+    if world > 1:
+        ctx = X.Context(spec, seed, device=local, cluster=X.cluster_spec(world, mem, ws), rank=rank, world=world,
+                        uid=uid)
+        comm_prof = ctx.profile([1], [1], [1], reps=5, tps=tps)       # collective
+    plan = None
     if rank == 0:
         ctx1 = X.Context(spec, seed, device=local, cluster=X.cluster_spec(1, mem, ws))
         prof = ctx1.profile(PROFILE_BATCH, PROFILE_CTX, PROFILE_TOKENS, reps=3, tps=tps)
-        prof.copy_comm(comm_prof)
+        if comm_prof is not None:
+            prof.copy_comm(comm_prof)
+        else:
+            prof.comm_model(COMM_ALPHA_S, COMM_BW)
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         prof.save(os.path.join(ROOT, "gpurun_out", "profile_multi.txt"))
-        plan[0] = multi_plans(X, prof, ctx1.mspec, X.cluster_spec(world, mem, ws), pin, pout, d.target_len,
-                              args.margin, args.little)
-        ctx1.close()
-        del ctx1
-        torch.cuda.empty_cache()
-    dist.broadcast_object_list(plan, src=0)
-    plan = plan[0]
+        plan = multi_plans(X, prof, ctx1.mspec, X.cluster_spec(max(world, 1), mem, ws), pin, pout, d.target_len,
+                           args.margin, args.little)
+        if world > 1:
+            ctx1.close()
+            del ctx1
+            torch.cuda.empty_cache()
+        else:
+            ctx = ctx1
+    plan = bcast(plan)
     if "sched" not in plan["pick"]:
         if rank == 0:
             print(json.dumps({"metric": METRIC, "value": None, "n_gpus": world, "unavailable":
                               "no schedule meets the bound: " + plan["pick"].get("infeasible", "")}))
         ctx.close()
-        dist.destroy_process_group()
+        if dist:
+            dist.destroy_process_group()
         return
     s = exg_schedule.from_buffer_copy(plan["pick"]["sched"])
     L_b = plan["latency_bound_s"]
@@ -477,10 +494,14 @@ def run_layout(args, rank, world, local):
     slot_ctx = len(d.pmf_in) + len(d.pmf_out)
     h2d = sum((r.input_len - 1) * 12 + 16 + 16 * r.output_len for r in reqs)
     d2h = sum(4 * r.output_len for r in reqs)
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+
     for _ in range(args.warmup):
         ctx.run(s, reqs, slot_ctx=slot_ctx)
-    torch.cuda.synchronize()
-    dist.barrier()
+    barrier()
     wall, toks, lat = 0.0, 0, None
     th0 = time.perf_counter()
     with Clocks(local) as clk:
@@ -488,13 +509,12 @@ def run_layout(args, rank, world, local):
             _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx)
             wall += st["wall_s"]     # rank 0: stamps of every rank on one clock
             toks += st["out_tokens"]
-        torch.cuda.synchronize()
-        dist.barrier()
+        barrier()
         host = time.perf_counter() - th0
     wall = reduce_over_ranks(wall, "max", dist)
     host = reduce_over_ranks(host, "max", dist)
     forced = None
-    if "sched" in plan["waa_tp2"]:
+    if "sched" in plan["waa_tp2"] and world > 1:
         sw = exg_schedule.from_buffer_copy(plan["waa_tp2"]["sched"])
         _, lat_w, st_w, _ = ctx.run(sw, reqs, slot_ctx=slot_ctx)
         forced = {"schedule": plan["waa_tp2"]["schedule"], "predicted_tok_s": plan["waa_tp2"]["predicted_tok_s"],
@@ -518,9 +538,11 @@ def run_layout(args, rank, world, local):
             "sla": {"sla_b_met": bool(max(upto) < L_b), "sla_a_met": bool(np.percentile(lat, 99) <= L_b),
                     "max_latency_upto_p99_len_s": float(max(upto)), "p99_latency_s": float(np.percentile(lat, 99))},
             "forced_waa_tp2": forced, "clocks": clk.summary(),
-            "comm": "measured: XProfiler tp_sync / pp_sync on this job's NCCL communicators"}))
+            "comm": ("measured: XProfiler tp_sync / pp_sync on this job's NCCL communicators" if world > 1 else
+                     "one-GPU dry run: alpha-beta interconnect model")}))
     ctx.close()
-    dist.destroy_process_group()
+    if dist:
+        dist.destroy_process_group()
 
 
 def run_reference(args, rank, world):
@@ -567,6 +589,8 @@ def main():
     ap.add_argument("--layout", default="plan", choices=["replicas", "plan"],
                     help="N > 1: config 4 under the scheduler's N-GPU plan as one NCCL job (default), or "
                          "independent config-2 replicas")
+    ap.add_argument("--plan-dry-run", action="store_true",
+                    help="run the N > 1 (config 4) path on one GPU (testing; no collective)")
     ap.add_argument("--multi-model", default=MULTI_MODEL)
     ap.add_argument("--multi-task", default=MULTI_TASK)
     ap.add_argument("--plan-gpus", type=lambda v: [int(x) for x in v.split(",") if x], default=[2, 4, 8],
@@ -584,7 +608,7 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
-    if args.layout == "plan" and world > 1:
+    if args.layout == "plan" and (world > 1 or args.plan_dry_run):
         run_layout(args, rank, world, local)
         return
 
