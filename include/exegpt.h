@@ -28,7 +28,7 @@
 extern "C" {
 #endif
 
-#define EXG_ABI_VERSION 4
+#define EXG_ABI_VERSION 5
 
 typedef enum {
   EXG_OK = 0,
@@ -61,11 +61,16 @@ typedef struct {
 } exg_model_spec;
 
 /* Cluster: GPUs used and usable bytes per GPU (memory check);
- * workspace_bytes is reserved per GPU for activations / scratch. */
+ * workspace_bytes is reserved per GPU for activations / scratch.  kv_page > 0:
+ * the runner pages the decoder KV cache (exg_run_opts.kv_page) and the
+ * simulator charges each decoder row the row-iteration average of its live
+ * positions, S_E - 1 + E[S(S+1)] / (2 E[S]) + 3 kv_page / 2, instead of
+ * max_in + max_out (decoder-only models; reading of PAPER.md:545). */
 typedef struct {
   int32_t n_gpus;
   int64_t mem_per_gpu_bytes;
   int64_t workspace_bytes;
+  int32_t kv_page;
 } exg_cluster_spec;
 
 /* A length distribution P(len = k) = prob[k-1], k = 1..max_len. */
@@ -154,6 +159,22 @@ typedef struct {
    * exg_run_stats.trace_records). */
   double* trace_out;
   int32_t trace_cap;
+  /* Paged KV cache ("the addition of
+   * vLLM's paging mechanism can further enhance WAA's performance"):
+   * kv_page > 0 stores K/V in pages of kv_page positions (a multiple of 64
+   * dividing 512) allocated as a row grows, instead of one slot of slot_ctx
+   * positions per row; kv_pages = pages in the pool (0: B_D x
+   * ceil(slot_ctx / kv_page), the slots' memory).  A row gets the pages of
+   * its encoded positions at admission and one more each time its next
+   * position crosses a page boundary; admission keeps one free page per
+   * active row in reserve.  When a row needs a page and none is free, the
+   * most recently admitted active row is preempted: its pages are freed and
+   * it is re-admitted (before any new request) with its generated tokens
+   * appended to its input, re-encoded, and continues (vLLM's recompute
+   * preemption).  Decoder-only bf16 models, RRA on one GPU; other scopes
+   * return EXG_E_INPUT.  0 = slots. */
+  int32_t kv_page;
+  int32_t kv_pages;
 } exg_run_opts;
 
 /* Kernel classes timed when exg_run_opts.kernel_timing = 1.  Work is the
@@ -185,6 +206,8 @@ typedef struct {
   double enc_stage_mean_s, enc_stage_p99dev_s, dec_stage_mean_s, dec_stage_p99dev_s;
   double mean_encode_batch;            /* requests per encode phase (admissions)  */
   int64_t trace_records;               /* records written to exg_run_opts.trace_out */
+  int64_t kv_preemptions;              /* paged KV: rows preempted (recomputed)    */
+  int64_t kv_pages_peak;               /* paged KV: most pages in use at once      */
 } exg_run_stats;
 
 typedef struct exg_ctx exg_ctx;           /* one per rank: device state + comms */

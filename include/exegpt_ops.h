@@ -101,6 +101,29 @@ exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, 
                                     int32_t n_slots, int32_t T, float scale, int32_t causal, const float* bias,
                                     int32_t bias_ld, int32_t bias_off, void* stream);
 
+/* Paged KV variants of K6 / K4: the
+ * cache is [n_pages][H][max_ctx][dh] with max_ctx = the page length P (a
+ * multiple of 64; for K6 it divides split_len), and key k of row i (K6: decode
+ * row; K4: request r) lives in page page_table[i*maxp + k/P] at offset k mod
+ * P.  page_table: device int32 [rows][maxp], caller-owned; every entry a row's
+ * keys reach must name a page of the cache (K4 reads whole 64-key halves of
+ * its 128-key tiles up to the row's last key).  slot[] is still read (K6:
+ * unused for addressing; K4: unused for addressing).  Same arithmetic as the
+ * slot variants: identical results for identical key values.  EXG_E_INPUT on
+ * a null page_table, maxp < 1 or a page length that is not a multiple of 64. */
+exg_status exg_op_decode_attention_paged(const void* q, int64_t ldq, const void* kc, const void* vc,
+                                         const int32_t* slot, const int32_t* n_keys, void* out, int64_t ldo,
+                                         int32_t B, int32_t H, int32_t dh, int32_t max_ctx, float scale,
+                                         int32_t split_len, int32_t max_splits, float* partial, const float* bias,
+                                         int32_t bias_ld, int32_t bias_off, const int32_t* page_table, int32_t maxp,
+                                         void* stream);
+exg_status exg_op_prefill_attention_paged(const void* q, int64_t ldq, const void* kc, const void* vc,
+                                          const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0,
+                                          int32_t R, int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh,
+                                          int32_t max_ctx, int32_t n_slots, int32_t T, float scale, int32_t causal,
+                                          const float* bias, int32_t bias_ld, int32_t bias_off,
+                                          const int32_t* page_table, int32_t maxp, void* stream);
+
 /* K8 -- out[i] = argmax_v logits[i][v] (fp32 [B][ld]), lowest index on ties;
  * *err_flag (device int32, may be NULL) set to 1 on a NaN. */
 exg_status exg_op_argmax(int32_t* out, const float* logits, int64_t ld, int32_t B, int32_t V, int32_t* err_flag,

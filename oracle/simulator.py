@@ -219,6 +219,7 @@ class SimCluster:
     n_gpus: int
     mem_per_gpu_bytes: float
     workspace_bytes: float = 0.0
+    kv_page: int = 0     # > 0: paged KV of this page length (decoder-only; NEXT-2)
 
 
 RRA, WAA_C, WAA_M, STATIC = 1, 2, 4, 8
@@ -331,6 +332,24 @@ class Simulator:
         self.s_e_sd = math.sqrt(var if var > 0.0 else 0.0)
         self.use_little = use_little_fraction
         self.n_layers = model.n_dec_layers                   # decoder-only: every layer runs both phases
+        # decoder KV context per row: slots hold Max_in + Max_out positions
+        # (S13); with paged KV (SimCluster.kv_page = P, decoder-only) a row
+        # holds only its live positions, and the memory model charges the
+        # row-iteration average of those (DESIGN.md reading):
+        # a request with input n and output S holds n - 1 + u keys at its
+        # decode iteration u = 1..S, so over its S iterations the mean is
+        # n - 1 + (S + 1)/2; weighting requests by their S iterations
+        # (renewal-reward) gives S_E - 1 + E[S(S+1)] / (2 E[S]), plus 3P/2:
+        # half a page of rounding on average and the one-page-per-row reserve
+        # the runner keeps at admission.  Fluctuations above the mean are
+        # absorbed by the runner's preemption.
+        self.kv_ctx_dec = float(self.max_in + self.max_out)
+        if cluster.kv_page > 0 and model.arch != "t5":
+            m2o = 0.0
+            for k in range(1, len(self.pmf_out) + 1):
+                m2o += float(k) * float(k) * float(self.pmf_out[k - 1])
+            live = self.s_e - 1.0 + (m2o + self.s_d) / (2.0 * self.s_d)
+            self.kv_ctx_dec = min(live + 1.5 * float(cluster.kv_page), float(self.max_in + self.max_out))
         self.k_dec = 3 if model.arch == "t5" else 2
         self._pu_cache: Dict[int, Tuple[List[float], float]] = {}
 
@@ -417,10 +436,10 @@ class Simulator:
         if s.strategy == STATIC:
             account(stage_layout(self.cl.n_gpus, 1, 0, self.n_layers), s.b_e, self.max_in + self.max_out)
         elif s.strategy == RRA:
-            account(s.stages, s.b_d, self.max_in + self.max_out)
+            account(s.stages, s.b_d, self.kv_ctx_dec)
         else:
             account([st for st in s.stages if st[0] < s.n_enc_gpus], s.b_e, self.max_in)
-            account([st for st in s.stages if st[0] >= s.n_enc_gpus], s.b_d, self.max_in + self.max_out)
+            account([st for st in s.stages if st[0] >= s.n_enc_gpus], s.b_d, self.kv_ctx_dec)
         return w, kv
 
     def mem_ok(self, stages, kv_rows: int, ctx: int) -> bool:
@@ -443,7 +462,7 @@ class Simulator:
         return Schedule(RRA, b_e, b_d, 0, n_d, t, c, 0, st)
 
     def simulate_rra(self, s: Schedule) -> Estimate:
-        if not self.mem_ok(s.stages, s.b_d, self.max_in + self.max_out):
+        if not self.mem_ok(s.stages, s.b_d, self.kv_ctx_dec):
             return Estimate(0.0, 0.0, INF, False)
         pu, f = self.pu(s.n_d)
         P = len(s.stages)
@@ -498,14 +517,15 @@ class Simulator:
         """Encoder GPUs out of N.  WAA-C (S7): proportional to the encoder /
         decoder compute per iteration.  WAA-M (reading): so the
         per-GPU memory of the two sides is equal -- M_E = weights + B_E max_in
-        KV rows, M_D = weights + B_D (max_in + max_out) KV rows, n_enc =
+        KV rows, M_D = weights + B_D kv_ctx_dec KV rows (max_in + max_out;
+        paged: the live average), n_enc =
         round(N M_E / (M_E + M_D))."""
         N = self.cl.n_gpus
         if strat == WAA_M:
             kv = self.kv_bytes_per_token_layer()
             W = self.n_layers * self.layer_bytes() + self.emb_bytes()
             M_E = W + (b_e * self.max_in * self.n_layers) * kv
-            M_D = W + (b_d * (self.max_in + self.max_out) * self.n_layers) * kv
+            M_D = W + (b_d * self.kv_ctx_dec * self.n_layers) * kv
             n_enc = int(math.floor(N * M_E / (M_E + M_D) + 0.5))
         else:
             C_E = self.n_layers * self.layer_enc(1, b_e)
@@ -533,7 +553,7 @@ class Simulator:
     def simulate_waa(self, s: Schedule) -> Estimate:
         enc = [st for st in s.stages if st[0] < s.n_enc_gpus]
         dec = [st for st in s.stages if st[0] >= s.n_enc_gpus]
-        if not (self.mem_ok(enc, s.b_e, self.max_in) and self.mem_ok(dec, s.b_d, self.max_in + self.max_out)):
+        if not (self.mem_ok(enc, s.b_e, self.max_in) and self.mem_ok(dec, s.b_d, self.kv_ctx_dec)):
             return Estimate(0.0, 0.0, INF, False)
         M = -(-s.b_d // s.b_m)
         try:

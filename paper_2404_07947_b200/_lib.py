@@ -39,7 +39,8 @@ class exg_model_spec(C.Structure):
 
 
 class exg_cluster_spec(C.Structure):
-    _fields_ = [("n_gpus", C.c_int32), ("mem_per_gpu_bytes", C.c_int64), ("workspace_bytes", C.c_int64)]
+    _fields_ = [("n_gpus", C.c_int32), ("mem_per_gpu_bytes", C.c_int64), ("workspace_bytes", C.c_int64),
+                ("kv_page", C.c_int32)]
 
 
 class exg_pmf(C.Structure):
@@ -88,7 +89,8 @@ class exg_request(C.Structure):
 class exg_run_opts(C.Structure):
     _fields_ = [("logits_out", C.POINTER(C.c_float)), ("dump_mask", C.POINTER(C.c_uint8)),
                 ("slot_ctx", C.c_int32), ("pin_nccl_algo", C.c_int32), ("kernel_timing", C.c_int32),
-                ("dyn_threshold", C.c_double), ("trace_out", C.POINTER(C.c_double)), ("trace_cap", C.c_int32)]
+                ("dyn_threshold", C.c_double), ("trace_out", C.POINTER(C.c_double)), ("trace_cap", C.c_int32),
+                ("kv_page", C.c_int32), ("kv_pages", C.c_int32)]
 
 
 K_CLASSES = ["prefill_gemm", "decode_gemm", "decode_attn", "prefill_attn"]
@@ -103,7 +105,8 @@ class exg_run_stats(C.Structure):
                 ("k_work", C.c_double * 4), ("k_launches", C.c_int64 * 4),
                 ("enc_stage_mean_s", C.c_double), ("enc_stage_p99dev_s", C.c_double),
                 ("dec_stage_mean_s", C.c_double), ("dec_stage_p99dev_s", C.c_double),
-                ("mean_encode_batch", C.c_double), ("trace_records", C.c_int64)]
+                ("mean_encode_batch", C.c_double), ("trace_records", C.c_int64),
+                ("kv_preemptions", C.c_int64), ("kv_pages_peak", C.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("k_")}
@@ -161,12 +164,19 @@ _SIGS = {
     "exg_op_prefill_attention": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, C.c_int32, _P,
                                            C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
                                            C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, _P]),
+    "exg_op_decode_attention_paged": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int64, C.c_int32,
+                                                C.c_int32, C.c_int32, C.c_int32, C.c_float, C.c_int32,
+                                                C.c_int32, _P, _P, C.c_int32, C.c_int32, _P, C.c_int32, _P]),
+    "exg_op_prefill_attention_paged": (C.c_int, [_P, C.c_int64, _P, _P, _P, _P, _P, C.c_int32, C.c_int32, _P,
+                                                 C.c_int64, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.c_int32, C.c_float, C.c_int32, _P, C.c_int32, C.c_int32, _P,
+                                                 C.c_int32, _P]),
     "exg_op_argmax": (C.c_int, [_P, _P, C.c_int64, C.c_int32, C.c_int32, _P, _P]),
     "exg_op_decode_workspace": (C.c_int64, [C.c_int32, C.c_int32, C.c_int32]),
 }
 
 _lib = None
-ABI_VERSION = 4   # include/exegpt.h EXG_ABI_VERSION
+ABI_VERSION = 5   # include/exegpt.h EXG_ABI_VERSION
 
 
 def lib():
@@ -203,8 +213,9 @@ def model_spec(spec, seed: int, dtype: int = EXG_BF16) -> exg_model_spec:
                           spec.d_head, spec.d_ff, spec.vocab, spec.max_pos, dtype, seed)
 
 
-def cluster_spec(n_gpus: int = 1, mem_per_gpu: float = 180e9, workspace: float = 6e9) -> exg_cluster_spec:
-    return exg_cluster_spec(n_gpus, int(mem_per_gpu), int(workspace))
+def cluster_spec(n_gpus: int = 1, mem_per_gpu: float = 180e9, workspace: float = 6e9,
+                 kv_page: int = 0) -> exg_cluster_spec:
+    return exg_cluster_spec(n_gpus, int(mem_per_gpu), int(workspace), int(kv_page))
 
 
 class Pmf:
@@ -268,7 +279,7 @@ class Context:
 
     def run(self, sched: exg_schedule, requests, dump: Optional[Sequence[int]] = None, slot_ctx: int = 0,
             kernel_timing: bool = False, dyn_threshold: float = 0.0, trace: Optional[list] = None,
-            pin_nccl_algo: bool = False):
+            pin_nccl_algo: bool = False, kv_page: int = 0, kv_pages: int = 0):
         """Returns (tokens per request, latencies [s], stats dict, logits per
         dumped request [S_r][V] or None).  trace: a list that receives the
         per-stage records [kind, start, duration, rows, work] (exegpt.h)."""
@@ -284,6 +295,8 @@ class Context:
         lat = np.zeros(n, dtype=np.float64)
         stats = exg_run_stats()
         opts = exg_run_opts(None, None, slot_ctx, int(pin_nccl_algo), int(kernel_timing), float(dyn_threshold))
+        opts.kv_page = int(kv_page)
+        opts.kv_pages = int(kv_pages)
         tbuf = None
         if trace is not None:
             cap = 8 * (n + 16) + 4 * total

@@ -117,6 +117,7 @@ struct FmhaParams {
   int causal;
   const float* bias;    // T5 relative bias: score += bias[h * bias_ld + bias_off + kpos - qpos]
   int bias_ld, bias_off;
+  KvMap kv;             // paged mode: page table of the requests
 };
 
 // Work item `id` -> (request, head, query tile); false if the tile is past
@@ -124,8 +125,7 @@ struct FmhaParams {
 // cost of a tile grows with its index), so the grid stride deals the
 // expensive items out first.
 struct Item {
-  int r, h, qb, t0, len, pos0, ntiles;
-  int64_t kv_row0;
+  int r, h, qb, t0, len, pos0, ntiles, slot, last_key;
 };
 __device__ __forceinline__ bool item_of(const FmhaParams& p, int id, Item& it) {
   const int rh = p.R * p.H;
@@ -140,7 +140,8 @@ __device__ __forceinline__ bool item_of(const FmhaParams& p, int id, Item& it) {
   it.pos0 = p.pos0[it.r];
   const int last_key = p.causal ? it.pos0 + min(it.len, it.qb + FQ) - 1 : it.pos0 + it.len - 1;  // inclusive
   it.ntiles = last_key / FK + 1;
-  it.kv_row0 = ((int64_t)p.slot[it.r] * p.H + it.h) * p.max_ctx;
+  it.last_key = last_key;
+  it.slot = p.slot[it.r];
   return true;
 }
 
@@ -211,11 +212,21 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
           const int s = g & 1;
           if (g >= KV_STAGES) mbar_wait(&kv_empty[s], ((g >> 1) & 1) ^ 1);
           mbar_arrive_expect_tx(&kv_full[s], 2 * KV_BYTES);
-          const int row = (int)(it.kv_row0 + j * FK);
-          tma_load_2d(sK + s * KV_BYTES, &tmK, &kv_full[s], 0, row);
-          tma_load_2d(sK + s * KV_BYTES + TILE_BYTES, &tmK, &kv_full[s], 64, row);
-          tma_load_2d(sV + s * KV_BYTES, &tmV, &kv_full[s], 0, row);
-          tma_load_2d(sV + s * KV_BYTES + TILE_BYTES, &tmV, &kv_full[s], 64, row);
+          // two 64-key halves (each inside one KV block: 64 | page length);
+          // a half entirely past the item's last key is loaded from the
+          // first half's rows (masked, finite)
+          const int row0 = (int)kv_row(p.kv, it.r, it.slot, p.H, it.h, p.max_ctx, j * FK);
+          const int k1 = j * FK + 64;
+          const int row1 = k1 <= it.last_key ? (int)kv_row(p.kv, it.r, it.slot, p.H, it.h, p.max_ctx, k1) : row0;
+#pragma unroll
+          for (int hf = 0; hf < 2; ++hf) {
+            const int row = hf ? row1 : row0;
+            const uint32_t o = hf * (TILE_BYTES / 2);
+            tma_load_2d(sK + s * KV_BYTES + o, &tmK, &kv_full[s], 0, row);
+            tma_load_2d(sK + s * KV_BYTES + TILE_BYTES + o, &tmK, &kv_full[s], 64, row);
+            tma_load_2d(sV + s * KV_BYTES + o, &tmV, &kv_full[s], 0, row);
+            tma_load_2d(sV + s * KV_BYTES + TILE_BYTES + o, &tmV, &kv_full[s], 64, row);
+          }
         }
       }
     }
@@ -460,12 +471,13 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   // [kv_rows = slots*H*max_ctx][dh]
   const int QT = (a.max_len + FQ - 1) / FQ;
   FmhaParams p{a.cu_seqlens, a.slot, a.pos0, a.H, a.max_ctx, a.R, QT,
-               a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo, a.causal, a.bias, a.bias_ld, a.bias_off};
+               a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo, a.causal, a.bias, a.bias_ld, a.bias_off, a.kv};
   const int n_items = QT * a.R * a.H;
   if (n_items <= 0) return true;
   const CUtensorMap tq = make_tmap_bf16(a.q, a.q_rows, a.ldq, a.ldq, 128);
-  const CUtensorMap tk = make_tmap_bf16(a.kc, a.kv_rows, FD, FD, 128);
-  const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 128);
+  // K / V boxes of 64 keys: a 128-key tile is two boxes per 64-column half
+  const CUtensorMap tk = make_tmap_bf16(a.kc, a.kv_rows, FD, FD, 64);
+  const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 64);
   // persistent grid: one CTA per SM (227 KB of shared memory, 512 TMEM columns)
   const int grid = std::min(n_items, sm_count());
   launch_pdl(fmha_prefill_kernel, dim3(grid), dim3(128 + 32 * SM_WARPS), FMHA_SMEM, st, tq, tk, tv, p);

@@ -597,6 +597,57 @@ exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, 
   });
 }
 
+exg_status exg_op_decode_attention_paged(const void* q, int64_t ldq, const void* kc, const void* vc, const int32_t* slot,
+                                   const int32_t* n_keys, void* out, int64_t ldo, int32_t B, int32_t H, int32_t dh,
+                                   int32_t max_ctx, float scale, int32_t split_len, int32_t max_splits, float* partial,
+                                   const float* bias, int32_t bias_ld, int32_t bias_off,
+                                         const int32_t* page_table, int32_t maxp, void* stream) {
+  return guarded([&] {
+    if (max_splits > 1 && !partial) throw std::invalid_argument("max_splits > 1 needs a partial buffer");
+    exg::DecodeAttnArgs a;
+    a.q = (const exg::bf16*)q;
+    a.ldq = ldq;
+    a.kc = (const exg::bf16*)kc;
+    a.vc = (const exg::bf16*)vc;
+    a.slot = slot;
+    a.n_keys = n_keys;
+    a.out = (exg::bf16*)out;
+    a.ldo = ldo;
+    a.B = B;
+    a.H = H;
+    a.dh = dh;
+    a.max_ctx = max_ctx;
+    a.scale = scale;
+    a.split_len = split_len;
+    a.max_splits = max_splits;
+    a.partial = partial;
+    a.bias = bias;
+    a.bias_ld = bias_ld;
+    a.bias_off = bias_off;
+    if (!page_table || maxp < 1) throw std::invalid_argument("paged: page_table / maxp");
+    a.kv = exg::KvMap{page_table, maxp};
+    exg::decode_attention(a, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
+exg_status exg_op_prefill_attention_paged(const void* q, int64_t ldq, const void* kc, const void* vc,
+                                    const int32_t* cu_seqlens, const int32_t* slot, const int32_t* pos0, int32_t R,
+                                    int32_t max_len, void* out, int64_t ldo, int32_t H, int32_t dh, int32_t max_ctx,
+                                    int32_t n_slots, int32_t T, float scale, int32_t causal, const float* bias,
+                                    int32_t bias_ld, int32_t bias_off, const int32_t* page_table, int32_t maxp,
+                                          void* stream) {
+  return guarded([&] {
+    exg::PrefillAttnArgs a{(const exg::bf16*)q, ldq, (const exg::bf16*)kc, (const exg::bf16*)vc, cu_seqlens, slot,
+                           pos0, R, max_len, (exg::bf16*)out, ldo, H, dh, max_ctx, scale, (int64_t)T,
+                           (int64_t)n_slots * H * max_ctx, causal, bias, bias_ld, bias_off};
+    if (!page_table || maxp < 1) throw std::invalid_argument("paged: page_table / maxp");
+    a.kv = exg::KvMap{page_table, maxp};
+    exg::prefill_attention(a, (cudaStream_t)stream);
+    return EXG_OK;
+  });
+}
+
 exg_status exg_op_argmax(int32_t* out, const float* logits, int64_t ld, int32_t B, int32_t V, int32_t* err_flag,
                          void* stream) {
   return guarded([&] {

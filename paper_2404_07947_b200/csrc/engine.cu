@@ -628,8 +628,8 @@ void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest, in
     EpiParams e = epi_bf16(w.bqkv, qkv_, 3 * il);
     e.kv_k = kc(l);
     e.kv_v = vc(l);
-    e.kv_slot = eb.tslot;
-    e.kv_pos = eb.pos;
+    e.kv_slot = eb.kv_blk ? eb.kv_blk : eb.tslot;
+    e.kv_pos = eb.kv_blk ? eb.kv_off : eb.pos;
     e.kv_inner = il;
     e.kv_H = D.Hl;
     e.kv_dh = D.dh;
@@ -638,13 +638,15 @@ void Engine::layer_encode(int l, const EncodeBatch& eb, bool attn, bool rest, in
       linear_pre(h_, d, T, w.Wqkv, 3 * il, d, e);
     } else {
       linear_pre(h_, d, T, w.Wqkv, 3 * il, d, epi_bf16(w.bqkv, qkv_, 3 * il));
-      kv_scatter(kc(l), vc(l), qkv_, eb.tslot, eb.pos, T, D.Hl, D.dh, slot_ctx_, st_);
+      kv_scatter(kc(l), vc(l), qkv_, eb.kv_blk ? eb.kv_blk : eb.tslot, eb.kv_blk ? eb.kv_off : eb.pos, T, D.Hl,
+                 D.dh, slot_ctx_, st_);
     }
   }
   if (attn) {
     PrefillAttnArgs pa{qkv_, 3 * il, kc(l), vc(l), eb.cu, eb.rslot, eb.pos0, eb.R, eb.max_len,
                        ctx_, il, D.Hl, D.dh, slot_ctx_, scale,
                        (int64_t)eb.T, (int64_t)kv_slots_ * D.Hl * slot_ctx_};
+    pa.kv = eb.kv;
     const int k = kbegin();
     prefill_attention(pa, st_);
     kend(k, EXG_K_PREFILL_ATTN, 4.0 * D.Hl * D.dh * eb.attn_pairs);
@@ -735,6 +737,7 @@ void Engine::layer_decode(int l, const DecodeBatch& db, bool attn, bool rest, in
     da.H = D.Hl;
     da.dh = D.dh;
     da.max_ctx = slot_ctx_;
+    da.kv = db.kv;
     da.scale = scale;
     const int sl = split_len();
     da.split_len = sl;
@@ -845,6 +848,7 @@ void Engine::dec_attention(int l, const DecodeBatch& db) {
   da.H = D.Hl;
   da.dh = D.dh;
   da.max_ctx = slot_ctx_;
+  da.kv = db.kv;
   da.scale = (float)(1.0 / std::sqrt((double)D.dh));
   const int sl = split_len();
   da.split_len = sl;
@@ -942,11 +946,13 @@ void Engine::layer_f32(int l, int rows, const int32_t* slot, const int32_t* pos)
 }
 
 void Engine::encode_f32(const EncodeBatch& eb) {
+  if (eb.kv.ptab) throw std::invalid_argument("paged KV is not supported on the fp32 path");
   embed_encode(eb);
   for (int l = 0; l < n_layers(); ++l) layer_f32(l, eb.T, eb.tslot, eb.pos);
 }
 
 void Engine::decode_f32(const DecodeBatch& db) {
+  if (db.kv.ptab) throw std::invalid_argument("paged KV is not supported on the fp32 path");
   embed_decode(db);
   for (int l = 0; l < n_layers(); ++l) layer_f32(l, db.B, db.slot, db.pos);
   layernorm_f32(hf_, D.d, x_, D.d, lnf_g_, lnf_b_, db.B, D.d, 1e-5f, st_);
@@ -1022,8 +1028,10 @@ void Engine::cross_kv(int l, const EncodeBatch& eb) {
 }
 
 void Engine::dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, int ctx, const DecodeBatch& db,
-                   const int32_t* nkeys, int max_keys, double sum_keys, const float* bias, bool append) {
+                   const int32_t* nkeys, int max_keys, double sum_keys, const float* bias, bool append,
+                   KvMap kv) {
   DecodeAttnArgs da;
+  da.kv = kv;
   if (append) {   // fused KV append of the new token (K7): K / V follow q in the qkv buffer
     da.knew = q + D.inner_l;
     da.vnew = q + 2 * D.inner_l;
@@ -1064,7 +1072,8 @@ void Engine::dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest) {
     linear_dec(h_, d, B, w.Wqkv, 3 * il, d, epi_bf16(nullptr, qkv_, 3 * il));
   }
   // the self-attention appends the new token's K / V to the cache itself
-  if (attn) dattn(qkv_, 3 * il, kc(l), vc(l), slot_ctx_, db, db.nkeys, db.max_keys, db.sum_keys, dec_bias_, true);
+  if (attn)
+    dattn(qkv_, 3 * il, kc(l), vc(l), slot_ctx_, db, db.nkeys, db.max_keys, db.sum_keys, dec_bias_, true, db.kv);
   if (rest) {
     resid_update(true, ctx_, il, B, w.Wo, il, nullptr);
     rmsnorm(h_, d, x_, d, w.lnx_g, B, d, T5_EPS, 1.f, st_);

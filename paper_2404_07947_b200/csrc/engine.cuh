@@ -59,6 +59,11 @@ struct EncodeBatch {
   double attn_pairs = 0;   // sum_r n_r (n_r + 1) / 2   (prefill-attention work)
   const int32_t *ids = nullptr, *pos = nullptr, *tslot = nullptr;      // [T]
   const int32_t *cu = nullptr, *rslot = nullptr, *pos0 = nullptr;      // [R+1], [R], [R]
+  // paged KV (NEXT-2): token t's K / V go to page kv_blk[t] at offset
+  // kv_off[t] (= pos mod P) and request r's keys are found through kv.ptab
+  // row r; null / empty = slot mode (tslot, pos)
+  const int32_t *kv_blk = nullptr, *kv_off = nullptr;                  // [T]
+  KvMap kv;
 };
 
 // Decode batch: B active rows, device arrays.
@@ -71,6 +76,8 @@ struct DecodeBatch {
   const int32_t* xkeys = nullptr;
   int max_xkeys = 0;
   double sum_xkeys = 0;
+  // paged KV (NEXT-2): row i's self-attention keys through kv.ptab row i
+  KvMap kv;
 };
 
 class Engine {
@@ -91,6 +98,8 @@ class Engine {
   void ensure_workspace(int max_tokens, int max_rows);
   // decoder self-attention KV (slot_ctx keys per slot); encoder-decoder
   // models also get the cross K/V cache of every decoder layer (xctx keys)
+  // Paged mode: slots = pages, slot_ctx = the page length (the cache is
+  // [block][Hl][block_len][dh] either way; batches carry the page tables).
   void ensure_kv(int slots, int slot_ctx, int layers = -1, int xctx = 0);
   // T5-style encoder-decoder: encode = encoder over all
   // n input tokens + cross K/V projections (K13); decode starts from token 0
@@ -178,7 +187,8 @@ class Engine {
   void enc_layer_t5(int l, const EncodeBatch& eb, bool attn, bool rest);
   void dec_layer_t5(int l, const DecodeBatch& db, bool attn, bool rest);
   void dattn(const bf16* q, int64_t ldq, const bf16* kc, const bf16* vc, int ctx, const DecodeBatch& db,
-             const int32_t* nkeys, int max_keys, double sum_keys, const float* bias, bool append = false);
+             const int32_t* nkeys, int max_keys, double sum_keys, const float* bias, bool append = false,
+             KvMap kv = KvMap());
   void linear_dec(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   void linear_pre(const bf16* X, int64_t ldx, int tokens, const bf16* W, int features, int K, EpiParams ep);
   // residual update x += W.act + b: fused epilogue (tp = 1) or partial ->

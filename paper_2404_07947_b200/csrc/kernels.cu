@@ -440,9 +440,9 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
   const int n = min(nk - k_begin, a.split_len);
   const int ntiles = (n + C::KT - 1) / C::KT;
   const int nsplit = (nk + a.split_len - 1) / a.split_len;
-  const int64_t head_off = ((int64_t)a.slot[i] * a.H + h) * a.max_ctx + k_begin;
-  const bf16* kbase = a.kc + head_off * DH;
-  const bf16* vbase = a.vc + head_off * DH;
+  const int slot_i = a.slot[i];
+  // cache row of key k_begin + t*KT (tile t never crosses a page: KT | P | split_len)
+  auto tile_row = [&](int t) { return kv_row(a.kv, i, slot_i, a.H, h, a.max_ctx, k_begin + t * C::KT); };
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
   if (tid == 0) {
@@ -474,7 +474,8 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
     } else {
       new_chunk = *reinterpret_cast<const int4*>((which ? a.vnew : a.knew) + (int64_t)i * a.ldnew + h * DH + c * 8);
     }
-    bf16* dst = const_cast<bf16*>(which ? vbase : kbase) + (int64_t)r_new * DH + c * 8;
+    const int64_t row = kv_row(a.kv, i, slot_i, a.H, h, a.max_ctx, nk - 1);
+    bf16* dst = const_cast<bf16*>(which ? a.vc : a.kc) + row * DH + c * 8;
     *reinterpret_cast<int4*>(dst) = new_chunk;
   }
   __syncthreads();
@@ -483,9 +484,10 @@ __global__ void __launch_bounds__(128, MB) decode_attn_kernel(DecodeAttnArgs a) 
     const int s = t % C::STAGES;
     const int nkt = min(C::KT, n - t * C::KT);
     const uint32_t bytes = (uint32_t)nkt * C::ROWB;
+    const int64_t off = tile_row(t) * DH;
     mbar_arrive_expect_tx(&bar[s], 2 * bytes);
-    bulk_load(sk + s * C::KT * C::ROWB, kbase + (int64_t)t * C::KT * DH, bytes, &bar[s]);
-    bulk_load(sv + s * C::KT * C::ROWB, vbase + (int64_t)t * C::KT * DH, bytes, &bar[s]);
+    bulk_load(sk + s * C::KT * C::ROWB, a.kc + off, bytes, &bar[s]);
+    bulk_load(sv + s * C::KT * C::ROWB, a.vc + off, bytes, &bar[s]);
   };
   if (tid == 0)
     for (int t = 0; t < min(C::STAGES, ntiles); ++t) issue(t);
@@ -713,6 +715,8 @@ void decode_attention(const DecodeAttnArgs& a_in, cudaStream_t st) {
   if (a_in.B <= 0) return;
   DecodeAttnArgs a = a_in;
   if (decode_force_combine()) a.counters = nullptr;
+  if (a.kv.ptab && (a.max_ctx % 64 != 0 || a.split_len % a.max_ctx != 0))
+    throw CudaError("decode_attention: the page length must be a multiple of 64 dividing the split length");
   switch (a.dh) {
     case 16: decode_attention_t<16>(a, st); break;
     case 64: decode_attention_t<64>(a, st); break;
@@ -743,9 +747,7 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
   const bool qvalid = qidx < len;
   const int p0 = a.pos0[r];
   const int my_pos = p0 + qidx;
-  const int64_t head_off = ((int64_t)a.slot[r] * a.H + h) * a.max_ctx;
-  const bf16* kbase = a.kc + head_off * DH;
-  const bf16* vbase = a.vc + head_off * DH;
+  const int slot_r = a.slot[r];
 
   float q[DPL], o[DPL];
 #pragma unroll
@@ -759,12 +761,12 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
   for (int kt = 0; kt <= last_key; kt += KTILE) {
     const int nkt = min(KTILE, last_key + 1 - kt);
     __syncthreads();
+    // the 32-key tile lies inside one page (32 | P)
+    const int64_t toff = kv_row(a.kv, r, slot_r, a.H, h, a.max_ctx, kt) * DH;
     for (int e = tid; e < nkt * DH / 8; e += blockDim.x) {
       const int row = e / (DH / 8), c = e % (DH / 8);
-      *reinterpret_cast<int4*>(&ks[row][c * 8]) =
-          *reinterpret_cast<const int4*>(kbase + (int64_t)(kt + row) * DH + c * 8);
-      *reinterpret_cast<int4*>(&vs[row][c * 8]) =
-          *reinterpret_cast<const int4*>(vbase + (int64_t)(kt + row) * DH + c * 8);
+      *reinterpret_cast<int4*>(&ks[row][c * 8]) = *reinterpret_cast<const int4*>(a.kc + toff + (int64_t)row * DH + c * 8);
+      *reinterpret_cast<int4*>(&vs[row][c * 8]) = *reinterpret_cast<const int4*>(a.vc + toff + (int64_t)row * DH + c * 8);
     }
     __syncthreads();
     float sc[KTILE];
@@ -808,6 +810,7 @@ __global__ void __launch_bounds__(128) prefill_attn_kernel(PrefillAttnArgs a) {
 
 void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st) {
   if (a.R <= 0 || a.max_len <= 0) return;
+  if (a.kv.ptab && a.max_ctx % 64 != 0) throw CudaError("prefill_attention: the page length must be a multiple of 64");
   if (prefill_attention_tc(a, st)) return;
   dim3 grid((a.max_len + 31) / 32, a.H, a.R);
   switch (a.dh) {

@@ -50,9 +50,29 @@ void rmsnorm(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf16* g, i
 void rel_bias_table(float* tab, const bf16* rel, const int32_t* bucket, int n, int Hl, int H_total, int h0,
                     cudaStream_t st);
 
+// ---- KV blocks: slots or pages -----------------------------------------------
+// The cache of a layer is an array of blocks [block][H][max_ctx][dh] (K and V
+// separately).  Slot mode (ptab == nullptr): block = the row's slot, max_ctx
+// = the slot length, key k at offset k.  Paged mode (NEXT-2):
+// max_ctx = the page length P (a multiple of 64), the row's page table
+// ptab[row * maxp + j] holds the page of keys [jP, (j+1)P), key k at offset
+// k mod P.  Every tile the kernels stream (32 / 64 / 128 keys, aligned to
+// its size from key 0) lies inside one page.
+struct KvMap {
+  const int32_t* ptab = nullptr;   // [rows][maxp] (row = decode row / encode request)
+  int maxp = 0;
+};
+// cache row index (in units of dh elements) of key k of (row, head h)
+__device__ __forceinline__ int64_t kv_row(const KvMap& m, int row, int slot, int H, int h, int max_ctx, int k) {
+  if (!m.ptab) return ((int64_t)slot * H + h) * max_ctx + k;
+  const int pg = __ldg(m.ptab + (int64_t)row * m.maxp + k / max_ctx);
+  return ((int64_t)pg * H + h) * max_ctx + k % max_ctx;
+}
+
 // ---- K7: scatter the K,V columns of a fused qkv buffer into cache slots -----
-// qkv: [T][3*inner] bf16; token t goes to (slot[t], pos[t]).
-// Cache layout per layer: [slot][H][max_ctx][dh] for K and for V.
+// qkv: [T][3*inner] bf16; token t goes to block slot[t], offset pos[t] (slot
+// mode: its slot and position; paged mode: its page and position mod P).
+// Cache layout per layer: [block][H][max_ctx][dh] for K and for V.
 void kv_scatter(bf16* kc, bf16* vc, const bf16* qkv, const int32_t* slot, const int32_t* pos, int T, int H,
                 int dh, int max_ctx, cudaStream_t st);
 
@@ -71,9 +91,9 @@ struct DecodeAttnArgs {
   const int32_t* n_keys;
   bf16* out;
   int64_t ldo;
-  int B, H, dh, max_ctx;
+  int B, H, dh, max_ctx;   // max_ctx: slot length, or the page length when paged
   float scale;
-  int split_len;
+  int split_len;           // a multiple of the page length when paged
   int max_splits;      // >= ceil(max_i n_keys[i] / split_len)
   float* partial;      // [B][H][max_splits][dh + 2] when max_splits > 1
   // optional [B][H] zeroed counters: the last split CTA of a (row, head)
@@ -97,6 +117,7 @@ struct DecodeAttnArgs {
   SegInfo qkv_si;
   const bf16* qkv_bias = nullptr;
   int qkv_inner = 0;
+  KvMap kv;   // paged mode: page table of the decode rows (max_ctx = page length)
 };
 void decode_attention(const DecodeAttnArgs& a, cudaStream_t st);
 int& decode_split_override();   // diagnostics: key split length (0 = default)
@@ -116,15 +137,16 @@ struct PrefillAttnArgs {
   int R, max_len;
   bf16* out;
   int64_t ldo;
-  int H, dh, max_ctx;
+  int H, dh, max_ctx;  // max_ctx: slot length, or the page length when paged
   float scale;
   int64_t q_rows;      // rows of the qkv buffer (tokens)
-  int64_t kv_rows;     // slots * H * max_ctx
+  int64_t kv_rows;     // blocks * H * max_ctx
   // causal = 0: every query attends to all keys pos0 .. pos0+len-1 of its
   // request (T5 encoder); bias: score(q, k) += bias[h * bias_ld + bias_off + kpos - qpos]
   int causal = 1;
   const float* bias = nullptr;
   int bias_ld = 0, bias_off = 0;
+  KvMap kv;   // paged mode: page table of the requests, row = r (max_ctx = page length)
 };
 // dh = 128: tcgen05 FMHA (attn_prefill_tc.cu); other head dims: SIMT kernel
 void prefill_attention(const PrefillAttnArgs& a, cudaStream_t st);

@@ -1378,6 +1378,7 @@ void MultiCtx::run(const exg_schedule& s, const exg_request* reqs, int n, int32_
                    exg_run_stats* stats, const exg_run_opts* opts) {
   EXG_CUDA(cudaSetDevice(p_->device));
   if (s.n_stages < 1 || s.n_stages > EXG_MAX_STAGES) throw std::invalid_argument("schedule has no stages");
+  if (opts && opts->kv_page > 0) throw std::invalid_argument("paged KV: RRA on one GPU only (exegpt.h kv_page)");
   Layout* lay = get_layout(p_, s);
   if (s.strategy == EXG_RRA)
     run_rra_multi(p_, lay, s, reqs, n, out_tokens, out_latency, stats, opts);

@@ -304,6 +304,16 @@ Simulator::Simulator(const Profile& p_, const exg_model_spec& m_, const exg_clus
   }
   n_layers = m.n_dec_layers;
   k_dec = m.arch == EXG_ARCH_T5 ? 3 : 2;
+  // decoder KV context per row (oracle/simulator.py kv_ctx_dec): slots of
+  // max_in + max_out, or with paged KV the row-iteration average of the live
+  // positions S_E - 1 + E[S(S+1)] / (2 E[S]) plus 3P/2
+  kv_ctx_dec = (double)(max_in + max_out);
+  if (cl.kv_page > 0 && m.arch != EXG_ARCH_T5) {
+    double m2o = 0.0;
+    for (size_t k = 1; k <= pmf_out.size(); ++k) m2o += (double)k * (double)k * pmf_out[k - 1];
+    const double live = s_e - 1.0 + (m2o + s_d) / (2.0 * s_d);
+    kv_ctx_dec = std::min(live + 1.5 * (double)cl.kv_page, (double)(max_in + max_out));
+  }
 }
 
 double Simulator::tp_sync(int t, double bytes) {
@@ -373,14 +383,14 @@ double Simulator::emb_bytes() const {
 }
 double Simulator::kv_bytes_per_token_layer() const { return 2.0 * ((int64_t)m.n_heads * m.d_head) * 2.0; }
 
-bool Simulator::mem_ok(const std::vector<Stage>& st, int64_t kv_rows, int64_t ctx) {
+bool Simulator::mem_ok(const std::vector<Stage>& st, int64_t kv_rows, double ctx) {
   const int P = (int)st.size();
   for (int k = 0; k < P; ++k) {
     const Stage& s = st[k];
     const int64_t nl = s.layer_end - s.layer_begin;
     double b = nl * layer_bytes() / s.n_gpus;
     if (k == 0 || k == P - 1) b += emb_bytes();
-    b += (double)(kv_rows * ctx * nl) * kv_bytes_per_token_layer() / s.n_gpus;
+    b += (double)kv_rows * ctx * (double)nl * kv_bytes_per_token_layer() / s.n_gpus;
     b += (double)cl.workspace_bytes;
     if (b > (double)cl.mem_per_gpu_bytes) return false;
   }
@@ -396,14 +406,14 @@ bool Simulator::mem_ok(const std::vector<Stage>& st, int64_t kv_rows, int64_t ct
 void Simulator::memory(const Sched& s, std::vector<double>& w, std::vector<double>& kv) {
   w.assign(cl.n_gpus, 0.0);
   kv.assign(cl.n_gpus, 0.0);
-  auto account = [&](const std::vector<Stage>& st, int64_t rows, int64_t ctx) {
+  auto account = [&](const std::vector<Stage>& st, int64_t rows, double ctx) {
     const int P = (int)st.size();
     for (int k = 0; k < P; ++k) {
       const Stage& g = st[k];
       const int64_t nl = g.layer_end - g.layer_begin;
       double b = nl * layer_bytes() / g.n_gpus;
       if (k == 0 || k == P - 1) b += emb_bytes();
-      const double c = (double)(rows * ctx * nl) * kv_bytes_per_token_layer() / g.n_gpus;
+      const double c = (double)rows * ctx * (double)nl * kv_bytes_per_token_layer() / g.n_gpus;
       for (int i = g.first_gpu; i < std::min(g.first_gpu + g.n_gpus, cl.n_gpus); ++i) {
         w[i] += b;
         kv[i] += c;
@@ -413,12 +423,12 @@ void Simulator::memory(const Sched& s, std::vector<double>& w, std::vector<doubl
   if (s.strategy == EXG_STATIC) {
     account(stage_layout(cl.n_gpus, 1, 0, n_layers, 0), s.b_e, (int64_t)max_in + max_out);
   } else if (s.strategy == EXG_RRA) {
-    account(s.stages, s.b_d, (int64_t)max_in + max_out);
+    account(s.stages, s.b_d, kv_ctx_dec);
   } else {
     std::vector<Stage> enc, dec;
     for (const Stage& st : s.stages) (st.first_gpu < s.n_enc_gpus ? enc : dec).push_back(st);
     account(enc, s.b_e, max_in);
-    account(dec, s.b_d, (int64_t)max_in + max_out);
+    account(dec, s.b_d, kv_ctx_dec);
   }
 }
 
@@ -443,7 +453,7 @@ int Simulator::waa_split(int b_e, int b_d, int strat) {
     const double kv = kv_bytes_per_token_layer();
     const double W = n_layers * layer_bytes() + emb_bytes();
     const double mem_e = W + (double)((int64_t)b_e * max_in * n_layers) * kv;
-    const double mem_d = W + (double)((int64_t)b_d * (max_in + max_out) * n_layers) * kv;
+    const double mem_d = W + ((double)b_d * kv_ctx_dec * (double)n_layers) * kv;
     n_enc = (int)std::floor(N * mem_e / (mem_e + mem_d) + 0.5);
   } else {
     const double C_E = n_layers * layer_enc(1, b_e);
@@ -484,7 +494,7 @@ Sched Simulator::waa_schedule(int b_e, int M, int t, int c, int strat) {
 
 Est Simulator::simulate_rra(const Sched& s) {
   Est bad{0.0, 0.0, INF, false};
-  if (!mem_ok(s.stages, s.b_d, (int64_t)max_in + max_out)) return bad;
+  if (!mem_ok(s.stages, s.b_d, kv_ctx_dec)) return bad;
   const auto& pf = pu(s.n_d);
   const int P = (int)s.stages.size();
   double T_encph;
@@ -541,7 +551,7 @@ Est Simulator::simulate_waa(const Sched& s) {
   Est bad{0.0, 0.0, INF, false};
   std::vector<Stage> enc, dec;
   for (const Stage& st : s.stages) (st.first_gpu < s.n_enc_gpus ? enc : dec).push_back(st);
-  if (!(mem_ok(enc, s.b_e, max_in) && mem_ok(dec, s.b_d, (int64_t)max_in + max_out))) return bad;
+  if (!(mem_ok(enc, s.b_e, max_in) && mem_ok(dec, s.b_d, kv_ctx_dec))) return bad;
   const int M = (s.b_d + s.b_m - 1) / s.b_m;
   std::vector<double> te, td;
   double handoff;

@@ -83,7 +83,7 @@ class Simulator {
   double layer_enc(int t, double b);
   double layer_dec(int t, double b);
   std::vector<double> stage_times(const std::vector<Stage>& st, bool enc, double b);
-  bool mem_ok(const std::vector<Stage>& st, int64_t kv_rows, int64_t ctx);
+  bool mem_ok(const std::vector<Stage>& st, int64_t kv_rows, double ctx);
   // per-GPU model / KV-cache bytes of a schedule (mem_ok's memory model)
   void memory(const Sched& s, std::vector<double>& w, std::vector<double>& kv);
 
@@ -93,6 +93,7 @@ class Simulator {
   std::vector<double> pmf_in, pmf_out;
   int target_len;
   double s_e, s_d, ctx_mean, s_e_rms, s_e_sd;
+  double kv_ctx_dec;   // decoder KV positions charged per row (slots, or the paged live average)
   int max_in, max_out, n_layers, k_dec;
   bool use_little;
 

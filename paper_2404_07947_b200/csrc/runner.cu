@@ -22,6 +22,7 @@
 // the argmax kernel straight into a device output array, and times come from
 // events recorded at phase / iteration boundaries (one device clock).
 #include <algorithm>
+#include <array>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -69,6 +70,7 @@ struct Staging {
 struct Row {
   int req, slot, pos, emitted;
   bool live = true;   // false: finished, still computed by the static batch
+  int64_t seq = 0;    // admission order (paged KV: the preemption victim is the latest)
 };
 
 struct EventPool {
@@ -130,12 +132,30 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   const int B_D = ft ? s.b_e : s.b_d, B_E = s.b_e;
   const int enc_drop = ed ? 0 : 1;   // input tokens the encode phase does not process
   const double dyn = (opts && !ft) ? opts->dyn_threshold : 0.0;
+  // paged KV (exegpt.h kv_page): pages
+  // of P positions from a pool of n_pages, a page table row of maxp entries
+  // per batch row
+  const int P = opts ? opts->kv_page : 0;
+  const bool paged = P > 0;
+  int maxp = 0, n_pages = 0;
+  if (paged) {
+    if (ft || ed || D.f32) throw std::invalid_argument("paged KV: decoder-only bf16 models under RRA");
+    if (P % 64 != 0 || 512 % P != 0) throw std::invalid_argument("kv_page must be a multiple of 64 dividing 512");
+    if (opts->kv_pages < 0) throw std::invalid_argument("kv_pages < 0");
+    maxp = (slot_ctx + P - 1) / P;
+    n_pages = opts->kv_pages > 0 ? opts->kv_pages : B_D * maxp;
+    if (n_pages < maxp + 1) throw std::invalid_argument("kv_pages below one request's pages + 1");
+  }
   // encode-phase capacity: B_E rows of at most max_in - enc_drop tokens.  The
   // dynamic adjustment may admit up to B_D rows, but never more tokens than
-  // this (its token target is clamped to enc_tok_cap below)
-  const int enc_tok_cap = std::max(1, B_E * (max_in - enc_drop));
+  // this (its token target is clamped to enc_tok_cap below).  A preempted
+  // row re-encodes up to max_ctx - 1 tokens.
+  const int enc_tok_cap = std::max({1, B_E * (max_in - enc_drop), paged ? max_ctx - 1 : 1});
   const int enc_row_cap = dyn > 0 ? B_D : B_E;
-  E.ensure_kv(B_D, slot_ctx, -1, ed ? max_in : 0);
+  if (paged)
+    E.ensure_kv(std::max(n_pages, B_D), P, -1, 0);
+  else
+    E.ensure_kv(B_D, slot_ctx, -1, ed ? max_in : 0);
   E.ensure_workspace(enc_tok_cap, B_D);
   cudaStream_t st = E.stream();
 
@@ -144,8 +164,9 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   struct DevFree {
     void operator()(int32_t* p) const { cudaFree(p); }
   };
-  const size_t enc_ints = (size_t)3 * enc_tok_cap + 3 * ((size_t)enc_row_cap + 1) + 2 * (size_t)enc_row_cap;
-  const size_t dec_ints = (size_t)5 * B_D;
+  const size_t enc_ints = (size_t)3 * enc_tok_cap + 3 * ((size_t)enc_row_cap + 1) + 2 * (size_t)enc_row_cap +
+                          (paged ? (size_t)2 * enc_tok_cap + (size_t)enc_row_cap * maxp : 0);
+  const size_t dec_ints = (size_t)5 * B_D + (paged ? (size_t)B_D * maxp : 0);
   const size_t tab_ints = std::max(enc_ints, dec_ints);
   int32_t* raw = nullptr;
   // + B_D scratch entries: the tokens of finished rows a static batch still computes
@@ -167,6 +188,22 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
 
   std::vector<int> free_slots(B_D);
   for (int i = 0; i < B_D; ++i) free_slots[i] = B_D - 1 - i;
+  // paged KV state: free page stack, pages of each slot, preempted requests
+  // waiting for re-admission (sorted by request index = arrival order)
+  std::vector<int> free_pages;
+  for (int i = n_pages - 1; i >= 0; --i) free_pages.push_back(i);
+  std::vector<std::vector<int>> slot_pages(paged ? B_D : 0);
+  struct Resume {
+    int req, emitted;
+  };
+  std::vector<Resume> resume;
+  int64_t pages_peak = 0, preemptions = 0, admit_seq = 0;
+  auto release_pages = [&](int slot) {
+    if (!paged) return;
+    for (int pg : slot_pages[slot]) free_pages.push_back(pg);
+    slot_pages[slot].clear();
+  };
+  auto note_peak = [&] { pages_peak = std::max<int64_t>(pages_peak, n_pages - (int64_t)free_pages.size()); };
   std::vector<Row> active;
   active.reserve(B_D);
   std::vector<int> order;   // decode-table row -> active row
@@ -198,9 +235,15 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   E.set_kernel_timing(opts && opts->kernel_timing);
   EXG_CUDA(cudaMemsetAsync(E.err_flag(), 0, sizeof(int32_t), st));
   record(0, 0);
-  while (next_req < n || !active.empty()) {
+  // admission candidates: preempted requests first (their generated tokens
+  // appended to the input), then new requests in arrival order
+  auto cand_req = [&](int k) { return k < (int)resume.size() ? resume[k].req : next_req + (k - (int)resume.size()); };
+  auto cand_emit = [&](int k) { return k < (int)resume.size() ? resume[k].emitted : 0; };
+  auto cand_len = [&](int k) { return reqs[cand_req(k)].input_len + cand_emit(k); };
+  while (next_req < n || !active.empty() || !resume.empty()) {
     // ---------------- encode phase ----------------
-    int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
+    const int waiting = (int)resume.size() + (n - next_req);
+    int admit = std::min({B_E, B_D - (int)active.size(), waiting});
     if (ft && !active.empty()) admit = 0;   // static batch: no admission until it has drained
     if (dyn > 0 && admit > 0) {
       // dynamic workload adjustment: decoder batch below /
@@ -212,16 +255,32 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       }
       be = std::max(1, std::min(be, B_D));
       // encoder workload (token sum) within +-dyn of be x the mean encoded length
-      const int cap = std::min(B_D - (int)active.size(), n - next_req);
+      const int cap = std::min(B_D - (int)active.size(), waiting);
       const double target = be * mean_enc_tokens;
       double tok = 0;
       int k = 0;
       while (k < cap) {
-        const double t = reqs[next_req + k].input_len - enc_drop;
+        const double t = cand_len(k) - enc_drop;
         if (k >= be && tok >= (1 - dyn) * target) break;
         if (k >= 1 && tok + t > (1 + dyn) * target) break;
         if (k >= 1 && tok + t > enc_tok_cap) break;   // workspace / staging capacity
         tok += t;
+        ++k;
+      }
+      admit = k;
+    }
+    if (paged && admit > 0) {
+      // pages for positions 0 .. n'-1 of each admitted row (its encoded
+      // tokens and its first decode position), one free page per active row
+      // kept in reserve; the encode workspace bounds the token sum
+      int64_t fr = (int64_t)free_pages.size();
+      int k = 0, tok = 0;
+      while (k < admit) {
+        const int need = (cand_len(k) + P - 1) / P;
+        if (fr - need < (int64_t)active.size() + k + 1) break;
+        if (k >= 1 && tok + cand_len(k) - enc_drop > enc_tok_cap) break;
+        fr -= need;
+        tok += cand_len(k) - enc_drop;
         ++k;
       }
       admit = k;
@@ -231,7 +290,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       Staging::Slot& sl = stage.acquire();
       int32_t* h = sl.host;
       int T = 0, maxlen = 0;
-      for (int k = 0; k < admit; ++k) T += reqs[next_req + k].input_len - enc_drop;
+      for (int k = 0; k < admit; ++k) T += cand_len(k) - enc_drop;
       int32_t* ids = h;
       int32_t* pos = ids + T;
       int32_t* tsl = pos + T;
@@ -239,38 +298,72 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       int32_t* rsl = cu + admit + 1;
       int32_t* p0 = rsl + admit;
       int32_t* last = p0 + admit;
+      int32_t* kvb = last + admit;            // paged: page / offset per token, page table per request
+      int32_t* kvo = kvb + (paged ? T : 0);
+      int32_t* ptab = kvo + (paged ? T : 0);
+      // tokens a preempted row generated live on the device (d_out): copied
+      // into the uploaded table after the upload (dst offset, src offset, count)
+      std::vector<std::array<int64_t, 3>> gen_copies;
       int t = 0;
       cu[0] = 0;
       for (int k = 0; k < admit; ++k) {
-        const int r = next_req + k;
+        const int r = cand_req(k), e = cand_emit(k);
         const exg_request& q = reqs[r];
+        const int n1 = q.input_len + e;   // prompt + generated tokens (a preempted row)
         const int slot = free_slots.back();
         free_slots.pop_back();
-        const int ne = q.input_len - enc_drop;
+        const int ne = n1 - enc_drop;
+        if (paged) {
+          auto& pg = slot_pages[slot];
+          for (int j = 0; j < (n1 + P - 1) / P; ++j) {
+            pg.push_back(free_pages.back());
+            free_pages.pop_back();
+          }
+          for (int j = 0; j < maxp; ++j) ptab[(int64_t)k * maxp + j] = pg[j < (int)pg.size() ? j : 0];
+        }
+        const int t_start = t;
         for (int j = 0; j < ne; ++j, ++t) {
-          ids[t] = q.input_ids[j];
+          ids[t] = j < q.input_len ? q.input_ids[j] : 0;
           pos[t] = j;
           tsl[t] = slot;
+          if (paged) {
+            kvb[t] = slot_pages[slot][j / P];
+            kvo[t] = j % P;
+          }
         }
+        if (ne > q.input_len) gen_copies.push_back({t_start + q.input_len, base[r], ne - q.input_len});
         cu[k + 1] = t;
         rsl[k] = slot;
         p0[k] = 0;
-        last[k] = ed ? 0 : q.input_ids[q.input_len - 1];
+        if (ed) {
+          last[k] = 0;
+        } else if (n1 - 1 < q.input_len) {
+          last[k] = q.input_ids[n1 - 1];
+        } else {
+          last[k] = 0;
+          gen_copies.push_back({-1 - (int64_t)k, base[r] + e - 1, 1});   // the last generated token
+        }
         maxlen = std::max(maxlen, ne);
-        active.push_back(Row{r, slot, ed ? 0 : q.input_len - 1, 0});
-        admit_ev[r] = ev_phase;
+        active.push_back(Row{r, slot, ed ? 0 : n1 - 1, e, true, admit_seq++});
+        if (admit_ev[r] < 0) admit_ev[r] = ev_phase;
       }
-      const size_t nints = (size_t)3 * T + (admit + 1) + 3 * admit;
+      note_peak();
+      const size_t nints = (size_t)3 * T + (admit + 1) + 3 * admit + (paged ? (size_t)2 * T + (size_t)admit * maxp : 0);
       EXG_CUDA(cudaMemcpyAsync(d_enc, h, nints * sizeof(int32_t), cudaMemcpyHostToDevice, st));
       EXG_CUDA(cudaEventRecord(sl.ev, st));
+      int32_t* d_last = d_enc + 3 * T + (admit + 1) + 2 * admit;
+      for (const auto& c : gen_copies) {
+        int32_t* dst = c[0] >= 0 ? d_enc + c[0] : d_last + (-1 - c[0]);
+        EXG_CUDA(cudaMemcpyAsync(dst, d_out + c[1], sizeof(int32_t) * c[2], cudaMemcpyDeviceToDevice, st));
+      }
       // last_tok[slot] = x[n-1] for the admitted rows
-      set_last_tokens(E.last_tok(), d_enc + 3 * T + (admit + 1), d_enc + 3 * T + (admit + 1) + 2 * admit, admit, st);
+      set_last_tokens(E.last_tok(), d_enc + 3 * T + (admit + 1), d_last, admit, st);
       EncodeBatch eb;
       eb.T = T;
       eb.R = admit;
       eb.max_len = maxlen;
       for (int k = 0; k < admit; ++k) {
-        const double m = reqs[next_req + k].input_len - enc_drop;
+        const double m = cand_len(k) - enc_drop;
         eb.attn_pairs += ed ? m * m : m * (m + 1) / 2;
       }
       eb.ids = d_enc;
@@ -279,9 +372,16 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       eb.cu = d_enc + 3 * T;
       eb.rslot = eb.cu + admit + 1;
       eb.pos0 = eb.rslot + admit;
+      if (paged) {
+        eb.kv_blk = d_last + admit;
+        eb.kv_off = eb.kv_blk + T;
+        eb.kv = KvMap{eb.kv_off + T, maxp};
+      }
       E.encode(eb);
       enc_T = T;
-      next_req += admit;
+      const int from_resume = std::min(admit, (int)resume.size());
+      resume.erase(resume.begin(), resume.begin() + from_resume);
+      next_req += admit - from_resume;
       ++encode_phases;
       ++admitted_phases;
     }
@@ -292,6 +392,41 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
     }
     // ---------------- N_D decode iterations ----------------
     for (int u = 0; (ft || u < s.n_d) && !active.empty(); ++u) {
+      if (paged) {
+        // every row writes key `pos` this iteration: give it the page when
+        // pos crosses into a new one; with none free, preempt the most
+        // recently admitted row (freeing its pages; re-admitted later with
+        // its generated tokens appended -- recompute preemption)
+        for (size_t i = 0; i < active.size();) {
+          const Row& rw = active[i];
+          auto& pg = slot_pages[rw.slot];
+          if (rw.pos / P < (int)pg.size()) {
+            ++i;
+            continue;
+          }
+          if (free_pages.empty()) {
+            size_t v = 0;
+            for (size_t j = 1; j < active.size(); ++j)
+              if (active[j].seq > active[v].seq) v = j;
+            const Row vr = active[v];
+            release_pages(vr.slot);
+            free_slots.push_back(vr.slot);
+            const Resume rs{vr.req, vr.emitted};
+            resume.insert(std::upper_bound(resume.begin(), resume.end(), rs,
+                                           [](const Resume& a, const Resume& b) { return a.req < b.req; }),
+                          rs);
+            active.erase(active.begin() + v);
+            ++preemptions;
+            if (v < i) --i;
+            continue;   // retry row i (or the row that moved into its place)
+          }
+          pg.push_back(free_pages.back());
+          free_pages.pop_back();
+          ++i;
+        }
+        note_peak();
+        if (active.empty()) break;
+      }
       const int B = (int)active.size();
       Staging::Slot& sl = stage.acquire();
       int32_t* h = sl.host;
@@ -323,12 +458,17 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         h[2 * B + i] = pos + 1;
         h[3 * B + i] = rw.live ? (int32_t)(base[rw.req] + rw.emitted) : (int32_t)(total_out + i);
         h[4 * B + i] = reqs[rw.req].input_len;
+        if (paged) {
+          const auto& pg = slot_pages[rw.slot];
+          for (int j = 0; j < maxp; ++j) h[5 * B + (int64_t)i * maxp + j] = pg[j < (int)pg.size() ? j : 0];
+        }
         max_keys = std::max(max_keys, pos + 1);
         sum_keys += pos + 1;
         max_xkeys = std::max(max_xkeys, reqs[rw.req].input_len);
         sum_xkeys += reqs[rw.req].input_len;
       }
-      EXG_CUDA(cudaMemcpyAsync(d_dec, h, (size_t)5 * B * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+      EXG_CUDA(cudaMemcpyAsync(d_dec, h, ((size_t)5 * B + (paged ? (size_t)B * maxp : 0)) * sizeof(int32_t),
+                               cudaMemcpyHostToDevice, st));
       EXG_CUDA(cudaEventRecord(sl.ev, st));
       DecodeBatch db;
       db.B = B;
@@ -344,6 +484,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         db.sum_xkeys = sum_xkeys;
       }
       db.out_tokens = d_out;
+      if (paged) db.kv = KvMap{d_dec + 5 * B, maxp};
       E.decode(db);
       if (dumping) {
         for (int i = 0; i < B; ++i) {
@@ -387,6 +528,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
         if (rw.emitted == reqs[rw.req].output_len) {
           done_ev[rw.req] = ev_it;
           free_slots.push_back(rw.slot);
+          release_pages(rw.slot);
         } else {
           active[w++] = rw;
         }
@@ -436,6 +578,8 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   if (stats) {
     std::memset(stats, 0, sizeof(*stats));
     stats->trace_records = n_trace;
+    stats->kv_preemptions = preemptions;
+    stats->kv_pages_peak = pages_peak;
     stats->kernel_launches = launches;
     for (int c = 0; c < EXG_K_CLASSES; ++c) {
       stats->k_time_s[c] = kt[c];

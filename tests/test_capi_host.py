@@ -40,7 +40,7 @@ def test_library_exports_every_declared_symbol(L):
     assert len(names) >= 20
     for n in sorted(names):
         assert hasattr(lib, n), n
-    assert L.lib().exg_abi_version() == L.ABI_VERSION == 4
+    assert L.lib().exg_abi_version() == L.ABI_VERSION == 5
 
 
 def _setup(task="S", model="opt-13b", n_gpus=1, mem=180e9, ws=4e9):
@@ -61,7 +61,7 @@ def _c_objects(L, spec, prof, d, cl, tmp_path):
     prof.save(path)
     P = L.Profile.load(path)
     mspec = L.model_spec(spec, 1)
-    ccl = L.cluster_spec(cl.n_gpus, cl.mem_per_gpu_bytes, cl.workspace_bytes)
+    ccl = L.cluster_spec(cl.n_gpus, cl.mem_per_gpu_bytes, cl.workspace_bytes, cl.kv_page)
     return P, mspec, ccl, L.Pmf(d.pmf_in), L.Pmf(d.pmf_out)
 
 
@@ -373,3 +373,85 @@ def test_profile_stage_time_matches_simulator_lookups(L, tmp_path):
         assert dec == pytest.approx(ref, rel=1e-12)
     with pytest.raises(L.ExgError):
         P.stage_time(2, 1.0, 1.0, 1)
+
+
+# ------------------------------------------------------ paged KV (NEXT-2) --
+def test_paged_kv_context_pins():
+    """The paged memory model's per-row context (oracle kv_ctx_dec, DESIGN.md
+    reading of PAPER.md:545) against (a) the row-iteration average of live
+    keys evaluated from its definition by brute force over the two PMFs
+    (sum_n sum_S p(n) p(S) sum_{u=1..S} (n - 1 + u) / E[S]) and (b) a
+    discrete-event simulation of a full decode batch with refill (every
+    finished row replaced at once), whose time-average of live keys per row
+    converges to the same value (renewal-reward)."""
+    from oracle import simulator as sim
+    from workload import MODELS, task_dists
+    d = task_dists("G")
+    m = sim.SimModel.from_spec(MODELS["opt-66b"])
+    P = 64
+    S = sim.Simulator(None, m, sim.SimCluster(1, 180e9, 4e9, kv_page=P), d.pmf_in, d.pmf_out, d.target_len)
+    pin, pout = np.asarray(d.pmf_in), np.asarray(d.pmf_out)
+    num = den = 0.0
+    for n in range(1, len(pin) + 1):
+        if pin[n - 1] == 0:
+            continue
+        for So in range(1, len(pout) + 1):
+            w = pin[n - 1] * pout[So - 1]
+            num += w * sum(n - 1 + u for u in range(1, So + 1))
+    for So in range(1, len(pout) + 1):
+        den += pout[So - 1] * So
+    live = num / den
+    assert S.kv_ctx_dec == pytest.approx(live + 1.5 * P, rel=1e-12)
+    # (b) event simulation: 64 rows, 4000 iterations, lengths drawn from the PMFs
+    rng = np.random.default_rng(7)
+    cin, cout = np.cumsum(pin), np.cumsum(pout)
+    draw = lambda c: int(np.searchsorted(c, rng.random() * c[-1])) + 1
+    rows = [[draw(cin), draw(cout), 1] for _ in range(64)]
+    tot = cnt = 0
+    for it in range(4000):
+        for r in rows:
+            if it >= 1000:
+                tot += r[0] - 1 + r[2]
+                cnt += 1
+            r[2] += 1
+            if r[2] > r[1]:
+                r[:] = [draw(cin), draw(cout), 1]
+    assert tot / cnt == pytest.approx(live, rel=0.02)
+    # slots and T5 keep max_in + max_out
+    S0 = sim.Simulator(None, m, sim.SimCluster(1, 180e9, 4e9), d.pmf_in, d.pmf_out, d.target_len)
+    assert S0.kv_ctx_dec == len(pin) + len(pout)
+
+
+@pytest.mark.parametrize("task,model,n_gpus,mask", [("G", "opt-66b", 1, 1), ("G", "opt-66b", 4, 7),
+                                                    ("C2", "gpt3-175b", 8, 3)])
+def test_paged_schedule_find_bit_identical(L, tmp_path, task, model, n_gpus, mask):
+    """C++ planner == oracle with the paged memory model, and paging admits
+    a larger decode batch where slots are memory-bound."""
+    from oracle import bnb, simulator as sim
+    spec, m, prof, d, cl = _setup(task, model, n_gpus)
+    cl.kv_page = 64
+    P, mspec, ccl, pin, pout = _c_objects(L, spec, prof, d, cl, tmp_path)
+    S = sim.Simulator(prof, m, cl, d.pmf_in, d.pmf_out, d.target_len)
+    opts = bnb.SearchOpts(b_e_max=48, m_max=6)
+    copts = L.search_opts(b_e_max=48, m_max=6)
+    for L_b in (1.0, 3.0, math.inf):
+        f = bnb.schedule_find(S, L_b, mask, opts)
+        if f is None:
+            with pytest.raises(L.ExgError):
+                L.schedule_find(P, mspec, ccl, pin, pout, d.target_len, L_b, mask, copts)
+            continue
+        s, est = L.schedule_find(P, mspec, ccl, pin, pout, d.target_len, L_b, mask, copts)
+        assert (s.strategy, s.b_e, s.b_d, s.b_m, s.n_d, s.tp_degree, s.tp_gpus, s.n_enc_gpus) == (
+            f.schedule.strategy, f.schedule.b_e, f.schedule.b_d, f.schedule.b_m, f.schedule.n_d,
+            f.schedule.tp_degree, f.schedule.tp_gpus, f.schedule.n_enc_gpus)
+        assert est.thrput_seq_s == f.estimate.thrput_seq_s and est.latency_s == f.estimate.latency_s
+        w_c, kv_c = L.schedule_memory(P, mspec, ccl, pin, pout, s)
+        assert (w_c, kv_c) == S.memory(f.schedule)
+    if n_gpus == 1:
+        # one 180 GB GPU under OPT-66B: slots cap the decode batch, pages do not
+        S0 = sim.Simulator(prof, m, sim.SimCluster(1, cl.mem_per_gpu_bytes, cl.workspace_bytes), d.pmf_in,
+                           d.pmf_out, d.target_len)
+        b_slots = max(b for b in range(1, 400) if S0.mem_ok(S0.rra_schedule(1, 1, 1, 0).stages, b,
+                                                               S0.kv_ctx_dec))
+        b_paged = max(b for b in range(1, 400) if S.mem_ok(S.rra_schedule(1, 1, 1, 0).stages, b, S.kv_ctx_dec))
+        assert b_paged > 2 * b_slots

@@ -378,3 +378,106 @@ def test_weightgen_bit_identical_to_oracle(L, kind, transposed, rows, cols, cano
     packed = blocked(L, out)
     torch.cuda.synchronize()
     assert torch.equal(blk, packed)
+
+
+# ------------------------------------------------------ paged KV (NEXT-2) --
+def _to_pages(C, lens, P, rng):
+    """Slot cache C [slots][H][ctx][dh] -> page pool [n_pages][H][P][dh] and
+    a page table [rows][maxp] (pages shuffled, unused entries -> page 0)."""
+    slots, H, ctx, dh = C.shape
+    maxp = (ctx + P - 1) // P
+    n_pages = slots * maxp + 3
+    perm = rng.permutation(n_pages)
+    pool = np.zeros((n_pages, H, P, dh))
+    tab = np.zeros((slots, maxp), dtype=np.int32)
+    k = 0
+    for s in range(slots):
+        for j in range((lens[s] + P - 1) // P):
+            pg = perm[k]; k += 1
+            tab[s, j] = pg
+            w = min(P, ctx - j * P)
+            pool[pg, :, :w] = C[s, :, j * P:j * P + w]
+    return pool, tab, n_pages, maxp
+
+
+@pytest.mark.parametrize("dh,P", [(16, 64), (64, 128), (128, 64), (128, 512)])
+def test_decode_attention_paged_matches_slots(L, dh, P):
+    """The paged kernel on a shuffled page pool gives bitwise the slot
+    kernel's output (same keys, same arithmetic), new-key append included."""
+    rng = np.random.default_rng(100 + dh + P)
+    H, max_ctx = 3, 1100
+    n_keys = np.array([1, 2, 63, 64, 65, 127, 128, 129, 511, 512, 513, 1000, 1100, 7], dtype=np.int32)
+    B = len(n_keys)
+    K = bf16_round_np(rng.standard_normal((B, H, max_ctx, dh)))
+    V = bf16_round_np(rng.standard_normal((B, H, max_ctx, dh)))
+    q = bf16_round_np(rng.standard_normal((B, 3 * H * dh)))
+    scale = float(np.float32(1 / math.sqrt(dh)))
+    slot = np.arange(B, dtype=np.int32)
+    split_len, max_splits = 512, 3
+    tq, tslot, tnk = bf16_tensor(q), torch.from_numpy(slot).to(dev()), torch.from_numpy(n_keys).to(dev())
+    part = torch.zeros(B * H * max_splits * (dh + 2), dtype=torch.float32, device=dev())
+    out_s = torch.zeros((B, H * dh), dtype=torch.bfloat16, device=dev())
+    _run(L, "exg_op_decode_attention", ptr(tq), 3 * H * dh, ptr(bf16_tensor(K)), ptr(bf16_tensor(V)), ptr(tslot),
+         ptr(tnk), ptr(out_s), H * dh, B, H, dh, max_ctx, scale, split_len, max_splits, ptr(part), None, 0, 0,
+         stream())
+    Kp, tab, n_pages, maxp = _to_pages(K, n_keys, P, rng)
+    Vp = np.zeros_like(Kp)   # V in the pages of the K table
+    for s in range(B):
+        for j in range((n_keys[s] + P - 1) // P):
+            w = min(P, max_ctx - j * P)
+            Vp[tab[s, j], :, :w] = V[s, :, j * P:j * P + w]
+    ttab = torch.from_numpy(tab).to(dev())
+    out_p = torch.zeros_like(out_s)
+    _run(L, "exg_op_decode_attention_paged", ptr(tq), 3 * H * dh, ptr(bf16_tensor(Kp)), ptr(bf16_tensor(Vp)),
+         ptr(tslot), ptr(tnk), ptr(out_p), H * dh, B, H, dh, P, scale, split_len, max_splits, ptr(part), None, 0, 0,
+         ptr(ttab), maxp, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(out_s.cpu(), out_p.cpu())
+    # and against the fp64 definition on a few rows
+    got = to_np(out_p)
+    for i in (0, 4, 11, 12):
+        for h in range(H):
+            s_ = (K[i, h, :n_keys[i]] @ q[i, h * dh:(h + 1) * dh]) * scale
+            p_ = np.exp(s_ - s_.max()); p_ /= p_.sum()
+            ref = p_ @ V[i, h, :n_keys[i]]
+            assert np.all(np.abs(got[i, h * dh:(h + 1) * dh] - ref) <= 2.0 ** -8 * np.abs(ref) + 2e-3)
+
+
+@pytest.mark.parametrize("dh,P", [(16, 64), (128, 64), (128, 128)])
+def test_prefill_attention_paged_matches_slots(L, dh, P):
+    """Paged prefill attention (SIMT dh=16, tcgen05 FMHA dh=128, 128-key
+    tiles split across 64-key pages) is bitwise the slot kernel."""
+    rng = np.random.default_rng(200 + dh + P)
+    H, max_ctx = 2, 448
+    lens = [1, 5, 63, 64, 65, 100, 128, 129, 257, 383, 448]
+    R = len(lens)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(cu[-1])
+    slot = np.arange(R, dtype=np.int32)
+    pos0 = np.zeros(R, dtype=np.int32)
+    qkv = bf16_round_np(rng.standard_normal((T, 3 * H * dh)))
+    K = np.zeros((R, H, max_ctx, dh)); V = np.zeros((R, H, max_ctx, dh))
+    for r in range(R):
+        for j in range(lens[r]):
+            t = cu[r] + j
+            K[r, :, j] = qkv[t, H * dh:2 * H * dh].reshape(H, dh)
+            V[r, :, j] = qkv[t, 2 * H * dh:].reshape(H, dh)
+    tq = bf16_tensor(qkv)
+    tcu, tsl, tp0 = (torch.from_numpy(a).to(dev()) for a in (cu, slot, pos0))
+    scale = float(np.float32(1 / math.sqrt(dh)))
+    out_s = torch.zeros((T, H * dh), dtype=torch.bfloat16, device=dev())
+    _run(L, "exg_op_prefill_attention", ptr(tq), 3 * H * dh, ptr(bf16_tensor(K)), ptr(bf16_tensor(V)), ptr(tcu),
+         ptr(tsl), ptr(tp0), R, max(lens), ptr(out_s), H * dh, H, dh, max_ctx, R, T, scale, 1, None, 0, 0, stream())
+    Kp, tab, n_pages, maxp = _to_pages(K, lens, P, rng)
+    Vp = np.zeros_like(Kp)
+    for s in range(R):
+        for j in range((lens[s] + P - 1) // P):
+            w = min(P, max_ctx - j * P)
+            Vp[tab[s, j], :, :w] = V[s, :, j * P:j * P + w]
+    ttab = torch.from_numpy(tab).to(dev())
+    out_p = torch.zeros_like(out_s)
+    _run(L, "exg_op_prefill_attention_paged", ptr(tq), 3 * H * dh, ptr(bf16_tensor(Kp)), ptr(bf16_tensor(Vp)),
+         ptr(tcu), ptr(tsl), ptr(tp0), R, max(lens), ptr(out_p), H * dh, H, dh, P, n_pages, T, scale, 1, None, 0, 0,
+         ptr(ttab), maxp, stream())
+    torch.cuda.synchronize()
+    assert torch.equal(out_s.cpu(), out_p.cpu())

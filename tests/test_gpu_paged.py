@@ -1,0 +1,91 @@
+"""Paged KV cache ("the addition of
+vLLM's paging mechanism can further enhance WAA's performance") through
+exg_run, on a decoder-only model with 128-wide heads (tcgen05 FMHA, 64-key
+page halves) and 512 positions:
+
+* paged without memory pressure is bit-identical to the slot cache (same
+  arithmetic, pages shuffled by the allocator);
+* under memory pressure rows are preempted and recomputed (re-encoded with
+  their generated tokens appended): ids equal oracle mode (iii) free-running
+  (near ties reported, parity.py), logits within 2e-2 -- the recomputed K/V
+  come from the prefill GEMM instead of the decode GEMM, another valid
+  evaluation of the same T4 rounding points;
+* out-of-scope requests are rejected (EXG_E_INPUT).
+"""
+import numpy as np
+import pytest
+
+from parity import compare_free_running, decoder_only_tf
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def setup():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    import paper_2404_07947_b200 as X
+    from oracle import transformer as T
+    from workload import ModelSpec, make_requests, uniform_pmf
+    spec = ModelSpec(name="paged-opt", arch="opt", n_enc_layers=0, n_dec_layers=2, d_model=256, n_heads=2,
+                     d_head=128, d_ff=512, vocab=512, max_pos=512)
+    seed = 0xE6E0_00A1
+    reqs = make_requests(24, uniform_pmf(20, 200), uniform_pmf(10, 120), spec.vocab, 0xE6E1_00A1)
+    ctx = X.Context(spec, seed)
+    W = T.Weights(spec, seed)
+    return X, T, spec, W, reqs, ctx
+
+
+@pytest.fixture(scope="module")
+def slots_run(setup):
+    X, T, spec, W, reqs, ctx = setup
+    return ctx.run(X.rra_schedule(4, 12, 4), reqs, dump=range(len(reqs)))
+
+
+@pytest.mark.parametrize("P", [64, 128, 512])
+def test_paged_without_pressure_is_bit_identical(setup, slots_run, P):
+    X, T, spec, W, reqs, ctx = setup
+    toks, _, st, lg = ctx.run(X.rra_schedule(4, 12, 4), reqs, dump=range(len(reqs)), kv_page=P)
+    assert st["kv_preemptions"] == 0 and st["kv_pages_peak"] > 0
+    assert toks == slots_run[0]
+    for r in range(len(reqs)):
+        assert np.array_equal(lg[r], slots_run[3][r]), r
+
+
+@pytest.mark.parametrize("P,pages", [(64, 24), (128, 12)])
+def test_paged_preemption_matches_oracle(setup, slots_run, P, pages):
+    X, T, spec, W, reqs, ctx = setup
+    toks, lat, st, lg = ctx.run(X.rra_schedule(4, 12, 4), reqs, dump=range(len(reqs)), kv_page=P, kv_pages=pages)
+    assert st["kv_preemptions"] > 0, st
+    assert st["kv_pages_peak"] <= pages
+    assert st["out_tokens"] == sum(q.output_len for q in reqs) and np.all(lat > 0)
+    ora = T.greedy_kv(W, reqs, "bf16", record_logits=True)
+    compare_free_running("paged-P%d" % P, toks, lg, ora, TOL, decoder_only_tf(W, reqs), max_near_ties=2)
+    # requests never preempted are bitwise the slot run's (T13)
+    same = sum(np.array_equal(lg[r], slots_run[3][r]) for r in range(len(reqs)))
+    assert same >= 1
+
+
+def test_paged_with_dynamic_adjustment(setup, slots_run):
+    X, T, spec, W, reqs, ctx = setup
+    toks, _, st, lg = ctx.run(X.rra_schedule(4, 12, 4), reqs, dump=range(len(reqs)), kv_page=64,
+                              dyn_threshold=0.1)
+    assert toks == slots_run[0]
+    for r in range(len(reqs)):
+        assert np.array_equal(lg[r], slots_run[3][r]), r
+
+
+def test_paged_rejections(setup):
+    X, T, spec, W, reqs, ctx = setup
+    for kw in ({"kv_page": 96}, {"kv_page": 1024}, {"kv_page": 64, "kv_pages": 3}):
+        with pytest.raises(X.ExgError) as ei:
+            ctx.run(X.rra_schedule(4, 12, 4), reqs[:4], **kw)
+        assert ei.value.status == 1, kw
+    s = X.rra_schedule(4, 12, 4)
+    s.strategy = 8   # EXG_STATIC: the FT baseline keeps slots
+    with pytest.raises(X.ExgError) as ei:
+        ctx.run(s, reqs[:4], kv_page=64)
+    assert ei.value.status == 1
