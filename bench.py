@@ -471,8 +471,17 @@ def run_layout(args, rank, world, local):
             prof.comm_model(COMM_ALPHA_S, COMM_BW)
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         prof.save(os.path.join(ROOT, "gpurun_out", "profile_multi.txt"))
-        plan = multi_plans(X, prof, ctx1.mspec, X.cluster_spec(max(world, 1), mem, ws), pin, pout, d.target_len,
-                           args.margin, args.little)
+        # paged KV (NEXT-2) in the one-GPU dry run: the planner charges each
+        # decode row its live positions (exegpt.h kv_page), the runner pages
+        paged = args.kv_page if world == 1 else 0
+        cl_plan = X.cluster_spec(max(world, 1), mem, ws, kv_page=paged)
+        plan = multi_plans(X, prof, ctx1.mspec, cl_plan, pin, pout, d.target_len, args.margin, args.little)
+        if paged and "sched" in plan["pick"]:
+            # page pool = the GPU's memory after weights and workspace
+            w_b, _ = X.schedule_memory(prof, ctx1.mspec, cl_plan, pin, pout,
+                                       exg_schedule.from_buffer_copy(plan["pick"]["sched"]))
+            page_bytes = spec.n_dec_layers * 2 * spec.n_heads * paged * spec.d_head * 2
+            plan["kv_pages"] = int((mem - w_b[0] - ws) // page_bytes)
         if world > 1:
             ctx1.close()
             del ctx1
@@ -490,6 +499,7 @@ def run_layout(args, rank, world, local):
         return
     s = exg_schedule.from_buffer_copy(plan["pick"]["sched"])
     L_b = plan["latency_bound_s"]
+    pkw = {"kv_page": args.kv_page, "kv_pages": plan["kv_pages"]} if plan.get("kv_pages") else {}
     reqs = make_requests(args.requests, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E1_0000 + MULTI_CONFIG_NO)
     slot_ctx = len(d.pmf_in) + len(d.pmf_out)
     h2d = sum((r.input_len - 1) * 12 + 16 + 16 * r.output_len for r in reqs)
@@ -500,13 +510,13 @@ def run_layout(args, rank, world, local):
             dist.barrier()
 
     for _ in range(args.warmup):
-        ctx.run(s, reqs, slot_ctx=slot_ctx)
+        ctx.run(s, reqs, slot_ctx=slot_ctx, **pkw)
     barrier()
     wall, toks, lat = 0.0, 0, None
     th0 = time.perf_counter()
     with Clocks(local) as clk:
         for _ in range(args.steps):
-            _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx)
+            _, lat, st, _ = ctx.run(s, reqs, slot_ctx=slot_ctx, **pkw)
             wall += st["wall_s"]     # rank 0: stamps of every rank on one clock
             toks += st["out_tokens"]
         barrier()
@@ -538,6 +548,9 @@ def run_layout(args, rank, world, local):
             "sla": {"sla_b_met": bool(max(upto) < L_b), "sla_a_met": bool(np.percentile(lat, 99) <= L_b),
                     "max_latency_upto_p99_len_s": float(max(upto)), "p99_latency_s": float(np.percentile(lat, 99))},
             "forced_waa_tp2": forced, "clocks": clk.summary(),
+            "paged_kv": ({"kv_page": pkw["kv_page"], "kv_pages": pkw["kv_pages"], "preemptions": st["kv_preemptions"],
+                          "pages_peak": st["kv_pages_peak"], "mean_decode_batch": st["mean_decode_batch"]}
+                         if pkw else None),
             "comm": ("measured: XProfiler tp_sync / pp_sync on this job's NCCL communicators" if world > 1 else
                      "one-GPU dry run: alpha-beta interconnect model")}))
     ctx.close()
@@ -589,6 +602,8 @@ def main():
     ap.add_argument("--layout", default="plan", choices=["replicas", "plan"],
                     help="N > 1: config 4 under the scheduler's N-GPU plan as one NCCL job (default), or "
                          "independent config-2 replicas")
+    ap.add_argument("--kv-page", type=int, default=0,
+                    help="one-GPU plan dry run: paged KV of this page length (planner and runner; 0 = slots)")
     ap.add_argument("--plan-dry-run", action="store_true",
                     help="run the N > 1 (config 4) path on one GPU (testing; no collective)")
     ap.add_argument("--multi-model", default=MULTI_MODEL)
@@ -719,6 +734,7 @@ def main():
     # disables their programmatic-dependent-launch overlap (~5 % of a step),
     # so the timed steps above run without them
     kdev = 0.0
+    enc_tokens_step = float(sum(r.input_len - 1 for r in reqs))   # decoder-only: n - 1 encoded per request
     for _ in range(args.roofline_steps):
         _, _, st, _ = ctx.run(sched, reqs, slot_ctx=slot_ctx, kernel_timing=True)
         kdev += st["wall_s"]
@@ -808,11 +824,27 @@ def main():
         peak = pk["bf16_sus"] if tensor else pk["hbm"]
         tr = traffic_ref.get(k)
         traffic = tr["dram_bytes_per_work"] * per_launch_work if tr else None
-        return {"bound": "tensor" if tensor else "hbm", "achieved": ach, "peak": peak,
-                "unit": "TFLOP/s" if tensor else "GB/s", "frac": ach / peak, "traffic": traffic,
-                "kernel": k, "launches": klaunch[k], "time_share": ktime[k] / kdev if kdev else None,
-                "measured": "CUDA events per launch on the engine stream, %d extra step(s)" % args.roofline_steps,
-                "peak_src": pk["src"] + (" sustained" if tensor else "")}
+        out = {"bound": "tensor" if tensor else "hbm", "achieved": ach, "peak": peak,
+               "unit": "TFLOP/s" if tensor else "GB/s", "frac": ach / peak, "traffic": traffic,
+               "kernel": k, "launches": klaunch[k], "time_share": ktime[k] / kdev if kdev else None,
+               "measured": "CUDA events per launch on the engine stream, %d extra step(s)" % args.roofline_steps,
+               "peak_src": pk["src"] + (" sustained" if tensor else "")}
+        if k == "prefill_attn":
+            # classical roofline: the FMHA's algorithmic bytes (q, k, v in, o
+            # out: 4 T H dh 2 per layer launch) against its flops -- at task-S
+            # lengths the arithmetic intensity is below the ridge, so HBM bounds
+            # it
+            byts = 4.0 * enc_tokens_step * spec.n_heads * spec.d_head * 2 * spec.n_dec_layers * args.roofline_steps
+            ai = kwork[k] / byts
+            ridge = pk["bf16_sus"] * 1e12 / (pk["hbm"] * 1e9)
+            out["tensor_view"] = {"achieved": ach, "peak": peak, "unit": "TFLOP/s", "frac": ach / peak}
+            out["intensity_flop_per_byte"] = ai
+            out["ridge_flop_per_byte"] = ridge
+            if ai < ridge:
+                bw = byts / klaunch[k] / avg_t / 1e9
+                out.update({"bound": "hbm", "achieved": bw, "peak": pk["hbm"], "unit": "GB/s",
+                            "frac": bw / pk["hbm"], "peak_src": pk["src"]})
+        return out
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

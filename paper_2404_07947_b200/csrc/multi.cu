@@ -1344,6 +1344,14 @@ void MultiCtx::profile_comm(const std::vector<int>& tps, int reps,
       std::vector<double> v;
       for (int r = 0; r <= reps; ++r) {
         if (me > 1) continue;
+        // handshake first (rank 1 -> rank 0, 4 bytes, both streams drained)
+        // so the timed round trip does not include the host skew between
+        // the two ranks' enqueues
+        if (me == 0)
+          p->comm->recv(buf2, 4, 1, st);
+        else
+          p->comm->send(buf, 4, 0, st);
+        EXG_CUDA(cudaStreamSynchronize(st));
         EXG_CUDA(cudaEventRecord(a, st));
         if (me == 0) {
           p->comm->send(buf, n, 1, st);
