@@ -154,7 +154,8 @@ typedef struct {
    * requests and per decode iteration, in time order --
    *   {kind (1 encode, 2 decode), start [s from the run's first event],
    *    duration [s], rows (admitted requests | decode batch),
-   *    work (encoded tokens | sum of attention keys)};
+   *    work (encoded tokens | sum of attention keys; encoder-decoder
+   *    models: self + cross-attention keys)};
    * at most trace_cap records are written (their count is
    * exg_run_stats.trace_records). */
   double* trace_out;
@@ -293,7 +294,8 @@ exg_status exg_profile_stage_time(const exg_profile* p, int32_t phase, int32_t t
  * model (weight shard + embeddings on the first / last stage of each side;
  * KV slots sized at max_in + max_out rows per decode row -- B_D for RRA / WAA
  * decoder stages, B for EXG_STATIC -- and max_in per encode row on WAA
- * encoder stages).  weight_bytes / kv_bytes: caller-owned double
+ * encoder stages; with cluster->kv_page > 0 a decode row of RRA / WAA is
+ * charged the paged live average instead, see exg_cluster_spec).  weight_bytes / kv_bytes: caller-owned double
  * [cluster->n_gpus]; GPUs outside the layout get 0.  Pure host. */
 exg_status exg_schedule_memory(const exg_profile* p, const exg_model_spec* spec, const exg_cluster_spec* cluster,
                                const exg_pmf* in, const exg_pmf* out_len, const exg_schedule* sched,

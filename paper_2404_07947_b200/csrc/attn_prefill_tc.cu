@@ -118,6 +118,7 @@ struct FmhaParams {
   const float* bias;    // T5 relative bias: score += bias[h * bias_ld + bias_off + kpos - qpos]
   int bias_ld, bias_off;
   KvMap kv;             // paged mode: page table of the requests
+  int pf_ahead;         // L2 prefetch distance in items (0 = off)
 };
 
 // Work item `id` -> (request, head, query tile); false if the tile is past
@@ -198,10 +199,48 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
 
   if (warp == 0) {
     if (lane == 0) {
+      // cache rows of the two 64-key halves of K/V tile j of an item (a half
+      // entirely past the item's last key reads the first half's rows)
+      auto kv_rows2 = [&](const Item& it, int j, int& row0, int& row1) {
+        row0 = (int)kv_row(p.kv, it.r, it.slot, p.H, it.h, p.max_ctx, j * FK);
+        const int k1 = j * FK + 64;
+        row1 = k1 <= it.last_key ? (int)kv_row(p.kv, it.r, it.slot, p.H, it.h, p.max_ctx, k1) : row0;
+      };
+      // L2 prefetch of the items pf_ahead ahead of the one being loaded: at
+      // task-S lengths the kernel is bound by HBM latency / bytes in flight
+      // (DESIGN.md §6), the prefetch keeps more of them in flight than the
+      // shared-memory stages can
+      int pf_id = blockIdx.x, pf_n = 0;
+      auto prefetch_upto = [&](int count) {
+        while (pf_n < count && pf_id < n_items) {
+          Item f;
+          const int id = pf_id;
+          pf_id += gridDim.x;
+          if (!item_of(p, id, f)) continue;
+          ++pf_n;
+          tma_prefetch_2d(&tmQ, f.h * FD, f.t0 + f.qb);
+          tma_prefetch_2d(&tmQ, f.h * FD + 64, f.t0 + f.qb);
+          for (int j = 0; j < f.ntiles; ++j) {
+            int r0, r1;
+            kv_rows2(f, j, r0, r1);
+            for (int hf = 0; hf < (r1 == r0 ? 1 : 2); ++hf) {
+              const int row = hf ? r1 : r0;
+              tma_prefetch_2d(&tmK, 0, row);
+              tma_prefetch_2d(&tmK, 64, row);
+              tma_prefetch_2d(&tmV, 0, row);
+              tma_prefetch_2d(&tmV, 64, row);
+            }
+          }
+        }
+      };
       uint32_t nq = 0, g = 0;   // items loaded, K/V tiles loaded by this CTA
       for (int id = blockIdx.x; id < n_items; id += gridDim.x) {
         Item it;
         if (!item_of(p, id, it)) continue;
+        if (p.pf_ahead > 0) {
+          if (nq == 0) pf_n = 1, pf_id = id + gridDim.x;   // this item's loads are issued now
+          prefetch_upto((int)nq + 1 + p.pf_ahead);
+        }
         const int qs = nq & 1;
         if (nq >= Q_STAGES) mbar_wait(&q_empty[qs], ((nq >> 1) & 1) ^ 1);
         mbar_arrive_expect_tx(&q_full[qs], Q_BYTES);
@@ -215,9 +254,8 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
           // two 64-key halves (each inside one KV block: 64 | page length);
           // a half entirely past the item's last key is loaded from the
           // first half's rows (masked, finite)
-          const int row0 = (int)kv_row(p.kv, it.r, it.slot, p.H, it.h, p.max_ctx, j * FK);
-          const int k1 = j * FK + 64;
-          const int row1 = k1 <= it.last_key ? (int)kv_row(p.kv, it.r, it.slot, p.H, it.h, p.max_ctx, k1) : row0;
+          int row0, row1;
+          kv_rows2(it, j, row0, row1);
 #pragma unroll
           for (int hf = 0; hf < 2; ++hf) {
             const int row = hf ? row1 : row0;
@@ -453,6 +491,12 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
 }
 }  // namespace
 
+// L2 prefetch distance of the FMHA producer in items (exg_diag_fmha_prefetch)
+int& fmha_prefetch_ahead() {
+  static int n = 2;
+  return n;
+}
+
 // diagnostics: 1 = route dh = 128 to the SIMT kernel (exg_diag_prefill_simt)
 int& prefill_force_simt() {
   static int f = 0;
@@ -471,7 +515,8 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   // [kv_rows = slots*H*max_ctx][dh]
   const int QT = (a.max_len + FQ - 1) / FQ;
   FmhaParams p{a.cu_seqlens, a.slot, a.pos0, a.H, a.max_ctx, a.R, QT,
-               a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo, a.causal, a.bias, a.bias_ld, a.bias_off, a.kv};
+               a.scale * 1.4426950408889634f, a.scale, a.out, a.ldo, a.causal, a.bias, a.bias_ld, a.bias_off, a.kv,
+               fmha_prefetch_ahead()};
   const int n_items = QT * a.R * a.H;
   if (n_items <= 0) return true;
   const CUtensorMap tq = make_tmap_bf16(a.q, a.q_rows, a.ldq, a.ldq, 128);
@@ -488,3 +533,4 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
 }  // namespace exg
 
 extern "C" void exg_diag_prefill_simt(int on) { exg::prefill_force_simt() = on; }
+extern "C" void exg_diag_fmha_prefetch(int ahead) { exg::fmha_prefetch_ahead() = ahead > 0 ? ahead : 0; }

@@ -55,17 +55,41 @@ def test_paged_without_pressure_is_bit_identical(setup, slots_run, P):
         assert np.array_equal(lg[r], slots_run[3][r]), r
 
 
-@pytest.mark.parametrize("P,pages", [(64, 24), (128, 12)])
-def test_paged_preemption_matches_oracle(setup, slots_run, P, pages):
+def test_no_preemption_when_n_d_at_most_page(setup):
+    """The admission reserve (one free page per active row) covers the
+    growth of N_D <= P decode iterations: no preemption, even on a pool that
+    throttles admission."""
     X, T, spec, W, reqs, ctx = setup
-    toks, lat, st, lg = ctx.run(X.rra_schedule(4, 12, 4), reqs, dump=range(len(reqs)), kv_page=P, kv_pages=pages)
+    _, _, st, _ = ctx.run(X.rra_schedule(4, 12, 4), reqs, kv_page=64, kv_pages=16)
+    assert st["kv_preemptions"] == 0 and st["kv_pages_peak"] <= 16
+
+
+@pytest.fixture(scope="module")
+def long_reqs(setup):
+    """Long outputs (100..300 tokens) on short inputs: rows outgrow a small
+    pool between admissions."""
+    X, T, spec, W, reqs, ctx = setup
+    from workload import make_requests, uniform_pmf
+    lr = make_requests(24, uniform_pmf(20, 100), uniform_pmf(100, 300), spec.vocab, 0xE6E1_00A2)
+    ora = T.greedy_kv(W, lr, "bf16", record_logits=True)
+    base = ctx.run(X.rra_schedule(8, 12, 200), lr, dump=range(len(lr)))
+    return lr, ora, base
+
+
+@pytest.mark.parametrize("P,pages", [(64, 16), (128, 8)])
+def test_paged_preemption_matches_oracle(setup, long_reqs, P, pages):
+    """N_D = 200 > P: rows cross several pages between admissions, the pool
+    runs dry and the latest-admitted rows are preempted, re-encoded with their
+    generated tokens and continued."""
+    X, T, spec, W, reqs, ctx = setup
+    lr, ora, base = long_reqs
+    toks, lat, st, lg = ctx.run(X.rra_schedule(8, 12, 200), lr, dump=range(len(lr)), kv_page=P, kv_pages=pages)
     assert st["kv_preemptions"] > 0, st
     assert st["kv_pages_peak"] <= pages
-    assert st["out_tokens"] == sum(q.output_len for q in reqs) and np.all(lat > 0)
-    ora = T.greedy_kv(W, reqs, "bf16", record_logits=True)
-    compare_free_running("paged-P%d" % P, toks, lg, ora, TOL, decoder_only_tf(W, reqs), max_near_ties=2)
+    assert st["out_tokens"] == sum(q.output_len for q in lr) and np.all(lat > 0)
+    compare_free_running("paged-P%d" % P, toks, lg, ora, TOL, decoder_only_tf(W, lr), max_near_ties=2)
     # requests never preempted are bitwise the slot run's (T13)
-    same = sum(np.array_equal(lg[r], slots_run[3][r]) for r in range(len(reqs)))
+    same = sum(np.array_equal(lg[r], base[3][r]) for r in range(len(lr)))
     assert same >= 1
 
 

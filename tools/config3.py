@@ -49,14 +49,26 @@ def main():
     reqs = make_requests(n, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E1_0003)
     slot_ctx = t.out_max
     ctx.run(s1, reqs, slot_ctx=slot_ctx)
-    toks1, lat, st, _ = ctx.run(s1, reqs, slot_ctx=slot_ctx)
+    trace = []
+    toks1, lat, st, _ = ctx.run(s1, reqs, slot_ctx=slot_ctx, trace=trace)
+    # simulator fidelity per stage: measured encode phases / decode iterations
+    # against the profile's time for the same rows and work
+    # (exg_profile_stage_time), and the batch trajectory
+    fid = {}
+    for kind, name, ph in ((1, "encode", 0), (2, "decode", 1)):
+        recs = [r for r in trace if int(r[0]) == kind and r[3] > 0]
+        meas = sum(r[2] for r in recs)
+        pred = sum(prof.stage_time(ph, r[3], r[4], spec.n_dec_layers) for r in recs)
+        fid[name] = {"stages": len(recs), "measured_s": meas, "profile_s": pred,
+                     "measured_over_profile": meas / pred if pred > 0 else None,
+                     "mean_rows": float(np.mean([r[3] for r in recs])) if recs else 0.0}
     out = {"workload": "config 3: T5-11B (seeded random init), task T, %d requests" % n,
            "profile_s": t_prof, "latency_bound_s": L_b, "bounds": bounds,
            "one_gpu": {"schedule": s1.as_dict(), "predicted_tok_s": e1.thrput_tok_s,
                        "predicted_latency_s": e1.latency_s, "tok_s": st["tok_s"], "tok_s_steady": st["tok_s_steady"],
                        "p99_latency_s": float(np.percentile(lat, 99)), "mean_decode_batch": st["mean_decode_batch"],
                        "encode_s": st["encode_s"], "decode_s": st["decode_s"],
-                       "sla_a_met": bool(np.percentile(lat, 99) <= L_b)}}
+                       "sla_a_met": bool(np.percentile(lat, 99) <= L_b), "stage_fidelity": fid}}
     if s2 is not None:
         ctx.close()
         del ctx

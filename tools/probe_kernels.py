@@ -189,7 +189,8 @@ def pattn_mix(R, H=40, dh=128, seed=0):
                                                  0, st()))
     t = timeit(fn)
     flops = sum(4.0 * H * dh * n * (n + 1) / 2 for n in lens)
-    print("prefill-attn mix R=%d mean n %.0f: %8.1f us  %7.1f TFLOP/s" % (R, T / R, t * 1e6, flops / t / 1e12))
+    print("prefill-attn mix R=%d mean n %.0f: %8.1f us  %7.1f TFLOP/s  %7.1f GB/s (q,k,v,o)" % (
+        R, T / R, t * 1e6, flops / t / 1e12, 4.0 * T * H * dh * 2 / t / 1e9))
 
 
 def stream_probe():
@@ -273,6 +274,16 @@ if __name__ == "__main__":
             pattn_mix(R)
         for R, n in ((16, 256), (16, 512), (8, 1024), (64, 128)):
             pattn(R, n)
+        sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "pmix_pf":
+        # A/B of the FMHA's L2 prefetch distance (exg_diag_fmha_prefetch)
+        for ahead in (0, 1, 2, 4):
+            L.lib().exg_diag_fmha_prefetch(ahead)
+            print("-- FMHA L2 prefetch ahead = %d" % ahead)
+            for R in (32, 52):
+                pattn_mix(R)
+            pattn(32, 256)
+        L.lib().exg_diag_fmha_prefetch(2)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pattn":
         pattn(int(sys.argv[2]), int(sys.argv[3]))
