@@ -27,6 +27,7 @@
 // stage) and iteration ends (on the rank owning the LM head); rank 0 gathers
 // them and the output tokens at the end.
 #include <algorithm>
+#include <functional>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -73,8 +74,11 @@ struct HandoffRow {
 //   mode 0: encoder cache -> decoder cache (both on this rank)
 //   mode 1: encoder cache -> packed message
 //   mode 2: packed message -> decoder cache
+// A paged decoder cache (dpt != nullptr; ctx_d = the page length) takes key k
+// of row i at page dpt[i * maxp + k / ctx_d], offset k mod ctx_d.
 __global__ void kv_handoff_kernel(const bf16* __restrict__ src, bf16* __restrict__ dst, const HandoffRow* rows,
-                                  int nrows, int He, int h0, int Hd, int ctx_e, int ctx_d, int dh, int mode) {
+                                  int nrows, int He, int h0, int Hd, int ctx_e, int ctx_d, int dh, int mode,
+                                  const int32_t* __restrict__ dpt = nullptr, int maxp = 0) {
   const int rh = blockIdx.x;
   const int i = rh / Hd, h = rh % Hd;
   if (i >= nrows) return;
@@ -82,8 +86,17 @@ __global__ void kv_handoff_kernel(const bf16* __restrict__ src, bf16* __restrict
   const int64_t pk = (r.off * Hd + (int64_t)h * r.len) * dh;
   const int4* s = reinterpret_cast<const int4*>(mode == 2 ? src + pk
                                                           : src + (((int64_t)r.src_slot * He + h0 + h) * ctx_e) * dh);
-  int4* d = reinterpret_cast<int4*>(mode == 1 ? dst + pk : dst + (((int64_t)r.dst_slot * Hd + h) * ctx_d) * dh);
   const int n = r.len * dh / 8;
+  if (mode != 1 && dpt) {
+    const int cpk = dh / 8;   // 16-byte chunks per key row
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      const int k = e / cpk, c = e % cpk;
+      const int64_t row = ((int64_t)dpt[(int64_t)i * maxp + k / ctx_d] * Hd + h) * ctx_d + k % ctx_d;
+      reinterpret_cast<int4*>(dst + row * dh)[c] = s[e];
+    }
+    return;
+  }
+  int4* d = reinterpret_cast<int4*>(mode == 1 ? dst + pk : dst + (((int64_t)r.dst_slot * Hd + h) * ctx_d) * dh);
   for (int e = threadIdx.x; e < n; e += blockDim.x) d[e] = s[e];
 }
 
@@ -548,6 +561,7 @@ static Layout* get_layout(MultiCtx::Impl* p, const exg_schedule& s) {
 namespace {
 struct Row {
   int req, slot, pos, emitted;
+  int64_t seq = 0;   // admission order (paged KV: the swap-out victim is the latest)
 };
 
 struct Tables {
@@ -601,6 +615,11 @@ struct RunState {
   std::vector<int64_t> iter_tokens;   // tokens emitted by the iteration ending at iter_ev[k]
   cudaStream_t st;
   int64_t decode_iters = 0, encode_phases = 0, batch_sum = 0;
+  // paged decoder KV (WAA; exegpt.h kv_page): page length, page-table row
+  // length, pages of each decoder slot
+  int P = 0, maxp = 0;
+  std::vector<std::vector<int>> slot_pages;
+  int64_t preemptions = 0, pages_peak = 0;
   ~RunState() {
     if (st) cudaStreamSynchronize(st);
     if (d_out) cudaFree(d_out);
@@ -685,7 +704,8 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
 
 DecodeBatch build_decode(const RunState& R, Tables& tb, const std::vector<Row>& rows, int i0, int B,
                          cudaStream_t st) {
-  tb.ensure((size_t)5 * B + 8);
+  const size_t pt = R.P > 0 ? (size_t)B * R.maxp : 0;   // paged: page table rows of the batch
+  tb.ensure((size_t)5 * B + pt + 8);
   int32_t* h = tb.begin();
   DecodeBatch db;
   for (int i = 0; i < B; ++i) {
@@ -700,8 +720,13 @@ DecodeBatch build_decode(const RunState& R, Tables& tb, const std::vector<Row>& 
     db.sum_keys += rw.pos + 1;
     db.max_xkeys = std::max(db.max_xkeys, n_in);
     db.sum_xkeys += n_in;
+    if (pt) {
+      const auto& pg = R.slot_pages[rw.slot];
+      for (int j = 0; j < R.maxp; ++j) h[5 * B + (int64_t)i * R.maxp + j] = pg[j < (int)pg.size() ? j : 0];
+    }
   }
-  tb.upload((size_t)5 * B, st);
+  tb.upload((size_t)5 * B + pt, st);
+  if (pt) db.kv = KvMap{tb.dev + 5 * B, R.maxp};
   if (R.ed) db.xkeys = tb.dev + 4 * B;
   db.B = B;
   db.slot = tb.dev;
@@ -775,7 +800,8 @@ void return_tokens(const Exec& X, std::vector<std::unique_ptr<Stage>>& pipe, int
            Fs.eng[r] ? Fs.eng[r]->last_tok() : nullptr, sizeof(int32_t) * slots);
 }
 
-void retire(RunState& R, std::vector<Row>& active, std::vector<int>& free_slots, int ev) {
+void retire(RunState& R, std::vector<Row>& active, std::vector<int>& free_slots, int ev,
+            std::vector<int>* free_pages = nullptr) {
   int w = 0;
   for (size_t i = 0; i < active.size(); ++i) {
     Row rw = active[i];
@@ -784,6 +810,10 @@ void retire(RunState& R, std::vector<Row>& active, std::vector<int>& free_slots,
     if (rw.emitted == R.reqs[rw.req].output_len) {
       R.done_ev[rw.req] = ev;
       free_slots.push_back(rw.slot);
+      if (free_pages) {
+        for (int pg : R.slot_pages[rw.slot]) free_pages->push_back(pg);
+        R.slot_pages[rw.slot].clear();
+      }
     } else {
       active[w++] = rw;
     }
@@ -870,6 +900,8 @@ void finish(const Exec& X, RunState& R, Stage& head_stage, int32_t* out_tokens, 
     stats->lat_max_s = s.back();
     stats->mean_decode_batch = R.decode_iters ? (double)R.batch_sum / R.decode_iters : 0;
     stats->mean_encode_batch = R.encode_phases ? (double)R.n / R.encode_phases : 0;
+    stats->kv_preemptions = R.preemptions;
+    stats->kv_pages_peak = R.pages_peak;
     // steady window: admission of request ceil(0.1 n) .. admission of the last
     const int r0 = std::min(R.n - 1, (int)std::ceil(0.1 * R.n));
     const double w0 = sec(R.admit_ev[r0]), w1 = sec(R.admit_ev[R.n - 1]);
@@ -1033,6 +1065,24 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   const int B_D = s.b_d, B_E = s.b_e;
   if (B_E < 1 || B_D < B_E) throw std::invalid_argument("WAA needs 1 <= B_E <= B_D");
   const int M = s.b_m > 0 ? std::max(1, (B_D + s.b_m - 1) / s.b_m) : 1;
+  // paged decoder KV (exegpt.h kv_page; "the addition of vLLM's
+  // paging mechanism can further enhance WAA's performance"): pages as on one
+  // GPU (runner.cu); a row that finds no free page swaps the latest-admitted
+  // row's pages out to pinned host memory and back in when pages free up
+  // (swap preemption: the K/V return unchanged, so results stay bit-identical)
+  const int P = opts ? opts->kv_page : 0;
+  const bool paged = P > 0;
+  int n_pages = 0;
+  if (paged) {
+    if (R.ed) throw std::invalid_argument("paged KV: decoder-only models");
+    if (P % 64 != 0 || 512 % P != 0) throw std::invalid_argument("kv_page must be a multiple of 64 dividing 512");
+    if (opts->kv_pages < 0) throw std::invalid_argument("kv_pages < 0");
+    R.P = P;
+    R.maxp = (slot_ctx + P - 1) / P;
+    n_pages = opts->kv_pages > 0 ? opts->kv_pages : B_D * R.maxp;
+    if (n_pages < R.maxp + 1) throw std::invalid_argument("kv_pages below one request's pages + 1");
+    R.slot_pages.assign(B_D, {});
+  }
   const int enc_ctx = std::max(1, R.max_in);
   const int drop = R.ed ? 0 : 1;
   const double dyn = opts ? opts->dyn_threshold : 0.0;
@@ -1056,7 +1106,10 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   for (auto& st : dec)
     for (auto& e : st->eng)
       if (e) {
-        e->ensure_kv(B_D, slot_ctx, -1, R.ed ? R.max_in : 0);
+        if (paged)
+          e->ensure_kv(std::max(n_pages, B_D), P, -1, 0);
+        else
+          e->ensure_kv(B_D, slot_ctx, -1, R.ed ? R.max_in : 0);
         e->ensure_workspace(1, B_D);
       }
   const bool first_mine = X.mine(enc.front()->gpu(0)), head_mine = X.mine(dec.back()->gpu(0));
@@ -1083,9 +1136,74 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   std::vector<Row> active;
   R.admit_ev.assign(n, -1);
   R.done_ev.assign(n, -1);
-  int next_req = 0, pend_r0 = -1, pend_k = 0, pend_ev = -1, ti = 0;
+  // paged KV state: free pages, swapped-out rows (sorted by request index),
+  // their pinned host images (freed after the run)
+  std::vector<int> free_pages;
+  for (int i = n_pages - 1; i >= 0; --i) free_pages.push_back(i);
+  struct Swapped {
+    Row row;
+    void* host;
+    int npg;
+  };
+  std::vector<Swapped> swapped;
+  std::vector<void*> host_bufs;
+  int64_t admit_seq = 0;
+  auto note_peak = [&] {
+    R.pages_peak = std::max<int64_t>(R.pages_peak, (int64_t)n_pages - (int64_t)free_pages.size());
+  };
+  // this rank's decoder K / V blocks of the given pages, in a fixed order
+  // (stage, TP rank, layer, K|V, page): fn(device block, bytes)
+  auto for_each_block = [&](const std::vector<int>& pages, const std::function<void(bf16*, size_t)>& fn) {
+    for (auto& ds : dec)
+      for (auto& e : ds->eng)
+        if (e) {
+          const size_t blk = (size_t)e->dims().Hl * P * dh;
+          for (int l = 0; l < e->n_layers(); ++l)
+            for (int kv = 0; kv < 2; ++kv)
+              for (int pg : pages) fn((kv ? e->vc(l) : e->kc(l)) + (size_t)pg * blk, blk * sizeof(bf16));
+        }
+  };
+  auto swap_out = [&](size_t v) {
+    const Row vr = active[v];
+    auto& pg = R.slot_pages[vr.slot];
+    size_t bytes = 0;
+    for_each_block(pg, [&](bf16*, size_t b) { bytes += b; });
+    void* hb = nullptr;
+    if (bytes) EXG_CUDA(cudaMallocHost(&hb, bytes));
+    host_bufs.push_back(hb);
+    size_t off = 0;
+    for_each_block(pg, [&](bf16* dptr, size_t b) {
+      EXG_CUDA(cudaMemcpyAsync(static_cast<char*>(hb) + off, dptr, b, cudaMemcpyDeviceToHost, R.st));
+      off += b;
+    });
+    const Swapped sw{vr, hb, (int)pg.size()};
+    for (int x : pg) free_pages.push_back(x);   // reused only by later work on this stream
+    pg.clear();
+    swapped.insert(std::upper_bound(swapped.begin(), swapped.end(), sw,
+                                    [](const Swapped& a, const Swapped& b) { return a.row.req < b.row.req; }),
+                   sw);
+    active.erase(active.begin() + v);   // the row keeps its slot (and last_tok[slot])
+    ++R.preemptions;
+  };
+  auto swap_in = [&]() {
+    const Swapped sw = swapped.front();
+    swapped.erase(swapped.begin());
+    auto& pg = R.slot_pages[sw.row.slot];
+    for (int j = 0; j < sw.npg; ++j) {
+      pg.push_back(free_pages.back());
+      free_pages.pop_back();
+    }
+    size_t off = 0;
+    for_each_block(pg, [&](bf16* dptr, size_t b) {
+      EXG_CUDA(cudaMemcpyAsync(dptr, static_cast<char*>(sw.host) + off, b, cudaMemcpyHostToDevice, R.st));
+      off += b;
+    });
+    active.push_back(sw.row);
+    note_peak();
+  };
+  int next_req = 0, pend_r0 = -1, pend_k = 0, pend_s0 = 0, pend_ev = -1, ti = 0;
   R.record(first_mine);
-  while (next_req < n || pend_k > 0 || !active.empty()) {
+  while (next_req < n || pend_k > 0 || !active.empty() || !swapped.empty()) {
     // encoder: keep one encoded batch ready (encoder slots 0..k-1)
     if (pend_k == 0 && next_req < n) {
       int k = std::min(B_E, n - next_req);
@@ -1126,13 +1244,32 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       }
       pend_r0 = next_req;
       pend_k = k;
+      pend_s0 = 0;
       next_req += k;
       ++R.encode_phases;
       R.enc_end_ev.push_back(R.record(X.mine(enc.back()->gpu(0))));
     }
+    // paged: swapped-out rows come back first, each when its pages fit with
+    // one page per active row in reserve
+    while (paged && !swapped.empty() &&
+           (int64_t)free_pages.size() - swapped.front().npg >= (int64_t)active.size() + 1)
+      swap_in();
     // handoff + merge at an iteration boundary when the decoder has room
-    if (pend_k > 0 && (int)free_slots.size() >= pend_k) {
-      std::vector<int> dslots(pend_k);
+    // (paged: no row swapped out; the longest prefix of the encoded batch
+    // whose pages fit with the reserve -- the rest stays pending)
+    int hk = pend_k;
+    if (paged && pend_k > 0) {
+      hk = 0;
+      int64_t fr = (int64_t)free_pages.size();
+      while (swapped.empty() && hk < pend_k && hk < (int)free_slots.size()) {
+        const int need = (reqs[pend_r0 + hk].input_len + P - 1) / P;   // positions 0 .. n-1
+        if (fr - need < (int64_t)active.size() + hk + 1) break;
+        fr -= need;
+        ++hk;
+      }
+    }
+    if (pend_k > 0 && hk > 0 && (int)free_slots.size() >= hk) {
+      std::vector<int> dslots(hk);
       int64_t rows_len = 0;
       // a row table slot is rewritten only once its previous upload is done
       const int hs = hr_next;
@@ -1140,17 +1277,35 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       if (hr_used[hs]) EXG_CUDA(cudaEventSynchronize(hr_ev[hs]));
       HandoffRow* hrow_h = h_hrows[hs];
       HandoffRow* hrow_d = d_hrows[hs];
-      for (int j = 0; j < pend_k; ++j) {
+      const int32_t* dpt = nullptr;   // paged: destination page table [hk][maxp]
+      if (paged) {
+        Tables& tp = tabs[ti++ % tabs.size()];
+        tp.ensure((size_t)hk * R.maxp + 8);
+        int32_t* hp = tp.begin();
+        for (int j = 0; j < hk; ++j) {
+          const int slot = free_slots[free_slots.size() - 1 - j];
+          auto& pg = R.slot_pages[slot];
+          for (int q = 0; q < (reqs[pend_r0 + j].input_len + P - 1) / P; ++q) {
+            pg.push_back(free_pages.back());
+            free_pages.pop_back();
+          }
+          for (int q = 0; q < R.maxp; ++q) hp[(int64_t)j * R.maxp + q] = pg[q < (int)pg.size() ? q : 0];
+        }
+        tp.upload((size_t)hk * R.maxp, R.st);
+        dpt = tp.dev;
+        note_peak();
+      }
+      for (int j = 0; j < hk; ++j) {
         dslots[j] = free_slots.back();
         free_slots.pop_back();
         const exg_request& q = reqs[pend_r0 + j];
         // handed-off K/V rows: positions 0..n-2 (decoder-only) / the n cross K/V rows (T5)
-        hrow_h[j] = HandoffRow{j, dslots[j], q.input_len - drop, rows_len};
+        hrow_h[j] = HandoffRow{pend_s0 + j, dslots[j], q.input_len - drop, rows_len};
         rows_len += q.input_len - drop;
-        active.push_back(Row{pend_r0 + j, dslots[j], R.ed ? 0 : q.input_len - 1, 0});
+        active.push_back(Row{pend_r0 + j, dslots[j], R.ed ? 0 : q.input_len - 1, 0, admit_seq++});
         R.admit_ev[pend_r0 + j] = pend_ev;
       }
-      EXG_CUDA(cudaMemcpyAsync(hrow_d, hrow_h, sizeof(HandoffRow) * pend_k, cudaMemcpyHostToDevice, R.st));
+      EXG_CUDA(cudaMemcpyAsync(hrow_d, hrow_h, sizeof(HandoffRow) * hk, cudaMemcpyHostToDevice, R.st));
       EXG_CUDA(cudaEventRecord(hr_ev[hs], R.st));
       hr_used[hs] = true;
       const size_t need = (size_t)rows_len * H * dh;   // largest slice (a TP-1 decoder stage)
@@ -1177,7 +1332,7 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
               Engine* src = es->eng[0].get();
               Engine* dst = ds->eng[r].get();
               const size_t bytes = sizeof(bf16) * (size_t)rows_len * Hd * dh;
-              const int ctx_d = R.ed ? R.max_in : slot_ctx;
+              const int ctx_d = R.ed ? R.max_in : (paged ? P : slot_ctx);
               for (int kv = 0; kv < 2; ++kv) {
                 const bf16* sp_ = nullptr;
                 bf16* dp = nullptr;
@@ -1186,27 +1341,27 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
                   dp = R.ed ? (kv ? dst->xvc(l - ds->l0) : dst->xkc(l - ds->l0))
                             : (kv ? dst->vc(l - ds->l0) : dst->kc(l - ds->l0));
                 if (src_mine && dst_mine && X.loop) {
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, stage_buf, hrow_d, pend_k, H, r * Hd, Hd,
-                                                                   enc_ctx, ctx_d, dh, 1);
+                  kv_handoff_kernel<<<hk * Hd, 128, 0, R.st>>>(sp_, stage_buf, hrow_d, hk, H, r * Hd, Hd,
+                                                               enc_ctx, ctx_d, dh, 1);
                   EXG_CHECK_LAUNCH();
                   p->comm->group_start();
                   p->comm->send(stage_buf, bytes, X.me, R.st);
                   p->comm->recv(stage_buf + stage_cap, bytes, X.me, R.st);
                   p->comm->group_end();
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(stage_buf + stage_cap, dp, hrow_d, pend_k, H,
-                                                                   r * Hd, Hd, enc_ctx, ctx_d, dh, 2);
+                  kv_handoff_kernel<<<hk * Hd, 128, 0, R.st>>>(stage_buf + stage_cap, dp, hrow_d, hk, H,
+                                                               r * Hd, Hd, enc_ctx, ctx_d, dh, 2, dpt, R.maxp);
                   EXG_CHECK_LAUNCH();
                 } else if (src_mine && dst_mine) {
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, dp, hrow_d, pend_k, H, r * Hd, Hd, enc_ctx,
-                                                                   ctx_d, dh, 0);
+                  kv_handoff_kernel<<<hk * Hd, 128, 0, R.st>>>(sp_, dp, hrow_d, hk, H, r * Hd, Hd, enc_ctx,
+                                                               ctx_d, dh, 0, dpt, R.maxp);
                   EXG_CHECK_LAUNCH();
                 } else if (src_mine) {
                   // pack into a send staging buffer (compute stream), send on the
                   // comm stream: the encoder rank goes on with the next batch
                   const int sl = X.tx->acquire(bytes);
                   if (X.tx->used[sl]) EXG_CUDA(cudaStreamWaitEvent(R.st, X.tx->done[sl], 0));
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(sp_, static_cast<bf16*>(X.tx->buf[sl]), hrow_d,
-                                                                   pend_k, H, r * Hd, Hd, enc_ctx, ctx_d, dh, 1);
+                  kv_handoff_kernel<<<hk * Hd, 128, 0, R.st>>>(sp_, static_cast<bf16*>(X.tx->buf[sl]), hrow_d,
+                                                               hk, H, r * Hd, Hd, enc_ctx, ctx_d, dh, 1);
                   EXG_CHECK_LAUNCH();
                   EXG_CUDA(cudaEventRecord(X.tx->ready[sl], R.st));
                   EXG_CUDA(cudaStreamWaitEvent(X.cst, X.tx->ready[sl], 0));
@@ -1221,9 +1376,9 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
                   p->comm->recv(X.rx->buf[sl], bytes, X.owner(ge), X.cst);
                   EXG_CUDA(cudaEventRecord(X.rx->ready[sl], X.cst));
                   EXG_CUDA(cudaStreamWaitEvent(R.st, X.rx->ready[sl], 0));
-                  kv_handoff_kernel<<<pend_k * Hd, 128, 0, R.st>>>(static_cast<const bf16*>(X.rx->buf[sl]), dp,
-                                                                   hrow_d, pend_k, H, r * Hd, Hd, enc_ctx, ctx_d, dh,
-                                                                   2);
+                  kv_handoff_kernel<<<hk * Hd, 128, 0, R.st>>>(static_cast<const bf16*>(X.rx->buf[sl]), dp,
+                                                               hrow_d, hk, H, r * Hd, Hd, enc_ctx, ctx_d, dh,
+                                                               2, dpt, R.maxp);
                   EXG_CHECK_LAUNCH();
                   EXG_CUDA(cudaEventRecord(X.rx->done[sl], R.st));
                   X.rx->used[sl] = true;
@@ -1234,17 +1389,43 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       }
       // x[n-1] of the merged requests -> last_tok[slot] on the decoder's first stage
       Tables& tl = tabs[ti++ % tabs.size()];
-      tl.ensure(2 * pend_k + 2);
+      tl.ensure(2 * hk + 2);
       int32_t* h = tl.begin();
-      for (int j = 0; j < pend_k; ++j) {
+      for (int j = 0; j < hk; ++j) {
         const exg_request& q = reqs[pend_r0 + j];
         h[j] = dslots[j];
-        h[pend_k + j] = R.ed ? 0 : q.input_ids[q.input_len - 1];   // T5: decoder start token 0
+        h[hk + j] = R.ed ? 0 : q.input_ids[q.input_len - 1];   // T5: decoder start token 0
       }
-      tl.upload(2 * pend_k, R.st);
+      tl.upload(2 * hk, R.st);
       for (auto& e : dec.front()->eng)
-        if (e) set_last_tokens(e->last_tok(), tl.dev, tl.dev + pend_k, pend_k, R.st);
-      pend_k = 0;
+        if (e) set_last_tokens(e->last_tok(), tl.dev, tl.dev + hk, hk, R.st);
+      pend_r0 += hk;
+      pend_s0 += hk;
+      pend_k -= hk;
+    }
+    if (paged) {
+      // every row writes key `pos` this iteration: a new page when it crosses
+      // into one; none free -> swap out the latest-admitted row
+      for (size_t i = 0; i < active.size();) {
+        const int slot = active[i].slot, pos = active[i].pos;
+        auto& pg = R.slot_pages[slot];
+        if (pos / P < (int)pg.size()) {
+          ++i;
+          continue;
+        }
+        if (free_pages.empty()) {
+          size_t v = 0;
+          for (size_t j = 1; j < active.size(); ++j)
+            if (active[j].seq > active[v].seq) v = j;
+          swap_out(v);
+          if (v < i) --i;
+          continue;
+        }
+        pg.push_back(free_pages.back());
+        free_pages.pop_back();
+        ++i;
+      }
+      note_peak();
     }
     if (active.empty()) continue;
     decode_pipeline(X, R, dec, tabs, ti, active, M, d, dump);
@@ -1258,10 +1439,12 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       steady_batch_sum += (double)active.size();
       ++steady_iters;
     }
-    retire(R, active, free_slots, ev);
+    retire(R, active, free_slots, ev, paged ? &free_pages : nullptr);
   }
   finish(X, R, *dec.back(), out_tokens, out_latency, stats);
   EXG_CUDA(cudaStreamSynchronize(R.st));
+  for (void* hb : host_bufs)
+    if (hb) cudaFreeHost(hb);
   if (stage_buf) cudaFree(stage_buf);
   for (int i = 0; i < HR; ++i) {
     cudaFree(d_hrows[i]);
@@ -1386,7 +1569,8 @@ void MultiCtx::run(const exg_schedule& s, const exg_request* reqs, int n, int32_
                    exg_run_stats* stats, const exg_run_opts* opts) {
   EXG_CUDA(cudaSetDevice(p_->device));
   if (s.n_stages < 1 || s.n_stages > EXG_MAX_STAGES) throw std::invalid_argument("schedule has no stages");
-  if (opts && opts->kv_page > 0) throw std::invalid_argument("paged KV: RRA on one GPU only (exegpt.h kv_page)");
+  if (opts && opts->kv_page > 0 && s.strategy == EXG_RRA)
+    throw std::invalid_argument("paged KV: RRA on one GPU or WAA (exegpt.h kv_page)");
   Layout* lay = get_layout(p_, s);
   if (s.strategy == EXG_RRA)
     run_rra_multi(p_, lay, s, reqs, n, out_tokens, out_latency, stats, opts);

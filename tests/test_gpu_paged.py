@@ -113,3 +113,61 @@ def test_paged_rejections(setup):
     with pytest.raises(X.ExgError) as ei:
         ctx.run(s, reqs[:4], kv_page=64)
     assert ei.value.status == 1
+
+
+# ----------------------------------------------- paged KV under WAA (multi) --
+# WAA's decoder GPUs page their KV; a row that finds no free page swaps the
+# latest-admitted row's pages to pinned host memory and back (swap
+# preemption), so paged WAA is bit-identical to slot WAA -- with or without
+# memory pressure, across decoder pipeline stages, TP ranks and rank threads.
+WAA_LAYOUTS = {
+    "enc1_dec1": (4, 12, 0, 1, [(0, 1, 0, 2), (1, 1, 0, 2)], 1, 0),
+    "dec_pp2_mb2": (4, 12, 6, 1, [(0, 1, 0, 2), (1, 1, 0, 1), (2, 1, 1, 2)], 1, 0),
+    "dec_tp2": (4, 12, 6, 1, [(0, 1, 0, 2), (1, 2, 0, 2)], 2, 2),
+}
+
+
+@pytest.fixture(scope="module")
+def multi(setup):
+    X, T, spec, W, reqs, ctx = setup
+    return X.Context(spec, 0xE6E0_00A1, cluster=X.cluster_spec(8))
+
+
+@pytest.mark.parametrize("name", list(WAA_LAYOUTS))
+def test_waa_paged_bit_identical(setup, long_reqs, multi, name):
+    X, T, spec, W, reqs, ctx = setup
+    from paper_2404_07947_b200 import _lib as L
+    lr, ora, base = long_reqs
+    b_e, b_d, b_m, n_enc, layout, t, c = WAA_LAYOUTS[name]
+    s = L.make_schedule(X.EXG_WAA_C, b_e, b_d, layout, b_m=b_m, n_enc_gpus=n_enc, tp_degree=t, tp_gpus=c)
+    ref_t, _, _, ref_l = multi.run(s, lr, dump=range(len(lr)))
+    if t == 1:   # no TP: WAA is bit-identical to the one-GPU run too
+        assert ref_t == base[0]
+    else:
+        compare_free_running("waa-" + name, ref_t, ref_l, ora, TOL, decoder_only_tf(W, lr), max_near_ties=2)
+    for pages, swaps in ((0, False), (16, True)):
+        toks, lat, st, lg = multi.run(s, lr, dump=range(len(lr)), kv_page=64, kv_pages=pages)
+        assert (st["kv_preemptions"] > 0) == swaps, (pages, st["kv_preemptions"])
+        if pages:
+            assert st["kv_pages_peak"] <= pages
+        assert toks == ref_t
+        for r in range(len(lr)):
+            assert np.array_equal(lg[r], ref_l[r]), (name, pages, r)
+
+
+def test_waa_paged_rank_threads_bit_identical(setup, long_reqs):
+    """Two rank threads (device-copy transport), paged decoder with swaps:
+    the same decisions on every rank, results equal to the one-rank run."""
+    X, T, spec, W, reqs, ctx = setup
+    from paper_2404_07947_b200 import _lib as L
+    lr, ora, base = long_reqs
+    s = L.make_schedule(X.EXG_WAA_C, 4, 12, [(0, 1, 0, 2), (1, 1, 0, 1), (2, 1, 1, 2)], b_m=6, n_enc_gpus=1)
+    group = X.local_group(spec, 0xE6E0_00A1, 2, X.cluster_spec(8))
+    res = X.run_group(group, s, lr, dump=range(len(lr)), kv_page=64, kv_pages=16)
+    toks, _, st, lg = res[0]
+    assert st["kv_preemptions"] > 0
+    assert toks == base[0]
+    for r in range(len(lr)):
+        assert np.array_equal(lg[r], base[3][r]), r
+    for g in group:
+        g.close()
