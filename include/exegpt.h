@@ -169,11 +169,15 @@ typedef struct {
    * its encoded positions at admission and one more each time its next
    * position crosses a page boundary; admission keeps one free page per
    * active row in reserve.  When a row needs a page and none is free, the
-   * most recently admitted active row is preempted: its pages are freed and
-   * it is re-admitted (before any new request) with its generated tokens
-   * appended to its input, re-encoded, and continues (vLLM's recompute
-   * preemption).  Decoder-only bf16 models, RRA on one GPU; other scopes
-   * return EXG_E_INPUT.  0 = slots. */
+   * most recently admitted active row is preempted.  RRA on one GPU:
+   * recompute -- its pages are freed and it is re-admitted (before any new
+   * request) with its generated tokens appended to its input, re-encoded, and
+   * continues.  WAA layouts (the decoder GPUs page; the encoder side keeps
+   * its per-batch slots): swap -- its pages are copied to pinned host memory
+   * and back into new pages once they fit (before any new handoff), so results
+   * are bit-identical to the slot cache; a handoff merges the longest prefix
+   * of the encoded batch whose pages fit.  Decoder-only bf16 models; other
+   * scopes (T5, fp32, multi-GPU RRA, EXG_STATIC) return EXG_E_INPUT.  0 = slots. */
   int32_t kv_page;
   int32_t kv_pages;
 } exg_run_opts;

@@ -491,9 +491,11 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
 }
 }  // namespace
 
-// L2 prefetch distance of the FMHA producer in items (exg_diag_fmha_prefetch)
+// L2 prefetch distance of the FMHA producer in items (exg_diag_fmha_prefetch);
+// off: measured slower at the task-S mix (tools/probe_kernels.py pmix_pf:
+// 280.6 us without, 294.9 / 310.2 / 311.3 us with 1 / 2 / 4 items ahead)
 int& fmha_prefetch_ahead() {
-  static int n = 2;
+  static int n = 0;
   return n;
 }
 

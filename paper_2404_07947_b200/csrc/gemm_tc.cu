@@ -47,7 +47,7 @@ PFN_encodeTiled_t encode_fn() {
 }
 
 // diagnostics only (exg_diag_gemm_flags): bit 0 = skip the MMAs, bit 6 = prefill on
-// the 1-CTA kernel instead of CTA pairs
+// the 1-CTA kernel instead of CTA pairs, bit 7 = no early stream-K fixup
 int& gemm_debug_flags() {
   static int f = 0;
   return f;
@@ -490,7 +490,61 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
       const uint32_t taddr = tmem + ((uint32_t)(q * 32) << 16) + a * BN;
       const bool row_ok = gm < M;
       float* pp = nullptr;
-      if (SWAP && ep.defer_out) {
+      // stream-K: a CTA that reaches a split tile after every other segment
+      // of it has landed (the usual case for a CTA's last unit: the tile's
+      // other segments opened the next CTAs' ranges) sums them with its own
+      // segment straight from TMEM -- in segment order, the fixup's
+      // arithmetic -- instead of storing its segment, counting in and
+      // reading it back
+      const bool fixup = !u.full && inkernel_fixup && !(SWAP && ep.defer_out);
+      bool early = false;
+      int* cnt = nullptr;
+      int nseg = 0;
+      if (fixup && !(g_dbg & 128)) {   // diagnostics bit 7: always count in (A/B)
+        const int64_t x0 = (int64_t)u.m * work.nkb;
+        nseg = sk_owner(work, x0 + work.nkb - 1) - sk_owner(work, x0) + 1;
+        cnt = counters + (u.n * work.tiles_m + u.m);
+        if (threadIdx.x == 128) {
+          int v;
+          asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+          *s_last = (v == nseg - 1);
+        }
+        epi_bar();
+        early = *s_last;
+        epi_bar();   // every thread has read s_last before it is written again
+      }
+      if (early) {
+        __threadfence();
+        const float* base = partial + ((int64_t)u.n * work.tiles_m + u.m) * work.max_segs * (int64_t)(BM * BN);
+        for (int c0 = c_lo; c0 < c_hi; c0 += 16) {
+          float own[16], acc[16];
+          tmem_ld16(taddr + c0, own);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+          for (int s0 = 0; s0 < nseg; s0 += 4) {
+            float v[4][16];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float* src = base + (int64_t)(s0 + q) * BM * BN + (int64_t)c0 * BM + r;
+              const bool other = s0 + q < nseg && s0 + q != u.seg;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) v[q][j] = other ? __ldcg(src + (int64_t)j * BM) : own[j];
+            }
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (s0 + q < nseg) acc[j] += v[q][j];
+          }
+          if (!row_ok) continue;
+          if (SWAP) {
+            if (u.n * BN + c0 < N) epi_store_col16(ep, u.n * BN + c0, gm, N, acc);
+          } else {
+            epi_store_row16(ep, gm, u.n * BN + c0, N, acc);
+          }
+        }
+        if (threadIdx.x == 128) *cnt = 0;
+      } else if (SWAP && ep.defer_out) {
         // deferred reduction: the raw segment, [seg][token][feature]
         // (a warp's 32 features of one token are one 128-byte line)
         float* dst = ep.defer_out + ((int64_t)u.seg * N) * M + gm;
@@ -530,11 +584,13 @@ __global__ void __launch_bounds__(EpiCfg<SWAP>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[a]);
       ++ui;
-      if (!u.full && inkernel_fixup && !(SWAP && ep.defer_out)) {
+      if (fixup && !early) {
         // stream-K fixup: the CTA completing the tile's last segment reduces
-        const int64_t x0 = (int64_t)u.m * work.nkb;
-        const int nseg = sk_owner(work, x0 + work.nkb - 1) - sk_owner(work, x0) + 1;
-        int* cnt = counters + (u.n * work.tiles_m + u.m);
+        if (g_dbg & 128) {
+          const int64_t x0 = (int64_t)u.m * work.nkb;
+          nseg = sk_owner(work, x0 + work.nkb - 1) - sk_owner(work, x0) + 1;
+          cnt = counters + (u.n * work.tiles_m + u.m);
+        }
         __threadfence();
         epi_bar();
         if (threadIdx.x == 128) *s_last = (atomicAdd(cnt, 1) == nseg - 1);

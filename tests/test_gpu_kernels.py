@@ -417,7 +417,8 @@ def test_decode_attention_paged_matches_slots(L, dh, P):
     tq, tslot, tnk = bf16_tensor(q), torch.from_numpy(slot).to(dev()), torch.from_numpy(n_keys).to(dev())
     part = torch.zeros(B * H * max_splits * (dh + 2), dtype=torch.float32, device=dev())
     out_s = torch.zeros((B, H * dh), dtype=torch.bfloat16, device=dev())
-    _run(L, "exg_op_decode_attention", ptr(tq), 3 * H * dh, ptr(bf16_tensor(K)), ptr(bf16_tensor(V)), ptr(tslot),
+    tK, tV = bf16_tensor(K), bf16_tensor(V)   # kept alive until the launches complete
+    _run(L, "exg_op_decode_attention", ptr(tq), 3 * H * dh, ptr(tK), ptr(tV), ptr(tslot),
          ptr(tnk), ptr(out_s), H * dh, B, H, dh, max_ctx, scale, split_len, max_splits, ptr(part), None, 0, 0,
          stream())
     Kp, tab, n_pages, maxp = _to_pages(K, n_keys, P, rng)
@@ -428,7 +429,8 @@ def test_decode_attention_paged_matches_slots(L, dh, P):
             Vp[tab[s, j], :, :w] = V[s, :, j * P:j * P + w]
     ttab = torch.from_numpy(tab).to(dev())
     out_p = torch.zeros_like(out_s)
-    _run(L, "exg_op_decode_attention_paged", ptr(tq), 3 * H * dh, ptr(bf16_tensor(Kp)), ptr(bf16_tensor(Vp)),
+    tKp, tVp = bf16_tensor(Kp), bf16_tensor(Vp)
+    _run(L, "exg_op_decode_attention_paged", ptr(tq), 3 * H * dh, ptr(tKp), ptr(tVp),
          ptr(tslot), ptr(tnk), ptr(out_p), H * dh, B, H, dh, P, scale, split_len, max_splits, ptr(part), None, 0, 0,
          ptr(ttab), maxp, stream())
     torch.cuda.synchronize()
@@ -466,7 +468,8 @@ def test_prefill_attention_paged_matches_slots(L, dh, P):
     tcu, tsl, tp0 = (torch.from_numpy(a).to(dev()) for a in (cu, slot, pos0))
     scale = float(np.float32(1 / math.sqrt(dh)))
     out_s = torch.zeros((T, H * dh), dtype=torch.bfloat16, device=dev())
-    _run(L, "exg_op_prefill_attention", ptr(tq), 3 * H * dh, ptr(bf16_tensor(K)), ptr(bf16_tensor(V)), ptr(tcu),
+    tK, tV = bf16_tensor(K), bf16_tensor(V)   # kept alive until the launches complete
+    _run(L, "exg_op_prefill_attention", ptr(tq), 3 * H * dh, ptr(tK), ptr(tV), ptr(tcu),
          ptr(tsl), ptr(tp0), R, max(lens), ptr(out_s), H * dh, H, dh, max_ctx, R, T, scale, 1, None, 0, 0, stream())
     Kp, tab, n_pages, maxp = _to_pages(K, lens, P, rng)
     Vp = np.zeros_like(Kp)
@@ -476,8 +479,22 @@ def test_prefill_attention_paged_matches_slots(L, dh, P):
             Vp[tab[s, j], :, :w] = V[s, :, j * P:j * P + w]
     ttab = torch.from_numpy(tab).to(dev())
     out_p = torch.zeros_like(out_s)
-    _run(L, "exg_op_prefill_attention_paged", ptr(tq), 3 * H * dh, ptr(bf16_tensor(Kp)), ptr(bf16_tensor(Vp)),
+    tKp, tVp = bf16_tensor(Kp), bf16_tensor(Vp)
+    _run(L, "exg_op_prefill_attention_paged", ptr(tq), 3 * H * dh, ptr(tKp), ptr(tVp),
          ptr(tcu), ptr(tsl), ptr(tp0), R, max(lens), ptr(out_p), H * dh, H, dh, P, n_pages, T, scale, 1, None, 0, 0,
          ptr(ttab), maxp, stream())
     torch.cuda.synchronize()
     assert torch.equal(out_s.cpu(), out_p.cpu())
+    # and against the fp64 definition on a few requests (causal)
+    got = to_np(out_p)
+    rel, ab = (2.0 ** -8, 2e-3) if dh != 128 else (2.0 ** -7, 4e-3)
+    for r in (0, 4, 9, 10):
+        for h in range(H):
+            qv = qkv[cu[r]:cu[r + 1], h * dh:(h + 1) * dh]
+            s_ = (qv @ K[r, h, :lens[r]].T) * scale
+            s_ = np.where(np.tril(np.ones_like(s_)) > 0, s_, -np.inf)
+            p_ = np.exp(s_ - s_.max(axis=1, keepdims=True))
+            p_ /= p_.sum(axis=1, keepdims=True)
+            ref = p_ @ V[r, h, :lens[r]]
+            g = got[cu[r]:cu[r + 1], h * dh:(h + 1) * dh]
+            assert np.all(np.abs(g - ref) <= rel * np.abs(ref) + ab), (r, h, np.abs(g - ref).max())

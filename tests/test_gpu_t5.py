@@ -51,7 +51,8 @@ def test_rmsnorm(L):
     g = bf16_round_np(1 + 0.1 * rng.standard_normal(d))
     y = torch.zeros((T, d), dtype=torch.bfloat16, device=dev())
     tx = torch.from_numpy(x).to(dev())
-    _run(L, "exg_op_rmsnorm", ptr(y), d, ptr(tx), d, ptr(bf16_tensor(g)), T, d, 1e-6, 1.0 / 32, stream())
+    tg = bf16_tensor(g)   # kept alive until the launch completes
+    _run(L, "exg_op_rmsnorm", ptr(y), d, ptr(tx), d, ptr(tg), T, d, 1e-6, 1.0 / 32, stream())
     torch.cuda.synchronize()
     x64 = x.astype(np.float64)
     ref = x64 / np.sqrt((x64 ** 2).mean(axis=1, keepdims=True) + 1e-6) * g / 32

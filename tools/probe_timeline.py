@@ -37,7 +37,7 @@ def run(T, N, K, mode=0):
         L.check(lib.exg_op_linear(X.data_ptr(), K, W.data_ptr(), T, N, K, mode, 0, None, out.data_ptr(), N, resid, N,
                                   1, ws.data_ptr(), nws, st()))
     fn()
-    lib.exg_diag_gemm_flags(4)
+    lib.exg_diag_gemm_flags(4 | int(os.environ.get("EXG_EXTRA_FLAGS", "0")))   # e.g. 128: no early fixup
     for rep in range(3):
         flush.sum()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
