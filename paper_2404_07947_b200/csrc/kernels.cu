@@ -193,7 +193,7 @@ static bool norm_reg(bf16* y, int64_t ldy, const float* x, int64_t ldx, const bf
 // preceding O-projection / FFN2, whose GEMM stored only its raw segments --
 // written back to x, then the LayerNorm of norm_reg_kernel on the updated row
 // (same arithmetic, bit-identical to the in-kernel fixup + LayerNorm).
-template <int NV>
+template <int NV, int MS = (NV <= 5 ? 6 : (NV <= 9 ? 3 : 1))>
 __global__ void __launch_bounds__(256) resid_reduce_ln_kernel(bf16* __restrict__ y, int64_t ldy, float* __restrict__ x,
                                                               int64_t ldx, const float* __restrict__ P, int tokens,
                                                               SegInfo si, const bf16* __restrict__ rbias,
@@ -207,16 +207,41 @@ __global__ void __launch_bounds__(256) resid_reduce_ln_kernel(bf16* __restrict__
   const int n4 = d >> 2;
   float4 v[NV];
   float s = 0.f;
+  // every segment load of this thread's NV chunks is issued before any sum
+  // (one memory round trip instead of NV x segments of them); the sums then
+  // run in segment order -- the fixup's arithmetic
+  constexpr int MAXS = MS;
+  const int64_t segstride4 = (int64_t)tokens * d / 4;
+  float4 pre[NV][MAXS], old[NV];
+  int nsk[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    const int i = threadIdx.x + k * 256;
+    nsk[k] = i < n4 ? seg_count(si, (4 * i) >> 7) : 0;
+    old[k] = i < n4 ? xr[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* p = reinterpret_cast<const float4*>(P + (int64_t)row * d + 4 * i);
+#pragma unroll
+    for (int sg = 0; sg < MAXS; ++sg)
+      pre[k][sg] = sg < nsk[k] ? __ldcg(p + sg * segstride4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     const int i = threadIdx.x + k * 256;
     if (i < n4) {
       const int f0 = 4 * i;
-      const int ns = seg_count(si, f0 >> 7);
+      const int ns = nsk[k];
       const float4* p = reinterpret_cast<const float4*>(P + (int64_t)row * d + f0);
-      const int64_t segstride4 = (int64_t)tokens * d / 4;
-      float4 acc = __ldcg(p);
-      for (int sg = 1; sg < ns; ++sg) {
+      float4 acc = pre[k][0];
+#pragma unroll
+      for (int sg = 1; sg < MAXS; ++sg) {
+        if (sg < ns) {
+          acc.x += pre[k][sg].x;
+          acc.y += pre[k][sg].y;
+          acc.z += pre[k][sg].z;
+          acc.w += pre[k][sg].w;
+        }
+      }
+      for (int sg = MAXS; sg < ns; ++sg) {   // rare: more segments than preloaded
         const float4 q = __ldcg(p + sg * segstride4);
         acc.x += q.x;
         acc.y += q.y;
@@ -232,8 +257,7 @@ __global__ void __launch_bounds__(256) resid_reduce_ln_kernel(bf16* __restrict__
         acc.z += b23.x;
         acc.w += b23.y;
       }
-      const float4 old = xr[i];
-      v[k] = make_float4(old.x + acc.x, old.y + acc.y, old.z + acc.z, old.w + acc.w);
+      v[k] = make_float4(old[k].x + acc.x, old[k].y + acc.y, old[k].z + acc.z, old[k].w + acc.w);
       xr[i] = v[k];
     } else {
       v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -272,6 +296,12 @@ __global__ void __launch_bounds__(256) resid_reduce_ln_kernel(bf16* __restrict__
   }
 }
 
+// diagnostics (exg_diag_ln_preload): 0 = preload only the first segment (A/B)
+int& ln_preload_segments() {
+  static int on = 1;
+  return on;
+}
+
 bool layernorm_deferred(bf16* y, int64_t ldy, float* x, int64_t ldx, const float* P, const SegInfo& si,
                         const bf16* rbias, const bf16* g, const bf16* b, int T, int d, float eps, cudaStream_t st) {
   if ((d & 3) || (ldx & 3) || (ldy & 3) || d > 16384) return false;
@@ -284,7 +314,8 @@ bool layernorm_deferred(bf16* y, int64_t ldy, float* x, int64_t ldx, const float
   if (nv <= 1) go(resid_reduce_ln_kernel<1>);
   else if (nv <= 2) go(resid_reduce_ln_kernel<2>);
   else if (nv <= 4) go(resid_reduce_ln_kernel<4>);
-  else if (nv <= 5) go(resid_reduce_ln_kernel<5>);
+  else if (nv <= 5 && ln_preload_segments()) go(resid_reduce_ln_kernel<5>);
+  else if (nv <= 5) go(resid_reduce_ln_kernel<5, 1>);
   else if (nv <= 8) go(resid_reduce_ln_kernel<8>);
   else if (nv <= 9) go(resid_reduce_ln_kernel<9>);
   else if (nv <= 12) go(resid_reduce_ln_kernel<12>);
@@ -872,3 +903,4 @@ void argmax_rows(int32_t* out, const float* logits, int64_t ld, int B, int V, in
 extern "C" void exg_diag_decode_stages(int s) { exg::decode_stages_override() = s; }
 extern "C" void exg_diag_decode_split(int s) { exg::decode_split_override() = s >= 128 ? s : 0; }
 extern "C" void exg_diag_decode_merge(int force_combine) { exg::decode_force_combine() = force_combine; }
+extern "C" void exg_diag_ln_preload(int on) { exg::ln_preload_segments() = on; }
