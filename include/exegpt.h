@@ -211,7 +211,7 @@ typedef struct {
   double enc_stage_mean_s, enc_stage_p99dev_s, dec_stage_mean_s, dec_stage_p99dev_s;
   double mean_encode_batch;            /* requests per encode phase (admissions)  */
   int64_t trace_records;               /* records written to exg_run_opts.trace_out */
-  int64_t kv_preemptions;              /* paged KV: rows preempted (recomputed)    */
+  int64_t kv_preemptions;              /* paged KV: rows preempted (recompute / swap) */
   int64_t kv_pages_peak;               /* paged KV: most pages in use at once      */
 } exg_run_stats;
 

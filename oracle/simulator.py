@@ -321,7 +321,18 @@ class Simulator:
         self.s_e = seqdist.pmf_mean(self.pmf_in)
         self.s_d = seqdist.pmf_mean(self.pmf_out)
         self.max_in, self.max_out = len(self.pmf_in), len(self.pmf_out)
-        self.ctx_mean = self.s_e + self.s_d / 2.0          # S5 decode-attention context
+        # decode-attention context of a row at a decode iteration (DESIGN.md
+        # reading, round 2; S5 used S_E + S_D/2): rows stay in the batch for
+        # S iterations, so an iteration sees a request with probability
+        # proportional to S and at a uniform age u = 1..S (renewal-reward) --
+        # the row-iteration mean of u is E[S(S+1)] / (2 E[S]); keys = n - 1 + u
+        # (decoder-only: n - 1 encoded positions + u decoded) or n cross + u
+        # self keys (T5, the profile's total at c = self + cross)
+        m2o_ = 0.0
+        for k in range(1, len(self.pmf_out) + 1):
+            m2o_ += float(k) * float(k) * float(self.pmf_out[k - 1])
+        self.age_mean = (m2o_ + self.s_d) / (2.0 * self.s_d)
+        self.ctx_mean = self.s_e + self.age_mean - (0.0 if model.arch == "t5" else 1.0)
         # encode-attention lookup length: the RMS input length (a request's
         # attention cost grows as n^2; DESIGN.md reading)
         m2 = 0.0
@@ -345,10 +356,7 @@ class Simulator:
         # absorbed by the runner's preemption.
         self.kv_ctx_dec = float(self.max_in + self.max_out)
         if cluster.kv_page > 0 and model.arch != "t5":
-            m2o = 0.0
-            for k in range(1, len(self.pmf_out) + 1):
-                m2o += float(k) * float(k) * float(self.pmf_out[k - 1])
-            live = self.s_e - 1.0 + (m2o + self.s_d) / (2.0 * self.s_d)
+            live = self.s_e - 1.0 + self.age_mean
             self.kv_ctx_dec = min(live + 1.5 * float(cluster.kv_page), float(self.max_in + self.max_out))
         self.k_dec = 3 if model.arch == "t5" else 2
         self._pu_cache: Dict[int, Tuple[List[float], float]] = {}

@@ -292,7 +292,14 @@ Simulator::Simulator(const Profile& p_, const exg_model_spec& m_, const exg_clus
   s_d = pmf_mean(pmf_out);
   max_in = (int)pmf_in.size();
   max_out = (int)pmf_out.size();
-  ctx_mean = s_e + s_d / 2.0;
+  // decode-attention context: the row-iteration mean age E[S(S+1)] / (2 E[S])
+  // on top of the input (oracle/simulator.py ctx_mean)
+  {
+    double m2o = 0.0;
+    for (size_t k = 1; k <= pmf_out.size(); ++k) m2o += (double)k * (double)k * pmf_out[k - 1];
+    age_mean = (m2o + s_d) / (2.0 * s_d);
+  }
+  ctx_mean = s_e + age_mean - (m.arch == EXG_ARCH_T5 ? 0.0 : 1.0);
   // RMS input length: the encode-attention lookup length (its per-request
   // cost grows as n^2, so b requests of this length cost sum_i n_i^2)
   {
@@ -309,9 +316,7 @@ Simulator::Simulator(const Profile& p_, const exg_model_spec& m_, const exg_clus
   // positions S_E - 1 + E[S(S+1)] / (2 E[S]) plus 3P/2
   kv_ctx_dec = (double)(max_in + max_out);
   if (cl.kv_page > 0 && m.arch != EXG_ARCH_T5) {
-    double m2o = 0.0;
-    for (size_t k = 1; k <= pmf_out.size(); ++k) m2o += (double)k * (double)k * pmf_out[k - 1];
-    const double live = s_e - 1.0 + (m2o + s_d) / (2.0 * s_d);
+    const double live = s_e - 1.0 + age_mean;
     kv_ctx_dec = std::min(live + 1.5 * (double)cl.kv_page, (double)(max_in + max_out));
   }
 }

@@ -92,7 +92,7 @@ class Simulator {
   exg_cluster_spec cl;
   std::vector<double> pmf_in, pmf_out;
   int target_len;
-  double s_e, s_d, ctx_mean, s_e_rms, s_e_sd;
+  double s_e, s_d, ctx_mean, s_e_rms, s_e_sd, age_mean;
   double kv_ctx_dec;   // decoder KV positions charged per row (slots, or the paged live average)
   int max_in, max_out, n_layers, k_dec;
   bool use_little;

@@ -455,3 +455,41 @@ def test_paged_schedule_find_bit_identical(L, tmp_path, task, model, n_gpus, mas
                                                                S0.kv_ctx_dec))
         b_paged = max(b for b in range(1, 400) if S.mem_ok(S.rra_schedule(1, 1, 1, 0).stages, b, S.kv_ctx_dec))
         assert b_paged > 2 * b_slots
+
+
+@pytest.mark.parametrize("model,task", [("opt-13b", "S"), ("t5-11b", "T")])
+def test_decode_context_pin(model, task):
+    """The simulator's decode-attention context (ctx_mean, DESIGN.md reading):
+    the keys a row holds, averaged over decode row-iterations -- brute force
+    over the two PMFs from the definition (decoder-only: n - 1 + u keys at
+    decode iteration u = 1..S; T5: n cross + u self keys), and a renewal
+    check: a refilled batch's time-average converges to it."""
+    from oracle import simulator as sim
+    from workload import MODELS, task_dists
+    d = task_dists(task)
+    m = sim.SimModel.from_spec(MODELS[model])
+    S = sim.Simulator(None, m, sim.SimCluster(1, 180e9, 4e9), d.pmf_in, d.pmf_out, d.target_len)
+    pin, pout = np.asarray(d.pmf_in), np.asarray(d.pmf_out)
+    off = 0 if model.startswith("t5") else -1
+    num = den = 0.0
+    for n in range(1, len(pin) + 1):
+        for So in range(1, len(pout) + 1):
+            w = pin[n - 1] * pout[So - 1]
+            if w:
+                num += w * sum(n + off + u for u in range(1, So + 1))
+                den += w * So
+    assert S.ctx_mean == pytest.approx(num / den, rel=1e-12)
+    rng = np.random.default_rng(11)
+    cin, cout = np.cumsum(pin), np.cumsum(pout)
+    draw = lambda c: int(np.searchsorted(c, rng.random() * c[-1])) + 1
+    rows = [[draw(cin), draw(cout), 1] for _ in range(64)]
+    tot = cnt = 0
+    for it in range(3000):
+        for r in rows:
+            if it >= 600:
+                tot += r[0] + off + r[2]
+                cnt += 1
+            r[2] += 1
+            if r[2] > r[1]:
+                r[:] = [draw(cin), draw(cout), 1]
+    assert tot / cnt == pytest.approx(S.ctx_mean, rel=0.02)
