@@ -172,12 +172,14 @@ typedef struct {
    * most recently admitted active row is preempted.  RRA on one GPU:
    * recompute -- its pages are freed and it is re-admitted (before any new
    * request) with its generated tokens appended to its input, re-encoded, and
-   * continues.  WAA layouts (the decoder GPUs page; the encoder side keeps
-   * its per-batch slots): swap -- its pages are copied to pinned host memory
-   * and back into new pages once they fit (before any new handoff), so results
-   * are bit-identical to the slot cache; a handoff merges the longest prefix
+   * continues.  Multi-GPU layouts (RRA pipelines / TP groups: every stage
+   * pages with the same page ids; WAA: the decoder GPUs page, the encoder side
+   * keeps its per-batch slots): swap -- every rank copies the row's pages of
+   * the layers it holds to pinned host memory and back into new pages once
+   * they fit (before any new admission / handoff), so results are
+   * bit-identical to the slot cache; a WAA handoff merges the longest prefix
    * of the encoded batch whose pages fit.  Decoder-only bf16 models; other
-   * scopes (T5, fp32, multi-GPU RRA, EXG_STATIC) return EXG_E_INPUT.  0 = slots. */
+   * scopes (T5, fp32, EXG_STATIC) return EXG_E_INPUT.  0 = slots. */
   int32_t kv_page;
   int32_t kv_pages;
 } exg_run_opts;

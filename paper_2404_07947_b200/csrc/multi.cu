@@ -668,7 +668,8 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
   const int drop = R.ed ? 0 : 1;   // T6: decoder-only encodes positions 0..n-2, T5 all n tokens
   int T = 0, maxlen = 0;
   for (int j = 0; j < k; ++j) T += R.reqs[r0 + j].input_len - drop;
-  tb.ensure((size_t)3 * T + 3 * (k + 1) + 8);
+  const size_t pgi = R.P > 0 ? (size_t)2 * T + (size_t)k * R.maxp : 0;   // paged: page / offset per token, page table
+  tb.ensure((size_t)3 * T + 3 * (k + 1) + pgi + 8);
   int32_t* h = tb.begin();
   int32_t *ids = h, *pos = ids + T, *tsl = pos + T, *cu = tsl + T, *rsl = cu + k + 1, *p0 = rsl + k;
   int t = 0;
@@ -689,7 +690,24 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
     eb.attn_pairs += R.ed ? m * m : m * (m + 1) / 2;
     if (last_ids) last_ids->push_back(R.ed ? 0 : q.input_ids[q.input_len - 1]);   // T5: decoder start token
   }
-  tb.upload((size_t)3 * T + (k + 1) + 2 * k, st);
+  if (pgi) {
+    int32_t *kvb = p0 + k, *kvo = kvb + T, *ptab = kvo + T;
+    int t2 = 0;
+    for (int j = 0; j < k; ++j) {
+      const auto& pg = R.slot_pages[slots[j]];
+      for (int p = 0; p < R.reqs[r0 + j].input_len - drop; ++p, ++t2) {
+        kvb[t2] = pg[p / R.P];
+        kvo[t2] = p % R.P;
+      }
+      for (int q = 0; q < R.maxp; ++q) ptab[(int64_t)j * R.maxp + q] = pg[q < (int)pg.size() ? q : 0];
+    }
+  }
+  tb.upload((size_t)3 * T + (k + 1) + 2 * k + pgi, st);
+  if (pgi) {
+    eb.kv_blk = tb.dev + 3 * T + (k + 1) + 2 * k;
+    eb.kv_off = eb.kv_blk + T;
+    eb.kv = KvMap{eb.kv_off + T, R.maxp};
+  }
   eb.T = T;
   eb.R = k;
   eb.max_len = maxlen;
@@ -944,6 +962,137 @@ void finish(const Exec& X, RunState& R, Stage& head_stage, int32_t* out_tokens, 
 // RRA over P pipeline stages with partial TP (S6: encode in
 // P micro-batches, decode in P micro-batches)
 // ---------------------------------------------------------------------------
+// Paged decoder KV of a multi-GPU executor (exegpt.h kv_page):
+// every rank runs the same host loop, so the page decisions are identical on
+// all ranks and each rank applies them to its own engines.  Pages are
+// allocated as rows grow (one page per active row kept in reserve at
+// admission); a row that finds no free page swaps the latest-admitted row's
+// pages -- the K/V of every layer this rank holds -- to pinned host memory and
+// back into new pages once they fit (swap preemption: the K/V return
+// unchanged, so paged results are bit-identical to slots).
+struct Pager {
+  RunState& R;
+  std::vector<std::unique_ptr<Stage>>& stages;   // the engines holding the paged KV
+  int P = 0, n_pages = 0, dh = 0;
+  std::vector<int> free_pages;
+  struct Swapped {
+    Row row;
+    void* host;
+    int npg;
+  };
+  std::vector<Swapped> swapped;   // sorted by request index (arrival order)
+  std::vector<void*> host_bufs;   // freed once the stream has drained
+
+  Pager(RunState& R_, std::vector<std::unique_ptr<Stage>>& st, const exg_run_opts* opts, int slot_ctx, int B_D,
+        int dh_)
+      : R(R_), stages(st), dh(dh_) {
+    P = opts ? opts->kv_page : 0;
+    if (P <= 0) {
+      P = 0;
+      return;
+    }
+    if (R.ed) throw std::invalid_argument("paged KV: decoder-only models");
+    if (P % 64 != 0 || 512 % P != 0) throw std::invalid_argument("kv_page must be a multiple of 64 dividing 512");
+    if (opts->kv_pages < 0) throw std::invalid_argument("kv_pages < 0");
+    R.P = P;
+    R.maxp = (slot_ctx + P - 1) / P;
+    n_pages = opts->kv_pages > 0 ? opts->kv_pages : B_D * R.maxp;
+    if (n_pages < R.maxp + 1) throw std::invalid_argument("kv_pages below one request's pages + 1");
+    R.slot_pages.assign(B_D, {});
+    for (int i = n_pages - 1; i >= 0; --i) free_pages.push_back(i);
+  }
+  ~Pager() {
+    if (!host_bufs.empty()) cudaStreamSynchronize(R.st);
+    for (void* hb : host_bufs)
+      if (hb) cudaFreeHost(hb);
+  }
+  bool on() const { return P > 0; }
+  int pages_for(int keys) const { return (keys + P - 1) / P; }
+  void note_peak() {
+    R.pages_peak = std::max<int64_t>(R.pages_peak, (int64_t)n_pages - (int64_t)free_pages.size());
+  }
+  void take(int slot, int npg) {
+    auto& pg = R.slot_pages[slot];
+    for (int j = 0; j < npg; ++j) {
+      pg.push_back(free_pages.back());
+      free_pages.pop_back();
+    }
+    note_peak();
+  }
+  // this rank's K / V blocks of the given pages, in a fixed order (stage, TP
+  // rank, layer, K|V, page)
+  void for_each_block(const std::vector<int>& pages, const std::function<void(bf16*, size_t)>& fn) {
+    for (auto& ds : stages)
+      for (auto& e : ds->eng)
+        if (e) {
+          const size_t blk = (size_t)e->dims().Hl * P * dh;
+          for (int l = 0; l < e->n_layers(); ++l)
+            for (int kv = 0; kv < 2; ++kv)
+              for (int pg : pages) fn((kv ? e->vc(l) : e->kc(l)) + (size_t)pg * blk, blk * sizeof(bf16));
+        }
+  }
+  void swap_out(std::vector<Row>& active, size_t v) {
+    const Row vr = active[v];
+    auto& pg = R.slot_pages[vr.slot];
+    size_t bytes = 0;
+    for_each_block(pg, [&](bf16*, size_t b) { bytes += b; });
+    void* hb = nullptr;
+    if (bytes) EXG_CUDA(cudaMallocHost(&hb, bytes));
+    host_bufs.push_back(hb);
+    size_t off = 0;
+    for_each_block(pg, [&](bf16* dptr, size_t b) {
+      EXG_CUDA(cudaMemcpyAsync(static_cast<char*>(hb) + off, dptr, b, cudaMemcpyDeviceToHost, R.st));
+      off += b;
+    });
+    const Swapped sw{vr, hb, (int)pg.size()};
+    for (int x : pg) free_pages.push_back(x);   // reused only by later work on this stream
+    pg.clear();
+    swapped.insert(std::upper_bound(swapped.begin(), swapped.end(), sw,
+                                    [](const Swapped& a, const Swapped& b) { return a.row.req < b.row.req; }),
+                   sw);
+    active.erase(active.begin() + v);   // the row keeps its slot (and last_tok[slot])
+    ++R.preemptions;
+  }
+  // swapped-out rows come back first, each when its pages fit with one page
+  // per active row in reserve
+  void swap_in_ready(std::vector<Row>& active) {
+    while (on() && !swapped.empty() &&
+           (int64_t)free_pages.size() - swapped.front().npg >= (int64_t)active.size() + 1) {
+      const Swapped sw = swapped.front();
+      swapped.erase(swapped.begin());
+      take(sw.row.slot, sw.npg);
+      size_t off = 0;
+      for_each_block(R.slot_pages[sw.row.slot], [&](bf16* dptr, size_t b) {
+        EXG_CUDA(cudaMemcpyAsync(dptr, static_cast<char*>(sw.host) + off, b, cudaMemcpyHostToDevice, R.st));
+        off += b;
+      });
+      active.push_back(sw.row);
+    }
+  }
+  // every row writes key `pos` this iteration: a new page when it crosses
+  // into one; none free -> swap out the latest-admitted row
+  void grow(std::vector<Row>& active) {
+    if (!on()) return;
+    for (size_t i = 0; i < active.size();) {
+      const int slot = active[i].slot, pos = active[i].pos;
+      if (pos / P < (int)R.slot_pages[slot].size()) {
+        ++i;
+        continue;
+      }
+      if (free_pages.empty()) {
+        size_t v = 0;
+        for (size_t j = 1; j < active.size(); ++j)
+          if (active[j].seq > active[v].seq) v = j;
+        swap_out(active, v);
+        if (v < i) --i;
+        continue;
+      }
+      take(slot, 1);
+      ++i;
+    }
+  }
+};
+
 static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s, const exg_request* reqs, int n,
                           int32_t* out_tokens, double* out_latency, exg_run_stats* stats, const exg_run_opts* opts) {
   auto& pipe = lay->dec;
@@ -961,10 +1110,15 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   const int B_D = s.b_d, B_E = s.b_e, P = (int)pipe.size();
   if (B_E < 1 || B_D < B_E || s.n_d < 1) throw std::invalid_argument("RRA needs 1 <= B_E <= B_D, N_D >= 1");
   const int drop = R.ed ? 0 : 1;
+  // paged KV on every stage (Pager: swap preemption across the pipeline)
+  Pager pgr(R, pipe, opts, slot_ctx, B_D, p->spec.d_head);
   for (auto& st : pipe)
     for (auto& e : st->eng)
       if (e) {
-        e->ensure_kv(B_D, slot_ctx, -1, R.ed ? R.max_in : 0);
+        if (pgr.on())
+          e->ensure_kv(std::max(pgr.n_pages, B_D), pgr.P, -1, 0);
+        else
+          e->ensure_kv(B_D, slot_ctx, -1, R.ed ? R.max_in : 0);
         e->ensure_workspace(std::max(1, B_E * (R.max_in - drop)), B_D);
       }
   const bool first_mine = X.mine(pipe.front()->gpu(0)), head_mine = X.mine(pipe.back()->gpu(0));
@@ -976,9 +1130,24 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   R.admit_ev.assign(n, -1);
   R.done_ev.assign(n, -1);
   int next_req = 0, ti = 0;
+  int64_t admit_seq = 0;
   R.record(first_mine);
-  while (next_req < n || !active.empty()) {
-    const int admit = std::min({B_E, B_D - (int)active.size(), n - next_req});
+  while (next_req < n || !active.empty() || !pgr.swapped.empty()) {
+    // paged: swapped-out rows first; new rows only while none is swapped out
+    // and their pages fit with one page per active row in reserve
+    pgr.swap_in_ready(active);
+    int admit = std::min({B_E, B_D - (int)active.size() - (int)pgr.swapped.size(), n - next_req});
+    if (pgr.on()) {
+      int64_t fr = (int64_t)pgr.free_pages.size();
+      int k = 0;
+      while (pgr.swapped.empty() && k < admit) {
+        const int need = pgr.pages_for(reqs[next_req + k].input_len);   // positions 0 .. n-1
+        if (fr - need < (int64_t)active.size() + k + 1) break;
+        fr -= need;
+        ++k;
+      }
+      admit = k;
+    }
     const int ev_phase = R.record(first_mine);
     if (admit > 0) R.enc_start_ev.push_back(ev_phase);
     if (admit > 0) {
@@ -987,7 +1156,8 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         slots[k] = free_slots.back();
         free_slots.pop_back();
         const exg_request& q = reqs[next_req + k];
-        active.push_back(Row{next_req + k, slots[k], R.ed ? 0 : q.input_len - 1, 0});
+        if (pgr.on()) pgr.take(slots[k], pgr.pages_for(q.input_len));
+        active.push_back(Row{next_req + k, slots[k], R.ed ? 0 : q.input_len - 1, 0, admit_seq++});
         R.admit_ev[next_req + k] = ev_phase;
       }
       for (const auto& mb : chunks(admit, P)) {
@@ -1025,7 +1195,9 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       ++R.encode_phases;
       R.enc_end_ev.push_back(R.record(head_mine));
     }
-    for (int u = 0; u < s.n_d && !active.empty(); ++u) {
+    for (int u = 0; u < s.n_d; ++u) {
+      pgr.grow(active);
+      if (active.empty()) break;
       decode_pipeline(X, R, pipe, tabs, ti, active, P, d, dump);
       return_tokens(X, pipe, B_D);
       const int ev = R.record(head_mine);
@@ -1033,7 +1205,7 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       R.iter_tokens.push_back((int64_t)active.size());
       ++R.decode_iters;
       R.batch_sum += (int64_t)active.size();
-      retire(R, active, free_slots, ev);
+      retire(R, active, free_slots, ev, pgr.on() ? &pgr.free_pages : nullptr);
     }
   }
   finish(X, R, *pipe.back(), out_tokens, out_latency, stats);
@@ -1066,23 +1238,11 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   if (B_E < 1 || B_D < B_E) throw std::invalid_argument("WAA needs 1 <= B_E <= B_D");
   const int M = s.b_m > 0 ? std::max(1, (B_D + s.b_m - 1) / s.b_m) : 1;
   // paged decoder KV (exegpt.h kv_page; "the addition of vLLM's
-  // paging mechanism can further enhance WAA's performance"): pages as on one
-  // GPU (runner.cu); a row that finds no free page swaps the latest-admitted
-  // row's pages out to pinned host memory and back in when pages free up
-  // (swap preemption: the K/V return unchanged, so results stay bit-identical)
-  const int P = opts ? opts->kv_page : 0;
-  const bool paged = P > 0;
-  int n_pages = 0;
-  if (paged) {
-    if (R.ed) throw std::invalid_argument("paged KV: decoder-only models");
-    if (P % 64 != 0 || 512 % P != 0) throw std::invalid_argument("kv_page must be a multiple of 64 dividing 512");
-    if (opts->kv_pages < 0) throw std::invalid_argument("kv_pages < 0");
-    R.P = P;
-    R.maxp = (slot_ctx + P - 1) / P;
-    n_pages = opts->kv_pages > 0 ? opts->kv_pages : B_D * R.maxp;
-    if (n_pages < R.maxp + 1) throw std::invalid_argument("kv_pages below one request's pages + 1");
-    R.slot_pages.assign(B_D, {});
-  }
+  // paging mechanism can further enhance WAA's performance"): the decoder
+  // GPUs page, the encoder side keeps its per-batch slots (Pager)
+  Pager pgr(R, dec, opts, slot_ctx, B_D, dh);
+  const bool paged = pgr.on();
+  const int P = pgr.P;
   const int enc_ctx = std::max(1, R.max_in);
   const int drop = R.ed ? 0 : 1;
   const double dyn = opts ? opts->dyn_threshold : 0.0;
@@ -1107,7 +1267,7 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
     for (auto& e : st->eng)
       if (e) {
         if (paged)
-          e->ensure_kv(std::max(n_pages, B_D), P, -1, 0);
+          e->ensure_kv(std::max(pgr.n_pages, B_D), P, -1, 0);
         else
           e->ensure_kv(B_D, slot_ctx, -1, R.ed ? R.max_in : 0);
         e->ensure_workspace(1, B_D);
@@ -1136,74 +1296,10 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   std::vector<Row> active;
   R.admit_ev.assign(n, -1);
   R.done_ev.assign(n, -1);
-  // paged KV state: free pages, swapped-out rows (sorted by request index),
-  // their pinned host images (freed after the run)
-  std::vector<int> free_pages;
-  for (int i = n_pages - 1; i >= 0; --i) free_pages.push_back(i);
-  struct Swapped {
-    Row row;
-    void* host;
-    int npg;
-  };
-  std::vector<Swapped> swapped;
-  std::vector<void*> host_bufs;
   int64_t admit_seq = 0;
-  auto note_peak = [&] {
-    R.pages_peak = std::max<int64_t>(R.pages_peak, (int64_t)n_pages - (int64_t)free_pages.size());
-  };
-  // this rank's decoder K / V blocks of the given pages, in a fixed order
-  // (stage, TP rank, layer, K|V, page): fn(device block, bytes)
-  auto for_each_block = [&](const std::vector<int>& pages, const std::function<void(bf16*, size_t)>& fn) {
-    for (auto& ds : dec)
-      for (auto& e : ds->eng)
-        if (e) {
-          const size_t blk = (size_t)e->dims().Hl * P * dh;
-          for (int l = 0; l < e->n_layers(); ++l)
-            for (int kv = 0; kv < 2; ++kv)
-              for (int pg : pages) fn((kv ? e->vc(l) : e->kc(l)) + (size_t)pg * blk, blk * sizeof(bf16));
-        }
-  };
-  auto swap_out = [&](size_t v) {
-    const Row vr = active[v];
-    auto& pg = R.slot_pages[vr.slot];
-    size_t bytes = 0;
-    for_each_block(pg, [&](bf16*, size_t b) { bytes += b; });
-    void* hb = nullptr;
-    if (bytes) EXG_CUDA(cudaMallocHost(&hb, bytes));
-    host_bufs.push_back(hb);
-    size_t off = 0;
-    for_each_block(pg, [&](bf16* dptr, size_t b) {
-      EXG_CUDA(cudaMemcpyAsync(static_cast<char*>(hb) + off, dptr, b, cudaMemcpyDeviceToHost, R.st));
-      off += b;
-    });
-    const Swapped sw{vr, hb, (int)pg.size()};
-    for (int x : pg) free_pages.push_back(x);   // reused only by later work on this stream
-    pg.clear();
-    swapped.insert(std::upper_bound(swapped.begin(), swapped.end(), sw,
-                                    [](const Swapped& a, const Swapped& b) { return a.row.req < b.row.req; }),
-                   sw);
-    active.erase(active.begin() + v);   // the row keeps its slot (and last_tok[slot])
-    ++R.preemptions;
-  };
-  auto swap_in = [&]() {
-    const Swapped sw = swapped.front();
-    swapped.erase(swapped.begin());
-    auto& pg = R.slot_pages[sw.row.slot];
-    for (int j = 0; j < sw.npg; ++j) {
-      pg.push_back(free_pages.back());
-      free_pages.pop_back();
-    }
-    size_t off = 0;
-    for_each_block(pg, [&](bf16* dptr, size_t b) {
-      EXG_CUDA(cudaMemcpyAsync(dptr, static_cast<char*>(sw.host) + off, b, cudaMemcpyHostToDevice, R.st));
-      off += b;
-    });
-    active.push_back(sw.row);
-    note_peak();
-  };
   int next_req = 0, pend_r0 = -1, pend_k = 0, pend_s0 = 0, pend_ev = -1, ti = 0;
   R.record(first_mine);
-  while (next_req < n || pend_k > 0 || !active.empty() || !swapped.empty()) {
+  while (next_req < n || pend_k > 0 || !active.empty() || !pgr.swapped.empty()) {
     // encoder: keep one encoded batch ready (encoder slots 0..k-1)
     if (pend_k == 0 && next_req < n) {
       int k = std::min(B_E, n - next_req);
@@ -1251,17 +1347,15 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
     }
     // paged: swapped-out rows come back first, each when its pages fit with
     // one page per active row in reserve
-    while (paged && !swapped.empty() &&
-           (int64_t)free_pages.size() - swapped.front().npg >= (int64_t)active.size() + 1)
-      swap_in();
+    pgr.swap_in_ready(active);
     // handoff + merge at an iteration boundary when the decoder has room
     // (paged: no row swapped out; the longest prefix of the encoded batch
     // whose pages fit with the reserve -- the rest stays pending)
     int hk = pend_k;
     if (paged && pend_k > 0) {
       hk = 0;
-      int64_t fr = (int64_t)free_pages.size();
-      while (swapped.empty() && hk < pend_k && hk < (int)free_slots.size()) {
+      int64_t fr = (int64_t)pgr.free_pages.size();
+      while (pgr.swapped.empty() && hk < pend_k && hk < (int)free_slots.size()) {
         const int need = (reqs[pend_r0 + hk].input_len + P - 1) / P;   // positions 0 .. n-1
         if (fr - need < (int64_t)active.size() + hk + 1) break;
         fr -= need;
@@ -1284,16 +1378,12 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         int32_t* hp = tp.begin();
         for (int j = 0; j < hk; ++j) {
           const int slot = free_slots[free_slots.size() - 1 - j];
-          auto& pg = R.slot_pages[slot];
-          for (int q = 0; q < (reqs[pend_r0 + j].input_len + P - 1) / P; ++q) {
-            pg.push_back(free_pages.back());
-            free_pages.pop_back();
-          }
+          pgr.take(slot, pgr.pages_for(reqs[pend_r0 + j].input_len));
+          const auto& pg = R.slot_pages[slot];
           for (int q = 0; q < R.maxp; ++q) hp[(int64_t)j * R.maxp + q] = pg[q < (int)pg.size() ? q : 0];
         }
         tp.upload((size_t)hk * R.maxp, R.st);
         dpt = tp.dev;
-        note_peak();
       }
       for (int j = 0; j < hk; ++j) {
         dslots[j] = free_slots.back();
@@ -1403,30 +1493,7 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       pend_s0 += hk;
       pend_k -= hk;
     }
-    if (paged) {
-      // every row writes key `pos` this iteration: a new page when it crosses
-      // into one; none free -> swap out the latest-admitted row
-      for (size_t i = 0; i < active.size();) {
-        const int slot = active[i].slot, pos = active[i].pos;
-        auto& pg = R.slot_pages[slot];
-        if (pos / P < (int)pg.size()) {
-          ++i;
-          continue;
-        }
-        if (free_pages.empty()) {
-          size_t v = 0;
-          for (size_t j = 1; j < active.size(); ++j)
-            if (active[j].seq > active[v].seq) v = j;
-          swap_out(v);
-          if (v < i) --i;
-          continue;
-        }
-        pg.push_back(free_pages.back());
-        free_pages.pop_back();
-        ++i;
-      }
-      note_peak();
-    }
+    pgr.grow(active);
     if (active.empty()) continue;
     decode_pipeline(X, R, dec, tabs, ti, active, M, d, dump);
     return_tokens(X, dec, B_D);
@@ -1439,12 +1506,10 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       steady_batch_sum += (double)active.size();
       ++steady_iters;
     }
-    retire(R, active, free_slots, ev, paged ? &free_pages : nullptr);
+    retire(R, active, free_slots, ev, paged ? &pgr.free_pages : nullptr);
   }
   finish(X, R, *dec.back(), out_tokens, out_latency, stats);
   EXG_CUDA(cudaStreamSynchronize(R.st));
-  for (void* hb : host_bufs)
-    if (hb) cudaFreeHost(hb);
   if (stage_buf) cudaFree(stage_buf);
   for (int i = 0; i < HR; ++i) {
     cudaFree(d_hrows[i]);
@@ -1569,8 +1634,6 @@ void MultiCtx::run(const exg_schedule& s, const exg_request* reqs, int n, int32_
                    exg_run_stats* stats, const exg_run_opts* opts) {
   EXG_CUDA(cudaSetDevice(p_->device));
   if (s.n_stages < 1 || s.n_stages > EXG_MAX_STAGES) throw std::invalid_argument("schedule has no stages");
-  if (opts && opts->kv_page > 0 && s.strategy == EXG_RRA)
-    throw std::invalid_argument("paged KV: RRA on one GPU or WAA (exegpt.h kv_page)");
   Layout* lay = get_layout(p_, s);
   if (s.strategy == EXG_RRA)
     run_rra_multi(p_, lay, s, reqs, n, out_tokens, out_latency, stats, opts);

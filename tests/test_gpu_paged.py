@@ -172,3 +172,48 @@ def test_waa_paged_rank_threads_bit_identical(setup, long_reqs):
         assert np.array_equal(res[head_rank][3][r], base[3][r]), r
     for g in group:
         g.close()
+
+
+# ----------------------------------------- paged KV under multi-GPU RRA --
+RRA_LAYOUTS = {
+    "pp2": ([(0, 1, 0, 1), (1, 1, 1, 2)], 1, 0),
+    "tp2": ([(0, 2, 0, 2)], 2, 2),
+    "tp2_then_single": ([(0, 2, 0, 1), (2, 1, 1, 2)], 2, 2),
+}
+
+
+@pytest.mark.parametrize("name", list(RRA_LAYOUTS))
+def test_rra_pipeline_paged_bit_identical(setup, long_reqs, multi, name):
+    """RRA over pipeline stages / TP ranks with every stage paged (same page
+    ids on every stage; swap preemption under pressure): bit-identical to the
+    slot run of the same layout."""
+    X, T, spec, W, reqs, ctx = setup
+    from paper_2404_07947_b200 import _lib as L
+    lr, ora, base = long_reqs
+    layout, t, c = RRA_LAYOUTS[name]
+    s = L.make_schedule(X.EXG_RRA, 8, 12, layout, n_d=200, tp_degree=t, tp_gpus=c)
+    ref_t, _, _, ref_l = multi.run(s, lr, dump=range(len(lr)))
+    if t == 1:
+        assert ref_t == base[0]
+    for pages, swaps in ((0, False), (16, True)):
+        toks, _, st, lg = multi.run(s, lr, dump=range(len(lr)), kv_page=64, kv_pages=pages)
+        assert (st["kv_preemptions"] > 0) == swaps, (pages, st["kv_preemptions"])
+        assert toks == ref_t
+        for r in range(len(lr)):
+            assert np.array_equal(lg[r], ref_l[r]), (name, pages, r)
+
+
+def test_rra_pipeline_paged_rank_threads(setup, long_reqs):
+    X, T, spec, W, reqs, ctx = setup
+    from paper_2404_07947_b200 import _lib as L
+    lr, ora, base = long_reqs
+    s = L.make_schedule(X.EXG_RRA, 8, 12, [(0, 1, 0, 1), (1, 1, 1, 2)], n_d=200)
+    group = X.local_group(spec, 0xE6E0_00A1, 2, X.cluster_spec(8))
+    res = X.run_group(group, s, lr, dump=range(len(lr)), kv_page=64, kv_pages=16)
+    toks, _, st, _ = res[0]
+    assert st["kv_preemptions"] > 0 and toks == base[0]
+    head_rank = max(range(2), key=lambda q: np.count_nonzero(res[q][3][0]))
+    for r in range(len(lr)):
+        assert np.array_equal(res[head_rank][3][r], base[3][r]), r
+    for g in group:
+        g.close()
