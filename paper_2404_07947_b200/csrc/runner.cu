@@ -496,7 +496,7 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
       }
       const int ev_it = record(2, live);
       ev_rows[ev_it] = B;
-      ev_work[ev_it] = sum_keys + sum_xkeys;   // T5: self + cross-attention keys
+      ev_work[ev_it] = sum_keys + (ed ? sum_xkeys : 0.0);   // T5: self + cross-attention keys
       ++decode_iters;
       batch_sum += B;
       if (next_req < n) {   // decode batch average while requests keep arriving (not the drain)
