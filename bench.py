@@ -471,17 +471,26 @@ def run_layout(args, rank, world, local):
             prof.comm_model(COMM_ALPHA_S, COMM_BW)
         os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
         prof.save(os.path.join(ROOT, "gpurun_out", "profile_multi.txt"))
-        # paged KV (NEXT-2) in the one-GPU dry run: the planner charges each
-        # decode row its live positions (exegpt.h kv_page), the runner pages
-        paged = args.kv_page if world == 1 else 0
+        # paged KV (NEXT-2, --kv-page): the planner charges each decode row its
+        # live positions (exegpt.h kv_page), every executor pages
+        paged = args.kv_page
         cl_plan = X.cluster_spec(max(world, 1), mem, ws, kv_page=paged)
         plan = multi_plans(X, prof, ctx1.mspec, cl_plan, pin, pout, d.target_len, args.margin, args.little)
-        if paged and "sched" in plan["pick"]:
-            # page pool = the GPU's memory after weights and workspace
-            w_b, _ = X.schedule_memory(prof, ctx1.mspec, cl_plan, pin, pout,
-                                       exg_schedule.from_buffer_copy(plan["pick"]["sched"]))
-            page_bytes = spec.n_dec_layers * 2 * spec.n_heads * paged * spec.d_head * 2
-            plan["kv_pages"] = int((mem - w_b[0] - ws) // page_bytes)
+        for key in ("pick", "waa_tp2"):
+            if not paged or "sched" not in plan[key]:
+                continue
+            # page pool: the same page count on every paged GPU, the most any
+            # of them fits after its weights and workspace
+            sp = exg_schedule.from_buffer_copy(plan[key]["sched"])
+            w_b, _ = X.schedule_memory(prof, ctx1.mspec, cl_plan, pin, pout, sp)
+            waa = sp.strategy in (X.EXG_WAA_C, X.EXG_WAA_M)
+            pools = []
+            for g0, ng, l0, l1 in sp.stages():
+                if waa and g0 < sp.n_enc_gpus:
+                    continue   # WAA encoder GPUs keep per-batch slots
+                page_bytes = (l1 - l0) * 2 * (spec.n_heads // ng) * paged * spec.d_head * 2
+                pools += [int((mem - w_b[g] - ws) // page_bytes) for g in range(g0, g0 + ng)]
+            plan[key]["kv_pages"] = max(1, min(pools))
         if world > 1:
             ctx1.close()
             del ctx1
@@ -499,7 +508,7 @@ def run_layout(args, rank, world, local):
         return
     s = exg_schedule.from_buffer_copy(plan["pick"]["sched"])
     L_b = plan["latency_bound_s"]
-    pkw = {"kv_page": args.kv_page, "kv_pages": plan["kv_pages"]} if plan.get("kv_pages") else {}
+    pkw = {"kv_page": args.kv_page, "kv_pages": plan["pick"]["kv_pages"]} if plan["pick"].get("kv_pages") else {}
     reqs = make_requests(args.requests, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E1_0000 + MULTI_CONFIG_NO)
     slot_ctx = len(d.pmf_in) + len(d.pmf_out)
     h2d = sum((r.input_len - 1) * 12 + 16 + 16 * r.output_len for r in reqs)
@@ -526,7 +535,9 @@ def run_layout(args, rank, world, local):
     forced = None
     if "sched" in plan["waa_tp2"] and world > 1:
         sw = exg_schedule.from_buffer_copy(plan["waa_tp2"]["sched"])
-        _, lat_w, st_w, _ = ctx.run(sw, reqs, slot_ctx=slot_ctx)
+        wkw = ({"kv_page": args.kv_page, "kv_pages": plan["waa_tp2"]["kv_pages"]}
+               if plan["waa_tp2"].get("kv_pages") else {})
+        _, lat_w, st_w, _ = ctx.run(sw, reqs, slot_ctx=slot_ctx, **wkw)
         forced = {"schedule": plan["waa_tp2"]["schedule"], "predicted_tok_s": plan["waa_tp2"]["predicted_tok_s"],
                   "tok_s": st_w["tok_s"], "p99_latency_s": float(np.percentile(lat_w, 99)) if rank == 0 else None}
     else:
@@ -603,7 +614,7 @@ def main():
                     help="N > 1: config 4 under the scheduler's N-GPU plan as one NCCL job (default), or "
                          "independent config-2 replicas")
     ap.add_argument("--kv-page", type=int, default=0,
-                    help="one-GPU plan dry run: paged KV of this page length (planner and runner; 0 = slots)")
+                    help="--layout plan: paged KV of this page length (planner and runner; 0 = slots)")
     ap.add_argument("--plan-dry-run", action="store_true",
                     help="run the N > 1 (config 4) path on one GPU (testing; no collective)")
     ap.add_argument("--multi-model", default=MULTI_MODEL)
