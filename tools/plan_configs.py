@@ -5,7 +5,9 @@ interconnect from the alpha-beta model; Algorithm 1 then plans the full model on
 N GPUs.  Predictions only (the layouts' arithmetic is checked at full width in
 tests/test_gpu_fullsize.py).
 
-    python tools/plan_configs.py > profiles/r1_plans.json
+    python tools/plan_configs.py > profiles/r2_plans.json
+
+Each config is planned with KV slots and with paged KV (kv_page = 64).
 """
 import json
 import math
@@ -23,6 +25,9 @@ CONFIGS = [  # (config, model, task, GPU counts, strategies)
     ("config 5 (C1)", "gpt3-175b", "C1", (8,), X.EXG_RRA | X.EXG_WAA_C | X.EXG_WAA_M),
     ("config 5 (C2)", "gpt3-175b", "C2", (8,), X.EXG_RRA | X.EXG_WAA_C | X.EXG_WAA_M),
 ]
+
+
+bench_margin = 0.03   # the bench's scheduler margin on top of the simulator's buffer time
 
 
 def main():
@@ -46,23 +51,28 @@ def main():
         pin, pout = X.Pmf(d.pmf_in), X.Pmf(d.pmf_out)
         row = {"config": name, "model": model, "task": task, "plans": {}}
         for n in gpus:
-            cl = X.cluster_spec(n, total - (6 << 30), 8 << 30)
-            try:
-                bounds = bench.static_bounds(X, prof, mspec, cl, pin, pout, d.target_len)
-            except Exception as e:  # noqa: BLE001
-                row["plans"][str(n)] = {"bounds": "static baseline infeasible: %s" % e}
-                continue
-            per = {}
-            for bname, L_b in bounds:
+            for kv_page, key in ((0, "plans"), (64, "plans_paged_kv")):
+                # paged KV (NEXT-2): the planner charges a decode row its live
+                # positions; the static-batch bounds keep slots (FT does not page)
+                cl = X.cluster_spec(n, total - (6 << 30), 8 << 30, kv_page=kv_page)
                 try:
-                    s, e = X.schedule_find(prof, mspec, cl, pin, pout, d.target_len,
-                                           L_b * 0.85 if math.isfinite(L_b) else L_b, mask,
-                                           X.search_opts(b_e_max=64, little=1))
-                    per[bname] = {"bound_s": L_b, "schedule": s.as_dict(), "predicted_tok_s": e.thrput_tok_s,
-                                  "predicted_latency_s": e.latency_s}
-                except X.ExgError as ex:
-                    per[bname] = {"bound_s": L_b, "infeasible": str(ex)}
-            row["plans"][str(n)] = per
+                    bounds = bench.static_bounds(X, prof, mspec, cl, pin, pout, d.target_len)
+                except Exception as e:  # noqa: BLE001
+                    row.setdefault(key, {})[str(n)] = {"bounds": "static baseline infeasible: %s" % e}
+                    continue
+                per = {}
+                for bname, L_b in bounds:
+                    try:
+                        s, e = X.schedule_find(prof, mspec, cl, pin, pout, d.target_len,
+                                               L_b * (1 - bench_margin) if math.isfinite(L_b) else L_b, mask,
+                                               X.search_opts(b_e_max=64, little=1))
+                        mem_w, mem_kv = X.schedule_memory(prof, mspec, cl, pin, pout, s)
+                        per[bname] = {"bound_s": L_b, "schedule": s.as_dict(), "predicted_tok_s": e.thrput_tok_s,
+                                      "predicted_latency_s": e.latency_s,
+                                      "max_gpu_gb": round(max(a + b for a, b in zip(mem_w, mem_kv)) / 1e9, 2)}
+                    except X.ExgError as ex:
+                        per[bname] = {"bound_s": L_b, "infeasible": str(ex)}
+                row.setdefault(key, {})[str(n)] = per
         print(json.dumps(row), flush=True)
 
 

@@ -2,7 +2,8 @@
 kernel family -- config 1 bf16 (RRA, static batch, dynamic adjustment) and
 fp32, a T5 model with tensor-core attention (dh = 128), a width-2048 model
 with split stream-K tiles (deferred and in-kernel reductions), an emulated
-WAA layout with a TP-2 decoder stage, and a small profile.
+WAA layout with a TP-2 decoder stage, a small profile, and paged KV (one-GPU
+RRA with recompute preemption, WAA with swap preemption; dh = 128 pages of 64).
 
     compute-sanitizer --tool memcheck python tools/sanitize_smoke.py
 """
@@ -42,5 +43,14 @@ m = X.Context(tiny, weight_seed(1), cluster=X.cluster_spec(4))
 s = L.make_schedule(X.EXG_WAA_C, 2, 8, [(0, 1, 0, 2), (1, 2, 0, 1), (3, 1, 1, 2)], b_m=4, n_enc_gpus=1, tp_degree=2,
                     tp_gpus=2)
 m.run(s, reqs, dump=range(len(reqs)))
+m.close()
+pg = ModelSpec("san-paged", "opt", 0, 2, 256, 2, 128, 512, 512, 512)
+rp = make_requests(12, uniform_pmf(20, 100), uniform_pmf(100, 300), pg.vocab, 0xE6E1_00A2)
+c = X.Context(pg, 0xE6E0_00A1)
+c.run(X.rra_schedule(8, 12, 200), rp, kv_page=64, kv_pages=12)
+c.close()
+m = X.Context(pg, 0xE6E0_00A1, cluster=X.cluster_spec(4))
+s = L.make_schedule(X.EXG_WAA_C, 4, 12, [(0, 1, 0, 2), (1, 1, 0, 1), (2, 1, 1, 2)], b_m=6, n_enc_gpus=1)
+m.run(s, rp, kv_page=64, kv_pages=12)
 m.close()
 print("sanitize smoke done")
