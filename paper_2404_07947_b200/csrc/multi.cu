@@ -663,12 +663,14 @@ void validate_requests(RunState& R, int V, int max_pos) {
 }
 
 // packed encode tables for requests [r0, r0+k) with the given slots
+// paged: the encoding engines page their KV (RRA pipelines; WAA encoders keep
+// per-batch slots) -- tokens carry page / offset and requests page tables
 EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int* slots, cudaStream_t st,
-                         std::vector<int32_t>* last_ids) {
+                         std::vector<int32_t>* last_ids, bool paged = false) {
   const int drop = R.ed ? 0 : 1;   // T6: decoder-only encodes positions 0..n-2, T5 all n tokens
   int T = 0, maxlen = 0;
   for (int j = 0; j < k; ++j) T += R.reqs[r0 + j].input_len - drop;
-  const size_t pgi = R.P > 0 ? (size_t)2 * T + (size_t)k * R.maxp : 0;   // paged: page / offset per token, page table
+  const size_t pgi = paged ? (size_t)2 * T + (size_t)k * R.maxp : 0;   // paged: page / offset per token, page table
   tb.ensure((size_t)3 * T + 3 * (k + 1) + pgi + 8);
   int32_t* h = tb.begin();
   int32_t *ids = h, *pos = ids + T, *tsl = pos + T, *cu = tsl + T, *rsl = cu + k + 1, *p0 = rsl + k;
@@ -695,6 +697,8 @@ EncodeBatch build_encode(const RunState& R, Tables& tb, int r0, int k, const int
     int t2 = 0;
     for (int j = 0; j < k; ++j) {
       const auto& pg = R.slot_pages[slots[j]];
+      if ((int)pg.size() * R.P < R.reqs[r0 + j].input_len - drop || pg.empty())
+        throw std::logic_error("paged encode: the request's pages are not allocated");
       for (int p = 0; p < R.reqs[r0 + j].input_len - drop; ++p, ++t2) {
         kvb[t2] = pg[p / R.P];
         kvo[t2] = p % R.P;
@@ -1163,7 +1167,8 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       for (const auto& mb : chunks(admit, P)) {
         Tables& tb = tabs[ti++ % tabs.size()];
         std::vector<int32_t> last;
-        EncodeBatch eb = build_encode(R, tb, next_req + mb.first, mb.second, slots.data() + mb.first, R.st, &last);
+        EncodeBatch eb =
+            build_encode(R, tb, next_req + mb.first, mb.second, slots.data() + mb.first, R.st, &last, pgr.on());
         // x[n-1] of every admitted request -> last_tok[slot] on the first stage
         Tables& tl = tabs[ti++ % tabs.size()];
         tl.ensure(2 * last.size() + 2);
