@@ -189,6 +189,7 @@ Engine::Engine(const exg_model_spec& s, int device, const EngineShard& shard, cu
 Engine::~Engine() {
   cudaSetDevice(dev_);
   cudaStreamSynchronize(st_);
+  run_cache_.reset();
   for (void* p : {(void*)wbuf_, (void*)x_, (void*)kv_, (void*)xkv_, (void*)last_tok_, (void*)err_,
                   (void*)enc_bias_, (void*)chain_ws_, (void*)chain_sync_})
     if (p) cudaFree(p);

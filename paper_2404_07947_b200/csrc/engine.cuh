@@ -9,6 +9,7 @@
 // true}.  Pipelines, TP groups and WAA encoder/decoder sets are built from
 // several Engines by the executors (runner.cu, multi.cu).
 #pragma once
+#include <memory>
 #include <vector>
 
 #include "../../include/exegpt.h"
@@ -160,6 +161,10 @@ class Engine {
   float* part() { return part_; }
 
   int32_t* err_flag() { return err_; }
+  // the runner's host-side state kept across runs (pinned staging ring,
+  // events, table buffers): allocating and pinning it per run costs host
+  // time that the end-to-end number pays
+  std::shared_ptr<void>& run_cache() { return run_cache_; }
   size_t weight_bytes() const { return wbytes_; }
 
   // per-launch CUDA-event timing of the kernel classes of exegpt.h
@@ -259,6 +264,7 @@ class Engine {
   bf16* kv_ = nullptr;
   int kv_slots_ = 0, slot_ctx_ = 0, kv_layers_ = 0;
   int32_t* last_tok_ = nullptr;
+  std::shared_ptr<void> run_cache_;
 
   size_t kv_layer_elems() const { return (size_t)kv_slots_ * D.Hl * slot_ctx_ * D.dh; }
 };

@@ -89,6 +89,30 @@ struct EventPool {
   }
 };
 
+// host-side state of the runner kept in the Engine across runs (pinned
+// staging ring, events, device table buffers), grown when a run needs more
+struct RunCache {
+  std::unique_ptr<Staging> stage;
+  EventPool evp;
+  int32_t* d_out = nullptr;
+  int32_t* d_tab = nullptr;
+  size_t out_cap = 0, tab_cap = 0;
+  ~RunCache() {
+    if (d_out) cudaFree(d_out);
+    if (d_tab) cudaFree(d_tab);
+  }
+  int32_t* ensure(int32_t*& p, size_t& cap, size_t n) {
+    if (n > cap) {
+      if (p) EXG_CUDA(cudaFree(p));
+      p = nullptr;
+      cap = 0;
+      EXG_CUDA(cudaMalloc(&p, sizeof(int32_t) * n));
+      cap = n;
+    }
+    return p;
+  }
+};
+
 double pct(std::vector<double> v, double q) {
   if (v.empty()) return 0.0;
   std::sort(v.begin(), v.end());
@@ -159,27 +183,26 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   E.ensure_workspace(enc_tok_cap, B_D);
   cudaStream_t st = E.stream();
 
-  // device arrays: output tokens, encode tables, decode tables (freed on
-  // every exit path)
-  struct DevFree {
-    void operator()(int32_t* p) const { cudaFree(p); }
-  };
+  // device arrays: output tokens, encode tables, decode tables, and the
+  // pinned staging ring -- all kept in the engine's run cache across runs
+  auto& rc_any = E.run_cache();
+  if (!rc_any) rc_any = std::make_shared<RunCache>();
+  RunCache& rc = *static_cast<RunCache*>(rc_any.get());
   const size_t enc_ints = (size_t)3 * enc_tok_cap + 3 * ((size_t)enc_row_cap + 1) + 2 * (size_t)enc_row_cap +
                           (paged ? (size_t)2 * enc_tok_cap + (size_t)enc_row_cap * maxp : 0);
   const size_t dec_ints = (size_t)5 * B_D + (paged ? (size_t)B_D * maxp : 0);
   const size_t tab_ints = std::max(enc_ints, dec_ints);
-  int32_t* raw = nullptr;
   // + B_D scratch entries: the tokens of finished rows a static batch still computes
-  EXG_CUDA(cudaMalloc(&raw, sizeof(int32_t) * (total_out + B_D)));
-  std::unique_ptr<int32_t, DevFree> d_out_own(raw);
-  raw = nullptr;
-  EXG_CUDA(cudaMalloc(&raw, sizeof(int32_t) * (enc_ints + dec_ints)));
-  std::unique_ptr<int32_t, DevFree> d_tab_own(raw);
-  int32_t* d_out = d_out_own.get();
-  int32_t* d_enc = d_tab_own.get();
+  int32_t* d_out = rc.ensure(rc.d_out, rc.out_cap, (size_t)total_out + B_D);
+  int32_t* d_enc = rc.ensure(rc.d_tab, rc.tab_cap, enc_ints + dec_ints);
   int32_t* d_dec = d_enc + enc_ints;
-  Staging stage(64, tab_ints);
-  EventPool evp;
+  if (!rc.stage || rc.stage->cap_ints < tab_ints) {
+    rc.stage.reset();
+    rc.stage = std::make_unique<Staging>(64, tab_ints);
+  }
+  Staging& stage = *rc.stage;
+  EventPool& evp = rc.evp;
+  evp.used = 0;   // events of an earlier run are re-recorded
   std::vector<float> dump_host;
   const bool dumping = opts && opts->logits_out && opts->dump_mask;
   std::vector<int64_t> dump_base(n + 1, 0);
@@ -540,8 +563,6 @@ void run_rra(Engine& E, const exg_schedule& s, const exg_request* reqs, int n, i
   int32_t err = 0;
   EXG_CUDA(cudaMemcpy(&err, E.err_flag(), sizeof(int32_t), cudaMemcpyDeviceToHost));
   if (out_tokens) EXG_CUDA(cudaMemcpy(out_tokens, d_out, sizeof(int32_t) * total_out, cudaMemcpyDeviceToHost));
-  d_out_own.reset();
-  d_tab_own.reset();
   if (err) throw std::runtime_error("NaN logit encountered (T7)");
 
   // ---------------- timing ----------------
