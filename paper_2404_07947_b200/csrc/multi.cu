@@ -415,6 +415,9 @@ struct MultiCtx::Impl {
   int rank = 0, world = 1;
   bool loopback = false;   // a one-rank communicator: route local exchanges through it
   std::map<std::string, std::unique_ptr<Layout>> layouts;
+  // the executors' table ring (device + pinned host buffers), kept across
+  // runs so the end-to-end path does not allocate and pin per run
+  std::shared_ptr<void> tab_cache;
 };
 
 MultiCtx::MultiCtx(const exg_model_spec& spec, int device, std::unique_ptr<Comm> comm) : p_(new Impl) {
@@ -438,6 +441,7 @@ MultiCtx::~MultiCtx() {
   if (p_->st) cudaStreamSynchronize(p_->st);
   if (p_->cst) cudaStreamSynchronize(p_->cst);
   p_->layouts.clear();
+  p_->tab_cache.reset();
   p_->tx.release();
   p_->rx.release();
   p_->comm.reset();
@@ -597,6 +601,12 @@ struct Tables {
     if (host) cudaFreeHost(host);
   }
 };
+
+// the executors' table ring, cached in the context across runs
+std::vector<Tables>& table_ring(std::shared_ptr<void>& cache) {
+  if (!cache) cache = std::make_shared<std::vector<Tables>>(8);
+  return *static_cast<std::vector<Tables>*>(cache.get());
+}
 
 struct RunState {
   const exg_request* reqs;
@@ -1126,7 +1136,7 @@ static void run_rra_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         e->ensure_workspace(std::max(1, B_E * (R.max_in - drop)), B_D);
       }
   const bool first_mine = X.mine(pipe.front()->gpu(0)), head_mine = X.mine(pipe.back()->gpu(0));
-  std::vector<Tables> tabs(8);
+  std::vector<Tables>& tabs = table_ring(p->tab_cache);
   const Dump dump = make_dump(R, opts);
   std::vector<int> free_slots(B_D);
   for (int i = 0; i < B_D; ++i) free_slots[i] = B_D - 1 - i;
@@ -1278,7 +1288,7 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         e->ensure_workspace(1, B_D);
       }
   const bool first_mine = X.mine(enc.front()->gpu(0)), head_mine = X.mine(dec.back()->gpu(0));
-  std::vector<Tables> tabs(8);
+  std::vector<Tables>& tabs = table_ring(p->tab_cache);
   const Dump dump = make_dump(R, opts);
   // handoff row tables: a ring of pinned host / device pairs recycled by
   // events (no host synchronisation per handoff); packed-message staging
