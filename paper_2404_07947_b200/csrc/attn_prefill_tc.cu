@@ -105,6 +105,17 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// O += P . V with P (the A operand) read from TMEM: 128 lanes = query rows,
+// bf16 pairs packed per 32-bit column (K-major), B from shared memory
+__device__ __forceinline__ void umma_bf16_tmem_a(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
 struct FmhaParams {
   const int32_t* cu_seqlens;
   const int32_t* slot;
@@ -146,6 +157,11 @@ __device__ __forceinline__ bool item_of(const FmhaParams& p, int id, Item& it) {
   return true;
 }
 
+// PT: P kept in TMEM (written over its S buffer by the softmax warps, read by
+// the P.V MMA as the A operand) instead of shared memory -- the softmax of
+// tile j+1 then never waits for the P.V of tile j (only a lazy rescale of O
+// does), and the P buffer's 32 KB of shared memory go unused
+template <bool PT>
 __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(const __grid_constant__ CUtensorMap tmQ,
                                                               const __grid_constant__ CUtensorMap tmK,
                                                               const __grid_constant__ CUtensorMap tmV,
@@ -324,12 +340,18 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
           const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + s * KV_BYTES);
 #pragma unroll
           for (int k = 0; k < FK / 16; ++k) {
-            // A (P, K-major): 64-key blocks of 16 KB, 32 B per 16 keys
-            const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
             // B (V, MN-major): 16 keys = two 8-key core groups of 1024 B
             const uint32_t b_off = k * 2048;
-            umma_bf16(d, umma_desc_sw128(pa + a_off), desc_mn_sw128(vb + b_off, TILE_BYTES, 1024), idesc_o,
-                      (j || k) ? 1u : 0u);
+            if constexpr (PT) {
+              // A (P) in TMEM over S buffer s: 16 keys = 8 packed columns
+              umma_bf16_tmem_a(d, tmem + s * 128 + k * 8, desc_mn_sw128(vb + b_off, TILE_BYTES, 1024), idesc_o,
+                               (j || k) ? 1u : 0u);
+            } else {
+              // A (P, K-major): 64-key blocks of 16 KB, 32 B per 16 keys
+              const uint32_t a_off = (k >> 2) * TILE_BYTES + (k & 3) * 32;
+              umma_bf16(d, umma_desc_sw128(pa + a_off), desc_mn_sw128(vb + b_off, TILE_BYTES, 1024), idesc_o,
+                        (j || k) ? 1u : 0u);
+            }
           }
           umma_commit(&o_full[gj & 1]);
           umma_commit(&kv_empty[s]);
@@ -393,8 +415,10 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
         pair_bar();
         mx = fmaxf(lx[r], lx[FQ + r]);
         pair_bar();   // both halves have read lx before it is written again
-        // the previous tile's P.V has completed: P may be overwritten and O read
-        if (j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
+        // smem P: the previous tile's P.V has completed before P is overwritten
+        // (and O read); TMEM P lives in this tile's own S buffer, so only a
+        // rescale of O below waits for it
+        if (!PT && j >= 1) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);
         // lazy rescale: the reference max moves only when this tile's max
         // exceeds it by more than 2^RESCALE_LOG2 (both threads of a row take the
         // same decision); the TMEM accesses are warp-collective, so a warp
@@ -404,6 +428,7 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
         const bool resc = move && j >= 1 && m != -INFINITY;
         if (__any_sync(0xffffffffu, resc)) {
           const float alpha = resc ? ex2((m - m_new) * LOG2E) : 1.f;
+          if (PT) mbar_wait(&o_full[(gj - 1) & 1], ((gj - 1) >> 1) & 1);   // O holds P.V up to tile j-1
           tc_fence_after();
 #pragma unroll
           for (int c = 0; c < HD; c += 16) {
@@ -422,6 +447,7 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
         const float nml = (m == -INFINITY) ? 0.f : -m * LOG2E;
         float sum = 0.f;
 #pragma unroll
+        float pw[16];   // TMEM P: 32 keys = 16 packed columns per store
         for (int c = 0; c < HD; c += 16) {
           uint32_t pk[8];
 #pragma unroll
@@ -433,14 +459,25 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
             sum += __low2float(b2) + __high2float(b2);   // the sum uses the bf16 P that feeds P.V
             pk[e / 2] = *reinterpret_cast<uint32_t*>(&b2);
           }
-          // row r, keys hf*64+c..+15: two 16-byte chunks in the SW128 K-major image
-          uint8_t* blk = sP + hf * TILE_BYTES;
-          const int ch = c >> 3;
-          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-          *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          if constexpr (PT) {
+            // row r, keys hf*64+c..+15 -> packed columns hf*32 + c/2 .. +8 of S buffer s
+#pragma unroll
+            for (int q = 0; q < 8; ++q) pw[(c & 16) / 2 + q] = __uint_as_float(pk[q]);
+            if (c & 16) tmem_st16(tmem + lane_base + s * 128 + hf * 32 + (c - 16) / 2, pw);
+          } else {
+            // row r, keys hf*64+c..+15: two 16-byte chunks in the SW128 K-major image
+            uint8_t* blk = sP + hf * TILE_BYTES;
+            const int ch = c >> 3;
+            *reinterpret_cast<uint4*>(blk + r * 128 + (((ch) ^ (r & 7)) << 4)) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+            *reinterpret_cast<uint4*>(blk + r * 128 + (((ch + 1) ^ (r & 7)) << 4)) =
+                make_uint4(pk[4], pk[5], pk[6], pk[7]);
+          }
         }
         l += sum;
-        fence_proxy_async_smem();
+        if (PT)
+          tmem_st_wait();
+        else
+          fence_proxy_async_smem();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) {
@@ -491,6 +528,12 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
 }
 }  // namespace
 
+// P in TMEM (1) or shared memory (0) (exg_diag_fmha_p_tmem, A/B)
+int& fmha_p_tmem() {
+  static int on = 1;
+  return on;
+}
+
 // L2 prefetch distance of the FMHA producer in items (exg_diag_fmha_prefetch);
 // off: measured slower at the task-S mix (tools/probe_kernels.py pmix_pf:
 // 280.6 us without, 294.9 / 310.2 / 311.3 us with 1 / 2 / 4 items ahead)
@@ -509,7 +552,10 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   if (a.dh != FD || prefill_force_simt()) return false;
   static bool attr = false;
   if (!attr) {
-    EXG_CUDA(cudaFuncSetAttribute(fmha_prefill_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FMHA_SMEM));
+    EXG_CUDA(cudaFuncSetAttribute(fmha_prefill_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)FMHA_SMEM));
+    EXG_CUDA(cudaFuncSetAttribute(fmha_prefill_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)FMHA_SMEM));
     attr = true;
   }
   // Q: the packed qkv buffer [q_rows][ldq] (rows past the last token are
@@ -527,7 +573,10 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
   const CUtensorMap tv = make_tmap_bf16(a.vc, a.kv_rows, FD, FD, 64);
   // persistent grid: one CTA per SM (227 KB of shared memory, 512 TMEM columns)
   const int grid = std::min(n_items, sm_count());
-  launch_pdl(fmha_prefill_kernel, dim3(grid), dim3(128 + 32 * SM_WARPS), FMHA_SMEM, st, tq, tk, tv, p);
+  if (fmha_p_tmem())
+    launch_pdl(fmha_prefill_kernel<true>, dim3(grid), dim3(128 + 32 * SM_WARPS), FMHA_SMEM, st, tq, tk, tv, p);
+  else
+    launch_pdl(fmha_prefill_kernel<false>, dim3(grid), dim3(128 + 32 * SM_WARPS), FMHA_SMEM, st, tq, tk, tv, p);
   EXG_CHECK_LAUNCH();
   return true;
 }
@@ -536,3 +585,4 @@ bool prefill_attention_tc(const PrefillAttnArgs& a, cudaStream_t st) {
 
 extern "C" void exg_diag_prefill_simt(int on) { exg::prefill_force_simt() = on; }
 extern "C" void exg_diag_fmha_prefetch(int ahead) { exg::fmha_prefetch_ahead() = ahead > 0 ? ahead : 0; }
+extern "C" void exg_diag_fmha_p_tmem(int on) { exg::fmha_p_tmem() = on; }

@@ -285,6 +285,17 @@ if __name__ == "__main__":
             pattn(32, 256)
         L.lib().exg_diag_fmha_prefetch(2)
         sys.exit(0)
+    if len(sys.argv) > 1 and sys.argv[1] == "pmix_pt":
+        # A/B of the FMHA's P buffer: shared memory (0) vs TMEM (1) (exg_diag_fmha_p_tmem)
+        for rep in range(2):
+            for on in (0, 1):
+                L.lib().exg_diag_fmha_p_tmem(on)
+                print("-- FMHA P in %s" % ("TMEM" if on else "shared memory"))
+                for R in (32, 52):
+                    pattn_mix(R)
+                pattn(32, 256)
+        L.lib().exg_diag_fmha_p_tmem(1)
+        sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pattn":
         pattn(int(sys.argv[2]), int(sys.argv[3]))
         sys.exit(0)
