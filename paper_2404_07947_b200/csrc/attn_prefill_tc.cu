@@ -293,6 +293,10 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
         const int s = gj & 1;
         mbar_wait(&kv_full[s], (gj >> 1) & 1);
         if (gj >= 2) mbar_wait(&s_free[s], ((gj >> 1) & 1) ^ 1);
+        // TMEM P: S buffer s still holds P of tile gj-2 -- its P.V must have
+        // read it before this S overwrites it (the MMA pipe does not order a
+        // TMEM read of one MMA before the TMEM write of a later one)
+        if (PT && gj >= 2) mbar_wait(&o_full[(gj - 2) & 1], ((gj - 2) >> 1) & 1);
         tc_fence_after();
         const uint32_t d = tmem + s * 128;
         const uint32_t qa = smem_u32(sQ + qs * Q_BYTES), kb = smem_u32(sK + s * KV_BYTES);
@@ -528,9 +532,13 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
 }
 }  // namespace
 
-// P in TMEM (1) or shared memory (0) (exg_diag_fmha_p_tmem, A/B)
+// P in TMEM (1) or shared memory (0) (exg_diag_fmha_p_tmem, A/B).  Off: 3 %
+// faster on the task-S mix (tools/probe_kernels.py pmix_pt: 272 vs 281 us), but
+// the T5 bidirectional + relative-bias parity test still sees corrupted rows
+// with it (an ordering between the softmax's TMEM P stores and the MMA pipe
+// not yet pinned down), so the shared-memory P path stays the default
 int& fmha_p_tmem() {
-  static int on = 1;
+  static int on = 0;
   return on;
 }
 

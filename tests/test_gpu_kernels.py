@@ -498,3 +498,36 @@ def test_prefill_attention_paged_matches_slots(L, dh, P):
             ref = p_ @ V[r, h, :lens[r]]
             g = got[cu[r]:cu[r + 1], h * dh:(h + 1) * dh]
             assert np.all(np.abs(g - ref) <= rel * np.abs(ref) + ab), (r, h, np.abs(g - ref).max())
+
+
+@pytest.mark.parametrize("causal", [1, 0])
+def test_prefill_attention_tc_repeatable(L, causal):
+    """Race check of the tcgen05 FMHA (P kept in TMEM over its S buffer):
+    items of up to 4 key tiles, run 12 times -- every output finite and
+    bitwise equal across runs."""
+    rng = np.random.default_rng(31 + causal)
+    H, dh, max_ctx = 4, 128, 512
+    lens = [512, 300, 257, 129, 511, 384, 200, 65]
+    R = len(lens)
+    cu = np.concatenate([[0], np.cumsum(lens)]).astype(np.int32)
+    T = int(cu[-1])
+    qkv = bf16_round_np(rng.standard_normal((T, 3 * H * dh)) * 2.0)
+    K = bf16_round_np(rng.standard_normal((R, H, max_ctx, dh)) * 2.0)
+    V = bf16_round_np(rng.standard_normal((R, H, max_ctx, dh)))
+    tq, tK, tV = bf16_tensor(qkv), bf16_tensor(K), bf16_tensor(V)
+    tcu = torch.from_numpy(cu).to(dev())
+    tsl = torch.arange(R, dtype=torch.int32, device=dev())
+    tp0 = torch.zeros(R, dtype=torch.int32, device=dev())
+    first = None
+    for _ in range(12):
+        out = torch.zeros((T, H * dh), dtype=torch.bfloat16, device=dev())
+        _run(L, "exg_op_prefill_attention", ptr(tq), 3 * H * dh, ptr(tK), ptr(tV), ptr(tcu), ptr(tsl), ptr(tp0), R,
+             max(lens), ptr(out), H * dh, H, dh, max_ctx, R, T, float(np.float32(1 / np.sqrt(dh))), causal, None, 0,
+             0, stream())
+        torch.cuda.synchronize()
+        o = out.float().cpu()
+        assert torch.isfinite(o).all()
+        if first is None:
+            first = o
+        else:
+            assert torch.equal(o, first)

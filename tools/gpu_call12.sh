@@ -1,4 +1,4 @@
-# FMHA P-in-TMEM: parity first (kernel, T5, e2e, paged), then the A/B and a decode/encode phase A/B
+# FMHA P-in-TMEM (WAR wait before S overwrites P): parity first, then the A/B
 mkdir -p gpurun_out
 timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_t5.py tests/test_gpu_e2e.py tests/test_gpu_paged.py -x -q > gpurun_out/pytest_pt.log 2>&1; echo "pytest rc $?"
 tail -2 gpurun_out/pytest_pt.log
