@@ -180,9 +180,9 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
   uint64_t* kv_empty = bars + 6;        // 2
   uint64_t* s_full = bars + 8;          // 2
   uint64_t* s_free = bars + 10;         // 2
-  uint64_t* p_full = bars + 12;         // 1
+  uint64_t* p_full = bars + 12;         // P of tile gj written: p_full[gj & 1] (slots 12 and 15)
   uint64_t* o_full = bars + 13;         // 2: P.V of a tile done (parity by tile)
-  uint64_t* o_free = bars + 15;         // 2: (unused slot kept for the layout)
+  uint64_t* p_full1 = bars + 15;        // the second p_full (by tile parity; 16 unused)
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 17);
   float* lx = reinterpret_cast<float*>(sP + P_BYTES + 256);   // [2][FQ] row-sum halves
 
@@ -200,7 +200,7 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], SM_WARPS);
       mbar_init(&o_full[i], 1);
-      mbar_init(&o_free[i], SM_WARPS);
+      if (i == 0) mbar_init(p_full1, SM_WARPS);
     }
     mbar_init(p_full, SM_WARPS);
     fence_barrier_init();
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
           // first tile, after reading out the previous item's O)
           const uint32_t gj = base + j;
           const int s = gj & 1;
-          mbar_wait(p_full, gj & 1);
+          mbar_wait((gj & 1) ? p_full1 : p_full, (gj >> 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem + 256;
           const uint32_t pa = smem_u32(sP), vb = smem_u32(sV + s * KV_BYTES);
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
         __syncwarp();
         if (lane == 0) {
           mbar_arrive(&s_free[s]);
-          mbar_arrive(p_full);
+          mbar_arrive((gj & 1) ? p_full1 : p_full);
         }
       }
       // the item's last P.V, then O out of TMEM: normalised by the row sum
