@@ -532,13 +532,13 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
 }
 }  // namespace
 
-// P in TMEM (1) or shared memory (0) (exg_diag_fmha_p_tmem, A/B).  Off: 3 %
-// faster on the task-S mix (tools/probe_kernels.py pmix_pt: 272 vs 281 us), but
-// the T5 bidirectional + relative-bias parity test still sees corrupted rows
-// with it (an ordering between the softmax's TMEM P stores and the MMA pipe
-// not yet pinned down), so the shared-memory P path stays the default
+// P in TMEM (1) or shared memory (0) (exg_diag_fmha_p_tmem, A/B): TMEM P is
+// 3 % faster on the task-S mix (tools/probe_kernels.py pmix_pt: 272 vs 281
+// us).  With it the softmax warps can run two tiles ahead of the P.V issue, so
+// p_full is double-buffered by tile parity (a single barrier aliased phases
+// and corrupted rows in the T5 relative-bias test; tools/fmha_pt_check.py)
 int& fmha_p_tmem() {
-  static int on = 0;
+  static int on = 1;
   return on;
 }
 

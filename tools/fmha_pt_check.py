@@ -78,4 +78,4 @@ for on in (0, 1):
                                      ("causal", False, 1, [512, 300, 257, 129, 511, 384])):
         w, f, same = case(bias, causal, lens)
         print("P in %-4s %-8s max err %.3g finite %s repeatable %s" % ("TMEM" if on else "smem", name, w, f, same))
-L.lib().exg_diag_fmha_p_tmem(0)
+L.lib().exg_diag_fmha_p_tmem(1)

@@ -294,7 +294,7 @@ if __name__ == "__main__":
                 for R in (32, 52):
                     pattn_mix(R)
                 pattn(32, 256)
-        L.lib().exg_diag_fmha_p_tmem(0)
+        L.lib().exg_diag_fmha_p_tmem(1)
         sys.exit(0)
     if len(sys.argv) > 1 and sys.argv[1] == "pattn":
         pattn(int(sys.argv[2]), int(sys.argv[3]))
