@@ -9,9 +9,10 @@
 //                          thread of the pair exponentiates one 64-key half of
 //                          the tile (both take the row max over all 128 keys,
 //                          so no exchange per tile); online max / half sums;
-//                          P_j -> smem as bf16
-//   O  += P_j . V_j        tcgen05.mma, A = P (K-major), B = V (MN-major), fp32,
-//                          accumulated in TMEM across the item's tiles
+//                          P_j -> TMEM as bf16, over S_j's own buffer
+//   O  += P_j . V_j        tcgen05.mma, A = P read from TMEM, B = V (MN-major),
+//                          fp32, accumulated in TMEM across the item's tiles
+//                          (a shared-memory P variant stays for A/B)
 // Lazy rescaling: P_j is exponentiated against the row's running reference
 // max m_ref, which moves (and O in TMEM is rescaled by the softmax warps) only
 // when a tile's max exceeds it by more than 8 in log2 units -- so p <= 2^8 and
@@ -533,7 +534,7 @@ __global__ void __launch_bounds__(128 + 32 * SM_WARPS, 1) fmha_prefill_kernel(co
 }  // namespace
 
 // P in TMEM (1) or shared memory (0) (exg_diag_fmha_p_tmem, A/B): TMEM P is
-// 3 % faster on the task-S mix (tools/probe_kernels.py pmix_pt: 272 vs 281
+// 6 % faster on the task-S mix (tools/probe_kernels.py pmix_pt: 270 vs 287
 // us).  With it the softmax warps can run two tiles ahead of the P.V issue, so
 // p_full is double-buffered by tile parity (a single barrier aliased phases
 // and corrupted rows in the T5 relative-bias test; tools/fmha_pt_check.py)
