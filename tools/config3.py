@@ -55,8 +55,20 @@ def main():
     # against the profile's time for the same rows and work
     # (exg_profile_stage_time), and the batch trajectory
     fid = {}
-    for kind, name, ph in ((1, "encode", 0), (2, "decode", 1)):
-        recs = [r for r in trace if int(r[0]) == kind and r[3] > 0]
+    # decode iterations >= 16 after the last encode phase (outside the clock
+    # recovery the simulator charges separately through its switch table)
+    since, late = 10 ** 9, []
+    for r in trace:
+        if int(r[0]) == 1 and r[3] > 0:
+            since = 0
+        elif int(r[0]) == 2:
+            since += 1
+            late.append(since > 16)
+    for kind, name, ph in ((1, "encode", 0), (2, "decode", 1), (3, "decode_after_recovery", 1)):
+        if kind == 3:
+            recs = [r for r, ok in zip([r for r in trace if int(r[0]) == 2], late) if ok and r[3] > 0]
+        else:
+            recs = [r for r in trace if int(r[0]) == kind and r[3] > 0]
         meas = sum(r[2] for r in recs)
         pred = sum(prof.stage_time(ph, r[3], r[4], spec.n_dec_layers) for r in recs)
         fid[name] = {"stages": len(recs), "measured_s": meas, "profile_s": pred,
