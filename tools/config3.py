@@ -70,9 +70,6 @@ def main():
     if len(enc_idx) >= 4:
         mid = [r[3] for r in trace[enc_idx[2]:enc_idx[-1]] if int(r[0]) == 2]
         fid["steady_mean_decode_batch"] = float(np.mean(mid)) if mid else None
-    from oracle import seqdist   # the model's batch trajectory (host arithmetic only)
-    bu = seqdist.rra_iteration_batches(s1.b_d, seqdist.completion_distribution(d.pmf_out, s1.n_d))
-    fid["model_mean_decode_batch"] = float(np.mean(bu))
     for kind, name, ph in ((1, "encode", 0), (2, "decode", 1), (3, "decode_after_recovery", 1)):
         if kind == 3:
             recs = [r for r, ok in zip([r for r in trace if int(r[0]) == 2], late) if ok and r[3] > 0]
