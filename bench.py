@@ -598,6 +598,9 @@ def run_reference(args, rank, world):
 
 # ----------------------------------------------------------------------------
 def main():
+    if os.environ.get("EXG_PROFILE_INSITU"):   # diagnostics (A/B): in-situ decode attention table
+        import paper_2404_07947_b200 as X
+        X.lib().exg_diag_profile_insitu(int(os.environ["EXG_PROFILE_INSITU"]))
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)

@@ -102,6 +102,15 @@ struct Timer {
 
 constexpr int kBurst = 8, kBurstEnc = 4;
 
+// diagnostics (exg_diag_profile_insitu): 1 = the decode attention table is
+// the in-situ increment of a PDL-chained burst of full layers over the rest
+// burst (it then also charges the kernel boundaries around the attention
+// launches); 0 = the attention launches timed alone (default)
+int& profile_insitu() {
+  static int on = 0;
+  return on;
+}
+
 // attention and "rest" tables of one layer of engine E under key t (+ the
 // decode head table when E holds the LM head and t = 1)
 static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profile& P) {
@@ -150,6 +159,7 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
   ae.t.assign(bs.size(), std::vector<double>(cs.size()));
   ad.t.assign(bs.size(), std::vector<double>(cs.size()));
   std::vector<int32_t> h_cu(slots + 1), h_nk(2 * max_b);
+  std::vector<std::vector<double>> full_dec(bs.size(), std::vector<double>(cs.size(), 0.0));
   for (size_t ib = 0; ib < bs.size(); ++ib) {
     const int b = bs[ib];
     for (size_t ic = 0; ic < cs.size(); ++ic) {
@@ -185,6 +195,7 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
       db.xkeys = d_aux + max_b;
       db.max_xkeys = c_x;
       ad.t[ib][ic] = tm.median(reps, [&] { E.layer_decode(0, db, true, false); });
+      if (profile_insitu()) full_dec[ib][ic] = tm.median(reps, [&] { E.layer_decode(0, db, true, true); }, kBurst);
     }
   }
   P.attn[{"enc", t}] = ae;
@@ -204,6 +215,12 @@ static void profile_one(Engine& E, int t, const exg_profile_grid& g, plan::Profi
     db.max_xkeys = 1;
     rd.x.push_back(b);
     rd.t.push_back(tm.median(reps, [&] { E.layer_decode(0, db, false, true); }, kBurst));
+  }
+  if (profile_insitu()) {
+    for (size_t ib = 0; ib < bs.size(); ++ib)
+      for (size_t ic = 0; ic < cs.size(); ++ic)
+        ad.t[ib][ic] = std::max(0.05 * full_dec[ib][ic], full_dec[ib][ic] - rd.t[ib]);
+    P.attn[{"dec", t}] = ad;
   }
   // head of a decode iteration on the last stage (final norm + tied LM head +
   // argmax), per decode batch: the model-level part of an iteration that the
@@ -401,3 +418,5 @@ void profile_layers(Engine& E, const exg_model_spec& spec, const exg_profile_gri
 }
 
 }  // namespace exg
+
+extern "C" void exg_diag_profile_insitu(int on) { exg::profile_insitu() = on; }

@@ -28,6 +28,8 @@ def main():
     t = TASKS["T"]
     d = task_dists("T")
     free, total = torch.cuda.mem_get_info(0)
+    if os.environ.get("EXG_PROFILE_INSITU"):   # diagnostics: in-situ decode attention table
+        X.lib().exg_diag_profile_insitu(int(os.environ["EXG_PROFILE_INSITU"]))
     t0 = time.perf_counter()
     ctx = X.Context(spec, weight_seed(3), cluster=X.cluster_spec(1, total - (40 << 30), 8 << 30))
     prof = ctx.profile([1, 2, 4, 8, 16, 32, 64, 96, 128, 192, 256], [1, 32, 64, 128, 192, 256, 384, 512, 576],
