@@ -56,13 +56,31 @@ def _compile(src: str, force: bool) -> str:
     return obj
 
 
+def _nccl_link_flags():
+    """Link the NCCL that torch ships (nvidia-nccl wheel) with an rpath, so the
+    library and torch.distributed share one NCCL whatever the import order
+    (the system libnccl is older than torch's; loading it first breaks torch).
+    Falls back to the system NCCL when the wheel is absent."""
+    try:
+        import importlib.util
+        spec = importlib.util.find_spec("nvidia")
+        for base in (spec.submodule_search_locations or []) if spec else []:
+            d = os.path.join(base, "nccl", "lib")
+            if os.path.exists(os.path.join(d, "libnccl.so.2")):
+                return ["-L" + d, "-l:libnccl.so.2", "-Xlinker", "-rpath=" + d]
+    except Exception:  # noqa: BLE001
+        pass
+    return ["-lnccl"]
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
     with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 4)) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), srcs))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static", "-lnccl", "-lrt", "-ldl", "-lpthread"]
+        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart_static"] + _nccl_link_flags() + \
+            ["-lrt", "-ldl", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError("link failed: %s\n%s\n%s" % (" ".join(cmd), r.stdout, r.stderr))
