@@ -31,12 +31,16 @@ def timeit(fn, reps=20):
     return float(np.median(ts))
 
 
-def dattn(B, keys, bias, H=128, dh=128, max_ctx=512):
+def dattn(B, keys, bias, H=128, dh=128, max_ctx=512, ragged=None):
     kc = torch.randn(B, H, max_ctx, dh, device=dev).to(torch.bfloat16)
     vc = torch.randn(B, H, max_ctx, dh, device=dev).to(torch.bfloat16)
     q = torch.randn(B, 3 * H * dh, device=dev).to(torch.bfloat16)
     slot = torch.arange(B, dtype=torch.int32, device=dev)
-    nk = torch.full((B,), keys, dtype=torch.int32, device=dev)
+    if ragged is None:
+        nk = torch.full((B,), keys, dtype=torch.int32, device=dev)
+    else:   # per-row key counts, longest first (the runner's row order)
+        nk = torch.tensor(sorted(ragged, reverse=True), dtype=torch.int32, device=dev)
+        keys = int(max(ragged))
     out = torch.empty(B, H * dh, device=dev, dtype=torch.bfloat16)
     ms = max(1, math.ceil(keys / 512))
     part = torch.empty(B * H * ms * (dh + 2), device=dev, dtype=torch.float32)
@@ -59,3 +63,13 @@ even = dattn(B, 107, True) + dattn(B, 107, False)
 real = dattn(B, 86, True) + dattn(B, 128, False)
 print("even split 107+107: %.1f us   task-T split 86 self + 128 cross: %.1f us   real/even %.3f" % (
     even * 1e6, real * 1e6, real / even))
+# raggedness: the same total keys as uniform rows vs spread rows (task T's self
+# keys ~ U(1..2*86), cross keys ~ the input PMF)
+rng = np.random.default_rng(0)
+for mean in (86, 128, 214):
+    rag = list(np.clip(rng.integers(1, 2 * mean, size=B), 1, 511))
+    rag = [int(x) for x in rag]
+    tu = dattn(B, int(round(np.mean(rag))), False)
+    tr = dattn(B, 0, False, ragged=rag)
+    print("B=%d mean keys %.0f: uniform %7.1f us  ragged (1..%d) %7.1f us  ragged/uniform %.3f" % (
+        B, np.mean(rag), tu * 1e6, 2 * mean, tr * 1e6, tr / tu))
