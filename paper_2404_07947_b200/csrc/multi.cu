@@ -415,9 +415,10 @@ struct MultiCtx::Impl {
   int rank = 0, world = 1;
   bool loopback = false;   // a one-rank communicator: route local exchanges through it
   std::map<std::string, std::unique_ptr<Layout>> layouts;
-  // the executors' table ring (device + pinned host buffers), kept across
-  // runs so the end-to-end path does not allocate and pin per run
-  std::shared_ptr<void> tab_cache;
+  // the executors' table ring (device + pinned host buffers) and WAA's
+  // handoff ring, kept across runs so the end-to-end path does not allocate
+  // and pin per run (and released with the context, whatever a run threw)
+  std::shared_ptr<void> tab_cache, hr_cache;
 };
 
 MultiCtx::MultiCtx(const exg_model_spec& spec, int device, std::unique_ptr<Comm> comm) : p_(new Impl) {
@@ -442,6 +443,7 @@ MultiCtx::~MultiCtx() {
   if (p_->cst) cudaStreamSynchronize(p_->cst);
   p_->layouts.clear();
   p_->tab_cache.reset();
+  p_->hr_cache.reset();
   p_->tx.release();
   p_->rx.release();
   p_->comm.reset();
@@ -601,6 +603,50 @@ struct Tables {
     if (host) cudaFreeHost(host);
   }
 };
+
+// WAA handoff row tables: a ring of pinned host / device pairs recycled by
+// events (no host synchronisation per handoff), plus the loopback transport's
+// staging buffer (both halves of a self-message); cached in the context
+struct HandoffRing {
+  static constexpr int N = 4;
+  HandoffRow* d[N] = {};
+  HandoffRow* h[N] = {};
+  cudaEvent_t ev[N] = {};
+  bool used[N] = {};
+  int next = 0, cap = 0;
+  bf16* stage = nullptr;
+  size_t stage_cap = 0;   // elements per half
+  void release() {
+    for (int i = 0; i < N; ++i) {
+      if (ev[i]) cudaEventSynchronize(ev[i]), cudaEventDestroy(ev[i]);
+      if (d[i]) cudaFree(d[i]);
+      if (h[i]) cudaFreeHost(h[i]);
+      d[i] = nullptr, h[i] = nullptr, ev[i] = nullptr, used[i] = false;
+    }
+    cap = 0;
+  }
+  ~HandoffRing() {
+    release();
+    if (stage) cudaFree(stage);
+  }
+  void ensure(int rows) {
+    if (rows <= cap) return;
+    release();
+    for (int i = 0; i < N; ++i) {
+      EXG_CUDA(cudaMalloc(&d[i], sizeof(HandoffRow) * rows));
+      EXG_CUDA(cudaMallocHost(&h[i], sizeof(HandoffRow) * rows));
+      EXG_CUDA(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+    }
+    cap = rows;
+  }
+};
+
+HandoffRing& handoff_ring(std::shared_ptr<void>& cache, int rows) {
+  if (!cache) cache = std::make_shared<HandoffRing>();
+  HandoffRing& r = *static_cast<HandoffRing*>(cache.get());
+  r.ensure(rows);
+  return r;
+}
 
 // the executors' table ring, cached in the context across runs
 std::vector<Tables>& table_ring(std::shared_ptr<void>& cache) {
@@ -1290,22 +1336,9 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   const bool first_mine = X.mine(enc.front()->gpu(0)), head_mine = X.mine(dec.back()->gpu(0));
   std::vector<Tables>& tabs = table_ring(p->tab_cache);
   const Dump dump = make_dump(R, opts);
-  // handoff row tables: a ring of pinned host / device pairs recycled by
-  // events (no host synchronisation per handoff); packed-message staging
-  // for transfers between ranks goes through the exchange rings of Exec
-  constexpr int HR = 4;
-  HandoffRow* d_hrows[HR] = {};
-  HandoffRow* h_hrows[HR] = {};
-  cudaEvent_t hr_ev[HR] = {};
-  bool hr_used[HR] = {};
-  int hr_next = 0;
-  for (int i = 0; i < HR; ++i) {
-    EXG_CUDA(cudaMalloc(&d_hrows[i], sizeof(HandoffRow) * enc_rows));
-    EXG_CUDA(cudaMallocHost(&h_hrows[i], sizeof(HandoffRow) * enc_rows));
-    EXG_CUDA(cudaEventCreateWithFlags(&hr_ev[i], cudaEventDisableTiming));
-  }
-  bf16* stage_buf = nullptr;   // loopback transport: both halves of a self-message
-  size_t stage_cap = 0;
+  // handoff row tables (cached ring, HandoffRow); packed-message staging for
+  // transfers between ranks goes through the exchange rings of Exec
+  HandoffRing& hr = handoff_ring(p->hr_cache, enc_rows);
   std::vector<int> free_slots(B_D);
   for (int i = 0; i < B_D; ++i) free_slots[i] = B_D - 1 - i;
   std::vector<Row> active;
@@ -1381,11 +1414,11 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
       std::vector<int> dslots(hk);
       int64_t rows_len = 0;
       // a row table slot is rewritten only once its previous upload is done
-      const int hs = hr_next;
-      hr_next = (hr_next + 1) % HR;
-      if (hr_used[hs]) EXG_CUDA(cudaEventSynchronize(hr_ev[hs]));
-      HandoffRow* hrow_h = h_hrows[hs];
-      HandoffRow* hrow_d = d_hrows[hs];
+      const int hs = hr.next;
+      hr.next = (hr.next + 1) % HandoffRing::N;
+      if (hr.used[hs]) EXG_CUDA(cudaEventSynchronize(hr.ev[hs]));
+      HandoffRow* hrow_h = hr.h[hs];
+      HandoffRow* hrow_d = hr.d[hs];
       const int32_t* dpt = nullptr;   // paged: destination page table [hk][maxp]
       if (paged) {
         Tables& tp = tabs[ti++ % tabs.size()];
@@ -1411,16 +1444,20 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
         R.admit_ev[pend_r0 + j] = pend_ev;
       }
       EXG_CUDA(cudaMemcpyAsync(hrow_d, hrow_h, sizeof(HandoffRow) * hk, cudaMemcpyHostToDevice, R.st));
-      EXG_CUDA(cudaEventRecord(hr_ev[hs], R.st));
-      hr_used[hs] = true;
+      EXG_CUDA(cudaEventRecord(hr.ev[hs], R.st));
+      hr.used[hs] = true;
       const size_t need = (size_t)rows_len * H * dh;   // largest slice (a TP-1 decoder stage)
-      if (X.loop && need > stage_cap) {
+      if (X.loop && need > hr.stage_cap) {
         EXG_CUDA(cudaStreamSynchronize(R.st));
-        if (stage_buf) cudaFree(stage_buf);
-        stage_cap = need;
+        if (hr.stage) cudaFree(hr.stage);
+        hr.stage = nullptr;
+        hr.stage_cap = 0;
         // loopback: a second half receives the message sent from the first
-        EXG_CUDA(cudaMalloc(&stage_buf, sizeof(bf16) * stage_cap * 2));
+        EXG_CUDA(cudaMalloc(&hr.stage, sizeof(bf16) * need * 2));
+        hr.stage_cap = need;
       }
+      bf16* stage_buf = hr.stage;
+      const size_t stage_cap = hr.stage_cap;
       // decoder-only: encoder stage es holds the KV of its layers [l0, l1);
       // T5: the last encoder stage holds the cross K/V of every decoder layer
       for (auto& es : enc) {
@@ -1525,12 +1562,6 @@ static void run_waa_multi(MultiCtx::Impl* p, Layout* lay, const exg_schedule& s,
   }
   finish(X, R, *dec.back(), out_tokens, out_latency, stats);
   EXG_CUDA(cudaStreamSynchronize(R.st));
-  if (stage_buf) cudaFree(stage_buf);
-  for (int i = 0; i < HR; ++i) {
-    cudaFree(d_hrows[i]);
-    cudaFreeHost(h_hrows[i]);
-    cudaEventDestroy(hr_ev[i]);
-  }
 }
 
 void MultiCtx::profile_comm(const std::vector<int>& tps, int reps,
