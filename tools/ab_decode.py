@@ -15,6 +15,8 @@ ctx = X.Context(spec, weight_seed(2))
 reqs = make_requests(256, d.pmf_in, d.pmf_out, spec.vocab, 0xE6E10002)
 if os.environ.get("EXG_DECODE_MERGE"):   # 1: separate combine kernel for attention splits
     X.lib().exg_diag_decode_merge(int(os.environ["EXG_DECODE_MERGE"]))
+if os.environ.get("EXG_DECODE_STAGES"):   # decode-attention ring depth / CTAs per SM variant
+    X.lib().exg_diag_decode_stages(int(os.environ["EXG_DECODE_STAGES"]))
 if os.environ.get("EXG_LN_PRELOAD"):    # 0: deferred LayerNorm preloads only the first segment
     X.lib().exg_diag_ln_preload(int(os.environ["EXG_LN_PRELOAD"]))
 if os.environ.get("EXG_DECODE_SPLIT"):
