@@ -107,10 +107,11 @@ exg_status exg_op_prefill_attention(const void* q, int64_t ldq, const void* kc, 
  * row; K4: request r) lives in page page_table[i*maxp + k/P] at offset k mod
  * P.  page_table: device int32 [rows][maxp], caller-owned; every entry a row's
  * keys reach must name a page of the cache (K4 reads whole 64-key halves of
- * its 128-key tiles up to the row's last key).  slot[] is still read (K6:
- * unused for addressing; K4: unused for addressing).  Same arithmetic as the
- * slot variants: identical results for identical key values.  EXG_E_INPUT on
- * a null page_table, maxp < 1 or a page length that is not a multiple of 64. */
+ * its 128-key tiles up to the row's last key).  slot[] must still be valid
+ * device memory of B (K6) / R (K4) entries but does not address the cache.
+ * Same arithmetic as the slot variants: identical results for identical key
+ * values.  EXG_E_INPUT on a null page_table, maxp < 1 or a page length that is
+ * not a multiple of 64 (K6: also one that does not divide split_len). */
 exg_status exg_op_decode_attention_paged(const void* q, int64_t ldq, const void* kc, const void* vc,
                                          const int32_t* slot, const int32_t* n_keys, void* out, int64_t ldo,
                                          int32_t B, int32_t H, int32_t dh, int32_t max_ctx, float scale,
