@@ -625,6 +625,8 @@ exg_status exg_op_decode_attention_paged(const void* q, int64_t ldq, const void*
     a.bias_ld = bias_ld;
     a.bias_off = bias_off;
     if (!page_table || maxp < 1) throw std::invalid_argument("paged: page_table / maxp");
+    if (max_ctx < 64 || max_ctx % 64 != 0 || split_len % max_ctx != 0)
+      throw std::invalid_argument("paged: the page length must be a multiple of 64 dividing split_len");
     a.kv = exg::KvMap{page_table, maxp};
     exg::decode_attention(a, (cudaStream_t)stream);
     return EXG_OK;
@@ -642,6 +644,7 @@ exg_status exg_op_prefill_attention_paged(const void* q, int64_t ldq, const void
                            pos0, R, max_len, (exg::bf16*)out, ldo, H, dh, max_ctx, scale, (int64_t)T,
                            (int64_t)n_slots * H * max_ctx, causal, bias, bias_ld, bias_off};
     if (!page_table || maxp < 1) throw std::invalid_argument("paged: page_table / maxp");
+    if (max_ctx < 64 || max_ctx % 64 != 0) throw std::invalid_argument("paged: the page length must be a multiple of 64");
     a.kv = exg::KvMap{page_table, maxp};
     exg::prefill_attention(a, (cudaStream_t)stream);
     return EXG_OK;
